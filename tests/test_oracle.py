@@ -1,0 +1,300 @@
+"""Pins for the CPU oracle (``-m "not gpu"``).
+
+Each test ties the oracle to something other than itself (the task's rule ③):
+SPEC worked examples (tests/golden/spec_examples.json, each cited), the
+generator's own pixel masks (built without any ray casting), closed forms
+(rectangles, combs as disjoint rectangle unions), exhaustive enumeration of tiny
+polyominoes against plain set arithmetic, the identity |p n q| + |p u q| =
+|p| + |q| with all four counted directly, grid symmetries, and nested-loop vs
+plane-sweep joins.  A dropped term, flipped sign, wrong index or transposed
+operand in oracle.c fails at least one of these.
+"""
+import itertools
+import json
+import math
+import os
+from fractions import Fraction
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from synth import combs
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden", "spec_examples.json")
+
+
+@pytest.fixture(scope="module")
+def golden():
+    with open(GOLDEN) as f:
+        return json.load(f)
+
+
+# ---------------------------------------------------------------- golden
+def test_golden_areas(golden):
+    for e in golden["areas"]:
+        assert oracle.area_shoelace(e["ring"]) == e["area"], e["cite"]
+        assert oracle.area_pixels(e["ring"], 0) == e["area"], e["cite"]
+        assert oracle.area_pixels(e["ring"], 1) == e["area"], e["cite"]
+
+
+def test_golden_pixels_and_mbrs(golden):
+    for e in golden["pixels"]:
+        assert oracle.pixel_in(e["ring"], *e["pixel"]) == e["inside"], e["cite"]
+    for e in golden["mbrs"]:
+        assert list(oracle.mbr(e["ring"])) == e["mbr"], e["cite"]
+
+
+def test_golden_pairs(golden):
+    for e in golden["pairs"]:
+        assert oracle.area_shoelace(e["p"]) == e["area_p"], e["cite"]
+        assert oracle.area_shoelace(e["q"]) == e["area_q"], e["cite"]
+        for mode in (0, 1):
+            assert oracle.pair(e["p"], e["q"], mode) == (e["inter"], e["union"]), e["cite"]
+            assert oracle.pair(e["q"], e["p"], mode) == (e["inter"], e["union"]), e["cite"]
+
+
+def test_golden_jaccard(golden):
+    for e in golden["jaccard"]:
+        j = oracle.jaccard(e["inter"], e["union"])
+        ex = oracle.jaccard_exact(e["inter"], e["union"])
+        if e["jprime_num"] is None:
+            assert math.isnan(j) and ex is None, e["cite"]
+        else:
+            assert ex == Fraction(e["jprime_num"], e["jprime_den"]), e["cite"]
+            assert j == e["jprime_num"] / e["jprime_den"], e["cite"]
+
+
+# ------------------------------------------------- generator masks (no PIP)
+def test_generator_masks_pin_pixel_test_and_shoelace(tile_sets):
+    """The generator builds each ring by tracing a pixel mask; the oracle's ray
+    casting must reproduce that mask exactly and the shoelace must equal its
+    cell count (pixel areas are exact for raster polygons)."""
+    for s in tile_sets:
+        for i in range(s.n):
+            x0, y0, m = s.masks[i]
+            h, w = m.shape
+            ring = s.ring(i)
+            # window one pixel larger on every side: nothing leaks outside
+            om = oracle.mask(ring, x0 - 1, y0 - 1, w + 2, h + 2, mode=1)
+            assert om[1:-1, 1:-1].tolist() == m.tolist()
+            assert om.sum() == m.sum()
+            assert oracle.area_shoelace(ring) == int(m.sum())
+            assert oracle.mbr(ring) == (x0, y0, x0 + w, y0 + h)
+
+
+def test_plain_and_prefilter_agree(tile_sets):
+    a, b = tile_sets
+    for i in range(0, a.n, 7):
+        x0, y0, m = a.masks[i]
+        h, w = m.shape
+        assert (oracle.mask(a.ring(i), x0 - 2, y0 - 2, w + 4, h + 4, 0) ==
+                oracle.mask(a.ring(i), x0 - 2, y0 - 2, w + 4, h + 4, 1)).all()
+    pairs = oracle.join(a, b)[::3]
+    i0, u0 = oracle.pair_areas(a, b, pairs, mode=0)
+    i1, u1 = oracle.pair_areas(a, b, pairs, mode=1)
+    assert (i0 == i1).all() and (u0 == u1).all()
+
+
+# ------------------------------------------------------------ closed forms
+def _rect(x0, y0, x1, y1):
+    return [[x0, y0], [x1, y0], [x1, y1], [x0, y1]]
+
+
+def test_rectangle_pairs_closed_form():
+    rng = np.random.default_rng(7)
+    for _ in range(400):
+        a = rng.integers(-20, 20, 2)
+        wa = rng.integers(1, 15, 2)
+        b = a + rng.integers(-16, 16, 2)
+        wb = rng.integers(1, 15, 2)
+        ra = _rect(a[0], a[1], a[0] + wa[0], a[1] + wa[1])
+        rb = _rect(b[0], b[1], b[0] + wb[0], b[1] + wb[1])
+        ow = max(0, min(a[0] + wa[0], b[0] + wb[0]) - max(a[0], b[0]))
+        oh = max(0, min(a[1] + wa[1], b[1] + wb[1]) - max(a[1], b[1]))
+        inter = ow * oh
+        uni = wa[0] * wa[1] + wb[0] * wb[1] - inter
+        assert oracle.pair(ra, rb) == (inter, uni)
+        assert oracle.area_shoelace(ra) == wa[0] * wa[1]
+
+
+def test_comb_closed_form():
+    """Combs are disjoint rectangle unions: |A| = sum |R_i|, |A n B| =
+    sum_ij |R_i n S_j| (SURVEY §8c pins), and comb area = W*b + k*w*h."""
+    for two in (False, True):
+        for k, w, g, h, b in [(3, 1, 1, 5, 2), (7, 2, 3, 9, 4), (12, 3, 1, 4, 1)]:
+            ring, rects = combs.comb(10, -5, k, w, g, h, b, two)
+            W = k * w + (k - 1) * g
+            expect = W * b + k * w * h * (2 if two else 1)
+            assert combs.rect_decomp_area(rects) == expect
+            assert oracle.area_shoelace(ring) == expect
+            assert oracle.area_pixels(ring, 0) == expect
+            assert len(ring) == (8 * k - 4 if two else 4 * k)
+    A, B, (RA, RB) = combs.generate(n_pairs=24, want_rects=True, max_vertices=800)
+    pairs = np.stack([np.arange(24), np.arange(24)], 1).astype(np.int32)
+    inter, uni = oracle.pair_areas(A, B, pairs)
+    for k in range(24):
+        ik = combs.rect_decomp_intersection(RA[k], RB[k])
+        assert inter[k] == ik
+        assert uni[k] == combs.rect_decomp_area(RA[k]) + combs.rect_decomp_area(RB[k]) - ik
+
+
+# ------------------------------------------------------------- exhaustive
+def _clean_polyominoes(k):
+    """All k x k masks that are one simply-connected, pinch-free 4-connected
+    region (the generator's clean() leaves them unchanged), with their rings."""
+    out = []
+    for bits in range(1, 1 << (k * k)):
+        m = np.array([(bits >> i) & 1 for i in range(k * k)], np.uint8).reshape(k, k)
+        ring, cleaned = synth.trace_mask(m)
+        if ring is not None and (cleaned == m).all():
+            out.append((m, ring))
+    return out
+
+
+def test_exhaustive_3x3_pairs():
+    polys = _clean_polyominoes(3)
+    assert len(polys) > 150
+    for m, ring in polys:
+        assert (oracle.mask(ring, -1, -1, 5, 5, 0)[1:4, 1:4] == m).all()
+        assert oracle.mask(ring, -1, -1, 5, 5, 0).sum() == m.sum() == oracle.area_shoelace(ring)
+    # bitboards on a 7x7 board: p at offset (2,2), q at (2+dx, 2+dy), |d| <= 2
+    def board(m, dx, dy):
+        v = 0
+        for (y, x) in zip(*np.nonzero(m)):
+            v |= 1 << ((y + 2 + dy) * 7 + (x + 2 + dx))
+        return v
+
+    rings_q, exp_i, exp_u, pairs = [], [], [], []
+    offs = list(itertools.product(range(-2, 3), repeat=2))
+    for qi, (mq, rq) in enumerate(polys):
+        for dx, dy in offs:
+            rings_q.append(rq + np.array([dx, dy], np.int32))
+    P = synth.pack([r for _, r in polys])
+    Q = synth.pack(rings_q)
+    bp = [board(m, 0, 0) for m, _ in polys]
+    for pi in range(len(polys)):
+        for qi, (mq, _) in enumerate(polys):
+            for oi, (dx, dy) in enumerate(offs):
+                bq = board(mq, dx, dy)
+                pairs.append((pi, qi * len(offs) + oi))
+                exp_i.append(bin(bp[pi] & bq).count("1"))
+                exp_u.append(bin(bp[pi] | bq).count("1"))
+    pairs = np.asarray(pairs, np.int32)
+    inter, uni = oracle.pair_areas(P, Q, pairs)
+    assert (inter == np.asarray(exp_i)).all()
+    assert (uni == np.asarray(exp_u)).all()
+
+
+def test_exhaustive_4x4_single():
+    polys = _clean_polyominoes(4)
+    assert len(polys) > 5000
+    for m, ring in polys:
+        om = oracle.mask(ring, -1, -1, 6, 6, 1)
+        assert (om[1:5, 1:5] == m).all() and om.sum() == m.sum()
+        assert oracle.area_shoelace(ring) == m.sum()
+
+
+# ------------------------------------------------------ invariants / symmetry
+def test_union_identity_counted_directly(tile_sets):
+    """|p n q| + |p u q| = |p| + |q| with all four counted pixel by pixel."""
+    a, b = tile_sets
+    pairs = oracle.join(a, b)
+    inter, uni = oracle.pair_areas(a, b, pairs, mode=0)
+    ap = np.array([oracle.area_pixels(a.ring(i), 0) for i in range(a.n)])
+    aq = np.array([oracle.area_pixels(b.ring(i), 0) for i in range(b.n)])
+    assert (inter + uni == ap[pairs[:, 0]] + aq[pairs[:, 1]]).all()
+    assert (inter <= np.minimum(ap[pairs[:, 0]], aq[pairs[:, 1]])).all()
+    assert (uni >= np.maximum(ap[pairs[:, 0]], aq[pairs[:, 1]])).all()
+    assert (inter > 0).sum() > 0.8 * len(pairs)
+
+
+D4 = [
+    lambda x, y: (x, y), lambda x, y: (-y, x), lambda x, y: (-x, -y), lambda x, y: (y, -x),
+    lambda x, y: (-x, y), lambda x, y: (x, -y), lambda x, y: (y, x), lambda x, y: (-y, -x),
+]
+
+
+def test_grid_symmetries_translation_scale(tile_sets):
+    a, b = tile_sets
+    pairs = oracle.join(a, b)[:150]
+    base_i, base_u = oracle.pair_areas(a, b, pairs)
+    for k, (p, q) in enumerate(pairs):
+        rp, rq = a.ring(int(p)).astype(np.int64), b.ring(int(q)).astype(np.int64)
+        assert oracle.pair(rq, rp) == (base_i[k], base_u[k])  # symmetry
+        for T in D4:
+            tp = np.array([T(x, y) for x, y in rp], np.int32)
+            tq = np.array([T(x, y) for x, y in rq], np.int32)
+            assert oracle.pair(tp, tq) == (base_i[k], base_u[k])
+        d = np.array([-1234, 777])
+        assert oracle.pair(rp + d, rq + d) == (base_i[k], base_u[k])  # translation
+        if k % 10 == 0:
+            for s in (2, 3):
+                assert oracle.pair(rp * s, rq * s) == (base_i[k] * s * s, base_u[k] * s * s)  # scale law
+    # idempotence
+    for i in range(0, a.n, 25):
+        ar = oracle.area_shoelace(a.ring(i))
+        assert oracle.pair(a.ring(i), a.ring(i)) == (ar, ar)
+
+
+# -------------------------------------------------------------------- join
+def test_join_nested_equals_sweep_and_transpose(tile_sets):
+    a, b = tile_sets
+    s = oracle.join(a, b, "sweep")
+    n = oracle.join(a, b, "nested")
+    assert s.tolist() == n.tolist()
+    t = oracle.join(b, a, "sweep")
+    assert sorted(t[:, ::-1].tolist()) == s.tolist()
+    keys = s[:, 0].astype(np.int64) * (1 << 32) + s[:, 1]
+    assert (np.diff(keys) > 0).all()
+
+
+def test_join_random_boxes_half_open():
+    rng = np.random.default_rng(3)
+    for trial in range(30):
+        n, m = rng.integers(1, 60, 2)
+        def boxes(k):
+            lo = rng.integers(0, 40, (k, 2))
+            wh = rng.integers(1, 12, (k, 2))
+            return np.concatenate([lo, lo + wh], 1).astype(np.int32)
+        bp, bq = boxes(n), boxes(m)
+        got = oracle.join_mbrs(bp, bq, "sweep").tolist()
+        exp = [[i, j] for i in range(n) for j in range(m)
+               if bp[i, 0] < bq[j, 2] and bq[j, 0] < bp[i, 2] and bp[i, 1] < bq[j, 3] and bq[j, 1] < bp[i, 3]]
+        assert got == exp
+    # touching boxes share no pixel: no pair (reading R4)
+    assert oracle.join_mbrs(np.array([[0, 0, 2, 2]], np.int32), np.array([[2, 0, 4, 2]], np.int32)).shape[0] == 0
+
+
+# ----------------------------------------------------------------- Eq. (1)
+def test_jaccard_exact_and_edge_cases(tile_sets):
+    a, b = tile_sets
+    pairs = oracle.join(a, b)
+    inter, uni = oracle.pair_areas(a, b, pairs)
+    j = oracle.jaccard(inter, uni)
+    ex = oracle.jaccard_exact(inter, uni)
+    assert abs(j - float(ex)) <= 1e-15 * float(ex)
+    # identical sets -> exactly 1
+    pa = oracle.join(a, a)
+    ia, ua = oracle.pair_areas(a, a, pa)
+    # pixel sets within one segmentation are disjoint, so only (p, p) has I > 0
+    assert oracle.jaccard(ia, ua) == 1.0
+    self_pairs = pa[pa[:, 0] == pa[:, 1]]
+    i2, u2 = oracle.pair_areas(a, a, self_pairs)
+    assert oracle.jaccard(i2, u2) == 1.0
+    # disjoint sets -> none
+    far = synth.pack([a.ring(i) + np.array([10**6, 0], np.int32) for i in range(a.n)])
+    assert len(oracle.join(a, far)) == 0
+    assert math.isnan(oracle.jaccard([], []))
+
+
+def test_sums_fields(tile_sets):
+    a, b = tile_sets
+    pairs = oracle.join(a, b)
+    inter, uni = oracle.pair_areas(a, b, pairs)
+    s = oracle.sums(a, b, pairs, inter, uni)
+    nz = inter > 0
+    assert s["n_pairs"] == len(pairs) and s["n_nonzero"] == int(nz.sum())
+    # all-pairs check: sum|p| + sum|q| - sum I = sum over all pairs of U
+    assert s["sum_area_p"] + s["sum_area_q"] - s["sum_inter"] == int(uni.sum())
