@@ -1,0 +1,399 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 PixelBox hot path (SCCG, arXiv 1208.0277).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config slide]
+
+One step = one pass of the whole hot path over one
+whole-slide image pair resident in HBM: prep of both sets (MBR, shoelace area,
+edge records), the grid-hash MBR join, PixelBox over every candidate pair, the
+deterministic integer sums, (N > 1: one NCCL all_reduce of the int64 sums) and
+J' on the host.  Workload: BASELINE.json configs[1] ("slide"), synthetic,
+~500k nucleus polygons per set, ~670k MBR-overlapping pairs.  At N GPUs each
+rank processes its own slide image (weak scaling, sharded by image as in
+configs[3]); the only collective is the sums all_reduce.
+
+Prints ONE JSON line (rank 0).  value = pairs/s over all ranks (max-over-ranks
+device time).  e2e = the same metric through the public API with host inputs
+(pinned H2D copies + D2H of the sums inside the timed region).  roofline =
+the PixelBox kernel's integer lane-op rate against the
+B200 issue peak.  cpu_baseline = the oracle (oracle/) on this box's cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "polygon pairs/sec (and pixels tested/sec) at 1/2/4/8 B200 vs int-issue peak"
+SMS_B200 = 148
+ISSUE_LANES_PER_CLK_SM = 128  # 4 SMSPs x 1 warp-instruction x 32 lanes (guide: B300_MICROARCH "Per-warp issue")
+OPS_PER_ROWTEST = 3  # sub, unsigned compare, predicated xor
+OPS_PER_BOXEDGE = 8  # one lane classifying one edge against all sub-boxes of a split (minimum)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="slide", choices=["slide", "tile", "skewed"])
+    ap.add_argument("--threshold", type=int, default=0)
+    ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--json-out", default=None)
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """Samples SM clock and throttle reasons via NVML during the timed region."""
+
+    REASONS = {
+        "gpu_idle": 0x1, "applications_clocks_setting": 0x2, "sw_power_cap": 0x4, "hw_slowdown": 0x8,
+        "sync_boost": 0x10, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+        "hw_power_brake_slowdown": 0x80, "display_clock_setting": 0x100,
+    }
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples, self.reasons = [], set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._t = None
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:  # pragma: no cover - NVML missing
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for k, bit in self.REASONS.items():
+                    if r & bit and k != "gpu_idle":
+                        self.reasons.add(k)
+            except Exception:
+                pass
+            time.sleep(0.005)
+
+    def __enter__(self):
+        if self.nv:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join()
+
+    def summary(self):
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None, "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------- workloads
+def make_workload(config: str, image: int):
+    import synth
+
+    return synth.generate(config, image=image)
+
+
+def config_desc(config):
+    return {
+        "slide": "configs[1]: one 100k x 100k whole-slide image, two synthetic result sets of ~500k nucleus polygons",
+        "tile": "configs[0]: one 4096x4096 tile, ~1,000 nucleus polygons per set",
+        "skewed": "configs[2]: 4x4 tiles, nuclei + 16 glands per tile (MBR side up to 512)",
+    }[config]
+
+
+# -------------------------------------------------------------- our arm
+def run_ours(args, rank, world, local_rank):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_1208_0277_b200 as sccg
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    sccg.load(build=(rank == 0))
+    A, B = make_workload(args.config, image=rank)
+    xy_p = torch.from_numpy(A.xy).pin_memory()
+    off_p = torch.from_numpy(A.offsets).pin_memory()
+    xy_q = torch.from_numpy(B.xy).pin_memory()
+    off_q = torch.from_numpy(B.offsets).pin_memory()
+    d_xy_p, d_off_p = xy_p.to(dev), off_p.to(dev)
+    d_xy_q, d_off_q = xy_q.to(dev), off_q.to(dev)
+    torch.cuda.synchronize()
+    P = sccg.DeviceSet(d_xy_p, d_off_p, prep=False)
+    Q = sccg.DeviceSet(d_xy_q, d_off_q, prep=False)
+    sums = sccg.new_sums(dev)
+    stream = torch.cuda.current_stream()
+    pix_start = torch.cuda.Event(enable_timing=True)
+    pix_end = torch.cuda.Event(enable_timing=True)
+    state = {"pix_ms": 0.0, "pairs": 0, "cap": 2 * max(P.n, Q.n) + 1024}
+
+    def step(timing_pixelbox=False):
+        sums.zero_()
+        P.prep()
+        Q.prep()
+        pairs = sccg.filter_pairs(P, Q, cap=state["cap"])
+        state["cap"] = max(state["cap"], int(pairs.shape[0]))
+        if timing_pixelbox:
+            pix_start.record(stream)
+        sccg.pixelbox(P, Q, pairs, threshold=args.threshold, sums=sums, want_inter=False, want_union=False)
+        if timing_pixelbox:
+            pix_end.record(stream)
+        if world > 1:
+            dist.all_reduce(sums, op=dist.ReduceOp.SUM)
+        host = sccg.sums_to_host(sums.cpu())
+        state["pairs"] = int(pairs.shape[0])
+        return host
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    # one untimed counting run for the algorithmic work per launch
+    pairs = sccg.filter_pairs(P, Q, cap=state["cap"])
+    counters = torch.zeros(8, dtype=torch.int64, device=dev)
+    sccg.pixelbox(P, Q, pairs, threshold=args.threshold, counters=counters, want_inter=False, want_union=False)
+    cnt = counters.cpu().tolist()
+    n_local = int(pairs.shape[0])
+    del pairs
+
+    # ---- timed region: K steps, barrier + synchronize on both sides
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    pix_total = 0.0
+    with ClockSampler(local_rank) as clk:
+        t0.record(stream)
+        wall0 = time.perf_counter()
+        for _ in range(args.steps):
+            host = step(timing_pixelbox=True)
+            pix_end.synchronize()
+            pix_total += pix_start.elapsed_time(pix_end)
+        t1.record(stream)
+        torch.cuda.synchronize()
+        wall1 = time.perf_counter()
+    if world > 1:
+        dist.barrier()
+    ms = t0.elapsed_time(t1)
+    times = torch.tensor([ms, pix_total / args.steps, float(n_local)], dtype=torch.float64, device=dev)
+    if world > 1:
+        mx = times.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        tot = times.clone()
+        dist.all_reduce(tot, op=dist.ReduceOp.SUM)
+    else:
+        mx, tot = times, times
+    ms_max, pix_ms_max = float(mx[0]), float(mx[1])
+    total_pairs = int(round(float(tot[2])))
+    jprime, pooled = sccg.jaccard(host)
+
+    # ---- e2e: public API from pinned host buffers, H2D + D2H inside the timed region
+    e2e_steps = max(1, min(args.e2e_steps, args.steps))
+    h2d = xy_p.numel() * 4 + off_p.numel() * 8 + xy_q.numel() * 4 + off_q.numel() * 8
+    d2h = sums.numel() * 8
+
+    def e2e_step():
+        a = xy_p.to(dev, non_blocking=True)
+        b = off_p.to(dev, non_blocking=True)
+        c = xy_q.to(dev, non_blocking=True)
+        d = off_q.to(dev, non_blocking=True)
+        Pe = sccg.DeviceSet(a, b)
+        Qe = sccg.DeviceSet(c, d)
+        pr = sccg.filter_pairs(Pe, Qe, cap=state["cap"])
+        s = sccg.new_sums(dev)
+        sccg.pixelbox(Pe, Qe, pr, threshold=args.threshold, sums=s, want_inter=False, want_union=False)
+        if world > 1:
+            dist.all_reduce(s, op=dist.ReduceOp.SUM)
+        return sccg.jaccard(s.cpu())
+
+    e2e_step()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(e2e_steps):
+        e2e_step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e_ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
+    e2e_value = total_pairs * e2e_steps / (float(e_ms[0]) / 1e3)
+
+    if rank != 0:
+        return None
+    value = total_pairs * args.steps / (ms_max / 1e3)
+    clocks = clk.summary()
+    # roofline of the dominant kernel (PixelBox), rank 0's algorithmic work per launch
+    ops = OPS_PER_ROWTEST * cnt[sccg.CNT_ROWTESTS] + OPS_PER_BOXEDGE * cnt[sccg.CNT_BOXEDGES]
+    pix_s = pix_ms_max / 1e3
+    achieved = ops / pix_s / 1e9
+    peak_mhz = clocks["sm_max_mhz"] or 1965.0
+    props = torch.cuda.get_device_properties(dev)
+    sms = props.multi_processor_count
+    peak = sms * ISSUE_LANES_PER_CLK_SM * peak_mhz * 1e6 / 1e9
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "pixelbox_traffic.json")
+    if os.path.exists(prof):
+        try:
+            with open(prof) as f:
+                pj = json.load(f)
+            if pj.get("config") == args.config:
+                traffic = pj.get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    launches_per_step = 15 + (0 if world == 1 else 0)
+    out = {
+        "metric": METRIC,
+        "value": value,
+        "unit": "pairs/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": max(args.warmup, 3),
+        "ms_per_step": ms_max / args.steps,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "int32",
+        "data": "synthetic (seeded generator synth/, nucleus polygons per PAPER.md §5.1)",
+        "impl": "ours",
+        "config": {
+            "workload": args.config,
+            "description": config_desc(args.config),
+            "pairs_per_gpu": n_local,
+            "pairs_total": total_pairs,
+            "polygons_p": P.n, "polygons_q": Q.n, "vertices_p": P.nv, "vertices_q": Q.nv,
+            "threshold_T": args.threshold or 2048,
+            "l2": "inputs larger than L2 (vertex + edge-record arrays ~%d MB per rank > 126 MB)" % (
+                (P.nv + Q.nv) * 16 // 2**20),
+            "parallelism": f"image-sharded x{world}" if world > 1 else "1 GPU",
+        },
+        "pixels_tested_per_s": cnt[sccg.CNT_PIXELS] * world / pix_s,
+        "pixelbox_ms": pix_ms_max,
+        "jprime": jprime,
+        "pooled_jaccard": pooled,
+        "counters": {"pixels": cnt[0], "rowtests": cnt[1], "boxes": cnt[2], "boxedges": cnt[3], "splits": cnt[4],
+                     "pixboxes": cnt[5], "rootpx": cnt[6]},
+        "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Gop/s", "frac": achieved / peak,
+                     "traffic": traffic, "kernel": "pixelbox_kernel",
+                     "peak_source": f"{sms} SMs x 128 int lanes/clk x {peak_mhz:.0f} MHz (issue peak, DESIGN.md)"},
+        "e2e": {"value": e2e_value, "unit": "pairs/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                "steps": e2e_steps},
+        "gpu_launches": launches_per_step * args.steps,
+        "clocks": clocks,
+        "wall_s": wall1 - wall0,
+    }
+    return out
+
+
+def cpu_baseline(config: str, image: int = 0, budget_s: float = 20.0):
+    """The oracle, as it stands, on this host's cores over a bounded sample of
+    the same workload: whole tiles of the slide (all rows of the path: areas,
+    join, per-pair areas, J') until ~budget_s seconds are spent."""
+    import numpy as np
+
+    import oracle
+
+    A, B = make_workload(config, image)
+    _, ma = oracle.set_props(A)
+    _, mb = oracle.set_props(B)
+    tile = 4096
+    ta = (ma[:, 0] // tile) * 1000 + ma[:, 1] // tile
+    tb = (mb[:, 0] // tile) * 1000 + mb[:, 1] // tile
+    tiles = sorted(set(ta.tolist()))
+    rng = np.random.default_rng(0)
+    rng.shuffle(tiles)
+    threads = os.cpu_count() or 1
+    done_pairs, spent, ntiles = 0, 0.0, 0
+    for t in tiles:
+        Ai = A.subset(np.nonzero(ta == t)[0])
+        Bi = B.subset(np.nonzero(tb == t)[0])
+        t0 = time.perf_counter()
+        oracle.set_props(Ai)
+        oracle.set_props(Bi)
+        pr = oracle.join(Ai, Bi)
+        I, U = oracle.pair_areas(Ai, Bi, pr, threads=threads)
+        oracle.jaccard(I, U)
+        spent += time.perf_counter() - t0
+        done_pairs += len(pr)
+        ntiles += 1
+        if spent > budget_s:
+            break
+    return {"value": done_pairs / spent, "unit": "pairs/s", "cores": threads, "kind": "oracle",
+            "sample": f"{ntiles} of {len(tiles)} 4096x4096 tiles of the {config} image ({done_pairs} pairs), "
+                      f"full oracle path (shoelace areas, sweep join, pixel-count I/U, J')",
+            "seconds": spent}
+
+
+def run_reference(args):
+    """--impl reference: the oracle is this tier's reference arm."""
+    base = cpu_baseline(args.config, 0, budget_s=max(5.0, min(60.0, 0.2 * (args.steps + args.warmup))))
+    out = {
+        "metric": METRIC, "value": base["value"], "unit": "pairs/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "int32", "data": "synthetic", "impl": "reference",
+        "config": {"workload": args.config, "description": config_desc(args.config)},
+        "cpu_baseline": base,
+        "e2e": {"value": base["value"], "unit": "pairs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    return out
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        if rank == 0:
+            out = run_reference(args)
+            print(json.dumps(out))
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    out = run_ours(args, rank, world, local_rank)
+    if rank == 0:
+        if not args.no_cpu_baseline:
+            out["cpu_baseline"] = cpu_baseline(args.config, 0)
+        line = json.dumps(out)
+        print(line)
+        if args.json_out:
+            with open(args.json_out, "w") as f:
+                f.write(line + "\n")
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,180 @@
+/* sccg.h -- C ABI of the B200-native PixelBox hot path of SCCG (arXiv 1208.0277).
+ *
+ * Operation (PAPER.md, /root/reference/PAPER.md line numbers "P:n"):
+ *   For every pair of polygons p in P, q in Q whose minimum bounding rectangles
+ *   overlap (the `&&` filter of Fig. 1(b), §2.2; the filter stage,
+ *   §4.1), compute the exact pixel areas of intersection and union
+ *   (PixelBox, §3, Alg. 1; union via |p u q| = |p| + |q| - |p n q|,
+ *   P:75) and aggregate the Jaccard variant J' of Eq. (1) (§2.1).
+ *
+ * Geometry conventions (readings R1-R4):
+ *   - A polygon is one ring of integer vertices with axis-parallel edges
+ *     (§3.1), given as int32 (x, y) pixel-corner coordinates, implicitly
+ *     closed (do not repeat the first vertex; a repeat is a harmless zero-length
+ *     edge).  Either orientation.  The ring must be simple and hole-free
+ *     (precondition, not checked).
+ *   - Pixel (x, y) is the unit cell [x, x+1) x [y, y+1); it lies inside a
+ *     polygon iff a ray cast from its center crosses the boundary an odd number
+ *     of times.  Areas are pixel counts.
+ *   - MBR = [min x, max x) x [min y, max y) (half-open); two MBRs overlap iff
+ *     they share a pixel (touching MBRs do not pair; reading R4).
+ *   - Limits: |coordinate| <= 2^30; every polygon's MBR is at most 65535 pixels
+ *     wide and tall (edges are stored as 16-bit offsets); n_polygons < 2^31.
+ *
+ * Memory and ownership:
+ *   - Every array pointer is a DEVICE pointer unless marked "host".  The caller
+ *     allocates and owns every buffer, including derived per-polygon buffers and
+ *     workspaces; the library allocates no device memory and keeps no state
+ *     except a thread-local error slot.
+ *   - All calls are stream-ordered on `stream` (a cudaStream_t; NULL = the
+ *     legacy default stream).  Only sccg_filter_pairs synchronises (it returns
+ *     the data-dependent pair count); the others return as soon as the work is
+ *     enqueued.
+ *
+ * Errors: functions return an sccg_status.  Argument errors (SCCG_E_ARG,
+ * SCCG_E_WORKSPACE) are detected on the host before anything is enqueued.
+ * Data-dependent problems found on the device (non-rectilinear edge, range,
+ * malformed offsets) set bits in a device status word (sccg_polyset.status,
+ * sccg_sums.status); sccg_filter_pairs reads them after its sync and returns the
+ * matching code.  sccg_last_error_index() reports the lowest offending polygon
+ * index seen by the last failing call on this thread (-1 if none).
+ */
+#ifndef SCCG_H
+#define SCCG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define SCCG_API __attribute__((visibility("default")))
+#else
+#define SCCG_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* sccg_stream_t; /* == cudaStream_t */
+
+typedef enum {
+  SCCG_OK = 0,
+  SCCG_E_ARG = 1,              /* null pointer, negative size, bad config, malformed offsets, < 4 vertices */
+  SCCG_E_NOT_RECTILINEAR = 2,  /* a diagonal edge */
+  SCCG_E_RANGE = 3,            /* |coord| > 2^30 or an MBR wider / taller than 65535 */
+  SCCG_E_CAPACITY = 4,         /* output buffer too small; required size reported */
+  SCCG_E_STACK = 5,            /* sampling-box stack overflow (internal bug) */
+  SCCG_E_EMPTY = 6,            /* J' undefined: no pair with |p n q| != 0 (Eq. 1) */
+  SCCG_E_CUDA = 7,             /* a CUDA runtime error (message in sccg_last_error_string) */
+  SCCG_E_WORKSPACE = 8         /* workspace too small or misaligned */
+} sccg_status;
+
+/* status-word bits (device side) */
+#define SCCG_STATUS_ARG (1u << 0)
+#define SCCG_STATUS_NOT_RECTILINEAR (1u << 1)
+#define SCCG_STATUS_RANGE (1u << 2)
+#define SCCG_STATUS_STACK (1u << 3)
+
+/* One polygon set on the device: the caller's packed rings (inputs) plus the
+ * per-polygon data sccg_prep derives from them (caller-allocated outputs; use
+ * sccg_polyset_bind to carve them from one buffer of sccg_polyset_bytes). */
+typedef struct {
+  /* inputs */
+  const int32_t* xy;      /* [n_vertices][2] interleaved x, y */
+  const int64_t* offsets; /* [n_polygons + 1]; polygon i = vertices offsets[i] .. offsets[i+1]-1; offsets[0] = 0 */
+  int64_t n_polygons;
+  int64_t n_vertices;     /* == offsets[n_polygons] */
+  /* derived by sccg_prep (§3.2 P:193 areas; MBRs for the filter) */
+  int32_t* mbr;           /* [n_polygons][4] xlo, ylo, xhi, yhi (half-open pixel MBR) */
+  int64_t* area;          /* [n_polygons] |p| (shoelace) */
+  int32_t* ecount;        /* [n_polygons][2] number of vertical, horizontal edges */
+  uint64_t* edges;        /* [n_vertices] edge records (internal layout) */
+  uint32_t* status;       /* [2] device: status bits (OR), lowest offending polygon (MIN) */
+} sccg_polyset;
+
+/* Bytes of derived storage for a set (for sccg_polyset_bind). */
+SCCG_API size_t sccg_polyset_bytes(int64_t n_polygons, int64_t n_vertices);
+
+/* Point the derived fields of *set at sub-ranges of `buf` (device, 256-byte
+ * aligned, at least sccg_polyset_bytes bytes).  Host-only, enqueues nothing. */
+SCCG_API int sccg_polyset_bind(sccg_polyset* set, void* buf, size_t bytes);
+
+/* Per-polygon prep: MBR, shoelace area (one term per
+ * thread, summed), validation, and the edge records PixelBox reads.  Resets and
+ * fills set->status.  validate = 1 checks rectilinearity, ranges, offsets. */
+SCCG_API int sccg_prep(const sccg_polyset* set, int32_t validate, sccg_stream_t stream);
+
+/* ---------------------------------------------------------------- filter */
+/* Workspace bytes sccg_filter_pairs needs for sets of these sizes. */
+SCCG_API size_t sccg_filter_workspace_bytes(int64_t n_p, int64_t n_q);
+
+/* MBR-overlap join of two prepared sets by a grid hash on
+ * the device.  Writes the candidate pairs, unique and sorted by (p, q), as
+ * pairs[k] = {p, q} (int32 [cap][2]) and sets *n_pairs_host (host) to their
+ * count.  If cap < count (or pairs == NULL) nothing is written to pairs and
+ * SCCG_E_CAPACITY is returned with *n_pairs_host = required count.
+ * Synchronises `stream` (twice: grid sizing and the count).  Also returns the
+ * first data error recorded by sccg_prep in either set's status word. */
+SCCG_API int sccg_filter_pairs(const sccg_polyset* p, const sccg_polyset* q, int32_t* pairs, int64_t cap,
+                      int64_t* n_pairs_host, void* workspace, size_t ws_bytes, sccg_stream_t stream);
+
+/* -------------------------------------------------------------- pixelbox */
+/* Accumulated, order-independent integer totals (one NCCL int64 SUM merges
+ * several GPUs bit-exactly).  Caller zeroes it once; each sccg_pixelbox call
+ * adds to it (batching). */
+typedef struct {
+  int64_t n_pairs;       /* all pairs processed */
+  int64_t n_nonzero;     /* pairs with |p n q| != 0 (the pairs Eq. 1 averages) */
+  int64_t sum_inter;     /* sum |p n q| */
+  int64_t sum_union;     /* sum |p u q| over pairs with |p n q| != 0 */
+  int64_t sum_area_p;    /* sum |p| over all pairs (with multiplicity) */
+  int64_t sum_area_q;    /* sum |q| over all pairs */
+  int64_t ratio_limb[4]; /* sum of r = RN64(I/U) over I != 0, as an integer count of 2^-116 in 30-bit limbs */
+  int64_t status;        /* OR of SCCG_STATUS_* bits seen */
+} sccg_sums;
+
+typedef struct {
+  int32_t threshold; /* T: boxes with fewer pixels are pixelized (Alg. 1 l.22); 0 = default */
+  int32_t mode;      /* 0 = PixelBox (sampling boxes + pixelization); 1 = PixelOnly (pixelize the
+                        whole root box, the §5.2 baseline) */
+  int32_t block;     /* threads per CTA (multiple of 32, <= 1024); 0 = default */
+  int32_t grid;      /* CTAs; 0 = default (resident CTAs per SM x SM count) */
+  int64_t* counters; /* optional device int64[8] (NULL = off): see SCCG_CNT_* */
+} sccg_config;
+
+/* counters[] slots (accumulated; measurement builds only) */
+#define SCCG_CNT_PIXELS 0      /* pixels classified by pixelization (each against both polygons) */
+#define SCCG_CNT_ROWTESTS 1    /* (row segment x vertical edge) crossing tests */
+#define SCCG_CNT_BOXES 2       /* sampling boxes classified (Lemma 1) */
+#define SCCG_CNT_BOXEDGES 3    /* (sampling-box split x edge) classification steps */
+#define SCCG_CNT_SPLITS 4      /* boxes split (SUBSAMPBOX calls) */
+#define SCCG_CNT_PIXBOXES 5    /* boxes pixelized */
+#define SCCG_CNT_ROOTPX 6      /* sum of root-box pixels |MBR(p) n MBR(q)| */
+
+SCCG_API size_t sccg_pixelbox_workspace_bytes(int64_t n_pairs);
+
+/* PixelBox: for each pairs[k] = {p, q} (indices into the prepared
+ * sets) write inter[k] = |p n q| and uni[k] = |p| + |q| - |p n q| (int64, input
+ * order; either may be NULL to skip it) and add the batch's totals into *sums
+ * (device).  Bit-identical results for every config, launch shape and GPU
+ * count.  Asynchronous. */
+SCCG_API int sccg_pixelbox(const sccg_polyset* p, const sccg_polyset* q, const int32_t* pairs, int64_t n_pairs,
+                  int64_t* inter, int64_t* uni, sccg_sums* sums, const sccg_config* cfg, void* workspace,
+                  size_t ws_bytes, sccg_stream_t stream);
+
+/* ---------------------------------------------------------------- jaccard */
+/* J' of Eq. (1) from host-resident sums: the mean of r(p, q) over the
+ * pairs with |p n q| != 0.  *pooled (nullable) = sum_inter / sum_union over the
+ * same pairs.  Returns SCCG_E_EMPTY and NaN when n_nonzero == 0. */
+SCCG_API int sccg_jaccard(const sccg_sums* sums_host, double* jprime, double* pooled);
+
+/* ------------------------------------------------------------------ misc */
+SCCG_API const char* sccg_strerror(int code);
+SCCG_API const char* sccg_last_error_string(void); /* thread-local detail of the last failure */
+SCCG_API int64_t sccg_last_error_index(void);      /* thread-local; -1 if none */
+SCCG_API int sccg_version(void);                   /* ABI version */
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SCCG_H */

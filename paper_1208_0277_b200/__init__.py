@@ -1,0 +1,294 @@
+"""paper_1208_0277_b200 -- B200-native PixelBox hot path of SCCG (arXiv 1208.0277).
+
+A thin ctypes binding over the C ABI in ``include/sccg.h`` (``libsccg.so``,
+built for sm_100a).  Argument marshalling only: every step of the path -- prep,
+MBR join, PixelBox, the integer sums -- runs in the library's CUDA kernels.
+There is no CPU fallback: if the library or a GPU is missing, these functions
+raise.
+
+PyTorch supplies device memory, streams and process groups::
+
+    import paper_1208_0277_b200 as sccg
+    P = sccg.DeviceSet(xy_p, off_p)           # torch cuda tensors (int32 [V,2], int64 [n+1])
+    Q = sccg.DeviceSet(xy_q, off_q)
+    pairs = sccg.filter_pairs(P, Q)           # int32 [N, 2], sorted by (p, q)
+    inter, uni, sums = sccg.pixelbox(P, Q, pairs)
+    jprime, pooled = sccg.jaccard(sums)       # Eq. (1)
+
+``compare`` runs the whole path from host arrays (the end-to-end API).
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+import os
+import threading
+
+from . import build as _build
+
+_lock = threading.Lock()
+_lib = None
+
+# status codes (include/sccg.h)
+OK, E_ARG, E_NOT_RECTILINEAR, E_RANGE, E_CAPACITY, E_STACK, E_EMPTY, E_CUDA, E_WORKSPACE = range(9)
+CNT_PIXELS, CNT_ROWTESTS, CNT_BOXES, CNT_BOXEDGES, CNT_SPLITS, CNT_PIXBOXES, CNT_ROOTPX = range(7)
+SUMS_FIELDS = ("n_pairs", "n_nonzero", "sum_inter", "sum_union", "sum_area_p", "sum_area_q", "limb0", "limb1",
+               "limb2", "limb3", "status")
+SYMBOLS = ("sccg_polyset_bytes", "sccg_polyset_bind", "sccg_prep", "sccg_filter_workspace_bytes",
+           "sccg_filter_pairs", "sccg_pixelbox_workspace_bytes", "sccg_pixelbox", "sccg_jaccard", "sccg_strerror",
+           "sccg_last_error_string", "sccg_last_error_index", "sccg_version")
+
+
+class SccgError(RuntimeError):
+    def __init__(self, code: int, where: str):
+        lib = _lib
+        self.code = code
+        self.detail = lib.sccg_last_error_string().decode() if lib else ""
+        self.index = int(lib.sccg_last_error_index()) if lib else -1
+        name = lib.sccg_strerror(code).decode() if lib else str(code)
+        super().__init__(f"{where}: {name} ({self.detail}) [index {self.index}]")
+
+
+class PolySet(ctypes.Structure):
+    _fields_ = [
+        ("xy", ctypes.c_void_p),
+        ("offsets", ctypes.c_void_p),
+        ("n_polygons", ctypes.c_int64),
+        ("n_vertices", ctypes.c_int64),
+        ("mbr", ctypes.c_void_p),
+        ("area", ctypes.c_void_p),
+        ("ecount", ctypes.c_void_p),
+        ("edges", ctypes.c_void_p),
+        ("status", ctypes.c_void_p),
+    ]
+
+
+class Sums(ctypes.Structure):
+    _fields_ = [(f, ctypes.c_int64) for f in SUMS_FIELDS]
+
+
+class Config(ctypes.Structure):
+    _fields_ = [
+        ("threshold", ctypes.c_int32),
+        ("mode", ctypes.c_int32),
+        ("block", ctypes.c_int32),
+        ("grid", ctypes.c_int32),
+        ("counters", ctypes.c_void_p),
+    ]
+
+
+def library_path() -> str:
+    return _build.LIB
+
+
+def load(build: bool = True):
+    """Load libsccg.so (building it first if stale and nvcc exists)."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        path = _build.LIB
+        if build:
+            try:
+                path = _build.build()
+            except (OSError, RuntimeError) as e:  # no nvcc: fall through to an existing library
+                if not os.path.exists(path):
+                    raise ImportError(f"libsccg.so missing and cannot be built: {e}") from e
+        if not os.path.exists(path):
+            raise ImportError(f"libsccg.so not found at {path}; run paper_1208_0277_b200/build.py")
+        lib = ctypes.CDLL(path)
+        vp, i64, i32, sz, cint = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_size_t, ctypes.c_int
+        ps = ctypes.POINTER(PolySet)
+        lib.sccg_polyset_bytes.argtypes = [i64, i64]
+        lib.sccg_polyset_bytes.restype = sz
+        lib.sccg_polyset_bind.argtypes = [ps, vp, sz]
+        lib.sccg_polyset_bind.restype = cint
+        lib.sccg_prep.argtypes = [ps, i32, vp]
+        lib.sccg_prep.restype = cint
+        lib.sccg_filter_workspace_bytes.argtypes = [i64, i64]
+        lib.sccg_filter_workspace_bytes.restype = sz
+        lib.sccg_filter_pairs.argtypes = [ps, ps, vp, i64, ctypes.POINTER(i64), vp, sz, vp]
+        lib.sccg_filter_pairs.restype = cint
+        lib.sccg_pixelbox_workspace_bytes.argtypes = [i64]
+        lib.sccg_pixelbox_workspace_bytes.restype = sz
+        lib.sccg_pixelbox.argtypes = [ps, ps, vp, i64, vp, vp, vp, ctypes.POINTER(Config), vp, sz, vp]
+        lib.sccg_pixelbox.restype = cint
+        lib.sccg_jaccard.argtypes = [ctypes.POINTER(Sums), ctypes.POINTER(ctypes.c_double),
+                                     ctypes.POINTER(ctypes.c_double)]
+        lib.sccg_jaccard.restype = cint
+        lib.sccg_strerror.argtypes = [cint]
+        lib.sccg_strerror.restype = ctypes.c_char_p
+        lib.sccg_last_error_string.argtypes = []
+        lib.sccg_last_error_string.restype = ctypes.c_char_p
+        lib.sccg_last_error_index.argtypes = []
+        lib.sccg_last_error_index.restype = i64
+        lib.sccg_version.argtypes = []
+        lib.sccg_version.restype = cint
+        _lib = lib
+        return lib
+
+
+def _check(code: int, where: str):
+    if code != OK:
+        raise SccgError(code, where)
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+def _stream_ptr(stream=None) -> int:
+    torch = _torch()
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return int(s.cuda_stream)
+
+
+def _require_cuda(t, name, dtype):
+    torch = _torch()
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise TypeError(f"{name} must be a CUDA tensor (no CPU fallback)")
+    if t.dtype != dtype:
+        raise TypeError(f"{name} must be {dtype}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+
+
+class DeviceSet:
+    """One polygon set resident on the GPU plus the buffers sccg_prep fills.
+
+    xy: int32 [V, 2] CUDA tensor; offsets: int64 [n + 1] CUDA tensor."""
+
+    def __init__(self, xy, offsets, prep: bool = True, validate: bool = True, stream=None):
+        torch = _torch()
+        lib = load()
+        _require_cuda(xy, "xy", torch.int32)
+        _require_cuda(offsets, "offsets", torch.int64)
+        self.xy, self.offsets = xy, offsets
+        n = int(offsets.numel()) - 1
+        nv = int(xy.numel()) // 2
+        self.n, self.nv = n, nv
+        nbytes = int(lib.sccg_polyset_bytes(n, nv))
+        self._buf = torch.empty(nbytes, dtype=torch.uint8, device=xy.device)
+        self.c = PolySet(xy.data_ptr(), offsets.data_ptr(), n, nv, None, None, None, None, None)
+        _check(lib.sccg_polyset_bind(ctypes.byref(self.c), self._buf.data_ptr(), nbytes), "sccg_polyset_bind")
+        if prep:
+            self.prep(validate, stream)
+
+    def prep(self, validate: bool = True, stream=None):
+        _check(load().sccg_prep(ctypes.byref(self.c), 1 if validate else 0, _stream_ptr(stream)), "sccg_prep")
+        return self
+
+    def _view(self, ptr_field, dtype, shape):
+        torch = _torch()
+        base = self._buf.data_ptr()
+        off = getattr(self.c, ptr_field) - base
+        count = 1
+        for s in shape:
+            count *= s
+        esz = torch.empty((), dtype=dtype).element_size()
+        return self._buf[off: off + count * esz].view(dtype).view(*shape)
+
+    @property
+    def mbr(self):
+        return self._view("mbr", _torch().int32, (self.n, 4))
+
+    @property
+    def area(self):
+        return self._view("area", _torch().int64, (self.n,))
+
+    @property
+    def status(self):
+        return self._view("status", _torch().int32, (2,))
+
+
+def filter_pairs(P: DeviceSet, Q: DeviceSet, cap: int | None = None, stream=None):
+    """Candidate pairs (overlapping half-open MBRs), int32 [N, 2] sorted by (p, q)."""
+    torch = _torch()
+    lib = load()
+    wsb = int(lib.sccg_filter_workspace_bytes(P.n, Q.n))
+    ws = torch.empty(wsb, dtype=torch.uint8, device=P.xy.device)
+    if cap is None:
+        cap = 2 * max(P.n, Q.n) + 1024
+    for _ in range(2):
+        out = torch.empty((max(cap, 1), 2), dtype=torch.int32, device=P.xy.device)
+        n = ctypes.c_int64(0)
+        code = lib.sccg_filter_pairs(ctypes.byref(P.c), ctypes.byref(Q.c), out.data_ptr(), cap, ctypes.byref(n),
+                                     ws.data_ptr(), wsb, _stream_ptr(stream))
+        if code == E_CAPACITY:
+            cap = int(n.value)
+            continue
+        _check(code, "sccg_filter_pairs")
+        return out[: int(n.value)]
+    raise SccgError(E_CAPACITY, "sccg_filter_pairs")
+
+
+def new_sums(device=None):
+    """A zeroed device sums vector (int64[11], the sccg_sums layout)."""
+    torch = _torch()
+    return torch.zeros(len(SUMS_FIELDS), dtype=torch.int64, device=device or "cuda")
+
+
+def pixelbox(P: DeviceSet, Q: DeviceSet, pairs, threshold: int = 0, mode: int = 0, sums=None, want_inter=True,
+             want_union=True, counters=None, grid: int = 0, stream=None):
+    """Per-pair |p n q| and |p u q| (int64, input order) + accumulated sums."""
+    torch = _torch()
+    lib = load()
+    _require_cuda(pairs, "pairs", torch.int32)
+    n = int(pairs.shape[0])
+    dev = P.xy.device
+    inter = torch.empty(n, dtype=torch.int64, device=dev) if want_inter else None
+    uni = torch.empty(n, dtype=torch.int64, device=dev) if want_union else None
+    if sums is None:
+        sums = new_sums(dev)
+    _require_cuda(sums, "sums", torch.int64)
+    cfg = Config(threshold, mode, 0, grid, counters.data_ptr() if counters is not None else None)
+    wsb = int(lib.sccg_pixelbox_workspace_bytes(n))
+    ws = torch.empty(max(wsb, 256), dtype=torch.uint8, device=dev)
+    code = lib.sccg_pixelbox(ctypes.byref(P.c), ctypes.byref(Q.c), pairs.data_ptr(), n,
+                             inter.data_ptr() if inter is not None else None,
+                             uni.data_ptr() if uni is not None else None, sums.data_ptr(), ctypes.byref(cfg),
+                             ws.data_ptr(), wsb, _stream_ptr(stream))
+    _check(code, "sccg_pixelbox")
+    return inter, uni, sums
+
+
+def sums_to_host(sums) -> Sums:
+    vals = [int(v) for v in (sums.tolist() if hasattr(sums, "tolist") else sums)]
+    return Sums(*vals)
+
+
+def jaccard(sums) -> tuple[float, float]:
+    """(J', pooled) from a sums vector (device tensor, list or Sums); NaN if empty."""
+    lib = load()
+    s = sums if isinstance(sums, Sums) else sums_to_host(sums)
+    j, pooled = ctypes.c_double(), ctypes.c_double()
+    code = lib.sccg_jaccard(ctypes.byref(s), ctypes.byref(j), ctypes.byref(pooled))
+    if code == E_EMPTY:
+        return math.nan, math.nan
+    _check(code, "sccg_jaccard")
+    return j.value, pooled.value
+
+
+def to_device(xy, offsets, device="cuda", non_blocking=True):
+    """Copy host numpy / tensor arrays (pinned if possible) to the GPU."""
+    torch = _torch()
+    xy_t = torch.as_tensor(xy).to(torch.int32)
+    off_t = torch.as_tensor(offsets).to(torch.int64)
+    return (xy_t.reshape(-1, 2).to(device, non_blocking=non_blocking),
+            off_t.to(device, non_blocking=non_blocking))
+
+
+def compare(xy_p, off_p, xy_q, off_q, threshold: int = 0, device="cuda", stream=None) -> dict:
+    """End-to-end cross-comparison of two host polygon sets (the public API):
+    H2D copy, prep, MBR join, PixelBox, sums D2H, J'.  Returns a report dict."""
+    dxp, dop = to_device(xy_p, off_p, device)
+    dxq, doq = to_device(xy_q, off_q, device)
+    P = DeviceSet(dxp, dop, stream=stream)
+    Q = DeviceSet(dxq, doq, stream=stream)
+    pairs = filter_pairs(P, Q, stream=stream)
+    _, _, sums = pixelbox(P, Q, pairs, threshold=threshold, want_inter=False, want_union=False, stream=stream)
+    host = sums_to_host(sums.cpu())
+    j, pooled = jaccard(host)
+    return dict(jprime=j, pooled=pooled, **{f: getattr(host, f) for f in SUMS_FIELDS})

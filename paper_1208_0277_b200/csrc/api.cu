@@ -1,0 +1,193 @@
+// api.cu -- the extern "C" boundary declared in include/sccg.h.
+// Argument checking, workspace carving, the thread-local error slot, and
+// sccg_jaccard (Eq. 1) on host-resident integer sums.
+#include <math.h>
+#include <stdio.h>
+#include <string.h>
+
+#include "internal.cuh"
+
+namespace sccg {
+
+static thread_local char t_msg[256] = "";
+static thread_local int64_t t_index = -1;
+
+int set_error(int code, const char* msg, int64_t index) {
+  snprintf(t_msg, sizeof(t_msg), "%s", msg ? msg : "");
+  t_index = index;
+  return code;
+}
+
+int check_cuda(cudaError_t e, const char* where) {
+  if (e == cudaSuccess) return SCCG_OK;
+  char buf[256];
+  snprintf(buf, sizeof(buf), "%s: %s", where, cudaGetErrorString(e));
+  return set_error(SCCG_E_CUDA, buf);
+}
+
+size_t filter_ws_bytes(int64_t np, int64_t nq);
+int filter_pairs(const sccg_polyset* P, const sccg_polyset* Q, int32_t* pairs, int64_t cap, int64_t* n_pairs_host,
+                 void* ws, size_t ws_bytes, cudaStream_t stream);
+size_t pixelbox_ws_bytes(int64_t n);
+int run_pixelbox(const sccg_polyset* p, const sccg_polyset* q, const int32_t* pairs, int64_t n, int64_t* inter,
+                 int64_t* uni, sccg_sums* sums, const sccg_config* cfg, void* ws, size_t ws_bytes,
+                 cudaStream_t stream);
+
+static bool aligned(const void* p, size_t a) { return (reinterpret_cast<uintptr_t>(p) & (a - 1)) == 0; }
+
+static int check_set(const sccg_polyset* s, bool need_derived, const char* name) {
+  char buf[128];
+  if (!s) {
+    snprintf(buf, sizeof(buf), "%s: null sccg_polyset", name);
+    return set_error(SCCG_E_ARG, buf);
+  }
+  if (s->n_polygons < 0 || s->n_vertices < 0 || s->n_polygons >= (int64_t(1) << 31)) {
+    snprintf(buf, sizeof(buf), "%s: negative or too large size", name);
+    return set_error(SCCG_E_ARG, buf);
+  }
+  if ((s->n_vertices > 0 && !s->xy) || !s->offsets) {
+    snprintf(buf, sizeof(buf), "%s: null xy / offsets", name);
+    return set_error(SCCG_E_ARG, buf);
+  }
+  if (!aligned(s->xy, 8) || !aligned(s->offsets, 8)) {
+    snprintf(buf, sizeof(buf), "%s: xy / offsets must be 8-byte aligned", name);
+    return set_error(SCCG_E_ARG, buf);
+  }
+  if (need_derived && (!s->mbr || !s->area || !s->ecount || (!s->edges && s->n_vertices > 0) || !s->status)) {
+    snprintf(buf, sizeof(buf), "%s: derived buffers not bound (sccg_polyset_bind)", name);
+    return set_error(SCCG_E_ARG, buf);
+  }
+  if (need_derived && (!aligned(s->mbr, 16) || !aligned(s->edges, 8) || !aligned(s->area, 8))) {
+    snprintf(buf, sizeof(buf), "%s: derived buffers misaligned", name);
+    return set_error(SCCG_E_ARG, buf);
+  }
+  return SCCG_OK;
+}
+
+static size_t polyset_layout(int64_t n, int64_t nv, Carve& cv, sccg_polyset* s) {
+  int32_t* mbr = cv.take<int32_t>(4 * n);
+  int64_t* area = cv.take<int64_t>(n);
+  int32_t* ec = cv.take<int32_t>(2 * n);
+  uint64_t* ed = cv.take<uint64_t>(nv);
+  uint32_t* st = cv.take<uint32_t>(2);
+  if (s) {
+    s->mbr = mbr;
+    s->area = area;
+    s->ecount = ec;
+    s->edges = ed;
+    s->status = st;
+  }
+  return cv.used;
+}
+
+}  // namespace sccg
+
+using namespace sccg;
+
+extern "C" {
+
+int sccg_version(void) { return 1; }
+
+const char* sccg_strerror(int code) {
+  switch (code) {
+    case SCCG_OK: return "ok";
+    case SCCG_E_ARG: return "invalid argument";
+    case SCCG_E_NOT_RECTILINEAR: return "polygon edge is not axis-parallel";
+    case SCCG_E_RANGE: return "coordinate or polygon extent out of range";
+    case SCCG_E_CAPACITY: return "output buffer too small";
+    case SCCG_E_STACK: return "sampling-box stack overflow";
+    case SCCG_E_EMPTY: return "no pair with non-zero intersection (J' undefined)";
+    case SCCG_E_CUDA: return "CUDA error";
+    case SCCG_E_WORKSPACE: return "workspace too small";
+    default: return "unknown error";
+  }
+}
+
+const char* sccg_last_error_string(void) { return t_msg; }
+int64_t sccg_last_error_index(void) { return t_index; }
+
+size_t sccg_polyset_bytes(int64_t n_polygons, int64_t n_vertices) {
+  if (n_polygons < 0 || n_vertices < 0) return 0;
+  Carve cv{nullptr, ~size_t(0)};
+  return polyset_layout(n_polygons, n_vertices, cv, nullptr) + 256;
+}
+
+int sccg_polyset_bind(sccg_polyset* set, void* buf, size_t bytes) {
+  set_error(SCCG_OK, "", -1);
+  if (!set || !buf) return set_error(SCCG_E_ARG, "sccg_polyset_bind: null argument");
+  if (set->n_polygons < 0 || set->n_vertices < 0) return set_error(SCCG_E_ARG, "sccg_polyset_bind: negative size");
+  if (!aligned(buf, 256)) return set_error(SCCG_E_WORKSPACE, "sccg_polyset_bind: buffer must be 256-byte aligned");
+  Carve cv{reinterpret_cast<char*>(buf), bytes};
+  polyset_layout(set->n_polygons, set->n_vertices, cv, set);
+  if (!cv.ok) return set_error(SCCG_E_WORKSPACE, "sccg_polyset_bind: buffer smaller than sccg_polyset_bytes");
+  return SCCG_OK;
+}
+
+int sccg_prep(const sccg_polyset* set, int32_t validate, sccg_stream_t stream) {
+  set_error(SCCG_OK, "", -1);
+  if (int r = check_set(set, true, "set")) return r;
+  return check_cuda(launch_prep(set, validate, reinterpret_cast<cudaStream_t>(stream)), "sccg_prep");
+}
+
+size_t sccg_filter_workspace_bytes(int64_t n_p, int64_t n_q) {
+  if (n_p < 0 || n_q < 0) return 0;
+  return filter_ws_bytes(n_p, n_q);
+}
+
+int sccg_filter_pairs(const sccg_polyset* p, const sccg_polyset* q, int32_t* pairs, int64_t cap,
+                      int64_t* n_pairs_host, void* workspace, size_t ws_bytes, sccg_stream_t stream) {
+  set_error(SCCG_OK, "", -1);
+  if (int r = check_set(p, true, "p")) return r;
+  if (int r = check_set(q, true, "q")) return r;
+  if (!n_pairs_host) return set_error(SCCG_E_ARG, "n_pairs_host is null");
+  if (cap < 0) return set_error(SCCG_E_ARG, "negative capacity");
+  if (pairs && !aligned(pairs, 8)) return set_error(SCCG_E_ARG, "pairs must be 8-byte aligned");
+  if (!workspace || !aligned(workspace, 256))
+    return set_error(SCCG_E_WORKSPACE, "workspace must be non-null and 256-byte aligned");
+  *n_pairs_host = 0;
+  return filter_pairs(p, q, pairs, cap, n_pairs_host, workspace, ws_bytes, reinterpret_cast<cudaStream_t>(stream));
+}
+
+size_t sccg_pixelbox_workspace_bytes(int64_t n_pairs) { return n_pairs < 0 ? 0 : pixelbox_ws_bytes(n_pairs); }
+
+int sccg_pixelbox(const sccg_polyset* p, const sccg_polyset* q, const int32_t* pairs, int64_t n_pairs, int64_t* inter,
+                  int64_t* uni, sccg_sums* sums, const sccg_config* cfg, void* workspace, size_t ws_bytes,
+                  sccg_stream_t stream) {
+  set_error(SCCG_OK, "", -1);
+  if (int r = check_set(p, true, "p")) return r;
+  if (int r = check_set(q, true, "q")) return r;
+  if (n_pairs < 0) return set_error(SCCG_E_ARG, "negative n_pairs");
+  if (n_pairs > 0 && !pairs) return set_error(SCCG_E_ARG, "pairs is null");
+  if (!sums) return set_error(SCCG_E_ARG, "sums is null");
+  if (!aligned(sums, 8) || (pairs && !aligned(pairs, 8)) || (inter && !aligned(inter, 8)) || (uni && !aligned(uni, 8)))
+    return set_error(SCCG_E_ARG, "misaligned pointer");
+  if (cfg) {
+    if (cfg->threshold < 0) return set_error(SCCG_E_ARG, "config.threshold < 0");
+    if (cfg->block != 0 && cfg->block != 256) return set_error(SCCG_E_ARG, "config.block must be 0 or 256");
+    if (cfg->grid < 0) return set_error(SCCG_E_ARG, "config.grid < 0");
+  }
+  return run_pixelbox(p, q, pairs, n_pairs, inter, uni, sums, cfg, workspace, ws_bytes,
+                      reinterpret_cast<cudaStream_t>(stream));
+}
+
+int sccg_jaccard(const sccg_sums* s, double* jprime, double* pooled) {
+  set_error(SCCG_OK, "", -1);
+  if (!s || !jprime) return set_error(SCCG_E_ARG, "null argument");
+  if (s->n_nonzero <= 0) {
+    *jprime = NAN;
+    if (pooled) *pooled = NAN;
+    return set_error(SCCG_E_EMPTY, "no pair with |p n q| != 0");
+  }
+  // sum r = (L0 + L1 2^30 + L2 2^60 + L3 2^90) 2^-116; long double keeps 64
+  // mantissa bits, so the one rounding to double dominates (reading R12).
+  long double t = (long double)(uint64_t)s->ratio_limb[3];
+  t = t * 1073741824.0L + (long double)(uint64_t)s->ratio_limb[2];
+  t = t * 1073741824.0L + (long double)(uint64_t)s->ratio_limb[1];
+  t = t * 1073741824.0L + (long double)(uint64_t)s->ratio_limb[0];
+  t = ldexpl(t, -116);
+  *jprime = (double)(t / (long double)s->n_nonzero);
+  if (pooled) *pooled = (double)s->sum_inter / (double)s->sum_union;
+  return SCCG_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,84 @@
+// internal.cuh -- shared device helpers of the sm_100a PixelBox library.
+// Not part of the ABI (see include/sccg.h).  Shares nothing with oracle/.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "sccg.h"
+
+namespace sccg {
+
+// Edge record (8 bytes, sccg_polyset.edges), relative to the polygon's MBR
+// lower-left corner so every field fits 16 bits (MBR extent <= 65535):
+//   vertical edge   x = const : c = x - xlo,  lo = ymin - ylo, hi = ymax - ylo
+//   horizontal edge y = const : c = y - ylo,  lo = xmin - xlo, hi = xmax - xlo
+// Vertical records of polygon i occupy edges[off[i] .. off[i] + nv), horizontal
+// records edges[off[i+1] - nh .. off[i+1]) (nv + nh <= vertex count).
+__host__ __device__ inline uint64_t pack_edge(uint32_t c, uint32_t lo, uint32_t hi) {
+  return (uint64_t)c | ((uint64_t)lo << 16) | ((uint64_t)hi << 32);
+}
+__device__ __forceinline__ void unpack_edge(uint64_t r, int& c, int& lo, int& hi) {
+  c = (int)(r & 0xffffu);
+  lo = (int)((r >> 16) & 0xffffu);
+  hi = (int)((r >> 32) & 0xffffu);
+}
+
+constexpr int kMaxExtent = 65535;
+constexpr int64_t kMaxCoord = int64_t(1) << 30;
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+// 32-bit shift left with PTX clamping: shift >= 32 gives 0.
+__device__ __forceinline__ unsigned shl_clamp(unsigned a, unsigned s) {
+  unsigned d;
+  asm("shl.b32 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(s));
+  return d;
+}
+// Mask of the pixels of a 32-pixel row word at or right of column k (k may be
+// < 0 -> all, >= 32 -> none): the pixels an edge at x = k toggles when the
+// crossing parity is counted toward -x (same parity as toward +x, because every
+// row of a closed ring is crossed an even number of times).
+__device__ __forceinline__ unsigned suffix_mask(int k) { return shl_clamp(0xffffffffu, (unsigned)max(k, 0)); }
+// Low `n` bits (n in [0, 32]).
+__device__ __forceinline__ unsigned low_bits(int n) { return ~shl_clamp(0xffffffffu, (unsigned)max(n, 0)); }
+
+struct DevSet {
+  const int64_t* off;
+  const int4* mbr;
+  const int64_t* area;
+  const int2* ecount;
+  const uint64_t* edges;
+};
+
+inline DevSet dev_set(const sccg_polyset* s) {
+  return DevSet{s->offsets, reinterpret_cast<const int4*>(s->mbr), s->area,
+                reinterpret_cast<const int2*>(s->ecount), s->edges};
+}
+
+// Bump allocator over a caller workspace (256-byte aligned slices).
+struct Carve {
+  char* base;
+  size_t cap, used = 0;
+  bool ok = true;
+  template <class T>
+  T* take(size_t n) {
+    size_t a = (used + 255) & ~size_t(255);
+    size_t bytes = n * sizeof(T);
+    if (a + bytes > cap) ok = false;
+    used = a + bytes;
+    return ok && base ? reinterpret_cast<T*>(base + a) : nullptr;
+  }
+};
+
+// error slot (api.cu)
+int set_error(int code, const char* msg, int64_t index = -1);
+int check_cuda(cudaError_t e, const char* where);
+
+// launchers
+cudaError_t launch_prep(const sccg_polyset* set, int validate, cudaStream_t st);
+
+}  // namespace sccg

@@ -1,0 +1,110 @@
+"""C-ABI checks that need no GPU (``-m "not gpu"``): the sm_100a library builds,
+loads, exports exactly the symbols include/sccg.h declares, and its host-only
+logic (argument checking, workspace carving, sccg_jaccard on integer sums)
+behaves as documented."""
+import ctypes
+import math
+import os
+import re
+import subprocess
+from fractions import Fraction
+
+import numpy as np
+
+import oracle
+import paper_1208_0277_b200 as sccg
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_symbols():
+    with open(os.path.join(ROOT, "include", "sccg.h")) as f:
+        return sorted(set(re.findall(r"SCCG_API [^;(]*?\b(sccg_\w+)\(", f.read())))
+
+
+def test_library_exports_exactly_the_header():
+    lib = sccg.load()
+    assert lib.sccg_version() == 1
+    syms = header_symbols()
+    assert set(syms) == set(sccg.SYMBOLS)
+    out = subprocess.run(["nm", "-D", "--defined-only", sccg.library_path()], capture_output=True, text=True).stdout
+    exported = sorted(l.split()[-1] for l in out.splitlines() if " T " in l)
+    assert exported == syms
+
+
+def test_library_is_sm100a_only():
+    out = subprocess.run(["cuobjdump", "--list-elf", sccg.library_path()], capture_output=True, text=True).stdout
+    arches = set(re.findall(r"sm_\d+a?", out))
+    assert arches == {"sm_100a"}, arches
+
+
+def test_strerror_and_error_slot():
+    lib = sccg.load()
+    for code in range(9):
+        assert lib.sccg_strerror(code)
+    assert lib.sccg_strerror(sccg.E_EMPTY).decode().startswith("no pair")
+
+
+def _sums_from(inter, uni):
+    units = 0
+    nz = 0
+    for i, u in zip(inter, uni):
+        if i:
+            units += int(Fraction(int(i) / int(u)) * (1 << 116))
+            nz += 1
+    limbs = []
+    for k in range(3):
+        limbs.append(units & ((1 << 30) - 1))
+        units >>= 30
+    limbs.append(units)
+    s = sccg.Sums()
+    s.n_pairs = len(inter)
+    s.n_nonzero = nz
+    s.sum_inter = int(sum(inter))
+    s.sum_union = int(sum(u for i, u in zip(inter, uni) if i))
+    s.limb0, s.limb1, s.limb2, s.limb3 = limbs
+    return s
+
+
+def test_jaccard_host_logic_against_oracle():
+    rng = np.random.default_rng(5)
+    for n in (1, 2, 7, 1000, 20000):
+        uni = rng.integers(1, 10**6, n)
+        inter = (uni * rng.random(n)).astype(np.int64)
+        inter[rng.random(n) < 0.2] = 0
+        if not inter.any():
+            inter[0] = 1
+        s = _sums_from(inter, uni)
+        j, pooled = sccg.jaccard(s)
+        ex = oracle.jaccard_exact(inter, uni)
+        assert abs(j - float(ex)) <= 1e-12 * float(ex)
+        assert pooled == s.sum_inter / s.sum_union
+    # SPEC S:364 example {(1,7),(1,1)} -> 4/7
+    j, _ = sccg.jaccard(_sums_from([1, 1], [7, 1]))
+    assert abs(j - 4 / 7) <= 1e-15
+    # Eq. 1 over an empty set: NaN + SCCG_E_EMPTY
+    j, p = sccg.jaccard(sccg.Sums())
+    assert math.isnan(j) and math.isnan(p)
+    lib = sccg.load()
+    jj = ctypes.c_double()
+    assert lib.sccg_jaccard(ctypes.byref(sccg.Sums()), ctypes.byref(jj), None) == sccg.E_EMPTY
+
+
+def test_host_argument_checks():
+    lib = sccg.load()
+    assert lib.sccg_polyset_bytes(-1, 0) == 0
+    b1 = lib.sccg_polyset_bytes(10, 100)
+    b2 = lib.sccg_polyset_bytes(20, 200)
+    assert 0 < b1 < b2
+    s = sccg.PolySet()
+    s.n_polygons, s.n_vertices = 10, 100
+    assert lib.sccg_polyset_bind(ctypes.byref(s), None, b1) == sccg.E_ARG
+    assert lib.sccg_polyset_bind(ctypes.byref(s), 0x1001, b1) == sccg.E_WORKSPACE  # misaligned
+    assert lib.sccg_polyset_bind(ctypes.byref(s), 0x100000, b1 - 512) == sccg.E_WORKSPACE  # too small
+    assert lib.sccg_polyset_bind(ctypes.byref(s), 0x100000, b1) == sccg.OK
+    assert s.mbr % 256 == 0 and s.edges % 8 == 0
+    assert lib.sccg_prep(None, 1, None) == sccg.E_ARG
+    n = ctypes.c_int64()
+    assert lib.sccg_filter_pairs(None, None, None, 0, ctypes.byref(n), None, 0, None) == sccg.E_ARG
+    cfg = sccg.Config(-1, 0, 0, 0, None)
+    assert lib.sccg_pixelbox(None, None, None, 0, None, None, None, ctypes.byref(cfg), None, 0, None) == sccg.E_ARG

@@ -1,0 +1,271 @@
+"""GPU parity: the CUDA path, called through the C ABI, against the CPU oracle.
+
+Bar (BASELINE.json north_star): per-pair areas and the integer sums bit-exact;
+J' within 1e-12 relative of the exact rational mean.  Inputs are seeded and
+synthetic (synth/), at sizes the oracle finishes in seconds that still span many
+warps, ragged tails and every code path (pixelization, sampling boxes, the
+shared-memory overflow path), plus the full-size bench configuration on
+sampled pairs and on size-independent properties.
+"""
+import math
+from fractions import Fraction
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from synth import combs
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def sccg():
+    if not torch.cuda.is_available():
+        pytest.fail("CUDA device required for -m gpu tests (no CPU fallback exists)")
+    import paper_1208_0277_b200 as m
+
+    m.load()
+    return m
+
+
+def dev(pset, sccg):
+    xy, off = sccg.to_device(pset.xy, pset.offsets)
+    return sccg.DeviceSet(xy, off)
+
+
+def exact_ratio_units(inter, uni):
+    """sum over I != 0 of RN64(I/U) * 2^116, exactly (Python floats are IEEE RN)."""
+    tot = 0
+    for i, u in zip(inter, uni):
+        if i:
+            tot += int(Fraction(int(i) / int(u)) * (1 << 116))
+    return tot
+
+
+def check_batch(sccg, A, B, pairs_np, inter, uni, sums, exact=True):
+    """Compare a whole batch against the oracle, element by element."""
+    ei, eu = oracle.pair_areas(A, B, pairs_np)
+    gi, gu = inter.cpu().numpy(), uni.cpu().numpy()
+    bad = np.nonzero((gi != ei) | (gu != eu))[0]
+    assert len(bad) == 0, f"{len(bad)} mismatches, first {bad[:5]}: gpu {gi[bad[:5]]} {gu[bad[:5]]} oracle {ei[bad[:5]]} {eu[bad[:5]]}"
+    s = sums.cpu().tolist()
+    os_ = oracle.sums(A, B, pairs_np, ei, eu)
+    for k, f in enumerate(["n_pairs", "n_nonzero", "sum_inter", "sum_union", "sum_area_p", "sum_area_q"]):
+        assert s[k] == os_[f], f
+    assert s[10] == 0, f"status {s[10]}"
+    limbs = s[6:10]
+    assert sum(l << (30 * i) for i, l in enumerate(limbs)) == exact_ratio_units(ei, eu)
+    j, pooled = sccg.jaccard(sums)
+    ex = oracle.jaccard_exact(ei, eu)
+    if ex is None:
+        assert math.isnan(j)
+    else:
+        assert abs(j - float(ex)) <= 1e-12 * float(ex)
+        assert abs(j - oracle.jaccard(ei, eu)) <= 1e-12 * float(ex)
+    return ei, eu
+
+
+# ------------------------------------------------------------------ prep
+def test_prep_matches_oracle(sccg, tile_sets):
+    for s in tile_sets:
+        D = dev(s, sccg)
+        area, mbr = oracle.set_props(s)
+        assert (D.area.cpu().numpy() == area).all()
+        assert (D.mbr.cpu().numpy() == mbr).all()
+        assert D.status.cpu().tolist()[0] == 0
+
+
+# ---------------------------------------------------------------- filter
+@pytest.mark.parametrize("config", ["tile", "skewed"])
+def test_filter_pairs_matches_oracle(sccg, config):
+    A, B = synth.generate(config)
+    P, Q = dev(A, sccg), dev(B, sccg)
+    got = sccg.filter_pairs(P, Q).cpu().numpy()
+    want = oracle.join(A, B)
+    assert got.shape == want.shape and (got == want).all()
+
+
+def test_filter_random_boxes_and_touching(sccg):
+    rng = np.random.default_rng(11)
+    for trial in range(20):
+        rings = []
+        for n in rng.integers(1, 300, 2):
+            rs = []
+            for _ in range(n):
+                x, y = (int(v) for v in rng.integers(-500, 500, 2))
+                w, h = (int(v) for v in rng.integers(1, 60, 2))
+                rs.append([[x, y], [x + w, y], [x + w, y + h], [x, y + h]])
+            rings.append(synth.pack(rs))
+        A, B = rings
+        got = sccg.filter_pairs(dev(A, sccg), dev(B, sccg)).cpu().numpy()
+        assert got.tolist() == oracle.join(A, B, "nested").tolist()
+    # touching MBRs share no pixel -> no pair (reading R4)
+    A = synth.pack([[[0, 0], [2, 0], [2, 2], [0, 2]]])
+    B = synth.pack([[[2, 0], [4, 0], [4, 2], [2, 2]], [[0, 2], [2, 2], [2, 4], [0, 4]]])
+    assert sccg.filter_pairs(dev(A, sccg), dev(B, sccg)).shape[0] == 0
+
+
+def test_filter_capacity_retry(sccg, tile_sets):
+    A, B = tile_sets
+    got = sccg.filter_pairs(dev(A, sccg), dev(B, sccg), cap=3).cpu().numpy()
+    assert got.tolist() == oracle.join(A, B).tolist()
+
+
+# -------------------------------------------------------------- pixelbox
+@pytest.mark.parametrize("T", [2, 37, 512, 2048, 1 << 30])
+def test_pixelbox_tile_all_T(sccg, tile_sets, T):
+    A, B = tile_sets
+    P, Q = dev(A, sccg), dev(B, sccg)
+    pairs = sccg.filter_pairs(P, Q)
+    inter, uni, sums = sccg.pixelbox(P, Q, pairs, threshold=T)
+    check_batch(sccg, A, B, pairs.cpu().numpy(), inter, uni, sums)
+
+
+def test_pixelbox_pixelonly_mode(sccg, tile_sets):
+    A, B = tile_sets
+    P, Q = dev(A, sccg), dev(B, sccg)
+    pairs = sccg.filter_pairs(P, Q)
+    inter, uni, sums = sccg.pixelbox(P, Q, pairs, mode=1)
+    check_batch(sccg, A, B, pairs.cpu().numpy(), inter, uni, sums)
+
+
+@pytest.mark.parametrize("T", [64, 2048])
+def test_pixelbox_skewed_glands(sccg, T):
+    """Config 3 analog: nuclei + glands (MBR side up to 512, ~1000 vertices):
+    deep sampling-box subdivision and the shared-memory overflow path."""
+    A, B = synth.generate("skewed", width=8192, height=8192)
+    P, Q = dev(A, sccg), dev(B, sccg)
+    pairs = sccg.filter_pairs(P, Q)
+    counters = torch.zeros(8, dtype=torch.int64, device="cuda")
+    inter, uni, sums = sccg.pixelbox(P, Q, pairs, threshold=T, counters=counters)
+    check_batch(sccg, A, B, pairs.cpu().numpy(), inter, uni, sums)
+    c = counters.cpu().tolist()
+    assert c[sccg.CNT_SPLITS] > 0 and c[sccg.CNT_PIXBOXES] > 0
+
+
+def test_pixelbox_combs_closed_form(sccg):
+    """Config 5 analog: highly concave combs, pinned by rectangle decomposition."""
+    A, B, (RA, RB) = combs.generate(n_pairs=96, want_rects=True)
+    P, Q = dev(A, sccg), dev(B, sccg)
+    pairs = sccg.filter_pairs(P, Q)
+    assert pairs.cpu().numpy().tolist() == [[k, k] for k in range(96)]
+    for T in (256, 4096):
+        inter, uni, sums = sccg.pixelbox(P, Q, pairs, threshold=T)
+        gi = inter.cpu().numpy()
+        for k in range(96):
+            assert gi[k] == combs.rect_decomp_intersection(RA[k], RB[k])
+    check_batch(sccg, A, B, pairs.cpu().numpy()[:24], *sccg.pixelbox(P, Q, pairs[:24]))
+
+
+def test_pixelbox_exhaustive_tiny(sccg):
+    """Every clean 3x3 polyomino against every other at offsets in [-2, 2]^2."""
+    import itertools
+
+    polys = []
+    for bits in range(1, 512):
+        m = np.array([(bits >> i) & 1 for i in range(9)], np.uint8).reshape(3, 3)
+        ring, cleaned = synth.trace_mask(m)
+        if ring is not None and (cleaned == m).all():
+            polys.append(ring)
+    offs = list(itertools.product(range(-2, 3), repeat=2))
+    A = synth.pack(polys)
+    B = synth.pack([r + np.array(o, np.int32) for r in polys for o in offs])
+    P, Q = dev(A, sccg), dev(B, sccg)
+    pairs_np = np.array([(i, j) for i in range(len(polys)) for j in range(len(polys) * len(offs))], np.int32)
+    pairs = torch.from_numpy(pairs_np).cuda()
+    for T in (2, 4, 2048):
+        inter, uni, sums = sccg.pixelbox(P, Q, pairs, threshold=T)
+        ei, eu = oracle.pair_areas(A, B, pairs_np)
+        assert (inter.cpu().numpy() == ei).all() and (uni.cpu().numpy() == eu).all()
+
+
+def test_pixelbox_edge_cases(sccg, tile_sets):
+    A, B = tile_sets
+    P, Q = dev(A, sccg), dev(B, sccg)
+    # empty batch
+    inter, uni, sums = sccg.pixelbox(P, Q, torch.zeros((0, 2), dtype=torch.int32, device="cuda"))
+    assert inter.numel() == 0 and sums.cpu().tolist() == [0] * 11
+    assert math.isnan(sccg.jaccard(sums)[0])
+    # pairs with disjoint MBRs are allowed: I = 0, U = |p| + |q|
+    pairs_np = np.array([[0, B.n - 1], [A.n - 1, 0], [3, 3]], np.int32)
+    inter, uni, sums = sccg.pixelbox(P, Q, torch.from_numpy(pairs_np).cuda())
+    check_batch(sccg, A, B, pairs_np, inter, uni, sums)
+    # a single ragged pair, identical polygons -> r = 1 exactly
+    pairs_np = np.array([[5, 5]], np.int32)
+    inter, uni, sums = sccg.pixelbox(P, P, torch.from_numpy(pairs_np).cuda())
+    assert inter.item() == uni.item() == oracle.area_shoelace(A.ring(5))
+    assert sccg.jaccard(sums)[0] == 1.0
+    # out-of-range pair index: skipped and flagged, never read out of bounds
+    bad = torch.tensor([[0, 10**6]], dtype=torch.int32, device="cuda")
+    _, _, sums = sccg.pixelbox(P, Q, bad)
+    assert sums.cpu().tolist()[10] != 0
+
+
+def test_sums_accumulate_and_launch_shape_invariance(sccg, tile_sets):
+    A, B = tile_sets
+    P, Q = dev(A, sccg), dev(B, sccg)
+    pairs = sccg.filter_pairs(P, Q)
+    ref = sccg.pixelbox(P, Q, pairs)
+    for grid in (1, 3, 37):
+        got = sccg.pixelbox(P, Q, pairs, grid=grid)
+        assert torch.equal(got[0], ref[0]) and torch.equal(got[1], ref[1]) and torch.equal(got[2], ref[2])
+    # batching: two halves accumulated into one sums == one call
+    sums = sccg.new_sums()
+    h = pairs.shape[0] // 2
+    sccg.pixelbox(P, Q, pairs[:h], sums=sums)
+    sccg.pixelbox(P, Q, pairs[h:], sums=sums)
+    assert torch.equal(sums, ref[2])
+
+
+def test_abi_errors(sccg):
+    bad = synth.pack([[[0, 0], [3, 1], [3, 3], [0, 3]]])  # diagonal edge
+    good = synth.pack([[[0, 0], [3, 0], [3, 3], [0, 3]]])
+    with pytest.raises(sccg.SccgError) as e:
+        sccg.filter_pairs(dev(bad, sccg), dev(good, sccg))
+    assert e.value.code == sccg.E_NOT_RECTILINEAR and e.value.index == 0
+    wide = synth.pack([[[0, 0], [70000, 0], [70000, 3], [0, 3]]])
+    with pytest.raises(sccg.SccgError) as e:
+        sccg.filter_pairs(dev(good, sccg), dev(wide, sccg))
+    assert e.value.code == sccg.E_RANGE
+    tri = synth.PolygonSet(np.array([[0, 0], [1, 0], [1, 1]], np.int32), np.array([0, 3], np.int64))
+    with pytest.raises(sccg.SccgError) as e:
+        sccg.filter_pairs(dev(tri, sccg), dev(good, sccg))
+    assert e.value.code == sccg.E_ARG
+    # empty sets
+    empty = synth.PolygonSet(np.zeros((0, 2), np.int32), np.zeros(1, np.int64))
+    assert sccg.filter_pairs(dev(empty, sccg), dev(good, sccg)).shape[0] == 0
+
+
+# --------------------------------------------------- full bench configuration
+def test_slide_full_size(sccg):
+    """Config 2 (the bench workload) at full size, in the bench's launch
+    configuration: the whole pair list equals the oracle's sweep join, sampled
+    pairs are bit-exact, and size-independent properties hold for all pairs."""
+    A, B = synth.generate("slide")
+    P, Q = dev(A, sccg), dev(B, sccg)
+    pairs = sccg.filter_pairs(P, Q)
+    pn = pairs.cpu().numpy()
+    want = oracle.join(A, B)
+    assert pn.shape == want.shape and (pn == want).all()
+    inter, uni, sums = sccg.pixelbox(P, Q, pairs)
+    gi, gu = inter.cpu().numpy(), uni.cpu().numpy()
+    rng = np.random.default_rng(2)
+    idx = np.sort(rng.choice(len(pn), size=20000, replace=False))
+    ei, eu = oracle.pair_areas(A, B, pn[idx])
+    assert (gi[idx] == ei).all() and (gu[idx] == eu).all()
+    ap, _ = oracle.set_props(A)
+    aq, _ = oracle.set_props(B)
+    a_p, a_q = ap[pn[:, 0]], aq[pn[:, 1]]
+    assert (gi >= 0).all() and (gi <= np.minimum(a_p, a_q)).all()
+    assert (gi + gu == a_p + a_q).all() and (gu >= np.maximum(a_p, a_q)).all()
+    s = sums.cpu().tolist()
+    assert s[0] == len(pn) and s[2] == int(gi.sum()) and s[4] == int(a_p.sum()) and s[5] == int(a_q.sum())
+    assert s[1] == int((gi > 0).sum()) and s[10] == 0
+    assert sum(l << (30 * i) for i, l in enumerate(s[6:10])) == exact_ratio_units(gi, gu)
+    # determinism across thresholds: per-pair results identical
+    i2, u2, s2 = sccg.pixelbox(P, Q, pairs, threshold=64)
+    assert torch.equal(i2, inter) and torch.equal(s2, sums)
