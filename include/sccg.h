@@ -90,6 +90,7 @@ typedef struct {
   int32_t* ecount;        /* [n_polygons][2] number of vertical, horizontal edges */
   uint64_t* edges;        /* [n_vertices] edge records (internal layout) */
   uint32_t* status;       /* [2] device: status bits (OR), lowest offending polygon (MIN) */
+  void* stats;            /* [128 bytes] device: set statistics the join sizes its grid from (internal) */
 } sccg_polyset;
 
 /* Bytes of derived storage for a set (for sccg_polyset_bind). */

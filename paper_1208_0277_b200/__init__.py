@@ -60,6 +60,7 @@ class PolySet(ctypes.Structure):
         ("ecount", ctypes.c_void_p),
         ("edges", ctypes.c_void_p),
         ("status", ctypes.c_void_p),
+        ("stats", ctypes.c_void_p),
     ]
 
 
@@ -78,6 +79,9 @@ class Config(ctypes.Structure):
 
 
 def library_path() -> str:
+    v = os.environ.get("SCCG_LIB")
+    if v:
+        return v if os.path.isabs(v) else os.path.join(os.path.dirname(_build.LIB), v)
     return _build.LIB
 
 
@@ -88,6 +92,10 @@ def load(build: bool = True):
         if _lib is not None:
             return _lib
         path = _build.LIB
+        variant = os.environ.get("SCCG_LIB")  # experiment variant built by build.py --variant
+        if variant:
+            path = variant if os.path.isabs(variant) else os.path.join(os.path.dirname(_build.LIB), variant)
+            build = False
         if build:
             try:
                 path = _build.build()
@@ -171,7 +179,7 @@ class DeviceSet:
         self.n, self.nv = n, nv
         nbytes = int(lib.sccg_polyset_bytes(n, nv))
         self._buf = torch.empty(nbytes, dtype=torch.uint8, device=xy.device)
-        self.c = PolySet(xy.data_ptr(), offsets.data_ptr(), n, nv, None, None, None, None, None)
+        self.c = PolySet(xy.data_ptr(), offsets.data_ptr(), n, nv, None, None, None, None, None, None)
         _check(lib.sccg_polyset_bind(ctypes.byref(self.c), self._buf.data_ptr(), nbytes), "sccg_polyset_bind")
         if prep:
             self.prep(validate, stream)

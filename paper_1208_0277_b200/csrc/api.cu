@@ -53,7 +53,7 @@ static int check_set(const sccg_polyset* s, bool need_derived, const char* name)
     snprintf(buf, sizeof(buf), "%s: xy / offsets must be 8-byte aligned", name);
     return set_error(SCCG_E_ARG, buf);
   }
-  if (need_derived && (!s->mbr || !s->area || !s->ecount || (!s->edges && s->n_vertices > 0) || !s->status)) {
+  if (need_derived && (!s->mbr || !s->area || !s->ecount || (!s->edges && s->n_vertices > 0) || !s->status || !s->stats)) {
     snprintf(buf, sizeof(buf), "%s: derived buffers not bound (sccg_polyset_bind)", name);
     return set_error(SCCG_E_ARG, buf);
   }
@@ -70,7 +70,9 @@ static size_t polyset_layout(int64_t n, int64_t nv, Carve& cv, sccg_polyset* s) 
   int32_t* ec = cv.take<int32_t>(2 * n);
   uint64_t* ed = cv.take<uint64_t>(nv);
   uint32_t* st = cv.take<uint32_t>(2);
+  SetStats* ss = cv.take<SetStats>(1);
   if (s) {
+    s->stats = ss;
     s->mbr = mbr;
     s->area = area;
     s->ecount = ec;

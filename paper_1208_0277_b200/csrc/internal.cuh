@@ -46,6 +46,19 @@ __device__ __forceinline__ unsigned suffix_mask(int k) { return shl_clamp(0xffff
 // Low `n` bits (n in [0, 32]).
 __device__ __forceinline__ unsigned low_bits(int n) { return ~shl_clamp(0xffffffffu, (unsigned)max(n, 0)); }
 
+// Per-set statistics written by sccg_prep (sccg_polyset.stats), read by the
+// join's on-device grid selection.  entries[k - kStatK0] = sum over non-empty
+// MBRs of the number of 2^k-pixel grid cells the MBR covers.
+constexpr int kStatK0 = 3, kStatNK = 11;
+struct SetStats {
+  int32_t bounds[4];  // xmin, ymin, xmax, ymax over non-empty MBRs
+  int32_t maxext[2];  // largest MBR width, height
+  int32_t pad[2];
+  unsigned long long nonempty;
+  unsigned long long entries[kStatNK];
+};
+static_assert(sizeof(SetStats) == 128, "SetStats layout");
+
 struct DevSet {
   const int64_t* off;
   const int4* mbr;

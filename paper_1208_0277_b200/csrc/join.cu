@@ -9,97 +9,72 @@
 // point (max xlo, max ylo) so it is found exactly once.  Each P's pairs are
 // written to its own segment (exclusive scan of per-P counts) and sorted by q
 // in place, so the output is sorted by (p, q) without a global sort.
+//
+// The cell size is chosen on the device from the per-set statistics sccg_prep
+// gathered (no host round trip); the only host synchronisation is the final
+// pair count the ABI returns.
 #include <cub/device/device_scan.cuh>
 
 #include "internal.cuh"
 
 namespace sccg {
 
-constexpr int kKMin = 3, kKMax = 30, kNK = kKMax - kKMin + 1;
-
-struct JoinStats {
-  int32_t bounds[4];              // xmin, ymin (atomicMin), xmax, ymax (atomicMax) over non-empty MBRs
-  unsigned long long entries[2][32];  // per set, per k: sum of cells covered
+struct Grid {
+  int k, cx0, cy0, ncx, ncy, empty;
+  __device__ __forceinline__ int cell(int x, int y) const { return ((y >> k) - cy0) * ncx + ((x >> k) - cx0); }
 };
 
 __device__ __forceinline__ bool mbr_empty(const int4& m) { return m.x >= m.z || m.y >= m.w; }
 
-__global__ void join_stats_kernel(const int4* __restrict__ mp, int64_t np, const int4* __restrict__ mq, int64_t nq,
-                                  JoinStats* st) {
-  __shared__ unsigned long long s_ent[2][kNK];
-  __shared__ int s_b[4];
-  for (int i = threadIdx.x; i < 2 * kNK; i += blockDim.x) (&s_ent[0][0])[i] = 0;
-  if (threadIdx.x == 0) {
-    s_b[0] = s_b[1] = INT_MAX;
-    s_b[2] = s_b[3] = INT_MIN;
+static int64_t cell_cap(int64_t np, int64_t nq) { return np + nq + 1024; }
+static int64_t entry_cap(int64_t nq) { return 4 * nq + 1024; }
+
+// Cell size 2^k minimising the expected work E_p + E_q + C/4 + E_p E_q / C
+// (bucket inserts + probes + scan + candidate tests) subject to the workspace
+// caps on cells C and Q-entries E_q.  Always feasible: once 2^k exceeds the
+// largest MBR extent each MBR covers at most 2 x 2 cells.
+__global__ void grid_select_kernel(const SetStats* __restrict__ sp, const SetStats* __restrict__ sq, long long ccap,
+                                   long long ecap, Grid* g) {
+  if (threadIdx.x != 0) return;
+  Grid r{30, 0, 0, 1, 1, 0};
+  if (sp->nonempty == 0 || sq->nonempty == 0) {
+    r.empty = 1;
+    *g = r;
+    return;
   }
-  __syncthreads();
-  int bx0 = INT_MAX, by0 = INT_MAX, bx1 = INT_MIN, by1 = INT_MIN;
-  for (int s = 0; s < 2; s++) {
-    const int4* m_ = s == 0 ? mp : mq;
-    const int64_t n_ = s == 0 ? np : nq;
-    unsigned long long ent[kNK];
-#pragma unroll
-    for (int k = 0; k < kNK; k++) ent[k] = 0;
-    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n_; i += int64_t(gridDim.x) * blockDim.x) {
-      const int4 m = m_[i];
-      if (mbr_empty(m)) continue;
-      bx0 = min(bx0, m.x);
-      by0 = min(by0, m.y);
-      bx1 = max(bx1, m.z);
-      by1 = max(by1, m.w);
-#pragma unroll
-      for (int k = 0; k < kNK; k++) {
-        const int kk = k + kKMin;
-        unsigned long long cx = (unsigned)(((m.z - 1) >> kk) - (m.x >> kk) + 1);
-        unsigned long long cy = (unsigned)(((m.w - 1) >> kk) - (m.y >> kk) + 1);
-        ent[k] += cx * cy;
-      }
+  const int xmin = min(sp->bounds[0], sq->bounds[0]), ymin = min(sp->bounds[1], sq->bounds[1]);
+  const int xmax = max(sp->bounds[2], sq->bounds[2]), ymax = max(sp->bounds[3], sq->bounds[3]);
+  double best = 1e300;
+  for (int k = kStatK0; k <= 30; k++) {
+    const double ncx = (double)(((xmax - 1) >> k) - (xmin >> k) + 1);
+    const double ncy = (double)(((ymax - 1) >> k) - (ymin >> k) + 1);
+    const double C = ncx * ncy;
+    double Ep, Eq;
+    if (k - kStatK0 < kStatNK) {
+      Ep = (double)sp->entries[k - kStatK0];
+      Eq = (double)sq->entries[k - kStatK0];
+    } else {
+      Ep = (double)sp->nonempty * (double)(((sp->maxext[0] - 1) >> k) + 2) * (double)(((sp->maxext[1] - 1) >> k) + 2);
+      Eq = (double)sq->nonempty * (double)(((sq->maxext[0] - 1) >> k) + 2) * (double)(((sq->maxext[1] - 1) >> k) + 2);
     }
-#pragma unroll
-    for (int k = 0; k < kNK; k++) {
-      unsigned long long v = ent[k];
-      for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-      if ((threadIdx.x & 31) == 0 && v) atomicAdd(&s_ent[s][k], v);
+    if (C > (double)ccap || Eq > (double)ecap) continue;
+    const double cost = Ep + Eq + 0.25 * C + Ep * Eq / C;
+    if (cost < best) {
+      best = cost;
+      r.k = k;
     }
   }
-  bx0 = __reduce_min_sync(0xffffffffu, bx0);
-  by0 = __reduce_min_sync(0xffffffffu, by0);
-  bx1 = __reduce_max_sync(0xffffffffu, bx1);
-  by1 = __reduce_max_sync(0xffffffffu, by1);
-  if ((threadIdx.x & 31) == 0) {
-    atomicMin(&s_b[0], bx0);
-    atomicMin(&s_b[1], by0);
-    atomicMax(&s_b[2], bx1);
-    atomicMax(&s_b[3], by1);
-  }
-  __syncthreads();
-  for (int i = threadIdx.x; i < 2 * kNK; i += blockDim.x) {
-    unsigned long long v = (&s_ent[0][0])[i];
-    if (v) atomicAdd(&st->entries[i / kNK][i % kNK], v);
-  }
-  if (threadIdx.x == 0) {
-    atomicMin(&st->bounds[0], s_b[0]);
-    atomicMin(&st->bounds[1], s_b[1]);
-    atomicMax(&st->bounds[2], s_b[2]);
-    atomicMax(&st->bounds[3], s_b[3]);
-  }
+  r.cx0 = xmin >> r.k;
+  r.cy0 = ymin >> r.k;
+  r.ncx = ((xmax - 1) >> r.k) - r.cx0 + 1;
+  r.ncy = ((ymax - 1) >> r.k) - r.cy0 + 1;
+  *g = r;
 }
 
-__global__ void join_stats_init(JoinStats* st) {
-  for (int i = threadIdx.x; i < 64; i += blockDim.x) (&st->entries[0][0])[i] = 0;
-  if (threadIdx.x == 0) {
-    st->bounds[0] = st->bounds[1] = INT_MAX;
-    st->bounds[2] = st->bounds[3] = INT_MIN;
-  }
-}
-
-struct Grid {
-  int k, cx0, cy0, ncx, ncy;
-  __device__ __forceinline__ int cell(int x, int y) const { return ((y >> k) - cy0) * ncx + ((x >> k) - cx0); }
-};
-
-__global__ void grid_count_kernel(const int4* __restrict__ mq, int64_t nq, Grid g, int* __restrict__ cell_count) {
+__global__ void grid_count_kernel(const int4* __restrict__ mq, int64_t nq, const Grid* __restrict__ gp,
+                                  int* __restrict__ cell_count) {
+  const Grid g = *gp;
+  if (g.empty) return;
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < nq; i += int64_t(gridDim.x) * blockDim.x) {
     const int4 m = mq[i];
     if (mbr_empty(m)) continue;
@@ -108,15 +83,20 @@ __global__ void grid_count_kernel(const int4* __restrict__ mq, int64_t nq, Grid 
   }
 }
 
-__global__ void grid_fill_kernel(const int4* __restrict__ mq, int64_t nq, Grid g, const int* __restrict__ cell_start,
-                                 int* __restrict__ cell_fill, int* __restrict__ items) {
+// Fill: counts are decremented back to zero as slots are taken, so the count
+// array needs no second memset.
+__global__ void grid_fill_kernel(const int4* __restrict__ mq, int64_t nq, const Grid* __restrict__ gp,
+                                 const int* __restrict__ cell_start, int* __restrict__ cell_count,
+                                 int* __restrict__ items) {
+  const Grid g = *gp;
+  if (g.empty) return;
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < nq; i += int64_t(gridDim.x) * blockDim.x) {
     const int4 m = mq[i];
     if (mbr_empty(m)) continue;
     for (int cy = m.y >> g.k; cy <= (m.w - 1) >> g.k; cy++)
       for (int cx = m.x >> g.k; cx <= (m.z - 1) >> g.k; cx++) {
         const int c = (cy - g.cy0) * g.ncx + cx - g.cx0;
-        items[cell_start[c] + atomicAdd(&cell_fill[c], 1)] = (int)i;
+        items[cell_start[c] + atomicSub(&cell_count[c], 1) - 1] = (int)i;
       }
   }
 }
@@ -125,14 +105,15 @@ __global__ void grid_fill_kernel(const int4* __restrict__ mq, int64_t nq, Grid g
 // its reference point (max xlo, max ylo).  WRITE=false counts, WRITE=true
 // writes the segment then insertion-sorts it by q.
 template <bool WRITE>
-__global__ void probe_kernel(const int4* __restrict__ mp, int64_t np, const int4* __restrict__ mq, Grid g,
-                             const int* __restrict__ cell_start, const int* __restrict__ items,
-                             long long* __restrict__ count, const long long* __restrict__ start,
-                             int2* __restrict__ pairs) {
+__global__ void probe_kernel(const int4* __restrict__ mp, int64_t np, const int4* __restrict__ mq,
+                             const Grid* __restrict__ gp, const int* __restrict__ cell_start,
+                             const int* __restrict__ items, long long* __restrict__ count,
+                             const long long* __restrict__ start, int2* __restrict__ pairs) {
+  const Grid g = *gp;
   for (int64_t p = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; p < np; p += int64_t(gridDim.x) * blockDim.x) {
     const int4 a = mp[p];
     long long n = 0;
-    if (!mbr_empty(a)) {
+    if (!g.empty && !mbr_empty(a)) {
       const long long base = WRITE ? start[p] : 0;
       for (int cy = a.y >> g.k; cy <= (a.w - 1) >> g.k; cy++)
         for (int cx = a.x >> g.k; cx <= (a.z - 1) >> g.k; cx++) {
@@ -148,7 +129,7 @@ __global__ void probe_kernel(const int4* __restrict__ mp, int64_t np, const int4
         }
       if (WRITE) {  // insertion sort of the segment by q (segments are short)
         for (long long i = 1; i < n; i++) {
-          int2 v = pairs[base + i];
+          const int2 v = pairs[base + i];
           long long j = i - 1;
           while (j >= 0 && pairs[base + j].y > v.y) {
             pairs[base + j + 1] = pairs[base + j];
@@ -163,9 +144,6 @@ __global__ void probe_kernel(const int4* __restrict__ mp, int64_t np, const int4
 }
 
 // --------------------------------------------------------------------- host
-static int64_t cell_cap(int64_t np, int64_t nq) { return 2 * (np + nq) + 1024; }
-static int64_t entry_cap(int64_t nq) { return 4 * nq + 1024; }
-
 static size_t cub_scan_bytes(int64_t n) {
   size_t b32 = 0, b64 = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, b32, (const int*)nullptr, (int*)nullptr, (int)n);
@@ -173,30 +151,31 @@ static size_t cub_scan_bytes(int64_t n) {
   return b32 > b64 ? b32 : b64;
 }
 
-static size_t filter_layout(int64_t np, int64_t nq, Carve& cv, JoinStats** st, int** cell_count, int** cell_start,
-                            int** cell_fill, int** items, long long** pcount, long long** pstart, void** tmp,
-                            size_t* tmp_bytes) {
+struct FilterWs {
+  Grid* grid;
+  int *cell_count, *cell_start, *items;
+  long long *pcount, *pstart;
+  void* tmp;
+  size_t tmp_bytes;
+};
+
+static size_t filter_layout(int64_t np, int64_t nq, Carve& cv, FilterWs& w) {
   const int64_t C = cell_cap(np, nq), E = entry_cap(nq);
-  *st = cv.take<JoinStats>(1);
-  *cell_count = cv.take<int>(C + 1);
-  *cell_start = cv.take<int>(C + 1);
-  *cell_fill = cv.take<int>(C + 1);
-  *items = cv.take<int>(E);
-  *pcount = cv.take<long long>(np + 1);
-  *pstart = cv.take<long long>(np + 1);
-  *tmp_bytes = cub_scan_bytes((C + 1) > (np + 1) ? (C + 1) : (np + 1));
-  *tmp = cv.take<char>(*tmp_bytes);
+  w.grid = cv.take<Grid>(1);
+  w.cell_count = cv.take<int>(C + 1);
+  w.cell_start = cv.take<int>(C + 1);
+  w.items = cv.take<int>(E);
+  w.pcount = cv.take<long long>(np + 1);
+  w.pstart = cv.take<long long>(np + 1);
+  w.tmp_bytes = cub_scan_bytes((C + 1) > (np + 1) ? (C + 1) : (np + 1));
+  w.tmp = cv.take<char>(w.tmp_bytes);
   return cv.used;
 }
 
 size_t filter_ws_bytes(int64_t np, int64_t nq) {
   Carve cv{nullptr, ~size_t(0)};
-  JoinStats* st;
-  int *a, *b, *c, *d;
-  long long *e, *f;
-  void* t;
-  size_t tb;
-  return filter_layout(np, nq, cv, &st, &a, &b, &c, &d, &e, &f, &t, &tb) + 256;
+  FilterWs w;
+  return filter_layout(np, nq, cv, w) + 256;
 }
 
 static int blocks_for(int64_t n, int threads) {
@@ -204,7 +183,7 @@ static int blocks_for(int64_t n, int threads) {
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   int64_t b = (n + threads - 1) / threads;
-  int64_t cap = (int64_t)sms * 8;
+  const int64_t cap = (int64_t)sms * 8;
   if (b > cap) b = cap;
   return (int)(b < 1 ? 1 : b);
 }
@@ -213,86 +192,52 @@ int filter_pairs(const sccg_polyset* P, const sccg_polyset* Q, int32_t* pairs, i
                  void* ws, size_t ws_bytes, cudaStream_t stream) {
   const int64_t np = P->n_polygons, nq = Q->n_polygons;
   Carve cv{reinterpret_cast<char*>(ws), ws_bytes};
-  JoinStats* st;
-  int *cell_count, *cell_start, *cell_fill, *items;
-  long long *pcount, *pstart;
-  void* tmp;
-  size_t tmp_bytes;
-  filter_layout(np, nq, cv, &st, &cell_count, &cell_start, &cell_fill, &items, &pcount, &pstart, &tmp, &tmp_bytes);
+  FilterWs w;
+  filter_layout(np, nq, cv, w);
   if (!cv.ok) return set_error(SCCG_E_WORKSPACE, "filter workspace too small (see sccg_filter_workspace_bytes)");
   const int4* mp = reinterpret_cast<const int4*>(P->mbr);
   const int4* mq = reinterpret_cast<const int4*>(Q->mbr);
+  const int64_t C = cell_cap(np, nq);
 
-  // 1. bounds + per-k cell-entry counts, then pick the cell size on the host
-  join_stats_init<<<1, 64, 0, stream>>>(st);
-  if (np + nq > 0) join_stats_kernel<<<blocks_for(np + nq, 256), 256, 0, stream>>>(mp, np, mq, nq, st);
-  JoinStats hs;
-  uint32_t stat_p[2], stat_q[2];
-  if (int r = check_cuda(cudaMemcpyAsync(&hs, st, sizeof(hs), cudaMemcpyDeviceToHost, stream), "stats copy")) return r;
-  if (int r = check_cuda(cudaMemcpyAsync(stat_p, P->status, 8, cudaMemcpyDeviceToHost, stream), "status copy")) return r;
-  if (int r = check_cuda(cudaMemcpyAsync(stat_q, Q->status, 8, cudaMemcpyDeviceToHost, stream), "status copy")) return r;
-  if (int r = check_cuda(cudaStreamSynchronize(stream), "filter sync 1")) return r;
-  for (int s = 0; s < 2; s++) {
-    uint32_t* sp = s ? stat_q : stat_p;
-    if (sp[0]) {
-      int code = (sp[0] & SCCG_STATUS_ARG) ? SCCG_E_ARG
-                 : (sp[0] & SCCG_STATUS_NOT_RECTILINEAR) ? SCCG_E_NOT_RECTILINEAR
-                                                          : SCCG_E_RANGE;
-      return set_error(code, s ? "invalid polygon in set q (sccg_prep status)" : "invalid polygon in set p (sccg_prep status)",
-                       (int64_t)sp[1]);
-    }
-  }
-  const bool empty = hs.bounds[0] > hs.bounds[2] || hs.bounds[1] > hs.bounds[3] || np == 0 || nq == 0 ||
-                     hs.entries[0][kNK - 1] == 0 || hs.entries[1][kNK - 1] == 0;
-  if (empty) {
-    *n_pairs_host = 0;
-    return SCCG_OK;
-  }
-  const int64_t Ccap = cell_cap(np, nq), Ecap = entry_cap(nq);
-  int best_k = kKMax;
-  double best_cost = 1e300;
-  for (int k = kKMin; k <= kKMax; k++) {
-    const int64_t ncx = (int64_t)((hs.bounds[2] - 1) >> k) - (hs.bounds[0] >> k) + 1;
-    const int64_t ncy = (int64_t)((hs.bounds[3] - 1) >> k) - (hs.bounds[1] >> k) + 1;
-    const double C = (double)ncx * (double)ncy;
-    const double Ep = (double)hs.entries[0][k - kKMin], Eq = (double)hs.entries[1][k - kKMin];
-    if (C > (double)Ccap || Eq > (double)Ecap) continue;
-    const double cost = Ep + Eq + 0.25 * C + Ep * Eq / C;
-    if (cost < best_cost) {
-      best_cost = cost;
-      best_k = k;
-    }
-  }
-  Grid g;
-  g.k = best_k;
-  g.cx0 = hs.bounds[0] >> best_k;
-  g.cy0 = hs.bounds[1] >> best_k;
-  g.ncx = ((hs.bounds[2] - 1) >> best_k) - g.cx0 + 1;
-  g.ncy = ((hs.bounds[3] - 1) >> best_k) - g.cy0 + 1;
-  const int C = g.ncx * g.ncy;
-
-  // 2. bucket Q
-  cudaMemsetAsync(cell_count, 0, sizeof(int) * (C + 1), stream);
-  cudaMemsetAsync(cell_fill, 0, sizeof(int) * (C + 1), stream);
-  grid_count_kernel<<<blocks_for(nq, 256), 256, 0, stream>>>(mq, nq, g, cell_count);
-  cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, cell_count, cell_start, C + 1, stream);
-  grid_fill_kernel<<<blocks_for(nq, 256), 256, 0, stream>>>(mq, nq, g, cell_start, cell_fill, items);
-  // 3. probe: count, scan, total
-  probe_kernel<false><<<blocks_for(np, 128), 128, 0, stream>>>(mp, np, mq, g, cell_start, items, pcount, nullptr,
-                                                                nullptr);
-  cudaMemsetAsync(pcount + np, 0, sizeof(long long), stream);
-  cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, pcount, pstart, (int)(np + 1), stream);
+  // 1. grid size from the prep statistics (device side), bucket Q
+  grid_select_kernel<<<1, 32, 0, stream>>>(reinterpret_cast<const SetStats*>(P->stats),
+                                           reinterpret_cast<const SetStats*>(Q->stats), C, entry_cap(nq), w.grid);
+  cudaMemsetAsync(w.cell_count, 0, sizeof(int) * (C + 1), stream);
+  if (nq > 0) grid_count_kernel<<<blocks_for(nq, 256), 256, 0, stream>>>(mq, nq, w.grid, w.cell_count);
+  cub::DeviceScan::ExclusiveSum(w.tmp, w.tmp_bytes, w.cell_count, w.cell_start, (int)(C + 1), stream);
+  if (nq > 0)
+    grid_fill_kernel<<<blocks_for(nq, 256), 256, 0, stream>>>(mq, nq, w.grid, w.cell_start, w.cell_count, w.items);
+  // 2. probe: count, scan, total
+  if (np > 0)
+    probe_kernel<false><<<blocks_for(np, 128), 128, 0, stream>>>(mp, np, mq, w.grid, w.cell_start, w.items, w.pcount,
+                                                                  nullptr, nullptr);
+  cudaMemsetAsync(w.pcount + np, 0, sizeof(long long), stream);
+  cub::DeviceScan::ExclusiveSum(w.tmp, w.tmp_bytes, w.pcount, w.pstart, (int)(np + 1), stream);
+  // 3. the one host synchronisation: pair count and both sets' prep status
   long long total = 0;
-  if (int r = check_cuda(cudaMemcpyAsync(&total, pstart + np, sizeof(total), cudaMemcpyDeviceToHost, stream),
+  uint32_t sp[2] = {0, 0}, sq[2] = {0, 0};
+  if (int r = check_cuda(cudaMemcpyAsync(&total, w.pstart + np, sizeof(long long), cudaMemcpyDeviceToHost, stream),
                          "count copy"))
     return r;
-  if (int r = check_cuda(cudaStreamSynchronize(stream), "filter sync 2")) return r;
+  if (int r = check_cuda(cudaMemcpyAsync(sp, P->status, 8, cudaMemcpyDeviceToHost, stream), "status copy")) return r;
+  if (int r = check_cuda(cudaMemcpyAsync(sq, Q->status, 8, cudaMemcpyDeviceToHost, stream), "status copy")) return r;
+  if (int r = check_cuda(cudaStreamSynchronize(stream), "filter sync")) return r;
+  for (int s = 0; s < 2; s++) {
+    const uint32_t* st = s ? sq : sp;
+    if (st[0]) {
+      const int code = (st[0] & SCCG_STATUS_ARG) ? SCCG_E_ARG
+                       : (st[0] & SCCG_STATUS_NOT_RECTILINEAR) ? SCCG_E_NOT_RECTILINEAR
+                                                                : SCCG_E_RANGE;
+      return set_error(code, s ? "invalid polygon in set q (sccg_prep status)" : "invalid polygon in set p (sccg_prep status)",
+                       (int64_t)st[1]);
+    }
+  }
   *n_pairs_host = total;
   if (pairs == nullptr || cap < total) return set_error(SCCG_E_CAPACITY, "pair buffer too small", total);
   // 4. write, segment-sorted by q
   if (total > 0)
-    probe_kernel<true><<<blocks_for(np, 128), 128, 0, stream>>>(mp, np, mq, g, cell_start, items, nullptr, pstart,
-                                                                 reinterpret_cast<int2*>(pairs));
+    probe_kernel<true><<<blocks_for(np, 128), 128, 0, stream>>>(mp, np, mq, w.grid, w.cell_start, w.items, nullptr,
+                                                                 w.pstart, reinterpret_cast<int2*>(pairs));
   return check_cuda(cudaGetLastError(), "probe write");
 }
 

@@ -256,17 +256,29 @@ __device__ long long sample(int W, int H, const PairCtx& P, const PairCtx& Q, ui
 
 // r = RN64(I / U) as an exact integer count of 2^-116, split into 30-bit limbs
 // (reading R12).  Requires 0 < I <= U < 2^63.
-__device__ __forceinline__ void add_ratio_limbs(long long I, long long U, unsigned long long limb[4]) {
+__device__ __forceinline__ void ratio_limbs(long long I, long long U, unsigned long long& l0, unsigned long long& l1,
+                                            unsigned long long& l2, unsigned long long& l3) {
   const double r = __ddiv_rn((double)I, (double)U);
   const unsigned long long bits = (unsigned long long)__double_as_longlong(r);
   const int ex = (int)((bits >> 52) & 0x7ff);
   const unsigned long long mant = (bits & ((1ull << 52) - 1)) | (1ull << 52);
   const int s = ex - 1075 + 116;  // in [1, 64] for r in (2^-63, 1]
   const unsigned __int128 v = (unsigned __int128)mant << s;
-  limb[0] += (unsigned long long)(v & 0x3fffffffu);
-  limb[1] += (unsigned long long)((v >> 30) & 0x3fffffffu);
-  limb[2] += (unsigned long long)((v >> 60) & 0x3fffffffu);
-  limb[3] += (unsigned long long)(v >> 90);
+  l0 = (unsigned long long)(v & 0x3fffffffu);
+  l1 = (unsigned long long)((v >> 30) & 0x3fffffffu);
+  l2 = (unsigned long long)((v >> 60) & 0x3fffffffu);
+  l3 = (unsigned long long)(v >> 90);
+}
+
+// r = RN64(I / U) as an exact integer count of 2^-116, split into 30-bit limbs
+// (reading R12), accumulated.  Requires 0 < I <= U < 2^63.
+__device__ __forceinline__ void add_ratio_limbs(long long I, long long U, unsigned long long limb[4]) {
+  unsigned long long a, b, c, d;
+  ratio_limbs(I, U, a, b, c, d);
+  limb[0] += a;
+  limb[1] += b;
+  limb[2] += c;
+  limb[3] += d;
 }
 
 __device__ __forceinline__ long long warp_sum64(long long v) {
@@ -274,75 +286,69 @@ __device__ __forceinline__ long long warp_sum64(long long v) {
   return v;
 }
 
+// --------------------------------------------------------------- large pairs
+// Generic warp-per-pair kernel: any box size, sampling boxes + pixelization,
+// shared-memory overflow path.  Consumes the pair indices the small-pair
+// kernel routed to it (list[0 .. *count)).
 template <bool COUNT>
-__global__ void __launch_bounds__(kWarps * 32, 3) pixelbox_kernel(DevSet Ps, DevSet Qs, const int2* __restrict__ pairs,
-                                                               long long n, long long* __restrict__ inter,
-                                                               long long* __restrict__ uni, sccg_sums* sums, int T,
-                                                               int mode, unsigned long long* queue,
-                                                               long long* counters, long long np_, long long nq_) {
+__global__ void __launch_bounds__(kWarps * 32, 3)
+    large_kernel(DevSet Ps, DevSet Qs, const int2* __restrict__ pairs, const long long* __restrict__ list,
+                 const unsigned* __restrict__ count, long long* __restrict__ inter, long long* __restrict__ uni,
+                 sccg_sums* sums, int T, int mode, unsigned long long* queue, long long* counters) {
   extern __shared__ int4 s_dyn[];  // [kWarps][2][kECap] edge scratch, then [kWarps][kStackCap] stack
   __shared__ unsigned long long s_red[kWarps][11];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   int4* sp = s_dyn + (size_t)warp * 2 * kECap;
   int4* sq = sp + kECap;
   uint64_t* stk = reinterpret_cast<uint64_t*>(s_dyn + (size_t)kWarps * 2 * kECap) + (size_t)warp * kStackCap;
-  // lane 0 accumulates the batch totals of this warp
+  const long long n = *count;
   unsigned long long a_n = 0, a_nz = 0, a_i = 0, a_u = 0, a_ap = 0, a_aq = 0, limb[4] = {0, 0, 0, 0};
   unsigned status = 0;
   for (;;) {
-    unsigned long long k0 = 0;
-    if (lane == 0) k0 = atomicAdd(queue, (unsigned long long)kChunk);
-    k0 = __shfl_sync(FULL, k0, 0);
-    if ((long long)k0 >= n) break;
-    const long long kend = min((long long)k0 + kChunk, n);
-    for (long long k = (long long)k0; k < kend; k++) {
-      const int2 pq = pairs[k];
-      if ((unsigned)pq.x >= (unsigned long long)np_ || (unsigned)pq.y >= (unsigned long long)nq_) {
-        status |= SCCG_STATUS_ARG;  // index out of range: pair skipped
-        continue;
-      }
-      const int4 mp = Ps.mbr[pq.x], mq = Qs.mbr[pq.y];
-      const int bx0 = max(mp.x, mq.x), by0 = max(mp.y, mq.y);
-      const int bx1 = min(mp.z, mq.z), by1 = min(mp.w, mq.w);
-      long long acc = 0;
-      if (bx0 < bx1 && by0 < by1) {  // empty root box: I = 0 (reading R18)
-        const int2 cp = Ps.ecount[pq.x], cq = Qs.ecount[pq.y];
-        PairCtx P, Q;
-        P.ev = Ps.edges + Ps.off[pq.x];
-        P.eh = Ps.edges + Ps.off[pq.x + 1] - cp.y;
-        P.nv = cp.x;
-        P.nh = cp.y;
-        P.dx = mp.x - bx0;
-        P.dy = mp.y - by0;
-        Q.ev = Qs.edges + Qs.off[pq.y];
-        Q.eh = Qs.edges + Qs.off[pq.y + 1] - cq.y;
-        Q.nv = cq.x;
-        Q.nh = cq.y;
-        Q.dx = mq.x - bx0;
-        Q.dy = mq.y - by0;
-        const int W = bx1 - bx0, H = by1 - by0;
-        if (COUNT && lane == 0)
-          atomicAdd((unsigned long long*)&counters[SCCG_CNT_ROOTPX], (unsigned long long)W * H);
-        if (mode == 1 || (long long)W * H < T)
-          acc = pixelize<COUNT>(0, 0, W, H, P, Q, sp, sq, counters);
-        else
-          acc = sample<COUNT>(W, H, P, Q, stk, sp, sq, T, counters, status);
-      }
-      const long long I = warp_sum64(acc);
-      if (lane == 0) {
-        const long long ap = Ps.area[pq.x], aq = Qs.area[pq.y];
-        const long long U = ap + aq - I;  // indirect union
-        if (inter) inter[k] = I;
-        if (uni) uni[k] = U;
-        a_n++;
-        a_i += I;
-        a_ap += ap;
-        a_aq += aq;
-        if (I != 0) {
-          a_nz++;
-          a_u += U;
-          add_ratio_limbs(I, U, limb);
-        }
+    unsigned long long i0 = 0;
+    if (lane == 0) i0 = atomicAdd(queue, 1ull);
+    i0 = __shfl_sync(FULL, i0, 0);
+    if ((long long)i0 >= n) break;
+    const long long k = list[i0];
+    const int2 pq = pairs[k];
+    const int4 mp = Ps.mbr[pq.x], mq = Qs.mbr[pq.y];
+    const int bx0 = max(mp.x, mq.x), by0 = max(mp.y, mq.y);
+    const int bx1 = min(mp.z, mq.z), by1 = min(mp.w, mq.w);
+    const int2 cp = Ps.ecount[pq.x], cq = Qs.ecount[pq.y];
+    PairCtx P, Q;
+    P.ev = Ps.edges + Ps.off[pq.x];
+    P.eh = Ps.edges + Ps.off[pq.x + 1] - cp.y;
+    P.nv = cp.x;
+    P.nh = cp.y;
+    P.dx = mp.x - bx0;
+    P.dy = mp.y - by0;
+    Q.ev = Qs.edges + Qs.off[pq.y];
+    Q.eh = Qs.edges + Qs.off[pq.y + 1] - cq.y;
+    Q.nv = cq.x;
+    Q.nh = cq.y;
+    Q.dx = mq.x - bx0;
+    Q.dy = mq.y - by0;
+    const int W = bx1 - bx0, H = by1 - by0;
+    if (COUNT && lane == 0) atomicAdd((unsigned long long*)&counters[SCCG_CNT_ROOTPX], (unsigned long long)W * H);
+    long long acc;
+    if (mode == 1 || (long long)W * H < T)
+      acc = pixelize<COUNT>(0, 0, W, H, P, Q, sp, sq, counters);
+    else
+      acc = sample<COUNT>(W, H, P, Q, stk, sp, sq, T, counters, status);
+    const long long I = warp_sum64(acc);
+    if (lane == 0) {
+      const long long ap = Ps.area[pq.x], aq = Qs.area[pq.y];
+      const long long U = ap + aq - I;  // indirect union
+      if (inter) inter[k] = I;
+      if (uni) uni[k] = U;
+      a_n++;
+      a_i += I;
+      a_ap += ap;
+      a_aq += aq;
+      if (I != 0) {
+        a_nz++;
+        a_u += U;
+        add_ratio_limbs(I, U, limb);
       }
     }
   }
@@ -369,15 +375,260 @@ __global__ void __launch_bounds__(kWarps * 32, 3) pixelbox_kernel(DevSet Ps, Dev
   }
 }
 
-size_t pixelbox_ws_bytes(int64_t) { return 256; }
+// --------------------------------------------------------------- small pairs
+// The common case (nucleus pairs): root box at most 32 x 32 pixels and below
+// T, each polygon at most kSmallCap vertical edges.  A warp claims 32 pairs,
+// loads their metadata lane-parallel (32 independent loads in flight), then
+// walks them with a software pipeline: while pair j is pixelized, pair j+1's
+// edge records are already in flight into registers.  Pixelization is one row
+// per lane (one 32-bit row word), half-warp per polygon when the box has at
+// most 16 rows.  Per-pair results and sums are written lane-parallel.
+constexpr int kSmallWarps = 8;
+constexpr int kSmallCap = 64;   // vertical edges per polygon on this path
+constexpr int kSmallQOff = 65;  // q buffer offset (records): p[j], q[j] in different bank groups
+
+__device__ __forceinline__ int stage_regs(uint64_t r0, uint64_t r1, int nv, int dx, int dy, int H, int4* buf) {
+  const int lane = threadIdx.x & 31;
+  int c, lo, hi;
+  unpack_edge(r0, c, lo, hi);
+  int yl = lo + dy, yh = hi + dy;
+  bool keep = lane < nv && yl < H && yh > 0;
+  unsigned b = __ballot_sync(FULL, keep);
+  if (keep) buf[__popc(b & lanemask_lt())] = make_int4(yl, yh - yl, (int)suffix_mask(c + dx), 0);
+  int cnt = __popc(b);
+  if (nv > 32) {
+    unpack_edge(r1, c, lo, hi);
+    yl = lo + dy;
+    yh = hi + dy;
+    keep = lane + 32 < nv && yl < H && yh > 0;
+    b = __ballot_sync(FULL, keep);
+    if (keep) buf[cnt + __popc(b & lanemask_lt())] = make_int4(yl, yh - yl, (int)suffix_mask(c + dx), 0);
+    cnt += __popc(b);
+  }
+  return cnt;
+}
+
+__device__ __forceinline__ unsigned row_word(const int4* __restrict__ b, int n, int row) {
+  unsigned m = 0;
+  for (int t = 0; t < n; t += 4) {
+#pragma unroll
+    for (int u = 0; u < 4; u++) {
+      const int4 r = b[t + u];
+      if ((unsigned)(row - r.x) < (unsigned)r.y) m ^= (unsigned)r.z;
+    }
+  }
+  return m;
+}
+
+__device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long v) {
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+  return v;
+}
+
+#ifndef SCCG_SMALL_MINB
+#define SCCG_SMALL_MINB 4
+#endif
+template <bool COUNT>
+__global__ void __launch_bounds__(kSmallWarps * 32, SCCG_SMALL_MINB)
+    small_kernel(DevSet Ps, DevSet Qs, const int2* __restrict__ pairs, long long n, long long* __restrict__ inter,
+                 long long* __restrict__ uni, sccg_sums* sums, int T, int mode, unsigned long long* queue,
+                 long long* __restrict__ large_list, unsigned* large_count, long long* counters, long long np_,
+                 long long nq_) {
+  __shared__ int4 s_buf[kSmallWarps][2 * kSmallQOff + 3];
+  __shared__ unsigned long long s_acc[kSmallWarps][16];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int4* bp = s_buf[warp];
+  int4* bq = bp + kSmallQOff;
+  if (lane < 16) s_acc[warp][lane] = 0;
+  unsigned status = 0;
+  for (;;) {
+    unsigned long long k0 = 0;
+    if (lane == 0) k0 = atomicAdd(queue, 32ull);
+    k0 = __shfl_sync(FULL, k0, 0);
+    if ((long long)k0 >= n) break;
+    const long long k = (long long)k0 + lane;
+    // ---- lane-parallel metadata of pair k0 + lane
+    bool ok = false, small = false, empty = false;
+    int2 pq = make_int2(0, 0);
+    unsigned m0 = 0, mdp = 0, mdq = 0;
+    int ep = 0, eq = 0;
+    if (k < n) {
+      pq = pairs[k];
+      ok = (unsigned)pq.x < (unsigned long long)np_ && (unsigned)pq.y < (unsigned long long)nq_;
+      if (!ok) status |= SCCG_STATUS_ARG;  // index out of range: pair skipped
+    }
+    if (ok) {
+      const int4 mp = Ps.mbr[pq.x], mq = Qs.mbr[pq.y];
+      const int2 cp = Ps.ecount[pq.x], cq = Qs.ecount[pq.y];
+      const long long op = Ps.off[pq.x], oq = Qs.off[pq.y];
+      const int bx0 = max(mp.x, mq.x), by0 = max(mp.y, mq.y);
+      const int W = min(mp.z, mq.z) - bx0, H = min(mp.w, mq.w) - by0;
+      const int dxp = mp.x - bx0, dyp = mp.y - by0, dxq = mq.x - bx0, dyq = mq.y - by0;
+      empty = !(W > 0 && H > 0);  // reading R18: I = 0
+      small = !empty && W <= 32 && H <= 32 && (mode == 1 || W * H < T) && cp.x <= kSmallCap && cq.x <= kSmallCap &&
+              op + cp.x < (1ll << 31) && oq + cq.x < (1ll << 31) && min(min(dxp, dyp), min(dxq, dyq)) >= -32768;
+      m0 = (unsigned)W | ((unsigned)H << 6) | ((unsigned)cp.x << 12) | ((unsigned)cq.x << 20);
+      mdp = ((unsigned)dxp & 0xffffu) | ((unsigned)dyp << 16);
+      mdq = ((unsigned)dxq & 0xffffu) | ((unsigned)dyq << 16);
+      ep = (int)op;
+      eq = (int)oq;
+    }
+    // ---- everything else goes to the generic kernel (warp-aggregated append)
+    const bool large = ok && !empty && !small;
+    const unsigned lb = __ballot_sync(FULL, large);
+    if (lb) {
+      unsigned base = 0;
+      if (lane == 0) base = atomicAdd(large_count, (unsigned)__popc(lb));
+      base = __shfl_sync(FULL, base, 0);
+      if (large) large_list[base + __popc(lb & lanemask_lt())] = k;
+    }
+    // ---- small pairs, software-pipelined
+    unsigned todo = __ballot_sync(FULL, small);
+    unsigned myI = 0;
+    uint64_t np0 = 0, np1 = 0, nq0 = 0, nq1 = 0;
+    auto prefetch = [&](int j) {
+      const unsigned mj = __shfl_sync(FULL, m0, j);
+      const int nvp = (mj >> 12) & 127, nvq = (mj >> 20) & 127;
+      const int epj = __shfl_sync(FULL, ep, j), eqj = __shfl_sync(FULL, eq, j);
+      np0 = lane < nvp ? __ldg(Ps.edges + epj + lane) : 0ull;
+      nq0 = lane < nvq ? __ldg(Qs.edges + eqj + lane) : 0ull;
+      np1 = lane + 32 < nvp ? __ldg(Ps.edges + epj + 32 + lane) : 0ull;
+      nq1 = lane + 32 < nvq ? __ldg(Qs.edges + eqj + 32 + lane) : 0ull;
+    };
+    if (todo) prefetch(__ffs(todo) - 1);
+    unsigned long long c_tests = 0, c_px = 0;
+    while (todo) {
+      const int j = __ffs(todo) - 1;
+      todo &= todo - 1;
+      const uint64_t cp0 = np0, cp1 = np1, cq0 = nq0, cq1 = nq1;
+      if (todo) prefetch(__ffs(todo) - 1);
+      const unsigned mj = __shfl_sync(FULL, m0, j);
+      const unsigned dpj = __shfl_sync(FULL, mdp, j), dqj = __shfl_sync(FULL, mdq, j);
+      const int W = mj & 63, H = (mj >> 6) & 63, nvp = (mj >> 12) & 127, nvq = (mj >> 20) & 127;
+      const int cntp = stage_regs(cp0, cp1, nvp, (int)(short)(dpj & 0xffffu), (int)dpj >> 16, H, bp);
+      const int cntq = stage_regs(cq0, cq1, nvq, (int)(short)(dqj & 0xffffu), (int)dqj >> 16, H, bq);
+      const unsigned wmask = low_bits(W);
+      unsigned cnt;
+      if (H <= 16) {  // half-warp per polygon
+        const int npad = (max(cntp, cntq) + 3) & ~3;
+        for (int t = cntp + lane; t < npad; t += 32) bp[t] = make_int4(0, 0, 0, 0);
+        for (int t = cntq + lane; t < npad; t += 32) bq[t] = make_int4(0, 0, 0, 0);
+        __syncwarp();
+        const int row = lane & 15;
+        const unsigned m = row_word(lane < 16 ? bp : bq, npad, row);
+        const unsigned mo = __shfl_xor_sync(FULL, m, 16);
+        cnt = (lane < 16 && row < H) ? __popc(m & mo & wmask) : 0u;
+      } else {  // one row per lane, both polygons
+        const int pp = (cntp + 3) & ~3, pq_ = (cntq + 3) & ~3;
+        if (cntp + lane < pp) bp[cntp + lane] = make_int4(0, 0, 0, 0);
+        if (cntq + lane < pq_) bq[cntq + lane] = make_int4(0, 0, 0, 0);
+        __syncwarp();
+        const unsigned mpw = row_word(bp, pp, lane);
+        const unsigned mqw = row_word(bq, pq_, lane);
+        cnt = lane < H ? __popc(mpw & mqw & wmask) : 0u;
+      }
+      const unsigned I = __reduce_add_sync(FULL, cnt);
+      if (lane == j) myI = I;
+      if (COUNT) {
+        c_tests += (unsigned long long)H * (cntp + cntq);
+        c_px += (unsigned long long)W * H;
+      }
+      __syncwarp();  // buffers are rewritten by the next pair
+    }
+    // ---- lane-parallel outputs and batch totals
+    const bool done = ok && (small || empty);
+    unsigned long long v_i = 0, v_u = 0, v_ap = 0, v_aq = 0, l0 = 0, l1 = 0, l2 = 0, l3 = 0;
+    unsigned nz = 0;
+    if (done) {
+      const long long ap = Ps.area[pq.x], aq = Qs.area[pq.y];
+      const long long I = small ? (long long)myI : 0;
+      const long long U = ap + aq - I;  // indirect union
+      if (inter) inter[k] = I;
+      if (uni) uni[k] = U;
+      v_i = I;
+      v_ap = ap;
+      v_aq = aq;
+      if (I != 0) {
+        nz = 1;
+        v_u = U;
+        ratio_limbs(I, U, l0, l1, l2, l3);
+      }
+    }
+    const unsigned n_done = __popc(__ballot_sync(FULL, done));
+    const unsigned n_nz = __popc(__ballot_sync(FULL, nz != 0));
+    v_i = __reduce_add_sync(FULL, (unsigned)v_i);  // <= 32 * 1024
+    v_u = warp_sum_u64(v_u);
+    v_ap = warp_sum_u64(v_ap);
+    v_aq = warp_sum_u64(v_aq);
+    l0 = warp_sum_u64(l0);
+    l1 = warp_sum_u64(l1);
+    l2 = warp_sum_u64(l2);
+    l3 = warp_sum_u64(l3);
+    if (lane == 0) {
+      unsigned long long* a = s_acc[warp];
+      a[0] += n_done;
+      a[1] += n_nz;
+      a[2] += v_i;
+      a[3] += v_u;
+      a[4] += v_ap;
+      a[5] += v_aq;
+      a[6] += l0;
+      a[7] += l1;
+      a[8] += l2;
+      a[9] += l3;
+      if (COUNT) {
+        a[11] += c_tests;
+        a[12] += c_px;
+        a[13] += __popc(__ballot_sync(FULL, small) & 0xffffffffu);
+      }
+    }
+  }
+  status = __reduce_or_sync(FULL, status);
+  if (lane == 0) s_acc[warp][10] |= status;
+  __syncthreads();
+  if (threadIdx.x < 14) {
+    unsigned long long v = 0;
+    for (int w = 0; w < kSmallWarps; w++) v = threadIdx.x == 10 ? (v | s_acc[w][10]) : v + s_acc[w][threadIdx.x];
+    unsigned long long* dst = reinterpret_cast<unsigned long long*>(sums);
+    if (threadIdx.x < 10) {
+      if (v) atomicAdd(&dst[threadIdx.x], v);
+    } else if (threadIdx.x == 10) {
+      if (v) atomicOr(&dst[10], v);
+    } else if (COUNT && v) {
+      const int slot = threadIdx.x == 11 ? SCCG_CNT_ROWTESTS : threadIdx.x == 12 ? SCCG_CNT_PIXELS : SCCG_CNT_PIXBOXES;
+      atomicAdd((unsigned long long*)&counters[slot], v);
+      if (threadIdx.x == 12) atomicAdd((unsigned long long*)&counters[SCCG_CNT_ROOTPX], v);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------- host
+struct PixelboxWs {
+  unsigned long long* queue;  // [2] small, large
+  unsigned* large_count;
+  long long* large_list;
+};
+
+static size_t pixelbox_layout(int64_t n, Carve& cv, PixelboxWs& w) {
+  w.queue = cv.take<unsigned long long>(4);
+  w.large_count = reinterpret_cast<unsigned*>(w.queue + 2);
+  w.large_list = cv.take<long long>(n > 0 ? n : 1);
+  return cv.used;
+}
+
+size_t pixelbox_ws_bytes(int64_t n) {
+  Carve cv{nullptr, ~size_t(0)};
+  PixelboxWs w;
+  return pixelbox_layout(n, cv, w) + 256;
+}
 
 constexpr size_t kDynSmem = (size_t)kWarps * (2 * kECap * sizeof(int4) + kStackCap * sizeof(uint64_t));
 
 static cudaError_t prepare_kernels() {
   static cudaError_t once = [] {
-    cudaError_t e = cudaFuncSetAttribute(pixelbox_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDynSmem);
+    cudaError_t e = cudaFuncSetAttribute(large_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDynSmem);
     if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(pixelbox_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDynSmem);
+      e = cudaFuncSetAttribute(large_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDynSmem);
     return e;
   }();
   return once;
@@ -386,38 +637,54 @@ static cudaError_t prepare_kernels() {
 int run_pixelbox(const sccg_polyset* p, const sccg_polyset* q, const int32_t* pairs, int64_t n, int64_t* inter,
                  int64_t* uni, sccg_sums* sums, const sccg_config* cfg, void* ws, size_t ws_bytes,
                  cudaStream_t stream) {
-  if (ws_bytes < sizeof(unsigned long long) || ws == nullptr)
-    return set_error(SCCG_E_WORKSPACE, "pixelbox workspace too small");
+  Carve cv{reinterpret_cast<char*>(ws), ws_bytes};
+  PixelboxWs w;
+  pixelbox_layout(n, cv, w);
+  if (!cv.ok || ws == nullptr) return set_error(SCCG_E_WORKSPACE, "pixelbox workspace too small");
   int T = cfg && cfg->threshold > 0 ? cfg->threshold : 2048;
-  int mode = cfg ? cfg->mode : 0;
+  const int mode = cfg ? cfg->mode : 0;
   if (T < 2) T = 2;
   if (mode != 0 && mode != 1) return set_error(SCCG_E_ARG, "config.mode must be 0 (PixelBox) or 1 (PixelOnly)");
-  unsigned long long* queue = reinterpret_cast<unsigned long long*>(ws);
-  cudaMemsetAsync(queue, 0, sizeof(*queue), stream);
+  cudaMemsetAsync(w.queue, 0, 4 * sizeof(unsigned long long), stream);
   if (n == 0) return check_cuda(cudaGetLastError(), "pixelbox");
   const bool count = cfg && cfg->counters;
+  long long* counters = count ? reinterpret_cast<long long*>(cfg->counters) : nullptr;
   if (int r = check_cuda(prepare_kernels(), "pixelbox smem attribute")) return r;
-  int dev = 0, sms = 148, per_sm = 1;
+  int dev = 0, sms = 148, per_sm_s = 1, per_sm_l = 1;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  if (count)
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pixelbox_kernel<true>, kWarps * 32, kDynSmem);
-  else
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pixelbox_kernel<false>, kWarps * 32, kDynSmem);
-  int64_t grid = cfg && cfg->grid > 0 ? cfg->grid : (int64_t)sms * (per_sm > 0 ? per_sm : 1);
-  const int64_t need = (n + kWarps * kChunk - 1) / (kWarps * kChunk);
-  if (grid > need) grid = need;
-  if (grid < 1) grid = 1;
+  if (count) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_s, small_kernel<true>, kSmallWarps * 32, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_l, large_kernel<true>, kWarps * 32, kDynSmem);
+  } else {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_s, small_kernel<false>, kSmallWarps * 32, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_l, large_kernel<false>, kWarps * 32, kDynSmem);
+  }
+  int64_t grid_s = cfg && cfg->grid > 0 ? cfg->grid : (int64_t)sms * (per_sm_s > 0 ? per_sm_s : 1);
+  const int64_t need = (n + kSmallWarps * 32 - 1) / (kSmallWarps * 32);
+  if (grid_s > need) grid_s = need;
+  if (grid_s < 1) grid_s = 1;
+  int64_t grid_l = cfg && cfg->grid > 0 ? cfg->grid : (int64_t)sms * (per_sm_l > 0 ? per_sm_l : 1);
+  const int64_t need_l = (n + kWarps - 1) / kWarps;
+  if (grid_l > need_l) grid_l = need_l;
+  if (grid_l < 1) grid_l = 1;
   DevSet Ps = dev_set(p), Qs = dev_set(q);
-  if (count)
-    pixelbox_kernel<true><<<(unsigned)grid, kWarps * 32, kDynSmem, stream>>>(
-        Ps, Qs, reinterpret_cast<const int2*>(pairs), n, reinterpret_cast<long long*>(inter),
-        reinterpret_cast<long long*>(uni), sums, T, mode, queue, reinterpret_cast<long long*>(cfg->counters),
-        p->n_polygons, q->n_polygons);
-  else
-    pixelbox_kernel<false><<<(unsigned)grid, kWarps * 32, kDynSmem, stream>>>(
-        Ps, Qs, reinterpret_cast<const int2*>(pairs), n, reinterpret_cast<long long*>(inter),
-        reinterpret_cast<long long*>(uni), sums, T, mode, queue, nullptr, p->n_polygons, q->n_polygons);
+  const int2* pr = reinterpret_cast<const int2*>(pairs);
+  long long* in = reinterpret_cast<long long*>(inter);
+  long long* un = reinterpret_cast<long long*>(uni);
+  if (count) {
+    small_kernel<true><<<(unsigned)grid_s, kSmallWarps * 32, 0, stream>>>(
+        Ps, Qs, pr, n, in, un, sums, T, mode, w.queue, w.large_list, w.large_count, counters, p->n_polygons,
+        q->n_polygons);
+    large_kernel<true><<<(unsigned)grid_l, kWarps * 32, kDynSmem, stream>>>(Ps, Qs, pr, w.large_list, w.large_count,
+                                                                          in, un, sums, T, mode, w.queue + 1, counters);
+  } else {
+    small_kernel<false><<<(unsigned)grid_s, kSmallWarps * 32, 0, stream>>>(
+        Ps, Qs, pr, n, in, un, sums, T, mode, w.queue, w.large_list, w.large_count, nullptr, p->n_polygons,
+        q->n_polygons);
+    large_kernel<false><<<(unsigned)grid_l, kWarps * 32, kDynSmem, stream>>>(Ps, Qs, pr, w.large_list, w.large_count,
+                                                                           in, un, sums, T, mode, w.queue + 1, nullptr);
+  }
   return check_cuda(cudaGetLastError(), "pixelbox launch");
 }
 
