@@ -554,6 +554,7 @@ __global__ void __launch_bounds__(kSmallWarps * 32, SCCG_SMALL_MINB)
         ratio_limbs(I, U, l0, l1, l2, l3);
       }
     }
+    const unsigned n_small = __popc(__ballot_sync(FULL, small));
     const unsigned n_done = __popc(__ballot_sync(FULL, done));
     const unsigned n_nz = __popc(__ballot_sync(FULL, nz != 0));
     v_i = __reduce_add_sync(FULL, (unsigned)v_i);  // <= 32 * 1024
@@ -579,7 +580,7 @@ __global__ void __launch_bounds__(kSmallWarps * 32, SCCG_SMALL_MINB)
       if (COUNT) {
         a[11] += c_tests;
         a[12] += c_px;
-        a[13] += __popc(__ballot_sync(FULL, small) & 0xffffffffu);
+        a[13] += n_small;
       }
     }
   }
