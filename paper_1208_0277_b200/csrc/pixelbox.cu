@@ -439,7 +439,8 @@ __global__ void __launch_bounds__(kSmallWarps * 32, SCCG_SMALL_MINB)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   int4* bp = s_buf[warp];
   int4* bq = bp + kSmallQOff;
-  if (lane < 16) s_acc[warp][lane] = 0;
+  if (lane == 0)
+    for (int i = 0; i < 16; i++) s_acc[warp][i] = 0;
   unsigned status = 0;
   for (;;) {
     unsigned long long k0 = 0;

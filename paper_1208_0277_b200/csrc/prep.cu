@@ -17,9 +17,9 @@
 
 namespace sccg {
 
-constexpr int kPrepThreads = 256;
-constexpr int kPrepPolys = 64;
-constexpr int kPrepVerts = 5888;  // 46 KB of int2 (static shared memory limit 48 KB)
+constexpr int kPrepThreads = 128;
+constexpr int kPrepPolys = 128;   // one ring per thread per tile
+constexpr int kPrepVerts = 5120;  // 40 KB of int2 staged per tile (dynamic shared memory)
 
 __device__ __forceinline__ void flag(uint32_t* status, uint32_t bit, int64_t poly) {
   atomicOr(&status[0], bit);
@@ -92,6 +92,85 @@ __device__ __forceinline__ void prep_polygon(const int2* v, int64_t V, int64_t p
   }
 }
 
+// One polygon by one thread (the common small ring): same arithmetic as
+// prep_polygon, serial over the ring's vertices in shared memory.
+__device__ __forceinline__ int4 prep_polygon_thread(const int2* v, int V, int64_t poly, int64_t b, int64_t e,
+                                                    int4* __restrict__ mbr, int64_t* __restrict__ area,
+                                                    int2* __restrict__ ecount, uint64_t* __restrict__ edges,
+                                                    uint32_t* __restrict__ status, int validate) {
+  int xmin = INT_MAX, ymin = INT_MAX, xmax = INT_MIN, ymax = INT_MIN;
+  bool bad_range = false;
+  for (int i = 0; i < V; i++) {
+    const int2 a = v[i];
+    xmin = min(xmin, a.x);
+    xmax = max(xmax, a.x);
+    ymin = min(ymin, a.y);
+    ymax = max(ymax, a.y);
+    bad_range |= (int64_t)a.x > kMaxCoord || (int64_t)a.x < -kMaxCoord || (int64_t)a.y > kMaxCoord ||
+                 (int64_t)a.y < -kMaxCoord;
+  }
+  bad_range = bad_range || (int64_t)xmax - xmin > kMaxExtent || (int64_t)ymax - ymin > kMaxExtent;
+  long long twice_area = 0;
+  bool diag = false;
+  int nvert = 0, nhor = 0;
+  int2 a = v[0];
+  for (int i = 0; i < V; i++) {
+    const int2 c = v[i + 1 == V ? 0 : i + 1];
+    const int ax = a.x - xmin, ay = a.y - ymin, cx = c.x - xmin, cy = c.y - ymin;
+    twice_area += (long long)ax * cy - (long long)cx * ay;  // P:193, one term per vertex
+    if (a.x == c.x && a.y != c.y) {
+      if (!bad_range) edges[b + nvert] = pack_edge((uint32_t)ax, (uint32_t)min(ay, cy), (uint32_t)max(ay, cy));
+      nvert++;
+    } else if (a.y == c.y && a.x != c.x) {
+      if (!bad_range) edges[e - 1 - nhor] = pack_edge((uint32_t)ay, (uint32_t)min(ax, cx), (uint32_t)max(ax, cx));
+      nhor++;
+    } else if (a.x != c.x && a.y != c.y) {
+      diag = true;
+    }
+    a = c;
+  }
+  const int4 m = make_int4(xmin, ymin, xmax, ymax);
+  area[poly] = (twice_area < 0 ? -twice_area : twice_area) / 2;
+  mbr[poly] = m;
+  ecount[poly] = bad_range ? make_int2(0, 0) : make_int2(nvert, nhor);
+  if (validate && diag) flag(status, SCCG_STATUS_NOT_RECTILINEAR, poly);
+  if (bad_range) flag(status, SCCG_STATUS_RANGE, poly);
+  return m;
+}
+
+struct StatAcc {
+  unsigned long long ent[kStatNK];
+  unsigned long long nonempty;
+  int bx0, by0, bx1, by1, mw, mh;
+  __device__ __forceinline__ void init() {
+#pragma unroll
+    for (int k = 0; k < kStatNK; k++) ent[k] = 0;
+    nonempty = 0;
+    bx0 = by0 = INT_MAX;
+    bx1 = by1 = INT_MIN;
+    mw = mh = 0;
+  }
+  __device__ __forceinline__ void add(const int4& m) {
+    if (!(m.x < m.z && m.y < m.w)) return;
+    nonempty++;
+    bx0 = min(bx0, m.x);
+    by0 = min(by0, m.y);
+    bx1 = max(bx1, m.z);
+    by1 = max(by1, m.w);
+    mw = max(mw, m.z - m.x);
+    mh = max(mh, m.w - m.y);
+#pragma unroll
+    for (int k = 0; k < kStatNK; k++) {
+      const int kk = k + kStatK0;
+      const unsigned cx = (unsigned)(((m.z - 1) >> kk) - (m.x >> kk) + 1);
+      const unsigned cy = (unsigned)(((m.w - 1) >> kk) - (m.y >> kk) + 1);
+      ent[k] += (unsigned long long)cx * cy;
+    }
+  }
+};
+
+constexpr int kThreadMaxV = 192;  // rings up to this size are prepped by one thread
+
 __global__ void __launch_bounds__(kPrepThreads) prep_kernel(const int2* __restrict__ xy,
                                                             const int64_t* __restrict__ off, int64_t n,
                                                             int64_t nv_total, int4* __restrict__ mbr,
@@ -99,61 +178,68 @@ __global__ void __launch_bounds__(kPrepThreads) prep_kernel(const int2* __restri
                                                             uint64_t* __restrict__ edges,
                                                             uint32_t* __restrict__ status, SetStats* stats,
                                                             int validate) {
-  __shared__ int2 s_xy[kPrepVerts];
+  extern __shared__ int4 s_dyn4[];  // kPrepVerts int2 (16-byte aligned)
+  int2* s_xy = reinterpret_cast<int2*>(s_dyn4);
   __shared__ int64_t s_off[kPrepPolys + 1];
+  __shared__ unsigned s_big[kPrepPolys / 32];
   __shared__ unsigned long long s_ent[kStatNK + 1];
   __shared__ int s_b[6];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  // per-thread (lane 0 of each warp) statistics
-  unsigned long long ent[kStatNK];
-#pragma unroll
-  for (int k = 0; k < kStatNK; k++) ent[k] = 0;
-  unsigned long long nonempty = 0;
-  int bx0 = INT_MAX, by0 = INT_MAX, bx1 = INT_MIN, by1 = INT_MIN, mw = 0, mh = 0;
+  StatAcc acc;
+  acc.init();
   const int64_t ntiles = (n + kPrepPolys - 1) / kPrepPolys;
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int64_t p0 = tile * kPrepPolys;
     const int np = (int)min((int64_t)kPrepPolys, n - p0);
     __syncthreads();  // previous tile's shared data fully consumed
     for (int i = threadIdx.x; i <= np; i += blockDim.x) s_off[i] = off[p0 + i];
+    if (threadIdx.x < kPrepPolys / 32) s_big[threadIdx.x] = 0;
     __syncthreads();
-    const int64_t v0 = s_off[0], v1 = s_off[np];
-    const bool tiled = v0 >= 0 && v1 <= nv_total && v1 >= v0 && v1 - v0 <= kPrepVerts;
-    if (tiled)
-      for (int64_t i = threadIdx.x; i < v1 - v0; i += blockDim.x) s_xy[i] = xy[v0 + i];
+    // stage the tile's vertex range with 16-byte loads (start rounded down to even)
+    const int64_t v0 = s_off[0] & ~int64_t(1), v1 = s_off[np];
+    const bool tiled = s_off[0] >= 0 && v1 <= nv_total && v1 >= s_off[0] && v1 - v0 <= kPrepVerts;
+    if (tiled) {
+      const int64_t nvec = (v1 - v0 + 1) >> 1;
+      const int4* src = reinterpret_cast<const int4*>(xy + v0);
+      const bool tail_odd = ((v1 - v0) & 1) != 0;
+      for (int64_t i = threadIdx.x; i < nvec; i += blockDim.x) {
+        if (tail_odd && i == nvec - 1) {
+          s_xy[2 * i] = xy[v0 + 2 * i];  // last vector would read past the array
+        } else {
+          s_dyn4[i] = __ldg(src + i);
+        }
+      }
+    }
     __syncthreads();
-    for (int j = warp; j < np; j += kPrepThreads / 32) {
+    // thread per small ring
+    for (int j = threadIdx.x; j < np; j += blockDim.x) {
       const int64_t poly = p0 + j;
       const int64_t b = s_off[j], e = s_off[j + 1];
       const int64_t V = e - b;
       if (b < 0 || e > nv_total || V < 4) {  // malformed offsets or too few vertices
-        if (lane == 0) {
-          mbr[poly] = make_int4(0, 0, 0, 0);
-          area[poly] = 0;
-          ecount[poly] = make_int2(0, 0);
-          flag(status, SCCG_STATUS_ARG, poly);
-        }
+        mbr[poly] = make_int4(0, 0, 0, 0);
+        area[poly] = 0;
+        ecount[poly] = make_int2(0, 0);
+        flag(status, SCCG_STATUS_ARG, poly);
         continue;
       }
+      if (V > kThreadMaxV || !(tiled && b >= v0 && e <= v1)) {
+        atomicOr(&s_big[j >> 5], 1u << (j & 31));
+        continue;
+      }
+      acc.add(prep_polygon_thread(s_xy + (b - v0), (int)V, poly, b, e, mbr, area, ecount, edges, status, validate));
+    }
+    __syncthreads();
+    // warp per large ring
+    for (int j = warp; j < np; j += kPrepThreads / 32) {
+      if (!((s_big[j >> 5] >> (j & 31)) & 1u)) continue;
+      const int64_t poly = p0 + j;
+      const int64_t b = s_off[j], e = s_off[j + 1];
       const bool in_smem = tiled && b >= v0 && e <= v1;
       int4 m;
-      prep_polygon(in_smem ? s_xy + (b - v0) : xy + b, V, poly, b, e, mbr, area, ecount, edges, status, validate, m);
-      if (lane == 0 && m.x < m.z && m.y < m.w) {  // join statistics over non-empty MBRs
-        nonempty++;
-        bx0 = min(bx0, m.x);
-        by0 = min(by0, m.y);
-        bx1 = max(bx1, m.z);
-        by1 = max(by1, m.w);
-        mw = max(mw, m.z - m.x);
-        mh = max(mh, m.w - m.y);
-#pragma unroll
-        for (int k = 0; k < kStatNK; k++) {
-          const int kk = k + kStatK0;
-          const unsigned cx = (unsigned)(((m.z - 1) >> kk) - (m.x >> kk) + 1);
-          const unsigned cy = (unsigned)(((m.w - 1) >> kk) - (m.y >> kk) + 1);
-          ent[k] += (unsigned long long)cx * cy;
-        }
-      }
+      prep_polygon(in_smem ? s_xy + (b - v0) : xy + b, e - b, poly, b, e, mbr, area, ecount, edges, status, validate,
+                   m);
+      if (lane == 0) acc.add(m);
     }
   }
   // block reduction of the statistics, then one atomic per field
@@ -164,18 +250,26 @@ __global__ void __launch_bounds__(kPrepThreads) prep_kernel(const int2* __restri
     s_b[4] = s_b[5] = 0;
   }
   __syncthreads();
+  for (int k = 0; k < kStatNK; k++) {
+    unsigned long long v = acc.ent[k];
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0 && v) atomicAdd(&s_ent[k], v);
+  }
+  {
+    unsigned long long v = acc.nonempty;
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0 && v) atomicAdd(&s_ent[kStatNK], v);
+  }
+  const int bx0 = __reduce_min_sync(0xffffffffu, acc.bx0), by0 = __reduce_min_sync(0xffffffffu, acc.by0);
+  const int bx1 = __reduce_max_sync(0xffffffffu, acc.bx1), by1 = __reduce_max_sync(0xffffffffu, acc.by1);
+  const int mw = __reduce_max_sync(0xffffffffu, acc.mw), mh = __reduce_max_sync(0xffffffffu, acc.mh);
   if (lane == 0) {
-    for (int k = 0; k < kStatNK; k++)
-      if (ent[k]) atomicAdd(&s_ent[k], ent[k]);
-    if (nonempty) {
-      atomicAdd(&s_ent[kStatNK], nonempty);
-      atomicMin(&s_b[0], bx0);
-      atomicMin(&s_b[1], by0);
-      atomicMax(&s_b[2], bx1);
-      atomicMax(&s_b[3], by1);
-      atomicMax(&s_b[4], mw);
-      atomicMax(&s_b[5], mh);
-    }
+    atomicMin(&s_b[0], bx0);
+    atomicMin(&s_b[1], by0);
+    atomicMax(&s_b[2], bx1);
+    atomicMax(&s_b[3], by1);
+    atomicMax(&s_b[4], mw);
+    atomicMax(&s_b[5], mh);
   }
   __syncthreads();
   if (threadIdx.x < kStatNK && s_ent[threadIdx.x]) atomicAdd(&stats->entries[threadIdx.x], s_ent[threadIdx.x]);
@@ -206,14 +300,18 @@ cudaError_t launch_prep(const sccg_polyset* s, int validate, cudaStream_t st) {
   SetStats* stats = reinterpret_cast<SetStats*>(s->stats);
   prep_init_kernel<<<1, 32, 0, st>>>(s->status, stats);
   if (s->n_polygons > 0) {
-    int dev = 0, sms = 148;
+    static cudaError_t attr = cudaFuncSetAttribute(prep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   (int)(kPrepVerts * sizeof(int2)));
+    if (attr != cudaSuccess) return attr;
+    int dev = 0, sms = 148, per_sm = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, prep_kernel, kPrepThreads, kPrepVerts * sizeof(int2));
     const int64_t ntiles = (s->n_polygons + kPrepPolys - 1) / kPrepPolys;
     int64_t blocks = ntiles;
-    const int64_t cap = (int64_t)sms * 4;  // 4 resident 256-thread CTAs per SM (48 KB smem each)
+    const int64_t cap = (int64_t)sms * (per_sm > 0 ? per_sm : 1);
     if (blocks > cap) blocks = cap;
-    prep_kernel<<<(unsigned)blocks, kPrepThreads, 0, st>>>(
+    prep_kernel<<<(unsigned)blocks, kPrepThreads, kPrepVerts * sizeof(int2), st>>>(
         reinterpret_cast<const int2*>(s->xy), s->offsets, s->n_polygons, s->n_vertices,
         reinterpret_cast<int4*>(s->mbr), s->area, reinterpret_cast<int2*>(s->ecount), s->edges, s->status, stats,
         validate);
