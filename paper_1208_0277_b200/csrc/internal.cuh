@@ -47,15 +47,16 @@ __device__ __forceinline__ unsigned suffix_mask(int k) { return shl_clamp(0xffff
 __device__ __forceinline__ unsigned low_bits(int n) { return ~shl_clamp(0xffffffffu, (unsigned)max(n, 0)); }
 
 // Per-set statistics written by sccg_prep (sccg_polyset.stats), read by the
-// join's on-device grid selection.  entries[k - kStatK0] = sum over non-empty
-// MBRs of the number of 2^k-pixel grid cells the MBR covers.
-constexpr int kStatK0 = 3, kStatNK = 11;
+// join's on-device grid selection: moments of the MBR extents over non-empty
+// MBRs (w, h = width, height): sw = sum(w - 1), sh = sum(h - 1),
+// swh = sum((w - 1)(h - 1)).  A 2^k grid cell count per MBR is at most
+// ((w-1)/2^k + 2)((h-1)/2^k + 2) and about (1 + (w-1)/2^k)(1 + (h-1)/2^k).
 struct SetStats {
   int32_t bounds[4];  // xmin, ymin, xmax, ymax over non-empty MBRs
   int32_t maxext[2];  // largest MBR width, height
   int32_t pad[2];
-  unsigned long long nonempty;
-  unsigned long long entries[kStatNK];
+  unsigned long long nonempty, sw, sh, swh;
+  unsigned long long reserved[8];
 };
 static_assert(sizeof(SetStats) == 128, "SetStats layout");
 

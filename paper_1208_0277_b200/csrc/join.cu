@@ -27,12 +27,22 @@ struct Grid {
 __device__ __forceinline__ bool mbr_empty(const int4& m) { return m.x >= m.z || m.y >= m.w; }
 
 static int64_t cell_cap(int64_t np, int64_t nq) { return np + nq + 1024; }
-static int64_t entry_cap(int64_t nq) { return 4 * nq + 1024; }
+static int64_t entry_cap(int64_t nq) { return 8 * nq + 1024; }
+
+// Upper bound and expectation of the 2^k-cell entries of one set (SetStats).
+__device__ __forceinline__ void set_entries(const SetStats* s, int k, double& bound, double& expect) {
+  const double c = 1.0 / (double)(1ll << k), n = (double)s->nonempty;
+  const double sw = (double)s->sw, sh = (double)s->sh, swh = (double)s->swh;
+  const double cont = swh * c * c + 2.0 * (sw + sh) * c + 4.0 * n;
+  const double ext = n * (double)(((s->maxext[0] - 1) >> k) + 2) * (double)(((s->maxext[1] - 1) >> k) + 2);
+  bound = cont < ext ? cont : ext;
+  expect = n + (sw + sh) * c + swh * c * c;
+}
 
 // Cell size 2^k minimising the expected work E_p + E_q + C/4 + E_p E_q / C
 // (bucket inserts + probes + scan + candidate tests) subject to the workspace
-// caps on cells C and Q-entries E_q.  Always feasible: once 2^k exceeds the
-// largest MBR extent each MBR covers at most 2 x 2 cells.
+// caps on cells C and (upper-bounded) Q-entries.  Always feasible: once 2^k
+// exceeds the largest MBR extent each MBR covers at most 2 x 2 cells.
 __global__ void grid_select_kernel(const SetStats* __restrict__ sp, const SetStats* __restrict__ sq, long long ccap,
                                    long long ecap, Grid* g) {
   if (threadIdx.x != 0) return;
@@ -45,20 +55,15 @@ __global__ void grid_select_kernel(const SetStats* __restrict__ sp, const SetSta
   const int xmin = min(sp->bounds[0], sq->bounds[0]), ymin = min(sp->bounds[1], sq->bounds[1]);
   const int xmax = max(sp->bounds[2], sq->bounds[2]), ymax = max(sp->bounds[3], sq->bounds[3]);
   double best = 1e300;
-  for (int k = kStatK0; k <= 30; k++) {
+  for (int k = 3; k <= 30; k++) {
     const double ncx = (double)(((xmax - 1) >> k) - (xmin >> k) + 1);
     const double ncy = (double)(((ymax - 1) >> k) - (ymin >> k) + 1);
     const double C = ncx * ncy;
-    double Ep, Eq;
-    if (k - kStatK0 < kStatNK) {
-      Ep = (double)sp->entries[k - kStatK0];
-      Eq = (double)sq->entries[k - kStatK0];
-    } else {
-      Ep = (double)sp->nonempty * (double)(((sp->maxext[0] - 1) >> k) + 2) * (double)(((sp->maxext[1] - 1) >> k) + 2);
-      Eq = (double)sq->nonempty * (double)(((sq->maxext[0] - 1) >> k) + 2) * (double)(((sq->maxext[1] - 1) >> k) + 2);
-    }
-    if (C > (double)ccap || Eq > (double)ecap) continue;
-    const double cost = Ep + Eq + 0.25 * C + Ep * Eq / C;
+    double bp, ep, bq, eq;
+    set_entries(sp, k, bp, ep);
+    set_entries(sq, k, bq, eq);
+    if (C > (double)ccap || bq > (double)ecap) continue;
+    const double cost = ep + eq + 0.25 * C + ep * eq / C;
     if (cost < best) {
       best = cost;
       r.k = k;

@@ -385,39 +385,62 @@ __global__ void __launch_bounds__(kWarps * 32, 3)
 // most 16 rows.  Per-pair results and sums are written lane-parallel.
 constexpr int kSmallWarps = 8;
 constexpr int kSmallCap = 64;   // vertical edges per polygon on this path
-constexpr int kSmallQOff = 65;  // q buffer offset (records): p[j], q[j] in different bank groups
+constexpr int kSmallQOff = 72;  // q buffer offset in records (8 B): 576 B, so p[t] and q[t] hit different banks
 
-__device__ __forceinline__ int stage_regs(uint64_t r0, uint64_t r1, int nv, int dx, int dy, int H, int4* buf) {
+// Stage one polygon's row-crossing edges for a box of H <= 32 rows and
+// W <= 32 columns as {row bits, pixel mask}: bit r of `rows` is set iff the
+// edge crosses row r of the box (ylo <= r < yhi), `mask` holds the pixels the
+// edge toggles.  Edges crossing no row are culled.  Branch-free (predicated
+// shared stores).  r0 / r1: the records of edges lane and lane + 32.
+__device__ __forceinline__ int stage_rows(uint64_t r0, uint64_t r1, int nv, int dx, int dy, int H, int2* buf) {
   const int lane = threadIdx.x & 31;
   int c, lo, hi;
   unpack_edge(r0, c, lo, hi);
-  int yl = lo + dy, yh = hi + dy;
-  bool keep = lane < nv && yl < H && yh > 0;
+  unsigned rows = low_bits(min(hi + dy, H)) & ~low_bits(lo + dy);
+  bool keep = lane < nv && rows != 0;
   unsigned b = __ballot_sync(FULL, keep);
-  if (keep) buf[__popc(b & lanemask_lt())] = make_int4(yl, yh - yl, (int)suffix_mask(c + dx), 0);
+  int2 v = make_int2((int)rows, (int)suffix_mask(c + dx));
+  if (keep) buf[__popc(b & lanemask_lt())] = v;
   int cnt = __popc(b);
   if (nv > 32) {
     unpack_edge(r1, c, lo, hi);
-    yl = lo + dy;
-    yh = hi + dy;
-    keep = lane + 32 < nv && yl < H && yh > 0;
+    rows = low_bits(min(hi + dy, H)) & ~low_bits(lo + dy);
+    keep = lane + 32 < nv && rows != 0;
     b = __ballot_sync(FULL, keep);
-    if (keep) buf[cnt + __popc(b & lanemask_lt())] = make_int4(yl, yh - yl, (int)suffix_mask(c + dx), 0);
+    v = make_int2((int)rows, (int)suffix_mask(c + dx));
+    if (keep) buf[cnt + __popc(b & lanemask_lt())] = v;
     cnt += __popc(b);
   }
   return cnt;
 }
 
-__device__ __forceinline__ unsigned row_word(const int4* __restrict__ b, int n, int row) {
-  unsigned m = 0;
-  for (int t = 0; t < n; t += 4) {
-#pragma unroll
-    for (int u = 0; u < 4; u++) {
-      const int4 r = b[t + u];
-      if ((unsigned)(row - r.x) < (unsigned)r.y) m ^= (unsigned)r.z;
+// m ^= mask if (rows & bit) != 0 -- one predicate-producing LOP3 and one
+// predicated LOP3 (the crossing test of one row against one edge).
+__device__ __forceinline__ void xor_if(unsigned& m, unsigned rows, unsigned bit, unsigned mask) {
+  asm("{\n\t.reg .pred p;\n\t.reg .b32 t;\n\tand.b32 t, %1, %2;\n\tsetp.ne.b32 p, t, 0;\n\t@p xor.b32 %0, %0, %3;\n\t}"
+      : "+r"(m)
+      : "r"(rows), "r"(bit), "r"(mask));
+}
+
+// Crossing parity words of rows `bit0` (and `bit1` when TWO) over n staged
+// edges (n a multiple of 4; two records per 16-byte shared load).
+template <bool TWO>
+__device__ __forceinline__ void row_words(const int2* __restrict__ b, int n, unsigned bit0, unsigned bit1,
+                                          unsigned& m0, unsigned& m1) {
+  const int4* b4 = reinterpret_cast<const int4*>(b);
+  for (int t = 0; t < (n >> 1); t += 2) {
+    const int4 u = b4[t], w = b4[t + 1];
+    xor_if(m0, u.x, bit0, u.y);
+    xor_if(m0, u.z, bit0, u.w);
+    xor_if(m0, w.x, bit0, w.y);
+    xor_if(m0, w.z, bit0, w.w);
+    if (TWO) {
+      xor_if(m1, u.x, bit1, u.y);
+      xor_if(m1, u.z, bit1, u.w);
+      xor_if(m1, w.x, bit1, w.y);
+      xor_if(m1, w.z, bit1, w.w);
     }
   }
-  return m;
 }
 
 __device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long v) {
@@ -434,11 +457,15 @@ __global__ void __launch_bounds__(kSmallWarps * 32, SCCG_SMALL_MINB)
                  long long* __restrict__ uni, sccg_sums* sums, int T, int mode, unsigned long long* queue,
                  long long* __restrict__ large_list, unsigned* large_count, long long* counters, long long np_,
                  long long nq_) {
-  __shared__ int4 s_buf[kSmallWarps][2 * kSmallQOff + 3];
+  __shared__ __align__(16) int2 s_buf[kSmallWarps][2 * kSmallQOff];
+  __shared__ int4 s_meta[kSmallWarps][32];
+  __shared__ int2 s_ep[kSmallWarps][32];
   __shared__ unsigned long long s_acc[kSmallWarps][16];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  int4* bp = s_buf[warp];
-  int4* bq = bp + kSmallQOff;
+  int2* bp = s_buf[warp];
+  int2* bq = bp + kSmallQOff;
+  int4* meta = s_meta[warp];
+  int2* epq = s_ep[warp];
   if (lane == 0)
     for (int i = 0; i < 16; i++) s_acc[warp][i] = 0;
   unsigned status = 0;
@@ -451,8 +478,6 @@ __global__ void __launch_bounds__(kSmallWarps * 32, SCCG_SMALL_MINB)
     // ---- lane-parallel metadata of pair k0 + lane
     bool ok = false, small = false, empty = false;
     int2 pq = make_int2(0, 0);
-    unsigned m0 = 0, mdp = 0, mdq = 0;
-    int ep = 0, eq = 0;
     if (k < n) {
       pq = pairs[k];
       ok = (unsigned)pq.x < (unsigned long long)np_ && (unsigned)pq.y < (unsigned long long)nq_;
@@ -468,12 +493,12 @@ __global__ void __launch_bounds__(kSmallWarps * 32, SCCG_SMALL_MINB)
       empty = !(W > 0 && H > 0);  // reading R18: I = 0
       small = !empty && W <= 32 && H <= 32 && (mode == 1 || W * H < T) && cp.x <= kSmallCap && cq.x <= kSmallCap &&
               op + cp.x < (1ll << 31) && oq + cq.x < (1ll << 31) && min(min(dxp, dyp), min(dxq, dyq)) >= -32768;
-      m0 = (unsigned)W | ((unsigned)H << 6) | ((unsigned)cp.x << 12) | ((unsigned)cq.x << 20);
-      mdp = ((unsigned)dxp & 0xffffu) | ((unsigned)dyp << 16);
-      mdq = ((unsigned)dxq & 0xffffu) | ((unsigned)dyq << 16);
-      ep = (int)op;
-      eq = (int)oq;
+      meta[lane] = make_int4((int)((unsigned)W | ((unsigned)H << 6) | ((unsigned)cp.x << 12) | ((unsigned)cq.x << 20)),
+                             (int)(((unsigned)dxp & 0xffffu) | ((unsigned)dyp << 16)),
+                             (int)(((unsigned)dxq & 0xffffu) | ((unsigned)dyq << 16)), 0);
+      epq[lane] = make_int2((int)op, (int)oq);
     }
+    __syncwarp();
     // ---- everything else goes to the generic kernel (warp-aggregated append)
     const bool large = ok && !empty && !small;
     const unsigned lb = __ballot_sync(FULL, large);
@@ -483,51 +508,49 @@ __global__ void __launch_bounds__(kSmallWarps * 32, SCCG_SMALL_MINB)
       base = __shfl_sync(FULL, base, 0);
       if (large) large_list[base + __popc(lb & lanemask_lt())] = k;
     }
-    // ---- small pairs, software-pipelined
+    // ---- small pairs, software-pipelined: records of the next pair are in
+    // flight into registers while the current pair is pixelized
     unsigned todo = __ballot_sync(FULL, small);
     unsigned myI = 0;
     uint64_t np0 = 0, np1 = 0, nq0 = 0, nq1 = 0;
     auto prefetch = [&](int j) {
-      const unsigned mj = __shfl_sync(FULL, m0, j);
+      const unsigned mj = (unsigned)meta[j].x;
+      const int2 e = epq[j];
       const int nvp = (mj >> 12) & 127, nvq = (mj >> 20) & 127;
-      const int epj = __shfl_sync(FULL, ep, j), eqj = __shfl_sync(FULL, eq, j);
-      np0 = lane < nvp ? __ldg(Ps.edges + epj + lane) : 0ull;
-      nq0 = lane < nvq ? __ldg(Qs.edges + eqj + lane) : 0ull;
-      np1 = lane + 32 < nvp ? __ldg(Ps.edges + epj + 32 + lane) : 0ull;
-      nq1 = lane + 32 < nvq ? __ldg(Qs.edges + eqj + 32 + lane) : 0ull;
+      const uint64_t* pe = Ps.edges + e.x;
+      const uint64_t* qe = Qs.edges + e.y;
+      np0 = lane < nvp ? __ldg(pe + lane) : 0ull;
+      nq0 = lane < nvq ? __ldg(qe + lane) : 0ull;
+      if (nvp > 32) np1 = lane + 32 < nvp ? __ldg(pe + 32 + lane) : 0ull;
+      if (nvq > 32) nq1 = lane + 32 < nvq ? __ldg(qe + 32 + lane) : 0ull;
     };
     if (todo) prefetch(__ffs(todo) - 1);
     unsigned long long c_tests = 0, c_px = 0;
+    const unsigned bit0 = 1u << (lane & 15), bit1 = 1u << ((lane & 15) + 16);
     while (todo) {
       const int j = __ffs(todo) - 1;
       todo &= todo - 1;
       const uint64_t cp0 = np0, cp1 = np1, cq0 = nq0, cq1 = nq1;
       if (todo) prefetch(__ffs(todo) - 1);
-      const unsigned mj = __shfl_sync(FULL, m0, j);
-      const unsigned dpj = __shfl_sync(FULL, mdp, j), dqj = __shfl_sync(FULL, mdq, j);
+      const int4 mm = meta[j];
+      const unsigned mj = (unsigned)mm.x, dpj = (unsigned)mm.y, dqj = (unsigned)mm.z;
       const int W = mj & 63, H = (mj >> 6) & 63, nvp = (mj >> 12) & 127, nvq = (mj >> 20) & 127;
-      const int cntp = stage_regs(cp0, cp1, nvp, (int)(short)(dpj & 0xffffu), (int)dpj >> 16, H, bp);
-      const int cntq = stage_regs(cq0, cq1, nvq, (int)(short)(dqj & 0xffffu), (int)dqj >> 16, H, bq);
+      const int cntp = stage_rows(cp0, cp1, nvp, (int)(short)(dpj & 0xffffu), (int)dpj >> 16, H, bp);
+      const int cntq = stage_rows(cq0, cq1, nvq, (int)(short)(dqj & 0xffffu), (int)dqj >> 16, H, bq);
+      // half-warp per polygon (lanes 0-15: p, 16-31: q), rows lane&15 (+16)
+      const int npad = (max(cntp, cntq) + 3) & ~3;
+      for (int t = cntp + lane; t < npad; t += 32) bp[t] = make_int2(0, 0);
+      for (int t = cntq + lane; t < npad; t += 32) bq[t] = make_int2(0, 0);
+      __syncwarp();
+      const int2* b = lane < 16 ? bp : bq;
+      unsigned m0 = 0, m1 = 0;
+      if (H <= 16)
+        row_words<false>(b, npad, bit0, bit1, m0, m1);
+      else
+        row_words<true>(b, npad, bit0, bit1, m0, m1);
+      const unsigned o0 = __shfl_xor_sync(FULL, m0, 16), o1 = __shfl_xor_sync(FULL, m1, 16);
       const unsigned wmask = low_bits(W);
-      unsigned cnt;
-      if (H <= 16) {  // half-warp per polygon
-        const int npad = (max(cntp, cntq) + 3) & ~3;
-        for (int t = cntp + lane; t < npad; t += 32) bp[t] = make_int4(0, 0, 0, 0);
-        for (int t = cntq + lane; t < npad; t += 32) bq[t] = make_int4(0, 0, 0, 0);
-        __syncwarp();
-        const int row = lane & 15;
-        const unsigned m = row_word(lane < 16 ? bp : bq, npad, row);
-        const unsigned mo = __shfl_xor_sync(FULL, m, 16);
-        cnt = (lane < 16 && row < H) ? __popc(m & mo & wmask) : 0u;
-      } else {  // one row per lane, both polygons
-        const int pp = (cntp + 3) & ~3, pq_ = (cntq + 3) & ~3;
-        if (cntp + lane < pp) bp[cntp + lane] = make_int4(0, 0, 0, 0);
-        if (cntq + lane < pq_) bq[cntq + lane] = make_int4(0, 0, 0, 0);
-        __syncwarp();
-        const unsigned mpw = row_word(bp, pp, lane);
-        const unsigned mqw = row_word(bq, pq_, lane);
-        cnt = lane < H ? __popc(mpw & mqw & wmask) : 0u;
-      }
+      const unsigned cnt = lane < 16 ? __popc(m0 & o0 & wmask) + __popc(m1 & o1 & wmask) : 0u;
       const unsigned I = __reduce_add_sync(FULL, cnt);
       if (lane == j) myI = I;
       if (COUNT) {

@@ -92,80 +92,83 @@ __device__ __forceinline__ void prep_polygon(const int2* v, int64_t V, int64_t p
   }
 }
 
-// One polygon by one thread (the common small ring): same arithmetic as
-// prep_polygon, serial over the ring's vertices in shared memory.
+// One polygon by one thread (the common small ring): same results as
+// prep_polygon, serial over the ring's vertices in shared memory, 32-bit
+// arithmetic on MBR-rebased coordinates (extents <= 65535, so each shoelace
+// product fits 32 bits unsigned; the sum is int64).
 __device__ __forceinline__ int4 prep_polygon_thread(const int2* v, int V, int64_t poly, int64_t b, int64_t e,
                                                     int4* __restrict__ mbr, int64_t* __restrict__ area,
                                                     int2* __restrict__ ecount, uint64_t* __restrict__ edges,
                                                     uint32_t* __restrict__ status, int validate) {
   int xmin = INT_MAX, ymin = INT_MAX, xmax = INT_MIN, ymax = INT_MIN;
-  bool bad_range = false;
+#pragma unroll 4
   for (int i = 0; i < V; i++) {
     const int2 a = v[i];
     xmin = min(xmin, a.x);
     xmax = max(xmax, a.x);
     ymin = min(ymin, a.y);
     ymax = max(ymax, a.y);
-    bad_range |= (int64_t)a.x > kMaxCoord || (int64_t)a.x < -kMaxCoord || (int64_t)a.y > kMaxCoord ||
-                 (int64_t)a.y < -kMaxCoord;
   }
-  bad_range = bad_range || (int64_t)xmax - xmin > kMaxExtent || (int64_t)ymax - ymin > kMaxExtent;
+  const int4 m = make_int4(xmin, ymin, xmax, ymax);
+  mbr[poly] = m;
+  const bool bad_range = (int64_t)xmin < -kMaxCoord || (int64_t)xmax > kMaxCoord || (int64_t)ymin < -kMaxCoord ||
+                         (int64_t)ymax > kMaxCoord || (int64_t)xmax - xmin > kMaxExtent ||
+                         (int64_t)ymax - ymin > kMaxExtent;
+  if (bad_range) {
+    area[poly] = 0;
+    ecount[poly] = make_int2(0, 0);
+    flag(status, SCCG_STATUS_RANGE, poly);
+    return m;
+  }
   long long twice_area = 0;
   bool diag = false;
   int nvert = 0, nhor = 0;
+  uint64_t* ev = edges + b;
+  uint64_t* eh = edges + e - 1;
   int2 a = v[0];
-  for (int i = 0; i < V; i++) {
-    const int2 c = v[i + 1 == V ? 0 : i + 1];
-    const int ax = a.x - xmin, ay = a.y - ymin, cx = c.x - xmin, cy = c.y - ymin;
-    twice_area += (long long)ax * cy - (long long)cx * ay;  // P:193, one term per vertex
-    if (a.x == c.x && a.y != c.y) {
-      if (!bad_range) edges[b + nvert] = pack_edge((uint32_t)ax, (uint32_t)min(ay, cy), (uint32_t)max(ay, cy));
-      nvert++;
-    } else if (a.y == c.y && a.x != c.x) {
-      if (!bad_range) edges[e - 1 - nhor] = pack_edge((uint32_t)ay, (uint32_t)min(ax, cx), (uint32_t)max(ax, cx));
-      nhor++;
-    } else if (a.x != c.x && a.y != c.y) {
+  unsigned ax = (unsigned)(a.x - xmin), ay = (unsigned)(a.y - ymin);
+  for (int i = 1; i <= V; i++) {
+    const int2 c = v[i == V ? 0 : i];
+    const unsigned cx = (unsigned)(c.x - xmin), cy = (unsigned)(c.y - ymin);
+    twice_area += (long long)(ax * cy) - (long long)(cx * ay);  // P:193, one term per vertex
+    if (ax == cx) {
+      if (ay != cy) ev[nvert++] = pack_edge(ax, min(ay, cy), max(ay, cy));
+    } else if (ay == cy) {
+      eh[-(nhor++)] = pack_edge(ay, min(ax, cx), max(ax, cx));
+    } else {
       diag = true;
     }
-    a = c;
+    ax = cx;
+    ay = cy;
   }
-  const int4 m = make_int4(xmin, ymin, xmax, ymax);
   area[poly] = (twice_area < 0 ? -twice_area : twice_area) / 2;
-  mbr[poly] = m;
-  ecount[poly] = bad_range ? make_int2(0, 0) : make_int2(nvert, nhor);
+  ecount[poly] = make_int2(nvert, nhor);
   if (validate && diag) flag(status, SCCG_STATUS_NOT_RECTILINEAR, poly);
-  if (bad_range) flag(status, SCCG_STATUS_RANGE, poly);
   return m;
 }
 
 struct StatAcc {
-  unsigned long long ent[kStatNK];
-  unsigned long long nonempty;
+  unsigned long long nonempty, sw, sh, swh;
   int bx0, by0, bx1, by1, mw, mh;
   __device__ __forceinline__ void init() {
-#pragma unroll
-    for (int k = 0; k < kStatNK; k++) ent[k] = 0;
-    nonempty = 0;
+    nonempty = sw = sh = swh = 0;
     bx0 = by0 = INT_MAX;
     bx1 = by1 = INT_MIN;
     mw = mh = 0;
   }
   __device__ __forceinline__ void add(const int4& m) {
     if (!(m.x < m.z && m.y < m.w)) return;
+    const unsigned w1 = (unsigned)(m.z - m.x - 1), h1 = (unsigned)(m.w - m.y - 1);
     nonempty++;
+    sw += w1;
+    sh += h1;
+    swh += (unsigned long long)w1 * h1;
     bx0 = min(bx0, m.x);
     by0 = min(by0, m.y);
     bx1 = max(bx1, m.z);
     by1 = max(by1, m.w);
     mw = max(mw, m.z - m.x);
     mh = max(mh, m.w - m.y);
-#pragma unroll
-    for (int k = 0; k < kStatNK; k++) {
-      const int kk = k + kStatK0;
-      const unsigned cx = (unsigned)(((m.z - 1) >> kk) - (m.x >> kk) + 1);
-      const unsigned cy = (unsigned)(((m.w - 1) >> kk) - (m.y >> kk) + 1);
-      ent[k] += (unsigned long long)cx * cy;
-    }
   }
 };
 
@@ -177,12 +180,12 @@ __global__ void __launch_bounds__(kPrepThreads) prep_kernel(const int2* __restri
                                                             int64_t* __restrict__ area, int2* __restrict__ ecount,
                                                             uint64_t* __restrict__ edges,
                                                             uint32_t* __restrict__ status, SetStats* stats,
-                                                            int validate) {
+                                                            int validate, int vec16) {
   extern __shared__ int4 s_dyn4[];  // kPrepVerts int2 (16-byte aligned)
   int2* s_xy = reinterpret_cast<int2*>(s_dyn4);
   __shared__ int64_t s_off[kPrepPolys + 1];
   __shared__ unsigned s_big[kPrepPolys / 32];
-  __shared__ unsigned long long s_ent[kStatNK + 1];
+  __shared__ unsigned long long s_acc[4];
   __shared__ int s_b[6];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   StatAcc acc;
@@ -195,19 +198,22 @@ __global__ void __launch_bounds__(kPrepThreads) prep_kernel(const int2* __restri
     for (int i = threadIdx.x; i <= np; i += blockDim.x) s_off[i] = off[p0 + i];
     if (threadIdx.x < kPrepPolys / 32) s_big[threadIdx.x] = 0;
     __syncthreads();
-    // stage the tile's vertex range with 16-byte loads (start rounded down to even)
+    // stage the tile's vertex range: 16-byte cp.async (LDGSTS) from an even
+    // start, no register round trip, many copies in flight per thread
     const int64_t v0 = s_off[0] & ~int64_t(1), v1 = s_off[np];
     const bool tiled = s_off[0] >= 0 && v1 <= nv_total && v1 >= s_off[0] && v1 - v0 <= kPrepVerts;
     if (tiled) {
-      const int64_t nvec = (v1 - v0 + 1) >> 1;
-      const int4* src = reinterpret_cast<const int4*>(xy + v0);
-      const bool tail_odd = ((v1 - v0) & 1) != 0;
-      for (int64_t i = threadIdx.x; i < nvec; i += blockDim.x) {
-        if (tail_odd && i == nvec - 1) {
-          s_xy[2 * i] = xy[v0 + 2 * i];  // last vector would read past the array
-        } else {
-          s_dyn4[i] = __ldg(src + i);
-        }
+      const int64_t nv = v1 - v0;
+      if (vec16) {
+        const int64_t nvec = nv >> 1;
+        const char* src = reinterpret_cast<const char*>(xy + v0);
+        const unsigned dst = (unsigned)__cvta_generic_to_shared(s_dyn4);
+        for (int64_t i = threadIdx.x; i < nvec; i += blockDim.x)
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst + (unsigned)(16 * i)), "l"(src + 16 * i));
+        if ((nv & 1) && threadIdx.x == 0) s_xy[nv - 1] = xy[v1 - 1];
+        asm volatile("cp.async.wait_all;\n" ::);
+      } else {
+        for (int64_t i = threadIdx.x; i < nv; i += blockDim.x) s_xy[i] = xy[v0 + i];
       }
     }
     __syncthreads();
@@ -243,22 +249,18 @@ __global__ void __launch_bounds__(kPrepThreads) prep_kernel(const int2* __restri
     }
   }
   // block reduction of the statistics, then one atomic per field
-  if (threadIdx.x < kStatNK + 1) s_ent[threadIdx.x] = 0;
+  if (threadIdx.x < 4) s_acc[threadIdx.x] = 0;
   if (threadIdx.x == 0) {
     s_b[0] = s_b[1] = INT_MAX;
     s_b[2] = s_b[3] = INT_MIN;
     s_b[4] = s_b[5] = 0;
   }
   __syncthreads();
-  for (int k = 0; k < kStatNK; k++) {
-    unsigned long long v = acc.ent[k];
-    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if (lane == 0 && v) atomicAdd(&s_ent[k], v);
-  }
-  {
-    unsigned long long v = acc.nonempty;
-    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if (lane == 0 && v) atomicAdd(&s_ent[kStatNK], v);
+  unsigned long long v[4] = {acc.nonempty, acc.sw, acc.sh, acc.swh};
+  for (int f = 0; f < 4; f++) {
+    unsigned long long x = v[f];
+    for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    if (lane == 0 && x) atomicAdd(&s_acc[f], x);
   }
   const int bx0 = __reduce_min_sync(0xffffffffu, acc.bx0), by0 = __reduce_min_sync(0xffffffffu, acc.by0);
   const int bx1 = __reduce_max_sync(0xffffffffu, acc.bx1), by1 = __reduce_max_sync(0xffffffffu, acc.by1);
@@ -272,9 +274,11 @@ __global__ void __launch_bounds__(kPrepThreads) prep_kernel(const int2* __restri
     atomicMax(&s_b[5], mh);
   }
   __syncthreads();
-  if (threadIdx.x < kStatNK && s_ent[threadIdx.x]) atomicAdd(&stats->entries[threadIdx.x], s_ent[threadIdx.x]);
-  if (threadIdx.x == 0 && s_ent[kStatNK]) {
-    atomicAdd(&stats->nonempty, s_ent[kStatNK]);
+  if (threadIdx.x == 0 && s_acc[0]) {
+    atomicAdd(&stats->nonempty, s_acc[0]);
+    atomicAdd(&stats->sw, s_acc[1]);
+    atomicAdd(&stats->sh, s_acc[2]);
+    atomicAdd(&stats->swh, s_acc[3]);
     atomicMin(&stats->bounds[0], s_b[0]);
     atomicMin(&stats->bounds[1], s_b[1]);
     atomicMax(&stats->bounds[2], s_b[2]);
@@ -291,9 +295,8 @@ __global__ void prep_init_kernel(uint32_t* status, SetStats* st) {
     st->bounds[0] = st->bounds[1] = INT_MAX;
     st->bounds[2] = st->bounds[3] = INT_MIN;
     st->maxext[0] = st->maxext[1] = 0;
-    st->nonempty = 0;
+    st->nonempty = st->sw = st->sh = st->swh = 0;
   }
-  if (threadIdx.x < kStatNK) st->entries[threadIdx.x] = 0;
 }
 
 cudaError_t launch_prep(const sccg_polyset* s, int validate, cudaStream_t st) {
@@ -314,7 +317,7 @@ cudaError_t launch_prep(const sccg_polyset* s, int validate, cudaStream_t st) {
     prep_kernel<<<(unsigned)blocks, kPrepThreads, kPrepVerts * sizeof(int2), st>>>(
         reinterpret_cast<const int2*>(s->xy), s->offsets, s->n_polygons, s->n_vertices,
         reinterpret_cast<int4*>(s->mbr), s->area, reinterpret_cast<int2*>(s->ecount), s->edges, s->status, stats,
-        validate);
+        validate, (reinterpret_cast<uintptr_t>(s->xy) & 15) == 0 ? 1 : 0);
   }
   return cudaGetLastError();
 }
