@@ -8,12 +8,14 @@
 
 namespace sccg {
 
-// Edge record (8 bytes, sccg_polyset.edges), relative to the polygon's MBR
-// lower-left corner so every field fits 16 bits (MBR extent <= 65535):
-//   vertical edge   x = const : c = x - xlo,  lo = ymin - ylo, hi = ymax - ylo
-//   horizontal edge y = const : c = y - ylo,  lo = xmin - xlo, hi = xmax - xlo
-// Vertical records of polygon i occupy edges[off[i] .. off[i] + nv), horizontal
-// records edges[off[i+1] - nh .. off[i+1]) (nv + nh <= vertex count).
+// Vertical-edge record (8 bytes, sccg_polyset.edges), relative to the
+// polygon's MBR lower-left corner so every field fits 16 bits (MBR extent
+// <= 65535): edge x = const from ymin to ymax:
+//   c = x - xlo, lo = ymin - ylo, hi = ymax - ylo.
+// The records of polygon i occupy edges[off[i] .. off[i] + nv) in ring order
+// (the rest of the polygon's slot is unspecified).  Horizontal edges are not
+// stored: only sampling-box classification needs them, and it reads them from
+// the ring itself.
 __host__ __device__ inline uint64_t pack_edge(uint32_t c, uint32_t lo, uint32_t hi) {
   return (uint64_t)c | ((uint64_t)lo << 16) | ((uint64_t)hi << 32);
 }
@@ -61,6 +63,7 @@ struct SetStats {
 static_assert(sizeof(SetStats) == 128, "SetStats layout");
 
 struct DevSet {
+  const int2* xy;
   const int64_t* off;
   const int4* mbr;
   const int64_t* area;
@@ -69,7 +72,7 @@ struct DevSet {
 };
 
 inline DevSet dev_set(const sccg_polyset* s) {
-  return DevSet{s->offsets, reinterpret_cast<const int4*>(s->mbr), s->area,
+  return DevSet{reinterpret_cast<const int2*>(s->xy), s->offsets, reinterpret_cast<const int4*>(s->mbr), s->area,
                 reinterpret_cast<const int2*>(s->ecount), s->edges};
 }
 

@@ -34,10 +34,11 @@ constexpr int kChunk = 4;        // pairs claimed per queue atomic
 constexpr unsigned FULL = 0xffffffffu;
 
 struct PairCtx {
-  const uint64_t* ev;  // vertical records
-  const uint64_t* eh;  // horizontal records
-  int nv, nh;
-  int dx, dy;  // polygon MBR origin minus root-box origin
+  const uint64_t* ev;  // vertical edge records (sccg_prep)
+  const int2* v;       // the ring's raw vertices (horizontal edges are read from these)
+  int nv, nh, V;       // vertical edges, horizontal edges, vertices
+  int dx, dy;          // polygon MBR origin minus root-box origin
+  int ox, oy;          // root-box origin (absolute)
 };
 
 struct Split {
@@ -90,10 +91,12 @@ __device__ __forceinline__ void classify(const PairCtx& c, int dx, int dy, int W
       }
     }
   }
-  for (int j = lane; j < c.nh; j += 32) {
-    int cc, lo, hi;
-    unpack_edge(__ldg(c.eh + j), cc, lo, hi);
-    const int y = cc + dy, xl = lo + dx, xh = hi + dx;
+  // horizontal edges straight from the ring: edge (v_j, v_j+1) with equal y
+  const int ax0 = c.ox + (c.dx - dx), ay0 = c.oy + (c.dy - dy);  // absolute origin of the box
+  for (int j = lane; j < c.V; j += 32) {
+    const int2 a = __ldg(c.v + j), b = __ldg(c.v + (j + 1 == c.V ? 0 : j + 1));
+    if (a.y != b.y || a.x == b.x) continue;
+    const int y = a.y - ay0, xl = min(a.x, b.x) - ax0, xh = max(a.x, b.x) - ax0;
     if (y > 0 && y < Hb && (y & (sy - 1)) != 0 && xl < Wb && xh > 0) {
       const int c_lo = max(0, xl >> g.lsx), c_hi = min(g.ncols - 1, (xh - 1) >> g.lsx);
       h |= low_bits(c_hi - c_lo + 1) << (((y >> g.lsy) << g.lkx) + c_lo);
@@ -240,7 +243,7 @@ __device__ long long sample(int W, int H, const PairCtx& P, const PairCtx& Q, ui
     if (COUNT && lane == 0) {
       atomicAdd((unsigned long long*)&counters[SCCG_CNT_BOXES], (unsigned long long)__popc(valid));
       atomicAdd((unsigned long long*)&counters[SCCG_CNT_BOXEDGES],
-                (unsigned long long)(P.nv + P.nh + Q.nv + Q.nh));
+                (unsigned long long)(P.nv + P.V + Q.nv + Q.V));
       atomicAdd((unsigned long long*)&counters[SCCG_CNT_SPLITS], 1ull);
     }
     if (top + ncont > kStackCap) {
@@ -316,18 +319,25 @@ __global__ void __launch_bounds__(kWarps * 32, 3)
     const int bx1 = min(mp.z, mq.z), by1 = min(mp.w, mq.w);
     const int2 cp = Ps.ecount[pq.x], cq = Qs.ecount[pq.y];
     PairCtx P, Q;
-    P.ev = Ps.edges + Ps.off[pq.x];
-    P.eh = Ps.edges + Ps.off[pq.x + 1] - cp.y;
+    const long long op = Ps.off[pq.x], oq = Qs.off[pq.y];
+    P.ev = Ps.edges + op;
+    P.v = Ps.xy + op;
+    P.V = (int)(Ps.off[pq.x + 1] - op);
     P.nv = cp.x;
     P.nh = cp.y;
     P.dx = mp.x - bx0;
     P.dy = mp.y - by0;
-    Q.ev = Qs.edges + Qs.off[pq.y];
-    Q.eh = Qs.edges + Qs.off[pq.y + 1] - cq.y;
+    P.ox = bx0;
+    P.oy = by0;
+    Q.ev = Qs.edges + oq;
+    Q.v = Qs.xy + oq;
+    Q.V = (int)(Qs.off[pq.y + 1] - oq);
     Q.nv = cq.x;
     Q.nh = cq.y;
     Q.dx = mq.x - bx0;
     Q.dy = mq.y - by0;
+    Q.ox = bx0;
+    Q.oy = by0;
     const int W = bx1 - bx0, H = by1 - by0;
     if (COUNT && lane == 0) atomicAdd((unsigned long long*)&counters[SCCG_CNT_ROOTPX], (unsigned long long)W * H);
     long long acc;
@@ -390,28 +400,30 @@ constexpr int kSmallQOff = 72;  // q buffer offset in records (8 B): 576 B, so p
 // Stage one polygon's row-crossing edges for a box of H <= 32 rows and
 // W <= 32 columns as {row bits, pixel mask}: bit r of `rows` is set iff the
 // edge crosses row r of the box (ylo <= r < yhi), `mask` holds the pixels the
-// edge toggles.  Edges crossing no row are culled.  Branch-free (predicated
-// shared stores).  r0 / r1: the records of edges lane and lane + 32.
-__device__ __forceinline__ int stage_rows(uint64_t r0, uint64_t r1, int nv, int dx, int dy, int H, int2* buf) {
+// edge toggles.  Edges crossing no row are culled; every slot of the 32-record
+// block (64 with `two`) is written -- kept records first, then zero records
+// (no-ops) -- so no padding pass is needed.  Returns the loop length.
+__device__ __forceinline__ int stage_rows(uint64_t r0, uint64_t r1, int nv, bool two, int dx, int dy, int H,
+                                          int2* buf) {
   const int lane = threadIdx.x & 31;
+  const unsigned lt = lanemask_lt();
   int c, lo, hi;
   unpack_edge(r0, c, lo, hi);
   unsigned rows = low_bits(min(hi + dy, H)) & ~low_bits(lo + dy);
   bool keep = lane < nv && rows != 0;
   unsigned b = __ballot_sync(FULL, keep);
-  int2 v = make_int2((int)rows, (int)suffix_mask(c + dx));
-  if (keep) buf[__popc(b & lanemask_lt())] = v;
   int cnt = __popc(b);
-  if (nv > 32) {
-    unpack_edge(r1, c, lo, hi);
-    rows = low_bits(min(hi + dy, H)) & ~low_bits(lo + dy);
-    keep = lane + 32 < nv && rows != 0;
-    b = __ballot_sync(FULL, keep);
-    v = make_int2((int)rows, (int)suffix_mask(c + dx));
-    if (keep) buf[cnt + __popc(b & lanemask_lt())] = v;
-    cnt += __popc(b);
-  }
-  return cnt;
+  buf[keep ? __popc(b & lt) : cnt + __popc(~b & lt)] =
+      keep ? make_int2((int)rows, (int)suffix_mask(c + dx)) : make_int2(0, 0);
+  if (!two) return cnt;
+  unpack_edge(r1, c, lo, hi);
+  rows = low_bits(min(hi + dy, H)) & ~low_bits(lo + dy);
+  keep = lane + 32 < nv && rows != 0;
+  b = __ballot_sync(FULL, keep);
+  cnt = __popc(b);
+  buf[32 + (keep ? __popc(b & lt) : cnt + __popc(~b & lt))] =
+      keep ? make_int2((int)rows, (int)suffix_mask(c + dx)) : make_int2(0, 0);
+  return 32 + cnt;
 }
 
 // m ^= mask if (rows & bit) != 0 -- one predicate-producing LOP3 and one
@@ -535,12 +547,11 @@ __global__ void __launch_bounds__(kSmallWarps * 32, SCCG_SMALL_MINB)
       const int4 mm = meta[j];
       const unsigned mj = (unsigned)mm.x, dpj = (unsigned)mm.y, dqj = (unsigned)mm.z;
       const int W = mj & 63, H = (mj >> 6) & 63, nvp = (mj >> 12) & 127, nvq = (mj >> 20) & 127;
-      const int cntp = stage_rows(cp0, cp1, nvp, (int)(short)(dpj & 0xffffu), (int)dpj >> 16, H, bp);
-      const int cntq = stage_rows(cq0, cq1, nvq, (int)(short)(dqj & 0xffffu), (int)dqj >> 16, H, bq);
+      const bool two = max(nvp, nvq) > 32;
+      const int cntp = stage_rows(cp0, cp1, nvp, two, (int)(short)(dpj & 0xffffu), (int)dpj >> 16, H, bp);
+      const int cntq = stage_rows(cq0, cq1, nvq, two, (int)(short)(dqj & 0xffffu), (int)dqj >> 16, H, bq);
       // half-warp per polygon (lanes 0-15: p, 16-31: q), rows lane&15 (+16)
       const int npad = (max(cntp, cntq) + 3) & ~3;
-      for (int t = cntp + lane; t < npad; t += 32) bp[t] = make_int2(0, 0);
-      for (int t = cntq + lane; t < npad; t += 32) bq[t] = make_int2(0, 0);
       __syncwarp();
       const int2* b = lane < 16 ? bp : bq;
       unsigned m0 = 0, m1 = 0;

@@ -26,29 +26,41 @@ __device__ __forceinline__ void flag(uint32_t* status, uint32_t bit, int64_t pol
   atomicMin(&status[1], (uint32_t)min(poly, (int64_t)0x7fffffff));
 }
 
-// One polygon by one warp; `v` points at its first vertex (shared or global).
-__device__ __forceinline__ void prep_polygon(const int2* v, int64_t V, int64_t poly, int64_t b, int64_t e,
+// One polygon by one warp.  `v` points at its first vertex (shared or
+// global); vertical-edge records are written to `out` (compacted, ring order).
+// When out aliases v (shared-memory tile) the writes are safe: a record lands
+// at or before the vertex slot the warp has already read in this chunk.
+__device__ __forceinline__ int4 prep_polygon(const int2* v, int64_t V, int64_t poly, uint64_t* out,
                                              int4* __restrict__ mbr, int64_t* __restrict__ area,
-                                             int2* __restrict__ ecount, uint64_t* __restrict__ edges,
-                                             uint32_t* __restrict__ status, int validate, int4& out_mbr) {
+                                             int2* __restrict__ ecount, uint32_t* __restrict__ status,
+                                             int validate) {
   const int lane = threadIdx.x & 31;
   int xmin = INT_MAX, ymin = INT_MAX, xmax = INT_MIN, ymax = INT_MIN;
-  bool bad_range = false;
   for (int64_t i = lane; i < V; i += 32) {
     const int2 a = v[i];
     xmin = min(xmin, a.x);
     xmax = max(xmax, a.x);
     ymin = min(ymin, a.y);
     ymax = max(ymax, a.y);
-    bad_range |= (int64_t)a.x > kMaxCoord || (int64_t)a.x < -kMaxCoord || (int64_t)a.y > kMaxCoord ||
-                 (int64_t)a.y < -kMaxCoord;
   }
   xmin = __reduce_min_sync(0xffffffffu, xmin);
   ymin = __reduce_min_sync(0xffffffffu, ymin);
   xmax = __reduce_max_sync(0xffffffffu, xmax);
   ymax = __reduce_max_sync(0xffffffffu, ymax);
-  bad_range = __any_sync(0xffffffffu, bad_range) || (int64_t)xmax - xmin > kMaxExtent ||
-              (int64_t)ymax - ymin > kMaxExtent;
+  const int4 m = make_int4(xmin, ymin, xmax, ymax);
+  const bool bad_range = (int64_t)xmin < -kMaxCoord || (int64_t)xmax > kMaxCoord || (int64_t)ymin < -kMaxCoord ||
+                         (int64_t)ymax > kMaxCoord || (int64_t)xmax - xmin > kMaxExtent ||
+                         (int64_t)ymax - ymin > kMaxExtent;
+  if (bad_range) {
+    if (lane == 0) {
+      mbr[poly] = m;
+      area[poly] = 0;
+      ecount[poly] = make_int2(0, 0);
+      flag(status, SCCG_STATUS_RANGE, poly);
+    }
+    return m;
+  }
+  const int2 first = v[0];
   long long twice_area = 0;
   bool diag = false;
   int nvert = 0, nhor = 0;
@@ -58,47 +70,39 @@ __device__ __forceinline__ void prep_polygon(const int2* v, int64_t V, int64_t p
     uint64_t rec = 0;
     if (i < V) {
       const int2 a = v[i];
-      const int2 c = v[i + 1 == V ? 0 : i + 1];
-      const long long ax = a.x - xmin, ay = a.y - ymin, cx = c.x - xmin, cy = c.y - ymin;
-      twice_area += ax * cy - cx * ay;  // P:193, one term per thread
-      if (a.x == c.x && a.y != c.y) {
-        is_v = true;
-        rec = pack_edge((uint32_t)ax, (uint32_t)min(ay, cy), (uint32_t)max(ay, cy));
-      } else if (a.y == c.y && a.x != c.x) {
-        is_h = true;
-        rec = pack_edge((uint32_t)ay, (uint32_t)min(ax, cx), (uint32_t)max(ax, cx));
-      } else if (a.x != c.x && a.y != c.y) {
-        diag = true;
-      }
+      const int2 c = i + 1 == V ? first : v[i + 1];
+      const unsigned ax = a.x - xmin, ay = a.y - ymin, cx = c.x - xmin, cy = c.y - ymin;
+      twice_area += (long long)(ax * cy) - (long long)(cx * ay);  // P:193, one term per thread
+      is_v = ax == cx && ay != cy;
+      is_h = ay == cy && ax != cx;
+      diag |= ax != cx && ay != cy;
+      rec = pack_edge(ax, min(ay, cy), max(ay, cy));
     }
-    const unsigned bv = __ballot_sync(0xffffffffu, is_v), bh = __ballot_sync(0xffffffffu, is_h);
-    if (!bad_range) {
-      if (is_v) edges[b + nvert + __popc(bv & lanemask_lt())] = rec;
-      if (is_h) edges[e - 1 - (nhor + __popc(bh & lanemask_lt()))] = rec;
-    }
+    const unsigned bv = __ballot_sync(0xffffffffu, is_v);  // all lanes have read before anyone writes
+    nhor += __popc(__ballot_sync(0xffffffffu, is_h));
+    if (is_v) out[nvert + __popc(bv & lanemask_lt())] = rec;
     nvert += __popc(bv);
-    nhor += __popc(bh);
+    __syncwarp();
   }
   for (int o = 16; o; o >>= 1) twice_area += __shfl_xor_sync(0xffffffffu, twice_area, o);
   diag = __any_sync(0xffffffffu, diag);
-  out_mbr = make_int4(xmin, ymin, xmax, ymax);
   if (lane == 0) {
-    const long long a2 = twice_area < 0 ? -twice_area : twice_area;
-    area[poly] = a2 / 2;
-    mbr[poly] = out_mbr;
-    ecount[poly] = bad_range ? make_int2(0, 0) : make_int2(nvert, nhor);
+    area[poly] = (twice_area < 0 ? -twice_area : twice_area) / 2;
+    mbr[poly] = m;
+    ecount[poly] = make_int2(nvert, nhor);
     if (validate && diag) flag(status, SCCG_STATUS_NOT_RECTILINEAR, poly);
-    if (bad_range) flag(status, SCCG_STATUS_RANGE, poly);
   }
+  return m;
 }
 
 // One polygon by one thread (the common small ring): same results as
-// prep_polygon, serial over the ring's vertices in shared memory, 32-bit
-// arithmetic on MBR-rebased coordinates (extents <= 65535, so each shoelace
-// product fits 32 bits unsigned; the sum is int64).
-__device__ __forceinline__ int4 prep_polygon_thread(const int2* v, int V, int64_t poly, int64_t b, int64_t e,
-                                                    int4* __restrict__ mbr, int64_t* __restrict__ area,
-                                                    int2* __restrict__ ecount, uint64_t* __restrict__ edges,
+// prep_polygon, serial over the ring's vertices in the shared-memory tile,
+// 32-bit arithmetic on MBR-rebased coordinates (extents <= 65535, so each
+// shoelace product fits 32 bits unsigned; the sum is int64).  Records are
+// written in place over the ring's own vertex slot: record k lands in slot
+// k <= i - 1 while vertex i is being read.
+__device__ __forceinline__ int4 prep_polygon_thread(int2* v, int V, int64_t poly, int4* __restrict__ mbr,
+                                                    int64_t* __restrict__ area, int2* __restrict__ ecount,
                                                     uint32_t* __restrict__ status, int validate) {
   int xmin = INT_MAX, ymin = INT_MAX, xmax = INT_MIN, ymax = INT_MIN;
 #pragma unroll 4
@@ -111,36 +115,35 @@ __device__ __forceinline__ int4 prep_polygon_thread(const int2* v, int V, int64_
   }
   const int4 m = make_int4(xmin, ymin, xmax, ymax);
   mbr[poly] = m;
-  const bool bad_range = (int64_t)xmin < -kMaxCoord || (int64_t)xmax > kMaxCoord || (int64_t)ymin < -kMaxCoord ||
-                         (int64_t)ymax > kMaxCoord || (int64_t)xmax - xmin > kMaxExtent ||
-                         (int64_t)ymax - ymin > kMaxExtent;
-  if (bad_range) {
+  if ((int64_t)xmin < -kMaxCoord || (int64_t)xmax > kMaxCoord || (int64_t)ymin < -kMaxCoord ||
+      (int64_t)ymax > kMaxCoord || (int64_t)xmax - xmin > kMaxExtent || (int64_t)ymax - ymin > kMaxExtent) {
     area[poly] = 0;
     ecount[poly] = make_int2(0, 0);
     flag(status, SCCG_STATUS_RANGE, poly);
     return m;
   }
+  uint64_t* out = reinterpret_cast<uint64_t*>(v);
   long long twice_area = 0;
   bool diag = false;
   int nvert = 0, nhor = 0;
-  uint64_t* ev = edges + b;
-  uint64_t* eh = edges + e - 1;
-  int2 a = v[0];
-  unsigned ax = (unsigned)(a.x - xmin), ay = (unsigned)(a.y - ymin);
-  for (int i = 1; i <= V; i++) {
-    const int2 c = v[i == V ? 0 : i];
-    const unsigned cx = (unsigned)(c.x - xmin), cy = (unsigned)(c.y - ymin);
+  const unsigned fx = v[0].x - xmin, fy = v[0].y - ymin;
+  unsigned ax = fx, ay = fy;
+  auto edge = [&](unsigned cx, unsigned cy) {
     twice_area += (long long)(ax * cy) - (long long)(cx * ay);  // P:193, one term per vertex
-    if (ax == cx) {
-      if (ay != cy) ev[nvert++] = pack_edge(ax, min(ay, cy), max(ay, cy));
-    } else if (ay == cy) {
-      eh[-(nhor++)] = pack_edge(ay, min(ax, cx), max(ax, cx));
-    } else {
-      diag = true;
-    }
+    const bool is_v = ax == cx && ay != cy;
+    nhor += (ay == cy && ax != cx) ? 1 : 0;
+    diag |= ax != cx && ay != cy;
+    const uint64_t rec = pack_edge(ax, min(ay, cy), max(ay, cy));
+    if (is_v) out[nvert] = rec;
+    nvert += is_v ? 1 : 0;
     ax = cx;
     ay = cy;
+  };
+  for (int i = 1; i < V; i++) {
+    const int2 c = v[i];
+    edge((unsigned)(c.x - xmin), (unsigned)(c.y - ymin));
   }
+  edge(fx, fy);  // closing edge back to the first vertex
   area[poly] = (twice_area < 0 ? -twice_area : twice_area) / 2;
   ecount[poly] = make_int2(nvert, nhor);
   if (validate && diag) flag(status, SCCG_STATUS_NOT_RECTILINEAR, poly);
@@ -217,7 +220,7 @@ __global__ void __launch_bounds__(kPrepThreads) prep_kernel(const int2* __restri
       }
     }
     __syncthreads();
-    // thread per small ring
+    // thread per small ring (records in place in the tile)
     for (int j = threadIdx.x; j < np; j += blockDim.x) {
       const int64_t poly = p0 + j;
       const int64_t b = s_off[j], e = s_off[j + 1];
@@ -229,23 +232,40 @@ __global__ void __launch_bounds__(kPrepThreads) prep_kernel(const int2* __restri
         flag(status, SCCG_STATUS_ARG, poly);
         continue;
       }
-      if (V > kThreadMaxV || !(tiled && b >= v0 && e <= v1)) {
+      if (V > kThreadMaxV || !tiled) {
         atomicOr(&s_big[j >> 5], 1u << (j & 31));
         continue;
       }
-      acc.add(prep_polygon_thread(s_xy + (b - v0), (int)V, poly, b, e, mbr, area, ecount, edges, status, validate));
+      acc.add(prep_polygon_thread(s_xy + (b - v0), (int)V, poly, mbr, area, ecount, status, validate));
     }
     __syncthreads();
-    // warp per large ring
-    for (int j = warp; j < np; j += kPrepThreads / 32) {
-      if (!((s_big[j >> 5] >> (j & 31)) & 1u)) continue;
-      const int64_t poly = p0 + j;
-      const int64_t b = s_off[j], e = s_off[j + 1];
-      const bool in_smem = tiled && b >= v0 && e <= v1;
-      int4 m;
-      prep_polygon(in_smem ? s_xy + (b - v0) : xy + b, e - b, poly, b, e, mbr, area, ecount, edges, status, validate,
-                   m);
-      if (lane == 0) acc.add(m);
+    // warp per large ring (in the tile when tiled, else straight from global)
+    for (int w = 0; w < kPrepPolys / 32; w++) {
+      unsigned bits = s_big[w];
+      for (int t = 0; bits; t++) {
+        const int bit = __ffs(bits) - 1;
+        bits &= bits - 1;
+        if ((t & (kPrepThreads / 32 - 1)) != warp) continue;
+        const int j = w * 32 + bit;
+        const int64_t poly = p0 + j;
+        const int64_t b = s_off[j], e = s_off[j + 1];
+        int2* src = tiled ? s_xy + (b - v0) : const_cast<int2*>(xy) + b;
+        uint64_t* out = tiled ? reinterpret_cast<uint64_t*>(src) : edges + b;
+        const int4 m = prep_polygon(src, e - b, poly, out, mbr, area, ecount, status, validate);
+        if (lane == 0) acc.add(m);
+      }
+    }
+    __syncthreads();
+    // coalesced write-out of the tile's records (16-byte stores when aligned)
+    if (tiled) {
+      const int64_t nv = v1 - v0;
+      if (vec16 && (reinterpret_cast<uintptr_t>(edges) & 15) == 0) {
+        int4* dst = reinterpret_cast<int4*>(edges + v0);
+        for (int64_t i = threadIdx.x; i < (nv >> 1); i += blockDim.x) dst[i] = s_dyn4[i];
+        if ((nv & 1) && threadIdx.x == 0) edges[v1 - 1] = reinterpret_cast<const uint64_t*>(s_xy)[nv - 1];
+      } else {
+        for (int64_t i = threadIdx.x; i < nv; i += blockDim.x) edges[v0 + i] = reinterpret_cast<const uint64_t*>(s_xy)[i];
+      }
     }
   }
   // block reduction of the statistics, then one atomic per field
