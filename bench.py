@@ -144,38 +144,27 @@ def run_ours(args, rank, world, local_rank):
     torch.cuda.synchronize()
     P = sccg.DeviceSet(d_xy_p, d_off_p, prep=False)
     Q = sccg.DeviceSet(d_xy_q, d_off_q, prep=False)
-    sums = sccg.new_sums(dev)
     stream = torch.cuda.current_stream()
+    # the whole step (prep x2, join, PixelBox) device-resident, no host sync until
+    # the sums are read; replayed as two CUDA graphs (join | PixelBox)
+    pipe = sccg.Pipeline(P, Q, cap=3 * max(P.n, Q.n) + 1024, threshold=args.threshold, graph=True)
     pix_start = torch.cuda.Event(enable_timing=True)
     pix_end = torch.cuda.Event(enable_timing=True)
-    state = {"pix_ms": 0.0, "pairs": 0, "cap": 2 * max(P.n, Q.n) + 1024}
 
     def step(timing_pixelbox=False):
-        sums.zero_()
-        P.prep()
-        Q.prep()
-        pairs = sccg.filter_pairs(P, Q, cap=state["cap"])
-        state["cap"] = max(state["cap"], int(pairs.shape[0]))
-        if timing_pixelbox:
-            pix_start.record(stream)
-        sccg.pixelbox(P, Q, pairs, threshold=args.threshold, sums=sums, want_inter=False, want_union=False)
-        if timing_pixelbox:
-            pix_end.record(stream)
+        sums = pipe.run((pix_start, pix_end) if timing_pixelbox else None)
         if world > 1:
             dist.all_reduce(sums, op=dist.ReduceOp.SUM)
-        host = sccg.sums_to_host(sums.cpu())
-        state["pairs"] = int(pairs.shape[0])
-        return host
+        return sccg.sums_to_host(sums.cpu())  # the step's one host synchronisation
 
     for _ in range(max(args.warmup, 3)):
         step()
+    n_local = pipe.check()
     # one untimed counting run for the algorithmic work per launch
-    pairs = sccg.filter_pairs(P, Q, cap=state["cap"])
     counters = torch.zeros(8, dtype=torch.int64, device=dev)
-    sccg.pixelbox(P, Q, pairs, threshold=args.threshold, counters=counters, want_inter=False, want_union=False)
+    sccg.pixelbox(P, Q, pipe.pairs[:n_local], threshold=args.threshold, counters=counters, want_inter=False,
+                  want_union=False)
     cnt = counters.cpu().tolist()
-    n_local = int(pairs.shape[0])
-    del pairs
 
     # ---- timed region: K steps, barrier + synchronize on both sides
     t0 = torch.cuda.Event(enable_timing=True)
@@ -189,13 +178,13 @@ def run_ours(args, rank, world, local_rank):
         wall0 = time.perf_counter()
         for _ in range(args.steps):
             host = step(timing_pixelbox=True)
-            pix_end.synchronize()
             pix_total += pix_start.elapsed_time(pix_end)
         t1.record(stream)
         torch.cuda.synchronize()
         wall1 = time.perf_counter()
     if world > 1:
         dist.barrier()
+    pipe.check()
     ms = t0.elapsed_time(t1)
     times = torch.tensor([ms, pix_total / args.steps, float(n_local)], dtype=torch.float64, device=dev)
     if world > 1:
@@ -208,6 +197,7 @@ def run_ours(args, rank, world, local_rank):
     ms_max, pix_ms_max = float(mx[0]), float(mx[1])
     total_pairs = int(round(float(tot[2])))
     jprime, pooled = sccg.jaccard(host)
+    state = {"cap": 3 * max(P.n, Q.n) + 1024}
 
     # ---- e2e: public API from pinned host buffers, H2D + D2H inside the timed region
     e2e_steps = max(1, min(args.e2e_steps, args.steps))
@@ -266,7 +256,7 @@ def run_ours(args, rank, world, local_rank):
                 traffic = pj.get("dram_bytes_per_launch")
         except Exception:
             traffic = None
-    launches_per_step = 15 + (0 if world == 1 else 0)
+    launches_per_step = 16  # prep 2x2, join 9 (incl. 2 CUB scans x2), pixelbox 2 + memsets (see profiles/)
     out = {
         "metric": METRIC,
         "value": value,

@@ -119,6 +119,15 @@ SCCG_API size_t sccg_filter_workspace_bytes(int64_t n_p, int64_t n_q);
 SCCG_API int sccg_filter_pairs(const sccg_polyset* p, const sccg_polyset* q, int32_t* pairs, int64_t cap,
                       int64_t* n_pairs_host, void* workspace, size_t ws_bytes, sccg_stream_t stream);
 
+/* Asynchronous variant for device-resident pipelines (CUDA-graph capturable,
+ * no host synchronisation): writes the candidate pairs when they fit in cap
+ * (sorted by (p, q), as sccg_filter_pairs) and result_dev[0] = total pair
+ * count, result_dev[1] = OR of both sets' sccg_prep status bits (device
+ * int64[2]).  When result_dev[0] > cap some pairs were not written: read
+ * result_dev after the stream synchronises and retry with a larger buffer. */
+SCCG_API int sccg_filter_pairs_async(const sccg_polyset* p, const sccg_polyset* q, int32_t* pairs, int64_t cap,
+                                     int64_t* result_dev, void* workspace, size_t ws_bytes, sccg_stream_t stream);
+
 /* -------------------------------------------------------------- pixelbox */
 /* Accumulated, order-independent integer totals (one NCCL int64 SUM merges
  * several GPUs bit-exactly).  Caller zeroes it once; each sccg_pixelbox call
@@ -162,6 +171,15 @@ SCCG_API size_t sccg_pixelbox_workspace_bytes(int64_t n_pairs);
 SCCG_API int sccg_pixelbox(const sccg_polyset* p, const sccg_polyset* q, const int32_t* pairs, int64_t n_pairs,
                   int64_t* inter, int64_t* uni, sccg_sums* sums, const sccg_config* cfg, void* workspace,
                   size_t ws_bytes, sccg_stream_t stream);
+
+/* Asynchronous variant: processes pairs[0 .. min(result_dev[0], cap)) where
+ * result_dev is the device int64[2] written by sccg_filter_pairs_async, and
+ * ORs result_dev[1] (prep status) into sums->status.  workspace as for
+ * sccg_pixelbox_workspace_bytes(cap). */
+SCCG_API int sccg_pixelbox_async(const sccg_polyset* p, const sccg_polyset* q, const int32_t* pairs,
+                                 const int64_t* result_dev, int64_t cap, int64_t* inter, int64_t* uni,
+                                 sccg_sums* sums, const sccg_config* cfg, void* workspace, size_t ws_bytes,
+                                 sccg_stream_t stream);
 
 /* ---------------------------------------------------------------- jaccard */
 /* J' of Eq. (1) from host-resident sums: the mean of r(p, q) over the

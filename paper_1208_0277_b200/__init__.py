@@ -35,8 +35,9 @@ CNT_PIXELS, CNT_ROWTESTS, CNT_BOXES, CNT_BOXEDGES, CNT_SPLITS, CNT_PIXBOXES, CNT
 SUMS_FIELDS = ("n_pairs", "n_nonzero", "sum_inter", "sum_union", "sum_area_p", "sum_area_q", "limb0", "limb1",
                "limb2", "limb3", "status")
 SYMBOLS = ("sccg_polyset_bytes", "sccg_polyset_bind", "sccg_prep", "sccg_filter_workspace_bytes",
-           "sccg_filter_pairs", "sccg_pixelbox_workspace_bytes", "sccg_pixelbox", "sccg_jaccard", "sccg_strerror",
-           "sccg_last_error_string", "sccg_last_error_index", "sccg_version")
+           "sccg_filter_pairs", "sccg_filter_pairs_async", "sccg_pixelbox_workspace_bytes", "sccg_pixelbox",
+           "sccg_pixelbox_async", "sccg_jaccard", "sccg_strerror", "sccg_last_error_string", "sccg_last_error_index",
+           "sccg_version")
 
 
 class SccgError(RuntimeError):
@@ -117,6 +118,10 @@ def load(build: bool = True):
         lib.sccg_filter_workspace_bytes.restype = sz
         lib.sccg_filter_pairs.argtypes = [ps, ps, vp, i64, ctypes.POINTER(i64), vp, sz, vp]
         lib.sccg_filter_pairs.restype = cint
+        lib.sccg_filter_pairs_async.argtypes = [ps, ps, vp, i64, vp, vp, sz, vp]
+        lib.sccg_filter_pairs_async.restype = cint
+        lib.sccg_pixelbox_async.argtypes = [ps, ps, vp, vp, i64, vp, vp, vp, ctypes.POINTER(Config), vp, sz, vp]
+        lib.sccg_pixelbox_async.restype = cint
         lib.sccg_pixelbox_workspace_bytes.argtypes = [i64]
         lib.sccg_pixelbox_workspace_bytes.restype = sz
         lib.sccg_pixelbox.argtypes = [ps, ps, vp, i64, vp, vp, vp, ctypes.POINTER(Config), vp, sz, vp]
@@ -230,6 +235,90 @@ def filter_pairs(P: DeviceSet, Q: DeviceSet, cap: int | None = None, stream=None
         _check(code, "sccg_filter_pairs")
         return out[: int(n.value)]
     raise SccgError(E_CAPACITY, "sccg_filter_pairs")
+
+
+class Pipeline:
+    """A device-resident, host-sync-free cross-comparison step for fixed sets:
+    prep(P), prep(Q), MBR join and PixelBox enqueued back to back on one stream
+    (sccg_filter_pairs_async / sccg_pixelbox_async: the pair count never leaves
+    the GPU), so the whole step can be captured and replayed as a CUDA graph.
+    ``run()`` returns the device sums vector; read it (one sync) for J'."""
+
+    def __init__(self, P: "DeviceSet", Q: "DeviceSet", cap: int | None = None, threshold: int = 0, graph: bool = True,
+                 validate: bool = True):
+        torch = _torch()
+        self.lib = load()
+        self.P, self.Q = P, Q
+        dev = P.xy.device
+        self.cap = int(cap) if cap is not None else 2 * max(P.n, Q.n) + 1024
+        self.pairs = torch.empty((max(self.cap, 1), 2), dtype=torch.int32, device=dev)
+        self.result = torch.zeros(2, dtype=torch.int64, device=dev)
+        self.sums = new_sums(dev)
+        self.fws_bytes = int(self.lib.sccg_filter_workspace_bytes(P.n, Q.n))
+        self.fws = torch.empty(self.fws_bytes, dtype=torch.uint8, device=dev)
+        self.pws_bytes = int(self.lib.sccg_pixelbox_workspace_bytes(self.cap))
+        self.pws = torch.empty(max(self.pws_bytes, 256), dtype=torch.uint8, device=dev)
+        self.cfg = Config(threshold, 0, 0, 0, None)
+        self.validate = 1 if validate else 0
+        self.graphs = None
+        if graph:
+            s = torch.cuda.Stream(device=dev)
+            s.wait_stream(torch.cuda.current_stream(dev))
+            with torch.cuda.stream(s):  # warm-up outside capture (one-time attribute setup)
+                self._enqueue_filter()
+                self._enqueue_pixelbox()
+            torch.cuda.current_stream(dev).wait_stream(s)
+            torch.cuda.synchronize(dev)
+            gf, gp = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gf):
+                self._enqueue_filter()
+            with torch.cuda.graph(gp):
+                self._enqueue_pixelbox()
+            self.graphs = (gf, gp)
+
+    def _enqueue_filter(self):
+        st = _stream_ptr()
+        lib = self.lib
+        self.sums.zero_()
+        _check(lib.sccg_prep(ctypes.byref(self.P.c), self.validate, st), "sccg_prep")
+        _check(lib.sccg_prep(ctypes.byref(self.Q.c), self.validate, st), "sccg_prep")
+        _check(lib.sccg_filter_pairs_async(ctypes.byref(self.P.c), ctypes.byref(self.Q.c), self.pairs.data_ptr(),
+                                           self.cap, self.result.data_ptr(), self.fws.data_ptr(), self.fws_bytes, st),
+               "sccg_filter_pairs_async")
+
+    def _enqueue_pixelbox(self):
+        _check(self.lib.sccg_pixelbox_async(ctypes.byref(self.P.c), ctypes.byref(self.Q.c), self.pairs.data_ptr(),
+                                            self.result.data_ptr(), self.cap, None, None, self.sums.data_ptr(),
+                                            ctypes.byref(self.cfg), self.pws.data_ptr(), self.pws_bytes, _stream_ptr()),
+               "sccg_pixelbox_async")
+
+    def run(self, pix_events=None):
+        """One step: prep x2 + join (graph 1), PixelBox (graph 2).  pix_events =
+        (start, end) CUDA events recorded around the PixelBox part."""
+        if self.graphs is not None:
+            self.graphs[0].replay()
+            if pix_events:
+                pix_events[0].record()
+            self.graphs[1].replay()
+            if pix_events:
+                pix_events[1].record()
+        else:
+            self._enqueue_filter()
+            if pix_events:
+                pix_events[0].record()
+            self._enqueue_pixelbox()
+            if pix_events:
+                pix_events[1].record()
+        return self.sums
+
+    def check(self):
+        """After a run: raise if the pair buffer overflowed or prep flagged input."""
+        n, status = (int(v) for v in self.result.tolist())
+        if n > self.cap:
+            raise SccgError(E_CAPACITY, f"Pipeline: {n} pairs > cap {self.cap}")
+        if status:
+            raise SccgError(E_ARG, f"Pipeline: prep status bits {status:#x}")
+        return n
 
 
 def new_sums(device=None):

@@ -29,9 +29,11 @@ size_t filter_ws_bytes(int64_t np, int64_t nq);
 int filter_pairs(const sccg_polyset* P, const sccg_polyset* Q, int32_t* pairs, int64_t cap, int64_t* n_pairs_host,
                  void* ws, size_t ws_bytes, cudaStream_t stream);
 size_t pixelbox_ws_bytes(int64_t n);
-int run_pixelbox(const sccg_polyset* p, const sccg_polyset* q, const int32_t* pairs, int64_t n, int64_t* inter,
-                 int64_t* uni, sccg_sums* sums, const sccg_config* cfg, void* ws, size_t ws_bytes,
-                 cudaStream_t stream);
+int filter_pairs_async(const sccg_polyset* P, const sccg_polyset* Q, int32_t* pairs, int64_t cap,
+                       int64_t* result_dev, void* ws, size_t ws_bytes, cudaStream_t stream);
+int run_pixelbox(const sccg_polyset* p, const sccg_polyset* q, const int32_t* pairs, int64_t n,
+                 const int64_t* dev_result, int64_t* inter, int64_t* uni, sccg_sums* sums, const sccg_config* cfg,
+                 void* ws, size_t ws_bytes, cudaStream_t stream);
 
 static bool aligned(const void* p, size_t a) { return (reinterpret_cast<uintptr_t>(p) & (a - 1)) == 0; }
 
@@ -150,12 +152,23 @@ int sccg_filter_pairs(const sccg_polyset* p, const sccg_polyset* q, int32_t* pai
   return filter_pairs(p, q, pairs, cap, n_pairs_host, workspace, ws_bytes, reinterpret_cast<cudaStream_t>(stream));
 }
 
+int sccg_filter_pairs_async(const sccg_polyset* p, const sccg_polyset* q, int32_t* pairs, int64_t cap,
+                            int64_t* result_dev, void* workspace, size_t ws_bytes, sccg_stream_t stream) {
+  set_error(SCCG_OK, "", -1);
+  if (int r = check_set(p, true, "p")) return r;
+  if (int r = check_set(q, true, "q")) return r;
+  if (!result_dev || !aligned(result_dev, 8)) return set_error(SCCG_E_ARG, "result_dev must be a non-null aligned device int64[2]");
+  if (cap < 0) return set_error(SCCG_E_ARG, "negative capacity");
+  if (pairs && !aligned(pairs, 8)) return set_error(SCCG_E_ARG, "pairs must be 8-byte aligned");
+  if (!workspace || !aligned(workspace, 256))
+    return set_error(SCCG_E_WORKSPACE, "workspace must be non-null and 256-byte aligned");
+  return filter_pairs_async(p, q, pairs, cap, result_dev, workspace, ws_bytes, reinterpret_cast<cudaStream_t>(stream));
+}
+
 size_t sccg_pixelbox_workspace_bytes(int64_t n_pairs) { return n_pairs < 0 ? 0 : pixelbox_ws_bytes(n_pairs); }
 
-int sccg_pixelbox(const sccg_polyset* p, const sccg_polyset* q, const int32_t* pairs, int64_t n_pairs, int64_t* inter,
-                  int64_t* uni, sccg_sums* sums, const sccg_config* cfg, void* workspace, size_t ws_bytes,
-                  sccg_stream_t stream) {
-  set_error(SCCG_OK, "", -1);
+static int pixelbox_checks(const sccg_polyset* p, const sccg_polyset* q, const int32_t* pairs, int64_t n_pairs,
+                           int64_t* inter, int64_t* uni, sccg_sums* sums, const sccg_config* cfg) {
   if (int r = check_set(p, true, "p")) return r;
   if (int r = check_set(q, true, "q")) return r;
   if (n_pairs < 0) return set_error(SCCG_E_ARG, "negative n_pairs");
@@ -168,7 +181,25 @@ int sccg_pixelbox(const sccg_polyset* p, const sccg_polyset* q, const int32_t* p
     if (cfg->block != 0 && cfg->block != 256) return set_error(SCCG_E_ARG, "config.block must be 0 or 256");
     if (cfg->grid < 0) return set_error(SCCG_E_ARG, "config.grid < 0");
   }
-  return run_pixelbox(p, q, pairs, n_pairs, inter, uni, sums, cfg, workspace, ws_bytes,
+  return SCCG_OK;
+}
+
+int sccg_pixelbox_async(const sccg_polyset* p, const sccg_polyset* q, const int32_t* pairs, const int64_t* result_dev,
+                        int64_t cap, int64_t* inter, int64_t* uni, sccg_sums* sums, const sccg_config* cfg,
+                        void* workspace, size_t ws_bytes, sccg_stream_t stream) {
+  set_error(SCCG_OK, "", -1);
+  if (!result_dev || !aligned(result_dev, 8)) return set_error(SCCG_E_ARG, "result_dev must be a non-null aligned device int64[2]");
+  if (int r = pixelbox_checks(p, q, pairs, cap, inter, uni, sums, cfg)) return r;
+  return run_pixelbox(p, q, pairs, cap, result_dev, inter, uni, sums, cfg, workspace, ws_bytes,
+                      reinterpret_cast<cudaStream_t>(stream));
+}
+
+int sccg_pixelbox(const sccg_polyset* p, const sccg_polyset* q, const int32_t* pairs, int64_t n_pairs, int64_t* inter,
+                  int64_t* uni, sccg_sums* sums, const sccg_config* cfg, void* workspace, size_t ws_bytes,
+                  sccg_stream_t stream) {
+  set_error(SCCG_OK, "", -1);
+  if (int r = pixelbox_checks(p, q, pairs, n_pairs, inter, uni, sums, cfg)) return r;
+  return run_pixelbox(p, q, pairs, n_pairs, nullptr, inter, uni, sums, cfg, workspace, ws_bytes,
                       reinterpret_cast<cudaStream_t>(stream));
 }
 

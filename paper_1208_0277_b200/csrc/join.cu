@@ -113,12 +113,12 @@ template <bool WRITE>
 __global__ void probe_kernel(const int4* __restrict__ mp, int64_t np, const int4* __restrict__ mq,
                              const Grid* __restrict__ gp, const int* __restrict__ cell_start,
                              const int* __restrict__ items, long long* __restrict__ count,
-                             const long long* __restrict__ start, int2* __restrict__ pairs) {
+                             const long long* __restrict__ start, int2* __restrict__ pairs, long long cap) {
   const Grid g = *gp;
   for (int64_t p = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; p < np; p += int64_t(gridDim.x) * blockDim.x) {
     const int4 a = mp[p];
     long long n = 0;
-    if (!g.empty && !mbr_empty(a)) {
+    if (!g.empty && !mbr_empty(a) && (!WRITE || start[p + 1] <= cap)) {
       const long long base = WRITE ? start[p] : 0;
       for (int cy = a.y >> g.k; cy <= (a.w - 1) >> g.k; cy++)
         for (int cx = a.x >> g.k; cx <= (a.z - 1) >> g.k; cx++) {
@@ -193,17 +193,12 @@ static int blocks_for(int64_t n, int threads) {
   return (int)(b < 1 ? 1 : b);
 }
 
-int filter_pairs(const sccg_polyset* P, const sccg_polyset* Q, int32_t* pairs, int64_t cap, int64_t* n_pairs_host,
-                 void* ws, size_t ws_bytes, cudaStream_t stream) {
+// Enqueue everything up to the per-P pair offsets (grid, buckets, counts, scan).
+static int filter_enqueue(const sccg_polyset* P, const sccg_polyset* Q, FilterWs& w, cudaStream_t stream) {
   const int64_t np = P->n_polygons, nq = Q->n_polygons;
-  Carve cv{reinterpret_cast<char*>(ws), ws_bytes};
-  FilterWs w;
-  filter_layout(np, nq, cv, w);
-  if (!cv.ok) return set_error(SCCG_E_WORKSPACE, "filter workspace too small (see sccg_filter_workspace_bytes)");
   const int4* mp = reinterpret_cast<const int4*>(P->mbr);
   const int4* mq = reinterpret_cast<const int4*>(Q->mbr);
   const int64_t C = cell_cap(np, nq);
-
   // 1. grid size from the prep statistics (device side), bucket Q
   grid_select_kernel<<<1, 32, 0, stream>>>(reinterpret_cast<const SetStats*>(P->stats),
                                            reinterpret_cast<const SetStats*>(Q->stats), C, entry_cap(nq), w.grid);
@@ -212,13 +207,33 @@ int filter_pairs(const sccg_polyset* P, const sccg_polyset* Q, int32_t* pairs, i
   cub::DeviceScan::ExclusiveSum(w.tmp, w.tmp_bytes, w.cell_count, w.cell_start, (int)(C + 1), stream);
   if (nq > 0)
     grid_fill_kernel<<<blocks_for(nq, 256), 256, 0, stream>>>(mq, nq, w.grid, w.cell_start, w.cell_count, w.items);
-  // 2. probe: count, scan, total
+  // 2. probe: count, scan
   if (np > 0)
     probe_kernel<false><<<blocks_for(np, 128), 128, 0, stream>>>(mp, np, mq, w.grid, w.cell_start, w.items, w.pcount,
-                                                                  nullptr, nullptr);
+                                                                  nullptr, nullptr, 0);
   cudaMemsetAsync(w.pcount + np, 0, sizeof(long long), stream);
   cub::DeviceScan::ExclusiveSum(w.tmp, w.tmp_bytes, w.pcount, w.pstart, (int)(np + 1), stream);
-  // 3. the one host synchronisation: pair count and both sets' prep status
+  return check_cuda(cudaGetLastError(), "filter enqueue");
+}
+
+static void probe_write(const sccg_polyset* P, const sccg_polyset* Q, FilterWs& w, int32_t* pairs, int64_t cap,
+                        cudaStream_t stream) {
+  const int64_t np = P->n_polygons;
+  if (np > 0 && pairs && cap > 0)
+    probe_kernel<true><<<blocks_for(np, 128), 128, 0, stream>>>(
+        reinterpret_cast<const int4*>(P->mbr), np, reinterpret_cast<const int4*>(Q->mbr), w.grid, w.cell_start,
+        w.items, nullptr, w.pstart, reinterpret_cast<int2*>(pairs), cap);
+}
+
+int filter_pairs(const sccg_polyset* P, const sccg_polyset* Q, int32_t* pairs, int64_t cap, int64_t* n_pairs_host,
+                 void* ws, size_t ws_bytes, cudaStream_t stream) {
+  const int64_t np = P->n_polygons, nq = Q->n_polygons;
+  Carve cv{reinterpret_cast<char*>(ws), ws_bytes};
+  FilterWs w;
+  filter_layout(np, nq, cv, w);
+  if (!cv.ok) return set_error(SCCG_E_WORKSPACE, "filter workspace too small (see sccg_filter_workspace_bytes)");
+  if (int r = filter_enqueue(P, Q, w, stream)) return r;
+  // the one host synchronisation: pair count and both sets' prep status
   long long total = 0;
   uint32_t sp[2] = {0, 0}, sq[2] = {0, 0};
   if (int r = check_cuda(cudaMemcpyAsync(&total, w.pstart + np, sizeof(long long), cudaMemcpyDeviceToHost, stream),
@@ -239,11 +254,31 @@ int filter_pairs(const sccg_polyset* P, const sccg_polyset* Q, int32_t* pairs, i
   }
   *n_pairs_host = total;
   if (pairs == nullptr || cap < total) return set_error(SCCG_E_CAPACITY, "pair buffer too small", total);
-  // 4. write, segment-sorted by q
-  if (total > 0)
-    probe_kernel<true><<<blocks_for(np, 128), 128, 0, stream>>>(mp, np, mq, w.grid, w.cell_start, w.items, nullptr,
-                                                                 w.pstart, reinterpret_cast<int2*>(pairs));
+  // write, segment-sorted by q
+  if (total > 0) probe_write(P, Q, w, pairs, cap, stream);
   return check_cuda(cudaGetLastError(), "probe write");
+}
+
+__global__ void filter_result_kernel(const long long* __restrict__ total, const uint32_t* __restrict__ sp,
+                                     const uint32_t* __restrict__ sq, long long* result) {
+  if (threadIdx.x == 0) {
+    result[0] = *total;
+    result[1] = (long long)(sp[0] | sq[0]);
+  }
+}
+
+int filter_pairs_async(const sccg_polyset* P, const sccg_polyset* Q, int32_t* pairs, int64_t cap,
+                       int64_t* result_dev, void* ws, size_t ws_bytes, cudaStream_t stream) {
+  const int64_t np = P->n_polygons, nq = Q->n_polygons;
+  Carve cv{reinterpret_cast<char*>(ws), ws_bytes};
+  FilterWs w;
+  filter_layout(np, nq, cv, w);
+  if (!cv.ok) return set_error(SCCG_E_WORKSPACE, "filter workspace too small (see sccg_filter_workspace_bytes)");
+  if (int r = filter_enqueue(P, Q, w, stream)) return r;
+  probe_write(P, Q, w, pairs, cap, stream);
+  filter_result_kernel<<<1, 32, 0, stream>>>(w.pstart + np, P->status, Q->status,
+                                             reinterpret_cast<long long*>(result_dev));
+  return check_cuda(cudaGetLastError(), "filter async");
 }
 
 }  // namespace sccg

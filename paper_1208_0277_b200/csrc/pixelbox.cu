@@ -465,10 +465,15 @@ __device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long v)
 #endif
 template <bool COUNT>
 __global__ void __launch_bounds__(kSmallWarps * 32, SCCG_SMALL_MINB)
-    small_kernel(DevSet Ps, DevSet Qs, const int2* __restrict__ pairs, long long n, long long* __restrict__ inter,
+    small_kernel(DevSet Ps, DevSet Qs, const int2* __restrict__ pairs, long long n_cap,
+                 const long long* __restrict__ dev_result, long long* __restrict__ inter,
                  long long* __restrict__ uni, sccg_sums* sums, int T, int mode, unsigned long long* queue,
                  long long* __restrict__ large_list, unsigned* large_count, long long* counters, long long np_,
                  long long nq_) {
+  // pair count: host-given, or (async path) the filter's device-side count clamped to the buffer
+  const long long n = dev_result ? min(dev_result[0], n_cap) : n_cap;
+  if (dev_result && blockIdx.x == 0 && threadIdx.x == 0 && dev_result[1])
+    atomicOr(reinterpret_cast<unsigned long long*>(&sums->status), (unsigned long long)dev_result[1]);
   __shared__ __align__(16) int2 s_buf[kSmallWarps][2 * kSmallQOff];
   __shared__ int4 s_meta[kSmallWarps][32];
   __shared__ int2 s_ep[kSmallWarps][32];
@@ -670,9 +675,9 @@ static cudaError_t prepare_kernels() {
   return once;
 }
 
-int run_pixelbox(const sccg_polyset* p, const sccg_polyset* q, const int32_t* pairs, int64_t n, int64_t* inter,
-                 int64_t* uni, sccg_sums* sums, const sccg_config* cfg, void* ws, size_t ws_bytes,
-                 cudaStream_t stream) {
+int run_pixelbox(const sccg_polyset* p, const sccg_polyset* q, const int32_t* pairs, int64_t n,
+                 const int64_t* dev_result, int64_t* inter, int64_t* uni, sccg_sums* sums, const sccg_config* cfg,
+                 void* ws, size_t ws_bytes, cudaStream_t stream) {
   Carve cv{reinterpret_cast<char*>(ws), ws_bytes};
   PixelboxWs w;
   pixelbox_layout(n, cv, w);
@@ -686,21 +691,21 @@ int run_pixelbox(const sccg_polyset* p, const sccg_polyset* q, const int32_t* pa
   const bool count = cfg && cfg->counters;
   long long* counters = count ? reinterpret_cast<long long*>(cfg->counters) : nullptr;
   if (int r = check_cuda(prepare_kernels(), "pixelbox smem attribute")) return r;
-  int dev = 0, sms = 148, per_sm_s = 1, per_sm_l = 1;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  if (count) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_s, small_kernel<true>, kSmallWarps * 32, 0);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_l, large_kernel<true>, kWarps * 32, kDynSmem);
-  } else {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_s, small_kernel<false>, kSmallWarps * 32, 0);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_l, large_kernel<false>, kWarps * 32, kDynSmem);
+  static int sms = 0, per_sm_s[2] = {0, 0}, per_sm_l[2] = {0, 0};
+  if (sms == 0) {  // launch geometry, queried once
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_s[1], small_kernel<true>, kSmallWarps * 32, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_l[1], large_kernel<true>, kWarps * 32, kDynSmem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_s[0], small_kernel<false>, kSmallWarps * 32, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_l[0], large_kernel<false>, kWarps * 32, kDynSmem);
   }
-  int64_t grid_s = cfg && cfg->grid > 0 ? cfg->grid : (int64_t)sms * (per_sm_s > 0 ? per_sm_s : 1);
+  int64_t grid_s = cfg && cfg->grid > 0 ? cfg->grid : (int64_t)sms * max(per_sm_s[count], 1);
   const int64_t need = (n + kSmallWarps * 32 - 1) / (kSmallWarps * 32);
   if (grid_s > need) grid_s = need;
   if (grid_s < 1) grid_s = 1;
-  int64_t grid_l = cfg && cfg->grid > 0 ? cfg->grid : (int64_t)sms * (per_sm_l > 0 ? per_sm_l : 1);
+  int64_t grid_l = cfg && cfg->grid > 0 ? cfg->grid : (int64_t)sms * max(per_sm_l[count], 1);
   const int64_t need_l = (n + kWarps - 1) / kWarps;
   if (grid_l > need_l) grid_l = need_l;
   if (grid_l < 1) grid_l = 1;
@@ -708,15 +713,16 @@ int run_pixelbox(const sccg_polyset* p, const sccg_polyset* q, const int32_t* pa
   const int2* pr = reinterpret_cast<const int2*>(pairs);
   long long* in = reinterpret_cast<long long*>(inter);
   long long* un = reinterpret_cast<long long*>(uni);
+  const long long* dr = reinterpret_cast<const long long*>(dev_result);
   if (count) {
     small_kernel<true><<<(unsigned)grid_s, kSmallWarps * 32, 0, stream>>>(
-        Ps, Qs, pr, n, in, un, sums, T, mode, w.queue, w.large_list, w.large_count, counters, p->n_polygons,
+        Ps, Qs, pr, n, dr, in, un, sums, T, mode, w.queue, w.large_list, w.large_count, counters, p->n_polygons,
         q->n_polygons);
     large_kernel<true><<<(unsigned)grid_l, kWarps * 32, kDynSmem, stream>>>(Ps, Qs, pr, w.large_list, w.large_count,
                                                                           in, un, sums, T, mode, w.queue + 1, counters);
   } else {
     small_kernel<false><<<(unsigned)grid_s, kSmallWarps * 32, 0, stream>>>(
-        Ps, Qs, pr, n, in, un, sums, T, mode, w.queue, w.large_list, w.large_count, nullptr, p->n_polygons,
+        Ps, Qs, pr, n, dr, in, un, sums, T, mode, w.queue, w.large_list, w.large_count, nullptr, p->n_polygons,
         q->n_polygons);
     large_kernel<false><<<(unsigned)grid_l, kWarps * 32, kDynSmem, stream>>>(Ps, Qs, pr, w.large_list, w.large_count,
                                                                            in, un, sums, T, mode, w.queue + 1, nullptr);

@@ -221,6 +221,27 @@ def test_sums_accumulate_and_launch_shape_invariance(sccg, tile_sets):
     assert torch.equal(sums, ref[2])
 
 
+def test_async_pipeline_matches_sync(sccg, tile_sets):
+    """sccg_filter_pairs_async + sccg_pixelbox_async (device-side pair count),
+    eager and captured as CUDA graphs, equal the synchronous path bit for bit."""
+    A, B = tile_sets
+    P, Q = dev(A, sccg), dev(B, sccg)
+    pairs = sccg.filter_pairs(P, Q)
+    ref = sccg.pixelbox(P, Q, pairs)[2]
+    for graph in (False, True):
+        pipe = sccg.Pipeline(P, Q, graph=graph)
+        for _ in range(3):
+            s = pipe.run()
+        assert torch.equal(s, ref)
+        assert pipe.check() == pairs.shape[0]
+        assert torch.equal(pipe.pairs[: pairs.shape[0]], pairs)
+    tiny = sccg.Pipeline(P, Q, cap=10, graph=False)
+    tiny.run()
+    with pytest.raises(sccg.SccgError) as e:
+        tiny.check()
+    assert e.value.code == sccg.E_CAPACITY
+
+
 def test_abi_errors(sccg):
     bad = synth.pack([[[0, 0], [3, 1], [3, 3], [0, 3]]])  # diagonal edge
     good = synth.pack([[[0, 0], [3, 0], [3, 3], [0, 3]]])
@@ -269,3 +290,9 @@ def test_slide_full_size(sccg):
     # determinism across thresholds: per-pair results identical
     i2, u2, s2 = sccg.pixelbox(P, Q, pairs, threshold=64)
     assert torch.equal(i2, inter) and torch.equal(s2, sums)
+    # the bench's launch configuration (device-resident pipeline, CUDA graphs)
+    pipe = sccg.Pipeline(P, Q, cap=3 * max(P.n, Q.n) + 1024, graph=True)
+    for _ in range(2):
+        ps = pipe.run()
+    assert pipe.check() == len(pn)
+    assert torch.equal(ps, sums)
