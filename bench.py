@@ -202,7 +202,7 @@ def run_ours(args, rank, world, local_rank):
     # ---- e2e: public API from pinned host buffers, H2D + D2H inside the timed region
     e2e_steps = max(1, min(args.e2e_steps, args.steps))
     h2d = xy_p.numel() * 4 + off_p.numel() * 8 + xy_q.numel() * 4 + off_q.numel() * 8
-    d2h = sums.numel() * 8
+    d2h = len(sccg.SUMS_FIELDS) * 8
 
     def e2e_step():
         a = xy_p.to(dev, non_blocking=True)
