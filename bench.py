@@ -43,8 +43,8 @@ OPS_PER_BOXEDGE = 8  # one lane classifying one edge against all sub-boxes of a 
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
-    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=300)
+    ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="slide", choices=["slide", "tile", "skewed"])
     ap.add_argument("--threshold", type=int, default=0)
@@ -130,6 +130,7 @@ def run_ours(args, rank, world, local_rank):
     import torch.distributed as dist
 
     import paper_1208_0277_b200 as sccg
+    from paper_1208_0277_b200 import dist as sdist
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
@@ -153,8 +154,7 @@ def run_ours(args, rank, world, local_rank):
 
     def step(timing_pixelbox=False):
         sums = pipe.run((pix_start, pix_end) if timing_pixelbox else None)
-        if world > 1:
-            dist.all_reduce(sums, op=dist.ReduceOp.SUM)
+        sdist.allreduce_sums(sums)  # row a9: the only collective (NCCL, int64 SUM)
         return sccg.sums_to_host(sums.cpu())  # the step's one host synchronisation
 
     for _ in range(max(args.warmup, 3)):

@@ -1,0 +1,101 @@
+"""Multi-process host logic of the sharded path (``-m "not gpu"``): gloo,
+world size 2, on CPU.  Each rank computes its images' integer sums (the
+``sccg_sums`` layout; here from the oracle, since there is no GPU), the sums are
+all-reduced, and J' from the reduced integers (through the library's
+``sccg_jaccard``) must equal the single-process value over all images,
+bit for bit, for any sharding."""
+import os
+import socket
+from fractions import Fraction
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_1208_0277_b200 import dist as sdist
+
+
+def test_lpt_shards_cover_each_item_once():
+    rng = np.random.default_rng(0)
+    for world in (1, 2, 3, 8):
+        costs = rng.integers(1, 100, 100).tolist()
+        shards = sdist.lpt_shards(costs, world)
+        flat = sorted(i for s in shards for i in s)
+        assert flat == list(range(100))
+        loads = [sum(costs[i] for i in s) for s in shards]
+        assert max(loads) - min(loads) <= max(costs)  # LPT bound
+        assert shards == sdist.lpt_shards(costs, world)  # deterministic
+    assert sdist.shard_for_rank(5, 2, 0) + sdist.shard_for_rank(5, 2, 1) != []
+    with pytest.raises(ValueError):
+        sdist.shard_for_rank(5, 2, 2)
+
+
+def image_sums(image):
+    """Integer sums of one synthetic image (C1 tile, seed per image) from the oracle."""
+    import oracle
+    import synth
+
+    A, B = synth.generate("tile", image=image)
+    A, B = A.subset(range(0, A.n, 5)), B.subset(range(0, B.n, 5))
+    pairs = oracle.join(A, B)
+    inter, uni = oracle.pair_areas(A, B, pairs, threads=1)
+    s = oracle.sums(A, B, pairs, inter, uni)
+    units = sum(int(Fraction(int(i) / int(u)) * (1 << 116)) for i, u in zip(inter, uni) if i)
+    limbs = [(units >> (30 * k)) & ((1 << 30) - 1) for k in range(3)] + [units >> 90]
+    vec = [s["n_pairs"], s["n_nonzero"], s["sum_inter"], s["sum_union"], s["sum_area_p"], s["sum_area_q"]] + limbs + [0]
+    return vec, list(zip(inter.tolist(), uni.tolist()))
+
+
+def _worker(rank, world, port, images, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    mine = sdist.shard_for_rank(len(images), world, rank, costs=[1 + (i % 3) for i in range(len(images))])
+    total = torch.zeros(11, dtype=torch.int64)
+    for i in mine:
+        v, _ = image_sums(images[i])
+        total += torch.tensor(v, dtype=torch.int64)
+    sdist.allreduce_sums(total)
+    out[rank] = total.tolist()
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+@pytest.mark.timeout(300)
+def test_gloo_two_ranks_allreduce_is_exact():
+    import oracle
+    import paper_1208_0277_b200 as sccg
+
+    images = [0, 1, 2, 3, 4]
+    ctx = mp.get_context("spawn")
+    mgr = ctx.Manager()
+    out = mgr.dict()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, images, out)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(240)
+        assert p.exitcode == 0
+    assert out[0] == out[1]
+    # single-process reference over all images
+    ref = [0] * 11
+    allpairs = []
+    for img in images:
+        v, iu = image_sums(img)
+        ref = [a + b for a, b in zip(ref, v)]
+        allpairs += iu
+    assert out[0] == ref
+    j, _ = sccg.jaccard(out[0])
+    ex = oracle.jaccard_exact([i for i, _ in allpairs], [u for _, u in allpairs])
+    assert abs(j - float(ex)) <= 1e-12 * float(ex)
