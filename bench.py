@@ -46,7 +46,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=300)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="slide", choices=["slide", "tile", "skewed"])
+    ap.add_argument("--config", default="slide", choices=["slide", "tile", "skewed", "combs"])
     ap.add_argument("--threshold", type=int, default=0)
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -120,6 +120,7 @@ def config_desc(config):
         "slide": "configs[1]: one 100k x 100k whole-slide image, two synthetic result sets of ~500k nucleus polygons",
         "tile": "configs[0]: one 4096x4096 tile, ~1,000 nucleus polygons per set",
         "skewed": "configs[2]: 4x4 tiles, nuclei + 16 glands per tile (MBR side up to 512)",
+        "combs": "configs[4] analog: 16,384 independent highly concave comb pairs, 500-2000 vertices",
     }[config]
 
 
