@@ -1,0 +1,586 @@
+// large.cu -- PixelBox for large pairs:
+// region work items with local edge culling.
+//
+// Every pair the small kernel cannot take (root box wider or taller than 32,
+// |box| >= T, or rings with more than 64 vertical edges) lands here.
+//  1. expand_kernel: the pair's root box MBR(p) n MBR(q) (reading R5) is cut
+//     into up to 32 x 32 disjoint regions of about 128 x 128 pixels -- the
+//     "huge-pair split into region work items" of SURVEY §8 a3 -- so one large
+//     pair is spread over many warps (the paper gives a whole pair to one
+//     block, which leaves a few big pairs on a few SMs).
+//  2. item_kernel: a warp takes one item (pair, region R) from a global queue:
+//     - it culls both polygons' edges to those meeting R (vertical edges with
+//       x strictly inside R's columns, horizontal edges strictly inside R's
+//       rows -- all other edges cannot reach R's open interior) into shared
+//       memory, and casts one ray for R's corner pixel;
+//     - it then runs Algorithm 1 on R with a warp-private DFS stack
+//       of sampling boxes.  Lemma 1 (reading R6-A) classifies the <= 32 aligned
+//       sub-boxes of a split edge-parallel (a lane owns an edge, the warp
+//       OR/XOR-reduces 32-bit sub-box masks); a sub-box corner's parity is its
+//       parent corner's parity plus the crossings along the parent's left
+//       column and the sub-box's bottom row, so only local edges are touched;
+//     - boxes below T are pixelized bit-parallel (a lane owns a 32-pixel row
+//       word: row parity at the box's left column, then one suffix mask per
+//       local vertical edge);
+//     - the item's pixel count is added into the pair's int64 accumulator.
+//     An item whose local lists overflow shared memory is split in two and
+//     retried (in the same warp), so any input is handled.
+//  3. large_epilogue_kernel: per pair, U = |p| + |q| - I, the
+//     outputs, and the exact batch totals (reading R12).
+// Regions are disjoint and cover the root box exactly, so the per-pair sums are
+// exact and independent of the split (integer atomics are order-free).
+#include "pixelbox_common.cuh"
+
+namespace sccg {
+
+constexpr int kLWarps = 4;          // warps per CTA
+constexpr int kLCap = 192;          // local records per list (vertical / horizontal) per polygon per warp
+constexpr int kLStage = 96;         // staged records per polygon for one pixelized box
+constexpr int kLStack = 256;        // sampling boxes per warp stack
+constexpr int kLItems = 48;         // in-warp item stack (overflow splits)
+constexpr int kRegion = 128;        // target region side
+constexpr int kMaxSplit = 32;       // regions per axis at most
+constexpr int kMaxRegion = 32766;   // local coordinates are 15-bit (plus clamp margin)
+
+struct PolyRef {
+  const uint64_t* ev;  // vertical records (relative to the polygon MBR origin)
+  const int2* v;       // raw ring (horizontal edges)
+  int nv, V;
+  int dx, dy;          // polygon MBR origin - root-box origin
+  int ox, oy;          // root-box origin (absolute)
+};
+
+// packed local records (relative to the item region origin, clamped so all
+// comparisons against boxes inside the region are preserved):
+//   vertical:   x (15 bit, 0 < x < Wr), ylo, yhi (int16, in [-1, Hr + 1])
+//   horizontal: y (15 bit, 0 < y < Hr), xlo, xhi (int16, in [-1, Wr + 1])
+__device__ __forceinline__ uint64_t pack_loc(int a, int lo, int hi) {
+  return (uint64_t)(uint32_t)(a & 0xffff) | ((uint64_t)(uint32_t)(lo & 0xffff) << 16) |
+         ((uint64_t)(uint32_t)(hi & 0xffff) << 32);
+}
+__device__ __forceinline__ void unpack_loc(uint64_t r, int& a, int& lo, int& hi) {
+  a = (int)(r & 0xffff);
+  lo = (int)(short)((r >> 16) & 0xffff);
+  hi = (int)(short)((r >> 32) & 0xffff);
+}
+
+struct LocalPoly {
+  uint64_t* V;  // [kLCap]
+  uint64_t* H;  // [kLCap]
+  int nV, nH;
+  int pi;       // parity of the region's corner pixel (1 = inside)
+};
+
+// Cull one polygon's edges to region R = [X0, X1) x [Y0, Y1) (root coords)
+// and cast the corner ray.  Returns false if a list overflows.
+__device__ bool build_local(const PolyRef& c, int X0, int Y0, int X1, int Y1, LocalPoly& L) {
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = lanemask_lt();
+  const int Wr = X1 - X0, Hr = Y1 - Y0;
+  int par = 0, cnt = 0;
+  for (int j0 = 0; j0 < c.nv; j0 += 32) {
+    const int j = j0 + lane;
+    bool keep = false;
+    uint64_t rec = 0;
+    if (j < c.nv) {
+      int cc, lo, hi;
+      unpack_edge(__ldg(c.ev + j), cc, lo, hi);
+      const int x = cc + c.dx, yl = lo + c.dy, yh = hi + c.dy;
+      par ^= (x > X0 && yl <= Y0 && Y0 < yh) ? 1 : 0;  // ray from (X0 + 1/2, Y0 + 1/2) toward +x
+      keep = x > X0 && x < X1 && yl < Y1 && yh > Y0;
+      rec = pack_loc(x - X0, max(yl - Y0, -1), min(yh - Y0, Hr + 1));
+    }
+    const unsigned b = __ballot_sync(FULL, keep);
+    const int pos = cnt + __popc(b & lt);
+    if (keep && pos < kLCap) L.V[pos] = rec;
+    cnt += __popc(b);
+  }
+  L.nV = cnt;
+  L.pi = __reduce_xor_sync(FULL, (unsigned)par) & 1;
+  cnt = 0;
+  for (int j0 = 0; j0 < c.V; j0 += 32) {
+    const int j = j0 + lane;
+    bool keep = false;
+    uint64_t rec = 0;
+    if (j < c.V) {
+      const int2 a = __ldg(c.v + j), b2 = __ldg(c.v + (j + 1 == c.V ? 0 : j + 1));
+      if (a.y == b2.y && a.x != b2.x) {
+        const int f = a.y - c.oy, xl = min(a.x, b2.x) - c.ox, xh = max(a.x, b2.x) - c.ox;
+        keep = f > Y0 && f < Y1 && xl < X1 && xh > X0;
+        rec = pack_loc(f - Y0, max(xl - X0, -1), min(xh - X0, Wr + 1));
+      }
+    }
+    const unsigned b = __ballot_sync(FULL, keep);
+    const int pos = cnt + __popc(b & lt);
+    if (keep && pos < kLCap) L.H[pos] = rec;
+    cnt += __popc(b);
+  }
+  L.nH = cnt;
+  return L.nV <= kLCap && L.nH <= kLCap;
+}
+
+// Lemma 1 (reading R6-A) for the sub-boxes of box B = [x0, x1) x [y0, y1)
+// (region coords), edge-parallel over the local lists.  pi = parity of B's
+// corner pixel (x0, y0).  hov: sub-boxes whose open interior meets an edge;
+// par: parity of each sub-box's corner pixel = pi + crossings up B's left
+// column (horizontal edges) + crossings along the sub-box's bottom row
+// (vertical edges) -- all local.
+__device__ __forceinline__ void classify_local(const LocalPoly& L, int x0, int y0, int Wb, int Hb, const Split& g,
+                                               int pi, unsigned& hov, unsigned& par) {
+  const int lane = threadIdx.x & 31;
+  const int sx = 1 << g.lsx, sy = 1 << g.lsy;
+  const unsigned kxmask = low_bits(g.kx);
+  unsigned h = 0, p = 0;
+  for (int j = lane; j < L.nV; j += 32) {
+    int x, yl, yh;
+    unpack_loc(L.V[j], x, yl, yh);
+    x -= x0;
+    yl -= y0;
+    yh -= y0;
+    if (yl < Hb && yh > 0) {
+      const int r_hi = min(g.nrows - 1, (yh - 1) >> g.lsy);
+      if (x > 0 && x < Wb && (x & (sx - 1)) != 0)  // edge inside a column's open x-range
+        h |= (g.colpat << (x >> g.lsx)) & row_range(max(0, yl >> g.lsy), r_hi, g);
+      if (x > 0) {  // crossed by the bottom row of sub-boxes (c, r) with c*sx >= x, yl <= r*sy < yh
+        const int c_lo = (x + sx - 1) >> g.lsx;
+        if (c_lo < g.ncols)
+          p ^= ((kxmask & ~low_bits(c_lo)) * g.colpat) & row_range(max(0, (yl + sy - 1) >> g.lsy), r_hi, g);
+      }
+    }
+  }
+  for (int j = lane; j < L.nH; j += 32) {
+    int y, xl, xh;
+    unpack_loc(L.H[j], y, xl, xh);
+    y -= y0;
+    xl -= x0;
+    xh -= x0;
+    if (y > 0 && y < Hb && (y & (sy - 1)) != 0 && xl < Wb && xh > 0) {
+      const int c_lo = max(0, xl >> g.lsx), c_hi = min(g.ncols - 1, (xh - 1) >> g.lsx);
+      h |= low_bits(c_hi - c_lo + 1) << (((y >> g.lsy) << g.lkx) + c_lo);
+    }
+    if (xl <= 0 && xh > 0 && y > 0) {  // crosses B's left column above its corner: rows r with r*sy >= y
+      const int r_lo = (y + sy - 1) >> g.lsy;
+      if (r_lo < g.nrows) p ^= row_range(r_lo, g.nrows - 1, g);
+    }
+  }
+  hov = __reduce_or_sync(FULL, h);
+  par = __reduce_xor_sync(FULL, p) ^ (pi ? FULL : 0u);
+}
+
+// Pixelization of box B (region coords) for one polygon into staged buffers:
+// vertical edges strictly inside B's columns crossing B's rows as
+// {ylo, span, x, 0} (box-relative), horizontal edges crossing B's left column
+// strictly inside B's rows as their row.  Returns counts (> kLStage: use the
+// local lists directly).
+__device__ __forceinline__ void stage_local(const LocalPoly& L, int x0, int y0, int x1, int y1, int4* sv, int* sh,
+                                            int& nv, int& nh) {
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = lanemask_lt();
+  int cnt = 0;
+  for (int j0 = 0; j0 < L.nV; j0 += 32) {
+    const int j = j0 + lane;
+    bool keep = false;
+    int x = 0, yl = 0, yh = 0;
+    if (j < L.nV) {
+      unpack_loc(L.V[j], x, yl, yh);
+      keep = x > x0 && x < x1 && yl < y1 && yh > y0;
+    }
+    const unsigned b = __ballot_sync(FULL, keep);
+    const int pos = cnt + __popc(b & lt);
+    if (keep && pos < kLStage) sv[pos] = make_int4(yl - y0, yh - yl, x - x0, 0);
+    cnt += __popc(b);
+  }
+  nv = cnt;
+  cnt = 0;
+  for (int j0 = 0; j0 < L.nH; j0 += 32) {
+    const int j = j0 + lane;
+    bool keep = false;
+    int y = 0, xl = 0, xh = 0;
+    if (j < L.nH) {
+      unpack_loc(L.H[j], y, xl, xh);
+      keep = xl <= x0 && xh > x0 && y > y0 && y < y1;
+    }
+    const unsigned b = __ballot_sync(FULL, keep);
+    const int pos = cnt + __popc(b & lt);
+    if (keep && pos < kLStage) sh[pos] = y - y0;
+    cnt += __popc(b);
+  }
+  nh = cnt;
+}
+
+// Row word (row, columns xs .. xs+31 of box B) of one polygon: parity of the
+// row's left-column pixel (pi + horizontal crossings), then one suffix mask
+// per vertical edge inside B crossing the row (reading R19).
+__device__ __forceinline__ unsigned row_word_local(const LocalPoly& L, const int4* sv, const int* sh, int nv, int nh,
+                                                   int x0, int y0, int x1, int y1, int pi, int row, int xs) {
+  int par = pi;
+  unsigned m = 0;
+  if (nh <= kLStage) {
+    for (int t = 0; t < nh; t++) par ^= (sh[t] <= row) ? 1 : 0;
+  } else {
+    for (int t = 0; t < L.nH; t++) {
+      int y, xl, xh;
+      unpack_loc(L.H[t], y, xl, xh);
+      par ^= (xl <= x0 && xh > x0 && y > y0 && y < y1 && y - y0 <= row) ? 1 : 0;
+    }
+  }
+  if (nv <= kLStage) {
+#pragma unroll 4
+    for (int t = 0; t < nv; t++) {
+      const int4 r = sv[t];
+      if ((unsigned)(row - r.x) < (unsigned)r.y) m ^= suffix_mask(r.z - xs);
+    }
+  } else {
+    for (int t = 0; t < L.nV; t++) {
+      int x, yl, yh;
+      unpack_loc(L.V[t], x, yl, yh);
+      if (x > x0 && x < x1 && (unsigned)(row + y0 - yl) < (unsigned)(yh - yl)) m ^= suffix_mask(x - x0 - xs);
+    }
+  }
+  return m ^ (par ? FULL : 0u);
+}
+
+template <bool COUNT>
+__device__ long long pixelize_local(const LocalPoly& P, const LocalPoly& Q, int x0, int y0, int x1, int y1, int pip,
+                                    int piq, int4* sv, int* sh, long long* counters) {
+  const int lane = threadIdx.x & 31;
+  int nvp, nhp, nvq, nhq;
+  stage_local(P, x0, y0, x1, y1, sv, sh, nvp, nhp);
+  stage_local(Q, x0, y0, x1, y1, sv + kLStage, sh + kLStage, nvq, nhq);
+  __syncwarp();
+  const int Wb = x1 - x0, Hb = y1 - y0, nw = (Wb + 31) >> 5, nseg = Hb * nw;
+  long long acc = 0;
+  for (int s0 = 0; s0 < nseg; s0 += 32) {
+    const int s = s0 + lane;
+    if (s < nseg) {
+      const int row = s / nw, xs = (s - row * nw) << 5;
+      const unsigned mp = row_word_local(P, sv, sh, nvp, nhp, x0, y0, x1, y1, pip, row, xs);
+      const unsigned mq = row_word_local(Q, sv + kLStage, sh + kLStage, nvq, nhq, x0, y0, x1, y1, piq, row, xs);
+      acc += __popc(mp & mq & low_bits(Wb - xs));
+    }
+  }
+  __syncwarp();
+  if (COUNT && lane == 0) {
+    atomicAdd((unsigned long long*)&counters[SCCG_CNT_PIXELS], (unsigned long long)Wb * Hb);
+    atomicAdd((unsigned long long*)&counters[SCCG_CNT_ROWTESTS], (unsigned long long)nseg * (nvp + nvq + nhp + nhq));
+    atomicAdd((unsigned long long*)&counters[SCCG_CNT_PIXBOXES], 1ull);
+  }
+  return acc;
+}
+
+// sampling-box stack entry: x0, y0, x1, y1 (15 bit each, region coords), parity bits of both polygons
+__device__ __forceinline__ uint64_t pack_sb(int x0, int y0, int x1, int y1, int pp, int pq) {
+  return (uint64_t)x0 | ((uint64_t)y0 << 15) | ((uint64_t)x1 << 30) | ((uint64_t)y1 << 45) | ((uint64_t)pp << 60) |
+         ((uint64_t)pq << 61);
+}
+
+// Algorithm 1 on one region with local lists (DFS, warp-private stack).
+template <bool COUNT>
+__device__ long long region_pixelbox(const LocalPoly& P, const LocalPoly& Q, int Wr, int Hr, int T, int mode,
+                                     uint64_t* stk, int4* sv, int* sh, long long* counters, unsigned& status) {
+  const int lane = threadIdx.x & 31;
+  if (mode == 1 || (long long)Wr * Hr < T) return pixelize_local<COUNT>(P, Q, 0, 0, Wr, Hr, P.pi, Q.pi, sv, sh, counters);
+  long long acc = 0;
+  if (lane == 0) stk[0] = pack_sb(0, 0, Wr, Hr, P.pi, Q.pi);
+  int top = 1;
+  __syncwarp();
+  while (top > 0) {
+    const uint64_t e = stk[top - 1];
+    top--;
+    __syncwarp();  // every lane has read the popped entry before it is overwritten (reading R11)
+    const int x0 = (int)(e & 0x7fff), y0 = (int)((e >> 15) & 0x7fff);
+    const int x1 = (int)((e >> 30) & 0x7fff), y1 = (int)((e >> 45) & 0x7fff);
+    const int pip = (int)((e >> 60) & 1), piq = (int)((e >> 61) & 1);
+    const int Wb = x1 - x0, Hb = y1 - y0;
+    if ((long long)Wb * Hb < T) {
+      acc += pixelize_local<COUNT>(P, Q, x0, y0, x1, y1, pip, piq, sv, sh, counters);
+      continue;
+    }
+    const Split g = make_split(Wb, Hb);
+    unsigned hp, pp, hq, pq;
+    classify_local(P, x0, y0, Wb, Hb, g, pip, hp, pp);
+    classify_local(Q, x0, y0, Wb, Hb, g, piq, hq, pq);
+    const int cc = lane & (g.kx - 1), rr = lane >> g.lkx;
+    const unsigned valid = __ballot_sync(FULL, cc < g.ncols && rr < g.nrows);
+    const unsigned in_p = ~hp & pp, out_p = ~hp & ~pp, in_q = ~hq & pq, out_q = ~hq & ~pq;
+    // BOXCONTRIBUTE / BOXCONTINUE (Alg. 1 l.33-35, reading R7)
+    const unsigned contrib = valid & in_p & in_q;
+    const unsigned cont = valid & ~(out_p | out_q) & ~contrib;
+    const int sx0 = cc << g.lsx, sy0 = rr << g.lsy;
+    const int sx1 = min(sx0 + (1 << g.lsx), Wb), sy1 = min(sy0 + (1 << g.lsy), Hb);
+    if ((contrib >> lane) & 1u) acc += (long long)(sx1 - sx0) * (sy1 - sy0);
+    const int ncont = __popc(cont);
+    if (COUNT && lane == 0) {
+      atomicAdd((unsigned long long*)&counters[SCCG_CNT_BOXES], (unsigned long long)__popc(valid));
+      atomicAdd((unsigned long long*)&counters[SCCG_CNT_BOXEDGES], (unsigned long long)(P.nV + P.nH + Q.nV + Q.nH));
+      atomicAdd((unsigned long long*)&counters[SCCG_CNT_SPLITS], 1ull);
+    }
+    if (top + ncont > kLStack) {  // cannot happen for regions <= 32766 (depth <= 8 levels x 32); guard anyway
+      status |= SCCG_STATUS_STACK;
+      break;
+    }
+    if ((cont >> lane) & 1u)
+      stk[top + __popc(cont & lanemask_lt())] =
+          pack_sb(x0 + sx0, y0 + sy0, x0 + sx1, y0 + sy1, (int)((pp >> lane) & 1u), (int)((pq >> lane) & 1u));
+    top += ncont;
+    __syncwarp();
+  }
+  return acc;
+}
+
+// ------------------------------------------------------------------ kernels
+// item: pair slot i (32 bit; 0xffffffff = no-op) | rx | ry | nx | ny (8 bit each)
+__device__ __forceinline__ uint64_t pack_item(unsigned i, int rx, int ry, int nx, int ny) {
+  return (uint64_t)i | ((uint64_t)rx << 32) | ((uint64_t)ry << 40) | ((uint64_t)nx << 48) | ((uint64_t)ny << 56);
+}
+
+struct LargeWs {
+  unsigned long long* ctr;  // [0] item queue, [1] extra item count
+  long long* acc;           // [n_cap] per large pair pixel count
+  uint64_t* items;          // [n_cap + extra_cap]
+  long long extra_cap;
+};
+
+__device__ __forceinline__ int4 root_box(const DevSet& Ps, const DevSet& Qs, int2 pq) {
+  const int4 mp = Ps.mbr[pq.x], mq = Qs.mbr[pq.y];
+  return make_int4(max(mp.x, mq.x), max(mp.y, mq.y), min(mp.z, mq.z), min(mp.w, mq.w));
+}
+
+__global__ void expand_kernel(DevSet Ps, DevSet Qs, const int2* __restrict__ pairs, const long long* __restrict__ list,
+                              const unsigned* __restrict__ count, long long n_cap, LargeWs w) {
+  const long long n = min((long long)*count, n_cap);
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const int4 rb = root_box(Ps, Qs, pairs[list[i]]);
+    const int W = rb.z - rb.x, H = rb.w - rb.y;
+    int nx = min(kMaxSplit, max((W + kRegion - 1) / kRegion, (W + kMaxRegion - 1) / kMaxRegion));
+    int ny = min(kMaxSplit, max((H + kRegion - 1) / kRegion, (H + kMaxRegion - 1) / kMaxRegion));
+    w.acc[i] = 0;
+    const int extra = nx * ny - 1;
+    if (extra > 0) {
+      const long long base = (long long)atomicAdd(&w.ctr[1], (unsigned long long)extra);
+      if (base + extra <= w.extra_cap) {
+        for (int r = 1; r <= extra; r++) w.items[n_cap + base + r - 1] = pack_item((unsigned)i, r % nx, r / nx, nx, ny);
+      } else {  // out of item space: this pair is one item (split in-warp on overflow)
+        for (long long t = base; t < w.extra_cap; t++) w.items[n_cap + t] = pack_item(0xffffffffu, 0, 0, 1, 1);
+        nx = ny = 1;
+      }
+    }
+    w.items[i] = pack_item((unsigned)i, 0, 0, nx, ny);
+  }
+}
+
+constexpr size_t kLSmemPerWarp = (size_t)4 * kLCap * sizeof(uint64_t) + (size_t)2 * kLStage * sizeof(int4) +
+                                 (size_t)2 * kLStage * sizeof(int) + (size_t)kLStack * sizeof(uint64_t) +
+                                 (size_t)kLItems * sizeof(int4);
+constexpr size_t kLSmem = kLWarps * kLSmemPerWarp;
+
+template <bool COUNT>
+__global__ void __launch_bounds__(kLWarps * 32)
+    item_kernel(DevSet Ps, DevSet Qs, const int2* __restrict__ pairs, const long long* __restrict__ list,
+                const unsigned* __restrict__ count, long long n_cap, LargeWs w, int T, int mode, long long* counters,
+                sccg_sums* sums) {
+  extern __shared__ __align__(16) unsigned char s_raw[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  unsigned char* base = s_raw + (size_t)warp * kLSmemPerWarp;
+  LocalPoly P, Q;
+  P.V = reinterpret_cast<uint64_t*>(base);
+  P.H = P.V + kLCap;
+  Q.V = P.H + kLCap;
+  Q.H = Q.V + kLCap;
+  int4* sv = reinterpret_cast<int4*>(Q.H + kLCap);
+  int* sh = reinterpret_cast<int*>(sv + 2 * kLStage);
+  uint64_t* stk = reinterpret_cast<uint64_t*>(sh + 2 * kLStage);
+  int4* istk = reinterpret_cast<int4*>(stk + kLStack);
+  const long long nl = min((long long)*count, n_cap);
+  const long long ne = min((long long)w.ctr[1], w.extra_cap);
+  const long long total = nl + ne;
+  unsigned status = 0;
+  for (;;) {
+    unsigned long long t = 0;
+    if (lane == 0) t = atomicAdd(&w.ctr[0], 1ull);
+    t = __shfl_sync(FULL, t, 0);
+    if ((long long)t >= total) break;
+    const uint64_t it = w.items[(long long)t < nl ? (long long)t : n_cap + ((long long)t - nl)];
+    const unsigned i = (unsigned)(it & 0xffffffffu);
+    if (i == 0xffffffffu) continue;
+    const int rx = (int)((it >> 32) & 0xff), ry = (int)((it >> 40) & 0xff);
+    const int nx = (int)((it >> 48) & 0xff), ny = (int)((it >> 56) & 0xff);
+    const int2 pq = pairs[list[i]];
+    const int4 rb = root_box(Ps, Qs, pq);
+    const int W = rb.z - rb.x, H = rb.w - rb.y;
+    PolyRef pr[2];
+    for (int s = 0; s < 2; s++) {
+      const DevSet& S = s ? Qs : Ps;
+      const int id = s ? pq.y : pq.x;
+      const int4 m = S.mbr[id];
+      const long long o = S.off[id];
+      pr[s].ev = S.edges + o;
+      pr[s].v = S.xy + o;
+      pr[s].nv = S.ecount[id].x;
+      pr[s].V = (int)(S.off[id + 1] - o);
+      pr[s].dx = m.x - rb.x;
+      pr[s].dy = m.y - rb.y;
+      pr[s].ox = rb.x;
+      pr[s].oy = rb.y;
+    }
+    long long acc = 0;
+    // in-warp item stack: the region, split in two while its local lists overflow
+    if (lane == 0)
+      istk[0] = make_int4((int)((long long)rx * W / nx), (int)((long long)ry * H / ny),
+                          (int)((long long)(rx + 1) * W / nx), (int)((long long)(ry + 1) * H / ny));
+    int itop = 1;
+    __syncwarp();
+    while (itop > 0) {
+      const int4 R = istk[itop - 1];
+      itop--;
+      __syncwarp();
+      const int Wr = R.z - R.x, Hr = R.w - R.y;
+      bool fits = Wr <= kMaxRegion && Hr <= kMaxRegion;
+      if (fits) {
+        const bool a = build_local(pr[0], R.x, R.y, R.z, R.w, P);
+        const bool b = build_local(pr[1], R.x, R.y, R.z, R.w, Q);
+        fits = a && b;
+      }
+      __syncwarp();
+      if (!fits) {
+        if (itop + 2 > kLItems) {
+          status |= SCCG_STATUS_STACK;
+          continue;
+        }
+        if (lane == 0) {
+          if (Wr >= Hr) {
+            const int xm = R.x + Wr / 2;
+            istk[itop] = make_int4(R.x, R.y, xm, R.w);
+            istk[itop + 1] = make_int4(xm, R.y, R.z, R.w);
+          } else {
+            const int ym = R.y + Hr / 2;
+            istk[itop] = make_int4(R.x, R.y, R.z, ym);
+            istk[itop + 1] = make_int4(R.x, ym, R.z, R.w);
+          }
+        }
+        itop += 2;
+        __syncwarp();
+        continue;
+      }
+      acc += region_pixelbox<COUNT>(P, Q, Wr, Hr, T, mode, stk, sv, sh, counters, status);
+      __syncwarp();
+    }
+    acc = (long long)warp_sum_u64((unsigned long long)acc);
+    if (lane == 0) atomicAdd(reinterpret_cast<unsigned long long*>(&w.acc[i]), (unsigned long long)acc);
+  }
+  status = __reduce_or_sync(FULL, status);
+  if (lane == 0 && status) atomicOr(reinterpret_cast<unsigned long long*>(&sums->status), (unsigned long long)status);
+}
+
+template <bool COUNT>
+__global__ void __launch_bounds__(256) large_epilogue_kernel(DevSet Ps, DevSet Qs, const int2* __restrict__ pairs,
+                                                             const long long* __restrict__ list,
+                                                             const unsigned* __restrict__ count, long long n_cap,
+                                                             LargeWs w, long long* __restrict__ inter,
+                                                             long long* __restrict__ uni, sccg_sums* sums,
+                                                             long long* counters) {
+  __shared__ unsigned long long s_acc[10];
+  if (threadIdx.x < 10) s_acc[threadIdx.x] = 0;
+  __syncthreads();
+  const long long n = min((long long)*count, n_cap);
+  unsigned long long a[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  unsigned long long rootpx = 0;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const long long k = list[i];
+    const int2 pq = pairs[k];
+    const long long I = w.acc[i];
+    const long long ap = Ps.area[pq.x], aq = Qs.area[pq.y];
+    const long long U = ap + aq - I;  // indirect union
+    if (inter) inter[k] = I;
+    if (uni) uni[k] = U;
+    a[0]++;
+    a[2] += I;
+    a[4] += ap;
+    a[5] += aq;
+    if (I != 0) {
+      unsigned long long l0, l1, l2, l3;
+      ratio_limbs(I, U, l0, l1, l2, l3);
+      a[1]++;
+      a[3] += U;
+      a[6] += l0;
+      a[7] += l1;
+      a[8] += l2;
+      a[9] += l3;
+    }
+    if (COUNT) {
+      const int4 rb = root_box(Ps, Qs, pq);
+      rootpx += (unsigned long long)(rb.z - rb.x) * (rb.w - rb.y);
+    }
+  }
+  for (int f = 0; f < 10; f++) {
+    const unsigned long long v = warp_sum_u64(a[f]);
+    if ((threadIdx.x & 31) == 0 && v) atomicAdd(&s_acc[f], v);
+  }
+  if (COUNT) {
+    const unsigned long long v = warp_sum_u64(rootpx);
+    if ((threadIdx.x & 31) == 0 && v) atomicAdd((unsigned long long*)&counters[SCCG_CNT_ROOTPX], v);
+  }
+  __syncthreads();
+  if (threadIdx.x < 10 && s_acc[threadIdx.x])
+    atomicAdd(reinterpret_cast<unsigned long long*>(sums) + threadIdx.x, s_acc[threadIdx.x]);
+}
+
+// ---------------------------------------------------------------------- host
+static long long extra_cap_for(long long n_cap) { return 4 * n_cap + 65536; }
+
+static size_t large_layout(long long n_cap, Carve& cv, LargeWs& w) {
+  w.ctr = cv.take<unsigned long long>(4);
+  w.acc = cv.take<long long>(n_cap > 0 ? n_cap : 1);
+  w.extra_cap = extra_cap_for(n_cap);
+  w.items = cv.take<uint64_t>(n_cap + w.extra_cap);
+  return cv.used;
+}
+
+size_t large_ws_bytes(long long n_cap) {
+  Carve cv{nullptr, ~size_t(0)};
+  LargeWs w;
+  return large_layout(n_cap, cv, w) + 256;
+}
+
+int launch_large(const DevSet& Ps, const DevSet& Qs, const int2* pairs, long long n_cap, const long long* large_list,
+                 const unsigned* large_count, long long* inter, long long* uni, sccg_sums* sums, int T, int mode,
+                 long long* counters, void* ws, size_t ws_bytes, cudaStream_t stream) {
+  Carve cv{reinterpret_cast<char*>(ws), ws_bytes};
+  LargeWs w;
+  large_layout(n_cap, cv, w);
+  if (!cv.ok) return set_error(SCCG_E_WORKSPACE, "pixelbox (large) workspace too small");
+  static cudaError_t attr = [] {
+    cudaError_t e = cudaFuncSetAttribute(item_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kLSmem);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(item_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kLSmem);
+    return e;
+  }();
+  if (int r = check_cuda(attr, "item kernel smem attribute")) return r;
+  static int sms = 0, per_sm[2] = {0, 0};
+  if (sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[0], item_kernel<false>, kLWarps * 32, kLSmem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[1], item_kernel<true>, kLWarps * 32, kLSmem);
+  }
+  const bool count = counters != nullptr;
+  cudaMemsetAsync(w.ctr, 0, 4 * sizeof(unsigned long long), stream);
+  const long long eb = min((long long)sms * 8, (n_cap + 255) / 256);
+  expand_kernel<<<(unsigned)max(eb, 1ll), 256, 0, stream>>>(Ps, Qs, pairs, large_list, large_count, n_cap, w);
+  const unsigned ib = (unsigned)(sms * max(per_sm[count], 1));
+  if (count) {
+    item_kernel<true><<<ib, kLWarps * 32, kLSmem, stream>>>(Ps, Qs, pairs, large_list, large_count, n_cap, w, T, mode,
+                                                          counters, sums);
+    large_epilogue_kernel<true><<<(unsigned)max(eb, 1ll), 256, 0, stream>>>(Ps, Qs, pairs, large_list, large_count,
+                                                                             n_cap, w, inter, uni, sums, counters);
+  } else {
+    item_kernel<false><<<ib, kLWarps * 32, kLSmem, stream>>>(Ps, Qs, pairs, large_list, large_count, n_cap, w, T,
+                                                           mode, nullptr, sums);
+    large_epilogue_kernel<false><<<(unsigned)max(eb, 1ll), 256, 0, stream>>>(Ps, Qs, pairs, large_list, large_count,
+                                                                              n_cap, w, inter, uni, sums, nullptr);
+  }
+  return check_cuda(cudaGetLastError(), "pixelbox large launch");
+}
+
+}  // namespace sccg

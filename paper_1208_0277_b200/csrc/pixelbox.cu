@@ -1,4 +1,5 @@
-// pixelbox.cu -- the PixelBox kernel for sm_100a.
+// pixelbox.cu -- the PixelBox kernel for small pairs
+// and the sccg_pixelbox launcher.
 //
 // PAPER.md §3 / Algorithm 1 computes, per polygon pair, the area
 // of intersection by recursively partitioning the pair's box into sampling
@@ -7,383 +8,17 @@
 // threshold T (Alg. 1 l.22) by ray-casting crossing counts (§3.1).
 // The union follows from |p u q| = |p| + |q| - |p n q|.
 //
-// B200 design: one warp per pair, pairs pulled from a
-// global work queue by a persistent grid; no __syncthreads in the pair loop
-// (the paper's block-wide barrier per stack pop, and its read/write
-// hazard, reading R11, disappear: the stack is warp-private and every pop is
-// separated from the next push by __syncwarp).  Both phases are bit-parallel:
-//   * pixelization: a lane owns a 32-pixel row word and accumulates the
-//     crossing parity of all 32 pixels at once -- each vertical edge that
-//     crosses the row toggles the pixels on one side of it (a shifted mask),
-//     so one (row word x edge) test decides 32 ray casts;
-//   * box classification (Lemma 1, reading R6-A): a box split into up to 32
-//     power-of-two-aligned sub-boxes is classified edge-parallel -- a lane owns
-//     an edge and writes the sub-boxes whose open interior the edge meets
-//     (hover) and the sub-box corner pixels whose rays it crosses (parity) as
-//     32-bit masks, OR / XOR-reduced across the warp with one REDUX each.
-// Areas are exact integers; per-pair results and the int64 sums are
+// B200 design: the common nucleus pair (root box at most
+// 32 x 32 and below T, so Alg. 1 pixelizes the root box directly) runs in the
+// software-pipelined small kernel below -- one warp per pair, bit-parallel
+// pixelization (a lane owns a 32-pixel row word; one crossing test decides 32
+// ray casts).  Every other pair is routed to the large-pair path (large.cu):
+// region work items, each a warp-private sampling-box DFS over locally culled
+// edges.  Areas are exact integers; per-pair results and the int64 sums are
 // bit-identical for every launch shape and threshold.
-#include "internal.cuh"
+#include "pixelbox_common.cuh"
 
 namespace sccg {
-
-constexpr int kWarps = 8;        // warps per CTA
-constexpr int kStackCap = 512;   // sampling boxes per warp stack (>= 32 x depth)
-constexpr int kECap = 128;       // staged vertical edges per polygon per warp
-constexpr int kChunk = 4;        // pairs claimed per queue atomic
-constexpr unsigned FULL = 0xffffffffu;
-
-struct PairCtx {
-  const uint64_t* ev;  // vertical edge records (sccg_prep)
-  const int2* v;       // the ring's raw vertices (horizontal edges are read from these)
-  int nv, nh, V;       // vertical edges, horizontal edges, vertices
-  int dx, dy;          // polygon MBR origin minus root-box origin
-  int ox, oy;          // root-box origin (absolute)
-};
-
-struct Split {
-  int kx, lkx, lsx, lsy, ncols, nrows;
-  unsigned colpat;  // bit r*kx for every row r
-};
-
-__device__ __forceinline__ int ceil_log2(int v) { return v <= 1 ? 0 : 32 - __clz(v - 1); }
-
-// SUBSAMPBOX (Alg. 1 l.30, reading R8): an aligned grid of power-of-two cells,
-// 8 x 4 (or 4 x 8 for tall boxes), clipped to the box; every sub-box non-empty.
-__device__ __forceinline__ Split make_split(int Wb, int Hb) {
-  Split g;
-  g.kx = Wb >= Hb ? 8 : 4;
-  g.lkx = Wb >= Hb ? 3 : 2;
-  const int ky = 32 / g.kx;
-  g.lsx = ceil_log2((Wb + g.kx - 1) / g.kx);
-  g.lsy = ceil_log2((Hb + ky - 1) / ky);
-  g.ncols = (Wb + (1 << g.lsx) - 1) >> g.lsx;
-  g.nrows = (Hb + (1 << g.lsy) - 1) >> g.lsy;
-  g.colpat = g.kx == 8 ? 0x01010101u : 0x11111111u;
-  return g;
-}
-
-// bits of sub-box rows r_lo..r_hi (empty if r_hi < r_lo)
-__device__ __forceinline__ unsigned row_range(int r_lo, int r_hi, const Split& g) {
-  return low_bits((r_hi - r_lo + 1) << g.lkx) << (max(r_lo, 0) << g.lkx);
-}
-
-// Lemma 1 (reading R6-A) for all sub-boxes of one split, edge-parallel.
-// hov: sub-boxes whose open interior meets a polygon edge; par: crossing
-// parity of each sub-box's lower-left pixel (inside iff set), valid where
-// hov == 0.  dx, dy: polygon MBR origin relative to the box origin.
-__device__ __forceinline__ void classify(const PairCtx& c, int dx, int dy, int Wb, int Hb, const Split& g,
-                                         unsigned& hov, unsigned& par) {
-  const int lane = threadIdx.x & 31;
-  const int sx = 1 << g.lsx, sy = 1 << g.lsy;
-  unsigned h = 0, p = 0;
-  for (int j = lane; j < c.nv; j += 32) {
-    int cc, lo, hi;
-    unpack_edge(__ldg(c.ev + j), cc, lo, hi);
-    const int x = cc + dx, yl = lo + dy, yh = hi + dy;
-    if (yl < Hb && yh > 0) {
-      const int r_hi = min(g.nrows - 1, (yh - 1) >> g.lsy);
-      if (x > 0 && x < Wb && (x & (sx - 1)) != 0)  // edge inside a column's open x-range
-        h |= (g.colpat << (x >> g.lsx)) & row_range(max(0, yl >> g.lsy), r_hi, g);
-      if (x > 0) {  // ray from corner pixel (c*sx, r*sy) crosses x iff c*sx < x and yl <= r*sy < yh
-        const int c_hi = min(g.ncols - 1, (x - 1) >> g.lsx);
-        p ^= (low_bits(c_hi + 1) * g.colpat) & row_range(max(0, (yl + sy - 1) >> g.lsy), r_hi, g);
-      }
-    }
-  }
-  // horizontal edges straight from the ring: edge (v_j, v_j+1) with equal y
-  const int ax0 = c.ox + (c.dx - dx), ay0 = c.oy + (c.dy - dy);  // absolute origin of the box
-  for (int j = lane; j < c.V; j += 32) {
-    const int2 a = __ldg(c.v + j), b = __ldg(c.v + (j + 1 == c.V ? 0 : j + 1));
-    if (a.y != b.y || a.x == b.x) continue;
-    const int y = a.y - ay0, xl = min(a.x, b.x) - ax0, xh = max(a.x, b.x) - ax0;
-    if (y > 0 && y < Hb && (y & (sy - 1)) != 0 && xl < Wb && xh > 0) {
-      const int c_lo = max(0, xl >> g.lsx), c_hi = min(g.ncols - 1, (xh - 1) >> g.lsx);
-      h |= low_bits(c_hi - c_lo + 1) << (((y >> g.lsy) << g.lkx) + c_lo);
-    }
-  }
-  hov = __reduce_or_sync(FULL, h);
-  par = __reduce_xor_sync(FULL, p);
-}
-
-// Stage the vertical edges of one polygon that cross any row of the box into
-// shared memory as {ylo, span, mask | x, 0}, box-relative.  Returns the count
-// (> kECap means the caller must stream edges from global memory instead).
-__device__ __forceinline__ int stage(const PairCtx& c, int dx, int dy, int Hb, bool one_word, int4* buf) {
-  const int lane = threadIdx.x & 31;
-  int cnt = 0;
-  for (int j0 = 0; j0 < c.nv; j0 += 32) {
-    const int j = j0 + lane;
-    bool keep = false;
-    int x = 0, yl = 0, yh = 0;
-    if (j < c.nv) {
-      int cc, lo, hi;
-      unpack_edge(__ldg(c.ev + j), cc, lo, hi);
-      x = cc + dx;
-      yl = lo + dy;
-      yh = hi + dy;
-      keep = yl < Hb && yh > 0;
-    }
-    const unsigned b = __ballot_sync(FULL, keep);
-    if (keep) {
-      const int pos = cnt + __popc(b & lanemask_lt());
-      if (pos < kECap) buf[pos] = make_int4(yl, yh - yl, one_word ? (int)suffix_mask(x) : x, 0);
-    }
-    cnt += __popc(b);
-  }
-  return cnt;
-}
-
-// Row-word crossing parity from staged edges.
-__device__ __forceinline__ unsigned row_parity_staged(const int4* buf, int n, int row, bool one_word, int xs) {
-  unsigned m = 0;
-  if (one_word) {
-#pragma unroll 4
-    for (int j = 0; j < n; j++) {
-      const int4 r = buf[j];
-      if ((unsigned)(row - r.x) < (unsigned)r.y) m ^= (unsigned)r.z;
-    }
-  } else {
-#pragma unroll 4
-    for (int j = 0; j < n; j++) {
-      const int4 r = buf[j];
-      if ((unsigned)(row - r.x) < (unsigned)r.y) m ^= suffix_mask(r.z - xs);
-    }
-  }
-  return m;
-}
-
-// Row-word crossing parity streaming every vertical edge from global memory
-// (shared-memory overflow path).
-__device__ __forceinline__ unsigned row_parity_global(const PairCtx& c, int dx, int dy, int row, int xs) {
-  unsigned m = 0;
-  for (int j = 0; j < c.nv; j++) {
-    int cc, lo, hi;
-    unpack_edge(__ldg(c.ev + j), cc, lo, hi);
-    if ((unsigned)(row - (lo + dy)) < (unsigned)(hi - lo)) m ^= suffix_mask(cc + dx - xs);
-  }
-  return m;
-}
-
-// Pixelization of box [X0, X1) x [Y0, Y1) (root-relative), Alg. 1 l.22-28:
-// returns this lane's share of the pixels inside both polygons.
-template <bool COUNT>
-__device__ long long pixelize(int X0, int Y0, int X1, int Y1, const PairCtx& P, const PairCtx& Q, int4* sp,
-                              int4* sq, long long* counters) {
-  const int lane = threadIdx.x & 31;
-  const int Wb = X1 - X0, Hb = Y1 - Y0;
-  const int nw = (Wb + 31) >> 5;
-  const bool one = nw == 1;
-  const int dxp = P.dx - X0, dyp = P.dy - Y0, dxq = Q.dx - X0, dyq = Q.dy - Y0;
-  const int np = stage(P, dxp, dyp, Hb, one, sp);
-  const int nq = stage(Q, dxq, dyq, Hb, one, sq);
-  __syncwarp();
-  const bool over_p = np > kECap, over_q = nq > kECap;
-  const int nseg = Hb * nw;
-  long long acc = 0;
-  for (int s0 = 0; s0 < nseg; s0 += 32) {
-    const int s = s0 + lane;
-    if (s < nseg) {
-      const int row = one ? s : s / nw;
-      const int xs = (s - row * nw) << 5;
-      const unsigned mp = over_p ? row_parity_global(P, dxp, dyp, row, xs) : row_parity_staged(sp, np, row, one, xs);
-      const unsigned mq = over_q ? row_parity_global(Q, dxq, dyq, row, xs) : row_parity_staged(sq, nq, row, one, xs);
-      acc += __popc(mp & mq & low_bits(Wb - xs));
-    }
-  }
-  __syncwarp();
-  if (COUNT && lane == 0) {
-    atomicAdd((unsigned long long*)&counters[SCCG_CNT_PIXELS], (unsigned long long)Wb * Hb);
-    atomicAdd((unsigned long long*)&counters[SCCG_CNT_ROWTESTS],
-              (unsigned long long)nseg * ((over_p ? P.nv : np) + (over_q ? Q.nv : nq)));
-    atomicAdd((unsigned long long*)&counters[SCCG_CNT_PIXBOXES], 1ull);
-  }
-  return acc;
-}
-
-__device__ __forceinline__ uint64_t pack_box(int x0, int y0, int x1, int y1) {
-  return (uint64_t)(uint32_t)x0 | ((uint64_t)(uint32_t)y0 << 16) | ((uint64_t)(uint32_t)x1 << 32) |
-         ((uint64_t)(uint32_t)y1 << 48);
-}
-
-// Sampling-box loop (Alg. 1 l.13-42) over a warp-private DFS stack.
-template <bool COUNT>
-__device__ long long sample(int W, int H, const PairCtx& P, const PairCtx& Q, uint64_t* stk, int4* sp, int4* sq, int T,
-                            long long* counters, unsigned& status) {
-  const int lane = threadIdx.x & 31;
-  long long acc = 0;
-  if (lane == 0) stk[0] = pack_box(0, 0, W, H);
-  int top = 1;
-  __syncwarp();
-  while (top > 0) {
-    const uint64_t bx = stk[top - 1];
-    top--;
-    __syncwarp();  // every lane has read the popped entry before it is overwritten
-    const int X0 = (int)(bx & 0xffff), Y0 = (int)((bx >> 16) & 0xffff);
-    const int X1 = (int)((bx >> 32) & 0xffff), Y1 = (int)(bx >> 48);
-    const int Wb = X1 - X0, Hb = Y1 - Y0;
-    if ((long long)Wb * Hb < T) {
-      acc += pixelize<COUNT>(X0, Y0, X1, Y1, P, Q, sp, sq, counters);
-      continue;
-    }
-    const Split g = make_split(Wb, Hb);
-    unsigned hp, pp, hq, pq;
-    classify(P, P.dx - X0, P.dy - Y0, Wb, Hb, g, hp, pp);
-    classify(Q, Q.dx - X0, Q.dy - Y0, Wb, Hb, g, hq, pq);
-    const int cc = lane & (g.kx - 1), rr = lane >> g.lkx;
-    const unsigned valid = __ballot_sync(FULL, cc < g.ncols && rr < g.nrows);
-    const unsigned in_p = ~hp & pp, out_p = ~hp & ~pp, in_q = ~hq & pq, out_q = ~hq & ~pq;
-    // BOXCONTRIBUTE / BOXCONTINUE (Alg. 1 l.33-35, reading R7)
-    const unsigned contrib = valid & in_p & in_q;
-    const unsigned cont = valid & ~(out_p | out_q) & ~contrib;
-    const int x0 = cc << g.lsx, y0 = rr << g.lsy;
-    const int x1 = min(x0 + (1 << g.lsx), Wb), y1 = min(y0 + (1 << g.lsy), Hb);
-    if ((contrib >> lane) & 1u) acc += (long long)(x1 - x0) * (y1 - y0);
-    const int ncont = __popc(cont);
-    if (COUNT && lane == 0) {
-      atomicAdd((unsigned long long*)&counters[SCCG_CNT_BOXES], (unsigned long long)__popc(valid));
-      atomicAdd((unsigned long long*)&counters[SCCG_CNT_BOXEDGES],
-                (unsigned long long)(P.nv + P.V + Q.nv + Q.V));
-      atomicAdd((unsigned long long*)&counters[SCCG_CNT_SPLITS], 1ull);
-    }
-    if (top + ncont > kStackCap) {
-      status |= SCCG_STATUS_STACK;
-      break;
-    }
-    if ((cont >> lane) & 1u) stk[top + __popc(cont & lanemask_lt())] = pack_box(X0 + x0, Y0 + y0, X0 + x1, Y0 + y1);
-    top += ncont;
-    __syncwarp();
-  }
-  return acc;
-}
-
-// r = RN64(I / U) as an exact integer count of 2^-116, split into 30-bit limbs
-// (reading R12).  Requires 0 < I <= U < 2^63.
-__device__ __forceinline__ void ratio_limbs(long long I, long long U, unsigned long long& l0, unsigned long long& l1,
-                                            unsigned long long& l2, unsigned long long& l3) {
-  const double r = __ddiv_rn((double)I, (double)U);
-  const unsigned long long bits = (unsigned long long)__double_as_longlong(r);
-  const int ex = (int)((bits >> 52) & 0x7ff);
-  const unsigned long long mant = (bits & ((1ull << 52) - 1)) | (1ull << 52);
-  const int s = ex - 1075 + 116;  // in [1, 64] for r in (2^-63, 1]
-  const unsigned __int128 v = (unsigned __int128)mant << s;
-  l0 = (unsigned long long)(v & 0x3fffffffu);
-  l1 = (unsigned long long)((v >> 30) & 0x3fffffffu);
-  l2 = (unsigned long long)((v >> 60) & 0x3fffffffu);
-  l3 = (unsigned long long)(v >> 90);
-}
-
-// r = RN64(I / U) as an exact integer count of 2^-116, split into 30-bit limbs
-// (reading R12), accumulated.  Requires 0 < I <= U < 2^63.
-__device__ __forceinline__ void add_ratio_limbs(long long I, long long U, unsigned long long limb[4]) {
-  unsigned long long a, b, c, d;
-  ratio_limbs(I, U, a, b, c, d);
-  limb[0] += a;
-  limb[1] += b;
-  limb[2] += c;
-  limb[3] += d;
-}
-
-__device__ __forceinline__ long long warp_sum64(long long v) {
-  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
-  return v;
-}
-
-// --------------------------------------------------------------- large pairs
-// Generic warp-per-pair kernel: any box size, sampling boxes + pixelization,
-// shared-memory overflow path.  Consumes the pair indices the small-pair
-// kernel routed to it (list[0 .. *count)).
-template <bool COUNT>
-__global__ void __launch_bounds__(kWarps * 32, 3)
-    large_kernel(DevSet Ps, DevSet Qs, const int2* __restrict__ pairs, const long long* __restrict__ list,
-                 const unsigned* __restrict__ count, long long* __restrict__ inter, long long* __restrict__ uni,
-                 sccg_sums* sums, int T, int mode, unsigned long long* queue, long long* counters) {
-  extern __shared__ int4 s_dyn[];  // [kWarps][2][kECap] edge scratch, then [kWarps][kStackCap] stack
-  __shared__ unsigned long long s_red[kWarps][11];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  int4* sp = s_dyn + (size_t)warp * 2 * kECap;
-  int4* sq = sp + kECap;
-  uint64_t* stk = reinterpret_cast<uint64_t*>(s_dyn + (size_t)kWarps * 2 * kECap) + (size_t)warp * kStackCap;
-  const long long n = *count;
-  unsigned long long a_n = 0, a_nz = 0, a_i = 0, a_u = 0, a_ap = 0, a_aq = 0, limb[4] = {0, 0, 0, 0};
-  unsigned status = 0;
-  for (;;) {
-    unsigned long long i0 = 0;
-    if (lane == 0) i0 = atomicAdd(queue, 1ull);
-    i0 = __shfl_sync(FULL, i0, 0);
-    if ((long long)i0 >= n) break;
-    const long long k = list[i0];
-    const int2 pq = pairs[k];
-    const int4 mp = Ps.mbr[pq.x], mq = Qs.mbr[pq.y];
-    const int bx0 = max(mp.x, mq.x), by0 = max(mp.y, mq.y);
-    const int bx1 = min(mp.z, mq.z), by1 = min(mp.w, mq.w);
-    const int2 cp = Ps.ecount[pq.x], cq = Qs.ecount[pq.y];
-    PairCtx P, Q;
-    const long long op = Ps.off[pq.x], oq = Qs.off[pq.y];
-    P.ev = Ps.edges + op;
-    P.v = Ps.xy + op;
-    P.V = (int)(Ps.off[pq.x + 1] - op);
-    P.nv = cp.x;
-    P.nh = cp.y;
-    P.dx = mp.x - bx0;
-    P.dy = mp.y - by0;
-    P.ox = bx0;
-    P.oy = by0;
-    Q.ev = Qs.edges + oq;
-    Q.v = Qs.xy + oq;
-    Q.V = (int)(Qs.off[pq.y + 1] - oq);
-    Q.nv = cq.x;
-    Q.nh = cq.y;
-    Q.dx = mq.x - bx0;
-    Q.dy = mq.y - by0;
-    Q.ox = bx0;
-    Q.oy = by0;
-    const int W = bx1 - bx0, H = by1 - by0;
-    if (COUNT && lane == 0) atomicAdd((unsigned long long*)&counters[SCCG_CNT_ROOTPX], (unsigned long long)W * H);
-    long long acc;
-    if (mode == 1 || (long long)W * H < T)
-      acc = pixelize<COUNT>(0, 0, W, H, P, Q, sp, sq, counters);
-    else
-      acc = sample<COUNT>(W, H, P, Q, stk, sp, sq, T, counters, status);
-    const long long I = warp_sum64(acc);
-    if (lane == 0) {
-      const long long ap = Ps.area[pq.x], aq = Qs.area[pq.y];
-      const long long U = ap + aq - I;  // indirect union
-      if (inter) inter[k] = I;
-      if (uni) uni[k] = U;
-      a_n++;
-      a_i += I;
-      a_ap += ap;
-      a_aq += aq;
-      if (I != 0) {
-        a_nz++;
-        a_u += U;
-        add_ratio_limbs(I, U, limb);
-      }
-    }
-  }
-  if (lane == 0) {
-    s_red[warp][0] = a_n;
-    s_red[warp][1] = a_nz;
-    s_red[warp][2] = a_i;
-    s_red[warp][3] = a_u;
-    s_red[warp][4] = a_ap;
-    s_red[warp][5] = a_aq;
-    for (int i = 0; i < 4; i++) s_red[warp][6 + i] = limb[i];
-    s_red[warp][10] = status;
-  }
-  __syncthreads();
-  if (threadIdx.x < 11) {
-    unsigned long long v = 0;
-    for (int w = 0; w < kWarps; w++) v = threadIdx.x == 10 ? (v | s_red[w][10]) : v + s_red[w][threadIdx.x];
-    unsigned long long* dst = reinterpret_cast<unsigned long long*>(sums);
-    if (threadIdx.x == 10) {
-      if (v) atomicOr(&dst[10], v);
-    } else if (v) {
-      atomicAdd(&dst[threadIdx.x], v);
-    }
-  }
-}
 
 // --------------------------------------------------------------- small pairs
 // The common case (nucleus pairs): root box at most 32 x 32 pixels and below
@@ -453,11 +88,6 @@ __device__ __forceinline__ void row_words(const int2* __restrict__ b, int n, uns
       xor_if(m1, w.z, bit1, w.w);
     }
   }
-}
-
-__device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long v) {
-  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
-  return v;
 }
 
 #ifndef SCCG_SMALL_MINB
@@ -645,15 +275,19 @@ __global__ void __launch_bounds__(kSmallWarps * 32, SCCG_SMALL_MINB)
 
 // ---------------------------------------------------------------------- host
 struct PixelboxWs {
-  unsigned long long* queue;  // [2] small, large
+  unsigned long long* queue;  // small-kernel queue
   unsigned* large_count;
   long long* large_list;
+  void* large_ws;
+  size_t large_bytes;
 };
 
 static size_t pixelbox_layout(int64_t n, Carve& cv, PixelboxWs& w) {
   w.queue = cv.take<unsigned long long>(4);
   w.large_count = reinterpret_cast<unsigned*>(w.queue + 2);
   w.large_list = cv.take<long long>(n > 0 ? n : 1);
+  w.large_bytes = large_ws_bytes(n);
+  w.large_ws = cv.take<char>(w.large_bytes);
   return cv.used;
 }
 
@@ -661,18 +295,6 @@ size_t pixelbox_ws_bytes(int64_t n) {
   Carve cv{nullptr, ~size_t(0)};
   PixelboxWs w;
   return pixelbox_layout(n, cv, w) + 256;
-}
-
-constexpr size_t kDynSmem = (size_t)kWarps * (2 * kECap * sizeof(int4) + kStackCap * sizeof(uint64_t));
-
-static cudaError_t prepare_kernels() {
-  static cudaError_t once = [] {
-    cudaError_t e = cudaFuncSetAttribute(large_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDynSmem);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(large_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDynSmem);
-    return e;
-  }();
-  return once;
 }
 
 int run_pixelbox(const sccg_polyset* p, const sccg_polyset* q, const int32_t* pairs, int64_t n,
@@ -690,44 +312,34 @@ int run_pixelbox(const sccg_polyset* p, const sccg_polyset* q, const int32_t* pa
   if (n == 0) return check_cuda(cudaGetLastError(), "pixelbox");
   const bool count = cfg && cfg->counters;
   long long* counters = count ? reinterpret_cast<long long*>(cfg->counters) : nullptr;
-  if (int r = check_cuda(prepare_kernels(), "pixelbox smem attribute")) return r;
-  static int sms = 0, per_sm_s[2] = {0, 0}, per_sm_l[2] = {0, 0};
+  static int sms = 0, per_sm_s[2] = {0, 0};
   if (sms == 0) {  // launch geometry, queried once
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_s[1], small_kernel<true>, kSmallWarps * 32, 0);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_l[1], large_kernel<true>, kWarps * 32, kDynSmem);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_s[0], small_kernel<false>, kSmallWarps * 32, 0);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_l[0], large_kernel<false>, kWarps * 32, kDynSmem);
   }
   int64_t grid_s = cfg && cfg->grid > 0 ? cfg->grid : (int64_t)sms * max(per_sm_s[count], 1);
   const int64_t need = (n + kSmallWarps * 32 - 1) / (kSmallWarps * 32);
   if (grid_s > need) grid_s = need;
   if (grid_s < 1) grid_s = 1;
-  int64_t grid_l = cfg && cfg->grid > 0 ? cfg->grid : (int64_t)sms * max(per_sm_l[count], 1);
-  const int64_t need_l = (n + kWarps - 1) / kWarps;
-  if (grid_l > need_l) grid_l = need_l;
-  if (grid_l < 1) grid_l = 1;
   DevSet Ps = dev_set(p), Qs = dev_set(q);
   const int2* pr = reinterpret_cast<const int2*>(pairs);
   long long* in = reinterpret_cast<long long*>(inter);
   long long* un = reinterpret_cast<long long*>(uni);
   const long long* dr = reinterpret_cast<const long long*>(dev_result);
-  if (count) {
+  if (count)
     small_kernel<true><<<(unsigned)grid_s, kSmallWarps * 32, 0, stream>>>(
         Ps, Qs, pr, n, dr, in, un, sums, T, mode, w.queue, w.large_list, w.large_count, counters, p->n_polygons,
         q->n_polygons);
-    large_kernel<true><<<(unsigned)grid_l, kWarps * 32, kDynSmem, stream>>>(Ps, Qs, pr, w.large_list, w.large_count,
-                                                                          in, un, sums, T, mode, w.queue + 1, counters);
-  } else {
+  else
     small_kernel<false><<<(unsigned)grid_s, kSmallWarps * 32, 0, stream>>>(
         Ps, Qs, pr, n, dr, in, un, sums, T, mode, w.queue, w.large_list, w.large_count, nullptr, p->n_polygons,
         q->n_polygons);
-    large_kernel<false><<<(unsigned)grid_l, kWarps * 32, kDynSmem, stream>>>(Ps, Qs, pr, w.large_list, w.large_count,
-                                                                           in, un, sums, T, mode, w.queue + 1, nullptr);
-  }
-  return check_cuda(cudaGetLastError(), "pixelbox launch");
+  if (int r = check_cuda(cudaGetLastError(), "pixelbox small launch")) return r;
+  return launch_large(Ps, Qs, pr, n, w.large_list, w.large_count, in, un, sums, T, mode, counters, w.large_ws,
+                      w.large_bytes, stream);
 }
 
 }  // namespace sccg
