@@ -308,159 +308,6 @@ __global__ void __launch_bounds__(kPrepThreads) prep_kernel(const int2* __restri
   }
 }
 
-// Group variant: an 8-lane group per ring, vertices read coalesced straight
-// from global memory (no shared-memory staging, so occupancy is not bounded
-// by tile size); the next vertex comes from the neighbouring lane, MBR and area
-// are group reductions, vertical-edge records are compacted with the group's
-// ballot bits.  Loops are warp-uniform (trip count = the warp's largest ring).
-constexpr int kGroup = 8;
-
-__global__ void __launch_bounds__(256) prep_group_kernel(const int2* __restrict__ xy, const int64_t* __restrict__ off,
-                                                         int64_t n, int64_t nv_total, int4* __restrict__ mbr,
-                                                         int64_t* __restrict__ area, int2* __restrict__ ecount,
-                                                         uint64_t* __restrict__ edges, uint32_t* __restrict__ status,
-                                                         SetStats* stats, int validate) {
-  __shared__ unsigned long long s_acc[4];
-  __shared__ int s_b[6];
-  const int lane = threadIdx.x & 31, sub = lane & (kGroup - 1), grp = lane >> 3;
-  const int gbase = grp * kGroup;
-  const unsigned below = (1u << sub) - 1u;
-  StatAcc acc;
-  acc.init();
-  const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
-  for (int64_t w0 = warp * 4; w0 < n; w0 += nwarps * 4) {
-    const int64_t poly = w0 + grp;
-    const bool valid = poly < n;
-    int64_t b = 0, e = 0;
-    if (valid) {
-      b = off[poly];
-      e = off[poly + 1];
-    }
-    const bool bad = valid && (b < 0 || e > nv_total || e - b < 4);  // malformed offsets / < 4 vertices
-    const int V = (valid && !bad) ? (int)min(e - b, (int64_t)INT_MAX) : 0;
-    if (bad && sub == 0) {
-      mbr[poly] = make_int4(0, 0, 0, 0);
-      area[poly] = 0;
-      ecount[poly] = make_int2(0, 0);
-      flag(status, SCCG_STATUS_ARG, poly);
-    }
-    const int itmax = __reduce_max_sync(0xffffffffu, (V + kGroup - 1) / kGroup);
-    // pass 1: MBR
-    int xmin = INT_MAX, ymin = INT_MAX, xmax = INT_MIN, ymax = INT_MIN;
-    for (int it = 0; it < itmax; it++) {
-      const int i = it * kGroup + sub;
-      if (i < V) {
-        const int2 a = __ldg(xy + b + i);
-        xmin = min(xmin, a.x);
-        xmax = max(xmax, a.x);
-        ymin = min(ymin, a.y);
-        ymax = max(ymax, a.y);
-      }
-    }
-#pragma unroll
-    for (int o = 1; o < kGroup; o <<= 1) {
-      xmin = min(xmin, __shfl_xor_sync(0xffffffffu, xmin, o));
-      xmax = max(xmax, __shfl_xor_sync(0xffffffffu, xmax, o));
-      ymin = min(ymin, __shfl_xor_sync(0xffffffffu, ymin, o));
-      ymax = max(ymax, __shfl_xor_sync(0xffffffffu, ymax, o));
-    }
-    const bool bad_range = V > 0 && ((int64_t)xmin < -kMaxCoord || (int64_t)xmax > kMaxCoord ||
-                                     (int64_t)ymin < -kMaxCoord || (int64_t)ymax > kMaxCoord ||
-                                     (int64_t)xmax - xmin > kMaxExtent || (int64_t)ymax - ymin > kMaxExtent);
-    const int Vw = bad_range ? 0 : V;  // ring to walk in pass 2
-    const int it2 = __reduce_max_sync(0xffffffffu, (Vw + kGroup - 1) / kGroup);
-    // pass 2: shoelace terms, validation, compacted vertical-edge records
-    int2 first = make_int2(0, 0);
-    if (Vw > 0 && sub == 0) first = __ldg(xy + b);
-    first.x = __shfl_sync(0xffffffffu, first.x, gbase);
-    first.y = __shfl_sync(0xffffffffu, first.y, gbase);
-    long long twice = 0;
-    bool diag = false;
-    int nvert = 0, nhor = 0;
-    for (int it = 0; it < it2; it++) {
-      const int i = it * kGroup + sub;
-      const bool act = i < Vw;
-      const int2 a = act ? __ldg(xy + b + i) : make_int2(0, 0);
-      int2 c;
-      c.x = __shfl_down_sync(0xffffffffu, a.x, 1);
-      c.y = __shfl_down_sync(0xffffffffu, a.y, 1);
-      if (act && (sub == kGroup - 1 || i + 1 == Vw)) c = (i + 1 == Vw) ? first : __ldg(xy + b + i + 1);
-      bool is_v = false, is_h = false;
-      uint64_t rec = 0;
-      if (act) {
-        const unsigned ax = (unsigned)(a.x - xmin), ay = (unsigned)(a.y - ymin);
-        const unsigned cx = (unsigned)(c.x - xmin), cy = (unsigned)(c.y - ymin);
-        twice += (long long)(ax * cy) - (long long)(cx * ay);  // one term per lane
-        is_v = ax == cx && ay != cy;
-        is_h = ay == cy && ax != cx;
-        diag |= ax != cx && ay != cy;
-        rec = pack_edge(ax, min(ay, cy), max(ay, cy));
-      }
-      const unsigned bv = (__ballot_sync(0xffffffffu, is_v) >> gbase) & 0xffu;
-      const unsigned bh = (__ballot_sync(0xffffffffu, is_h) >> gbase) & 0xffu;
-      if (is_v) edges[b + nvert + __popc(bv & below)] = rec;
-      nvert += __popc(bv);
-      nhor += __popc(bh);
-    }
-#pragma unroll
-    for (int o = 1; o < kGroup; o <<= 1) twice += __shfl_xor_sync(0xffffffffu, twice, o);
-    const bool gdiag = ((__ballot_sync(0xffffffffu, diag) >> gbase) & 0xffu) != 0;
-    if (valid && !bad && sub == 0) {
-      const int4 m = make_int4(xmin, ymin, xmax, ymax);
-      mbr[poly] = m;
-      if (bad_range) {
-        area[poly] = 0;
-        ecount[poly] = make_int2(0, 0);
-        flag(status, SCCG_STATUS_RANGE, poly);
-      } else {
-        area[poly] = (twice < 0 ? -twice : twice) / 2;
-        ecount[poly] = make_int2(nvert, nhor);
-        if (validate && gdiag) flag(status, SCCG_STATUS_NOT_RECTILINEAR, poly);
-      }
-      acc.add(m);
-    }
-  }
-  // block reduction of the statistics, then one atomic per field
-  if (threadIdx.x < 4) s_acc[threadIdx.x] = 0;
-  if (threadIdx.x == 0) {
-    s_b[0] = s_b[1] = INT_MAX;
-    s_b[2] = s_b[3] = INT_MIN;
-    s_b[4] = s_b[5] = 0;
-  }
-  __syncthreads();
-  unsigned long long v[4] = {acc.nonempty, acc.sw, acc.sh, acc.swh};
-  for (int f = 0; f < 4; f++) {
-    unsigned long long x = v[f];
-    for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-    if (lane == 0 && x) atomicAdd(&s_acc[f], x);
-  }
-  const int bx0 = __reduce_min_sync(0xffffffffu, acc.bx0), by0 = __reduce_min_sync(0xffffffffu, acc.by0);
-  const int bx1 = __reduce_max_sync(0xffffffffu, acc.bx1), by1 = __reduce_max_sync(0xffffffffu, acc.by1);
-  const int mw = __reduce_max_sync(0xffffffffu, acc.mw), mh = __reduce_max_sync(0xffffffffu, acc.mh);
-  if (lane == 0) {
-    atomicMin(&s_b[0], bx0);
-    atomicMin(&s_b[1], by0);
-    atomicMax(&s_b[2], bx1);
-    atomicMax(&s_b[3], by1);
-    atomicMax(&s_b[4], mw);
-    atomicMax(&s_b[5], mh);
-  }
-  __syncthreads();
-  if (threadIdx.x == 0 && s_acc[0]) {
-    atomicAdd(&stats->nonempty, s_acc[0]);
-    atomicAdd(&stats->sw, s_acc[1]);
-    atomicAdd(&stats->sh, s_acc[2]);
-    atomicAdd(&stats->swh, s_acc[3]);
-    atomicMin(&stats->bounds[0], s_b[0]);
-    atomicMin(&stats->bounds[1], s_b[1]);
-    atomicMax(&stats->bounds[2], s_b[2]);
-    atomicMax(&stats->bounds[3], s_b[3]);
-    atomicMax(&stats->maxext[0], s_b[4]);
-    atomicMax(&stats->maxext[1], s_b[5]);
-  }
-}
-
 __global__ void prep_init_kernel(uint32_t* status, SetStats* st) {
   if (threadIdx.x == 0) {
     status[0] = 0;
@@ -475,24 +322,6 @@ __global__ void prep_init_kernel(uint32_t* status, SetStats* st) {
 cudaError_t launch_prep(const sccg_polyset* s, int validate, cudaStream_t st) {
   SetStats* stats = reinterpret_cast<SetStats*>(s->stats);
   prep_init_kernel<<<1, 32, 0, st>>>(s->status, stats);
-#ifndef SCCG_PREP_TILED
-  if (s->n_polygons > 0) {
-    static int sms = 0, per_sm = 1;
-    if (sms == 0) {
-      int dev = 0;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, prep_group_kernel, 256, 0);
-    }
-    const int64_t need = (s->n_polygons + 31) / 32;  // 32 rings per 256-thread CTA
-    const int64_t blocks = min(need, (int64_t)sms * max(per_sm, 1));
-    prep_group_kernel<<<(unsigned)max(blocks, (int64_t)1), 256, 0, st>>>(
-        reinterpret_cast<const int2*>(s->xy), s->offsets, s->n_polygons, s->n_vertices,
-        reinterpret_cast<int4*>(s->mbr), s->area, reinterpret_cast<int2*>(s->ecount), s->edges, s->status, stats,
-        validate);
-  }
-  return cudaGetLastError();
-#endif
   if (s->n_polygons > 0) {
     static cudaError_t attr = cudaFuncSetAttribute(prep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                    (int)(kPrepVerts * sizeof(int2)));
