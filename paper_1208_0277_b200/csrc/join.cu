@@ -45,35 +45,47 @@ __device__ __forceinline__ void set_entries(const SetStats* s, int k, double& bo
 // exceeds the largest MBR extent each MBR covers at most 2 x 2 cells.
 __global__ void grid_select_kernel(const SetStats* __restrict__ sp, const SetStats* __restrict__ sq, long long ccap,
                                    long long ecap, Grid* g) {
-  if (threadIdx.x != 0) return;
-  Grid r{30, 0, 0, 1, 1, 0};
-  if (sp->nonempty == 0 || sq->nonempty == 0) {
-    r.empty = 1;
-    *g = r;
-    return;
-  }
+  // one warp: lane j evaluates k = 3 + j (k <= 30), then an argmin over lanes
+  const int lane = threadIdx.x & 31;
+  if (threadIdx.x >= 32) return;
+  const bool empty = sp->nonempty == 0 || sq->nonempty == 0;
   const int xmin = min(sp->bounds[0], sq->bounds[0]), ymin = min(sp->bounds[1], sq->bounds[1]);
   const int xmax = max(sp->bounds[2], sq->bounds[2]), ymax = max(sp->bounds[3], sq->bounds[3]);
-  double best = 1e300;
-  for (int k = 3; k <= 30; k++) {
+  const int k = 3 + lane;
+  double cost = 1e300;
+  if (!empty && k <= 30) {
     const double ncx = (double)(((xmax - 1) >> k) - (xmin >> k) + 1);
     const double ncy = (double)(((ymax - 1) >> k) - (ymin >> k) + 1);
     const double C = ncx * ncy;
     double bp, ep, bq, eq;
     set_entries(sp, k, bp, ep);
     set_entries(sq, k, bq, eq);
-    if (C > (double)ccap || bq > (double)ecap) continue;
-    const double cost = ep + eq + 0.25 * C + ep * eq / C;
-    if (cost < best) {
-      best = cost;
-      r.k = k;
+    if (C <= (double)ccap && bq <= (double)ecap) cost = ep + eq + 0.25 * C + ep * eq / C;
+  }
+  // argmin (ties -> smaller k); k = 30 is always feasible
+  int best = k <= 30 ? k : 30;
+  double bc = cost;
+  for (int o = 16; o; o >>= 1) {
+    const double oc = __shfl_xor_sync(0xffffffffu, bc, o);
+    const int ok = __shfl_xor_sync(0xffffffffu, best, o);
+    if (oc < bc || (oc == bc && ok < best)) {
+      bc = oc;
+      best = ok;
     }
   }
-  r.cx0 = xmin >> r.k;
-  r.cy0 = ymin >> r.k;
-  r.ncx = ((xmax - 1) >> r.k) - r.cx0 + 1;
-  r.ncy = ((ymax - 1) >> r.k) - r.cy0 + 1;
-  *g = r;
+  if (lane == 0) {
+    Grid r{30, 0, 0, 1, 1, 0};
+    if (empty) {
+      r.empty = 1;
+    } else {
+      r.k = bc < 1e300 ? best : 30;
+      r.cx0 = xmin >> r.k;
+      r.cy0 = ymin >> r.k;
+      r.ncx = ((xmax - 1) >> r.k) - r.cx0 + 1;
+      r.ncy = ((ymax - 1) >> r.k) - r.cy0 + 1;
+    }
+    *g = r;
+  }
 }
 
 __global__ void grid_count_kernel(const int4* __restrict__ mq, int64_t nq, const Grid* __restrict__ gp,
@@ -184,11 +196,14 @@ size_t filter_ws_bytes(int64_t np, int64_t nq) {
 }
 
 static int blocks_for(int64_t n, int threads) {
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  static int sms = 0;
+  if (sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
   int64_t b = (n + threads - 1) / threads;
-  const int64_t cap = (int64_t)sms * 8;
+  const int64_t cap = (int64_t)sms * (2048 / threads);  // a full SM of threads (these kernels are latency-bound)
   if (b > cap) b = cap;
   return (int)(b < 1 ? 1 : b);
 }

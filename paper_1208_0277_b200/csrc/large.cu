@@ -3,11 +3,12 @@
 //
 // Every pair the small kernel cannot take (root box wider or taller than 32,
 // |box| >= T, or rings with more than 64 vertical edges) lands here.
-//  1. expand_kernel: the pair's root box MBR(p) n MBR(q) (reading R5) is cut
-//     into up to 32 x 32 disjoint regions of about 128 x 128 pixels -- the
-//     "huge-pair split into region work items" of SURVEY §8 a3 -- so one large
-//     pair is spread over many warps (the paper gives a whole pair to one
-//     block, which leaves a few big pairs on a few SMs).
+//  1. (in the small kernel, emit_large) the pair's root box MBR(p) n MBR(q)
+//     (reading R5) is cut into up to 32 x 32 disjoint regions of about
+//     128 x 128 pixels -- the "huge-pair split into region work items" of
+//     so one large pair is spread over many warps (the paper
+//     gives a whole pair to one block, which leaves a few big pairs on
+//     a few SMs).
 //  2. item_kernel: a warp takes one item (pair, region R) from a global queue:
 //     - it culls both polygons' edges to those meeting R (vertical edges with
 //       x strictly inside R's columns, horizontal edges strictly inside R's
@@ -22,11 +23,11 @@
 //     - boxes below T are pixelized bit-parallel (a lane owns a 32-pixel row
 //       word: row parity at the box's left column, then one suffix mask per
 //       local vertical edge);
-//     - the item's pixel count is added into the pair's int64 accumulator.
+//     - the item's pixel count is added into the pair's int64 accumulator;
+//       the warp finishing a pair's last item finalizes the pair: U = |p| +
+//       |q| - I, the outputs, the exact totals (reading R12).
 //     An item whose local lists overflow shared memory is split in two and
 //     retried (in the same warp), so any input is handled.
-//  3. large_epilogue_kernel: per pair, U = |p| + |q| - I, the
-//     outputs, and the exact batch totals (reading R12).
 // Regions are disjoint and cover the root box exactly, so the per-pair sums are
 // exact and independent of the split (integer atomics are order-free).
 #include "pixelbox_common.cuh"
@@ -38,9 +39,6 @@ constexpr int kLCap = 192;          // local records per list (vertical / horizo
 constexpr int kLStage = 96;         // staged records per polygon for one pixelized box
 constexpr int kLStack = 256;        // sampling boxes per warp stack
 constexpr int kLItems = 48;         // in-warp item stack (overflow splits)
-constexpr int kRegion = 128;        // target region side
-constexpr int kMaxSplit = 32;       // regions per axis at most
-constexpr int kMaxRegion = 32766;   // local coordinates are 15-bit (plus clamp margin)
 
 struct PolyRef {
   const uint64_t* ev;  // vertical records (relative to the polygon MBR origin)
@@ -329,44 +327,9 @@ __device__ long long region_pixelbox(const LocalPoly& P, const LocalPoly& Q, int
 }
 
 // ------------------------------------------------------------------ kernels
-// item: pair slot i (32 bit; 0xffffffff = no-op) | rx | ry | nx | ny (8 bit each)
-__device__ __forceinline__ uint64_t pack_item(unsigned i, int rx, int ry, int nx, int ny) {
-  return (uint64_t)i | ((uint64_t)rx << 32) | ((uint64_t)ry << 40) | ((uint64_t)nx << 48) | ((uint64_t)ny << 56);
-}
-
-struct LargeWs {
-  unsigned long long* ctr;  // [0] item queue, [1] extra item count
-  long long* acc;           // [n_cap] per large pair pixel count
-  uint64_t* items;          // [n_cap + extra_cap]
-  long long extra_cap;
-};
-
 __device__ __forceinline__ int4 root_box(const DevSet& Ps, const DevSet& Qs, int2 pq) {
   const int4 mp = Ps.mbr[pq.x], mq = Qs.mbr[pq.y];
   return make_int4(max(mp.x, mq.x), max(mp.y, mq.y), min(mp.z, mq.z), min(mp.w, mq.w));
-}
-
-__global__ void expand_kernel(DevSet Ps, DevSet Qs, const int2* __restrict__ pairs, const long long* __restrict__ list,
-                              const unsigned* __restrict__ count, long long n_cap, LargeWs w) {
-  const long long n = min((long long)*count, n_cap);
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-    const int4 rb = root_box(Ps, Qs, pairs[list[i]]);
-    const int W = rb.z - rb.x, H = rb.w - rb.y;
-    int nx = min(kMaxSplit, max((W + kRegion - 1) / kRegion, (W + kMaxRegion - 1) / kMaxRegion));
-    int ny = min(kMaxSplit, max((H + kRegion - 1) / kRegion, (H + kMaxRegion - 1) / kMaxRegion));
-    w.acc[i] = 0;
-    const int extra = nx * ny - 1;
-    if (extra > 0) {
-      const long long base = (long long)atomicAdd(&w.ctr[1], (unsigned long long)extra);
-      if (base + extra <= w.extra_cap) {
-        for (int r = 1; r <= extra; r++) w.items[n_cap + base + r - 1] = pack_item((unsigned)i, r % nx, r / nx, nx, ny);
-      } else {  // out of item space: this pair is one item (split in-warp on overflow)
-        for (long long t = base; t < w.extra_cap; t++) w.items[n_cap + t] = pack_item(0xffffffffu, 0, 0, 1, 1);
-        nx = ny = 1;
-      }
-    }
-    w.items[i] = pack_item((unsigned)i, 0, 0, nx, ny);
-  }
 }
 
 constexpr size_t kLSmemPerWarp = (size_t)4 * kLCap * sizeof(uint64_t) + (size_t)2 * kLStage * sizeof(int4) +
@@ -376,9 +339,8 @@ constexpr size_t kLSmem = kLWarps * kLSmemPerWarp;
 
 template <bool COUNT>
 __global__ void __launch_bounds__(kLWarps * 32)
-    item_kernel(DevSet Ps, DevSet Qs, const int2* __restrict__ pairs, const long long* __restrict__ list,
-                const unsigned* __restrict__ count, long long n_cap, LargeWs w, int T, int mode, long long* counters,
-                sccg_sums* sums) {
+    item_kernel(DevSet Ps, DevSet Qs, const int2* __restrict__ pairs, LargeWs w, int T, int mode,
+                long long* __restrict__ inter, long long* __restrict__ uni, long long* counters, sccg_sums* sums) {
   extern __shared__ __align__(16) unsigned char s_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   unsigned char* base = s_raw + (size_t)warp * kLSmemPerWarp;
@@ -391,10 +353,13 @@ __global__ void __launch_bounds__(kLWarps * 32)
   int* sh = reinterpret_cast<int*>(sv + 2 * kLStage);
   uint64_t* stk = reinterpret_cast<uint64_t*>(sh + 2 * kLStage);
   int4* istk = reinterpret_cast<int4*>(stk + kLStack);
-  const long long nl = min((long long)*count, n_cap);
+  const long long n_cap = w.n_cap;
+  const long long nl = min((long long)(w.ctr[2] & 0xffffffffull), n_cap);
   const long long ne = min((long long)w.ctr[1], w.extra_cap);
   const long long total = nl + ne;
   unsigned status = 0;
+  // batch totals of the pairs this warp finalizes (lane 0)
+  unsigned long long a_n = 0, a_nz = 0, a_i = 0, a_u = 0, a_ap = 0, a_aq = 0, l0 = 0, l1 = 0, l2 = 0, l3 = 0, rootpx = 0;
   for (;;) {
     unsigned long long t = 0;
     if (lane == 0) t = atomicAdd(&w.ctr[0], 1ull);
@@ -405,7 +370,8 @@ __global__ void __launch_bounds__(kLWarps * 32)
     if (i == 0xffffffffu) continue;
     const int rx = (int)((it >> 32) & 0xff), ry = (int)((it >> 40) & 0xff);
     const int nx = (int)((it >> 48) & 0xff), ny = (int)((it >> 56) & 0xff);
-    const int2 pq = pairs[list[i]];
+    const long long k = w.list[i];
+    const int2 pq = pairs[k];
     const int4 rb = root_box(Ps, Qs, pq);
     const int W = rb.z - rb.x, H = rb.w - rb.y;
     PolyRef pr[2];
@@ -466,73 +432,57 @@ __global__ void __launch_bounds__(kLWarps * 32)
       __syncwarp();
     }
     acc = (long long)warp_sum_u64((unsigned long long)acc);
-    if (lane == 0) atomicAdd(reinterpret_cast<unsigned long long*>(&w.acc[i]), (unsigned long long)acc);
+    if (lane == 0) {
+      atomicAdd(reinterpret_cast<unsigned long long*>(&w.acc[i]), (unsigned long long)acc);
+      __threadfence();
+      if (atomicSub(&w.rem[i], 1u) == 1u) {  // last region of the pair: finalize it
+        __threadfence();
+        const long long I = (long long)atomicAdd(reinterpret_cast<unsigned long long*>(&w.acc[i]), 0ull);
+        const long long ap = Ps.area[pq.x], aq = Qs.area[pq.y];
+        const long long U = ap + aq - I;  // indirect union
+        if (inter) inter[k] = I;
+        if (uni) uni[k] = U;
+        a_n++;
+        a_i += I;
+        a_ap += ap;
+        a_aq += aq;
+        if (I != 0) {
+          unsigned long long b0, b1, b2, b3;
+          ratio_limbs(I, U, b0, b1, b2, b3);
+          a_nz++;
+          a_u += U;
+          l0 += b0;
+          l1 += b1;
+          l2 += b2;
+          l3 += b3;
+        }
+        if (COUNT) rootpx += (unsigned long long)W * H;
+      }
+    }
   }
   status = __reduce_or_sync(FULL, status);
-  if (lane == 0 && status) atomicOr(reinterpret_cast<unsigned long long*>(&sums->status), (unsigned long long)status);
-}
-
-template <bool COUNT>
-__global__ void __launch_bounds__(256) large_epilogue_kernel(DevSet Ps, DevSet Qs, const int2* __restrict__ pairs,
-                                                             const long long* __restrict__ list,
-                                                             const unsigned* __restrict__ count, long long n_cap,
-                                                             LargeWs w, long long* __restrict__ inter,
-                                                             long long* __restrict__ uni, sccg_sums* sums,
-                                                             long long* counters) {
-  __shared__ unsigned long long s_acc[10];
-  if (threadIdx.x < 10) s_acc[threadIdx.x] = 0;
-  __syncthreads();
-  const long long n = min((long long)*count, n_cap);
-  unsigned long long a[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
-  unsigned long long rootpx = 0;
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-    const long long k = list[i];
-    const int2 pq = pairs[k];
-    const long long I = w.acc[i];
-    const long long ap = Ps.area[pq.x], aq = Qs.area[pq.y];
-    const long long U = ap + aq - I;  // indirect union
-    if (inter) inter[k] = I;
-    if (uni) uni[k] = U;
-    a[0]++;
-    a[2] += I;
-    a[4] += ap;
-    a[5] += aq;
-    if (I != 0) {
-      unsigned long long l0, l1, l2, l3;
-      ratio_limbs(I, U, l0, l1, l2, l3);
-      a[1]++;
-      a[3] += U;
-      a[6] += l0;
-      a[7] += l1;
-      a[8] += l2;
-      a[9] += l3;
-    }
-    if (COUNT) {
-      const int4 rb = root_box(Ps, Qs, pq);
-      rootpx += (unsigned long long)(rb.z - rb.x) * (rb.w - rb.y);
-    }
+  if (lane == 0) {
+    if (status) atomicOr(reinterpret_cast<unsigned long long*>(&sums->status), (unsigned long long)status);
+    unsigned long long* d = reinterpret_cast<unsigned long long*>(sums);
+    const unsigned long long v[10] = {a_n, a_nz, a_i, a_u, a_ap, a_aq, l0, l1, l2, l3};
+    for (int f = 0; f < 10; f++)
+      if (v[f]) atomicAdd(d + f, v[f]);
+    if (COUNT && rootpx) atomicAdd((unsigned long long*)&counters[SCCG_CNT_ROOTPX], rootpx);
   }
-  for (int f = 0; f < 10; f++) {
-    const unsigned long long v = warp_sum_u64(a[f]);
-    if ((threadIdx.x & 31) == 0 && v) atomicAdd(&s_acc[f], v);
-  }
-  if (COUNT) {
-    const unsigned long long v = warp_sum_u64(rootpx);
-    if ((threadIdx.x & 31) == 0 && v) atomicAdd((unsigned long long*)&counters[SCCG_CNT_ROOTPX], v);
-  }
-  __syncthreads();
-  if (threadIdx.x < 10 && s_acc[threadIdx.x])
-    atomicAdd(reinterpret_cast<unsigned long long*>(sums) + threadIdx.x, s_acc[threadIdx.x]);
 }
 
 // ---------------------------------------------------------------------- host
 static long long extra_cap_for(long long n_cap) { return 4 * n_cap + 65536; }
 
 static size_t large_layout(long long n_cap, Carve& cv, LargeWs& w) {
+  const long long n = n_cap > 0 ? n_cap : 1;
   w.ctr = cv.take<unsigned long long>(4);
-  w.acc = cv.take<long long>(n_cap > 0 ? n_cap : 1);
+  w.list = cv.take<long long>(n);
+  w.acc = cv.take<long long>(n);
+  w.rem = cv.take<unsigned>(n);
+  w.n_cap = n_cap;
   w.extra_cap = extra_cap_for(n_cap);
-  w.items = cv.take<uint64_t>(n_cap + w.extra_cap);
+  w.items = cv.take<uint64_t>(n + w.extra_cap);
   return cv.used;
 }
 
@@ -542,13 +492,16 @@ size_t large_ws_bytes(long long n_cap) {
   return large_layout(n_cap, cv, w) + 256;
 }
 
-int launch_large(const DevSet& Ps, const DevSet& Qs, const int2* pairs, long long n_cap, const long long* large_list,
-                 const unsigned* large_count, long long* inter, long long* uni, sccg_sums* sums, int T, int mode,
-                 long long* counters, void* ws, size_t ws_bytes, cudaStream_t stream) {
+LargeWs large_ws(long long n_cap, void* ws, size_t ws_bytes, bool& ok) {
   Carve cv{reinterpret_cast<char*>(ws), ws_bytes};
   LargeWs w;
   large_layout(n_cap, cv, w);
-  if (!cv.ok) return set_error(SCCG_E_WORKSPACE, "pixelbox (large) workspace too small");
+  ok = cv.ok && ws != nullptr;
+  return w;
+}
+
+int launch_large(const DevSet& Ps, const DevSet& Qs, const int2* pairs, const LargeWs& w, long long* inter,
+                 long long* uni, sccg_sums* sums, int T, int mode, long long* counters, cudaStream_t stream) {
   static cudaError_t attr = [] {
     cudaError_t e = cudaFuncSetAttribute(item_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kLSmem);
     if (e == cudaSuccess)
@@ -565,21 +518,11 @@ int launch_large(const DevSet& Ps, const DevSet& Qs, const int2* pairs, long lon
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[1], item_kernel<true>, kLWarps * 32, kLSmem);
   }
   const bool count = counters != nullptr;
-  cudaMemsetAsync(w.ctr, 0, 4 * sizeof(unsigned long long), stream);
-  const long long eb = min((long long)sms * 8, (n_cap + 255) / 256);
-  expand_kernel<<<(unsigned)max(eb, 1ll), 256, 0, stream>>>(Ps, Qs, pairs, large_list, large_count, n_cap, w);
   const unsigned ib = (unsigned)(sms * max(per_sm[count], 1));
-  if (count) {
-    item_kernel<true><<<ib, kLWarps * 32, kLSmem, stream>>>(Ps, Qs, pairs, large_list, large_count, n_cap, w, T, mode,
-                                                          counters, sums);
-    large_epilogue_kernel<true><<<(unsigned)max(eb, 1ll), 256, 0, stream>>>(Ps, Qs, pairs, large_list, large_count,
-                                                                             n_cap, w, inter, uni, sums, counters);
-  } else {
-    item_kernel<false><<<ib, kLWarps * 32, kLSmem, stream>>>(Ps, Qs, pairs, large_list, large_count, n_cap, w, T,
-                                                           mode, nullptr, sums);
-    large_epilogue_kernel<false><<<(unsigned)max(eb, 1ll), 256, 0, stream>>>(Ps, Qs, pairs, large_list, large_count,
-                                                                              n_cap, w, inter, uni, sums, nullptr);
-  }
+  if (count)
+    item_kernel<true><<<ib, kLWarps * 32, kLSmem, stream>>>(Ps, Qs, pairs, w, T, mode, inter, uni, counters, sums);
+  else
+    item_kernel<false><<<ib, kLWarps * 32, kLSmem, stream>>>(Ps, Qs, pairs, w, T, mode, inter, uni, nullptr, sums);
   return check_cuda(cudaGetLastError(), "pixelbox large launch");
 }
 

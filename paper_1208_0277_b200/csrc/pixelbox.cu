@@ -98,7 +98,7 @@ __global__ void __launch_bounds__(kSmallWarps * 32, SCCG_SMALL_MINB)
     small_kernel(DevSet Ps, DevSet Qs, const int2* __restrict__ pairs, long long n_cap,
                  const long long* __restrict__ dev_result, long long* __restrict__ inter,
                  long long* __restrict__ uni, sccg_sums* sums, int T, int mode, unsigned long long* queue,
-                 long long* __restrict__ large_list, unsigned* large_count, long long* counters, long long np_,
+                 LargeWs lw, long long* counters, long long np_,
                  long long nq_) {
   // pair count: host-given, or (async path) the filter's device-side count clamped to the buffer
   const long long n = dev_result ? min(dev_result[0], n_cap) : n_cap;
@@ -125,6 +125,7 @@ __global__ void __launch_bounds__(kSmallWarps * 32, SCCG_SMALL_MINB)
     // ---- lane-parallel metadata of pair k0 + lane
     bool ok = false, small = false, empty = false;
     int2 pq = make_int2(0, 0);
+    int W = 0, H = 0;
     if (k < n) {
       pq = pairs[k];
       ok = (unsigned)pq.x < (unsigned long long)np_ && (unsigned)pq.y < (unsigned long long)nq_;
@@ -135,7 +136,8 @@ __global__ void __launch_bounds__(kSmallWarps * 32, SCCG_SMALL_MINB)
       const int2 cp = Ps.ecount[pq.x], cq = Qs.ecount[pq.y];
       const long long op = Ps.off[pq.x], oq = Qs.off[pq.y];
       const int bx0 = max(mp.x, mq.x), by0 = max(mp.y, mq.y);
-      const int W = min(mp.z, mq.z) - bx0, H = min(mp.w, mq.w) - by0;
+      W = min(mp.z, mq.z) - bx0;
+      H = min(mp.w, mq.w) - by0;
       const int dxp = mp.x - bx0, dyp = mp.y - by0, dxq = mq.x - bx0, dyq = mq.y - by0;
       empty = !(W > 0 && H > 0);  // reading R18: I = 0
       small = !empty && W <= 32 && H <= 32 && (mode == 1 || W * H < T) && cp.x <= kSmallCap && cq.x <= kSmallCap &&
@@ -151,9 +153,9 @@ __global__ void __launch_bounds__(kSmallWarps * 32, SCCG_SMALL_MINB)
     const unsigned lb = __ballot_sync(FULL, large);
     if (lb) {
       unsigned base = 0;
-      if (lane == 0) base = atomicAdd(large_count, (unsigned)__popc(lb));
+      if (lane == 0) base = (unsigned)atomicAdd(&lw.ctr[2], (unsigned long long)__popc(lb));
       base = __shfl_sync(FULL, base, 0);
-      if (large) large_list[base + __popc(lb & lanemask_lt())] = k;
+      if (large) emit_large(lw, base + __popc(lb & lanemask_lt()), k, W, H);
     }
     // ---- small pairs, software-pipelined: records of the next pair are in
     // flight into registers while the current pair is pixelized
@@ -276,18 +278,14 @@ __global__ void __launch_bounds__(kSmallWarps * 32, SCCG_SMALL_MINB)
 // ---------------------------------------------------------------------- host
 struct PixelboxWs {
   unsigned long long* queue;  // small-kernel queue
-  unsigned* large_count;
-  long long* large_list;
-  void* large_ws;
+  void* large;
   size_t large_bytes;
 };
 
 static size_t pixelbox_layout(int64_t n, Carve& cv, PixelboxWs& w) {
   w.queue = cv.take<unsigned long long>(4);
-  w.large_count = reinterpret_cast<unsigned*>(w.queue + 2);
-  w.large_list = cv.take<long long>(n > 0 ? n : 1);
   w.large_bytes = large_ws_bytes(n);
-  w.large_ws = cv.take<char>(w.large_bytes);
+  w.large = cv.take<char>(w.large_bytes);
   return cv.used;
 }
 
@@ -308,7 +306,11 @@ int run_pixelbox(const sccg_polyset* p, const sccg_polyset* q, const int32_t* pa
   const int mode = cfg ? cfg->mode : 0;
   if (T < 2) T = 2;
   if (mode != 0 && mode != 1) return set_error(SCCG_E_ARG, "config.mode must be 0 (PixelBox) or 1 (PixelOnly)");
+  bool lok = true;
+  const LargeWs lw = large_ws(n, w.large, w.large_bytes, lok);
+  if (!lok) return set_error(SCCG_E_WORKSPACE, "pixelbox (large) workspace too small");
   cudaMemsetAsync(w.queue, 0, 4 * sizeof(unsigned long long), stream);
+  cudaMemsetAsync(lw.ctr, 0, 4 * sizeof(unsigned long long), stream);
   if (n == 0) return check_cuda(cudaGetLastError(), "pixelbox");
   const bool count = cfg && cfg->counters;
   long long* counters = count ? reinterpret_cast<long long*>(cfg->counters) : nullptr;
@@ -331,15 +333,14 @@ int run_pixelbox(const sccg_polyset* p, const sccg_polyset* q, const int32_t* pa
   const long long* dr = reinterpret_cast<const long long*>(dev_result);
   if (count)
     small_kernel<true><<<(unsigned)grid_s, kSmallWarps * 32, 0, stream>>>(
-        Ps, Qs, pr, n, dr, in, un, sums, T, mode, w.queue, w.large_list, w.large_count, counters, p->n_polygons,
+        Ps, Qs, pr, n, dr, in, un, sums, T, mode, w.queue, lw, counters, p->n_polygons,
         q->n_polygons);
   else
     small_kernel<false><<<(unsigned)grid_s, kSmallWarps * 32, 0, stream>>>(
-        Ps, Qs, pr, n, dr, in, un, sums, T, mode, w.queue, w.large_list, w.large_count, nullptr, p->n_polygons,
+        Ps, Qs, pr, n, dr, in, un, sums, T, mode, w.queue, lw, nullptr, p->n_polygons,
         q->n_polygons);
   if (int r = check_cuda(cudaGetLastError(), "pixelbox small launch")) return r;
-  return launch_large(Ps, Qs, pr, n, w.large_list, w.large_count, in, un, sums, T, mode, counters, w.large_ws,
-                      w.large_bytes, stream);
+  return launch_large(Ps, Qs, pr, lw, in, un, sums, T, mode, counters, stream);
 }
 
 }  // namespace sccg

@@ -75,11 +75,55 @@ __device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long v)
   return v;
 }
 
-// PixelBox over the pairs the small kernel routed to the large path
-// (large.cu): region work items with local edge culling.
-int launch_large(const DevSet& Ps, const DevSet& Qs, const int2* pairs, long long n_cap, const long long* large_list,
-                 const unsigned* large_count, long long* inter, long long* uni, sccg_sums* sums, int T, int mode,
-                 long long* counters, void* ws, size_t ws_bytes, cudaStream_t stream);
+// ---------------------------------------------------------- large-pair items
+// A pair routed to the large path (large.cu) is cut into region work items
+// (SURVEY §8 a3): its root box is split into nx x ny regions of about
+// kRegion pixels per side.  Slot i of `items` (i = the pair's index in the
+// large list) always holds region 0; the other regions are appended after
+// n_cap.  rem[i] counts the pair's unfinished items; acc[i] accumulates its
+// pixel count.
+constexpr int kRegion = 128;       // target region side
+constexpr int kMaxSplit = 32;      // regions per axis at most
+constexpr int kMaxRegion = 32766;  // local coordinates are 15-bit (plus clamp margin)
+
+struct LargeWs {
+  unsigned long long* ctr;  // [0] item queue, [1] extra item count, [2] large-pair count (low 32 bits)
+  long long* list;          // [n_cap] pair index of large pair i
+  long long* acc;           // [n_cap] pixel count of large pair i
+  unsigned* rem;            // [n_cap] items of pair i not yet finished
+  uint64_t* items;          // [n_cap + extra_cap]
+  long long n_cap, extra_cap;
+};
+
+// item: pair slot i (32 bit; 0xffffffff = no-op) | rx | ry | nx | ny (8 bit each)
+__device__ __forceinline__ uint64_t pack_item(unsigned i, int rx, int ry, int nx, int ny) {
+  return (uint64_t)i | ((uint64_t)rx << 32) | ((uint64_t)ry << 40) | ((uint64_t)nx << 48) | ((uint64_t)ny << 56);
+}
+
+// Register large pair i (pair index k, root box W x H) and its region items.
+__device__ __forceinline__ void emit_large(const LargeWs& w, unsigned i, long long k, int W, int H) {
+  int nx = min(kMaxSplit, max((W + kRegion - 1) / kRegion, (W + kMaxRegion - 1) / kMaxRegion));
+  int ny = min(kMaxSplit, max((H + kRegion - 1) / kRegion, (H + kMaxRegion - 1) / kMaxRegion));
+  w.list[i] = k;
+  w.acc[i] = 0;
+  const int extra = nx * ny - 1;
+  if (extra > 0) {
+    const long long base = (long long)atomicAdd(&w.ctr[1], (unsigned long long)extra);
+    if (base + extra <= w.extra_cap) {
+      for (int r = 1; r <= extra; r++) w.items[w.n_cap + base + r - 1] = pack_item(i, r % nx, r / nx, nx, ny);
+    } else {  // out of item space: the pair is one item (split in-warp on overflow)
+      for (long long t = base; t < w.extra_cap; t++) w.items[w.n_cap + t] = pack_item(0xffffffffu, 0, 0, 1, 1);
+      nx = ny = 1;
+    }
+  }
+  w.rem[i] = (unsigned)(nx * ny);
+  w.items[i] = pack_item(i, 0, 0, nx, ny);
+}
+
 size_t large_ws_bytes(long long n_cap);
+LargeWs large_ws(long long n_cap, void* ws, size_t ws_bytes, bool& ok);
+// the region-item kernel over everything the small kernel routed to the large path
+int launch_large(const DevSet& Ps, const DevSet& Qs, const int2* pairs, const LargeWs& w, long long* inter,
+                 long long* uni, sccg_sums* sums, int T, int mode, long long* counters, cudaStream_t stream);
 
 }  // namespace sccg

@@ -326,10 +326,13 @@ cudaError_t launch_prep(const sccg_polyset* s, int validate, cudaStream_t st) {
     static cudaError_t attr = cudaFuncSetAttribute(prep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                    (int)(kPrepVerts * sizeof(int2)));
     if (attr != cudaSuccess) return attr;
-    int dev = 0, sms = 148, per_sm = 1;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, prep_kernel, kPrepThreads, kPrepVerts * sizeof(int2));
+    static int sms = 0, per_sm = 1;
+    if (sms == 0) {  // launch geometry, queried once per process
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, prep_kernel, kPrepThreads, kPrepVerts * sizeof(int2));
+    }
     const int64_t ntiles = (s->n_polygons + kPrepPolys - 1) / kPrepPolys;
     int64_t blocks = ntiles;
     const int64_t cap = (int64_t)sms * (per_sm > 0 ? per_sm : 1);
