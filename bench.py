@@ -133,9 +133,14 @@ def run_ours(args, rank, world, local_rank):
     import paper_1208_0277_b200 as sccg
     from paper_1208_0277_b200 import dist as sdist
 
+    local_rank = local_rank % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
-    sccg.load(build=(rank == 0))
+    if rank == 0:
+        sccg.load(build=True)  # rebuild only if stale; other ranks wait, then load
+    if world > 1:
+        dist.barrier()
+    sccg.load(build=False)
     A, B = make_workload(args.config, image=rank)
     xy_p = torch.from_numpy(A.xy).pin_memory()
     off_p = torch.from_numpy(A.offsets).pin_memory()
@@ -368,8 +373,14 @@ def main():
         import torch
         import torch.distributed as dist
 
-        torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        # NCCL over NVLink/NVSwitch; SCCG_DIST_BACKEND=gloo lets several ranks share one
+        # GPU for testing the multi-rank path (NCCL refuses two ranks on one device)
+        backend = os.environ.get("SCCG_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            torch.cuda.set_device(local_rank)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        else:
+            dist.init_process_group(backend)
     out = run_ours(args, rank, world, local_rank)
     if rank == 0:
         if not args.no_cpu_baseline:
