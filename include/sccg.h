@@ -145,8 +145,10 @@ typedef struct {
 
 typedef struct {
   int32_t threshold; /* T: boxes with fewer pixels are pixelized (Alg. 1 l.22); 0 = default */
-  int32_t mode;      /* 0 = PixelBox (sampling boxes + pixelization); 1 = PixelOnly (pixelize the
-                        whole root box, the §5.2 baseline) */
+  int32_t mode;      /* 0 = PixelBox (Alg. 1: sampling boxes + pixelization over MBR(p) n MBR(q), union
+                        from |p| + |q| - |p n q|); the paper's §5.2 baselines, which count the
+                        union directly over the box of MBR(p) u MBR(q): 1 = PixelOnly (pixelization
+                        only), 2 = PixelBox-NoSep (sampling boxes deciding both areas) */
   int32_t block;     /* threads per CTA (multiple of 32, <= 1024); 0 = default */
   int32_t grid;      /* CTAs; 0 = default (resident CTAs per SM x SM count) */
   int64_t* counters; /* optional device int64[8] (NULL = off): see SCCG_CNT_* */

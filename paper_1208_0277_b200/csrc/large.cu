@@ -238,23 +238,27 @@ __device__ __forceinline__ unsigned row_word_local(const LocalPoly& L, const int
   return m ^ (par ? FULL : 0u);
 }
 
+// Pixelization of box B (region coords): (|B n p n q|, |B n (p u q)|); the
+// union only when `uni` (modes 1 and 2 count it directly).
 template <bool COUNT>
-__device__ long long pixelize_local(const LocalPoly& P, const LocalPoly& Q, int x0, int y0, int x1, int y1, int pip,
-                                    int piq, int4* sv, int* sh, long long* counters) {
+__device__ longlong2 pixelize_local(const LocalPoly& P, const LocalPoly& Q, int x0, int y0, int x1, int y1, int pip,
+                                    int piq, bool uni, int4* sv, int* sh, long long* counters) {
   const int lane = threadIdx.x & 31;
   int nvp, nhp, nvq, nhq;
   stage_local(P, x0, y0, x1, y1, sv, sh, nvp, nhp);
   stage_local(Q, x0, y0, x1, y1, sv + kLStage, sh + kLStage, nvq, nhq);
   __syncwarp();
   const int Wb = x1 - x0, Hb = y1 - y0, nw = (Wb + 31) >> 5, nseg = Hb * nw;
-  long long acc = 0;
+  long long ai = 0, au = 0;
   for (int s0 = 0; s0 < nseg; s0 += 32) {
     const int s = s0 + lane;
     if (s < nseg) {
       const int row = s / nw, xs = (s - row * nw) << 5;
       const unsigned mp = row_word_local(P, sv, sh, nvp, nhp, x0, y0, x1, y1, pip, row, xs);
       const unsigned mq = row_word_local(Q, sv + kLStage, sh + kLStage, nvq, nhq, x0, y0, x1, y1, piq, row, xs);
-      acc += __popc(mp & mq & low_bits(Wb - xs));
+      const unsigned valid = low_bits(Wb - xs);
+      ai += __popc(mp & mq & valid);
+      if (uni) au += __popc((mp | mq) & valid);
     }
   }
   __syncwarp();
@@ -263,7 +267,7 @@ __device__ long long pixelize_local(const LocalPoly& P, const LocalPoly& Q, int 
     atomicAdd((unsigned long long*)&counters[SCCG_CNT_ROWTESTS], (unsigned long long)nseg * (nvp + nvq + nhp + nhq));
     atomicAdd((unsigned long long*)&counters[SCCG_CNT_PIXBOXES], 1ull);
   }
-  return acc;
+  return make_longlong2(ai, au);
 }
 
 // sampling-box stack entry: x0, y0, x1, y1 (15 bit each, region coords), parity bits of both polygons
@@ -273,12 +277,18 @@ __device__ __forceinline__ uint64_t pack_sb(int x0, int y0, int x1, int y1, int 
 }
 
 // Algorithm 1 on one region with local lists (DFS, warp-private stack).
+// mode 0 = PixelBox (intersection only; the union follows from the areas),
+// mode 1 = PixelOnly (pixelize the region, count both), mode 2 = PixelBox-NoSep
+// (§5.2: a box is decided only when both its intersection and union
+// contributions are).  Returns this lane's (I, U) share.
 template <bool COUNT>
-__device__ long long region_pixelbox(const LocalPoly& P, const LocalPoly& Q, int Wr, int Hr, int T, int mode,
+__device__ longlong2 region_pixelbox(const LocalPoly& P, const LocalPoly& Q, int Wr, int Hr, int T, int mode,
                                      uint64_t* stk, int4* sv, int* sh, long long* counters, unsigned& status) {
   const int lane = threadIdx.x & 31;
-  if (mode == 1 || (long long)Wr * Hr < T) return pixelize_local<COUNT>(P, Q, 0, 0, Wr, Hr, P.pi, Q.pi, sv, sh, counters);
-  long long acc = 0;
+  const bool uni = mode != 0;
+  if (mode == 1 || (long long)Wr * Hr < T)
+    return pixelize_local<COUNT>(P, Q, 0, 0, Wr, Hr, P.pi, Q.pi, uni, sv, sh, counters);
+  long long ai = 0, au = 0;
   if (lane == 0) stk[0] = pack_sb(0, 0, Wr, Hr, P.pi, Q.pi);
   int top = 1;
   __syncwarp();
@@ -291,7 +301,9 @@ __device__ long long region_pixelbox(const LocalPoly& P, const LocalPoly& Q, int
     const int pip = (int)((e >> 60) & 1), piq = (int)((e >> 61) & 1);
     const int Wb = x1 - x0, Hb = y1 - y0;
     if ((long long)Wb * Hb < T) {
-      acc += pixelize_local<COUNT>(P, Q, x0, y0, x1, y1, pip, piq, sv, sh, counters);
+      const longlong2 r = pixelize_local<COUNT>(P, Q, x0, y0, x1, y1, pip, piq, uni, sv, sh, counters);
+      ai += r.x;
+      au += r.y;
       continue;
     }
     const Split g = make_split(Wb, Hb);
@@ -302,11 +314,16 @@ __device__ long long region_pixelbox(const LocalPoly& P, const LocalPoly& Q, int
     const unsigned valid = __ballot_sync(FULL, cc < g.ncols && rr < g.nrows);
     const unsigned in_p = ~hp & pp, out_p = ~hp & ~pp, in_q = ~hq & pq, out_q = ~hq & ~pq;
     // BOXCONTRIBUTE / BOXCONTINUE (Alg. 1 l.33-35, reading R7)
-    const unsigned contrib = valid & in_p & in_q;
-    const unsigned cont = valid & ~(out_p | out_q) & ~contrib;
+    const unsigned i_dec = out_p | out_q | (in_p & in_q);
+    const unsigned u_dec = in_p | in_q | (out_p & out_q);
+    const unsigned cont = valid & ~(mode == 2 ? (i_dec & u_dec) : i_dec);
+    const unsigned contrib_i = valid & in_p & in_q & ~cont;
+    const unsigned contrib_u = valid & (in_p | in_q) & ~cont;
     const int sx0 = cc << g.lsx, sy0 = rr << g.lsy;
     const int sx1 = min(sx0 + (1 << g.lsx), Wb), sy1 = min(sy0 + (1 << g.lsy), Hb);
-    if ((contrib >> lane) & 1u) acc += (long long)(sx1 - sx0) * (sy1 - sy0);
+    const long long sz = (long long)(sx1 - sx0) * (sy1 - sy0);
+    if ((contrib_i >> lane) & 1u) ai += sz;
+    if (uni && ((contrib_u >> lane) & 1u)) au += sz;
     const int ncont = __popc(cont);
     if (COUNT && lane == 0) {
       atomicAdd((unsigned long long*)&counters[SCCG_CNT_BOXES], (unsigned long long)__popc(valid));
@@ -323,12 +340,15 @@ __device__ long long region_pixelbox(const LocalPoly& P, const LocalPoly& Q, int
     top += ncont;
     __syncwarp();
   }
-  return acc;
+  return make_longlong2(ai, au);
 }
 
 // ------------------------------------------------------------------ kernels
-__device__ __forceinline__ int4 root_box(const DevSet& Ps, const DevSet& Qs, int2 pq) {
+// mode 0: MBR(p) n MBR(q) (reading R5); modes 1, 2 count the union directly
+// over the bounding box of MBR(p) u MBR(q).
+__device__ __forceinline__ int4 root_box(const DevSet& Ps, const DevSet& Qs, int2 pq, int mode) {
   const int4 mp = Ps.mbr[pq.x], mq = Qs.mbr[pq.y];
+  if (mode != 0) return make_int4(min(mp.x, mq.x), min(mp.y, mq.y), max(mp.z, mq.z), max(mp.w, mq.w));
   return make_int4(max(mp.x, mq.x), max(mp.y, mq.y), min(mp.z, mq.z), min(mp.w, mq.w));
 }
 
@@ -372,7 +392,7 @@ __global__ void __launch_bounds__(kLWarps * 32)
     const int nx = (int)((it >> 48) & 0xff), ny = (int)((it >> 56) & 0xff);
     const long long k = w.list[i];
     const int2 pq = pairs[k];
-    const int4 rb = root_box(Ps, Qs, pq);
+    const int4 rb = root_box(Ps, Qs, pq, mode);
     const int W = rb.z - rb.x, H = rb.w - rb.y;
     PolyRef pr[2];
     for (int s = 0; s < 2; s++) {
@@ -389,7 +409,7 @@ __global__ void __launch_bounds__(kLWarps * 32)
       pr[s].ox = rb.x;
       pr[s].oy = rb.y;
     }
-    long long acc = 0;
+    long long acc = 0, acc_u = 0;
     // in-warp item stack: the region, split in two while its local lists overflow
     if (lane == 0)
       istk[0] = make_int4((int)((long long)rx * W / nx), (int)((long long)ry * H / ny),
@@ -428,18 +448,24 @@ __global__ void __launch_bounds__(kLWarps * 32)
         __syncwarp();
         continue;
       }
-      acc += region_pixelbox<COUNT>(P, Q, Wr, Hr, T, mode, stk, sv, sh, counters, status);
+      const longlong2 r = region_pixelbox<COUNT>(P, Q, Wr, Hr, T, mode, stk, sv, sh, counters, status);
+      acc += r.x;
+      acc_u += r.y;
       __syncwarp();
     }
     acc = (long long)warp_sum_u64((unsigned long long)acc);
+    if (mode != 0) acc_u = (long long)warp_sum_u64((unsigned long long)acc_u);
     if (lane == 0) {
       atomicAdd(reinterpret_cast<unsigned long long*>(&w.acc[i]), (unsigned long long)acc);
+      if (mode != 0) atomicAdd(reinterpret_cast<unsigned long long*>(&w.acc_u[i]), (unsigned long long)acc_u);
       __threadfence();
       if (atomicSub(&w.rem[i], 1u) == 1u) {  // last region of the pair: finalize it
         __threadfence();
         const long long I = (long long)atomicAdd(reinterpret_cast<unsigned long long*>(&w.acc[i]), 0ull);
         const long long ap = Ps.area[pq.x], aq = Qs.area[pq.y];
-        const long long U = ap + aq - I;  // indirect union
+        // indirect union; counted directly by the §5.2 baselines
+        const long long U = mode == 0 ? ap + aq - I
+                                      : (long long)atomicAdd(reinterpret_cast<unsigned long long*>(&w.acc_u[i]), 0ull);
         if (inter) inter[k] = I;
         if (uni) uni[k] = U;
         a_n++;
@@ -479,6 +505,7 @@ static size_t large_layout(long long n_cap, Carve& cv, LargeWs& w) {
   w.ctr = cv.take<unsigned long long>(4);
   w.list = cv.take<long long>(n);
   w.acc = cv.take<long long>(n);
+  w.acc_u = cv.take<long long>(n);
   w.rem = cv.take<unsigned>(n);
   w.n_cap = n_cap;
   w.extra_cap = extra_cap_for(n_cap);

@@ -140,8 +140,13 @@ __global__ void __launch_bounds__(kSmallWarps * 32, SCCG_SMALL_MINB)
       H = min(mp.w, mq.w) - by0;
       const int dxp = mp.x - bx0, dyp = mp.y - by0, dxq = mq.x - bx0, dyq = mq.y - by0;
       empty = !(W > 0 && H > 0);  // reading R18: I = 0
-      small = !empty && W <= 32 && H <= 32 && (mode == 1 || W * H < T) && cp.x <= kSmallCap && cq.x <= kSmallCap &&
+      small = mode == 0 && !empty && W <= 32 && H <= 32 && W * H < T && cp.x <= kSmallCap && cq.x <= kSmallCap &&
               op + cp.x < (1ll << 31) && oq + cq.x < (1ll << 31) && min(min(dxp, dyp), min(dxq, dyq)) >= -32768;
+      if (mode != 0) {  // PixelOnly / NoSep (§5.2 baselines): the box of MBR(p) u MBR(q), union counted directly
+        empty = false;
+        W = max(mp.z, mq.z) - min(mp.x, mq.x);
+        H = max(mp.w, mq.w) - min(mp.y, mq.y);
+      }
       meta[lane] = make_int4((int)((unsigned)W | ((unsigned)H << 6) | ((unsigned)cp.x << 12) | ((unsigned)cq.x << 20)),
                              (int)(((unsigned)dxp & 0xffffu) | ((unsigned)dyp << 16)),
                              (int)(((unsigned)dxq & 0xffffu) | ((unsigned)dyq << 16)), 0);
@@ -305,7 +310,7 @@ int run_pixelbox(const sccg_polyset* p, const sccg_polyset* q, const int32_t* pa
   int T = cfg && cfg->threshold > 0 ? cfg->threshold : 2048;
   const int mode = cfg ? cfg->mode : 0;
   if (T < 2) T = 2;
-  if (mode != 0 && mode != 1) return set_error(SCCG_E_ARG, "config.mode must be 0 (PixelBox) or 1 (PixelOnly)");
+  if (mode < 0 || mode > 2) return set_error(SCCG_E_ARG, "config.mode must be 0 (PixelBox), 1 (PixelOnly) or 2 (NoSep)");
   bool lok = true;
   const LargeWs lw = large_ws(n, w.large, w.large_bytes, lok);
   if (!lok) return set_error(SCCG_E_WORKSPACE, "pixelbox (large) workspace too small");

@@ -89,7 +89,8 @@ constexpr int kMaxRegion = 32766;  // local coordinates are 15-bit (plus clamp m
 struct LargeWs {
   unsigned long long* ctr;  // [0] item queue, [1] extra item count, [2] large-pair count (low 32 bits)
   long long* list;          // [n_cap] pair index of large pair i
-  long long* acc;           // [n_cap] pixel count of large pair i
+  long long* acc;           // [n_cap] |p n q| of large pair i
+  long long* acc_u;         // [n_cap] |p u q| of large pair i (modes 1, 2: union counted directly)
   unsigned* rem;            // [n_cap] items of pair i not yet finished
   uint64_t* items;          // [n_cap + extra_cap]
   long long n_cap, extra_cap;
@@ -106,6 +107,7 @@ __device__ __forceinline__ void emit_large(const LargeWs& w, unsigned i, long lo
   int ny = min(kMaxSplit, max((H + kRegion - 1) / kRegion, (H + kMaxRegion - 1) / kMaxRegion));
   w.list[i] = k;
   w.acc[i] = 0;
+  w.acc_u[i] = 0;
   const int extra = nx * ny - 1;
   if (extra > 0) {
     const long long base = (long long)atomicAdd(&w.ctr[1], (unsigned long long)extra);

@@ -125,12 +125,27 @@ def test_pixelbox_tile_all_T(sccg, tile_sets, T):
     check_batch(sccg, A, B, pairs.cpu().numpy(), inter, uni, sums)
 
 
-def test_pixelbox_pixelonly_mode(sccg, tile_sets):
+@pytest.mark.parametrize("mode", [1, 2])
+def test_pixelbox_baseline_modes(sccg, tile_sets, mode):
+    """The §5.2 baselines: PixelOnly (1) and PixelBox-NoSep (2) count
+    the union directly -- it must equal the oracle's directly counted union,
+    which also checks |p u q| = |p| + |q| - |p n q| on the GPU side."""
     A, B = tile_sets
     P, Q = dev(A, sccg), dev(B, sccg)
     pairs = sccg.filter_pairs(P, Q)
-    inter, uni, sums = sccg.pixelbox(P, Q, pairs, mode=1)
-    check_batch(sccg, A, B, pairs.cpu().numpy(), inter, uni, sums)
+    for T in (64, 2048):
+        inter, uni, sums = sccg.pixelbox(P, Q, pairs, mode=mode, threshold=T)
+        check_batch(sccg, A, B, pairs.cpu().numpy(), inter, uni, sums)
+    S, R = synth.generate("skewed", width=4096, height=4096)
+    P, Q = dev(S, sccg), dev(R, sccg)
+    pairs = sccg.filter_pairs(P, Q)
+    inter, uni, sums = sccg.pixelbox(P, Q, pairs, mode=mode, threshold=256)
+    check_batch(sccg, S, R, pairs.cpu().numpy(), inter, uni, sums)
+    C, D = combs.generate(n_pairs=8)
+    P, Q = dev(C, sccg), dev(D, sccg)
+    pairs = sccg.filter_pairs(P, Q)
+    inter, uni, sums = sccg.pixelbox(P, Q, pairs, mode=mode, threshold=512)
+    check_batch(sccg, C, D, pairs.cpu().numpy(), inter, uni, sums)
 
 
 @pytest.mark.parametrize("T", [64, 2048])
