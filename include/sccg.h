@@ -152,6 +152,8 @@ typedef struct {
   int32_t block;     /* threads per CTA (multiple of 32, <= 1024); 0 = default */
   int32_t grid;      /* CTAs; 0 = default (resident CTAs per SM x SM count) */
   int64_t* counters; /* optional device int64[8] (NULL = off): see SCCG_CNT_* */
+  uint32_t* hit_p;   /* optional device bitmaps, ceil(n/32) words, caller-zeroed: bit p (bit q) is set   */
+  uint32_t* hit_q;   /* when polygon p of P (q of Q) has a pair with |p n q| != 0 (for missing counts)  */
 } sccg_config;
 
 /* counters[] slots (accumulated; measurement builds only) */
@@ -182,6 +184,12 @@ SCCG_API int sccg_pixelbox_async(const sccg_polyset* p, const sccg_polyset* q, c
                                  const int64_t* result_dev, int64_t cap, int64_t* inter, int64_t* uni,
                                  sccg_sums* sums, const sccg_config* cfg, void* workspace, size_t ws_bytes,
                                  sccg_stream_t stream);
+
+/* Missing polygons: the polygons of a set that appear in no pair with
+ * |p n q| != 0, from a hit bitmap filled by sccg_pixelbox (config.hit_p /
+ * hit_q).  Writes the count (n - set bits) to *missing_dev (device int64);
+ * asynchronous. */
+SCCG_API int sccg_count_missing(const uint32_t* hit, int64_t n, int64_t* missing_dev, sccg_stream_t stream);
 
 /* ---------------------------------------------------------------- jaccard */
 /* J' of Eq. (1) from host-resident sums: the mean of r(p, q) over the

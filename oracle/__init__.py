@@ -224,3 +224,12 @@ def sums(pset, qset, pairs, inter, uni) -> dict:
         sum_area_p=int(ap[pairs[:, 0]].sum()) if len(pairs) else 0,
         sum_area_q=int(aq[pairs[:, 1]].sum()) if len(pairs) else 0,
     )
+
+
+def missing(n: int, pairs, inter, side: int) -> int:
+    """Missing polygons: polygons of a set (side 0 = P, 1 = Q) of size n
+    that appear in no pair with |p n q| != 0."""
+    pairs = np.asarray(pairs, np.int64).reshape(-1, 2)
+    inter = np.asarray(inter, np.int64)
+    seen = set(pairs[inter != 0, side].tolist())
+    return int(n - len(seen))

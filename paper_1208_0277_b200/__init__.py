@@ -36,7 +36,7 @@ SUMS_FIELDS = ("n_pairs", "n_nonzero", "sum_inter", "sum_union", "sum_area_p", "
                "limb2", "limb3", "status")
 SYMBOLS = ("sccg_polyset_bytes", "sccg_polyset_bind", "sccg_prep", "sccg_filter_workspace_bytes",
            "sccg_filter_pairs", "sccg_filter_pairs_async", "sccg_pixelbox_workspace_bytes", "sccg_pixelbox",
-           "sccg_pixelbox_async", "sccg_jaccard", "sccg_strerror", "sccg_last_error_string", "sccg_last_error_index",
+           "sccg_pixelbox_async", "sccg_count_missing", "sccg_jaccard", "sccg_strerror", "sccg_last_error_string", "sccg_last_error_index",
            "sccg_version")
 
 
@@ -76,6 +76,8 @@ class Config(ctypes.Structure):
         ("block", ctypes.c_int32),
         ("grid", ctypes.c_int32),
         ("counters", ctypes.c_void_p),
+        ("hit_p", ctypes.c_void_p),
+        ("hit_q", ctypes.c_void_p),
     ]
 
 
@@ -126,6 +128,8 @@ def load(build: bool = True):
         lib.sccg_pixelbox_workspace_bytes.restype = sz
         lib.sccg_pixelbox.argtypes = [ps, ps, vp, i64, vp, vp, vp, ctypes.POINTER(Config), vp, sz, vp]
         lib.sccg_pixelbox.restype = cint
+        lib.sccg_count_missing.argtypes = [vp, i64, vp, vp]
+        lib.sccg_count_missing.restype = cint
         lib.sccg_jaccard.argtypes = [ctypes.POINTER(Sums), ctypes.POINTER(ctypes.c_double),
                                      ctypes.POINTER(ctypes.c_double)]
         lib.sccg_jaccard.restype = cint
@@ -258,7 +262,7 @@ class Pipeline:
         self.fws = torch.empty(self.fws_bytes, dtype=torch.uint8, device=dev)
         self.pws_bytes = int(self.lib.sccg_pixelbox_workspace_bytes(self.cap))
         self.pws = torch.empty(max(self.pws_bytes, 256), dtype=torch.uint8, device=dev)
-        self.cfg = Config(threshold, 0, 0, 0, None)
+        self.cfg = Config(threshold, 0, 0, 0, None, None, None)
         self.validate = 1 if validate else 0
         self.graphs = None
         if graph:
@@ -328,8 +332,10 @@ def new_sums(device=None):
 
 
 def pixelbox(P: DeviceSet, Q: DeviceSet, pairs, threshold: int = 0, mode: int = 0, sums=None, want_inter=True,
-             want_union=True, counters=None, grid: int = 0, stream=None):
-    """Per-pair |p n q| and |p u q| (int64, input order) + accumulated sums."""
+             want_union=True, counters=None, grid: int = 0, hits=None, stream=None):
+    """Per-pair |p n q| and |p u q| (int64, input order) + accumulated sums.
+    hits = (hit_p, hit_q): optional int32 bitmaps (new_hits) marking polygons
+    with a non-zero intersection, for missing_polygons()."""
     torch = _torch()
     lib = load()
     _require_cuda(pairs, "pairs", torch.int32)
@@ -340,7 +346,8 @@ def pixelbox(P: DeviceSet, Q: DeviceSet, pairs, threshold: int = 0, mode: int = 
     if sums is None:
         sums = new_sums(dev)
     _require_cuda(sums, "sums", torch.int64)
-    cfg = Config(threshold, mode, 0, grid, counters.data_ptr() if counters is not None else None)
+    cfg = Config(threshold, mode, 0, grid, counters.data_ptr() if counters is not None else None,
+                 hits[0].data_ptr() if hits is not None else None, hits[1].data_ptr() if hits is not None else None)
     wsb = int(lib.sccg_pixelbox_workspace_bytes(n))
     ws = torch.empty(max(wsb, 256), dtype=torch.uint8, device=dev)
     code = lib.sccg_pixelbox(ctypes.byref(P.c), ctypes.byref(Q.c), pairs.data_ptr(), n,
@@ -349,6 +356,33 @@ def pixelbox(P: DeviceSet, Q: DeviceSet, pairs, threshold: int = 0, mode: int = 
                              ws.data_ptr(), wsb, _stream_ptr(stream))
     _check(code, "sccg_pixelbox")
     return inter, uni, sums
+
+
+def new_hits(P: "DeviceSet", Q: "DeviceSet"):
+    """Zeroed hit bitmaps (int32 words) for sets P and Q."""
+    torch = _torch()
+    dev = P.xy.device
+    return (torch.zeros((P.n + 31) // 32 + 1, dtype=torch.int32, device=dev),
+            torch.zeros((Q.n + 31) // 32 + 1, dtype=torch.int32, device=dev))
+
+
+def missing_polygons(hits, P: "DeviceSet", Q: "DeviceSet", stream=None) -> tuple[int, int]:
+    """(missing in P, missing in Q): polygons with no intersecting counterpart
+    (P:63), from the bitmaps pixelbox(..., hits=...) filled."""
+    torch = _torch()
+    lib = load()
+    out = torch.zeros(2, dtype=torch.int64, device=P.xy.device)
+    _check(lib.sccg_count_missing(hits[0].data_ptr(), P.n, out.data_ptr(), _stream_ptr(stream)), "sccg_count_missing")
+    _check(lib.sccg_count_missing(hits[1].data_ptr(), Q.n, out.data_ptr() + 8, _stream_ptr(stream)),
+           "sccg_count_missing")
+    a, b = out.tolist()
+    return int(a), int(b)
+
+
+def contains(inter, area_inner):
+    """ST_Contains by areas: the inner polygon lies in the outer one iff
+    |outer n inner| == |inner| (pixel sets; per pair, elementwise)."""
+    return inter == area_inner
 
 
 def sums_to_host(sums) -> Sums:

@@ -29,6 +29,7 @@ size_t filter_ws_bytes(int64_t np, int64_t nq);
 int filter_pairs(const sccg_polyset* P, const sccg_polyset* Q, int32_t* pairs, int64_t cap, int64_t* n_pairs_host,
                  void* ws, size_t ws_bytes, cudaStream_t stream);
 size_t pixelbox_ws_bytes(int64_t n);
+int count_missing(const uint32_t* hit, int64_t n, int64_t* out, cudaStream_t st);
 int filter_pairs_async(const sccg_polyset* P, const sccg_polyset* Q, int32_t* pairs, int64_t cap,
                        int64_t* result_dev, void* ws, size_t ws_bytes, cudaStream_t stream);
 int run_pixelbox(const sccg_polyset* p, const sccg_polyset* q, const int32_t* pairs, int64_t n,
@@ -201,6 +202,13 @@ int sccg_pixelbox(const sccg_polyset* p, const sccg_polyset* q, const int32_t* p
   if (int r = pixelbox_checks(p, q, pairs, n_pairs, inter, uni, sums, cfg)) return r;
   return run_pixelbox(p, q, pairs, n_pairs, nullptr, inter, uni, sums, cfg, workspace, ws_bytes,
                       reinterpret_cast<cudaStream_t>(stream));
+}
+
+int sccg_count_missing(const uint32_t* hit, int64_t n, int64_t* missing_dev, sccg_stream_t stream) {
+  set_error(SCCG_OK, "", -1);
+  if (n < 0 || !missing_dev || (n > 0 && !hit)) return set_error(SCCG_E_ARG, "sccg_count_missing: bad argument");
+  if (!aligned(hit, 4) || !aligned(missing_dev, 8)) return set_error(SCCG_E_ARG, "sccg_count_missing: misaligned");
+  return count_missing(hit, n, missing_dev, reinterpret_cast<cudaStream_t>(stream));
 }
 
 int sccg_jaccard(const sccg_sums* s, double* jprime, double* pooled) {

@@ -360,7 +360,8 @@ constexpr size_t kLSmem = kLWarps * kLSmemPerWarp;
 template <bool COUNT>
 __global__ void __launch_bounds__(kLWarps * 32)
     item_kernel(DevSet Ps, DevSet Qs, const int2* __restrict__ pairs, LargeWs w, int T, int mode,
-                long long* __restrict__ inter, long long* __restrict__ uni, long long* counters, sccg_sums* sums) {
+                long long* __restrict__ inter, long long* __restrict__ uni, long long* counters, sccg_sums* sums,
+                unsigned* __restrict__ hit_p, unsigned* __restrict__ hit_q) {
   extern __shared__ __align__(16) unsigned char s_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   unsigned char* base = s_raw + (size_t)warp * kLSmemPerWarp;
@@ -473,6 +474,8 @@ __global__ void __launch_bounds__(kLWarps * 32)
         a_ap += ap;
         a_aq += aq;
         if (I != 0) {
+          if (hit_p) atomicOr(&hit_p[pq.x >> 5], 1u << (pq.x & 31));
+          if (hit_q) atomicOr(&hit_q[pq.y >> 5], 1u << (pq.y & 31));
           unsigned long long b0, b1, b2, b3;
           ratio_limbs(I, U, b0, b1, b2, b3);
           a_nz++;
@@ -528,7 +531,8 @@ LargeWs large_ws(long long n_cap, void* ws, size_t ws_bytes, bool& ok) {
 }
 
 int launch_large(const DevSet& Ps, const DevSet& Qs, const int2* pairs, const LargeWs& w, long long* inter,
-                 long long* uni, sccg_sums* sums, int T, int mode, long long* counters, cudaStream_t stream) {
+                 long long* uni, sccg_sums* sums, int T, int mode, long long* counters, unsigned* hit_p,
+                 unsigned* hit_q, cudaStream_t stream) {
   static cudaError_t attr = [] {
     cudaError_t e = cudaFuncSetAttribute(item_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kLSmem);
     if (e == cudaSuccess)
@@ -547,9 +551,9 @@ int launch_large(const DevSet& Ps, const DevSet& Qs, const int2* pairs, const La
   const bool count = counters != nullptr;
   const unsigned ib = (unsigned)(sms * max(per_sm[count], 1));
   if (count)
-    item_kernel<true><<<ib, kLWarps * 32, kLSmem, stream>>>(Ps, Qs, pairs, w, T, mode, inter, uni, counters, sums);
+    item_kernel<true><<<ib, kLWarps * 32, kLSmem, stream>>>(Ps, Qs, pairs, w, T, mode, inter, uni, counters, sums, hit_p, hit_q);
   else
-    item_kernel<false><<<ib, kLWarps * 32, kLSmem, stream>>>(Ps, Qs, pairs, w, T, mode, inter, uni, nullptr, sums);
+    item_kernel<false><<<ib, kLWarps * 32, kLSmem, stream>>>(Ps, Qs, pairs, w, T, mode, inter, uni, nullptr, sums, hit_p, hit_q);
   return check_cuda(cudaGetLastError(), "pixelbox large launch");
 }
 

@@ -98,7 +98,8 @@ __global__ void __launch_bounds__(kSmallWarps * 32, SCCG_SMALL_MINB)
     small_kernel(DevSet Ps, DevSet Qs, const int2* __restrict__ pairs, long long n_cap,
                  const long long* __restrict__ dev_result, long long* __restrict__ inter,
                  long long* __restrict__ uni, sccg_sums* sums, int T, int mode, unsigned long long* queue,
-                 LargeWs lw, long long* counters, long long np_,
+                 LargeWs lw, long long* counters, unsigned* __restrict__ hit_p, unsigned* __restrict__ hit_q,
+                 long long np_,
                  long long nq_) {
   // pair count: host-given, or (async path) the filter's device-side count clamped to the buffer
   const long long n = dev_result ? min(dev_result[0], n_cap) : n_cap;
@@ -228,6 +229,8 @@ __global__ void __launch_bounds__(kSmallWarps * 32, SCCG_SMALL_MINB)
       if (I != 0) {
         nz = 1;
         v_u = U;
+        if (hit_p) atomicOr(&hit_p[pq.x >> 5], 1u << (pq.x & 31));
+        if (hit_q) atomicOr(&hit_q[pq.y >> 5], 1u << (pq.y & 31));
         ratio_limbs(I, U, l0, l1, l2, l3);
       }
     }
@@ -336,16 +339,54 @@ int run_pixelbox(const sccg_polyset* p, const sccg_polyset* q, const int32_t* pa
   long long* in = reinterpret_cast<long long*>(inter);
   long long* un = reinterpret_cast<long long*>(uni);
   const long long* dr = reinterpret_cast<const long long*>(dev_result);
+  unsigned* hp = cfg ? reinterpret_cast<unsigned*>(cfg->hit_p) : nullptr;
+  unsigned* hq = cfg ? reinterpret_cast<unsigned*>(cfg->hit_q) : nullptr;
   if (count)
     small_kernel<true><<<(unsigned)grid_s, kSmallWarps * 32, 0, stream>>>(
-        Ps, Qs, pr, n, dr, in, un, sums, T, mode, w.queue, lw, counters, p->n_polygons,
+        Ps, Qs, pr, n, dr, in, un, sums, T, mode, w.queue, lw, counters, hp, hq, p->n_polygons,
         q->n_polygons);
   else
     small_kernel<false><<<(unsigned)grid_s, kSmallWarps * 32, 0, stream>>>(
-        Ps, Qs, pr, n, dr, in, un, sums, T, mode, w.queue, lw, nullptr, p->n_polygons,
+        Ps, Qs, pr, n, dr, in, un, sums, T, mode, w.queue, lw, nullptr, hp, hq, p->n_polygons,
         q->n_polygons);
   if (int r = check_cuda(cudaGetLastError(), "pixelbox small launch")) return r;
-  return launch_large(Ps, Qs, pr, lw, in, un, sums, T, mode, counters, stream);
+  return launch_large(Ps, Qs, pr, lw, in, un, sums, T, mode, counters, hp, hq, stream);
+}
+
+}  // namespace sccg
+
+namespace sccg {
+
+__global__ void count_missing_kernel(const unsigned* __restrict__ hit, long long n, long long* out) {
+  __shared__ unsigned long long s;
+  if (threadIdx.x == 0) s = 0;
+  __syncthreads();
+  unsigned long long c = 0;
+  const long long nw = (n + 31) / 32;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < nw; i += (long long)gridDim.x * blockDim.x) {
+    unsigned v = hit[i];
+    if (i == nw - 1 && (n & 31)) v &= (1u << (n & 31)) - 1u;  // ignore bits past n
+    c += (unsigned long long)__popc(v);
+  }
+  c = warp_sum_u64(c);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(&s, c);
+  __syncthreads();
+  if (threadIdx.x == 0 && s) atomicAdd(reinterpret_cast<unsigned long long*>(out), s);
+}
+
+__global__ void set_kernel(long long* out, long long v) { *out = v; }
+__global__ void finish_missing_kernel(long long* out, long long n) { *out = n - *out; }
+
+int count_missing(const uint32_t* hit, int64_t n, int64_t* out, cudaStream_t st) {
+  // missing = n - (number of set bits): start at n, subtract via a negative add
+  set_kernel<<<1, 1, 0, st>>>(reinterpret_cast<long long*>(out), 0);
+  if (n > 0) {
+    const long long nw = (n + 31) / 32;
+    const unsigned blocks = (unsigned)min((nw + 255) / 256, 1024ll);
+    count_missing_kernel<<<blocks, 256, 0, st>>>(hit, n, reinterpret_cast<long long*>(out));
+  }
+  finish_missing_kernel<<<1, 1, 0, st>>>(reinterpret_cast<long long*>(out), n);
+  return check_cuda(cudaGetLastError(), "count missing");
 }
 
 }  // namespace sccg

@@ -257,6 +257,25 @@ def test_async_pipeline_matches_sync(sccg, tile_sets):
     assert e.value.code == sccg.E_CAPACITY
 
 
+def test_missing_polygons_and_contains(sccg, tile_sets):
+    """NEXT(f3)/(f4): missing-polygon counts from the kernels' hit
+    bitmaps, and ST_Contains by areas, against the oracle."""
+    A, B = tile_sets
+    for cfg in ("tile", "skewed"):
+        if cfg == "skewed":
+            A, B = synth.generate("skewed", width=4096, height=4096)
+        P, Q = dev(A, sccg), dev(B, sccg)
+        pairs = sccg.filter_pairs(P, Q)
+        hits = sccg.new_hits(P, Q)
+        inter, uni, sums = sccg.pixelbox(P, Q, pairs, hits=hits)
+        pn = pairs.cpu().numpy()
+        ei, _ = oracle.pair_areas(A, B, pn)
+        assert sccg.missing_polygons(hits, P, Q) == (oracle.missing(A.n, pn, ei, 0), oracle.missing(B.n, pn, ei, 1))
+        aq, _ = oracle.set_props(B)
+        got = sccg.contains(inter, Q.area[pairs[:, 1].long()]).cpu().numpy()
+        assert (got == (ei == aq[pn[:, 1]])).all()
+
+
 def test_abi_errors(sccg):
     bad = synth.pack([[[0, 0], [3, 1], [3, 3], [0, 3]]])  # diagonal edge
     good = synth.pack([[[0, 0], [3, 0], [3, 3], [0, 3]]])

@@ -298,3 +298,16 @@ def test_sums_fields(tile_sets):
     assert s["n_pairs"] == len(pairs) and s["n_nonzero"] == int(nz.sum())
     # all-pairs check: sum|p| + sum|q| - sum I = sum over all pairs of U
     assert s["sum_area_p"] + s["sum_area_q"] - s["sum_inter"] == int(uni.sum())
+
+
+def test_missing_polygons(tile_sets):
+    a, b = tile_sets
+    pa = oracle.join(a, a)
+    ia, _ = oracle.pair_areas(a, a, pa)
+    assert oracle.missing(a.n, pa, ia, 0) == 0 and oracle.missing(a.n, pa, ia, 1) == 0  # identical sets
+    pairs = oracle.join(a, b)
+    inter, _ = oracle.pair_areas(a, b, pairs)
+    ma, mb = oracle.missing(a.n, pairs, inter, 0), oracle.missing(b.n, pairs, inter, 1)
+    # set B drops ~5 % of A's nuclei (synth recipe): A has about that many missing
+    assert 0.02 * a.n < ma < 0.10 * a.n and 0 <= mb < 0.15 * b.n
+    assert oracle.missing(7, np.zeros((0, 2)), [], 0) == 7
