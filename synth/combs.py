@@ -102,12 +102,25 @@ def generate(image: int = 0, seed: int | None = None, n_pairs: int = 16384, cell
 
 
 def rect_decomp_intersection(ra, rb) -> int:
-    """Closed form: |A n B| for disjoint rectangle decompositions of A and B."""
+    """Closed form: |A n B| for disjoint rectangle decompositions of A and B,
+    sum_i sum_j |R_i n S_j| (only x-overlapping candidates are visited)."""
     a = np.asarray(ra, np.int64).reshape(-1, 4)
     b = np.asarray(rb, np.int64).reshape(-1, 4)
-    ow = np.minimum(a[:, None, 2], b[None, :, 2]) - np.maximum(a[:, None, 0], b[None, :, 0])
-    oh = np.minimum(a[:, None, 3], b[None, :, 3]) - np.maximum(a[:, None, 1], b[None, :, 1])
-    return int((np.clip(ow, 0, None) * np.clip(oh, 0, None)).sum())
+    if len(a) * len(b) <= 1 << 20:
+        ow = np.minimum(a[:, None, 2], b[None, :, 2]) - np.maximum(a[:, None, 0], b[None, :, 0])
+        oh = np.minimum(a[:, None, 3], b[None, :, 3]) - np.maximum(a[:, None, 1], b[None, :, 1])
+        return int((np.clip(ow, 0, None) * np.clip(oh, 0, None)).sum())
+    b = b[np.argsort(b[:, 0], kind="stable")]
+    wmax = int((b[:, 2] - b[:, 0]).max())
+    tot = 0
+    for r in a:
+        lo = np.searchsorted(b[:, 0], r[0] - wmax, side="left")
+        hi = np.searchsorted(b[:, 0], r[2], side="left")
+        c = b[lo:hi]
+        ow = np.minimum(c[:, 2], r[2]) - np.maximum(c[:, 0], r[0])
+        oh = np.minimum(c[:, 3], r[3]) - np.maximum(c[:, 1], r[1])
+        tot += int((np.clip(ow, 0, None) * np.clip(oh, 0, None)).sum())
+    return tot
 
 
 def rect_decomp_area(ra) -> int:

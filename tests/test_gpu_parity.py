@@ -276,6 +276,40 @@ def test_missing_polygons_and_contains(sccg, tile_sets):
         assert (got == (ei == aq[pn[:, 1]])).all()
 
 
+def test_maximum_sizes_closed_form(sccg):
+    """Limits of the ABI (R20): MBR extents of 65535 pixels, coordinates near
+    +-2^30, |p n q| > 2^32 -- pinned by rectangle closed forms and disjoint-
+    rectangle-union combs (no oracle scan of 4e9 pixels)."""
+    big = (1 << 30) - 70000
+    rects_p = [(big, big, big + 65535, big + 65535), (-(1 << 30), 0, -(1 << 30) + 65535, 3),
+               (0, -(1 << 30), 40000, -(1 << 30) + 65535)]
+    rects_q = [(big + 1000, big + 999, big + 65535, big + 65535), (-(1 << 30) + 5, 1, -(1 << 30) + 65000, 2),
+               (39999, -(1 << 30) + 1, 50000, -(1 << 30) + 65534)]
+    ring = lambda r: [[r[0], r[1]], [r[2], r[1]], [r[2], r[3]], [r[0], r[3]]]
+    A, B = synth.pack([ring(r) for r in rects_p]), synth.pack([ring(r) for r in rects_q])
+    P, Q = dev(A, sccg), dev(B, sccg)
+    pairs = sccg.filter_pairs(P, Q)
+    assert pairs.cpu().numpy().tolist() == [[0, 0], [1, 1], [2, 2]]
+    for T in (64, 2048):
+        inter, uni, sums = sccg.pixelbox(P, Q, pairs, threshold=T)
+        for k, (a, b) in enumerate(zip(rects_p, rects_q)):
+            ow = max(0, min(a[2], b[2]) - max(a[0], b[0]))
+            oh = max(0, min(a[3], b[3]) - max(a[1], b[1]))
+            area = lambda r: (r[2] - r[0]) * (r[3] - r[1])
+            assert inter[k].item() == ow * oh and uni[k].item() == area(a) + area(b) - ow * oh
+        assert inter[0].item() > 1 << 32
+    # a comb spanning the full extent against its shifted copy (closed form)
+    ra, Ra = combs.comb(-50000, 7, 16383, 2, 2, 60000, 5)  # W = 65534
+    rb, Rb = combs.comb(-49999, 9, 16383, 2, 2, 60000, 5)
+    C, D = synth.pack([ra]), synth.pack([rb])
+    P, Q = dev(C, sccg), dev(D, sccg)
+    pairs = sccg.filter_pairs(P, Q)
+    inter, uni, _ = sccg.pixelbox(P, Q, pairs)
+    want = combs.rect_decomp_intersection(Ra, Rb)
+    assert inter.item() == want
+    assert uni.item() == combs.rect_decomp_area(Ra) + combs.rect_decomp_area(Rb) - want
+
+
 def test_abi_errors(sccg):
     bad = synth.pack([[[0, 0], [3, 1], [3, 3], [0, 3]]])  # diagonal edge
     good = synth.pack([[[0, 0], [3, 0], [3, 3], [0, 3]]])
