@@ -278,7 +278,7 @@ def test_missing_polygons_and_contains(sccg, tile_sets):
 
 def test_maximum_sizes_closed_form(sccg):
     """Limits of the ABI (R20): MBR extents of 65535 pixels, coordinates near
-    +-2^30, |p n q| > 2^32 -- pinned by rectangle closed forms and disjoint-
+    +-2^30, |p n q| > 2^31 -- pinned by rectangle closed forms and disjoint-
     rectangle-union combs (no oracle scan of 4e9 pixels)."""
     big = (1 << 30) - 70000
     rects_p = [(big, big, big + 65535, big + 65535), (-(1 << 30), 0, -(1 << 30) + 65535, 3),
@@ -297,7 +297,7 @@ def test_maximum_sizes_closed_form(sccg):
             oh = max(0, min(a[3], b[3]) - max(a[1], b[1]))
             area = lambda r: (r[2] - r[0]) * (r[3] - r[1])
             assert inter[k].item() == ow * oh and uni[k].item() == area(a) + area(b) - ow * oh
-        assert inter[0].item() > 1 << 32
+        assert inter[0].item() > 1 << 31  # beyond int32
     # a comb spanning the full extent against its shifted copy (closed form)
     ra, Ra = combs.comb(-50000, 7, 16383, 2, 2, 60000, 5)  # W = 65534
     rb, Rb = combs.comb(-49999, 9, 16383, 2, 2, 60000, 5)
