@@ -149,12 +149,16 @@ typedef struct {
                         from |p| + |q| - |p n q|); the paper's §5.2 baselines, which count the
                         union directly over the box of MBR(p) u MBR(q): 1 = PixelOnly (pixelization
                         only), 2 = PixelBox-NoSep (sampling boxes deciding both areas) */
-  int32_t block;     /* threads per CTA (multiple of 32, <= 1024); 0 = default */
+  int32_t flags;     /* SCCG_FLAG_* bits; 0 = default */
   int32_t grid;      /* CTAs; 0 = default (resident CTAs per SM x SM count) */
   int64_t* counters; /* optional device int64[8] (NULL = off): see SCCG_CNT_* */
   uint32_t* hit_p;   /* optional device bitmaps, ceil(n/32) words, caller-zeroed: bit p (bit q) is set   */
   uint32_t* hit_q;   /* when polygon p of P (q of Q) has a pair with |p n q| != 0 (for missing counts)  */
 } sccg_config;
+
+/* flags: per-pair pixelization from edge records even where prep stored a ring's
+ * raster (the paper's schedule, Alg. 1 l.24-25; results are identical) */
+#define SCCG_FLAG_NO_RASTER 1
 
 /* counters[] slots (accumulated; measurement builds only) */
 #define SCCG_CNT_PIXELS 0      /* pixels classified by pixelization (each against both polygons) */

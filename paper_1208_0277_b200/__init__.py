@@ -31,6 +31,7 @@ _lib = None
 
 # status codes (include/sccg.h)
 OK, E_ARG, E_NOT_RECTILINEAR, E_RANGE, E_CAPACITY, E_STACK, E_EMPTY, E_CUDA, E_WORKSPACE = range(9)
+FLAG_NO_RASTER = 1
 CNT_PIXELS, CNT_ROWTESTS, CNT_BOXES, CNT_BOXEDGES, CNT_SPLITS, CNT_PIXBOXES, CNT_ROOTPX = range(7)
 SUMS_FIELDS = ("n_pairs", "n_nonzero", "sum_inter", "sum_union", "sum_area_p", "sum_area_q", "limb0", "limb1",
                "limb2", "limb3", "status")
@@ -73,7 +74,7 @@ class Config(ctypes.Structure):
     _fields_ = [
         ("threshold", ctypes.c_int32),
         ("mode", ctypes.c_int32),
-        ("block", ctypes.c_int32),
+        ("flags", ctypes.c_int32),
         ("grid", ctypes.c_int32),
         ("counters", ctypes.c_void_p),
         ("hit_p", ctypes.c_void_p),
@@ -249,7 +250,7 @@ class Pipeline:
     ``run()`` returns the device sums vector; read it (one sync) for J'."""
 
     def __init__(self, P: "DeviceSet", Q: "DeviceSet", cap: int | None = None, threshold: int = 0, graph: bool = True,
-                 validate: bool = True):
+                 validate: bool = True, raster: bool = True):
         torch = _torch()
         self.lib = load()
         self.P, self.Q = P, Q
@@ -262,7 +263,7 @@ class Pipeline:
         self.fws = torch.empty(self.fws_bytes, dtype=torch.uint8, device=dev)
         self.pws_bytes = int(self.lib.sccg_pixelbox_workspace_bytes(self.cap))
         self.pws = torch.empty(max(self.pws_bytes, 256), dtype=torch.uint8, device=dev)
-        self.cfg = Config(threshold, 0, 0, 0, None, None, None)
+        self.cfg = Config(threshold, 0, 0 if raster else FLAG_NO_RASTER, 0, None, None, None)
         self.validate = 1 if validate else 0
         self.graphs = None
         if graph:
@@ -332,7 +333,7 @@ def new_sums(device=None):
 
 
 def pixelbox(P: DeviceSet, Q: DeviceSet, pairs, threshold: int = 0, mode: int = 0, sums=None, want_inter=True,
-             want_union=True, counters=None, grid: int = 0, hits=None, stream=None):
+             want_union=True, counters=None, grid: int = 0, hits=None, raster: bool = True, stream=None):
     """Per-pair |p n q| and |p u q| (int64, input order) + accumulated sums.
     hits = (hit_p, hit_q): optional int32 bitmaps (new_hits) marking polygons
     with a non-zero intersection, for missing_polygons()."""
@@ -346,7 +347,8 @@ def pixelbox(P: DeviceSet, Q: DeviceSet, pairs, threshold: int = 0, mode: int = 
     if sums is None:
         sums = new_sums(dev)
     _require_cuda(sums, "sums", torch.int64)
-    cfg = Config(threshold, mode, 0, grid, counters.data_ptr() if counters is not None else None,
+    cfg = Config(threshold, mode, 0 if raster else FLAG_NO_RASTER, grid,
+                 counters.data_ptr() if counters is not None else None,
                  hits[0].data_ptr() if hits is not None else None, hits[1].data_ptr() if hits is not None else None)
     wsb = int(lib.sccg_pixelbox_workspace_bytes(n))
     ws = torch.empty(max(wsb, 256), dtype=torch.uint8, device=dev)

@@ -48,6 +48,11 @@ __device__ __forceinline__ unsigned suffix_mask(int k) { return shl_clamp(0xffff
 // Low `n` bits (n in [0, 32]).
 __device__ __forceinline__ unsigned low_bits(int n) { return ~shl_clamp(0xffffffffu, (unsigned)max(n, 0)); }
 
+// ecount[i].y carries this flag when polygon i has a raster: H = ymax - ylo
+// 32-bit row words (bit x = pixel (xlo + x, ylo + r) inside) stored right after
+// its vertical records, i.e. at (uint32*)(edges + off[i] + nv) (prep.cu).
+constexpr int kRasterFlag = 1 << 30;
+
 // Per-set statistics written by sccg_prep (sccg_polyset.stats), read by the
 // join's on-device grid selection: moments of the MBR extents over non-empty
 // MBRs (w, h = width, height): sw = sum(w - 1), sh = sum(h - 1),

@@ -97,7 +97,8 @@ template <bool COUNT>
 __global__ void __launch_bounds__(kSmallWarps * 32, SCCG_SMALL_MINB)
     small_kernel(DevSet Ps, DevSet Qs, const int2* __restrict__ pairs, long long n_cap,
                  const long long* __restrict__ dev_result, long long* __restrict__ inter,
-                 long long* __restrict__ uni, sccg_sums* sums, int T, int mode, unsigned long long* queue,
+                 long long* __restrict__ uni, sccg_sums* sums, int T, int mode, bool use_raster,
+                 unsigned long long* queue,
                  LargeWs lw, long long* counters, unsigned* __restrict__ hit_p, unsigned* __restrict__ hit_q,
                  long long np_,
                  long long nq_) {
@@ -148,7 +149,10 @@ __global__ void __launch_bounds__(kSmallWarps * 32, SCCG_SMALL_MINB)
         W = max(mp.z, mq.z) - min(mp.x, mq.x);
         H = max(mp.w, mq.w) - min(mp.y, mq.y);
       }
-      meta[lane] = make_int4((int)((unsigned)W | ((unsigned)H << 6) | ((unsigned)cp.x << 12) | ((unsigned)cq.x << 20)),
+      // both rings carry a raster (prep): the pair reads pixel classifications instead of edges
+      const unsigned rast = (small && use_raster && (cp.y & kRasterFlag) && (cq.y & kRasterFlag)) ? 1u : 0u;
+      meta[lane] = make_int4((int)((unsigned)W | ((unsigned)H << 6) | ((unsigned)cp.x << 12) | ((unsigned)cq.x << 20) |
+                                   (rast << 26)),
                              (int)(((unsigned)dxp & 0xffffu) | ((unsigned)dyp << 16)),
                              (int)(((unsigned)dxq & 0xffffu) | ((unsigned)dyq << 16)), 0);
       epq[lane] = make_int2((int)op, (int)oq);
@@ -169,11 +173,20 @@ __global__ void __launch_bounds__(kSmallWarps * 32, SCCG_SMALL_MINB)
     unsigned myI = 0;
     uint64_t np0 = 0, np1 = 0, nq0 = 0, nq1 = 0;
     auto prefetch = [&](int j) {
-      const unsigned mj = (unsigned)meta[j].x;
+      const int4 mm = meta[j];
+      const unsigned mj = (unsigned)mm.x;
       const int2 e = epq[j];
       const int nvp = (mj >> 12) & 127, nvq = (mj >> 20) & 127;
       const uint64_t* pe = Ps.edges + e.x;
       const uint64_t* qe = Qs.edges + e.y;
+      if ((mj >> 26) & 1u) {  // raster pair: this lane's box row of both rasters
+        const int H = (mj >> 6) & 63;
+        const unsigned* rp = reinterpret_cast<const unsigned*>(pe + nvp);
+        const unsigned* rq = reinterpret_cast<const unsigned*>(qe + nvq);
+        np0 = lane < H ? __ldg(rp + lane - (mm.y >> 16)) : 0u;
+        nq0 = lane < H ? __ldg(rq + lane - (mm.z >> 16)) : 0u;
+        return;
+      }
       np0 = lane < nvp ? __ldg(pe + lane) : 0ull;
       nq0 = lane < nvq ? __ldg(qe + lane) : 0ull;
       if (nvp > 32) np1 = lane + 32 < nvp ? __ldg(pe + 32 + lane) : 0ull;
@@ -190,6 +203,16 @@ __global__ void __launch_bounds__(kSmallWarps * 32, SCCG_SMALL_MINB)
       const int4 mm = meta[j];
       const unsigned mj = (unsigned)mm.x, dpj = (unsigned)mm.y, dqj = (unsigned)mm.z;
       const int W = mj & 63, H = (mj >> 6) & 63, nvp = (mj >> 12) & 127, nvq = (mj >> 20) & 127;
+      if ((mj >> 26) & 1u) {
+        // memoized pixelization: row words of both rasters, aligned to the box's
+        // first column (bit x = box column x), AND, popcount, one REDUX
+        const unsigned wp = (unsigned)cp0 >> (-(int)(short)(dpj & 0xffffu));
+        const unsigned wq = (unsigned)cq0 >> (-(int)(short)(dqj & 0xffffu));
+        const unsigned I = __reduce_add_sync(FULL, __popc(wp & wq & low_bits(W)));
+        if (lane == j) myI = I;
+        if (COUNT) c_px += (unsigned long long)W * H;
+        continue;
+      }
       const bool two = max(nvp, nvq) > 32;
       const int cntp = stage_rows(cp0, cp1, nvp, two, (int)(short)(dpj & 0xffffu), (int)dpj >> 16, H, bp);
       const int cntq = stage_rows(cq0, cq1, nvq, two, (int)(short)(dqj & 0xffffu), (int)dqj >> 16, H, bq);
@@ -312,6 +335,7 @@ int run_pixelbox(const sccg_polyset* p, const sccg_polyset* q, const int32_t* pa
   if (!cv.ok || ws == nullptr) return set_error(SCCG_E_WORKSPACE, "pixelbox workspace too small");
   int T = cfg && cfg->threshold > 0 ? cfg->threshold : 2048;
   const int mode = cfg ? cfg->mode : 0;
+  const bool use_raster = !(cfg && (cfg->flags & SCCG_FLAG_NO_RASTER));
   if (T < 2) T = 2;
   if (mode < 0 || mode > 2) return set_error(SCCG_E_ARG, "config.mode must be 0 (PixelBox), 1 (PixelOnly) or 2 (NoSep)");
   bool lok = true;
@@ -343,11 +367,11 @@ int run_pixelbox(const sccg_polyset* p, const sccg_polyset* q, const int32_t* pa
   unsigned* hq = cfg ? reinterpret_cast<unsigned*>(cfg->hit_q) : nullptr;
   if (count)
     small_kernel<true><<<(unsigned)grid_s, kSmallWarps * 32, 0, stream>>>(
-        Ps, Qs, pr, n, dr, in, un, sums, T, mode, w.queue, lw, counters, hp, hq, p->n_polygons,
+        Ps, Qs, pr, n, dr, in, un, sums, T, mode, use_raster, w.queue, lw, counters, hp, hq, p->n_polygons,
         q->n_polygons);
   else
     small_kernel<false><<<(unsigned)grid_s, kSmallWarps * 32, 0, stream>>>(
-        Ps, Qs, pr, n, dr, in, un, sums, T, mode, w.queue, lw, nullptr, hp, hq, p->n_polygons,
+        Ps, Qs, pr, n, dr, in, un, sums, T, mode, use_raster, w.queue, lw, nullptr, hp, hq, p->n_polygons,
         q->n_polygons);
   if (int r = check_cuda(cudaGetLastError(), "pixelbox small launch")) return r;
   return launch_large(Ps, Qs, pr, lw, in, un, sums, T, mode, counters, hp, hq, stream);

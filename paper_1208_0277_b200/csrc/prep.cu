@@ -145,7 +145,33 @@ __device__ __forceinline__ int4 prep_polygon_thread(int2* v, int V, int64_t poly
   }
   edge(fx, fy);  // closing edge back to the first vertex
   area[poly] = (twice_area < 0 ? -twice_area : twice_area) / 2;
-  ecount[poly] = make_int2(nvert, nhor);
+  // Raster: pixel (x, y) of the MBR is inside
+  // iff an odd number of the row's vertical edges lie at or left of x (R19) --
+  // PIXELINPOLY depends on the polygon alone, so it is computed once here.
+  // Row r as a 32-bit word (bit x = column xlo + x): difference trick -- each
+  // vertical edge XORs its suffix mask into rows lo and hi -- then a prefix XOR
+  // over rows.  Stored in the slot's free tail (words 2 nv .. 2 nv + H), which
+  // exists when 2 (V - nv) >= H; MBR width <= 32.
+  const int W = xmax - xmin, H = ymax - ymin;
+  bool raster = !diag && W <= 32 && 2 * (V - nvert) >= H;
+  if (raster) {
+    unsigned* D = reinterpret_cast<unsigned*>(out + nvert);
+    for (int r = 0; r < H; r++) D[r] = 0u;
+    for (int k = 0; k < nvert; k++) {
+      int c, lo, hi;
+      unpack_edge(out[k], c, lo, hi);
+      const unsigned m = suffix_mask(c);
+      D[lo] ^= m;
+      if (hi < H) D[hi] ^= m;
+    }
+    unsigned acc = 0u;
+    const unsigned wmask = low_bits(W);
+    for (int r = 0; r < H; r++) {
+      acc ^= D[r];
+      D[r] = acc & wmask;
+    }
+  }
+  ecount[poly] = make_int2(nvert, nhor | (raster ? kRasterFlag : 0));
   if (validate && diag) flag(status, SCCG_STATUS_NOT_RECTILINEAR, poly);
   return m;
 }

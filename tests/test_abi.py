@@ -106,5 +106,5 @@ def test_host_argument_checks():
     assert lib.sccg_prep(None, 1, None) == sccg.E_ARG
     n = ctypes.c_int64()
     assert lib.sccg_filter_pairs(None, None, None, 0, ctypes.byref(n), None, 0, None) == sccg.E_ARG
-    cfg = sccg.Config(-1, 0, 0, 0, None)
+    cfg = sccg.Config(-1, 0, 0, 0, None, None, None)
     assert lib.sccg_pixelbox(None, None, None, 0, None, None, None, ctypes.byref(cfg), None, 0, None) == sccg.E_ARG

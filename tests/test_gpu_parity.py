@@ -116,12 +116,15 @@ def test_filter_capacity_retry(sccg, tile_sets):
 
 
 # -------------------------------------------------------------- pixelbox
+@pytest.mark.parametrize("raster", [True, False])
 @pytest.mark.parametrize("T", [2, 37, 512, 2048, 1 << 30])
-def test_pixelbox_tile_all_T(sccg, tile_sets, T):
+def test_pixelbox_tile_all_T(sccg, tile_sets, T, raster):
+    """Every path and threshold; raster=False forces the per-pair edge
+    pixelization (the paper's schedule) where prep stored a ring's raster."""
     A, B = tile_sets
     P, Q = dev(A, sccg), dev(B, sccg)
     pairs = sccg.filter_pairs(P, Q)
-    inter, uni, sums = sccg.pixelbox(P, Q, pairs, threshold=T)
+    inter, uni, sums = sccg.pixelbox(P, Q, pairs, threshold=T, raster=raster)
     check_batch(sccg, A, B, pairs.cpu().numpy(), inter, uni, sums)
 
 
@@ -355,9 +358,11 @@ def test_slide_full_size(sccg):
     assert s[0] == len(pn) and s[2] == int(gi.sum()) and s[4] == int(a_p.sum()) and s[5] == int(a_q.sum())
     assert s[1] == int((gi > 0).sum()) and s[10] == 0
     assert sum(l << (30 * i) for i, l in enumerate(s[6:10])) == exact_ratio_units(gi, gu)
-    # determinism across thresholds: per-pair results identical
+    # determinism across thresholds and pixelization schedules: per-pair results identical
     i2, u2, s2 = sccg.pixelbox(P, Q, pairs, threshold=64)
     assert torch.equal(i2, inter) and torch.equal(s2, sums)
+    i3, u3, s3 = sccg.pixelbox(P, Q, pairs, raster=False)
+    assert torch.equal(i3, inter) and torch.equal(s3, sums)
     # the bench's launch configuration (device-resident pipeline, CUDA graphs)
     pipe = sccg.Pipeline(P, Q, cap=3 * max(P.n, Q.n) + 1024, graph=True)
     for _ in range(2):
