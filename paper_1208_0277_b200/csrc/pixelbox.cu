@@ -149,10 +149,11 @@ __global__ void __launch_bounds__(kSmallWarps * 32, SCCG_SMALL_MINB)
         W = max(mp.z, mq.z) - min(mp.x, mq.x);
         H = max(mp.w, mq.w) - min(mp.y, mq.y);
       }
-      // both rings carry a raster (prep): the pair reads pixel classifications instead of edges
+      // both rings carry a raster (prep): the pair reads pixel classifications instead of edges.
+      // meta.x: W (bits 0-5), H (6-11), nv_p (12-18), nv_q (20-26), raster (28)
       const unsigned rast = (small && use_raster && (cp.y & kRasterFlag) && (cq.y & kRasterFlag)) ? 1u : 0u;
       meta[lane] = make_int4((int)((unsigned)W | ((unsigned)H << 6) | ((unsigned)cp.x << 12) | ((unsigned)cq.x << 20) |
-                                   (rast << 26)),
+                                   (rast << 28)),
                              (int)(((unsigned)dxp & 0xffffu) | ((unsigned)dyp << 16)),
                              (int)(((unsigned)dxq & 0xffffu) | ((unsigned)dyq << 16)), 0);
       epq[lane] = make_int2((int)op, (int)oq);
@@ -179,7 +180,7 @@ __global__ void __launch_bounds__(kSmallWarps * 32, SCCG_SMALL_MINB)
       const int nvp = (mj >> 12) & 127, nvq = (mj >> 20) & 127;
       const uint64_t* pe = Ps.edges + e.x;
       const uint64_t* qe = Qs.edges + e.y;
-      if ((mj >> 26) & 1u) {  // raster pair: this lane's box row of both rasters
+      if ((mj >> 28) & 1u) {  // raster pair: this lane's box row of both rasters
         const int H = (mj >> 6) & 63;
         const unsigned* rp = reinterpret_cast<const unsigned*>(pe + nvp);
         const unsigned* rq = reinterpret_cast<const unsigned*>(qe + nvq);
@@ -203,7 +204,7 @@ __global__ void __launch_bounds__(kSmallWarps * 32, SCCG_SMALL_MINB)
       const int4 mm = meta[j];
       const unsigned mj = (unsigned)mm.x, dpj = (unsigned)mm.y, dqj = (unsigned)mm.z;
       const int W = mj & 63, H = (mj >> 6) & 63, nvp = (mj >> 12) & 127, nvq = (mj >> 20) & 127;
-      if ((mj >> 26) & 1u) {
+      if ((mj >> 28) & 1u) {
         // memoized pixelization: row words of both rasters, aligned to the box's
         // first column (bit x = box column x), AND, popcount, one REDUX
         const unsigned wp = (unsigned)cp0 >> (-(int)(short)(dpj & 0xffffu));
