@@ -110,6 +110,8 @@ __global__ void __launch_bounds__(kSmallWarps * 32, SCCG_SMALL_MINB)
   __shared__ int4 s_meta[kSmallWarps][32];
   __shared__ int2 s_ep[kSmallWarps][32];
   __shared__ unsigned long long s_acc[kSmallWarps][16];
+  __shared__ int s_rstart[kSmallWarps][33];  // raster pairs: first (pair, row) item of each pair
+  __shared__ unsigned s_rcnt[kSmallWarps][32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   int2* bp = s_buf[warp];
   int2* bq = bp + kSmallQOff;
@@ -128,6 +130,7 @@ __global__ void __launch_bounds__(kSmallWarps * 32, SCCG_SMALL_MINB)
     bool ok = false, small = false, empty = false;
     int2 pq = make_int2(0, 0);
     int W = 0, H = 0;
+    unsigned rast = 0u;
     if (k < n) {
       pq = pairs[k];
       ok = (unsigned)pq.x < (unsigned long long)np_ && (unsigned)pq.y < (unsigned long long)nq_;
@@ -151,7 +154,7 @@ __global__ void __launch_bounds__(kSmallWarps * 32, SCCG_SMALL_MINB)
       }
       // both rings carry a raster (prep): the pair reads pixel classifications instead of edges.
       // meta.x: W (bits 0-5), H (6-11), nv_p (12-18), nv_q (20-26), raster (28)
-      const unsigned rast = (small && use_raster && (cp.y & kRasterFlag) && (cq.y & kRasterFlag)) ? 1u : 0u;
+      rast = (small && use_raster && (cp.y & kRasterFlag) && (cq.y & kRasterFlag)) ? 1u : 0u;
       meta[lane] = make_int4((int)((unsigned)W | ((unsigned)H << 6) | ((unsigned)cp.x << 12) | ((unsigned)cq.x << 20) |
                                    (rast << 28)),
                              (int)(((unsigned)dxp & 0xffffu) | ((unsigned)dyp << 16)),
@@ -170,8 +173,44 @@ __global__ void __launch_bounds__(kSmallWarps * 32, SCCG_SMALL_MINB)
     }
     // ---- small pairs, software-pipelined: records of the next pair are in
     // flight into registers while the current pair is pixelized
-    unsigned todo = __ballot_sync(FULL, small);
     unsigned myI = 0;
+    // ---- raster pairs, batched: the chunk's (pair, row) items are spread over
+    // the lanes, so each lane has many independent row loads in flight; a row
+    // costs two loads, two shifts, an AND and a popcount (memoized pixelization)
+    const unsigned rmask = __ballot_sync(FULL, rast != 0u);
+    if (rmask) {
+      const int hl = rast ? H : 0;
+      int sc = hl;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(FULL, sc, o);
+        if (lane >= o) sc += t;
+      }
+      const int R = __shfl_sync(FULL, sc, 31);
+      int* rstart = s_rstart[warp];
+      unsigned* rcnt = s_rcnt[warp];
+      rstart[lane] = sc - hl;
+      if (lane == 31) rstart[32] = R;
+      rcnt[lane] = 0u;
+      __syncwarp();
+      int jr = 0;
+#pragma unroll 2
+      for (int t = lane; t < R; t += 32) {
+        while (rstart[jr + 1] <= t) jr++;
+        const int r = t - rstart[jr];
+        const int4 mm = meta[jr];
+        const int2 e = epq[jr];
+        const unsigned mj = (unsigned)mm.x;
+        const unsigned* rp = reinterpret_cast<const unsigned*>(Ps.edges + e.x + ((mj >> 12) & 127));
+        const unsigned* rq = reinterpret_cast<const unsigned*>(Qs.edges + e.y + ((mj >> 20) & 127));
+        const unsigned wp = __ldg(rp + r - (mm.y >> 16)) >> (-(int)(short)(mm.y & 0xffff));
+        const unsigned wq = __ldg(rq + r - (mm.z >> 16)) >> (-(int)(short)(mm.z & 0xffff));
+        atomicAdd(&rcnt[jr], (unsigned)__popc(wp & wq & low_bits(mj & 63)));
+      }
+      __syncwarp();
+      if (rast) myI = rcnt[lane];
+    }
+    unsigned todo = __ballot_sync(FULL, small) & ~rmask;
     uint64_t np0 = 0, np1 = 0, nq0 = 0, nq1 = 0;
     auto prefetch = [&](int j) {
       const int4 mm = meta[j];
@@ -180,21 +219,13 @@ __global__ void __launch_bounds__(kSmallWarps * 32, SCCG_SMALL_MINB)
       const int nvp = (mj >> 12) & 127, nvq = (mj >> 20) & 127;
       const uint64_t* pe = Ps.edges + e.x;
       const uint64_t* qe = Qs.edges + e.y;
-      if ((mj >> 28) & 1u) {  // raster pair: this lane's box row of both rasters
-        const int H = (mj >> 6) & 63;
-        const unsigned* rp = reinterpret_cast<const unsigned*>(pe + nvp);
-        const unsigned* rq = reinterpret_cast<const unsigned*>(qe + nvq);
-        np0 = lane < H ? __ldg(rp + lane - (mm.y >> 16)) : 0u;
-        nq0 = lane < H ? __ldg(rq + lane - (mm.z >> 16)) : 0u;
-        return;
-      }
       np0 = lane < nvp ? __ldg(pe + lane) : 0ull;
       nq0 = lane < nvq ? __ldg(qe + lane) : 0ull;
       if (nvp > 32) np1 = lane + 32 < nvp ? __ldg(pe + 32 + lane) : 0ull;
       if (nvq > 32) nq1 = lane + 32 < nvq ? __ldg(qe + 32 + lane) : 0ull;
     };
     if (todo) prefetch(__ffs(todo) - 1);
-    unsigned long long c_tests = 0, c_px = 0;
+    unsigned long long c_tests = 0;
     const unsigned bit0 = 1u << (lane & 15), bit1 = 1u << ((lane & 15) + 16);
     while (todo) {
       const int j = __ffs(todo) - 1;
@@ -204,16 +235,6 @@ __global__ void __launch_bounds__(kSmallWarps * 32, SCCG_SMALL_MINB)
       const int4 mm = meta[j];
       const unsigned mj = (unsigned)mm.x, dpj = (unsigned)mm.y, dqj = (unsigned)mm.z;
       const int W = mj & 63, H = (mj >> 6) & 63, nvp = (mj >> 12) & 127, nvq = (mj >> 20) & 127;
-      if ((mj >> 28) & 1u) {
-        // memoized pixelization: row words of both rasters, aligned to the box's
-        // first column (bit x = box column x), AND, popcount, one REDUX
-        const unsigned wp = (unsigned)cp0 >> (-(int)(short)(dpj & 0xffffu));
-        const unsigned wq = (unsigned)cq0 >> (-(int)(short)(dqj & 0xffffu));
-        const unsigned I = __reduce_add_sync(FULL, __popc(wp & wq & low_bits(W)));
-        if (lane == j) myI = I;
-        if (COUNT) c_px += (unsigned long long)W * H;
-        continue;
-      }
       const bool two = max(nvp, nvq) > 32;
       const int cntp = stage_rows(cp0, cp1, nvp, two, (int)(short)(dpj & 0xffffu), (int)dpj >> 16, H, bp);
       const int cntq = stage_rows(cq0, cq1, nvq, two, (int)(short)(dqj & 0xffffu), (int)dqj >> 16, H, bq);
@@ -231,13 +252,11 @@ __global__ void __launch_bounds__(kSmallWarps * 32, SCCG_SMALL_MINB)
       const unsigned cnt = lane < 16 ? __popc(m0 & o0 & wmask) + __popc(m1 & o1 & wmask) : 0u;
       const unsigned I = __reduce_add_sync(FULL, cnt);
       if (lane == j) myI = I;
-      if (COUNT) {
-        c_tests += (unsigned long long)H * (cntp + cntq);
-        c_px += (unsigned long long)W * H;
-      }
+      if (COUNT) c_tests += (unsigned long long)H * (cntp + cntq);
       __syncwarp();  // buffers are rewritten by the next pair
     }
     // ---- lane-parallel outputs and batch totals
+    const unsigned long long c_px_all = COUNT ? warp_sum_u64(small ? (unsigned long long)W * H : 0ull) : 0ull;
     const bool done = ok && (small || empty);
     unsigned long long v_i = 0, v_u = 0, v_ap = 0, v_aq = 0, l0 = 0, l1 = 0, l2 = 0, l3 = 0;
     unsigned nz = 0;
@@ -283,7 +302,7 @@ __global__ void __launch_bounds__(kSmallWarps * 32, SCCG_SMALL_MINB)
       a[9] += l3;
       if (COUNT) {
         a[11] += c_tests;
-        a[12] += c_px;
+        a[12] += c_px_all;
         a[13] += n_small;
       }
     }
