@@ -194,18 +194,35 @@ __global__ void __launch_bounds__(kSmallWarps * 32, SCCG_SMALL_MINB)
       rcnt[lane] = 0u;
       __syncwarp();
       int jr = 0;
-#pragma unroll 2
-      for (int t = lane; t < R; t += 32) {
-        while (rstart[jr + 1] <= t) jr++;
-        const int r = t - rstart[jr];
-        const int4 mm = meta[jr];
-        const int2 e = epq[jr];
-        const unsigned mj = (unsigned)mm.x;
-        const unsigned* rp = reinterpret_cast<const unsigned*>(Ps.edges + e.x + ((mj >> 12) & 127));
-        const unsigned* rq = reinterpret_cast<const unsigned*>(Qs.edges + e.y + ((mj >> 20) & 127));
-        const unsigned wp = __ldg(rp + r - (mm.y >> 16)) >> (-(int)(short)(mm.y & 0xffff));
-        const unsigned wq = __ldg(rq + r - (mm.z >> 16)) >> (-(int)(short)(mm.z & 0xffff));
-        atomicAdd(&rcnt[jr], (unsigned)__popc(wp & wq & low_bits(mj & 63)));
+      const unsigned le = lanemask_lt() | (1u << lane);
+      for (int t0 = 0; t0 < R; t0 += 32) {  // warp-uniform trip count
+        const int t = t0 + lane;
+        const bool act = t < R;
+        unsigned c = 0u;
+        bool head = false;
+        if (act) {
+          while (rstart[jr + 1] <= t) jr++;
+          const int r = t - rstart[jr];
+          head = r == 0 || lane == 0;
+          const int4 mm = meta[jr];
+          const int2 e = epq[jr];
+          const unsigned mj = (unsigned)mm.x;
+          const unsigned* rp = reinterpret_cast<const unsigned*>(Ps.edges + e.x + ((mj >> 12) & 127));
+          const unsigned* rq = reinterpret_cast<const unsigned*>(Qs.edges + e.y + ((mj >> 20) & 127));
+          const unsigned wp = __ldg(rp + r - (mm.y >> 16)) >> (-(int)(short)(mm.y & 0xffff));
+          const unsigned wq = __ldg(rq + r - (mm.z >> 16)) >> (-(int)(short)(mm.z & 0xffff));
+          c = (unsigned)__popc(wp & wq & low_bits(mj & 63));
+        }
+        // lanes hold consecutive items, so each pair is one lane segment: reduce
+        // per segment (REDUX with the segment's member mask), one add per pair
+        const unsigned heads = __ballot_sync(FULL, head || !act);
+        const unsigned mine = 31 - __clz(heads & le);
+        const unsigned after = heads & ~le;
+        const unsigned next = after ? (unsigned)(__ffs(after) - 1) : 32u;
+        const unsigned seg = low_bits((int)next) & ~low_bits((int)mine);
+        const unsigned tot = __reduce_add_sync(seg, c);
+        if (act && lane == (int)mine) rcnt[jr] += tot;
+        __syncwarp();
       }
       __syncwarp();
       if (rast) myI = rcnt[lane];
