@@ -112,6 +112,10 @@ __global__ void __launch_bounds__(kSmallWarps * 32, SCCG_SMALL_MINB)
   __shared__ unsigned long long s_acc[kSmallWarps][16];
   __shared__ int s_rstart[kSmallWarps][33];  // raster pairs: first (pair, row) item of each pair
   __shared__ unsigned s_rcnt[kSmallWarps][32];
+  __shared__ const unsigned* s_rp[kSmallWarps][32];  // raster row of box row 0, per pair (p and q)
+  __shared__ const unsigned* s_rq[kSmallWarps][32];
+  __shared__ unsigned s_rsh[kSmallWarps][32];        // column shifts (p, q) and box width
+  __shared__ unsigned char s_rmap[kSmallWarps][1024]; // item -> pair
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   int2* bp = s_buf[warp];
   int2* bq = bp + kSmallQOff;
@@ -189,39 +193,52 @@ __global__ void __launch_bounds__(kSmallWarps * 32, SCCG_SMALL_MINB)
       const int R = __shfl_sync(FULL, sc, 31);
       int* rstart = s_rstart[warp];
       unsigned* rcnt = s_rcnt[warp];
+      unsigned char* rmap = s_rmap[warp];
       rstart[lane] = sc - hl;
-      if (lane == 31) rstart[32] = R;
       rcnt[lane] = 0u;
+      if (rast) {
+        const int4 mm = meta[lane];
+        const int2 e = epq[lane];
+        const unsigned mj = (unsigned)mm.x;
+        s_rp[warp][lane] = reinterpret_cast<const unsigned*>(Ps.edges + e.x + ((mj >> 12) & 127)) - (mm.y >> 16);
+        s_rq[warp][lane] = reinterpret_cast<const unsigned*>(Qs.edges + e.y + ((mj >> 20) & 127)) - (mm.z >> 16);
+        s_rsh[warp][lane] = (unsigned)(-(int)(short)(mm.y & 0xffff)) | ((unsigned)(-(int)(short)(mm.z & 0xffff)) << 8) |
+                            ((unsigned)W << 16);
+      }
+      // item -> pair map, written cooperatively pair by pair
+      for (unsigned m = rmask; m; m &= m - 1) {
+        const int j = __ffs(m) - 1;
+        const int st = __shfl_sync(FULL, sc - hl, j), hj = __shfl_sync(FULL, hl, j);
+        if (lane < hj) rmap[st + lane] = (unsigned char)j;
+      }
       __syncwarp();
-      int jr = 0;
       const unsigned le = lanemask_lt() | (1u << lane);
       for (int t0 = 0; t0 < R; t0 += 32) {  // warp-uniform trip count
         const int t = t0 + lane;
         const bool act = t < R;
         unsigned c = 0u;
-        bool head = false;
+        int jr = 0;
+        bool head = !act || lane == 0;
         if (act) {
-          while (rstart[jr + 1] <= t) jr++;
+          jr = rmap[t];
           const int r = t - rstart[jr];
-          head = r == 0 || lane == 0;
-          const int4 mm = meta[jr];
-          const int2 e = epq[jr];
-          const unsigned mj = (unsigned)mm.x;
-          const unsigned* rp = reinterpret_cast<const unsigned*>(Ps.edges + e.x + ((mj >> 12) & 127));
-          const unsigned* rq = reinterpret_cast<const unsigned*>(Qs.edges + e.y + ((mj >> 20) & 127));
-          const unsigned wp = __ldg(rp + r - (mm.y >> 16)) >> (-(int)(short)(mm.y & 0xffff));
-          const unsigned wq = __ldg(rq + r - (mm.z >> 16)) >> (-(int)(short)(mm.z & 0xffff));
-          c = (unsigned)__popc(wp & wq & low_bits(mj & 63));
+          head |= r == 0;
+          const unsigned sh = s_rsh[warp][jr];
+          const unsigned wp = __ldg(s_rp[warp][jr] + r) >> (sh & 0xffu);
+          const unsigned wq = __ldg(s_rq[warp][jr] + r) >> ((sh >> 8) & 0xffu);
+          c = (unsigned)__popc(wp & wq & low_bits((int)(sh >> 16)));
         }
-        // lanes hold consecutive items, so each pair is one lane segment: reduce
-        // per segment (REDUX with the segment's member mask), one add per pair
-        const unsigned heads = __ballot_sync(FULL, head || !act);
-        const unsigned mine = 31 - __clz(heads & le);
+        // each pair's items occupy consecutive lanes: segmented shuffle sum, the
+        // segment's first lane adds it to the pair's count
+        const unsigned heads = __ballot_sync(FULL, head);
         const unsigned after = heads & ~le;
-        const unsigned next = after ? (unsigned)(__ffs(after) - 1) : 32u;
-        const unsigned seg = low_bits((int)next) & ~low_bits((int)mine);
-        const unsigned tot = __reduce_add_sync(seg, c);
-        if (act && lane == (int)mine) rcnt[jr] += tot;
+        const int next = after ? __ffs(after) - 1 : 32;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const unsigned v = __shfl_down_sync(FULL, c, o);
+          if (lane + o < next) c += v;
+        }
+        if (act && ((heads >> lane) & 1u)) rcnt[jr] += c;
         __syncwarp();
       }
       __syncwarp();

@@ -9,17 +9,50 @@
 // polygon's vertex slot, horizontal edges to the back); and the per-set
 // statistics the grid-hash join sizes its grid from.
 //
-// HBM-bound pass: a CTA stages the vertex range of 64 consecutive polygons
-// (one coalesced sweep) in shared memory, then each warp derives its polygons
-// from shared memory.  Ranges larger than the tile fall back to reading the
-// polygon's vertices from global memory (same code, other pointer).
+// A CTA stages the vertex range of 128 consecutive polygons in shared memory
+// with one TMA bulk copy, derives each small polygon by one thread (large ones
+// by a warp) in place, and writes the slots back with one TMA bulk store.
+// Ranges larger than the tile fall back to reading the polygon's vertices from
+// global memory (warp per polygon).
 #include "internal.cuh"
 
 namespace sccg {
 
 constexpr int kPrepThreads = 128;
 constexpr int kPrepPolys = 128;   // one ring per thread per tile
+constexpr int kPrepWarps = kPrepThreads / 32;
+static_assert(kPrepPolys == kPrepThreads, "one ring per thread per tile");
 constexpr int kPrepVerts = 5120;  // 40 KB of int2 staged per tile (dynamic shared memory)
+
+
+// ---- 1-D bulk copies on the TMA engine (cp.async.bulk): the tile is staged
+// and written back without LSU traffic.  Addresses 16-byte aligned, sizes a
+// multiple of 16.
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra.uni WAIT%=;\n}\n" ::"r"(
+          smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_store(void* dst, const void* src, unsigned bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(dst), "r"(smem_u32(src)), "r"(bytes)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+}
+__device__ __forceinline__ void bulk_store_drain() { asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
 
 __device__ __forceinline__ void flag(uint32_t* status, uint32_t bit, int64_t poly) {
   atomicOr(&status[0], bit);
@@ -101,18 +134,23 @@ __device__ __forceinline__ int4 prep_polygon(const int2* v, int64_t V, int64_t p
 // shoelace product fits 32 bits unsigned; the sum is int64).  Records are
 // written in place over the ring's own vertex slot: record k lands in slot
 // k <= i - 1 while vertex i is being read.
-__device__ __forceinline__ int4 prep_polygon_thread(int2* v, int V, int64_t poly, int4* __restrict__ mbr,
+__device__ __forceinline__ int4 prep_polygon_thread(int2* v, int V, int rot, int64_t poly, int4* __restrict__ mbr,
                                                     int64_t* __restrict__ area, int2* __restrict__ ecount,
                                                     uint32_t* __restrict__ status, int validate) {
+  // MBR: order-free, so each thread starts at vertex `rot` (chosen by the
+  // caller so the lockstep reads of a half-warp hit distinct bank pairs) and
+  // wraps around
   int xmin = INT_MAX, ymin = INT_MAX, xmax = INT_MIN, ymax = INT_MIN;
-#pragma unroll 4
-  for (int i = 0; i < V; i++) {
-    const int2 a = v[i];
+  auto take = [&](const int2 a) {
     xmin = min(xmin, a.x);
     xmax = max(xmax, a.x);
     ymin = min(ymin, a.y);
     ymax = max(ymax, a.y);
-  }
+  };
+#pragma unroll 4
+  for (int i = rot; i < V; i++) take(v[i]);
+#pragma unroll 4
+  for (int i = 0; i < rot; i++) take(v[i]);
   const int4 m = make_int4(xmin, ymin, xmax, ymax);
   mbr[poly] = m;
   if ((int64_t)xmin < -kMaxCoord || (int64_t)xmax > kMaxCoord || (int64_t)ymin < -kMaxCoord ||
@@ -139,7 +177,19 @@ __device__ __forceinline__ int4 prep_polygon_thread(int2* v, int V, int64_t poly
     ax = cx;
     ay = cy;
   };
-  for (int i = 1; i < V; i++) {
+  // Vertices are loaded four at a time ahead of the record stores: the store of
+  // edge i lands in slot <= i - 1, below every prefetched vertex, so loading
+  // early is safe (the compiler cannot prove it and would otherwise serialise
+  // each load behind the previous store).
+  int i = 1;
+  for (; i + 4 <= V; i += 4) {
+    const int2 c0 = v[i], c1 = v[i + 1], c2 = v[i + 2], c3 = v[i + 3];
+    edge((unsigned)(c0.x - xmin), (unsigned)(c0.y - ymin));
+    edge((unsigned)(c1.x - xmin), (unsigned)(c1.y - ymin));
+    edge((unsigned)(c2.x - xmin), (unsigned)(c2.y - ymin));
+    edge((unsigned)(c3.x - xmin), (unsigned)(c3.y - ymin));
+  }
+  for (; i < V; i++) {
     const int2 c = v[i];
     edge((unsigned)(c.x - xmin), (unsigned)(c.y - ymin));
   }
@@ -155,18 +205,42 @@ __device__ __forceinline__ int4 prep_polygon_thread(int2* v, int V, int64_t poly
   const int W = xmax - xmin, H = ymax - ymin;
   bool raster = !diag && W <= 32 && 2 * (V - nvert) >= H;
   if (raster) {
+    // The row updates are return-free shared atomics (no load -> store chain
+    // per update) fed by records read four at a time; the prefix pass reads
+    // four rows ahead of its stores (distinct rows, so reordering is safe).
     unsigned* D = reinterpret_cast<unsigned*>(out + nvert);
     for (int r = 0; r < H; r++) D[r] = 0u;
-    for (int k = 0; k < nvert; k++) {
+    auto apply = [&](uint64_t rec) {
       int c, lo, hi;
-      unpack_edge(out[k], c, lo, hi);
+      unpack_edge(rec, c, lo, hi);
       const unsigned m = suffix_mask(c);
-      D[lo] ^= m;
-      if (hi < H) D[hi] ^= m;
+      atomicXor(&D[lo], m);
+      if (hi < H) atomicXor(&D[hi], m);
+    };
+    int k = 0;
+    for (; k + 4 <= nvert; k += 4) {
+      const uint64_t r0 = out[k], r1 = out[k + 1], r2 = out[k + 2], r3 = out[k + 3];
+      apply(r0);
+      apply(r1);
+      apply(r2);
+      apply(r3);
     }
+    for (; k < nvert; k++) apply(out[k]);
     unsigned acc = 0u;
     const unsigned wmask = low_bits(W);
-    for (int r = 0; r < H; r++) {
+    int r = 0;
+    for (; r + 4 <= H; r += 4) {
+      const unsigned d0 = D[r], d1 = D[r + 1], d2 = D[r + 2], d3 = D[r + 3];
+      acc ^= d0;
+      D[r] = acc & wmask;
+      acc ^= d1;
+      D[r + 1] = acc & wmask;
+      acc ^= d2;
+      D[r + 2] = acc & wmask;
+      acc ^= d3;
+      D[r + 3] = acc & wmask;
+    }
+    for (; r < H; r++) {
       acc ^= D[r];
       D[r] = acc & wmask;
     }
@@ -202,6 +276,7 @@ struct StatAcc {
 };
 
 constexpr int kThreadMaxV = 192;  // rings up to this size are prepped by one thread
+constexpr int kSortKeys = 64;     // counting-sort buckets (V / 4) for dealing rings to threads
 
 __global__ void __launch_bounds__(kPrepThreads) prep_kernel(const int2* __restrict__ xy,
                                                             const int64_t* __restrict__ off, int64_t n,
@@ -209,14 +284,20 @@ __global__ void __launch_bounds__(kPrepThreads) prep_kernel(const int2* __restri
                                                             int64_t* __restrict__ area, int2* __restrict__ ecount,
                                                             uint64_t* __restrict__ edges,
                                                             uint32_t* __restrict__ status, SetStats* stats,
-                                                            int validate, int vec16) {
+                                                            int validate, int bulk) {
   extern __shared__ int4 s_dyn4[];  // kPrepVerts int2 (16-byte aligned)
   int2* s_xy = reinterpret_cast<int2*>(s_dyn4);
   __shared__ int64_t s_off[kPrepPolys + 1];
   __shared__ unsigned s_big[kPrepPolys / 32];
+  __shared__ int s_cnt[kSortKeys];
+  __shared__ unsigned char s_perm[kPrepPolys];
   __shared__ unsigned long long s_acc[4];
   __shared__ int s_b[6];
+  __shared__ uint64_t s_bar;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  unsigned phase = 0;
+  if (threadIdx.x == 0) mbar_init(&s_bar);
+  __syncthreads();
   StatAcc acc;
   acc.init();
   const int64_t ntiles = (n + kPrepPolys - 1) / kPrepPolys;
@@ -226,28 +307,48 @@ __global__ void __launch_bounds__(kPrepThreads) prep_kernel(const int2* __restri
     __syncthreads();  // previous tile's shared data fully consumed
     for (int i = threadIdx.x; i <= np; i += blockDim.x) s_off[i] = off[p0 + i];
     if (threadIdx.x < kPrepPolys / 32) s_big[threadIdx.x] = 0;
+    if (threadIdx.x < kSortKeys) s_cnt[threadIdx.x] = 0;
+    s_perm[threadIdx.x] = 0xff;
     __syncthreads();
-    // stage the tile's vertex range: 16-byte cp.async (LDGSTS) from an even
-    // start, no register round trip, many copies in flight per thread
+    // Rings are dealt to threads in order of vertex count (counting sort on
+    // V / 4), round-robin over the warps: the lanes of a warp run loops of
+    // similar length and the warps finish together at the next barrier.
+    int key = 0, pos = 0;
+    if (threadIdx.x < np) {
+      key = (int)min((s_off[threadIdx.x + 1] - s_off[threadIdx.x]) >> 2, (int64_t)kSortKeys - 1);
+      key = max(key, 0);
+      pos = atomicAdd(&s_cnt[key], 1);
+    }
+    // stage the tile's vertex range [v0, v1) (v0 even): one TMA bulk copy of the
+    // 16-byte-aligned body, the odd last vertex by a thread
     const int64_t v0 = s_off[0] & ~int64_t(1), v1 = s_off[np];
     const bool tiled = s_off[0] >= 0 && v1 <= nv_total && v1 >= s_off[0] && v1 - v0 <= kPrepVerts;
     if (tiled) {
       const int64_t nv = v1 - v0;
-      if (vec16) {
-        const int64_t nvec = nv >> 1;
-        const char* src = reinterpret_cast<const char*>(xy + v0);
-        const unsigned dst = (unsigned)__cvta_generic_to_shared(s_dyn4);
-        for (int64_t i = threadIdx.x; i < nvec; i += blockDim.x)
-          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst + (unsigned)(16 * i)), "l"(src + 16 * i));
-        if ((nv & 1) && threadIdx.x == 0) s_xy[nv - 1] = xy[v1 - 1];
-        asm volatile("cp.async.wait_all;\n" ::);
+      if (bulk) {
+        if (threadIdx.x == 0) {
+          bulk_store_drain();  // the previous tile's write-back has read the buffer
+          fence_async_smem();
+          if (nv >= 2) bulk_load(s_dyn4, xy + v0, (unsigned)(nv >> 1) * 16u, &s_bar);
+          if (nv & 1) s_xy[nv - 1] = xy[v1 - 1];
+        }
+        if (nv >= 2) {
+          mbar_wait(&s_bar, phase);
+          phase ^= 1u;
+        }
       } else {
         for (int64_t i = threadIdx.x; i < nv; i += blockDim.x) s_xy[i] = xy[v0 + i];
       }
     }
+    if (threadIdx.x < np) {
+      int rank = pos;
+      for (int k = 0; k < key; k++) rank += s_cnt[k];
+      s_perm[(rank % kPrepWarps) * 32 + rank / kPrepWarps] = (unsigned char)threadIdx.x;
+    }
     __syncthreads();
     // thread per small ring (records in place in the tile)
-    for (int j = threadIdx.x; j < np; j += blockDim.x) {
+    if (s_perm[threadIdx.x] != 0xff) {
+      const int j = s_perm[threadIdx.x];
       const int64_t poly = p0 + j;
       const int64_t b = s_off[j], e = s_off[j + 1];
       const int64_t V = e - b;
@@ -256,13 +357,12 @@ __global__ void __launch_bounds__(kPrepThreads) prep_kernel(const int2* __restri
         area[poly] = 0;
         ecount[poly] = make_int2(0, 0);
         flag(status, SCCG_STATUS_ARG, poly);
-        continue;
-      }
-      if (V > kThreadMaxV || !tiled) {
+      } else if (V > kThreadMaxV || !tiled) {
         atomicOr(&s_big[j >> 5], 1u << (j & 31));
-        continue;
+      } else {
+        const int rot = (int)((lane - (b - v0)) & 15) % (int)V;
+        acc.add(prep_polygon_thread(s_xy + (b - v0), (int)V, rot, poly, mbr, area, ecount, status, validate));
       }
-      acc.add(prep_polygon_thread(s_xy + (b - v0), (int)V, poly, mbr, area, ecount, status, validate));
     }
     __syncthreads();
     // warp per large ring (in the tile when tiled, else straight from global)
@@ -282,18 +382,27 @@ __global__ void __launch_bounds__(kPrepThreads) prep_kernel(const int2* __restri
       }
     }
     __syncthreads();
-    // coalesced write-out of the tile's records (16-byte stores when aligned)
+    // write-back of the tile's slots [off[p0], v1) -- exactly this tile's rings
+    // (v0 may be the previous tile's last slot): one TMA bulk store of the
+    // 16-byte-aligned body, the odd ends by a thread
     if (tiled) {
-      const int64_t nv = v1 - v0;
-      if (vec16 && (reinterpret_cast<uintptr_t>(edges) & 15) == 0) {
-        int4* dst = reinterpret_cast<int4*>(edges + v0);
-        for (int64_t i = threadIdx.x; i < (nv >> 1); i += blockDim.x) dst[i] = s_dyn4[i];
-        if ((nv & 1) && threadIdx.x == 0) edges[v1 - 1] = reinterpret_cast<const uint64_t*>(s_xy)[nv - 1];
+      const int64_t s0 = s_off[0];
+      const int64_t a0 = (s0 + 1) & ~int64_t(1), a1 = v1 & ~int64_t(1);
+      const uint64_t* rec = reinterpret_cast<const uint64_t*>(s_xy);
+      if (bulk) {
+        fence_async_smem();  // this thread's shared-memory records -> async proxy
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          if (a1 > a0) bulk_store(edges + a0, rec + (a0 - v0), (unsigned)(a1 - a0) * 8u);
+          if (s0 < a0 && s0 < v1) edges[s0] = rec[s0 - v0];
+          if (a1 < v1 && a1 >= a0) edges[a1] = rec[a1 - v0];
+        }
       } else {
-        for (int64_t i = threadIdx.x; i < nv; i += blockDim.x) edges[v0 + i] = reinterpret_cast<const uint64_t*>(s_xy)[i];
+        for (int64_t i = s0 + threadIdx.x; i < v1; i += blockDim.x) edges[i] = rec[i - v0];
       }
     }
   }
+  if (threadIdx.x == 0) bulk_store_drain();
   // block reduction of the statistics, then one atomic per field
   if (threadIdx.x < 4) s_acc[threadIdx.x] = 0;
   if (threadIdx.x == 0) {
@@ -366,7 +475,7 @@ cudaError_t launch_prep(const sccg_polyset* s, int validate, cudaStream_t st) {
     prep_kernel<<<(unsigned)blocks, kPrepThreads, kPrepVerts * sizeof(int2), st>>>(
         reinterpret_cast<const int2*>(s->xy), s->offsets, s->n_polygons, s->n_vertices,
         reinterpret_cast<int4*>(s->mbr), s->area, reinterpret_cast<int2*>(s->ecount), s->edges, s->status, stats,
-        validate, (reinterpret_cast<uintptr_t>(s->xy) & 15) == 0 ? 1 : 0);
+        validate, ((reinterpret_cast<uintptr_t>(s->xy) | reinterpret_cast<uintptr_t>(s->edges)) & 15) == 0 ? 1 : 0);
   }
   return cudaGetLastError();
 }

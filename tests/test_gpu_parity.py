@@ -79,6 +79,32 @@ def test_prep_matches_oracle(sccg, tile_sets):
         assert D.status.cpu().tolist()[0] == 0
 
 
+def test_prep_tiles_at_odd_offsets(sccg):
+    """Prep's 128-ring tiles start at odd vertex offsets (an odd-V ring opens
+    every tile) and every tile ends with a 4-vertex rect whose records + raster
+    fill its whole slot: a tile's write-back must not touch the previous tile's
+    last slot.  The rects' pairs are checked against the oracle."""
+    penta = lambda x, y: [[x, y], [x + 4, y], [x + 4, y + 2], [x + 2, y + 4], [x, y + 4]]
+    rect = lambda x, y, w, h: [[x, y], [x + w, y], [x + w, y + h], [x, y + h]]
+    rings_p, rings_q = [], []
+    rng = np.random.default_rng(17)
+    for t in range(300):
+        y0 = 40 * t
+        rings_p.append(penta(0, y0))
+        rings_p += [rect(10 + 3 * i, y0, 2, 2) for i in range(126)]
+        h = int(rng.integers(3, 5))
+        rings_p.append(rect(500, y0, 5, h))  # raster: 2 records + ceil(h/2) row slots = V
+        rings_q.append(rect(502, y0 + 1, 6, 5))
+    A, B = synth.pack(rings_p), synth.pack(rings_q)
+    xy, off = sccg.to_device(A.xy, A.offsets)
+    P = sccg.DeviceSet(xy, off, validate=False)
+    Q = dev(B, sccg)
+    pairs = sccg.filter_pairs(P, Q)
+    assert pairs.shape[0] == 300
+    inter, uni, sums = sccg.pixelbox(P, Q, pairs, threshold=2048)
+    check_batch(sccg, A, B, pairs.cpu().numpy(), inter, uni, sums)
+
+
 # ---------------------------------------------------------------- filter
 @pytest.mark.parametrize("config", ["tile", "skewed"])
 def test_filter_pairs_matches_oracle(sccg, config):
