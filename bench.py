@@ -15,8 +15,10 @@ configs[3]); the only collective is the sums all_reduce.
 Prints ONE JSON line (rank 0).  value = pairs/s over all ranks (max-over-ranks
 device time).  e2e = the same metric through the public API with host inputs
 (pinned H2D copies + D2H of the sums inside the timed region).  roofline =
-the PixelBox kernel's integer lane-op rate against the
-B200 issue peak.  cpu_baseline = the oracle (oracle/) on this box's cores.
+the dominant kernel, prep (about half the step): its algorithmic HBM bytes per
+launch over its live CUDA-event time inside the timed
+region, against the measured HBM copy bandwidth (MEASURED_PEAKS.json).
+cpu_baseline = the oracle (oracle/) on this box's cores.
 """
 from __future__ import annotations
 
@@ -109,6 +111,28 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------- workloads
+def prep_algorithmic_bytes(sccg, S) -> int:
+    """Bytes prep must move for set S: read the vertices (8 B)
+    and offsets (8 B); write MBR (16 B), area (8 B), ecount (8 B) per polygon,
+    one 8-byte record per vertical edge and one 4-byte word per raster row."""
+    ec = S.ecount.long()
+    m = S.mbr.long()
+    rast = (ec[:, 1] & sccg.RASTER_FLAG) != 0
+    rows = int(((m[:, 3] - m[:, 1]) * rast).sum())
+    return 8 * S.nv + 8 * (S.n + 1) + 32 * S.n + 8 * int(ec[:, 0].sum()) + 4 * rows
+
+
+def hbm_peak():
+    """Measured HBM copy bandwidth (MEASURED_PEAKS.json), else the profiling
+    guide's fallback."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            v = float(json.load(f)["hbm_gbs"])
+        return v, "MEASURED_PEAKS.json hbm_gbs (copy bandwidth, read+write)"
+    except Exception:
+        return 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
+
+
 def make_workload(config: str, image: int):
     import synth
 
@@ -155,11 +179,10 @@ def run_ours(args, rank, world, local_rank):
     # the whole step (prep x2, join, PixelBox) device-resident, no host sync until
     # the sums are read; replayed as two CUDA graphs (join | PixelBox)
     pipe = sccg.Pipeline(P, Q, cap=3 * max(P.n, Q.n) + 1024, threshold=args.threshold, graph=True)
-    pix_start = torch.cuda.Event(enable_timing=True)
-    pix_end = torch.cuda.Event(enable_timing=True)
+    stage_ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
 
-    def step(timing_pixelbox=False):
-        sums = pipe.run((pix_start, pix_end) if timing_pixelbox else None)
+    def step(timing=False):
+        sums = pipe.run(stage_ev if timing else None)
         sdist.allreduce_sums(sums)  # row a9: the only collective (NCCL, int64 SUM)
         return sccg.sums_to_host(sums.cpu())  # the step's one host synchronisation
 
@@ -178,13 +201,14 @@ def run_ours(args, rank, world, local_rank):
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    pix_total = 0.0
+    stage_ms = [0.0, 0.0, 0.0]  # prep x2 | join | PixelBox, live CUDA events on the launch stream
     with ClockSampler(local_rank) as clk:
         t0.record(stream)
         wall0 = time.perf_counter()
         for _ in range(args.steps):
-            host = step(timing_pixelbox=True)
-            pix_total += pix_start.elapsed_time(pix_end)
+            host = step(timing=True)
+            for k in range(3):
+                stage_ms[k] += stage_ev[k].elapsed_time(stage_ev[k + 1])
         t1.record(stream)
         torch.cuda.synchronize()
         wall1 = time.perf_counter()
@@ -192,7 +216,8 @@ def run_ours(args, rank, world, local_rank):
         dist.barrier()
     pipe.check()
     ms = t0.elapsed_time(t1)
-    times = torch.tensor([ms, pix_total / args.steps, float(n_local)], dtype=torch.float64, device=dev)
+    times = torch.tensor([ms] + [t / args.steps for t in stage_ms] + [float(n_local)], dtype=torch.float64,
+                         device=dev)
     if world > 1:
         mx = times.clone()
         dist.all_reduce(mx, op=dist.ReduceOp.MAX)
@@ -200,8 +225,8 @@ def run_ours(args, rank, world, local_rank):
         dist.all_reduce(tot, op=dist.ReduceOp.SUM)
     else:
         mx, tot = times, times
-    ms_max, pix_ms_max = float(mx[0]), float(mx[1])
-    total_pairs = int(round(float(tot[2])))
+    ms_max, prep_ms_max, join_ms_max, pix_ms_max = (float(v) for v in mx[:4])
+    total_pairs = int(round(float(tot[4])))
     jprime, pooled = sccg.jaccard(host)
     state = {"cap": 3 * max(P.n, Q.n) + 1024}
 
@@ -244,16 +269,15 @@ def run_ours(args, rank, world, local_rank):
         return None
     value = total_pairs * args.steps / (ms_max / 1e3)
     clocks = clk.summary()
-    # roofline of the dominant kernel (PixelBox), rank 0's algorithmic work per launch
-    ops = OPS_PER_ROWTEST * cnt[sccg.CNT_ROWTESTS] + OPS_PER_BOXEDGE * cnt[sccg.CNT_BOXEDGES]
-    pix_s = pix_ms_max / 1e3
-    achieved = ops / pix_s / 1e9
-    peak_mhz = clocks["sm_max_mhz"] or 1965.0
-    props = torch.cuda.get_device_properties(dev)
-    sms = props.multi_processor_count
-    peak = sms * ISSUE_LANES_PER_CLK_SM * peak_mhz * 1e6 / 1e9
+    # roofline of the dominant kernel: prep (HBM-bound), rank 0's algorithmic
+    # bytes per launch (inputs read once + outputs written once)
+    # over its live per-launch time (the prep interval holds 2 launches)
+    alg = prep_algorithmic_bytes(sccg, P) + prep_algorithmic_bytes(sccg, Q)
+    prep_launch_s = prep_ms_max / 2 / 1e3
+    achieved = (alg / 2) / prep_launch_s / 1e9
+    peak, peak_src = hbm_peak()
     traffic = None
-    prof = os.path.join(ROOT, "profiles", "pixelbox_traffic.json")
+    prof = os.path.join(ROOT, "profiles", "prep_traffic.json")
     if os.path.exists(prof):
         try:
             with open(prof) as f:
@@ -262,6 +286,12 @@ def run_ours(args, rank, world, local_rank):
                 traffic = pj.get("dram_bytes_per_launch")
         except Exception:
             traffic = None
+    # PixelBox (second kernel group): integer lane-op rate vs the issue peak, context only
+    ops = OPS_PER_ROWTEST * cnt[sccg.CNT_ROWTESTS] + OPS_PER_BOXEDGE * cnt[sccg.CNT_BOXEDGES]
+    pix_s = pix_ms_max / 1e3
+    peak_mhz = clocks["sm_max_mhz"] or 1965.0
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    alu_peak = sms * ISSUE_LANES_PER_CLK_SM * peak_mhz * 1e6 / 1e9
     launches_per_step = 16  # prep 2x2, join 9 (incl. 2 CUB scans x2), pixelbox 2 + memsets (see profiles/)
     out = {
         "metric": METRIC,
@@ -289,14 +319,17 @@ def run_ours(args, rank, world, local_rank):
             "parallelism": f"image-sharded x{world}" if world > 1 else "1 GPU",
         },
         "pixels_tested_per_s": cnt[sccg.CNT_PIXELS] * world / pix_s,
-        "pixelbox_ms": pix_ms_max,
+        "stage_ms": {"prep_x2": prep_ms_max, "join": join_ms_max, "pixelbox": pix_ms_max},
         "jprime": jprime,
         "pooled_jaccard": pooled,
         "counters": {"pixels": cnt[0], "rowtests": cnt[1], "boxes": cnt[2], "boxedges": cnt[3], "splits": cnt[4],
                      "pixboxes": cnt[5], "rootpx": cnt[6]},
-        "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Gop/s", "frac": achieved / peak,
-                     "traffic": traffic, "kernel": "pixelbox_kernel",
-                     "peak_source": f"{sms} SMs x 128 int lanes/clk x {peak_mhz:.0f} MHz (issue peak, DESIGN.md)"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": traffic, "kernel": "prep_kernel", "algorithmic_bytes_per_launch": alg / 2,
+                     "peak_source": peak_src},
+        "pixelbox_alu": {"achieved": ops / pix_s / 1e9, "peak": alu_peak, "unit": "Gop/s",
+                         "frac": ops / pix_s / 1e9 / alu_peak,
+                         "peak_source": f"{sms} SMs x 128 int lanes/clk x {peak_mhz:.0f} MHz (issue peak)"},
         "e2e": {"value": e2e_value, "unit": "pairs/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                 "steps": e2e_steps},
         "gpu_launches": launches_per_step * args.steps,

@@ -31,6 +31,7 @@ _lib = None
 
 # status codes (include/sccg.h)
 OK, E_ARG, E_NOT_RECTILINEAR, E_RANGE, E_CAPACITY, E_STACK, E_EMPTY, E_CUDA, E_WORKSPACE = range(9)
+RASTER_FLAG = 1 << 30  # ecount[i, 1] bit: prep stored polygon i's raster rows
 FLAG_NO_RASTER = 1
 CNT_PIXELS, CNT_ROWTESTS, CNT_BOXES, CNT_BOXEDGES, CNT_SPLITS, CNT_PIXBOXES, CNT_ROOTPX = range(7)
 SUMS_FIELDS = ("n_pairs", "n_nonzero", "sum_inter", "sum_union", "sum_area_p", "sum_area_q", "limb0", "limb1",
@@ -217,6 +218,11 @@ class DeviceSet:
         return self._view("area", _torch().int64, (self.n,))
 
     @property
+    def ecount(self):
+        """int32 [n, 2]: vertical-edge records, horizontal edges | RASTER_FLAG."""
+        return self._view("ecount", _torch().int32, (self.n, 2))
+
+    @property
     def status(self):
         return self._view("status", _torch().int32, (2,))
 
@@ -270,26 +276,33 @@ class Pipeline:
             s = torch.cuda.Stream(device=dev)
             s.wait_stream(torch.cuda.current_stream(dev))
             with torch.cuda.stream(s):  # warm-up outside capture (one-time attribute setup)
-                self._enqueue_filter()
-                self._enqueue_pixelbox()
+                for stage in self._stages:
+                    stage()
             torch.cuda.current_stream(dev).wait_stream(s)
             torch.cuda.synchronize(dev)
-            gf, gp = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
-            with torch.cuda.graph(gf):
-                self._enqueue_filter()
-            with torch.cuda.graph(gp):
-                self._enqueue_pixelbox()
-            self.graphs = (gf, gp)
+            graphs = []
+            for stage in self._stages:
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g):
+                    stage()
+                graphs.append(g)
+            self.graphs = tuple(graphs)
 
-    def _enqueue_filter(self):
+    @property
+    def _stages(self):
+        return (self._enqueue_prep, self._enqueue_join, self._enqueue_pixelbox)
+
+    def _enqueue_prep(self):
         st = _stream_ptr()
         lib = self.lib
         self.sums.zero_()
         _check(lib.sccg_prep(ctypes.byref(self.P.c), self.validate, st), "sccg_prep")
         _check(lib.sccg_prep(ctypes.byref(self.Q.c), self.validate, st), "sccg_prep")
-        _check(lib.sccg_filter_pairs_async(ctypes.byref(self.P.c), ctypes.byref(self.Q.c), self.pairs.data_ptr(),
-                                           self.cap, self.result.data_ptr(), self.fws.data_ptr(), self.fws_bytes, st),
-               "sccg_filter_pairs_async")
+
+    def _enqueue_join(self):
+        _check(self.lib.sccg_filter_pairs_async(ctypes.byref(self.P.c), ctypes.byref(self.Q.c), self.pairs.data_ptr(),
+                                                self.cap, self.result.data_ptr(), self.fws.data_ptr(), self.fws_bytes,
+                                                _stream_ptr()), "sccg_filter_pairs_async")
 
     def _enqueue_pixelbox(self):
         _check(self.lib.sccg_pixelbox_async(ctypes.byref(self.P.c), ctypes.byref(self.Q.c), self.pairs.data_ptr(),
@@ -297,23 +310,20 @@ class Pipeline:
                                             ctypes.byref(self.cfg), self.pws.data_ptr(), self.pws_bytes, _stream_ptr()),
                "sccg_pixelbox_async")
 
-    def run(self, pix_events=None):
-        """One step: prep x2 + join (graph 1), PixelBox (graph 2).  pix_events =
-        (start, end) CUDA events recorded around the PixelBox part."""
-        if self.graphs is not None:
-            self.graphs[0].replay()
-            if pix_events:
-                pix_events[0].record()
-            self.graphs[1].replay()
-            if pix_events:
-                pix_events[1].record()
-        else:
-            self._enqueue_filter()
-            if pix_events:
-                pix_events[0].record()
-            self._enqueue_pixelbox()
-            if pix_events:
-                pix_events[1].record()
+    def run(self, events=None):
+        """One step: prep(P) + prep(Q) | MBR join | PixelBox, three graphs (or
+        eager launches) back to back on the current stream.  events = four CUDA
+        events recorded before prep, after prep, after the join and after
+        PixelBox (per-stage device times)."""
+        for k, stage in enumerate(self._stages):
+            if events:
+                events[k].record()
+            if self.graphs is not None:
+                self.graphs[k].replay()
+            else:
+                stage()
+        if events:
+            events[3].record()
         return self.sums
 
     def check(self):
