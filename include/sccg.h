@@ -105,6 +105,13 @@ SCCG_API int sccg_polyset_bind(sccg_polyset* set, void* buf, size_t bytes);
  * fills set->status.  validate = 1 checks rectilinearity, ranges, offsets. */
 SCCG_API int sccg_prep(const sccg_polyset* set, int32_t validate, sccg_stream_t stream);
 
+/* sccg_prep of `count` (1..4) independent sets in ONE launch: the sets' tiles
+ * share one dynamically scheduled index space (one tail instead of one per
+ * set).  `sets` is a host array of bound sets whose derived buffers are
+ * disjoint; results are identical to calling sccg_prep on each.  Errors:
+ * SCCG_E_ARG for count outside 1..4, a bad set, or shared derived buffers. */
+SCCG_API int sccg_prep_sets(const sccg_polyset* sets, int32_t count, int32_t validate, sccg_stream_t stream);
+
 /* ---------------------------------------------------------------- filter */
 /* Workspace bytes sccg_filter_pairs needs for sets of these sizes. */
 SCCG_API size_t sccg_filter_workspace_bytes(int64_t n_p, int64_t n_q);

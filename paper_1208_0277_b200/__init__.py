@@ -36,7 +36,7 @@ FLAG_NO_RASTER = 1
 CNT_PIXELS, CNT_ROWTESTS, CNT_BOXES, CNT_BOXEDGES, CNT_SPLITS, CNT_PIXBOXES, CNT_ROOTPX = range(7)
 SUMS_FIELDS = ("n_pairs", "n_nonzero", "sum_inter", "sum_union", "sum_area_p", "sum_area_q", "limb0", "limb1",
                "limb2", "limb3", "status")
-SYMBOLS = ("sccg_polyset_bytes", "sccg_polyset_bind", "sccg_prep", "sccg_filter_workspace_bytes",
+SYMBOLS = ("sccg_polyset_bytes", "sccg_polyset_bind", "sccg_prep", "sccg_prep_sets", "sccg_filter_workspace_bytes",
            "sccg_filter_pairs", "sccg_filter_pairs_async", "sccg_pixelbox_workspace_bytes", "sccg_pixelbox",
            "sccg_pixelbox_async", "sccg_count_missing", "sccg_jaccard", "sccg_strerror", "sccg_last_error_string", "sccg_last_error_index",
            "sccg_version")
@@ -118,6 +118,8 @@ def load(build: bool = True):
         lib.sccg_polyset_bind.restype = cint
         lib.sccg_prep.argtypes = [ps, i32, vp]
         lib.sccg_prep.restype = cint
+        lib.sccg_prep_sets.argtypes = [ps, i32, i32, vp]
+        lib.sccg_prep_sets.restype = cint
         lib.sccg_filter_workspace_bytes.argtypes = [i64, i64]
         lib.sccg_filter_workspace_bytes.restype = sz
         lib.sccg_filter_pairs.argtypes = [ps, ps, vp, i64, ctypes.POINTER(i64), vp, sz, vp]
@@ -226,6 +228,30 @@ class DeviceSet:
     def status(self):
         return self._view("status", _torch().int32, (2,))
 
+    def stats_bytes(self):
+        """The 128-byte join statistics block (internal layout)."""
+        return self._view("stats", _torch().uint8, (128,))
+
+    def used_edge_words(self):
+        """The defined part of `edges` after prep, concatenated over polygons:
+        each polygon's vertical-edge records, then its raster rows (as 32-bit
+        words, when ecount flags one).  For tests and diagnostics."""
+        torch = _torch()
+        edges = self._view("edges", torch.int64, (self.nv,))
+        ec = self.ecount.long()
+        m = self.mbr.long()
+        rast = (ec[:, 1] & RASTER_FLAG) != 0
+        used = ec[:, 0] + torch.where(rast, (m[:, 3] - m[:, 1] + 1) // 2, torch.zeros_like(ec[:, 0]))
+        off = self.offsets[:-1]
+        idx = torch.repeat_interleave(off, used) + (
+            torch.arange(int(used.sum()), device=used.device) - torch.repeat_interleave(torch.cumsum(used, 0) - used, used))
+        words = edges[idx].clone()
+        # an odd raster row count leaves the upper half of the last slot undefined
+        odd = rast & ((m[:, 3] - m[:, 1]) % 2 == 1)
+        last = (torch.cumsum(used, 0) - 1)[odd]
+        words[last] &= 0xFFFFFFFF
+        return words
+
 
 def filter_pairs(P: DeviceSet, Q: DeviceSet, cap: int | None = None, stream=None):
     """Candidate pairs (overlapping half-open MBRs), int32 [N, 2] sorted by (p, q)."""
@@ -271,6 +297,7 @@ class Pipeline:
         self.pws = torch.empty(max(self.pws_bytes, 256), dtype=torch.uint8, device=dev)
         self.cfg = Config(threshold, 0, 0 if raster else FLAG_NO_RASTER, 0, None, None, None)
         self.validate = 1 if validate else 0
+        self._sets = (PolySet * 2)(P.c, Q.c)  # copies of the bound descriptors (pointers only)
         self.graphs = None
         if graph:
             s = torch.cuda.Stream(device=dev)
@@ -296,8 +323,7 @@ class Pipeline:
         st = _stream_ptr()
         lib = self.lib
         self.sums.zero_()
-        _check(lib.sccg_prep(ctypes.byref(self.P.c), self.validate, st), "sccg_prep")
-        _check(lib.sccg_prep(ctypes.byref(self.Q.c), self.validate, st), "sccg_prep")
+        _check(lib.sccg_prep_sets(self._sets, 2, self.validate, st), "sccg_prep_sets")
 
     def _enqueue_join(self):
         _check(self.lib.sccg_filter_pairs_async(ctypes.byref(self.P.c), ctypes.byref(self.Q.c), self.pairs.data_ptr(),

@@ -131,7 +131,21 @@ int sccg_polyset_bind(sccg_polyset* set, void* buf, size_t bytes) {
 int sccg_prep(const sccg_polyset* set, int32_t validate, sccg_stream_t stream) {
   set_error(SCCG_OK, "", -1);
   if (int r = check_set(set, true, "set")) return r;
-  return check_cuda(launch_prep(set, validate, reinterpret_cast<cudaStream_t>(stream)), "sccg_prep");
+  return check_cuda(launch_prep(&set, 1, validate, reinterpret_cast<cudaStream_t>(stream)), "sccg_prep");
+}
+
+int sccg_prep_sets(const sccg_polyset* sets, int32_t count, int32_t validate, sccg_stream_t stream) {
+  set_error(SCCG_OK, "", -1);
+  if (!sets || count < 1 || count > 4) return set_error(SCCG_E_ARG, "sccg_prep_sets: sets must hold 1..4 sets");
+  const sccg_polyset* ptrs[4];
+  for (int i = 0; i < count; i++) {
+    if (int r = check_set(&sets[i], true, "sets[i]")) return r;
+    for (int j = 0; j < i; j++)
+      if (sets[j].stats == sets[i].stats || sets[j].status == sets[i].status)
+        return set_error(SCCG_E_ARG, "sccg_prep_sets: sets must not share derived buffers");
+    ptrs[i] = &sets[i];
+  }
+  return check_cuda(launch_prep(ptrs, count, validate, reinterpret_cast<cudaStream_t>(stream)), "sccg_prep_sets");
 }
 
 size_t sccg_filter_workspace_bytes(int64_t n_p, int64_t n_q) {

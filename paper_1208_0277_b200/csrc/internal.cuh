@@ -101,6 +101,6 @@ int set_error(int code, const char* msg, int64_t index = -1);
 int check_cuda(cudaError_t e, const char* where);
 
 // launchers
-cudaError_t launch_prep(const sccg_polyset* set, int validate, cudaStream_t st);
+cudaError_t launch_prep(const sccg_polyset* const* sets, int count, int validate, cudaStream_t st);
 
 }  // namespace sccg

@@ -7,8 +7,9 @@
 // cheaper: Q's MBRs are bucketed into every cell they cover, each P MBR probes
 // its cells, and a pair is emitted only from the cell holding its reference
 // point (max xlo, max ylo) so it is found exactly once.  Each P's pairs are
-// written to its own segment (exclusive scan of per-P counts) and sorted by q
-// in place, so the output is sorted by (p, q) without a global sort.
+// written to its own segment (one-pass probe with a decoupled look-back scan
+// of per-P counts) and sorted by q in place, so the output is sorted by (p, q)
+// without a global sort.
 //
 // The cell size is chosen on the device from the per-set statistics sccg_prep
 // gathered (no host round trip); the only host synchronisation is the final
@@ -104,7 +105,7 @@ __global__ void grid_count_kernel(const int4* __restrict__ mq, int64_t nq, const
 // array needs no second memset.
 __global__ void grid_fill_kernel(const int4* __restrict__ mq, int64_t nq, const Grid* __restrict__ gp,
                                  const int* __restrict__ cell_start, int* __restrict__ cell_count,
-                                 int* __restrict__ items) {
+                                 int* __restrict__ items, int4* __restrict__ item_mbr) {
   const Grid g = *gp;
   if (g.empty) return;
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < nq; i += int64_t(gridDim.x) * blockDim.x) {
@@ -113,65 +114,192 @@ __global__ void grid_fill_kernel(const int4* __restrict__ mq, int64_t nq, const 
     for (int cy = m.y >> g.k; cy <= (m.w - 1) >> g.k; cy++)
       for (int cx = m.x >> g.k; cx <= (m.z - 1) >> g.k; cx++) {
         const int c = (cy - g.cy0) * g.ncx + cx - g.cx0;
-        items[cell_start[c] + atomicSub(&cell_count[c], 1) - 1] = (int)i;
+        const int slot = cell_start[c] + atomicSub(&cell_count[c], 1) - 1;
+        items[slot] = (int)i;
+        item_mbr[slot] = m;  // the probe tests MBRs straight from the cell's entries
       }
   }
 }
 
-// Probe: for each p, visit its cells; a pair is owned by the cell that holds
-// its reference point (max xlo, max ylo).  WRITE=false counts, WRITE=true
-// writes the segment then insertion-sorts it by q.
+// Probe, one pass.  Thread per p, CTA per tile of kProbeTile consecutive p
+// (tiles taken in order from an atomic ticket).  A pair is owned by the cell
+// that holds its reference point (max xlo, max ylo).  Each thread counts its
+// pairs; the CTA scans the counts and obtains its tile's output offset by
+// decoupled look-back over the preceding tiles' published aggregates /
+// prefixes; then every thread re-visits its (cache-hot) cells, writes its
+// segment and insertion-sorts it by q -- output sorted by (p, q), no global
+// scan or sort.  Pairs past `cap` are not written; the total is always exact.
+constexpr int kProbeTile = 128;
+constexpr unsigned long long kFlagAgg = 1ull << 62, kFlagPrefix = 2ull << 62, kValMask = (1ull << 62) - 1;
+
+constexpr int kKeep = 4;  // hits kept in registers by the counting pass
+
+// Visit p's cells; count the pairs it owns.  WRITE: store them to out[0..n);
+// otherwise keep the first kKeep q indices in keep[].  Entries are tested four
+// at a time (independent 16-byte loads in flight).
+__device__ __forceinline__ bool owns(const int4& a, const int4& b, int k, int cx0, int cy0, int ncx, int c) {
+  return a.x < b.z && b.x < a.z && a.y < b.w && b.y < a.w &&
+         ((max(a.y, b.y) >> k) - cy0) * ncx + ((max(a.x, b.x) >> k) - cx0) == c;
+}
+
 template <bool WRITE>
-__global__ void probe_kernel(const int4* __restrict__ mp, int64_t np, const int4* __restrict__ mq,
-                             const Grid* __restrict__ gp, const int* __restrict__ cell_start,
-                             const int* __restrict__ items, long long* __restrict__ count,
-                             const long long* __restrict__ start, int2* __restrict__ pairs, long long cap) {
+__device__ __forceinline__ int probe_cells(const int4& a, long long p, const Grid& gr, const int* __restrict__ cell_start,
+                                           const int* __restrict__ items, const int4* __restrict__ item_mbr,
+                                           int2* __restrict__ out, int4& keep) {
+  const int k = gr.k, cx0 = gr.cx0, cy0 = gr.cy0, ncx = gr.ncx;
+  int n = 0;
+  int4 kp = keep;
+#define SCCG_TAKE(IT)                          \
+  {                                            \
+    const int q = items[IT];                   \
+    if (WRITE) {                               \
+      out[n] = make_int2((int)p, q);           \
+    } else {                                   \
+      kp.x = n == 0 ? q : kp.x;                \
+      kp.y = n == 1 ? q : kp.y;                \
+      kp.z = n == 2 ? q : kp.z;                \
+      kp.w = n == 3 ? q : kp.w;                \
+    }                                          \
+    n++;                                       \
+  }
+  for (int cy = a.y >> k; cy <= (a.w - 1) >> k; cy++)
+    for (int cx = a.x >> k; cx <= (a.z - 1) >> k; cx++) {
+      const int c = (cy - cy0) * ncx + cx - cx0;
+      int it = cell_start[c];
+      const int e = cell_start[c + 1];
+      for (; it + 4 <= e; it += 4) {
+        const int4 b0 = item_mbr[it], b1 = item_mbr[it + 1], b2 = item_mbr[it + 2], b3 = item_mbr[it + 3];
+        if (owns(a, b0, k, cx0, cy0, ncx, c)) SCCG_TAKE(it)
+        if (owns(a, b1, k, cx0, cy0, ncx, c)) SCCG_TAKE(it + 1)
+        if (owns(a, b2, k, cx0, cy0, ncx, c)) SCCG_TAKE(it + 2)
+        if (owns(a, b3, k, cx0, cy0, ncx, c)) SCCG_TAKE(it + 3)
+      }
+      for (; it < e; it++)
+        if (owns(a, item_mbr[it], k, cx0, cy0, ncx, c)) SCCG_TAKE(it)
+    }
+#undef SCCG_TAKE
+  keep = kp;
+  return n;
+}
+
+__global__ void __launch_bounds__(kProbeTile) probe_kernel(const int4* __restrict__ mp, int64_t np,
+                                                           const Grid* __restrict__ gp,
+                                                           const int* __restrict__ cell_start,
+                                                           const int* __restrict__ items,
+                                                           const int4* __restrict__ item_mbr,
+                                                           unsigned long long* __restrict__ tile_state,
+                                                           unsigned* __restrict__ ticket, long long* __restrict__ total,
+                                                           int2* __restrict__ pairs, long long cap) {
+  __shared__ int s_tile;
+  __shared__ long long s_warp[kProbeTile / 32];
+  __shared__ long long s_base;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) s_tile = (int)atomicAdd(ticket, 1u);
+  __syncthreads();
+  const int tile = s_tile;
+  const int64_t p = (int64_t)tile * kProbeTile + threadIdx.x;
   const Grid g = *gp;
-  for (int64_t p = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; p < np; p += int64_t(gridDim.x) * blockDim.x) {
-    const int4 a = mp[p];
-    long long n = 0;
-    if (!g.empty && !mbr_empty(a) && (!WRITE || start[p + 1] <= cap)) {
-      const long long base = WRITE ? start[p] : 0;
-      for (int cy = a.y >> g.k; cy <= (a.w - 1) >> g.k; cy++)
-        for (int cx = a.x >> g.k; cx <= (a.z - 1) >> g.k; cx++) {
-          const int c = (cy - g.cy0) * g.ncx + cx - g.cx0;
-          for (int it = cell_start[c], e = cell_start[c + 1]; it < e; it++) {
-            const int q = items[it];
-            const int4 b = mq[q];
-            if (a.x < b.z && b.x < a.z && a.y < b.w && b.y < a.w && g.cell(max(a.x, b.x), max(a.y, b.y)) == c) {
-              if (WRITE) pairs[base + n] = make_int2((int)p, q);
-              n++;
-            }
-          }
+  int4 a = make_int4(0, 0, 0, 0);
+  const bool live = p < np && !g.empty;
+  if (live) a = mp[p];
+  const bool act = live && !mbr_empty(a);
+  int4 keep = make_int4(0, 0, 0, 0);
+  const int n = act ? probe_cells<false>(a, p, g, cell_start, items, item_mbr, nullptr, keep) : 0;
+  // CTA exclusive scan of the counts
+  long long x = n;
+  for (int o = 1; o < 32; o <<= 1) {
+    const long long y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) s_warp[warp] = x;
+  __syncthreads();
+  long long wbase = 0, agg = 0;
+  for (int w = 0; w < kProbeTile / 32; w++) {
+    const long long v = s_warp[w];
+    wbase += w < warp ? v : 0;
+    agg += v;
+  }
+  const long long excl = wbase + x - n;
+  // decoupled look-back (warp 0): publish the aggregate, then scan the
+  // predecessors 32 at a time (lane l reads tile - 1 - l): sum aggregates back
+  // to the nearest published inclusive prefix; retry a window while any tile in
+  // it has published nothing yet; publish our inclusive prefix
+  if (warp == 0) {
+    volatile unsigned long long* st = tile_state;
+    if (lane == 0) st[tile] = (tile == 0 ? (kFlagPrefix | 0ull) : (kFlagAgg | 0ull)) | (unsigned long long)agg;
+    long long prefix = 0;
+    int j0 = tile - 1;
+    while (j0 >= 0) {
+      const int j = j0 - lane;
+      unsigned long long v = j >= 0 ? st[j] : (kFlagPrefix | 0ull);  // before tile 0: prefix 0
+      if (__any_sync(0xffffffffu, (v & (kFlagAgg | kFlagPrefix)) == 0)) continue;  // window not ready
+      const unsigned pm = __ballot_sync(0xffffffffu, (v & kFlagPrefix) != 0);
+      const int stop = pm ? __ffs(pm) - 1 : 32;  // nearest prefix in the window
+      long long add = lane <= stop && j >= 0 ? (long long)(v & kValMask) : 0;
+      for (int o = 16; o; o >>= 1) add += __shfl_xor_sync(0xffffffffu, add, o);
+      prefix += add;
+      if (pm) break;
+      j0 -= 32;
+    }
+    if (lane == 0) {
+      if (tile > 0) st[tile] = kFlagPrefix | (unsigned long long)(prefix + agg);
+      s_base = prefix;
+      if ((int64_t)(tile + 1) * kProbeTile >= np) *total = prefix + agg;  // last tile
+    }
+  }
+  __syncthreads();
+  const long long base = s_base + excl;
+  if (pairs && n > 0 && base + n <= cap) {
+    int2* seg = pairs + base;
+    if (n <= kKeep) {  // the counting pass kept them: sort in registers, write
+      const int big = 0x7fffffff;  // pad the unused slots so a 4-sorting network applies
+      int k0 = keep.x, k1 = n > 1 ? keep.y : big, k2 = n > 2 ? keep.z : big, k3 = n > 3 ? keep.w : big;
+#define SCCG_CSWAP(U, V)        \
+  {                             \
+    const int lo = min(U, V);   \
+    V = max(U, V);              \
+    U = lo;                     \
+  }
+      SCCG_CSWAP(k0, k1)
+      SCCG_CSWAP(k2, k3)
+      SCCG_CSWAP(k0, k2)
+      SCCG_CSWAP(k1, k3)
+      SCCG_CSWAP(k1, k2)
+#undef SCCG_CSWAP
+      seg[0] = make_int2((int)p, k0);
+      if (n > 1) seg[1] = make_int2((int)p, k1);
+      if (n > 2) seg[2] = make_int2((int)p, k2);
+      if (n > 3) seg[3] = make_int2((int)p, k3);
+    } else {
+      probe_cells<true>(a, p, g, cell_start, items, item_mbr, seg, keep);
+      for (int i = 1; i < n; i++) {  // insertion sort of the segment by q (segments are short)
+        const int2 v = seg[i];
+        int j = i - 1;
+        while (j >= 0 && seg[j].y > v.y) {
+          seg[j + 1] = seg[j];
+          j--;
         }
-      if (WRITE) {  // insertion sort of the segment by q (segments are short)
-        for (long long i = 1; i < n; i++) {
-          const int2 v = pairs[base + i];
-          long long j = i - 1;
-          while (j >= 0 && pairs[base + j].y > v.y) {
-            pairs[base + j + 1] = pairs[base + j];
-            j--;
-          }
-          pairs[base + j + 1] = v;
-        }
+        seg[j + 1] = v;
       }
     }
-    if (!WRITE) count[p] = n;
   }
 }
 
 // --------------------------------------------------------------------- host
 static size_t cub_scan_bytes(int64_t n) {
-  size_t b32 = 0, b64 = 0;
+  size_t b32 = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, b32, (const int*)nullptr, (int*)nullptr, (int)n);
-  cub::DeviceScan::ExclusiveSum(nullptr, b64, (const long long*)nullptr, (long long*)nullptr, (int)n);
-  return b32 > b64 ? b32 : b64;
+  return b32;
 }
+
+static int64_t probe_tiles(int64_t np) { return (np + kProbeTile - 1) / kProbeTile; }
 
 struct FilterWs {
   Grid* grid;
   int *cell_count, *cell_start, *items;
-  long long *pcount, *pstart;
+  int4* item_mbr;
+  unsigned long long* tile_state;  // [T] tile states, then the ticket and the total (zeroed together)
+  long long* total;
   void* tmp;
   size_t tmp_bytes;
 };
@@ -182,9 +310,10 @@ static size_t filter_layout(int64_t np, int64_t nq, Carve& cv, FilterWs& w) {
   w.cell_count = cv.take<int>(C + 1);
   w.cell_start = cv.take<int>(C + 1);
   w.items = cv.take<int>(E);
-  w.pcount = cv.take<long long>(np + 1);
-  w.pstart = cv.take<long long>(np + 1);
-  w.tmp_bytes = cub_scan_bytes((C + 1) > (np + 1) ? (C + 1) : (np + 1));
+  w.item_mbr = cv.take<int4>(E);
+  w.tile_state = cv.take<unsigned long long>(probe_tiles(np) + 2);
+  w.total = reinterpret_cast<long long*>(w.tile_state + probe_tiles(np) + 1);
+  w.tmp_bytes = cub_scan_bytes(C + 1);
   w.tmp = cv.take<char>(w.tmp_bytes);
   return cv.used;
 }
@@ -208,12 +337,14 @@ static int blocks_for(int64_t n, int threads) {
   return (int)(b < 1 ? 1 : b);
 }
 
-// Enqueue everything up to the per-P pair offsets (grid, buckets, counts, scan).
-static int filter_enqueue(const sccg_polyset* P, const sccg_polyset* Q, FilterWs& w, cudaStream_t stream) {
+// Enqueue the whole join: grid, buckets, one-pass probe (pairs written when
+// they fit in `cap`; the exact total always lands in w.total).
+static int filter_enqueue(const sccg_polyset* P, const sccg_polyset* Q, FilterWs& w, int32_t* pairs, int64_t cap,
+                          cudaStream_t stream) {
   const int64_t np = P->n_polygons, nq = Q->n_polygons;
   const int4* mp = reinterpret_cast<const int4*>(P->mbr);
   const int4* mq = reinterpret_cast<const int4*>(Q->mbr);
-  const int64_t C = cell_cap(np, nq);
+  const int64_t C = cell_cap(np, nq), T = probe_tiles(np);
   // 1. grid size from the prep statistics (device side), bucket Q
   grid_select_kernel<<<1, 32, 0, stream>>>(reinterpret_cast<const SetStats*>(P->stats),
                                            reinterpret_cast<const SetStats*>(Q->stats), C, entry_cap(nq), w.grid);
@@ -221,23 +352,15 @@ static int filter_enqueue(const sccg_polyset* P, const sccg_polyset* Q, FilterWs
   if (nq > 0) grid_count_kernel<<<blocks_for(nq, 256), 256, 0, stream>>>(mq, nq, w.grid, w.cell_count);
   cub::DeviceScan::ExclusiveSum(w.tmp, w.tmp_bytes, w.cell_count, w.cell_start, (int)(C + 1), stream);
   if (nq > 0)
-    grid_fill_kernel<<<blocks_for(nq, 256), 256, 0, stream>>>(mq, nq, w.grid, w.cell_start, w.cell_count, w.items);
-  // 2. probe: count, scan
+    grid_fill_kernel<<<blocks_for(nq, 256), 256, 0, stream>>>(mq, nq, w.grid, w.cell_start, w.cell_count, w.items,
+                                                               w.item_mbr);
+  // 2. probe (tile states, ticket and total zeroed: one memset, contiguous)
+  cudaMemsetAsync(w.tile_state, 0, sizeof(unsigned long long) * (T + 2), stream);
   if (np > 0)
-    probe_kernel<false><<<blocks_for(np, 128), 128, 0, stream>>>(mp, np, mq, w.grid, w.cell_start, w.items, w.pcount,
-                                                                  nullptr, nullptr, 0);
-  cudaMemsetAsync(w.pcount + np, 0, sizeof(long long), stream);
-  cub::DeviceScan::ExclusiveSum(w.tmp, w.tmp_bytes, w.pcount, w.pstart, (int)(np + 1), stream);
+    probe_kernel<<<(unsigned)T, kProbeTile, 0, stream>>>(mp, np, w.grid, w.cell_start, w.items, w.item_mbr,
+                                                          w.tile_state, reinterpret_cast<unsigned*>(w.tile_state + T),
+                                                          w.total, reinterpret_cast<int2*>(pairs), pairs ? cap : 0);
   return check_cuda(cudaGetLastError(), "filter enqueue");
-}
-
-static void probe_write(const sccg_polyset* P, const sccg_polyset* Q, FilterWs& w, int32_t* pairs, int64_t cap,
-                        cudaStream_t stream) {
-  const int64_t np = P->n_polygons;
-  if (np > 0 && pairs && cap > 0)
-    probe_kernel<true><<<blocks_for(np, 128), 128, 0, stream>>>(
-        reinterpret_cast<const int4*>(P->mbr), np, reinterpret_cast<const int4*>(Q->mbr), w.grid, w.cell_start,
-        w.items, nullptr, w.pstart, reinterpret_cast<int2*>(pairs), cap);
 }
 
 int filter_pairs(const sccg_polyset* P, const sccg_polyset* Q, int32_t* pairs, int64_t cap, int64_t* n_pairs_host,
@@ -247,11 +370,11 @@ int filter_pairs(const sccg_polyset* P, const sccg_polyset* Q, int32_t* pairs, i
   FilterWs w;
   filter_layout(np, nq, cv, w);
   if (!cv.ok) return set_error(SCCG_E_WORKSPACE, "filter workspace too small (see sccg_filter_workspace_bytes)");
-  if (int r = filter_enqueue(P, Q, w, stream)) return r;
+  if (int r = filter_enqueue(P, Q, w, pairs, cap, stream)) return r;
   // the one host synchronisation: pair count and both sets' prep status
   long long total = 0;
   uint32_t sp[2] = {0, 0}, sq[2] = {0, 0};
-  if (int r = check_cuda(cudaMemcpyAsync(&total, w.pstart + np, sizeof(long long), cudaMemcpyDeviceToHost, stream),
+  if (int r = check_cuda(cudaMemcpyAsync(&total, w.total, sizeof(long long), cudaMemcpyDeviceToHost, stream),
                          "count copy"))
     return r;
   if (int r = check_cuda(cudaMemcpyAsync(sp, P->status, 8, cudaMemcpyDeviceToHost, stream), "status copy")) return r;
@@ -269,9 +392,7 @@ int filter_pairs(const sccg_polyset* P, const sccg_polyset* Q, int32_t* pairs, i
   }
   *n_pairs_host = total;
   if (pairs == nullptr || cap < total) return set_error(SCCG_E_CAPACITY, "pair buffer too small", total);
-  // write, segment-sorted by q
-  if (total > 0) probe_write(P, Q, w, pairs, cap, stream);
-  return check_cuda(cudaGetLastError(), "probe write");
+  return SCCG_OK;
 }
 
 __global__ void filter_result_kernel(const long long* __restrict__ total, const uint32_t* __restrict__ sp,
@@ -289,10 +410,8 @@ int filter_pairs_async(const sccg_polyset* P, const sccg_polyset* Q, int32_t* pa
   FilterWs w;
   filter_layout(np, nq, cv, w);
   if (!cv.ok) return set_error(SCCG_E_WORKSPACE, "filter workspace too small (see sccg_filter_workspace_bytes)");
-  if (int r = filter_enqueue(P, Q, w, stream)) return r;
-  probe_write(P, Q, w, pairs, cap, stream);
-  filter_result_kernel<<<1, 32, 0, stream>>>(w.pstart + np, P->status, Q->status,
-                                             reinterpret_cast<long long*>(result_dev));
+  if (int r = filter_enqueue(P, Q, w, pairs, cap, stream)) return r;
+  filter_result_kernel<<<1, 32, 0, stream>>>(w.total, P->status, Q->status, reinterpret_cast<long long*>(result_dev));
   return check_cuda(cudaGetLastError(), "filter async");
 }
 

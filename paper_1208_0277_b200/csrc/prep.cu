@@ -20,9 +20,9 @@ namespace sccg {
 
 constexpr int kPrepThreads = 128;
 constexpr int kPrepPolys = 128;   // one ring per thread per tile
-constexpr int kPrepWarps = kPrepThreads / 32;
 static_assert(kPrepPolys == kPrepThreads, "one ring per thread per tile");
-constexpr int kPrepVerts = 5120;  // 40 KB of int2 staged per tile (dynamic shared memory)
+constexpr int kPrepVerts = 5120;
+constexpr size_t kPrepSmem = kPrepVerts * sizeof(int2);  // 40 KB of int2 staged per tile (dynamic shared memory)
 
 
 // ---- 1-D bulk copies on the TMA engine (cp.async.bulk): the tile is staged
@@ -278,13 +278,75 @@ struct StatAcc {
 constexpr int kThreadMaxV = 192;  // rings up to this size are prepped by one thread
 constexpr int kSortKeys = 64;     // counting-sort buckets (V / 4) for dealing rings to threads
 
-__global__ void __launch_bounds__(kPrepThreads) prep_kernel(const int2* __restrict__ xy,
-                                                            const int64_t* __restrict__ off, int64_t n,
-                                                            int64_t nv_total, int4* __restrict__ mbr,
-                                                            int64_t* __restrict__ area, int2* __restrict__ ecount,
-                                                            uint64_t* __restrict__ edges,
-                                                            uint32_t* __restrict__ status, SetStats* stats,
-                                                            int validate, int bulk) {
+// One launch preps up to kPrepMaxSets sets: their tiles form one index
+// space, handed out by a device ticket (dynamic, so the last wave is short);
+// a CTA flushes its statistics whenever it moves on to the next set.
+constexpr int kPrepMaxSets = 4;
+struct PrepSet {
+  const int2* xy;
+  const int64_t* off;
+  int64_t n, nv_total;
+  int4* mbr;
+  int64_t* area;
+  int2* ecount;
+  uint64_t* edges;
+  uint32_t* status;
+  SetStats* stats;
+  int bulk;
+};
+struct PrepArgs {
+  PrepSet set[kPrepMaxSets];
+  int64_t tile_end[kPrepMaxSets];  // exclusive prefix ends of the sets' tile ranges
+  int nsets;
+  int validate;
+  unsigned long long* ticket;
+};
+
+// Block reduction of a CTA's statistics, then one atomic per field.
+__device__ void flush_stats(StatAcc& acc, SetStats* stats, unsigned long long* s_acc, int* s_b) {
+  const int lane = threadIdx.x & 31;
+  __syncthreads();
+  if (threadIdx.x < 4) s_acc[threadIdx.x] = 0;
+  if (threadIdx.x == 0) {
+    s_b[0] = s_b[1] = INT_MAX;
+    s_b[2] = s_b[3] = INT_MIN;
+    s_b[4] = s_b[5] = 0;
+  }
+  __syncthreads();
+  unsigned long long v[4] = {acc.nonempty, acc.sw, acc.sh, acc.swh};
+  for (int f = 0; f < 4; f++) {
+    unsigned long long x = v[f];
+    for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    if (lane == 0 && x) atomicAdd(&s_acc[f], x);
+  }
+  const int bx0 = __reduce_min_sync(0xffffffffu, acc.bx0), by0 = __reduce_min_sync(0xffffffffu, acc.by0);
+  const int bx1 = __reduce_max_sync(0xffffffffu, acc.bx1), by1 = __reduce_max_sync(0xffffffffu, acc.by1);
+  const int mw = __reduce_max_sync(0xffffffffu, acc.mw), mh = __reduce_max_sync(0xffffffffu, acc.mh);
+  if (lane == 0) {
+    atomicMin(&s_b[0], bx0);
+    atomicMin(&s_b[1], by0);
+    atomicMax(&s_b[2], bx1);
+    atomicMax(&s_b[3], by1);
+    atomicMax(&s_b[4], mw);
+    atomicMax(&s_b[5], mh);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && s_acc[0]) {
+    atomicAdd(&stats->nonempty, s_acc[0]);
+    atomicAdd(&stats->sw, s_acc[1]);
+    atomicAdd(&stats->sh, s_acc[2]);
+    atomicAdd(&stats->swh, s_acc[3]);
+    atomicMin(&stats->bounds[0], s_b[0]);
+    atomicMin(&stats->bounds[1], s_b[1]);
+    atomicMax(&stats->bounds[2], s_b[2]);
+    atomicMax(&stats->bounds[3], s_b[3]);
+    atomicMax(&stats->maxext[0], s_b[4]);
+    atomicMax(&stats->maxext[1], s_b[5]);
+  }
+  acc.init();
+}
+
+__global__ void __launch_bounds__(kPrepThreads) prep_kernel(const __grid_constant__ PrepArgs args) {
   extern __shared__ int4 s_dyn4[];  // kPrepVerts int2 (16-byte aligned)
   int2* s_xy = reinterpret_cast<int2*>(s_dyn4);
   __shared__ int64_t s_off[kPrepPolys + 1];
@@ -294,14 +356,38 @@ __global__ void __launch_bounds__(kPrepThreads) prep_kernel(const int2* __restri
   __shared__ unsigned long long s_acc[4];
   __shared__ int s_b[6];
   __shared__ uint64_t s_bar;
+  __shared__ long long s_tile;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   unsigned phase = 0;
   if (threadIdx.x == 0) mbar_init(&s_bar);
-  __syncthreads();
   StatAcc acc;
   acc.init();
-  const int64_t ntiles = (n + kPrepPolys - 1) / kPrepPolys;
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+  const int validate = args.validate;
+  const int64_t ntiles = args.tile_end[args.nsets - 1];
+  int cur = -1;  // set of the statistics in acc
+  for (;;) {
+    __syncthreads();  // previous tile's shared data fully consumed
+    if (threadIdx.x == 0) s_tile = (long long)atomicAdd(args.ticket, 1ull);
+    __syncthreads();
+    const int64_t gt = s_tile;
+    if (gt >= ntiles) break;
+    int si = 0;
+    while (gt >= args.tile_end[si]) si++;
+    if (si != cur) {
+      if (cur >= 0) flush_stats(acc, args.set[cur].stats, s_acc, s_b);
+      cur = si;
+    }
+    const PrepSet& S = args.set[si];
+    const int2* __restrict__ xy = S.xy;
+    const int64_t* __restrict__ off = S.off;
+    const int64_t n = S.n, nv_total = S.nv_total;
+    int4* __restrict__ mbr = S.mbr;
+    int64_t* __restrict__ area = S.area;
+    int2* __restrict__ ecount = S.ecount;
+    uint64_t* __restrict__ edges = S.edges;
+    uint32_t* __restrict__ status = S.status;
+    const int bulk = S.bulk;
+    const int64_t tile = gt - (si ? args.tile_end[si - 1] : 0);
     const int64_t p0 = tile * kPrepPolys;
     const int np = (int)min((int64_t)kPrepPolys, n - p0);
     __syncthreads();  // previous tile's shared data fully consumed
@@ -404,48 +490,14 @@ __global__ void __launch_bounds__(kPrepThreads) prep_kernel(const int2* __restri
     }
   }
   if (threadIdx.x == 0) bulk_store_drain();
-  // block reduction of the statistics, then one atomic per field
-  if (threadIdx.x < 4) s_acc[threadIdx.x] = 0;
-  if (threadIdx.x == 0) {
-    s_b[0] = s_b[1] = INT_MAX;
-    s_b[2] = s_b[3] = INT_MIN;
-    s_b[4] = s_b[5] = 0;
-  }
-  __syncthreads();
-  unsigned long long v[4] = {acc.nonempty, acc.sw, acc.sh, acc.swh};
-  for (int f = 0; f < 4; f++) {
-    unsigned long long x = v[f];
-    for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-    if (lane == 0 && x) atomicAdd(&s_acc[f], x);
-  }
-  const int bx0 = __reduce_min_sync(0xffffffffu, acc.bx0), by0 = __reduce_min_sync(0xffffffffu, acc.by0);
-  const int bx1 = __reduce_max_sync(0xffffffffu, acc.bx1), by1 = __reduce_max_sync(0xffffffffu, acc.by1);
-  const int mw = __reduce_max_sync(0xffffffffu, acc.mw), mh = __reduce_max_sync(0xffffffffu, acc.mh);
-  if (lane == 0) {
-    atomicMin(&s_b[0], bx0);
-    atomicMin(&s_b[1], by0);
-    atomicMax(&s_b[2], bx1);
-    atomicMax(&s_b[3], by1);
-    atomicMax(&s_b[4], mw);
-    atomicMax(&s_b[5], mh);
-  }
-  __syncthreads();
-  if (threadIdx.x == 0 && s_acc[0]) {
-    atomicAdd(&stats->nonempty, s_acc[0]);
-    atomicAdd(&stats->sw, s_acc[1]);
-    atomicAdd(&stats->sh, s_acc[2]);
-    atomicAdd(&stats->swh, s_acc[3]);
-    atomicMin(&stats->bounds[0], s_b[0]);
-    atomicMin(&stats->bounds[1], s_b[1]);
-    atomicMax(&stats->bounds[2], s_b[2]);
-    atomicMax(&stats->bounds[3], s_b[3]);
-    atomicMax(&stats->maxext[0], s_b[4]);
-    atomicMax(&stats->maxext[1], s_b[5]);
-  }
+  if (cur >= 0) flush_stats(acc, args.set[cur].stats, s_acc, s_b);
 }
 
-__global__ void prep_init_kernel(uint32_t* status, SetStats* st) {
-  if (threadIdx.x == 0) {
+__global__ void prep_init_kernel(PrepArgs args) {
+  const int i = threadIdx.x;
+  if (i < args.nsets) {
+    uint32_t* status = args.set[i].status;
+    SetStats* st = args.set[i].stats;
     status[0] = 0;
     status[1] = 0xffffffffu;
     st->bounds[0] = st->bounds[1] = INT_MAX;
@@ -453,30 +505,49 @@ __global__ void prep_init_kernel(uint32_t* status, SetStats* st) {
     st->maxext[0] = st->maxext[1] = 0;
     st->nonempty = st->sw = st->sh = st->swh = 0;
   }
+  if (i == 0) *args.ticket = 0;
 }
 
-cudaError_t launch_prep(const sccg_polyset* s, int validate, cudaStream_t st) {
-  SetStats* stats = reinterpret_cast<SetStats*>(s->stats);
-  prep_init_kernel<<<1, 32, 0, st>>>(s->status, stats);
-  if (s->n_polygons > 0) {
-    static cudaError_t attr = cudaFuncSetAttribute(prep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                   (int)(kPrepVerts * sizeof(int2)));
+cudaError_t launch_prep(const sccg_polyset* const* sets, int count, int validate, cudaStream_t st) {
+  PrepArgs a{};
+  a.nsets = count;
+  a.validate = validate;
+  int64_t tiles = 0;
+  for (int i = 0; i < count; i++) {
+    const sccg_polyset* s = sets[i];
+    PrepSet& d = a.set[i];
+    d.xy = reinterpret_cast<const int2*>(s->xy);
+    d.off = s->offsets;
+    d.n = s->n_polygons;
+    d.nv_total = s->n_vertices;
+    d.mbr = reinterpret_cast<int4*>(s->mbr);
+    d.area = s->area;
+    d.ecount = reinterpret_cast<int2*>(s->ecount);
+    d.edges = s->edges;
+    d.status = s->status;
+    d.stats = reinterpret_cast<SetStats*>(s->stats);
+    d.bulk = ((reinterpret_cast<uintptr_t>(s->xy) | reinterpret_cast<uintptr_t>(s->edges)) & 15) == 0 ? 1 : 0;
+    tiles += (s->n_polygons + kPrepPolys - 1) / kPrepPolys;
+    a.tile_end[i] = tiles;
+  }
+  // the ticket lives in the first set's statistics block (reserved words)
+  a.ticket = &reinterpret_cast<SetStats*>(sets[0]->stats)->reserved[0];
+  prep_init_kernel<<<1, 32, 0, st>>>(a);
+  if (tiles > 0) {
+    static cudaError_t attr =
+        cudaFuncSetAttribute(prep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPrepSmem);
     if (attr != cudaSuccess) return attr;
     static int sms = 0, per_sm = 1;
     if (sms == 0) {  // launch geometry, queried once per process
       int dev = 0;
       cudaGetDevice(&dev);
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, prep_kernel, kPrepThreads, kPrepVerts * sizeof(int2));
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, prep_kernel, kPrepThreads, kPrepSmem);
     }
-    const int64_t ntiles = (s->n_polygons + kPrepPolys - 1) / kPrepPolys;
-    int64_t blocks = ntiles;
+    int64_t blocks = tiles;
     const int64_t cap = (int64_t)sms * (per_sm > 0 ? per_sm : 1);
     if (blocks > cap) blocks = cap;
-    prep_kernel<<<(unsigned)blocks, kPrepThreads, kPrepVerts * sizeof(int2), st>>>(
-        reinterpret_cast<const int2*>(s->xy), s->offsets, s->n_polygons, s->n_vertices,
-        reinterpret_cast<int4*>(s->mbr), s->area, reinterpret_cast<int2*>(s->ecount), s->edges, s->status, stats,
-        validate, ((reinterpret_cast<uintptr_t>(s->xy) | reinterpret_cast<uintptr_t>(s->edges)) & 15) == 0 ? 1 : 0);
+    prep_kernel<<<(unsigned)blocks, kPrepThreads, kPrepSmem, st>>>(a);
   }
   return cudaGetLastError();
 }

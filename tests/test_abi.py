@@ -104,6 +104,10 @@ def test_host_argument_checks():
     assert lib.sccg_polyset_bind(ctypes.byref(s), 0x100000, b1) == sccg.OK
     assert s.mbr % 256 == 0 and s.edges % 8 == 0
     assert lib.sccg_prep(None, 1, None) == sccg.E_ARG
+    sets = (sccg.PolySet * 2)()
+    assert lib.sccg_prep_sets(None, 1, 1, None) == sccg.E_ARG
+    assert lib.sccg_prep_sets(sets, 0, 1, None) == sccg.E_ARG
+    assert lib.sccg_prep_sets(sets, 5, 1, None) == sccg.E_ARG
     n = ctypes.c_int64()
     assert lib.sccg_filter_pairs(None, None, None, 0, ctypes.byref(n), None, 0, None) == sccg.E_ARG
     cfg = sccg.Config(-1, 0, 0, 0, None, None, None)

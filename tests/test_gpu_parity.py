@@ -79,6 +79,28 @@ def test_prep_matches_oracle(sccg, tile_sets):
         assert D.status.cpu().tolist()[0] == 0
 
 
+def test_prep_sets_one_launch_equals_separate(sccg):
+    """sccg_prep_sets over several sets in one launch (shared dynamic tile
+    space) gives exactly the per-set results of sccg_prep."""
+    sets = [synth.generate("tile", image=i)[i % 2] for i in range(3)]
+    sets.append(synth.generate("skewed")[0])
+    one = [dev(s, sccg) for s in sets]  # prepped one by one
+    many = []
+    for s in sets:
+        xy, off = sccg.to_device(s.xy, s.offsets)
+        many.append(sccg.DeviceSet(xy, off, prep=False))
+    arr = (sccg.PolySet * len(many))(*[m.c for m in many])
+    assert sccg.load().sccg_prep_sets(arr, len(many), 1, None) == 0
+    torch.cuda.synchronize()
+    for a, b in zip(one, many):
+        for f in ("mbr", "area", "ecount", "status"):
+            assert torch.equal(getattr(a, f), getattr(b, f)), f
+        assert torch.equal(a.stats_bytes()[:48], b.stats_bytes()[:48])  # bounds, extents, moments
+        assert torch.equal(a.used_edge_words(), b.used_edge_words())  # records + raster rows
+    shared = (sccg.PolySet * 2)(many[0].c, many[0].c)
+    assert sccg.load().sccg_prep_sets(shared, 2, 1, None) == sccg.E_ARG
+
+
 def test_prep_tiles_at_odd_offsets(sccg):
     """Prep's 128-ring tiles start at odd vertex offsets (an odd-V ring opens
     every tile) and every tile ends with a 4-vertex rect whose records + raster
