@@ -89,35 +89,57 @@ __global__ void grid_select_kernel(const SetStats* __restrict__ sp, const SetSta
   }
 }
 
-__global__ void grid_count_kernel(const int4* __restrict__ mq, int64_t nq, const Grid* __restrict__ gp,
-                                  int* __restrict__ cell_count) {
-  const Grid g = *gp;
-  if (g.empty) return;
-  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < nq; i += int64_t(gridDim.x) * blockDim.x) {
-    const int4 m = mq[i];
-    if (mbr_empty(m)) continue;
-    for (int cy = m.y >> g.k; cy <= (m.w - 1) >> g.k; cy++)
-      for (int cx = m.x >> g.k; cx <= (m.z - 1) >> g.k; cx++) atomicAdd(&cell_count[(cy - g.cy0) * g.ncx + cx - g.cx0], 1);
-  }
+// MBRs covering more than kCoopCells cells (a gland among nuclei, C3) are
+// handled by their whole warp, lanes spread over the cells, so one polygon is
+// not a serial critical path of hundreds of dependent cell visits.
+constexpr int kCoopCells = 32;
+
+__device__ __forceinline__ int mbr_cells(const int4& m, int k) {
+  return (((m.z - 1) >> k) - (m.x >> k) + 1) * (((m.w - 1) >> k) - (m.y >> k) + 1);
 }
 
-// Fill: counts are decremented back to zero as slots are taken, so the count
-// array needs no second memset.
-__global__ void grid_fill_kernel(const int4* __restrict__ mq, int64_t nq, const Grid* __restrict__ gp,
-                                 const int* __restrict__ cell_start, int* __restrict__ cell_count,
-                                 int* __restrict__ items, int4* __restrict__ item_mbr) {
+// Bucket Q: COUNT (FILL = false) adds one per covered cell; FILL takes a slot
+// per covered cell (counts are decremented back to zero as slots are taken,
+// so the count array needs no second memset) and stores q and its MBR there.
+template <bool FILL>
+__global__ void grid_bucket_kernel(const int4* __restrict__ mq, int64_t nq, const Grid* __restrict__ gp,
+                                   const int* __restrict__ cell_start, int* __restrict__ cell_count,
+                                   int* __restrict__ items, int4* __restrict__ item_mbr) {
   const Grid g = *gp;
   if (g.empty) return;
-  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < nq; i += int64_t(gridDim.x) * blockDim.x) {
-    const int4 m = mq[i];
-    if (mbr_empty(m)) continue;
-    for (int cy = m.y >> g.k; cy <= (m.w - 1) >> g.k; cy++)
-      for (int cx = m.x >> g.k; cx <= (m.z - 1) >> g.k; cx++) {
-        const int c = (cy - g.cy0) * g.ncx + cx - g.cx0;
-        const int slot = cell_start[c] + atomicSub(&cell_count[c], 1) - 1;
-        items[slot] = (int)i;
-        item_mbr[slot] = m;  // the probe tests MBRs straight from the cell's entries
-      }
+  const int lane = threadIdx.x & 31;
+  const int64_t wid = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  auto insert = [&](int c, int q, const int4& m) {
+    if (FILL) {
+      const int slot = cell_start[c] + atomicSub(&cell_count[c], 1) - 1;
+      items[slot] = q;
+      item_mbr[slot] = m;  // the probe tests MBRs straight from the cell's entries
+    } else {
+      atomicAdd(&cell_count[c], 1);
+    }
+  };
+  for (int64_t base = wid * 32; base < nq; base += nw * 32) {  // warp-uniform trip count
+    const int64_t i = base + lane;
+    int4 m = make_int4(0, 0, 0, 0);
+    bool ok = false;
+    if (i < nq) {
+      m = mq[i];
+      ok = !mbr_empty(m);
+    }
+    const bool coop = ok && mbr_cells(m, g.k) > kCoopCells;
+    if (ok && !coop)
+      for (int cy = m.y >> g.k; cy <= (m.w - 1) >> g.k; cy++)
+        for (int cx = m.x >> g.k; cx <= (m.z - 1) >> g.k; cx++) insert((cy - g.cy0) * g.ncx + cx - g.cx0, (int)i, m);
+    for (unsigned bm = __ballot_sync(0xffffffffu, coop); bm; bm &= bm - 1) {
+      const int j = __ffs(bm) - 1;
+      const int4 mj = make_int4(__shfl_sync(0xffffffffu, m.x, j), __shfl_sync(0xffffffffu, m.y, j),
+                                __shfl_sync(0xffffffffu, m.z, j), __shfl_sync(0xffffffffu, m.w, j));
+      const int qj = (int)(base + j);
+      const int x0 = mj.x >> g.k, y0 = mj.y >> g.k, w = ((mj.z - 1) >> g.k) - x0 + 1;
+      const int nc = w * (((mj.w - 1) >> g.k) - y0 + 1);
+      for (int t = lane; t < nc; t += 32) insert((y0 + t / w - g.cy0) * g.ncx + x0 + t % w - g.cx0, qj, mj);
+    }
   }
 }
 
@@ -182,6 +204,95 @@ __device__ __forceinline__ int probe_cells(const int4& a, long long p, const Gri
   return n;
 }
 
+__device__ __forceinline__ int4 shfl4(const int4& v, int j) {
+  return make_int4(__shfl_sync(0xffffffffu, v.x, j), __shfl_sync(0xffffffffu, v.y, j), __shfl_sync(0xffffffffu, v.z, j),
+                   __shfl_sync(0xffffffffu, v.w, j));
+}
+
+// A big MBR probed by its whole warp: lane l visits cells l, l + 32, ... of
+// its cell rectangle.  COUNT returns the pairs it owns (every lane gets the
+// total); WRITE appends them to seg[] in arbitrary order (slots from *fill,
+// reset here) -- warp_sort_segment restores the q order.
+template <bool WRITE>
+__device__ int coop_cells(const int4 a, long long p, const Grid& g, const int* __restrict__ cell_start,
+                          const int* __restrict__ items, const int4* __restrict__ item_mbr, int2* __restrict__ seg,
+                          int* fill) {
+  const int lane = threadIdx.x & 31;
+  const int k = g.k, cx0 = g.cx0, cy0 = g.cy0, ncx = g.ncx;
+  const int x0 = a.x >> k, y0 = a.y >> k, w = ((a.z - 1) >> k) - x0 + 1;
+  const int nc = w * (((a.w - 1) >> k) - y0 + 1);
+  if (WRITE) {
+    if (lane == 0) *fill = 0;
+    __syncwarp();
+  }
+  int cnt = 0;
+  for (int t = lane; t < nc; t += 32) {
+    const int c = (y0 + t / w - cy0) * ncx + (x0 + t % w - cx0);
+    for (int it = cell_start[c], e = cell_start[c + 1]; it < e; it++)
+      if (owns(a, item_mbr[it], k, cx0, cy0, ncx, c)) {
+        if (WRITE) seg[atomicAdd(fill, 1)] = make_int2((int)p, items[it]);
+        cnt++;
+      }
+  }
+  for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+  return cnt;
+}
+
+// Sort seg[0..n) by q (distinct within a segment) with the warp: a bitonic
+// network in its ascending-only form (each merge starts by comparing i with
+// its mirror i ^ (k - 1)), so positions >= n behave as +inf and are never
+// touched -- no padding needed.  Up to kSortBuf keys are sorted in a shared
+// buffer (one per CTA, under a lock -- long segments are rare; kept small so
+// the L1 the probe lives on stays large); longer segments in place in global
+// memory (L1/L2-resident).
+constexpr int kSortBuf = 1024;
+constexpr int kThreadSortMax = 32;  // segments up to this length: the owning thread sorts
+
+template <typename Key, typename Get, typename Put>
+__device__ __forceinline__ void warp_bitonic(int n, Get get, Put put) {
+  const int lane = threadIdx.x & 31;
+  int m = 1;
+  while (m < n) m <<= 1;
+  for (int k = 2; k <= m; k <<= 1)
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = lane; i < m; i += 32) {
+        const int l = j == (k >> 1) ? (i ^ (k - 1)) : (i ^ j);  // mirror first, then halves
+        if (l > i && l < n) {
+          const Key u = get(i), v = get(l);
+          if (v < u) {
+            put(i, v);
+            put(l, u);
+          }
+        }
+      }
+      __syncwarp();
+    }
+}
+
+__device__ void warp_sort_segment(int2* seg, int n, int* buf, int* lock) {
+  const int lane = threadIdx.x & 31;
+  if (n <= 1) return;
+  if (n <= kSortBuf) {
+    if (lane == 0)
+      while (atomicCAS(lock, 0, 1) != 0) {
+      }
+    __syncwarp();
+    const int p = seg[0].x;
+    for (int i = lane; i < n; i += 32) buf[i] = seg[i].y;
+    __syncwarp();
+    warp_bitonic<int>(n, [&](int i) { return buf[i]; }, [&](int i, int v) { buf[i] = v; });
+    for (int i = lane; i < n; i += 32) seg[i] = make_int2(p, buf[i]);
+    __threadfence_block();
+    __syncwarp();
+    if (lane == 0) atomicExch(lock, 0);
+  } else {
+    const int p = seg[0].x;
+    __syncwarp();
+    warp_bitonic<int>(n, [&](int i) { return seg[i].y; }, [&](int i, int v) { seg[i] = make_int2(p, v); });
+  }
+  __syncwarp();
+}
+
 __global__ void __launch_bounds__(kProbeTile) probe_kernel(const int4* __restrict__ mp, int64_t np,
                                                            const Grid* __restrict__ gp,
                                                            const int* __restrict__ cell_start,
@@ -193,6 +304,10 @@ __global__ void __launch_bounds__(kProbeTile) probe_kernel(const int4* __restric
   __shared__ int s_tile;
   __shared__ long long s_warp[kProbeTile / 32];
   __shared__ long long s_base;
+  __shared__ int s_fill[kProbeTile / 32];
+  __shared__ int s_sort[kSortBuf];
+  __shared__ int s_lock;
+  if (threadIdx.x == 0) s_lock = 0;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (threadIdx.x == 0) s_tile = (int)atomicAdd(ticket, 1u);
   __syncthreads();
@@ -204,7 +319,15 @@ __global__ void __launch_bounds__(kProbeTile) probe_kernel(const int4* __restric
   if (live) a = mp[p];
   const bool act = live && !mbr_empty(a);
   int4 keep = make_int4(0, 0, 0, 0);
-  const int n = act ? probe_cells<false>(a, p, g, cell_start, items, item_mbr, nullptr, keep) : 0;
+  const bool coop = act && mbr_cells(a, g.k) > kCoopCells;  // big MBR: its warp probes it together
+  int n = act && !coop ? probe_cells<false>(a, p, g, cell_start, items, item_mbr, nullptr, keep) : 0;
+  const unsigned coop_mask = __ballot_sync(0xffffffffu, coop);
+  for (unsigned bm = coop_mask; bm; bm &= bm - 1) {
+    const int j = __ffs(bm) - 1;
+    const int cnt = coop_cells<false>(shfl4(a, j), p - threadIdx.x + (warp * 32 + j), g, cell_start, items, item_mbr,
+                                      nullptr, nullptr);
+    if (lane == j) n = cnt;
+  }
   // CTA exclusive scan of the counts
   long long x = n;
   for (int o = 1; o < 32; o <<= 1) {
@@ -249,7 +372,15 @@ __global__ void __launch_bounds__(kProbeTile) probe_kernel(const int4* __restric
   }
   __syncthreads();
   const long long base = s_base + excl;
-  if (pairs && n > 0 && base + n <= cap) {
+  const bool fits = pairs && n > 0 && base + n <= cap;
+  // big MBRs: gathered by the warp, unsorted
+  for (unsigned bm = __ballot_sync(0xffffffffu, coop && fits); bm; bm &= bm - 1) {
+    const int j = __ffs(bm) - 1;
+    int2* seg = pairs + __shfl_sync(0xffffffffu, base, j);
+    coop_cells<true>(shfl4(a, j), p - threadIdx.x + (warp * 32 + j), g, cell_start, items, item_mbr, seg,
+                     &s_fill[warp]);
+  }
+  if (fits && !coop) {
     int2* seg = pairs + base;
     if (n <= kKeep) {  // the counting pass kept them: sort in registers, write
       const int big = 0x7fffffff;  // pad the unused slots so a 4-sorting network applies
@@ -272,16 +403,23 @@ __global__ void __launch_bounds__(kProbeTile) probe_kernel(const int4* __restric
       if (n > 3) seg[3] = make_int2((int)p, k3);
     } else {
       probe_cells<true>(a, p, g, cell_start, items, item_mbr, seg, keep);
-      for (int i = 1; i < n; i++) {  // insertion sort of the segment by q (segments are short)
-        const int2 v = seg[i];
-        int j = i - 1;
-        while (j >= 0 && seg[j].y > v.y) {
-          seg[j + 1] = seg[j];
-          j--;
+      if (n <= kThreadSortMax)
+        for (int i = 1; i < n; i++) {  // insertion sort of a short segment by q
+          const int2 v = seg[i];
+          int j = i - 1;
+          while (j >= 0 && seg[j].y > v.y) {
+            seg[j + 1] = seg[j];
+            j--;
+          }
+          seg[j + 1] = v;
         }
-        seg[j + 1] = v;
-      }
     }
+  }
+  // long segments (big MBRs, or many hits): sorted by the warp
+  __syncwarp();
+  for (unsigned bm = __ballot_sync(0xffffffffu, fits && (coop || n > kThreadSortMax)); bm; bm &= bm - 1) {
+    const int j = __ffs(bm) - 1;
+    warp_sort_segment(pairs + __shfl_sync(0xffffffffu, base, j), __shfl_sync(0xffffffffu, n, j), s_sort, &s_lock);
   }
 }
 
@@ -349,11 +487,13 @@ static int filter_enqueue(const sccg_polyset* P, const sccg_polyset* Q, FilterWs
   grid_select_kernel<<<1, 32, 0, stream>>>(reinterpret_cast<const SetStats*>(P->stats),
                                            reinterpret_cast<const SetStats*>(Q->stats), C, entry_cap(nq), w.grid);
   cudaMemsetAsync(w.cell_count, 0, sizeof(int) * (C + 1), stream);
-  if (nq > 0) grid_count_kernel<<<blocks_for(nq, 256), 256, 0, stream>>>(mq, nq, w.grid, w.cell_count);
+  if (nq > 0)
+    grid_bucket_kernel<false><<<blocks_for(nq, 256), 256, 0, stream>>>(mq, nq, w.grid, nullptr, w.cell_count,
+                                                                        nullptr, nullptr);
   cub::DeviceScan::ExclusiveSum(w.tmp, w.tmp_bytes, w.cell_count, w.cell_start, (int)(C + 1), stream);
   if (nq > 0)
-    grid_fill_kernel<<<blocks_for(nq, 256), 256, 0, stream>>>(mq, nq, w.grid, w.cell_start, w.cell_count, w.items,
-                                                               w.item_mbr);
+    grid_bucket_kernel<true><<<blocks_for(nq, 256), 256, 0, stream>>>(mq, nq, w.grid, w.cell_start, w.cell_count,
+                                                                        w.items, w.item_mbr);
   // 2. probe (tile states, ticket and total zeroed: one memset, contiguous)
   cudaMemsetAsync(w.tile_state, 0, sizeof(unsigned long long) * (T + 2), stream);
   if (np > 0)

@@ -157,6 +157,29 @@ def test_filter_random_boxes_and_touching(sccg):
     assert sccg.filter_pairs(dev(A, sccg), dev(B, sccg)).shape[0] == 0
 
 
+def test_filter_long_segments(sccg):
+    """Polygons of P that pair with many Q (a gland over nuclei, C3): segments
+    of 5..32 (thread sort), 33..4096 (warp bitonic sort) and > 4096 (fallback)
+    pairs, from MBRs covering few or many grid cells, all sorted by (p, q)."""
+    rng = np.random.default_rng(23)
+    rings_q = []
+    for i in range(9000):  # small boxes on a jittered lattice
+        x, y = 3 * (i % 100) + int(rng.integers(0, 2)), 3 * (i // 100) + int(rng.integers(0, 2))
+        rings_q.append([[x, y], [x + 2, y], [x + 2, y + 2], [x, y + 2]])
+    rings_p = [
+        [[0, 0], [300, 0], [300, 300], [0, 300]],  # > 4096 pairs
+        [[10, 10], [70, 10], [70, 70], [10, 70]],  # ~400 pairs
+        [[100, 100], [112, 100], [112, 106], [100, 106]],  # ~10-30 pairs
+        [[150, 150], [152, 150], [152, 152], [150, 152]],  # a few
+    ]
+    A, B = synth.pack(rings_p), synth.pack(rings_q)
+    got = sccg.filter_pairs(dev(A, sccg), dev(B, sccg)).cpu().numpy()
+    want = oracle.join(A, B)
+    assert got.tolist() == want.tolist()
+    counts = np.bincount(want[:, 0], minlength=4)
+    assert counts[0] > 4096 and 32 < counts[1] <= 4096 and 4 < counts[2] <= 32, counts
+
+
 def test_filter_capacity_retry(sccg, tile_sets):
     A, B = tile_sets
     got = sccg.filter_pairs(dev(A, sccg), dev(B, sccg), cap=3).cpu().numpy()
