@@ -179,15 +179,26 @@ def run_ours(args, rank, world, local_rank):
     # the whole step (prep x2, join, PixelBox) device-resident, no host sync until
     # the sums are read; replayed as two CUDA graphs (join | PixelBox)
     pipe = sccg.Pipeline(P, Q, cap=3 * max(P.n, Q.n) + 1024, threshold=args.threshold, graph=True)
-    stage_ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    # Steps are pipelined on the host: step i+1 is enqueued before step i's
+    # sums are read (the D2H copy is in-stream into one of two pinned buffers),
+    # so the GPU never idles on the host's per-step read-back; every step's
+    # result is still read and checked.
+    host_bufs = [torch.zeros(len(sccg.SUMS_FIELDS), dtype=torch.int64).pin_memory() for _ in range(2)]
+    done_ev = [torch.cuda.Event() for _ in range(2)]
 
-    def step(timing=False):
-        sums = pipe.run(stage_ev if timing else None)
+    def enqueue(i, events=None):
+        sums = pipe.run(events)
         sdist.allreduce_sums(sums)  # row a9: the only collective (NCCL, int64 SUM)
-        return sccg.sums_to_host(sums.cpu())  # the step's one host synchronisation
+        host_bufs[i % 2].copy_(sums, non_blocking=True)
+        done_ev[i % 2].record()
 
-    for _ in range(max(args.warmup, 3)):
-        step()
+    def collect(i):
+        done_ev[i % 2].synchronize()
+        return sccg.sums_to_host(host_bufs[i % 2])
+
+    for i in range(max(args.warmup, 3)):
+        enqueue(i)
+        first = collect(i)
     n_local = pipe.check()
     # one untimed counting run for the algorithmic work per launch
     counters = torch.zeros(8, dtype=torch.int64, device=dev)
@@ -201,17 +212,24 @@ def run_ours(args, rank, world, local_rank):
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    stage_ms = [0.0, 0.0, 0.0]  # prep x2 | join | PixelBox, live CUDA events on the launch stream
+    # prep | join | PixelBox: live CUDA events on the launch stream, per step
+    stage_ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    results = []
     with ClockSampler(local_rank) as clk:
         t0.record(stream)
         wall0 = time.perf_counter()
-        for _ in range(args.steps):
-            host = step(timing=True)
-            for k in range(3):
-                stage_ms[k] += stage_ev[k].elapsed_time(stage_ev[k + 1])
+        for i in range(args.steps):
+            enqueue(i, stage_ev[i])
+            if i > 0:
+                results.append(collect(i - 1))
+        results.append(collect(args.steps - 1))
         t1.record(stream)
         torch.cuda.synchronize()
         wall1 = time.perf_counter()
+    stage_ms = [sum(ev[k].elapsed_time(ev[k + 1]) for ev in stage_ev) for k in range(3)]
+    host = results[-1]
+    if any(bytes(r) != bytes(first) for r in results):
+        raise RuntimeError("a timed step's sums differ from the warm-up's (nondeterminism)")
     if world > 1:
         dist.barrier()
     pipe.check()
