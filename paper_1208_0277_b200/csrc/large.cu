@@ -378,6 +378,7 @@ __global__ void __launch_bounds__(kLWarps * 32)
   const long long nl = min((long long)(w.ctr[2] & 0xffffffffull), n_cap);
   const long long ne = min((long long)w.ctr[1], w.extra_cap);
   const long long total = nl + ne;
+  if (total == 0) return;  // no large pairs in this batch
   unsigned status = 0;
   // batch totals of the pairs this warp finalizes (lane 0)
   unsigned long long a_n = 0, a_nz = 0, a_i = 0, a_u = 0, a_ap = 0, a_aq = 0, l0 = 0, l1 = 0, l2 = 0, l3 = 0, rootpx = 0;

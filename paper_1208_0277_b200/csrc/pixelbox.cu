@@ -29,8 +29,9 @@ namespace sccg {
 // per lane (one 32-bit row word), half-warp per polygon when the box has at
 // most 16 rows.  Per-pair results and sums are written lane-parallel.
 constexpr int kSmallWarps = 8;
-constexpr int kSmallCap = 64;   // vertical edges per polygon on this path
-constexpr int kSmallQOff = 72;  // q buffer offset in records (8 B): 576 B, so p[t] and q[t] hit different banks
+constexpr int kSmallCap = 128;   // vertical edges per polygon on this path (> 64: the non-pipelined loop)
+constexpr int kPipeCap = 64;     // ... on the pipelined loop (two records per lane in registers)
+constexpr int kSmallQOff = 136;  // q buffer offset in records (8 B): 1088 B, so p[t] and q[t] hit different banks
 
 // Stage one polygon's row-crossing edges for a box of H <= 32 rows and
 // W <= 32 columns as {row bits, pixel mask}: bit r of `rows` is set iff the
@@ -59,6 +60,29 @@ __device__ __forceinline__ int stage_rows(uint64_t r0, uint64_t r1, int nv, bool
   buf[32 + (keep ? __popc(b & lt) : cnt + __popc(~b & lt))] =
       keep ? make_int2((int)rows, (int)suffix_mask(c + dx)) : make_int2(0, 0);
   return 32 + cnt;
+}
+
+// stage_rows for up to 4 blocks of 32 records read from `rec` (L1-resident
+// after the first window); returns 32 (nb - 1) + the last block's kept count.
+__device__ __forceinline__ int stage_blocks(const uint64_t* __restrict__ rec, int nv, int nb, int dx, int dy, int H,
+                                            int2* buf) {
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = lanemask_lt();
+  int cnt = 0;
+#pragma unroll
+  for (int blk = 0; blk < 4; blk++) {
+    if (blk < nb) {
+      int c, lo, hi;
+      unpack_edge(lane + 32 * blk < nv ? __ldg(rec + 32 * blk + lane) : 0ull, c, lo, hi);
+      const unsigned rows = low_bits(min(hi + dy, H)) & ~low_bits(lo + dy);
+      const bool keep = lane + 32 * blk < nv && rows != 0;
+      const unsigned b = __ballot_sync(FULL, keep);
+      cnt = __popc(b);
+      buf[32 * blk + (keep ? __popc(b & lt) : cnt + __popc(~b & lt))] =
+          keep ? make_int2((int)rows, (int)suffix_mask(c + dx)) : make_int2(0, 0);
+    }
+  }
+  return 32 * (nb - 1) + cnt;
 }
 
 // m ^= mask if (rows & bit) != 0 -- one predicate-producing LOP3 and one
@@ -149,7 +173,7 @@ __global__ void __launch_bounds__(kSmallWarps * 32, SCCG_SMALL_MINB)
       H = min(mp.w, mq.w) - by0;
       const int dxp = mp.x - bx0, dyp = mp.y - by0, dxq = mq.x - bx0, dyq = mq.y - by0;
       empty = !(W > 0 && H > 0);  // reading R18: I = 0
-      small = mode == 0 && !empty && W <= 32 && H <= 32 && W * H < T && cp.x <= kSmallCap && cq.x <= kSmallCap &&
+      small = mode == 0 && !empty && W <= 64 && H <= 64 && W * H < T && cp.x <= kSmallCap && cq.x <= kSmallCap &&
               op + cp.x < (1ll << 31) && oq + cq.x < (1ll << 31) && min(min(dxp, dyp), min(dxq, dyq)) >= -32768;
       if (mode != 0) {  // PixelOnly / NoSep (§5.2 baselines): the box of MBR(p) u MBR(q), union counted directly
         empty = false;
@@ -157,10 +181,10 @@ __global__ void __launch_bounds__(kSmallWarps * 32, SCCG_SMALL_MINB)
         H = max(mp.w, mq.w) - min(mp.y, mq.y);
       }
       // both rings carry a raster (prep): the pair reads pixel classifications instead of edges.
-      // meta.x: W (bits 0-5), H (6-11), nv_p (12-18), nv_q (20-26), raster (28)
-      rast = (small && use_raster && (cp.y & kRasterFlag) && (cq.y & kRasterFlag)) ? 1u : 0u;
-      meta[lane] = make_int4((int)((unsigned)W | ((unsigned)H << 6) | ((unsigned)cp.x << 12) | ((unsigned)cq.x << 20) |
-                                   (rast << 28)),
+      // meta.x: W (bits 0-6), H (7-13), nv_p (14-21), nv_q (22-29), raster (30)
+      rast = (small && use_raster && W <= 32 && H <= 32 && (cp.y & kRasterFlag) && (cq.y & kRasterFlag)) ? 1u : 0u;
+      meta[lane] = make_int4((int)((unsigned)W | ((unsigned)H << 7) | ((unsigned)cp.x << 14) | ((unsigned)cq.x << 22) |
+                                   (rast << 30)),
                              (int)(((unsigned)dxp & 0xffffu) | ((unsigned)dyp << 16)),
                              (int)(((unsigned)dxq & 0xffffu) | ((unsigned)dyq << 16)), 0);
       epq[lane] = make_int2((int)op, (int)oq);
@@ -200,8 +224,8 @@ __global__ void __launch_bounds__(kSmallWarps * 32, SCCG_SMALL_MINB)
         const int4 mm = meta[lane];
         const int2 e = epq[lane];
         const unsigned mj = (unsigned)mm.x;
-        s_rp[warp][lane] = reinterpret_cast<const unsigned*>(Ps.edges + e.x + ((mj >> 12) & 127)) - (mm.y >> 16);
-        s_rq[warp][lane] = reinterpret_cast<const unsigned*>(Qs.edges + e.y + ((mj >> 20) & 127)) - (mm.z >> 16);
+        s_rp[warp][lane] = reinterpret_cast<const unsigned*>(Ps.edges + e.x + ((mj >> 14) & 255)) - (mm.y >> 16);
+        s_rq[warp][lane] = reinterpret_cast<const unsigned*>(Qs.edges + e.y + ((mj >> 22) & 255)) - (mm.z >> 16);
         s_rsh[warp][lane] = (unsigned)(-(int)(short)(mm.y & 0xffff)) | ((unsigned)(-(int)(short)(mm.z & 0xffff)) << 8) |
                             ((unsigned)W << 16);
       }
@@ -244,13 +268,15 @@ __global__ void __launch_bounds__(kSmallWarps * 32, SCCG_SMALL_MINB)
       __syncwarp();
       if (rast) myI = rcnt[lane];
     }
-    unsigned todo = __ballot_sync(FULL, small) & ~rmask;
+    const unsigned wide = __ballot_sync(FULL, small && max(((unsigned)meta[lane].x >> 14) & 255,
+                                                             ((unsigned)meta[lane].x >> 22) & 255) > kPipeCap);
+    unsigned todo = __ballot_sync(FULL, small) & ~rmask & ~wide;
     uint64_t np0 = 0, np1 = 0, nq0 = 0, nq1 = 0;
     auto prefetch = [&](int j) {
       const int4 mm = meta[j];
       const unsigned mj = (unsigned)mm.x;
       const int2 e = epq[j];
-      const int nvp = (mj >> 12) & 127, nvq = (mj >> 20) & 127;
+      const int nvp = (mj >> 14) & 255, nvq = (mj >> 22) & 255;
       const uint64_t* pe = Ps.edges + e.x;
       const uint64_t* qe = Qs.edges + e.y;
       np0 = lane < nvp ? __ldg(pe + lane) : 0ull;
@@ -268,26 +294,71 @@ __global__ void __launch_bounds__(kSmallWarps * 32, SCCG_SMALL_MINB)
       if (todo) prefetch(__ffs(todo) - 1);
       const int4 mm = meta[j];
       const unsigned mj = (unsigned)mm.x, dpj = (unsigned)mm.y, dqj = (unsigned)mm.z;
-      const int W = mj & 63, H = (mj >> 6) & 63, nvp = (mj >> 12) & 127, nvq = (mj >> 20) & 127;
+      const int Wb = mj & 127, Hb = (mj >> 7) & 127, nvp = (mj >> 14) & 255, nvq = (mj >> 22) & 255;
       const bool two = max(nvp, nvq) > 32;
-      const int cntp = stage_rows(cp0, cp1, nvp, two, (int)(short)(dpj & 0xffffu), (int)dpj >> 16, H, bp);
-      const int cntq = stage_rows(cq0, cq1, nvq, two, (int)(short)(dqj & 0xffffu), (int)dqj >> 16, H, bq);
-      // half-warp per polygon (lanes 0-15: p, 16-31: q), rows lane&15 (+16)
-      const int npad = (max(cntp, cntq) + 3) & ~3;
-      __syncwarp();
-      const int2* b = lane < 16 ? bp : bq;
-      unsigned m0 = 0, m1 = 0;
-      if (H <= 16)
-        row_words<false>(b, npad, bit0, bit1, m0, m1);
-      else
-        row_words<true>(b, npad, bit0, bit1, m0, m1);
-      const unsigned o0 = __shfl_xor_sync(FULL, m0, 16), o1 = __shfl_xor_sync(FULL, m1, 16);
-      const unsigned wmask = low_bits(W);
-      const unsigned cnt = lane < 16 ? __popc(m0 & o0 & wmask) + __popc(m1 & o1 & wmask) : 0u;
-      const unsigned I = __reduce_add_sync(FULL, cnt);
-      if (lane == j) myI = I;
-      if (COUNT) c_tests += (unsigned long long)H * (cntp + cntq);
-      __syncwarp();  // buffers are rewritten by the next pair
+      const int dxp = (int)(short)(dpj & 0xffffu), dyp = (int)dpj >> 16;
+      const int dxq = (int)(short)(dqj & 0xffffu), dyq = (int)dqj >> 16;
+      // boxes up to 64 x 64 in windows of <= 32 x 32: the records stay in
+      // registers; a record left of a window toggles all of its pixels
+      unsigned Ij = 0;
+      for (int wy = 0; wy < Hb; wy += 32)
+        for (int wx = 0; wx < Wb; wx += 32) {
+          const int W = min(32, Wb - wx), H = min(32, Hb - wy);
+          const int cntp = stage_rows(cp0, cp1, nvp, two, dxp - wx, dyp - wy, H, bp);
+          const int cntq = stage_rows(cq0, cq1, nvq, two, dxq - wx, dyq - wy, H, bq);
+          // half-warp per polygon (lanes 0-15: p, 16-31: q), rows lane&15 (+16)
+          const int npad = (max(cntp, cntq) + 3) & ~3;
+          __syncwarp();
+          const int2* b = lane < 16 ? bp : bq;
+          unsigned m0 = 0, m1 = 0;
+          if (H <= 16)
+            row_words<false>(b, npad, bit0, bit1, m0, m1);
+          else
+            row_words<true>(b, npad, bit0, bit1, m0, m1);
+          const unsigned o0 = __shfl_xor_sync(FULL, m0, 16), o1 = __shfl_xor_sync(FULL, m1, 16);
+          const unsigned wmask = low_bits(W);
+          const unsigned cnt = lane < 16 ? __popc(m0 & o0 & wmask) + __popc(m1 & o1 & wmask) : 0u;
+          Ij += __reduce_add_sync(FULL, cnt);
+          if (COUNT) c_tests += (unsigned long long)H * (cntp + cntq);
+          __syncwarp();  // buffers are rewritten by the next window / pair
+        }
+      if (lane == j) myI = Ij;
+    }
+    // ---- small pairs with more than kPipeCap edges in a polygon: records
+    // loaded straight into registers (up to 4 per lane), not pipelined
+    for (unsigned wd = wide; wd; wd &= wd - 1) {
+      const int j = __ffs(wd) - 1;
+      const int4 mm = meta[j];
+      const unsigned mj = (unsigned)mm.x, dpj = (unsigned)mm.y, dqj = (unsigned)mm.z;
+      const int Wb = mj & 127, Hb = (mj >> 7) & 127, nvp = (mj >> 14) & 255, nvq = (mj >> 22) & 255;
+      const int nb = (max(nvp, nvq) + 31) >> 5;
+      const int2 e = epq[j];
+      const uint64_t* rp = Ps.edges + e.x;
+      const uint64_t* rq = Qs.edges + e.y;
+      const int dxp = (int)(short)(dpj & 0xffffu), dyp = (int)dpj >> 16;
+      const int dxq = (int)(short)(dqj & 0xffffu), dyq = (int)dqj >> 16;
+      unsigned Ij = 0;
+      for (int wy = 0; wy < Hb; wy += 32)
+        for (int wx = 0; wx < Wb; wx += 32) {
+          const int W = min(32, Wb - wx), H = min(32, Hb - wy);
+          const int cntp = stage_blocks(rp, nvp, nb, dxp - wx, dyp - wy, H, bp);
+          const int cntq = stage_blocks(rq, nvq, nb, dxq - wx, dyq - wy, H, bq);
+          const int npad = (max(cntp, cntq) + 3) & ~3;
+          __syncwarp();
+          const int2* b = lane < 16 ? bp : bq;
+          unsigned m0 = 0, m1 = 0;
+          if (H <= 16)
+            row_words<false>(b, npad, bit0, bit1, m0, m1);
+          else
+            row_words<true>(b, npad, bit0, bit1, m0, m1);
+          const unsigned o0 = __shfl_xor_sync(FULL, m0, 16), o1 = __shfl_xor_sync(FULL, m1, 16);
+          const unsigned wmask = low_bits(W);
+          const unsigned cnt = lane < 16 ? __popc(m0 & o0 & wmask) + __popc(m1 & o1 & wmask) : 0u;
+          Ij += __reduce_add_sync(FULL, cnt);
+          if (COUNT) c_tests += (unsigned long long)H * (cntp + cntq);
+          __syncwarp();
+        }
+      if (lane == j) myI = Ij;
     }
     // ---- lane-parallel outputs and batch totals
     const unsigned long long c_px_all = COUNT ? warp_sum_u64(small ? (unsigned long long)W * H : 0ull) : 0ull;

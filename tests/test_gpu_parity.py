@@ -236,6 +236,62 @@ def test_pixelbox_skewed_glands(sccg, T):
     assert c[sccg.CNT_SPLITS] > 0 and c[sccg.CNT_PIXBOXES] > 0
 
 
+def _staircase(x0, y0, n, step=1):
+    """Rectilinear staircase ring with n unit steps: n + 1 vertical edges."""
+    ring = [[x0, y0], [x0 + n * step, y0]]
+    for i in range(n, 0, -1):
+        ring += [[x0 + i * step, y0 + (n - i + 1) * step], [x0 + (i - 1) * step, y0 + (n - i + 1) * step]]
+    return ring[:-1] + [[x0, y0 + n * step]]
+
+
+def test_pixelbox_windows_and_wide_pairs(sccg):
+    """Pair boxes of 33..64 px (pixelized in <= 32 x 32 windows) and polygons
+    with 65..128 vertical edges (the non-pipelined loop), against the oracle."""
+    rng = np.random.default_rng(31)
+    rp, rq = [], []
+    for t in range(400):
+        x0, y0 = 400 * (t % 20), 400 * (t // 20)
+        kind = t % 4
+        if kind == 0:  # windows: random rects, boxes up to 64
+            w1, h1, w2, h2 = (int(v) for v in rng.integers(20, 65, 4))
+            dx, dy = (int(v) for v in rng.integers(-10, 10, 2))
+            rp.append([[x0, y0], [x0 + w1, y0], [x0 + w1, y0 + h1], [x0, y0 + h1]])
+            rq.append([[x0 + dx, y0 + dy], [x0 + dx + w2, y0 + dy], [x0 + dx + w2, y0 + dy + h2], [x0 + dx, y0 + dy + h2]])
+        elif kind == 1:  # wide: a staircase of 65..127 steps over a box <= 64
+            n = int(rng.integers(65, 128))
+            rp.append(_staircase(x0, y0, n))
+            a, b = int(rng.integers(0, n - 64)), int(rng.integers(0, n - 64))
+            rq.append([[x0 + a, y0 + b], [x0 + a + 60, y0 + b], [x0 + a + 60, y0 + b + 50], [x0 + a, y0 + b + 50]])
+        elif kind == 2:  # wide on both sides
+            n, m = (int(v) for v in rng.integers(65, 128, 2))
+            rp.append(_staircase(x0, y0, n))
+            ox, oy = x0 + n - 60, y0 + n - 60  # MBR overlap 60 x 60
+            rq.append([[ox + x, oy + m - y] for x, y in _staircase(0, 0, m)][::-1])
+        else:  # a 1-px-step staircase against a staircase: many edges, box 33..64
+            n = int(rng.integers(33, 64))
+            rp.append(_staircase(x0, y0, n))
+            rq.append(_staircase(x0 + 2, y0 + 1, n))
+    A, B = synth.pack(rp), synth.pack(rq)
+    P, Q = dev(A, sccg), dev(B, sccg)
+    pairs = sccg.filter_pairs(P, Q)
+    assert pairs.shape[0] >= 400
+    # by construction every pair is on the small kernel (box <= 64 x 64, <= 128
+    # vertical edges per polygon), and both new routes occur
+    pr = pairs.long()
+    mp, mq = P.mbr.long()[pr[:, 0]], Q.mbr.long()[pr[:, 1]]
+    W = torch.minimum(mp[:, 2], mq[:, 2]) - torch.maximum(mp[:, 0], mq[:, 0])
+    H = torch.minimum(mp[:, 3], mq[:, 3]) - torch.maximum(mp[:, 1], mq[:, 1])
+    nv = torch.maximum(P.ecount.long()[pr[:, 0], 0], Q.ecount.long()[pr[:, 1], 0])
+    assert int(W.max()) <= 64 and int(H.max()) <= 64 and int(nv.max()) <= 128
+    assert int(((W > 32) | (H > 32)).sum()) > 50 and int((nv > 64).sum()) > 50
+    for raster in (True, False):
+        inter, uni, sums = sccg.pixelbox(P, Q, pairs, threshold=1 << 30, raster=raster)
+        check_batch(sccg, A, B, pairs.cpu().numpy(), inter, uni, sums)
+    counters = torch.zeros(8, dtype=torch.int64, device="cuda")
+    sccg.pixelbox(P, Q, pairs, threshold=1 << 30, counters=counters)
+    assert int(counters[sccg.CNT_BOXES]) == 0  # every pair took the small kernel's pixelization
+
+
 def test_pixelbox_combs_closed_form(sccg):
     """Config 5 analog: highly concave combs, pinned by rectangle decomposition."""
     A, B, (RA, RB) = combs.generate(n_pairs=96, want_rects=True)
