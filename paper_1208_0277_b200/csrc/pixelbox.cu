@@ -237,33 +237,50 @@ __global__ void __launch_bounds__(kSmallWarps * 32, SCCG_SMALL_MINB)
       }
       __syncwarp();
       const unsigned le = lanemask_lt() | (1u << lane);
-      for (int t0 = 0; t0 < R; t0 += 32) {  // warp-uniform trip count
-        const int t = t0 + lane;
-        const bool act = t < R;
-        unsigned c = 0u;
-        int jr = 0;
-        bool head = !act || lane == 0;
-        if (act) {
-          jr = rmap[t];
-          const int r = t - rstart[jr];
-          head |= r == 0;
-          const unsigned sh = s_rsh[warp][jr];
-          const unsigned wp = __ldg(s_rp[warp][jr] + r) >> (sh & 0xffu);
-          const unsigned wq = __ldg(s_rq[warp][jr] + r) >> ((sh >> 8) & 0xffu);
-          c = (unsigned)__popc(wp & wq & low_bits((int)(sh >> 16)));
-        }
-        // each pair's items occupy consecutive lanes: segmented shuffle sum, the
-        // segment's first lane adds it to the pair's count
-        const unsigned heads = __ballot_sync(FULL, head);
-        const unsigned after = heads & ~le;
-        const int next = after ? __ffs(after) - 1 : 32;
+      // four 32-item groups per round: all eight row loads are issued before
+      // any is consumed (many loads in flight per lane)
+      constexpr int kU = 4;
+      for (int t0 = 0; t0 < R; t0 += 32 * kU) {  // warp-uniform trip count
+        unsigned wpv[kU], wqv[kU], shv[kU];
+        int jrv[kU];
+        bool hv[kU], av[kU];
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const unsigned v = __shfl_down_sync(FULL, c, o);
-          if (lane + o < next) c += v;
+        for (int u = 0; u < kU; u++) {
+          const int t = t0 + 32 * u + lane;
+          av[u] = t < R;
+          hv[u] = !av[u] || lane == 0;
+          jrv[u] = 0;
+          wpv[u] = wqv[u] = shv[u] = 0u;
+          if (av[u]) {
+            const int jr = rmap[t];
+            const int r = t - rstart[jr];
+            hv[u] |= r == 0;
+            jrv[u] = jr;
+            shv[u] = s_rsh[warp][jr];
+            wpv[u] = __ldg(s_rp[warp][jr] + r);
+            wqv[u] = __ldg(s_rq[warp][jr] + r);
+          }
         }
-        if (act && ((heads >> lane) & 1u)) rcnt[jr] += c;
-        __syncwarp();
+#pragma unroll
+        for (int u = 0; u < kU; u++) {
+          if (t0 + 32 * u >= R) break;  // warp-uniform
+          const unsigned sh = shv[u];
+          unsigned c = av[u] ? (unsigned)__popc((wpv[u] >> (sh & 0xffu)) & (wqv[u] >> ((sh >> 8) & 0xffu)) &
+                                                low_bits((int)(sh >> 16)))
+                             : 0u;
+          // each pair's items occupy consecutive lanes: segmented shuffle sum,
+          // the segment's first lane adds it to the pair's count
+          const unsigned heads = __ballot_sync(FULL, hv[u]);
+          const unsigned after = heads & ~le;
+          const int next = after ? __ffs(after) - 1 : 32;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const unsigned v = __shfl_down_sync(FULL, c, o);
+            if (lane + o < next) c += v;
+          }
+          if (av[u] && ((heads >> lane) & 1u)) rcnt[jrv[u]] += c;
+          __syncwarp();
+        }
       }
       __syncwarp();
       if (rast) myI = rcnt[lane];
