@@ -1,0 +1,87 @@
+"""Turn a round's raw GPU outputs (scripts/gpu_profile.sh) into the tracked
+summaries under profiles/<round>/: bench lines, the launch list and its per-step
+summary, and key ncu metrics of each captured kernel.
+
+    python scripts/collect_profiles.py gpurun_out/round_r01 profiles/r01
+"""
+import csv
+import json
+import os
+import shutil
+import subprocess
+import sys
+
+KEYS = [
+    "gpu__time_duration.sum", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+    "smsp__issue_active.avg.pct_of_peak_sustained_active", "sm__warps_active.avg.per_cycle_active",
+    "smsp__inst_executed.sum", "smsp__thread_inst_executed_per_inst_executed.ratio",
+    "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active",
+    "l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed",
+    "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+    "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "launch__grid_size", "launch__block_size",
+    "launch__registers_per_thread", "sm__cycles_elapsed.avg.per_second",
+]
+
+
+def ncu_summary(rep):
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(raw.splitlines()))
+    h, units, vals = rows[0], rows[1], rows[2]
+    d = {h[i]: (vals[i], units[i]) for i in range(len(h))}
+    lines = [f"kernel: {d.get('Kernel Name', ('?', ''))[0]}"]
+    for k in KEYS:
+        if k in d:
+            lines.append(f"{k:70s} {d[k][0]} {d[k][1]}")
+    st = []
+    for k, (v, _) in d.items():
+        if k.startswith("smsp__average_warps_issue_stalled") and k.endswith("per_issue_active.ratio"):
+            try:
+                st.append((float(v), k[len("smsp__average_warps_issue_stalled_"):-len("_per_issue_active.ratio")]))
+            except ValueError:
+                pass
+    lines.append("stalls (warps per issue): " + ", ".join(f"{n}={v:.2f}" for v, n in sorted(st, reverse=True)[:8]))
+    return "\n".join(lines) + "\n"
+
+
+def launch_summary(path):
+    rows = list(csv.reader(open(path)))
+    hi = [i for i, r in enumerate(rows) if "Kernel Name" in r][0]
+    h, data = rows[hi], rows[hi + 1:]
+    ki, vi = h.index("Kernel Name"), h.index("Metric Value")
+    seq = [(r[ki], float(r[vi].replace(",", ""))) for r in data]
+    idx = [i for i, s in enumerate(seq) if s[0].startswith("sccg::prep_init")] + [len(seq)]
+    # the last timed Pipeline step: a prep_init .. next prep_init window that
+    # holds the async join's filter_result_kernel (e2e steps use the sync join)
+    wins = [seq[a:b] for a, b in zip(idx, idx[1:]) if any("filter_result" in n for n, _ in seq[a:b])]
+    step = wins[-1] if wins else seq
+    out = ["one bench step (timed Pipeline), ncu --metrics gpu__time_duration.sum --clock-control none",
+           "(cold caches, serialised: compare shares, not absolute times)", ""]
+    tot = sum(t for _, t in step)
+    for name, t in step:
+        out.append(f"{t / 1000:9.1f} us  {100 * t / tot:5.1f} %  {name[:90]}")
+    out.append(f"total {tot / 1000:.1f} us over {len(step)} launches")
+    return "\n".join(out) + "\n"
+
+
+def main(src, dst):
+    os.makedirs(dst, exist_ok=True)
+    for name in sorted(os.listdir(src)):
+        p = os.path.join(src, name)
+        if name.startswith("bench_") and name.endswith(".json"):
+            with open(p) as f:
+                line = f.read().strip().splitlines()[-1]
+            json.loads(line)
+            with open(os.path.join(dst, name), "w") as f:
+                f.write(line + "\n")
+        elif name == "launches_slide.csv":
+            shutil.copy(p, os.path.join(dst, name))
+            with open(os.path.join(dst, "launches_slide_summary.txt"), "w") as f:
+                f.write(launch_summary(p))
+        elif name.endswith(".ncu-rep"):
+            with open(os.path.join(dst, name.replace(".ncu-rep", ".txt")), "w") as f:
+                f.write(ncu_summary(p))
+
+
+if __name__ == "__main__":
+    main(sys.argv[1], sys.argv[2])

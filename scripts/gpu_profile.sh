@@ -1,13 +1,25 @@
 #!/bin/bash
-# Profile round: ncu launch list of a short bench + one full capture of the PixelBox kernel.
+# Round profile (one gpurun call): the default bench line, the bench's launch
+# list (ncu gpu__time_duration, --clock-control none), one ncu --set full
+# capture per hot kernel, and one bench line per other config.  Outputs land in
+# gpurun_out/round_${TAG}/; scripts/collect_profiles.py turns them into profiles/.
 set -u
-mkdir -p gpurun_out
-TAG=${1:-v}
-timeout 300 python __graft_entry__.py > gpurun_out/build.txt 2>&1
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_${TAG}.csv \
-  python bench.py --steps 2 --warmup 3 --no-cpu-baseline --e2e-steps 1 > gpurun_out/ncu_launch_bench_${TAG}.txt 2>&1
+TAG=${1:-r01}
+OUT=gpurun_out/round_${TAG}
+mkdir -p $OUT
+timeout 300 python __graft_entry__.py > $OUT/build.txt 2>&1
+echo "build rc=$?"
+timeout 900 python bench.py > $OUT/bench_slide.json 2> $OUT/bench_slide.err
+echo "bench rc=$?"
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches_slide.csv \
+  python bench.py --steps 2 --warmup 3 --no-cpu-baseline --e2e-steps 1 > $OUT/launches_bench.txt 2>&1
 echo "launch list rc=$?"
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:pixelbox_kernel -s 3 -c 1 \
-  -o gpurun_out/prof_${TAG} -f python bench.py --steps 1 --warmup 3 --no-cpu-baseline --e2e-steps 1 > gpurun_out/ncu_full_${TAG}.txt 2>&1
-echo "full rc=$?"
-tail -3 gpurun_out/ncu_full_${TAG}.txt
+for k in prep_kernel probe_kernel small_kernel; do
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:$k -s 1 -c 1 \
+    -o $OUT/ncu_$k -f python bench.py --steps 1 --warmup 3 --no-cpu-baseline --e2e-steps 1 > $OUT/ncu_$k.txt 2>&1
+  echo "ncu $k rc=$?"
+done
+for c in tile skewed combs; do
+  timeout 900 python bench.py --config $c --steps 20 --warmup 3 --no-cpu-baseline > $OUT/bench_$c.json 2> $OUT/bench_$c.err
+  echo "bench $c rc=$?"
+done
