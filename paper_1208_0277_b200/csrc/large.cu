@@ -238,10 +238,11 @@ __device__ __forceinline__ unsigned row_word_local(const LocalPoly& L, const int
   return m ^ (par ? FULL : 0u);
 }
 
-// Pixelization of box B (region coords): (|B n p n q|, |B n (p u q)|); the
-// union only when `uni` (modes 1 and 2 count it directly).
+// Pixelization of a small box B (region coords) by crossing parity, one
+// (row, 32-column word) per lane: (|B n p n q|, |B n (p u q)|); the union only
+// when `uni` (modes 1 and 2 count it directly).
 template <bool COUNT>
-__device__ longlong2 pixelize_local(const LocalPoly& P, const LocalPoly& Q, int x0, int y0, int x1, int y1, int pip,
+__device__ longlong2 pixelize_rows(const LocalPoly& P, const LocalPoly& Q, int x0, int y0, int x1, int y1, int pip,
                                     int piq, bool uni, int4* sv, int* sh, long long* counters) {
   const int lane = threadIdx.x & 31;
   int nvp, nhp, nvq, nhq;
@@ -268,6 +269,124 @@ __device__ longlong2 pixelize_local(const LocalPoly& P, const LocalPoly& Q, int 
     atomicAdd((unsigned long long*)&counters[SCCG_CNT_PIXBOXES], 1ull);
   }
   return make_longlong2(ai, au);
+}
+
+// Pixelization of a larger box B (region coords), same results as
+// pixelize_rows, row by row with the difference trick (the one prep uses for rasters): pixel
+// (x, y) and pixel (x, y - 1) differ in inside-ness exactly when a horizontal
+// edge on the line y spans column x, so row y's words are row y - 1's XOR the
+// range masks of the horizontal edges at y.  Only the box's first row is found
+// by crossing parity (corner parity + one suffix mask per vertical edge, R19);
+// every further row costs its share of the horizontal edges plus a prefix XOR.
+// The box is processed in column strips of <= 128 pixels (4 words) and bands
+// of rows that fit the row buffer (the staging area, reused once the first row
+// is done); a band starts from the previous band's last row.
+constexpr int kDWords = (int)((2 * kLStage * sizeof(int4) + 2 * kLStage * sizeof(int)) / sizeof(unsigned) / 2);
+
+template <bool COUNT>
+__device__ longlong2 pixelize_bands(const LocalPoly& P, const LocalPoly& Q, int x0, int y0, int x1, int y1, int pip,
+                                    int piq, bool uni, int4* sv, int* sh, long long* counters) {
+  const int lane = threadIdx.x & 31;
+  unsigned* DP = reinterpret_cast<unsigned*>(sv);  // row words, [row][word], per polygon
+  unsigned* DQ = DP + kDWords;
+  const int Wb = x1 - x0, Hb = y1 - y0;
+  long long ai = 0, au = 0;
+  unsigned long long tests = 0;
+  for (int sx = 0; sx < Wb; sx += 128) {  // column strips (warp-uniform)
+    const int sw = min(128, Wb - sx), nw = (sw + 31) >> 5;
+    const int RB = kDWords / nw;
+    // first row of the strip by crossing parity: lanes 0..nw-1 for p, 8..8+nw-1 for q
+    int nvp, nhp, nvq, nhq;
+    stage_local(P, x0, y0, x1, y1, sv, sh, nvp, nhp);
+    stage_local(Q, x0, y0, x1, y1, sv + kLStage, sh + kLStage, nvq, nhq);
+    __syncwarp();
+    unsigned carry = 0;
+    if (lane < nw)
+      carry = row_word_local(P, sv, sh, nvp, nhp, x0, y0, x1, y1, pip, 0, sx + 32 * lane);
+    else if (lane >= 8 && lane < 8 + nw)
+      carry = row_word_local(Q, sv + kLStage, sh + kLStage, nvq, nhq, x0, y0, x1, y1, piq, 0, sx + 32 * (lane - 8));
+    if (COUNT) tests += (unsigned long long)nw * (nvp + nvq);
+    __syncwarp();  // the staging area becomes the row buffer
+    for (int by = 0; by < Hb; by += RB) {  // bands of rows (warp-uniform)
+      const int rb = min(RB, Hb - by);
+      for (int i = lane; i < rb * nw; i += 32) DP[i] = DQ[i] = 0u;
+      __syncwarp();
+      if (lane < nw) DP[lane] = carry;  // band row 0 starts from the row below it
+      if (lane >= 8 && lane < 8 + nw) DQ[lane - 8] = carry;
+      __syncwarp();
+      // horizontal edges on the lines y0 + by + r (r >= 1 in the first band):
+      // toggle row r over the strip columns they span
+      const int cx0 = x0 + sx, cx1 = x0 + sx + sw;
+      for (int side = 0; side < 2; side++) {
+        const LocalPoly& L = side ? Q : P;
+        unsigned* D = side ? DQ : DP;
+        for (int t = lane; t < L.nH; t += 32) {
+          int y, xl, xh;
+          unpack_loc(L.H[t], y, xl, xh);
+          const int r = y - y0 - by;
+          const int a = max(xl, cx0) - cx0, b = min(xh, cx1) - cx0;
+          if (y > y0 && r >= 0 && r < rb && a < b)
+            for (int w = a >> 5; w <= (b - 1) >> 5; w++)
+              atomicXor(&D[r * nw + w], low_bits(min(b - 32 * w, 32)) & ~low_bits(max(a - 32 * w, 0)));
+        }
+      }
+      __syncwarp();
+      // prefix XOR down the rows: four lanes per (polygon, word) sequence
+      {
+        const int g = lane >> 2, sub = lane & 3, w = g & 3;
+        unsigned* D = (g >> 2) ? DQ : DP;
+        const bool act = w < nw;
+        const int per = (rb + 3) >> 2, r0 = min(rb, sub * per), r1 = min(rb, r0 + per);
+        unsigned tot = 0;
+        if (act)
+          for (int r = r0; r < r1; r++) tot ^= D[r * nw + w];
+        unsigned ex = tot;  // exclusive XOR-scan over the group's 4 lanes
+        unsigned v = __shfl_up_sync(0xffffffffu, ex, 1, 4);
+        ex = sub >= 1 ? ex ^ v : ex;
+        v = __shfl_up_sync(0xffffffffu, ex, 2, 4);
+        ex = sub >= 2 ? ex ^ v : ex;
+        ex ^= tot;
+        if (act) {
+          unsigned acc = ex;
+          for (int r = r0; r < r1; r++) {
+            acc ^= D[r * nw + w];
+            D[r * nw + w] = acc;
+          }
+        }
+      }
+      __syncwarp();
+      for (int i = lane; i < rb * nw; i += 32) {
+        const int w = i % nw;
+        const unsigned valid = low_bits(sw - 32 * w);
+        const unsigned mp = DP[i], mq = DQ[i];
+        ai += __popc(mp & mq & valid);
+        if (uni) au += __popc((mp | mq) & valid);
+      }
+      if (lane < nw) carry = DP[(rb - 1) * nw + lane];
+      if (lane >= 8 && lane < 8 + nw) carry = DQ[(rb - 1) * nw + lane - 8];
+      __syncwarp();
+    }
+  }
+  if (COUNT) {
+    if (lane == 0) {  // tests is warp-uniform
+      atomicAdd((unsigned long long*)&counters[SCCG_CNT_PIXELS], (unsigned long long)Wb * Hb);
+      atomicAdd((unsigned long long*)&counters[SCCG_CNT_ROWTESTS], tests);
+      atomicAdd((unsigned long long*)&counters[SCCG_CNT_PIXBOXES], 1ull);
+    }
+  }
+  return make_longlong2(ai, au);
+}
+
+// Boxes of up to eight (row, word) items per lane pixelize by crossing parity;
+// larger ones by bands (first row by crossings, the rest by the difference
+// trick), whose cost grows with edges + rows instead of edges x rows.
+template <bool COUNT>
+__device__ __forceinline__ longlong2 pixelize_local(const LocalPoly& P, const LocalPoly& Q, int x0, int y0, int x1,
+                                                   int y1, int pip, int piq, bool uni, int4* sv, int* sh,
+                                                   long long* counters) {
+  if ((y1 - y0) * ((x1 - x0 + 31) >> 5) <= 256)
+    return pixelize_rows<COUNT>(P, Q, x0, y0, x1, y1, pip, piq, uni, sv, sh, counters);
+  return pixelize_bands<COUNT>(P, Q, x0, y0, x1, y1, pip, piq, uni, sv, sh, counters);
 }
 
 // sampling-box stack entry: x0, y0, x1, y1 (15 bit each, region coords), parity bits of both polygons
@@ -358,7 +477,7 @@ constexpr size_t kLSmemPerWarp = (size_t)4 * kLCap * sizeof(uint64_t) + (size_t)
 constexpr size_t kLSmem = kLWarps * kLSmemPerWarp;
 
 template <bool COUNT>
-__global__ void __launch_bounds__(kLWarps * 32)
+__global__ void __launch_bounds__(kLWarps * 32, 4)
     item_kernel(DevSet Ps, DevSet Qs, const int2* __restrict__ pairs, LargeWs w, int T, int mode,
                 long long* __restrict__ inter, long long* __restrict__ uni, long long* counters, sccg_sums* sums,
                 unsigned* __restrict__ hit_p, unsigned* __restrict__ hit_q) {

@@ -298,11 +298,15 @@ def test_pixelbox_combs_closed_form(sccg):
     P, Q = dev(A, sccg), dev(B, sccg)
     pairs = sccg.filter_pairs(P, Q)
     assert pairs.cpu().numpy().tolist() == [[k, k] for k in range(96)]
-    for T in (256, 4096):
-        inter, uni, sums = sccg.pixelbox(P, Q, pairs, threshold=T)
-        gi = inter.cpu().numpy()
+    # small T: many small leaf boxes (per-row crossings); 2^30: whole regions
+    # pixelized in bands (difference trick); modes 1/2 count the union directly
+    for T, mode in ((256, 0), (4096, 0), (1 << 30, 0), (1 << 30, 1), (4096, 2)):
+        inter, uni, sums = sccg.pixelbox(P, Q, pairs, threshold=T, mode=mode)
+        gi, gu = inter.cpu().numpy(), uni.cpu().numpy()
         for k in range(96):
-            assert gi[k] == combs.rect_decomp_intersection(RA[k], RB[k])
+            want = combs.rect_decomp_intersection(RA[k], RB[k])
+            assert gi[k] == want, (T, mode, k)
+            assert gu[k] == combs.rect_decomp_area(RA[k]) + combs.rect_decomp_area(RB[k]) - want, (T, mode, k)
     check_batch(sccg, A, B, pairs.cpu().numpy()[:24], *sccg.pixelbox(P, Q, pairs[:24]))
 
 
