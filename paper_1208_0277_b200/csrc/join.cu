@@ -143,16 +143,7 @@ __global__ void grid_bucket_kernel(const int4* __restrict__ mq, int64_t nq, cons
   }
 }
 
-// Probe, one pass.  Thread per p, CTA per tile of kProbeTile consecutive p
-// (tiles taken in order from an atomic ticket).  A pair is owned by the cell
-// that holds its reference point (max xlo, max ylo).  Each thread counts its
-// pairs; the CTA scans the counts and obtains its tile's output offset by
-// decoupled look-back over the preceding tiles' published aggregates /
-// prefixes; then every thread re-visits its (cache-hot) cells, writes its
-// segment and insertion-sorts it by q -- output sorted by (p, q), no global
-// scan or sort.  Pairs past `cap` are not written; the total is always exact.
-constexpr int kProbeTile = 128;
-constexpr unsigned long long kFlagAgg = 1ull << 62, kFlagPrefix = 2ull << 62, kValMask = (1ull << 62) - 1;
+constexpr int kProbeTile = 128;  // p per probe CTA
 
 constexpr int kKeep = 4;  // hits kept in registers by the counting pass
 
@@ -293,25 +284,48 @@ __device__ void warp_sort_segment(int2* seg, int n, int* buf, int* lock) {
   __syncwarp();
 }
 
+// Probe, per CTA tile of kProbeTile consecutive p (thread per p).  A pair is
+// owned by the cell that holds its reference point (max xlo, max ylo).  Each
+// thread counts its pairs (keeping up to kKeep hits in registers; MBRs over
+// many cells are counted by their whole warp) and the CTA scans the counts.
+// BUCKET pass: the tile writes its (p, q)-sorted pairs into its own bucket of
+// kBucket slots (no cross-CTA dependency) and records its count.  COMPACT pass
+// (after a scan of the tile counts): each tile copies its bucket to its final
+// offset, or -- when the tile overflowed its bucket -- probes again and writes
+// there directly.  Pairs past `cap` are not written; the total is exact.
+constexpr int kBucket = 1024;
+
+template <bool COMPACT>
 __global__ void __launch_bounds__(kProbeTile) probe_kernel(const int4* __restrict__ mp, int64_t np,
                                                            const Grid* __restrict__ gp,
                                                            const int* __restrict__ cell_start,
                                                            const int* __restrict__ items,
                                                            const int4* __restrict__ item_mbr,
-                                                           unsigned long long* __restrict__ tile_state,
-                                                           unsigned* __restrict__ ticket, long long* __restrict__ total,
-                                                           int2* __restrict__ pairs, long long cap) {
-  __shared__ int s_tile;
-  __shared__ long long s_warp[kProbeTile / 32];
-  __shared__ long long s_base;
+                                                           int* __restrict__ tile_cnt,
+                                                           const long long* __restrict__ tile_off,
+                                                           int2* __restrict__ bucket, int2* __restrict__ pairs,
+                                                           long long cap) {
+  __shared__ int s_warp[kProbeTile / 32];
   __shared__ int s_fill[kProbeTile / 32];
   __shared__ int s_sort[kSortBuf];
   __shared__ int s_lock;
-  if (threadIdx.x == 0) s_lock = 0;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (threadIdx.x == 0) s_tile = (int)atomicAdd(ticket, 1u);
-  __syncthreads();
-  const int tile = s_tile;
+  const int tile = blockIdx.x;
+  int2* dst;  // this tile's output: its bucket, or its final place
+  if (COMPACT) {
+    const int cnt = tile_cnt[tile];
+    const long long off = tile_off[tile];
+    if (cnt == 0 || pairs == nullptr || off + cnt > cap) return;
+    if (cnt <= kBucket) {  // copy the bucket
+      const int2* src = bucket + (size_t)tile * kBucket;
+      for (int i = threadIdx.x; i < cnt; i += kProbeTile) pairs[off + i] = src[i];
+      return;
+    }
+    dst = pairs + off;  // overflowed tile: probe again, write in place
+  } else {
+    dst = bucket + (size_t)tile * kBucket;
+  }
+  if (threadIdx.x == 0) s_lock = 0;
   const int64_t p = (int64_t)tile * kProbeTile + threadIdx.x;
   const Grid g = *gp;
   int4 a = make_int4(0, 0, 0, 0);
@@ -329,59 +343,34 @@ __global__ void __launch_bounds__(kProbeTile) probe_kernel(const int4* __restric
     if (lane == j) n = cnt;
   }
   // CTA exclusive scan of the counts
-  long long x = n;
+  int x = n;
   for (int o = 1; o < 32; o <<= 1) {
-    const long long y = __shfl_up_sync(0xffffffffu, x, o);
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
     if (lane >= o) x += y;
   }
   if (lane == 31) s_warp[warp] = x;
   __syncthreads();
-  long long wbase = 0, agg = 0;
+  int wbase = 0, agg = 0;
   for (int w = 0; w < kProbeTile / 32; w++) {
-    const long long v = s_warp[w];
+    const int v = s_warp[w];
     wbase += w < warp ? v : 0;
     agg += v;
   }
-  const long long excl = wbase + x - n;
-  // decoupled look-back (warp 0): publish the aggregate, then scan the
-  // predecessors 32 at a time (lane l reads tile - 1 - l): sum aggregates back
-  // to the nearest published inclusive prefix; retry a window while any tile in
-  // it has published nothing yet; publish our inclusive prefix
-  if (warp == 0) {
-    volatile unsigned long long* st = tile_state;
-    if (lane == 0) st[tile] = (tile == 0 ? (kFlagPrefix | 0ull) : (kFlagAgg | 0ull)) | (unsigned long long)agg;
-    long long prefix = 0;
-    int j0 = tile - 1;
-    while (j0 >= 0) {
-      const int j = j0 - lane;
-      unsigned long long v = j >= 0 ? st[j] : (kFlagPrefix | 0ull);  // before tile 0: prefix 0
-      if (__any_sync(0xffffffffu, (v & (kFlagAgg | kFlagPrefix)) == 0)) continue;  // window not ready
-      const unsigned pm = __ballot_sync(0xffffffffu, (v & kFlagPrefix) != 0);
-      const int stop = pm ? __ffs(pm) - 1 : 32;  // nearest prefix in the window
-      long long add = lane <= stop && j >= 0 ? (long long)(v & kValMask) : 0;
-      for (int o = 16; o; o >>= 1) add += __shfl_xor_sync(0xffffffffu, add, o);
-      prefix += add;
-      if (pm) break;
-      j0 -= 32;
-    }
-    if (lane == 0) {
-      if (tile > 0) st[tile] = kFlagPrefix | (unsigned long long)(prefix + agg);
-      s_base = prefix;
-      if ((int64_t)(tile + 1) * kProbeTile >= np) *total = prefix + agg;  // last tile
-    }
+  const int base = wbase + x - n;
+  if (!COMPACT) {
+    if (threadIdx.x == 0) tile_cnt[tile] = agg;
+    if (agg > kBucket) return;  // rare: the compact pass probes this tile again
   }
-  __syncthreads();
-  const long long base = s_base + excl;
-  const bool fits = pairs && n > 0 && base + n <= cap;
+  const bool fits = n > 0;
   // big MBRs: gathered by the warp, unsorted
   for (unsigned bm = __ballot_sync(0xffffffffu, coop && fits); bm; bm &= bm - 1) {
     const int j = __ffs(bm) - 1;
-    int2* seg = pairs + __shfl_sync(0xffffffffu, base, j);
+    int2* seg = dst + __shfl_sync(0xffffffffu, base, j);
     coop_cells<true>(shfl4(a, j), p - threadIdx.x + (warp * 32 + j), g, cell_start, items, item_mbr, seg,
                      &s_fill[warp]);
   }
   if (fits && !coop) {
-    int2* seg = pairs + base;
+    int2* seg = dst + base;
     if (n <= kKeep) {  // the counting pass kept them: sort in registers, write
       const int big = 0x7fffffff;  // pad the unused slots so a 4-sorting network applies
       int k0 = keep.x, k1 = n > 1 ? keep.y : big, k2 = n > 2 ? keep.z : big, k3 = n > 3 ? keep.w : big;
@@ -416,18 +405,19 @@ __global__ void __launch_bounds__(kProbeTile) probe_kernel(const int4* __restric
     }
   }
   // long segments (big MBRs, or many hits): sorted by the warp
-  __syncwarp();
+  __syncthreads();  // s_lock initialised; every segment written
   for (unsigned bm = __ballot_sync(0xffffffffu, fits && (coop || n > kThreadSortMax)); bm; bm &= bm - 1) {
     const int j = __ffs(bm) - 1;
-    warp_sort_segment(pairs + __shfl_sync(0xffffffffu, base, j), __shfl_sync(0xffffffffu, n, j), s_sort, &s_lock);
+    warp_sort_segment(dst + __shfl_sync(0xffffffffu, base, j), __shfl_sync(0xffffffffu, n, j), s_sort, &s_lock);
   }
 }
 
 // --------------------------------------------------------------------- host
 static size_t cub_scan_bytes(int64_t n) {
-  size_t b32 = 0;
+  size_t b32 = 0, b64 = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, b32, (const int*)nullptr, (int*)nullptr, (int)n);
-  return b32;
+  cub::DeviceScan::ExclusiveSum(nullptr, b64, (const int*)nullptr, (long long*)nullptr, (int)n);
+  return b32 > b64 ? b32 : b64;
 }
 
 static int64_t probe_tiles(int64_t np) { return (np + kProbeTile - 1) / kProbeTile; }
@@ -436,7 +426,9 @@ struct FilterWs {
   Grid* grid;
   int *cell_count, *cell_start, *items;
   int4* item_mbr;
-  unsigned long long* tile_state;  // [T] tile states, then the ticket and the total (zeroed together)
+  int* tile_cnt;        // [T + 1] pairs per probe tile (the last slot 0)
+  long long* tile_off;  // [T + 1] exclusive scan; tile_off[T] = total
+  int2* bucket;         // [T][kBucket] per-tile pair buckets
   long long* total;
   void* tmp;
   size_t tmp_bytes;
@@ -449,9 +441,12 @@ static size_t filter_layout(int64_t np, int64_t nq, Carve& cv, FilterWs& w) {
   w.cell_start = cv.take<int>(C + 1);
   w.items = cv.take<int>(E);
   w.item_mbr = cv.take<int4>(E);
-  w.tile_state = cv.take<unsigned long long>(probe_tiles(np) + 2);
-  w.total = reinterpret_cast<long long*>(w.tile_state + probe_tiles(np) + 1);
-  w.tmp_bytes = cub_scan_bytes(C + 1);
+  const int64_t T = probe_tiles(np);
+  w.tile_cnt = cv.take<int>(T + 1);
+  w.tile_off = cv.take<long long>(T + 1);
+  w.total = w.tile_off + T;
+  w.bucket = cv.take<int2>(T * kBucket);
+  w.tmp_bytes = cub_scan_bytes((C + 1) > (T + 1) ? (C + 1) : (T + 1));
   w.tmp = cv.take<char>(w.tmp_bytes);
   return cv.used;
 }
@@ -475,8 +470,9 @@ static int blocks_for(int64_t n, int threads) {
   return (int)(b < 1 ? 1 : b);
 }
 
-// Enqueue the whole join: grid, buckets, one-pass probe (pairs written when
-// they fit in `cap`; the exact total always lands in w.total).
+// Enqueue the whole join: grid, Q buckets, probe into per-tile buckets, scan
+// of the tile counts, compaction (pairs written when they fit in `cap`; the
+// exact total always lands in w.total).
 static int filter_enqueue(const sccg_polyset* P, const sccg_polyset* Q, FilterWs& w, int32_t* pairs, int64_t cap,
                           cudaStream_t stream) {
   const int64_t np = P->n_polygons, nq = Q->n_polygons;
@@ -494,12 +490,16 @@ static int filter_enqueue(const sccg_polyset* P, const sccg_polyset* Q, FilterWs
   if (nq > 0)
     grid_bucket_kernel<true><<<blocks_for(nq, 256), 256, 0, stream>>>(mq, nq, w.grid, w.cell_start, w.cell_count,
                                                                         w.items, w.item_mbr);
-  // 2. probe (tile states, ticket and total zeroed: one memset, contiguous)
-  cudaMemsetAsync(w.tile_state, 0, sizeof(unsigned long long) * (T + 2), stream);
+  // 2. probe into tile buckets, scan the tile counts, compact
+  cudaMemsetAsync(w.tile_cnt + T, 0, sizeof(int), stream);
   if (np > 0)
-    probe_kernel<<<(unsigned)T, kProbeTile, 0, stream>>>(mp, np, w.grid, w.cell_start, w.items, w.item_mbr,
-                                                          w.tile_state, reinterpret_cast<unsigned*>(w.tile_state + T),
-                                                          w.total, reinterpret_cast<int2*>(pairs), pairs ? cap : 0);
+    probe_kernel<false><<<(unsigned)T, kProbeTile, 0, stream>>>(mp, np, w.grid, w.cell_start, w.items, w.item_mbr,
+                                                                 w.tile_cnt, nullptr, w.bucket, nullptr, 0);
+  cub::DeviceScan::ExclusiveSum(w.tmp, w.tmp_bytes, w.tile_cnt, w.tile_off, (int)(T + 1), stream);
+  if (np > 0 && pairs)
+    probe_kernel<true><<<(unsigned)T, kProbeTile, 0, stream>>>(mp, np, w.grid, w.cell_start, w.items, w.item_mbr,
+                                                                w.tile_cnt, w.tile_off, w.bucket,
+                                                                reinterpret_cast<int2*>(pairs), cap);
   return check_cuda(cudaGetLastError(), "filter enqueue");
 }
 
