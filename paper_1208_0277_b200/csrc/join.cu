@@ -289,10 +289,12 @@ __device__ void warp_sort_segment(int2* seg, int n, int* buf, int* lock) {
 // thread counts its pairs (keeping up to kKeep hits in registers; MBRs over
 // many cells are counted by their whole warp) and the CTA scans the counts.
 // BUCKET pass: the tile writes its (p, q)-sorted pairs into its own bucket of
-// kBucket slots (no cross-CTA dependency) and records its count.  COMPACT pass
-// (after a scan of the tile counts): each tile copies its bucket to its final
-// offset, or -- when the tile overflowed its bucket -- probes again and writes
-// there directly.  Pairs past `cap` are not written; the total is exact.
+// kBucket slots (no cross-CTA dependency) and records its count.  COMPACT pass:
+// each tile sums the preceding tiles' counts (all known by then; a few
+// vectorized L2 loads per thread) for its offset, copies its bucket there, or
+// -- when the tile overflowed its bucket -- probes again and writes there
+// directly; the last tile writes the total (and the async result word).  Pairs
+// past `cap` are not written; the total is exact.
 constexpr int kBucket = 1024;
 
 template <bool COMPACT>
@@ -302,10 +304,13 @@ __global__ void __launch_bounds__(kProbeTile) probe_kernel(const int4* __restric
                                                            const int* __restrict__ items,
                                                            const int4* __restrict__ item_mbr,
                                                            int* __restrict__ tile_cnt,
-                                                           const long long* __restrict__ tile_off,
                                                            int2* __restrict__ bucket, int2* __restrict__ pairs,
-                                                           long long cap) {
+                                                           long long cap, long long* __restrict__ total,
+                                                           long long* __restrict__ result,
+                                                           const uint32_t* __restrict__ status_p,
+                                                           const uint32_t* __restrict__ status_q) {
   __shared__ int s_warp[kProbeTile / 32];
+  __shared__ long long s_sum[kProbeTile / 32];
   __shared__ int s_fill[kProbeTile / 32];
   __shared__ int s_sort[kSortBuf];
   __shared__ int s_lock;
@@ -313,8 +318,26 @@ __global__ void __launch_bounds__(kProbeTile) probe_kernel(const int4* __restric
   const int tile = blockIdx.x;
   int2* dst;  // this tile's output: its bucket, or its final place
   if (COMPACT) {
+    long long sum = 0;  // this tile's offset: the preceding tiles' counts
+    const int4* c4 = reinterpret_cast<const int4*>(tile_cnt);
+    for (int i = threadIdx.x; i < (tile >> 2); i += kProbeTile) {
+      const int4 v = c4[i];
+      sum += (long long)v.x + v.y + v.z + v.w;
+    }
+    for (int i = (tile & ~3) + threadIdx.x; i < tile; i += kProbeTile) sum += tile_cnt[i];
+    for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    if (lane == 0) s_sum[warp] = sum;
+    __syncthreads();
+    long long off = 0;
+    for (int w = 0; w < kProbeTile / 32; w++) off += s_sum[w];
     const int cnt = tile_cnt[tile];
-    const long long off = tile_off[tile];
+    if (tile == (int)gridDim.x - 1 && threadIdx.x == 0) {
+      *total = off + cnt;
+      if (result) {
+        result[0] = off + cnt;
+        result[1] = (long long)(status_p[0] | status_q[0]);
+      }
+    }
     if (cnt == 0 || pairs == nullptr || off + cnt > cap) return;
     if (cnt <= kBucket) {  // copy the bucket
       const int2* src = bucket + (size_t)tile * kBucket;
@@ -414,10 +437,9 @@ __global__ void __launch_bounds__(kProbeTile) probe_kernel(const int4* __restric
 
 // --------------------------------------------------------------------- host
 static size_t cub_scan_bytes(int64_t n) {
-  size_t b32 = 0, b64 = 0;
+  size_t b32 = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, b32, (const int*)nullptr, (int*)nullptr, (int)n);
-  cub::DeviceScan::ExclusiveSum(nullptr, b64, (const int*)nullptr, (long long*)nullptr, (int)n);
-  return b32 > b64 ? b32 : b64;
+  return b32;
 }
 
 static int64_t probe_tiles(int64_t np) { return (np + kProbeTile - 1) / kProbeTile; }
@@ -426,9 +448,8 @@ struct FilterWs {
   Grid* grid;
   int *cell_count, *cell_start, *items;
   int4* item_mbr;
-  int* tile_cnt;        // [T + 1] pairs per probe tile (the last slot 0)
-  long long* tile_off;  // [T + 1] exclusive scan; tile_off[T] = total
-  int2* bucket;         // [T][kBucket] per-tile pair buckets
+  int* tile_cnt;   // [T] pairs per probe tile
+  int2* bucket;    // [T][kBucket] per-tile pair buckets
   long long* total;
   void* tmp;
   size_t tmp_bytes;
@@ -442,11 +463,10 @@ static size_t filter_layout(int64_t np, int64_t nq, Carve& cv, FilterWs& w) {
   w.items = cv.take<int>(E);
   w.item_mbr = cv.take<int4>(E);
   const int64_t T = probe_tiles(np);
-  w.tile_cnt = cv.take<int>(T + 1);
-  w.tile_off = cv.take<long long>(T + 1);
-  w.total = w.tile_off + T;
+  w.tile_cnt = cv.take<int>(T + 4);
+  w.total = cv.take<long long>(1);
   w.bucket = cv.take<int2>(T * kBucket);
-  w.tmp_bytes = cub_scan_bytes((C + 1) > (T + 1) ? (C + 1) : (T + 1));
+  w.tmp_bytes = cub_scan_bytes(C + 1);
   w.tmp = cv.take<char>(w.tmp_bytes);
   return cv.used;
 }
@@ -470,11 +490,19 @@ static int blocks_for(int64_t n, int threads) {
   return (int)(b < 1 ? 1 : b);
 }
 
+__global__ void filter_result_kernel(const long long* __restrict__ total, const uint32_t* __restrict__ sp,
+                                     const uint32_t* __restrict__ sq, long long* result) {
+  if (threadIdx.x == 0) {
+    result[0] = *total;
+    result[1] = (long long)(sp[0] | sq[0]);
+  }
+}
+
 // Enqueue the whole join: grid, Q buckets, probe into per-tile buckets, scan
 // of the tile counts, compaction (pairs written when they fit in `cap`; the
 // exact total always lands in w.total).
 static int filter_enqueue(const sccg_polyset* P, const sccg_polyset* Q, FilterWs& w, int32_t* pairs, int64_t cap,
-                          cudaStream_t stream) {
+                          long long* result, cudaStream_t stream) {
   const int64_t np = P->n_polygons, nq = Q->n_polygons;
   const int4* mp = reinterpret_cast<const int4*>(P->mbr);
   const int4* mq = reinterpret_cast<const int4*>(Q->mbr);
@@ -490,16 +518,19 @@ static int filter_enqueue(const sccg_polyset* P, const sccg_polyset* Q, FilterWs
   if (nq > 0)
     grid_bucket_kernel<true><<<blocks_for(nq, 256), 256, 0, stream>>>(mq, nq, w.grid, w.cell_start, w.cell_count,
                                                                         w.items, w.item_mbr);
-  // 2. probe into tile buckets, scan the tile counts, compact
-  cudaMemsetAsync(w.tile_cnt + T, 0, sizeof(int), stream);
-  if (np > 0)
+  // 2. probe into tile buckets; compaction (offsets, copies, total)
+  if (np > 0) {
     probe_kernel<false><<<(unsigned)T, kProbeTile, 0, stream>>>(mp, np, w.grid, w.cell_start, w.items, w.item_mbr,
-                                                                 w.tile_cnt, nullptr, w.bucket, nullptr, 0);
-  cub::DeviceScan::ExclusiveSum(w.tmp, w.tmp_bytes, w.tile_cnt, w.tile_off, (int)(T + 1), stream);
-  if (np > 0 && pairs)
+                                                                 w.tile_cnt, w.bucket, nullptr, 0, nullptr, nullptr,
+                                                                 nullptr, nullptr);
     probe_kernel<true><<<(unsigned)T, kProbeTile, 0, stream>>>(mp, np, w.grid, w.cell_start, w.items, w.item_mbr,
-                                                                w.tile_cnt, w.tile_off, w.bucket,
-                                                                reinterpret_cast<int2*>(pairs), cap);
+                                                                w.tile_cnt, w.bucket, reinterpret_cast<int2*>(pairs),
+                                                                pairs ? cap : 0, w.total, result, P->status,
+                                                                Q->status);
+  } else {
+    cudaMemsetAsync(w.total, 0, sizeof(long long), stream);
+    if (result) filter_result_kernel<<<1, 32, 0, stream>>>(w.total, P->status, Q->status, result);
+  }
   return check_cuda(cudaGetLastError(), "filter enqueue");
 }
 
@@ -510,7 +541,7 @@ int filter_pairs(const sccg_polyset* P, const sccg_polyset* Q, int32_t* pairs, i
   FilterWs w;
   filter_layout(np, nq, cv, w);
   if (!cv.ok) return set_error(SCCG_E_WORKSPACE, "filter workspace too small (see sccg_filter_workspace_bytes)");
-  if (int r = filter_enqueue(P, Q, w, pairs, cap, stream)) return r;
+  if (int r = filter_enqueue(P, Q, w, pairs, cap, nullptr, stream)) return r;
   // the one host synchronisation: pair count and both sets' prep status
   long long total = 0;
   uint32_t sp[2] = {0, 0}, sq[2] = {0, 0};
@@ -535,14 +566,6 @@ int filter_pairs(const sccg_polyset* P, const sccg_polyset* Q, int32_t* pairs, i
   return SCCG_OK;
 }
 
-__global__ void filter_result_kernel(const long long* __restrict__ total, const uint32_t* __restrict__ sp,
-                                     const uint32_t* __restrict__ sq, long long* result) {
-  if (threadIdx.x == 0) {
-    result[0] = *total;
-    result[1] = (long long)(sp[0] | sq[0]);
-  }
-}
-
 int filter_pairs_async(const sccg_polyset* P, const sccg_polyset* Q, int32_t* pairs, int64_t cap,
                        int64_t* result_dev, void* ws, size_t ws_bytes, cudaStream_t stream) {
   const int64_t np = P->n_polygons, nq = Q->n_polygons;
@@ -550,8 +573,7 @@ int filter_pairs_async(const sccg_polyset* P, const sccg_polyset* Q, int32_t* pa
   FilterWs w;
   filter_layout(np, nq, cv, w);
   if (!cv.ok) return set_error(SCCG_E_WORKSPACE, "filter workspace too small (see sccg_filter_workspace_bytes)");
-  if (int r = filter_enqueue(P, Q, w, pairs, cap, stream)) return r;
-  filter_result_kernel<<<1, 32, 0, stream>>>(w.total, P->status, Q->status, reinterpret_cast<long long*>(result_dev));
+  if (int r = filter_enqueue(P, Q, w, pairs, cap, reinterpret_cast<long long*>(result_dev), stream)) return r;
   return check_cuda(cudaGetLastError(), "filter async");
 }
 
