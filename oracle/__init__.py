@@ -20,6 +20,8 @@ DESIGN.md):
   pairs with I != 0 (a multiset over pairs, reading R9), by ``math.fsum`` of
   the IEEE-rounded ratios and, for checks, exactly with ``fractions``.
 * ``sums`` -- the integer totals the C-ABI reports in ``sccg_sums``.
+* ``touches`` -- ST_Touches (reading R21) on the pixel model: no common
+  pixel and some pixel of each polygon sharing at least a corner.
 
 Pins (tests/test_oracle.py) tie each of these to something other than itself:
 generator masks, the shoelace closed form, rectangles / combs / the SPEC
@@ -86,6 +88,10 @@ def _load():
             lib.oracle_join_nested.restype = i64
             lib.oracle_join_sweep.argtypes = [vp, i64, vp, i64, vp, i64]
             lib.oracle_join_sweep.restype = i64
+            lib.oracle_join_nested_closed.argtypes = [vp, i64, vp, i64, vp, i64]
+            lib.oracle_join_nested_closed.restype = i64
+            lib.oracle_touches.argtypes = [vp, i64, vp, i64]
+            lib.oracle_touches.restype = cint
             _lib = lib
     return _lib
 
@@ -172,8 +178,11 @@ def join(pset, qset, method: str = "sweep") -> np.ndarray:
 
 
 def join_mbrs(mp: np.ndarray, mq: np.ndarray, method: str = "sweep") -> np.ndarray:
+    """method: "sweep" / "nested" (half-open boxes, R4) or "closed" (touching
+    boxes pair too; nested loop -- the ST_Touches candidates)."""
     lib = _load()
-    fn = lib.oracle_join_sweep if method == "sweep" else lib.oracle_join_nested
+    fn = {"sweep": lib.oracle_join_sweep, "nested": lib.oracle_join_nested,
+          "closed": lib.oracle_join_nested_closed}[method]
     mp = np.ascontiguousarray(mp, np.int32)
     mq = np.ascontiguousarray(mq, np.int32)
     n = fn(mp.ctypes.data, len(mp), mq.ctypes.data, len(mq), None, 0)
@@ -181,6 +190,22 @@ def join_mbrs(mp: np.ndarray, mq: np.ndarray, method: str = "sweep") -> np.ndarr
     n2 = fn(mp.ctypes.data, len(mp), mq.ctypes.data, len(mq), out.ctypes.data, n)
     assert n2 == n
     return out[:n]
+
+
+def touches(ring_p, ring_q) -> bool:
+    """ST_Touches (reading R21): no common pixel, and some pixel of p
+    and some pixel of q share at least a corner (closed squares meet)."""
+    a, b = _ring(ring_p), _ring(ring_q)
+    return bool(_load().oracle_touches(a.ctypes.data, len(a), b.ctypes.data, len(b)))
+
+
+def touches_pairs(pset, qset, pairs) -> np.ndarray:
+    """uint8 [n]: touches(p, q) for each pair of a batch."""
+    pairs = np.asarray(pairs, np.int64).reshape(-1, 2)
+    out = np.zeros(len(pairs), np.uint8)
+    for k, (p, q) in enumerate(pairs):
+        out[k] = touches(pset.ring(int(p)), qset.ring(int(q)))
+    return out
 
 
 # ---------------------------------------------------------------- Eq. (1)

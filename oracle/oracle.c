@@ -23,7 +23,13 @@
  *     identity |p u q| = |p| + |q| - |p n q| is a test, not an input.
  *   - MBR join: every (p, q) whose half-open MBRs overlap (the `&&` predicate of
  *     Fig. 1(b); half-open reading R4), by nested loop and by a
- *     textbook x-sorted plane sweep; output sorted by (p, q).
+ *     textbook x-sorted plane sweep; output sorted by (p, q).  The closed-box
+ *     variant (touching MBRs pair too) feeds ST_Touches.
+ *   - ST_Touches (reading R21): the closed polygons meet but their
+ *     interiors do not.  Written out on the pixel model: no pixel lies in both
+ *     (|p n q| = 0) and some pixel of p shares at least a corner with some
+ *     pixel of q (their closed unit squares intersect) -- counted pixel by pixel,
+ *     no edge arithmetic.
  * Parallelism: pairs are split statically across threads; results do not
  * depend on the split.
  */
@@ -297,4 +303,54 @@ int64_t oracle_join_sweep(const int32_t* mbrp, int64_t np, const int32_t* mbrq, 
   free(act[1]);
   free(ev);
   return n;
+}
+
+/* Nested loop over all (p, q) with CLOSED MBRs intersecting (touching boxes
+ * included; the candidates of ST_Touches).  Sorted output, total returned. */
+int64_t oracle_join_nested_closed(const int32_t* mbrp, int64_t np, const int32_t* mbrq, int64_t nq, int32_t* out,
+                                  int64_t cap) {
+  int64_t n = 0;
+  for (int64_t p = 0; p < np; p++)
+    for (int64_t q = 0; q < nq; q++) {
+      const int32_t *a = mbrp + 4 * p, *b = mbrq + 4 * q;
+      if (a[0] <= b[2] && b[0] <= a[2] && a[1] <= b[3] && b[1] <= a[3]) {
+        if (n < cap) {
+          out[2 * n] = (int32_t)p;
+          out[2 * n + 1] = (int32_t)q;
+        }
+        n++;
+      }
+    }
+  return n;
+}
+
+/* ST_Touches on the pixel model (reading R21): 1 iff no pixel is inside both
+ * polygons and some pixel inside p and some pixel inside q are equal-or-
+ * 8-adjacent (their closed unit squares meet).  Scans the bounding box of both
+ * MBRs grown by one pixel; pixel classification by the PNPOLY ray test. */
+int oracle_touches(const int32_t* xp, int64_t np, const int32_t* xq, int64_t nq) {
+  int32_t a[4], b[4];
+  oracle_mbr(xp, np, a);
+  oracle_mbr(xq, nq, b);
+  const int32_t x0 = (a[0] < b[0] ? a[0] : b[0]) - 1, y0 = (a[1] < b[1] ? a[1] : b[1]) - 1;
+  const int32_t x1 = (a[2] > b[2] ? a[2] : b[2]) + 1, y1 = (a[3] > b[3] ? a[3] : b[3]) + 1;
+  const int32_t w = x1 - x0, h = y1 - y0;
+  uint8_t* mp = (uint8_t*)calloc((size_t)w * h, 1);
+  uint8_t* mq = (uint8_t*)calloc((size_t)w * h, 1);
+  oracle_mask(xp, np, x0, y0, w, h, mp, 0);
+  oracle_mask(xq, nq, x0, y0, w, h, mq, 0);
+  int both = 0, near = 0;
+  for (int32_t j = 0; j < h; j++)
+    for (int32_t i = 0; i < w; i++) {
+      if (!mp[(int64_t)j * w + i]) continue;
+      if (mq[(int64_t)j * w + i]) both = 1;
+      for (int dj = -1; dj <= 1; dj++)
+        for (int di = -1; di <= 1; di++) {
+          const int32_t jj = j + dj, ii = i + di;
+          if (jj >= 0 && jj < h && ii >= 0 && ii < w && mq[(int64_t)jj * w + ii]) near = 1;
+        }
+    }
+  free(mp);
+  free(mq);
+  return !both && near;
 }

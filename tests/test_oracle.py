@@ -187,6 +187,68 @@ def test_exhaustive_3x3_pairs():
     assert (uni == np.asarray(exp_u)).all()
 
 
+def test_touches_rectangles_closed_form():
+    """ST_Touches (R21) of two rectangles: their closed boxes meet and
+    their open boxes do not -- interval arithmetic, no pixels."""
+    rng = np.random.default_rng(41)
+    for _ in range(400):
+        ax, ay, bx, by = (int(v) for v in rng.integers(0, 12, 4))
+        aw, ah, bw, bh = (int(v) for v in rng.integers(1, 6, 4))
+        A, B = _rect(ax, ay, ax + aw, ay + ah), _rect(bx, by, bx + bw, by + bh)
+        closed = ax <= bx + bw and bx <= ax + aw and ay <= by + bh and by <= ay + ah
+        opened = ax < bx + bw and bx < ax + aw and ay < by + bh and by < ay + ah
+        assert oracle.touches(A, B) == (closed and not opened), (A, B)
+        assert oracle.touches(B, A) == oracle.touches(A, B)
+    # the P:277 literal rule calls identical / contained-with-shared-edge rings
+    # touching; they overlap, so they do not touch (R21)
+    assert not oracle.touches(_rect(0, 0, 2, 2), _rect(0, 0, 2, 2))
+    assert not oracle.touches(_rect(0, 0, 2, 2), _rect(0, 0, 2, 1))
+
+
+def test_touches_exhaustive_polyominoes_and_symmetry():
+    """Pairs of clean 3x3 polyominoes at offsets in [-3, 3]^2: touches iff the
+    cell sets are disjoint and the 8-neighbourhood of one meets the other
+    (bitboards); invariant under the 8 grid symmetries."""
+    polys = _clean_polyominoes(3)[::2]
+    B = 11
+
+    def board(m, dx, dy):
+        v = 0
+        for (y, x) in zip(*np.nonzero(m)):
+            v |= 1 << ((int(y) + 4 + dy) * B + (int(x) + 4 + dx))
+        return v
+
+    def dilate(v):
+        out = 0
+        for y in range(B):
+            for x in range(B):
+                if v >> (y * B + x) & 1:
+                    for dy in (-1, 0, 1):
+                        for dx in (-1, 0, 1):
+                            if 0 <= y + dy < B and 0 <= x + dx < B:
+                                out |= 1 << ((y + dy) * B + (x + dx))
+        return out
+
+    offs = list(itertools.product(range(-3, 4), repeat=2))
+    for mp, rp in polys:
+        bp = board(mp, 0, 0)
+        dp = dilate(bp)
+        for mq, rq in polys[::3]:
+            for dx, dy in offs:
+                bq = board(mq, dx, dy)
+                want = (bp & bq) == 0 and (dp & bq) != 0
+                got = oracle.touches(rp, rq + np.array([dx, dy], np.int32))
+                assert got == want, (rp.tolist(), rq.tolist(), dx, dy)
+    rng = np.random.default_rng(43)
+    for _ in range(60):
+        (mp, rp), (mq, rq) = polys[int(rng.integers(len(polys)))], polys[int(rng.integers(len(polys)))]
+        rq = rq + np.array([int(v) for v in rng.integers(-3, 4, 2)], np.int32)
+        t = oracle.touches(rp, rq)
+        for sx, sy, sw in itertools.product((1, -1), (1, -1), (False, True)):
+            f = lambda r: (r[:, ::-1] if sw else r) * np.array([sx, sy], np.int32)
+            assert oracle.touches(f(rp), f(rq)) == t
+
+
 def test_exhaustive_4x4_single():
     polys = _clean_polyominoes(4)
     assert len(polys) > 5000
