@@ -119,12 +119,20 @@ SCCG_API size_t sccg_filter_workspace_bytes(int64_t n_p, int64_t n_q);
 /* MBR-overlap join of two prepared sets by a grid hash on
  * the device.  Writes the candidate pairs, unique and sorted by (p, q), as
  * pairs[k] = {p, q} (int32 [cap][2]) and sets *n_pairs_host (host) to their
- * count.  If cap < count (or pairs == NULL) nothing is written to pairs and
- * SCCG_E_CAPACITY is returned with *n_pairs_host = required count.
- * Synchronises `stream` (twice: grid sizing and the count).  Also returns the
- * first data error recorded by sccg_prep in either set's status word. */
+ * count.  If cap < count (or pairs == NULL) SCCG_E_CAPACITY is returned with
+ * *n_pairs_host = required count (the contents of pairs are then unspecified:
+ * retry with a larger buffer).  Synchronises `stream` once (the count).  Also
+ * returns the first data error recorded by sccg_prep in either set's status
+ * word. */
 SCCG_API int sccg_filter_pairs(const sccg_polyset* p, const sccg_polyset* q, int32_t* pairs, int64_t cap,
                       int64_t* n_pairs_host, void* workspace, size_t ws_bytes, sccg_stream_t stream);
+
+/* As sccg_filter_pairs with CLOSED boxes: (p, q) pair when their MBRs share at
+ * least a boundary point (touching MBRs included) -- the candidates of
+ * sccg_touches.  Same workspace, errors and ordering. */
+SCCG_API int sccg_filter_pairs_closed(const sccg_polyset* p, const sccg_polyset* q, int32_t* pairs, int64_t cap,
+                                      int64_t* n_pairs_host, void* workspace, size_t ws_bytes,
+                                      sccg_stream_t stream);
 
 /* Asynchronous variant for device-resident pipelines (CUDA-graph capturable,
  * no host synchronisation): writes the candidate pairs when they fit in cap
@@ -201,6 +209,19 @@ SCCG_API int sccg_pixelbox_async(const sccg_polyset* p, const sccg_polyset* q, c
  * hit_q).  Writes the count (n - set bits) to *missing_dev (device int64);
  * asynchronous. */
 SCCG_API int sccg_count_missing(const uint32_t* hit, int64_t n, int64_t* missing_dev, sccg_stream_t stream);
+
+/* ST_Touches (§3.4, reading R21 in DESIGN.md): touches[k] = 1
+ * iff polygons p = pairs[k].x and q = pairs[k].y meet but their interiors do
+ * not, i.e. inter[k] == 0 (the |p n q| sccg_pixelbox computed for the same
+ * pairs; no common pixel) and some vertex of one ring lies on a (closed) edge
+ * of the other -- the P:277 vertex-on-edge test; with no common pixel the
+ * boundaries can only meet that way.  Candidates come from
+ * sccg_filter_pairs_closed.  pairs: device int32 [n][2]; inter: device
+ * int64 [n]; touches: device uint8 [n] (written).  Rings must be rectilinear
+ * (sccg_prep validate).  Asynchronous; SCCG_E_ARG for null / negative /
+ * misaligned arguments. */
+SCCG_API int sccg_touches(const sccg_polyset* p, const sccg_polyset* q, const int32_t* pairs, int64_t n_pairs,
+                          const int64_t* inter, uint8_t* touches, sccg_stream_t stream);
 
 /* ---------------------------------------------------------------- jaccard */
 /* J' of Eq. (1) from host-resident sums: the mean of r(p, q) over the

@@ -37,7 +37,7 @@ CNT_PIXELS, CNT_ROWTESTS, CNT_BOXES, CNT_BOXEDGES, CNT_SPLITS, CNT_PIXBOXES, CNT
 SUMS_FIELDS = ("n_pairs", "n_nonzero", "sum_inter", "sum_union", "sum_area_p", "sum_area_q", "limb0", "limb1",
                "limb2", "limb3", "status")
 SYMBOLS = ("sccg_polyset_bytes", "sccg_polyset_bind", "sccg_prep", "sccg_prep_sets", "sccg_filter_workspace_bytes",
-           "sccg_filter_pairs", "sccg_filter_pairs_async", "sccg_pixelbox_workspace_bytes", "sccg_pixelbox",
+           "sccg_filter_pairs", "sccg_filter_pairs_closed", "sccg_filter_pairs_async", "sccg_touches", "sccg_pixelbox_workspace_bytes", "sccg_pixelbox",
            "sccg_pixelbox_async", "sccg_count_missing", "sccg_jaccard", "sccg_strerror", "sccg_last_error_string", "sccg_last_error_index",
            "sccg_version")
 
@@ -123,6 +123,10 @@ def load(build: bool = True):
         lib.sccg_filter_workspace_bytes.argtypes = [i64, i64]
         lib.sccg_filter_workspace_bytes.restype = sz
         lib.sccg_filter_pairs.argtypes = [ps, ps, vp, i64, ctypes.POINTER(i64), vp, sz, vp]
+        lib.sccg_filter_pairs_closed.argtypes = [ps, ps, vp, i64, ctypes.POINTER(i64), vp, sz, vp]
+        lib.sccg_filter_pairs_closed.restype = cint
+        lib.sccg_touches.argtypes = [ps, ps, vp, i64, vp, vp, vp]
+        lib.sccg_touches.restype = cint
         lib.sccg_filter_pairs.restype = cint
         lib.sccg_filter_pairs_async.argtypes = [ps, ps, vp, i64, vp, vp, sz, vp]
         lib.sccg_filter_pairs_async.restype = cint
@@ -253,10 +257,12 @@ class DeviceSet:
         return words
 
 
-def filter_pairs(P: DeviceSet, Q: DeviceSet, cap: int | None = None, stream=None):
-    """Candidate pairs (overlapping half-open MBRs), int32 [N, 2] sorted by (p, q)."""
+def filter_pairs(P: DeviceSet, Q: DeviceSet, cap: int | None = None, stream=None, closed: bool = False):
+    """Candidate pairs (overlapping half-open MBRs; closed=True: closed MBRs
+    that meet, touching included), int32 [N, 2] sorted by (p, q)."""
     torch = _torch()
     lib = load()
+    fn = lib.sccg_filter_pairs_closed if closed else lib.sccg_filter_pairs
     wsb = int(lib.sccg_filter_workspace_bytes(P.n, Q.n))
     ws = torch.empty(wsb, dtype=torch.uint8, device=P.xy.device)
     if cap is None:
@@ -264,8 +270,8 @@ def filter_pairs(P: DeviceSet, Q: DeviceSet, cap: int | None = None, stream=None
     for _ in range(2):
         out = torch.empty((max(cap, 1), 2), dtype=torch.int32, device=P.xy.device)
         n = ctypes.c_int64(0)
-        code = lib.sccg_filter_pairs(ctypes.byref(P.c), ctypes.byref(Q.c), out.data_ptr(), cap, ctypes.byref(n),
-                                     ws.data_ptr(), wsb, _stream_ptr(stream))
+        code = fn(ctypes.byref(P.c), ctypes.byref(Q.c), out.data_ptr(), cap, ctypes.byref(n), ws.data_ptr(), wsb,
+                  _stream_ptr(stream))
         if code == E_CAPACITY:
             cap = int(n.value)
             continue
@@ -360,6 +366,20 @@ class Pipeline:
         if status:
             raise SccgError(E_ARG, f"Pipeline: prep status bits {status:#x}")
         return n
+
+
+def touches(P: DeviceSet, Q: DeviceSet, pairs, inter, stream=None):
+    """ST_Touches (reading R21) per pair: uint8 [N], 1 iff |p n q| == 0
+    (inter: the pairs' intersections from pixelbox) and the boundaries meet.
+    Use pairs from filter_pairs(..., closed=True)."""
+    torch = _torch()
+    _require_cuda(pairs, "pairs", torch.int32)
+    _require_cuda(inter, "inter", torch.int64)
+    n = int(pairs.shape[0])
+    out = torch.empty(n, dtype=torch.uint8, device=pairs.device)
+    _check(load().sccg_touches(ctypes.byref(P.c), ctypes.byref(Q.c), pairs.data_ptr(), n, inter.data_ptr(),
+                               out.data_ptr(), _stream_ptr(stream)), "sccg_touches")
+    return out
 
 
 def new_sums(device=None):

@@ -27,7 +27,9 @@ int check_cuda(cudaError_t e, const char* where) {
 
 size_t filter_ws_bytes(int64_t np, int64_t nq);
 int filter_pairs(const sccg_polyset* P, const sccg_polyset* Q, int32_t* pairs, int64_t cap, int64_t* n_pairs_host,
-                 void* ws, size_t ws_bytes, cudaStream_t stream);
+                 void* ws, size_t ws_bytes, int closed, cudaStream_t stream);
+int run_touches(const sccg_polyset* P, const sccg_polyset* Q, const int32_t* pairs, int64_t n, const int64_t* inter,
+                uint8_t* out, cudaStream_t stream);
 size_t pixelbox_ws_bytes(int64_t n);
 int count_missing(const uint32_t* hit, int64_t n, int64_t* out, cudaStream_t st);
 int filter_pairs_async(const sccg_polyset* P, const sccg_polyset* Q, int32_t* pairs, int64_t cap,
@@ -153,8 +155,8 @@ size_t sccg_filter_workspace_bytes(int64_t n_p, int64_t n_q) {
   return filter_ws_bytes(n_p, n_q);
 }
 
-int sccg_filter_pairs(const sccg_polyset* p, const sccg_polyset* q, int32_t* pairs, int64_t cap,
-                      int64_t* n_pairs_host, void* workspace, size_t ws_bytes, sccg_stream_t stream) {
+static int filter_checked(const sccg_polyset* p, const sccg_polyset* q, int32_t* pairs, int64_t cap,
+                          int64_t* n_pairs_host, void* workspace, size_t ws_bytes, int closed, sccg_stream_t stream) {
   set_error(SCCG_OK, "", -1);
   if (int r = check_set(p, true, "p")) return r;
   if (int r = check_set(q, true, "q")) return r;
@@ -164,7 +166,31 @@ int sccg_filter_pairs(const sccg_polyset* p, const sccg_polyset* q, int32_t* pai
   if (!workspace || !aligned(workspace, 256))
     return set_error(SCCG_E_WORKSPACE, "workspace must be non-null and 256-byte aligned");
   *n_pairs_host = 0;
-  return filter_pairs(p, q, pairs, cap, n_pairs_host, workspace, ws_bytes, reinterpret_cast<cudaStream_t>(stream));
+  return filter_pairs(p, q, pairs, cap, n_pairs_host, workspace, ws_bytes, closed,
+                      reinterpret_cast<cudaStream_t>(stream));
+}
+
+int sccg_filter_pairs(const sccg_polyset* p, const sccg_polyset* q, int32_t* pairs, int64_t cap,
+                      int64_t* n_pairs_host, void* workspace, size_t ws_bytes, sccg_stream_t stream) {
+  return filter_checked(p, q, pairs, cap, n_pairs_host, workspace, ws_bytes, 0, stream);
+}
+
+int sccg_filter_pairs_closed(const sccg_polyset* p, const sccg_polyset* q, int32_t* pairs, int64_t cap,
+                             int64_t* n_pairs_host, void* workspace, size_t ws_bytes, sccg_stream_t stream) {
+  return filter_checked(p, q, pairs, cap, n_pairs_host, workspace, ws_bytes, 1, stream);
+}
+
+int sccg_touches(const sccg_polyset* p, const sccg_polyset* q, const int32_t* pairs, int64_t n_pairs,
+                 const int64_t* inter, uint8_t* touches, sccg_stream_t stream) {
+  set_error(SCCG_OK, "", -1);
+  if (int r = check_set(p, true, "p")) return r;
+  if (int r = check_set(q, true, "q")) return r;
+  if (n_pairs < 0) return set_error(SCCG_E_ARG, "negative pair count");
+  if (n_pairs == 0) return SCCG_OK;
+  if (!pairs || !aligned(pairs, 8)) return set_error(SCCG_E_ARG, "pairs must be a non-null 8-byte aligned device array");
+  if (!inter || !aligned(inter, 8)) return set_error(SCCG_E_ARG, "inter must be a non-null aligned device int64 array");
+  if (!touches) return set_error(SCCG_E_ARG, "touches is null");
+  return run_touches(p, q, pairs, n_pairs, inter, touches, reinterpret_cast<cudaStream_t>(stream));
 }
 
 int sccg_filter_pairs_async(const sccg_polyset* p, const sccg_polyset* q, int32_t* pairs, int64_t cap,

@@ -31,11 +31,13 @@ static int64_t cell_cap(int64_t np, int64_t nq) { return np + nq + 1024; }
 static int64_t entry_cap(int64_t nq) { return 8 * nq + 1024; }
 
 // Upper bound and expectation of the 2^k-cell entries of one set (SetStats).
-__device__ __forceinline__ void set_entries(const SetStats* s, int k, double& bound, double& expect) {
+// `grow` = 1: the boxes are grown by one pixel on the high side (closed join).
+__device__ __forceinline__ void set_entries(const SetStats* s, int k, int grow, double& bound, double& expect) {
   const double c = 1.0 / (double)(1ll << k), n = (double)s->nonempty;
-  const double sw = (double)s->sw, sh = (double)s->sh, swh = (double)s->swh;
+  const double sw = (double)s->sw + grow * n, sh = (double)s->sh + grow * n;
+  const double swh = (double)s->swh + grow * ((double)s->sw + (double)s->sh + n);
   const double cont = swh * c * c + 2.0 * (sw + sh) * c + 4.0 * n;
-  const double ext = n * (double)(((s->maxext[0] - 1) >> k) + 2) * (double)(((s->maxext[1] - 1) >> k) + 2);
+  const double ext = n * (double)(((s->maxext[0] - 1 + grow) >> k) + 2) * (double)(((s->maxext[1] - 1 + grow) >> k) + 2);
   bound = cont < ext ? cont : ext;
   expect = n + (sw + sh) * c + swh * c * c;
 }
@@ -45,13 +47,13 @@ __device__ __forceinline__ void set_entries(const SetStats* s, int k, double& bo
 // caps on cells C and (upper-bounded) Q-entries.  Always feasible: once 2^k
 // exceeds the largest MBR extent each MBR covers at most 2 x 2 cells.
 __global__ void grid_select_kernel(const SetStats* __restrict__ sp, const SetStats* __restrict__ sq, long long ccap,
-                                   long long ecap, Grid* g) {
+                                   long long ecap, int grow, Grid* g) {
   // one warp: lane j evaluates k = 3 + j (k <= 30), then an argmin over lanes
   const int lane = threadIdx.x & 31;
   if (threadIdx.x >= 32) return;
   const bool empty = sp->nonempty == 0 || sq->nonempty == 0;
   const int xmin = min(sp->bounds[0], sq->bounds[0]), ymin = min(sp->bounds[1], sq->bounds[1]);
-  const int xmax = max(sp->bounds[2], sq->bounds[2]), ymax = max(sp->bounds[3], sq->bounds[3]);
+  const int xmax = max(sp->bounds[2], sq->bounds[2]) + grow, ymax = max(sp->bounds[3], sq->bounds[3]) + grow;
   const int k = 3 + lane;
   double cost = 1e300;
   if (!empty && k <= 30) {
@@ -59,8 +61,8 @@ __global__ void grid_select_kernel(const SetStats* __restrict__ sp, const SetSta
     const double ncy = (double)(((ymax - 1) >> k) - (ymin >> k) + 1);
     const double C = ncx * ncy;
     double bp, ep, bq, eq;
-    set_entries(sp, k, bp, ep);
-    set_entries(sq, k, bq, eq);
+    set_entries(sp, k, grow, bp, ep);
+    set_entries(sq, k, grow, bq, eq);
     if (C <= (double)ccap && bq <= (double)ecap) cost = ep + eq + 0.25 * C + ep * eq / C;
   }
   // argmin (ties -> smaller k); k = 30 is always feasible
@@ -104,7 +106,7 @@ __device__ __forceinline__ int mbr_cells(const int4& m, int k) {
 template <bool FILL>
 __global__ void grid_bucket_kernel(const int4* __restrict__ mq, int64_t nq, const Grid* __restrict__ gp,
                                    const int* __restrict__ cell_start, int* __restrict__ cell_count,
-                                   int* __restrict__ items, int4* __restrict__ item_mbr) {
+                                   int* __restrict__ items, int4* __restrict__ item_mbr, int grow) {
   const Grid g = *gp;
   if (g.empty) return;
   const int lane = threadIdx.x & 31;
@@ -126,6 +128,8 @@ __global__ void grid_bucket_kernel(const int4* __restrict__ mq, int64_t nq, cons
     if (i < nq) {
       m = mq[i];
       ok = !mbr_empty(m);
+      m.z += grow;  // closed join: boxes grown by one pixel on the high side
+      m.w += grow;
     }
     const bool coop = ok && mbr_cells(m, g.k) > kCoopCells;
     if (ok && !coop)
@@ -308,7 +312,7 @@ __global__ void __launch_bounds__(kProbeTile) probe_kernel(const int4* __restric
                                                            long long cap, long long* __restrict__ total,
                                                            long long* __restrict__ result,
                                                            const uint32_t* __restrict__ status_p,
-                                                           const uint32_t* __restrict__ status_q) {
+                                                           const uint32_t* __restrict__ status_q, int grow) {
   __shared__ int s_warp[kProbeTile / 32];
   __shared__ long long s_sum[kProbeTile / 32];
   __shared__ int s_fill[kProbeTile / 32];
@@ -355,6 +359,8 @@ __global__ void __launch_bounds__(kProbeTile) probe_kernel(const int4* __restric
   const bool live = p < np && !g.empty;
   if (live) a = mp[p];
   const bool act = live && !mbr_empty(a);
+  a.z += grow;  // closed join: boxes grown by one pixel on the high side
+  a.w += grow;
   int4 keep = make_int4(0, 0, 0, 0);
   const bool coop = act && mbr_cells(a, g.k) > kCoopCells;  // big MBR: its warp probes it together
   int n = act && !coop ? probe_cells<false>(a, p, g, cell_start, items, item_mbr, nullptr, keep) : 0;
@@ -502,31 +508,32 @@ __global__ void filter_result_kernel(const long long* __restrict__ total, const 
 // of the tile counts, compaction (pairs written when they fit in `cap`; the
 // exact total always lands in w.total).
 static int filter_enqueue(const sccg_polyset* P, const sccg_polyset* Q, FilterWs& w, int32_t* pairs, int64_t cap,
-                          long long* result, cudaStream_t stream) {
+                          long long* result, int grow, cudaStream_t stream) {
   const int64_t np = P->n_polygons, nq = Q->n_polygons;
   const int4* mp = reinterpret_cast<const int4*>(P->mbr);
   const int4* mq = reinterpret_cast<const int4*>(Q->mbr);
   const int64_t C = cell_cap(np, nq), T = probe_tiles(np);
   // 1. grid size from the prep statistics (device side), bucket Q
   grid_select_kernel<<<1, 32, 0, stream>>>(reinterpret_cast<const SetStats*>(P->stats),
-                                           reinterpret_cast<const SetStats*>(Q->stats), C, entry_cap(nq), w.grid);
+                                           reinterpret_cast<const SetStats*>(Q->stats), C, entry_cap(nq), grow,
+                                           w.grid);
   cudaMemsetAsync(w.cell_count, 0, sizeof(int) * (C + 1), stream);
   if (nq > 0)
     grid_bucket_kernel<false><<<blocks_for(nq, 256), 256, 0, stream>>>(mq, nq, w.grid, nullptr, w.cell_count,
-                                                                        nullptr, nullptr);
+                                                                        nullptr, nullptr, grow);
   cub::DeviceScan::ExclusiveSum(w.tmp, w.tmp_bytes, w.cell_count, w.cell_start, (int)(C + 1), stream);
   if (nq > 0)
     grid_bucket_kernel<true><<<blocks_for(nq, 256), 256, 0, stream>>>(mq, nq, w.grid, w.cell_start, w.cell_count,
-                                                                        w.items, w.item_mbr);
+                                                                        w.items, w.item_mbr, grow);
   // 2. probe into tile buckets; compaction (offsets, copies, total)
   if (np > 0) {
     probe_kernel<false><<<(unsigned)T, kProbeTile, 0, stream>>>(mp, np, w.grid, w.cell_start, w.items, w.item_mbr,
                                                                  w.tile_cnt, w.bucket, nullptr, 0, nullptr, nullptr,
-                                                                 nullptr, nullptr);
+                                                                 nullptr, nullptr, grow);
     probe_kernel<true><<<(unsigned)T, kProbeTile, 0, stream>>>(mp, np, w.grid, w.cell_start, w.items, w.item_mbr,
                                                                 w.tile_cnt, w.bucket, reinterpret_cast<int2*>(pairs),
                                                                 pairs ? cap : 0, w.total, result, P->status,
-                                                                Q->status);
+                                                                Q->status, grow);
   } else {
     cudaMemsetAsync(w.total, 0, sizeof(long long), stream);
     if (result) filter_result_kernel<<<1, 32, 0, stream>>>(w.total, P->status, Q->status, result);
@@ -535,13 +542,13 @@ static int filter_enqueue(const sccg_polyset* P, const sccg_polyset* Q, FilterWs
 }
 
 int filter_pairs(const sccg_polyset* P, const sccg_polyset* Q, int32_t* pairs, int64_t cap, int64_t* n_pairs_host,
-                 void* ws, size_t ws_bytes, cudaStream_t stream) {
+                 void* ws, size_t ws_bytes, int closed, cudaStream_t stream) {
   const int64_t np = P->n_polygons, nq = Q->n_polygons;
   Carve cv{reinterpret_cast<char*>(ws), ws_bytes};
   FilterWs w;
   filter_layout(np, nq, cv, w);
   if (!cv.ok) return set_error(SCCG_E_WORKSPACE, "filter workspace too small (see sccg_filter_workspace_bytes)");
-  if (int r = filter_enqueue(P, Q, w, pairs, cap, nullptr, stream)) return r;
+  if (int r = filter_enqueue(P, Q, w, pairs, cap, nullptr, closed ? 1 : 0, stream)) return r;
   // the one host synchronisation: pair count and both sets' prep status
   long long total = 0;
   uint32_t sp[2] = {0, 0}, sq[2] = {0, 0};
@@ -573,7 +580,7 @@ int filter_pairs_async(const sccg_polyset* P, const sccg_polyset* Q, int32_t* pa
   FilterWs w;
   filter_layout(np, nq, cv, w);
   if (!cv.ok) return set_error(SCCG_E_WORKSPACE, "filter workspace too small (see sccg_filter_workspace_bytes)");
-  if (int r = filter_enqueue(P, Q, w, pairs, cap, reinterpret_cast<long long*>(result_dev), stream)) return r;
+  if (int r = filter_enqueue(P, Q, w, pairs, cap, reinterpret_cast<long long*>(result_dev), 0, stream)) return r;
   return check_cuda(cudaGetLastError(), "filter async");
 }
 

@@ -218,3 +218,39 @@ def pack(rings) -> PolygonSet:
     np.cumsum([len(r) for r in rings], out=off[1:])
     xy = np.concatenate([np.asarray(r, np.int32).reshape(-1, 2) for r in rings]) if rings else np.zeros((0, 2), np.int32)
     return PolygonSet(np.ascontiguousarray(xy, np.int32), off)
+
+
+def partition(seed: int, n: int = 96, k: int = 60, ox: int = 0, oy: int = 0) -> "PolygonSet":
+    """A seeded partition of the n x n square into rectilinear pieces (region
+    growing from k seeds in random order), keeping the pieces that trace to one
+    clean ring.  Neighbouring pieces share sides, T-junctions and corners: the
+    ST_Touches workload.  Input generation only."""
+    rng = np.random.default_rng(seed)
+    lab = -np.ones((n, n), np.int32)
+    front = []
+    for i, (y, x) in enumerate(rng.integers(0, n, (k, 2))):
+        if lab[y, x] < 0:
+            lab[y, x] = i
+            front.append((int(y), int(x)))
+    while front:
+        j = int(rng.integers(len(front)))
+        y, x = front[j]
+        front[j] = front[-1]
+        front.pop()
+        for dy, dx in ((0, 1), (1, 0), (0, -1), (-1, 0)):
+            yy, xx = y + dy, x + dx
+            if 0 <= yy < n and 0 <= xx < n and lab[yy, xx] < 0:
+                lab[yy, xx] = lab[y, x]
+                front.append((yy, xx))
+    rings = []
+    for i in range(k):
+        m = (lab == i).astype(np.uint8)
+        if not m.any():
+            continue
+        ys, xs = np.nonzero(m)
+        y0, x0 = int(ys.min()), int(xs.min())
+        sub = m[y0:ys.max() + 1, x0:xs.max() + 1]
+        ring, cleaned = trace_mask(sub)
+        if ring is not None and (cleaned == sub).all():
+            rings.append(ring + np.array([x0 + ox, y0 + oy], np.int32))
+    return pack(rings)

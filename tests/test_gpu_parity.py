@@ -180,6 +180,86 @@ def test_filter_long_segments(sccg):
     assert counts[0] > 4096 and 32 < counts[1] <= 4096 and 4 < counts[2] <= 32, counts
 
 
+def test_filter_closed_matches_oracle(sccg, tile_sets):
+    """Closed-box join (touching MBRs pair too): the ST_Touches candidates."""
+    A, B = tile_sets
+    got = sccg.filter_pairs(dev(A, sccg), dev(B, sccg), closed=True).cpu().numpy()
+    _, mp = oracle.set_props(A)
+    _, mq = oracle.set_props(B)
+    assert got.tolist() == oracle.join_mbrs(mp, mq, "closed").tolist()
+    rng = np.random.default_rng(13)
+    for trial in range(10):
+        sets = []
+        for n in rng.integers(1, 200, 2):
+            rs = []
+            for _ in range(n):
+                x, y = (int(v) for v in rng.integers(0, 60, 2))
+                w, h = (int(v) for v in rng.integers(1, 8, 2))
+                rs.append([[x, y], [x + w, y], [x + w, y + h], [x, y + h]])
+            sets.append(synth.pack(rs))
+        S, T = sets
+        got = sccg.filter_pairs(dev(S, sccg), dev(T, sccg), closed=True).cpu().numpy()
+        want = oracle.join_mbrs(oracle.set_props(S)[1], oracle.set_props(T)[1], "closed")
+        assert got.tolist() == want.tolist()
+
+
+def _touch_sets():
+    """Hand-made contact cases (one pair each, far apart) and the expected
+    answers: shared side, partial side, corner, gap, overlap, identical,
+    contained with a shared side, L-shape notch contact, containing."""
+    sq = lambda x, y, w, h: [[x, y], [x + w, y], [x + w, y + h], [x, y + h]]
+    L = lambda x, y: [[x, y], [x + 4, y], [x + 4, y + 2], [x + 2, y + 2], [x + 2, y + 4], [x, y + 4]]
+    cases = [
+        (sq(0, 0, 2, 2), sq(2, 0, 2, 2), True),
+        (sq(0, 0, 4, 4), sq(4, 1, 2, 2), True),
+        (sq(0, 0, 2, 2), sq(2, 2, 2, 2), True),
+        (sq(0, 0, 2, 2), sq(3, 0, 2, 2), False),
+        (sq(0, 0, 3, 3), sq(2, 2, 3, 3), False),
+        (sq(0, 0, 2, 2), sq(0, 0, 2, 2), False),
+        (sq(0, 0, 4, 4), sq(0, 0, 2, 4), False),
+        (L(0, 0), sq(2, 2, 2, 2), True),
+        (L(0, 0), sq(3, 3, 1, 1), False),
+        (sq(0, 0, 6, 6), sq(2, 2, 2, 2), False),
+    ]
+    P, Q, want = [], [], []
+    for i, (a, b, t) in enumerate(cases):
+        off = np.array([20 * i, 0], np.int32)
+        P.append(np.asarray(a, np.int32) + off)
+        Q.append(np.asarray(b, np.int32) + off)
+        want.append(t)
+    return synth.pack(P), synth.pack(Q), want
+
+
+def test_touches_matches_oracle(sccg, tile_sets):
+    """ST_Touches (R21) through the C ABI: closed-join candidates,
+    PixelBox intersections, then the vertex-on-edge test -- against the
+    oracle's pixel-adjacency definition, on hand-made cases, on the tile
+    sets and on rectilinear blobs packed edge to edge."""
+    A, B, want = _touch_sets()
+    P, Q = dev(A, sccg), dev(B, sccg)
+    pairs = sccg.filter_pairs(P, Q, closed=True)
+    pl = pairs.cpu().numpy()
+    assert pl.tolist() == oracle.join(A, B, "closed").tolist()  # the gap case's MBRs do not even meet
+    inter, _, _ = sccg.pixelbox(P, Q, pairs)
+    t = dict(zip(map(tuple, pl.tolist()), sccg.touches(P, Q, pairs, inter).cpu().numpy().astype(bool).tolist()))
+    assert [t.get((k, k), False) for k in range(len(want))] == want
+    assert [oracle.touches(A.ring(k), B.ring(k)) for k in range(len(want))] == want
+    # tile sets (nuclei hardly ever touch), partitions of a square against
+    # themselves (neighbouring pieces touch along sides / at corners) and
+    # against another partition of the same square (mostly overlapping)
+    parts = [synth.partition(s) for s in (3, 4, 5)]
+    total = 0
+    for S, T in (tile_sets, (parts[0], parts[0]), (parts[1], parts[1]), (parts[1], parts[2])):
+        P, Q = dev(S, sccg), dev(T, sccg)
+        pairs = sccg.filter_pairs(P, Q, closed=True)
+        inter, _, _ = sccg.pixelbox(P, Q, pairs)
+        got = sccg.touches(P, Q, pairs, inter).cpu().numpy()
+        exp = oracle.touches_pairs(S, T, pairs.cpu().numpy())
+        assert (got == exp).all(), np.nonzero(got != exp)[0][:10]
+        total += int(exp.sum())
+    assert total > 300
+
+
 def test_filter_capacity_retry(sccg, tile_sets):
     A, B = tile_sets
     got = sccg.filter_pairs(dev(A, sccg), dev(B, sccg), cap=3).cpu().numpy()
