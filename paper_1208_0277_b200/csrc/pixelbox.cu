@@ -202,12 +202,13 @@ __global__ void __launch_bounds__(kSmallWarps * 32, SCCG_SMALL_MINB)
     // ---- small pairs, software-pipelined: records of the next pair are in
     // flight into registers while the current pair is pixelized
     unsigned myI = 0;
-    // ---- raster pairs, batched: the chunk's (pair, row) items are spread over
-    // the lanes, so each lane has many independent row loads in flight; a row
-    // costs two loads, two shifts, an AND and a popcount (memoized pixelization)
+    // ---- raster pairs, batched: the chunk's (pair, two rows) items are spread
+    // over the lanes, so each lane has many independent row loads in flight; a
+    // row costs two loads, two shifts, an AND and a popcount (memoized
+    // pixelization)
     const unsigned rmask = __ballot_sync(FULL, rast != 0u);
     if (rmask) {
-      const int hl = rast ? H : 0;
+      const int hl = rast ? (H + 1) >> 1 : 0;  // items: row pairs
       int sc = hl;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
@@ -227,7 +228,7 @@ __global__ void __launch_bounds__(kSmallWarps * 32, SCCG_SMALL_MINB)
         s_rp[warp][lane] = reinterpret_cast<const unsigned*>(Ps.edges + e.x + ((mj >> 14) & 255)) - (mm.y >> 16);
         s_rq[warp][lane] = reinterpret_cast<const unsigned*>(Qs.edges + e.y + ((mj >> 22) & 255)) - (mm.z >> 16);
         s_rsh[warp][lane] = (unsigned)(-(int)(short)(mm.y & 0xffff)) | ((unsigned)(-(int)(short)(mm.z & 0xffff)) << 8) |
-                            ((unsigned)W << 16);
+                            ((unsigned)W << 16) | ((unsigned)H << 24);
       }
       // item -> pair map, written cooperatively pair by pair
       for (unsigned m = rmask; m; m &= m - 1) {
@@ -237,11 +238,11 @@ __global__ void __launch_bounds__(kSmallWarps * 32, SCCG_SMALL_MINB)
       }
       __syncwarp();
       const unsigned le = lanemask_lt() | (1u << lane);
-      // four 32-item groups per round: all eight row loads are issued before
-      // any is consumed (many loads in flight per lane)
+      // four 32-item groups per round: all row loads are issued before any is
+      // consumed (many loads in flight per lane)
       constexpr int kU = 4;
       for (int t0 = 0; t0 < R; t0 += 32 * kU) {  // warp-uniform trip count
-        unsigned wpv[kU], wqv[kU], shv[kU];
+        unsigned wpv[kU], wqv[kU], wpw[kU], wqw[kU], shv[kU];
         int jrv[kU];
         bool hv[kU], av[kU];
 #pragma unroll
@@ -250,23 +251,31 @@ __global__ void __launch_bounds__(kSmallWarps * 32, SCCG_SMALL_MINB)
           av[u] = t < R;
           hv[u] = !av[u] || lane == 0;
           jrv[u] = 0;
-          wpv[u] = wqv[u] = shv[u] = 0u;
+          wpv[u] = wqv[u] = wpw[u] = wqw[u] = shv[u] = 0u;
           if (av[u]) {
             const int jr = rmap[t];
-            const int r = t - rstart[jr];
-            hv[u] |= r == 0;
+            const int i = t - rstart[jr], r = 2 * i;
+            hv[u] |= i == 0;
             jrv[u] = jr;
-            shv[u] = s_rsh[warp][jr];
-            wpv[u] = __ldg(s_rp[warp][jr] + r);
-            wqv[u] = __ldg(s_rq[warp][jr] + r);
+            const unsigned sh = s_rsh[warp][jr];
+            shv[u] = sh;
+            const unsigned* rp = s_rp[warp][jr] + r;
+            const unsigned* rq = s_rq[warp][jr] + r;
+            wpv[u] = __ldg(rp);
+            wqv[u] = __ldg(rq);
+            if (r + 1 < (int)(sh >> 24)) {  // an odd box height leaves the last item one row
+              wpw[u] = __ldg(rp + 1);
+              wqw[u] = __ldg(rq + 1);
+            }
           }
         }
 #pragma unroll
         for (int u = 0; u < kU; u++) {
           if (t0 + 32 * u >= R) break;  // warp-uniform
           const unsigned sh = shv[u];
-          unsigned c = av[u] ? (unsigned)__popc((wpv[u] >> (sh & 0xffu)) & (wqv[u] >> ((sh >> 8) & 0xffu)) &
-                                                low_bits((int)(sh >> 16)))
+          const unsigned sp = sh & 0xffu, sq = (sh >> 8) & 0xffu, wm = low_bits((int)((sh >> 16) & 0xffu));
+          unsigned c = av[u] ? (unsigned)(__popc((wpv[u] >> sp) & (wqv[u] >> sq) & wm) +
+                                          __popc((wpw[u] >> sp) & (wqw[u] >> sq) & wm))
                              : 0u;
           // each pair's items occupy consecutive lanes: segmented shuffle sum,
           // the segment's first lane adds it to the pair's count
