@@ -503,6 +503,7 @@ __global__ void prep_init_kernel(PrepArgs args) {
     st->bounds[0] = st->bounds[1] = INT_MAX;
     st->bounds[2] = st->bounds[3] = INT_MIN;
     st->maxext[0] = st->maxext[1] = 0;
+    st->pad[0] = st->pad[1] = 0;
     st->nonempty = st->sw = st->sh = st->swh = 0;
   }
   if (i == 0) *args.ticket = 0;

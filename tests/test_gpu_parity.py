@@ -95,7 +95,8 @@ def test_prep_sets_one_launch_equals_separate(sccg):
     for a, b in zip(one, many):
         for f in ("mbr", "area", "ecount", "status"):
             assert torch.equal(getattr(a, f), getattr(b, f)), f
-        assert torch.equal(a.stats_bytes()[:48], b.stats_bytes()[:48])  # bounds, extents, moments
+        sa, sb = a.stats_bytes(), b.stats_bytes()
+        assert torch.equal(sa[:24], sb[:24]) and torch.equal(sa[32:64], sb[32:64])  # bounds, extents, moments
         assert torch.equal(a.used_edge_words(), b.used_edge_words())  # records + raster rows
     shared = (sccg.PolySet * 2)(many[0].c, many[0].c)
     assert sccg.load().sccg_prep_sets(shared, 2, 1, None) == sccg.E_ARG
