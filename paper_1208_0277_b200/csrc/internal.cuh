@@ -16,6 +16,9 @@ namespace sccg {
 // (the rest of the polygon's slot is unspecified).  Horizontal edges are not
 // stored: only sampling-box classification needs them, and it reads them from
 // the ring itself.
+// bit 48 of a vertical record: the ring traverses the edge upward (lo -> hi);
+// decoders mask the three 16-bit fields and ignore it.
+constexpr uint64_t kEdgeUp = 1ull << 48;
 __host__ __device__ inline uint64_t pack_edge(uint32_t c, uint32_t lo, uint32_t hi) {
   return (uint64_t)c | ((uint64_t)lo << 16) | ((uint64_t)hi << 32);
 }

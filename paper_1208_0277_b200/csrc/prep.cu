@@ -171,7 +171,7 @@ __device__ __forceinline__ int4 prep_polygon_thread(int2* v, int V, int rot, int
     const bool is_v = ax == cx && ay != cy;
     nhor += (ay == cy && ax != cx) ? 1 : 0;
     diag |= ax != cx && ay != cy;
-    const uint64_t rec = pack_edge(ax, min(ay, cy), max(ay, cy));
+    const uint64_t rec = pack_edge(ax, min(ay, cy), max(ay, cy)) | (cy > ay ? kEdgeUp : 0ull);
     if (is_v) out[nvert] = rec;
     nvert += is_v ? 1 : 0;
     ax = cx;
@@ -199,25 +199,34 @@ __device__ __forceinline__ int4 prep_polygon_thread(int2* v, int V, int rot, int
   // iff an odd number of the row's vertical edges lie at or left of x (R19) --
   // PIXELINPOLY depends on the polygon alone, so it is computed once here.
   // Row r as a 32-bit word (bit x = column xlo + x): difference trick -- each
-  // vertical edge XORs its suffix mask into rows lo and hi -- then a prefix XOR
-  // over rows.  Stored in the slot's free tail (words 2 nv .. 2 nv + H), which
+  // vertical edge XORs its suffix mask into rows lo and hi (paired per row
+  // below) -- then a prefix XOR over rows.  Stored in the slot's free tail (words 2 nv .. 2 nv + H), which
   // exists when 2 (V - nv) >= H; MBR width <= 32.
   const int W = xmax - xmin, H = ymax - ymin;
-  bool raster = !diag && W <= 32 && 2 * (V - nvert) >= H;
+#ifndef SCCG_PREP_RASTER
+#define SCCG_PREP_RASTER 1
+#endif
+  bool raster = SCCG_PREP_RASTER && !diag && W <= 32 && 2 * (V - nvert) >= H;
   if (raster) {
-    // The row updates are return-free shared atomics (no load -> store chain
-    // per update) fed by records read four at a time; the prefix pass reads
-    // four rows ahead of its stores (distinct rows, so reordering is safe).
+    // In ring order a record's exit row (its upper end when traversed upward,
+    // kEdgeUp) is the next record's entry row -- y only changes along vertical
+    // edges -- so every endpoint row gets both of its suffix masks in ONE
+    // update: D[exit_k] ^= mask_k ^ mask_{k+1} (cyclically).  Updates are
+    // return-free shared atomics (no load -> store chain), records read four
+    // at a time; the prefix pass reads four rows ahead of its stores.
     unsigned* D = reinterpret_cast<unsigned*>(out + nvert);
     for (int r = 0; r < H; r++) D[r] = 0u;
-    auto apply = [&](uint64_t rec) {
-      int c, lo, hi;
-      unpack_edge(rec, c, lo, hi);
-      const unsigned m = suffix_mask(c);
-      atomicXor(&D[lo], m);
-      if (hi < H) atomicXor(&D[hi], m);
+    const uint64_t first = out[0];
+    uint64_t cur = first;
+    auto apply = [&](uint64_t nxt) {
+      int c, lo, hi, cn, lon, hin;
+      unpack_edge(cur, c, lo, hi);
+      unpack_edge(nxt, cn, lon, hin);
+      const int y = (cur & kEdgeUp) ? hi : lo;
+      if (y < H) atomicXor(&D[y], suffix_mask(c) ^ suffix_mask(cn));
+      cur = nxt;
     };
-    int k = 0;
+    int k = 1;
     for (; k + 4 <= nvert; k += 4) {
       const uint64_t r0 = out[k], r1 = out[k + 1], r2 = out[k + 2], r3 = out[k + 3];
       apply(r0);
@@ -226,6 +235,7 @@ __device__ __forceinline__ int4 prep_polygon_thread(int2* v, int V, int rot, int
       apply(r3);
     }
     for (; k < nvert; k++) apply(out[k]);
+    apply(first);  // the last record's exit is the first record's entry
     unsigned acc = 0u;
     const unsigned wmask = low_bits(W);
     int r = 0;
