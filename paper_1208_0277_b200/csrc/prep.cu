@@ -374,34 +374,54 @@ __global__ void __launch_bounds__(kPrepThreads) prep_kernel(const __grid_constan
   acc.init();
   const int validate = args.validate;
   const int64_t ntiles = args.tile_end[args.nsets - 1];
+  // Tile gt's polygon range (set, first polygon, count) and the offsets this
+  // thread stages for it (offsets[p0 + t], thread 0 also offsets[p0 + np]):
+  // fetched one tile ahead, so their round trips overlap the current tile.
+  auto tile_range = [&](int64_t g, int& si, int64_t& p0, int& np) {
+    si = 0;
+    while (g >= args.tile_end[si]) si++;
+    p0 = (g - (si ? args.tile_end[si - 1] : 0)) * kPrepPolys;
+    np = (int)min((int64_t)kPrepPolys, args.set[si].n - p0);
+  };
+  int64_t off_a = 0, off_b = 0;
+  auto fetch_offsets = [&](int64_t g) {
+    if (g >= ntiles) return;
+    int si2, np2;
+    int64_t p02;
+    tile_range(g, si2, p02, np2);
+    const int64_t* o = args.set[si2].off;
+    if ((int)threadIdx.x <= np2) off_a = o[p02 + threadIdx.x];
+    if (threadIdx.x == 0) off_b = o[p02 + np2];
+  };
+  if (threadIdx.x == 0) s_tile = (long long)atomicAdd(args.ticket, 1ull);
+  __syncthreads();
+  int64_t gt = s_tile;
+  fetch_offsets(gt);
   int cur = -1;  // set of the statistics in acc
   for (;;) {
-    __syncthreads();  // previous tile's shared data fully consumed
-    if (threadIdx.x == 0) s_tile = (long long)atomicAdd(args.ticket, 1ull);
-    __syncthreads();
-    const int64_t gt = s_tile;
     if (gt >= ntiles) break;
-    int si = 0;
-    while (gt >= args.tile_end[si]) si++;
+    int si;
+    int64_t p0;
+    int np;
+    tile_range(gt, si, p0, np);
     if (si != cur) {
       if (cur >= 0) flush_stats(acc, args.set[cur].stats, s_acc, s_b);
       cur = si;
     }
     const PrepSet& S = args.set[si];
     const int2* __restrict__ xy = S.xy;
-    const int64_t* __restrict__ off = S.off;
-    const int64_t n = S.n, nv_total = S.nv_total;
+    const int64_t nv_total = S.nv_total;
     int4* __restrict__ mbr = S.mbr;
     int64_t* __restrict__ area = S.area;
     int2* __restrict__ ecount = S.ecount;
     uint64_t* __restrict__ edges = S.edges;
     uint32_t* __restrict__ status = S.status;
     const int bulk = S.bulk;
-    const int64_t tile = gt - (si ? args.tile_end[si - 1] : 0);
-    const int64_t p0 = tile * kPrepPolys;
-    const int np = (int)min((int64_t)kPrepPolys, n - p0);
     __syncthreads();  // previous tile's shared data fully consumed
-    for (int i = threadIdx.x; i <= np; i += blockDim.x) s_off[i] = off[p0 + i];
+    if ((int)threadIdx.x <= np) s_off[threadIdx.x] = off_a;
+    if (threadIdx.x == 0) s_off[np] = off_b;
+    long long next_gt = 0;
+    if (threadIdx.x == 0) next_gt = (long long)atomicAdd(args.ticket, 1ull);  // the next tile, in flight
     if (threadIdx.x < kPrepPolys / 32) s_big[threadIdx.x] = 0;
     if (threadIdx.x < kSortKeys) s_cnt[threadIdx.x] = 0;
     s_perm[threadIdx.x] = 0xff;
@@ -461,7 +481,10 @@ __global__ void __launch_bounds__(kPrepThreads) prep_kernel(const __grid_constan
         acc.add(prep_polygon_thread(s_xy + (b - v0), (int)V, rot, poly, mbr, area, ecount, status, validate));
       }
     }
+    if (threadIdx.x == 0) s_tile = next_gt;
     __syncthreads();
+    const int64_t gt_next = s_tile;
+    fetch_offsets(gt_next);  // in flight during the rest of this tile
     // warp per large ring (in the tile when tiled, else straight from global)
     for (int w = 0; w < kPrepPolys / 32; w++) {
       unsigned bits = s_big[w];
@@ -498,6 +521,7 @@ __global__ void __launch_bounds__(kPrepThreads) prep_kernel(const __grid_constan
         for (int64_t i = s0 + threadIdx.x; i < v1; i += blockDim.x) edges[i] = rec[i - v0];
       }
     }
+    gt = gt_next;
   }
   if (threadIdx.x == 0) bulk_store_drain();
   if (cur >= 0) flush_stats(acc, args.set[cur].stats, s_acc, s_b);
