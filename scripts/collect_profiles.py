@@ -51,10 +51,14 @@ def launch_summary(path):
     ki, vi = h.index("Kernel Name"), h.index("Metric Value")
     seq = [(r[ki], float(r[vi].replace(",", ""))) for r in data]
     idx = [i for i, s in enumerate(seq) if s[0].startswith("sccg::prep_init")] + [len(seq)]
-    # the last timed Pipeline step: a prep_init .. next prep_init window that
-    # holds the async join's filter_result_kernel (e2e steps use the sync join)
-    wins = [seq[a:b] for a, b in zip(idx, idx[1:]) if any("filter_result" in n for n, _ in seq[a:b])]
-    step = wins[-1] if wins else seq
+    # the last timed Pipeline step: a prep_init .. next prep_init window holding
+    # the join (grid_select) right after another such window -- an e2e step is
+    # a P-only prep window followed by the Q prep + join + PixelBox window
+    wins = [seq[a:b] for a, b in zip(idx, idx[1:])]
+    has_join = [any("grid_select" in n for n, _ in w) for w in wins]
+    full = [wins[i] for i in range(1, len(wins)) if has_join[i] and has_join[i - 1]
+            and not any("small_kernel<1>" in n for n, _ in wins[i])]
+    step = full[-1] if full else seq
     out = ["one bench step (timed Pipeline), ncu --metrics gpu__time_duration.sum --clock-control none",
            "(cold caches, serialised: compare shares, not absolute times)", ""]
     tot = sum(t for _, t in step)
