@@ -94,7 +94,10 @@ __global__ void grid_select_kernel(const SetStats* __restrict__ sp, const SetSta
 // MBRs covering more than kCoopCells cells (a gland among nuclei, C3) are
 // handled by their whole warp, lanes spread over the cells, so one polygon is
 // not a serial critical path of hundreds of dependent cell visits.
-constexpr int kCoopCells = 32;
+#ifndef SCCG_COOP_CELLS
+#define SCCG_COOP_CELLS 32
+#endif
+constexpr int kCoopCells = SCCG_COOP_CELLS;
 
 __device__ __forceinline__ int mbr_cells(const int4& m, int k) {
   return (((m.z - 1) >> k) - (m.x >> k) + 1) * (((m.w - 1) >> k) - (m.y >> k) + 1);
@@ -308,6 +311,7 @@ __global__ void __launch_bounds__(kProbeTile) probe_kernel(const int4* __restric
                                                            const int* __restrict__ items,
                                                            const int4* __restrict__ item_mbr,
                                                            int* __restrict__ tile_cnt,
+                                                           unsigned char* __restrict__ tile_long,
                                                            int2* __restrict__ bucket, int2* __restrict__ pairs,
                                                            long long cap, long long* __restrict__ total,
                                                            long long* __restrict__ result,
@@ -318,6 +322,9 @@ __global__ void __launch_bounds__(kProbeTile) probe_kernel(const int4* __restric
   __shared__ int s_fill[kProbeTile / 32];
   __shared__ int s_sort[kSortBuf];
   __shared__ int s_lock;
+  __shared__ int2 s_pairs[COMPACT ? kBucket : 1];      // compaction: the tile's bucket
+  __shared__ unsigned s_head[COMPACT ? kBucket / 32 : 1];  // ... first pair of each p
+  __shared__ int s_runs[COMPACT ? 2 * kProbeTile + 1 : 1];  // ... long runs (start, length), count
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int tile = blockIdx.x;
   int2* dst;  // this tile's output: its bucket, or its final place
@@ -343,9 +350,65 @@ __global__ void __launch_bounds__(kProbeTile) probe_kernel(const int4* __restric
       }
     }
     if (cnt == 0 || pairs == nullptr || off + cnt > cap) return;
-    if (cnt <= kBucket) {  // copy the bucket
+    if (cnt <= kBucket && !tile_long[tile]) {  // copy the bucket
       const int2* src = bucket + (size_t)tile * kBucket;
       for (int i = threadIdx.x; i < cnt; i += kProbeTile) pairs[off + i] = src[i];
+      return;
+    }
+    if (cnt <= kBucket) {
+      // stage the bucket; runs of one p longer than kThreadSortMax were left
+      // unsorted by the bucket pass -- the whole CTA sorts each by q here
+      const int2* src = bucket + (size_t)tile * kBucket;
+      for (int i = threadIdx.x; i < kBucket / 32; i += kProbeTile) s_head[i] = 0u;
+      if (threadIdx.x == 0) s_runs[2 * kProbeTile] = 0;
+      __syncthreads();
+      for (int i = threadIdx.x; i < cnt; i += kProbeTile) {
+        const int2 v = src[i];
+        s_pairs[i] = v;
+        if (i == 0 || src[i - 1].x != v.x) atomicOr(&s_head[i >> 5], 1u << (i & 31));
+      }
+      __syncthreads();
+      for (int i = threadIdx.x; i < cnt; i += kProbeTile) {
+        if (!((s_head[i >> 5] >> (i & 31)) & 1u)) continue;
+        int e = i + 1;  // next head (or the end)
+        while (e < cnt) {
+          const unsigned w = s_head[e >> 5] >> (e & 31);
+          if (w) {
+            e += __ffs(w) - 1;
+            break;
+          }
+          e = (e | 31) + 1;
+        }
+        if (e > cnt) e = cnt;
+        if (e - i > kThreadSortMax) {
+          const int r = atomicAdd(&s_runs[2 * kProbeTile], 1);
+          s_runs[2 * r] = i;
+          s_runs[2 * r + 1] = e - i;
+        }
+      }
+      __syncthreads();
+      const int nruns = s_runs[2 * kProbeTile];
+      for (int r = 0; r < nruns; r++) {  // CTA-wide ascending-only bitonic network on the run's q
+        int2* run = s_pairs + s_runs[2 * r];
+        const int n = s_runs[2 * r + 1];
+        int m = 1;
+        while (m < n) m <<= 1;
+        for (int k = 2; k <= m; k <<= 1)
+          for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int i = threadIdx.x; i < m; i += kProbeTile) {
+              const int l = j == (k >> 1) ? (i ^ (k - 1)) : (i ^ j);
+              if (l > i && l < n) {
+                const int2 u = run[i], v = run[l];
+                if (v.y < u.y) {
+                  run[i] = v;
+                  run[l] = u;
+                }
+              }
+            }
+            __syncthreads();
+          }
+      }
+      for (int i = threadIdx.x; i < cnt; i += kProbeTile) pairs[off + i] = s_pairs[i];
       return;
     }
     dst = pairs + off;  // overflowed tile: probe again, write in place
@@ -433,7 +496,13 @@ __global__ void __launch_bounds__(kProbeTile) probe_kernel(const int4* __restric
         }
     }
   }
-  // long segments (big MBRs, or many hits): sorted by the warp
+  // long segments (big MBRs, or many hits): sorted by the compaction pass for
+  // a bucket, here by the warp when writing in place (an overflowed tile)
+  if (!COMPACT) {
+    const int any_long = __syncthreads_or(fits && (coop || n > kThreadSortMax));
+    if (threadIdx.x == 0) tile_long[tile] = any_long ? 1 : 0;
+    return;
+  }
   __syncthreads();  // s_lock initialised; every segment written
   for (unsigned bm = __ballot_sync(0xffffffffu, fits && (coop || n > kThreadSortMax)); bm; bm &= bm - 1) {
     const int j = __ffs(bm) - 1;
@@ -455,6 +524,7 @@ struct FilterWs {
   int *cell_count, *cell_start, *items;
   int4* item_mbr;
   int* tile_cnt;   // [T] pairs per probe tile
+  unsigned char* tile_long;  // [T] the tile's bucket holds a segment the compaction sorts
   int2* bucket;    // [T][kBucket] per-tile pair buckets
   long long* total;
   void* tmp;
@@ -470,6 +540,7 @@ static size_t filter_layout(int64_t np, int64_t nq, Carve& cv, FilterWs& w) {
   w.item_mbr = cv.take<int4>(E);
   const int64_t T = probe_tiles(np);
   w.tile_cnt = cv.take<int>(T + 4);
+  w.tile_long = cv.take<unsigned char>(T + 1);
   w.total = cv.take<long long>(1);
   w.bucket = cv.take<int2>(T * kBucket);
   w.tmp_bytes = cub_scan_bytes(C + 1);
@@ -528,10 +599,12 @@ static int filter_enqueue(const sccg_polyset* P, const sccg_polyset* Q, FilterWs
   // 2. probe into tile buckets; compaction (offsets, copies, total)
   if (np > 0) {
     probe_kernel<false><<<(unsigned)T, kProbeTile, 0, stream>>>(mp, np, w.grid, w.cell_start, w.items, w.item_mbr,
-                                                                 w.tile_cnt, w.bucket, nullptr, 0, nullptr, nullptr,
+                                                                 w.tile_cnt, w.tile_long, w.bucket, nullptr, 0, nullptr,
+                                                                 nullptr,
                                                                  nullptr, nullptr, grow);
     probe_kernel<true><<<(unsigned)T, kProbeTile, 0, stream>>>(mp, np, w.grid, w.cell_start, w.items, w.item_mbr,
-                                                                w.tile_cnt, w.bucket, reinterpret_cast<int2*>(pairs),
+                                                                w.tile_cnt, w.tile_long, w.bucket,
+                                                                reinterpret_cast<int2*>(pairs),
                                                                 pairs ? cap : 0, w.total, result, P->status,
                                                                 Q->status, grow);
   } else {

@@ -167,18 +167,19 @@ def test_filter_long_segments(sccg):
     for i in range(9000):  # small boxes on a jittered lattice
         x, y = 3 * (i % 100) + int(rng.integers(0, 2)), 3 * (i // 100) + int(rng.integers(0, 2))
         rings_q.append([[x, y], [x + 2, y], [x + 2, y + 2], [x, y + 2]])
-    rings_p = [
-        [[0, 0], [300, 0], [300, 300], [0, 300]],  # > 4096 pairs
-        [[10, 10], [70, 10], [70, 70], [10, 70]],  # ~400 pairs
-        [[100, 100], [112, 100], [112, 106], [100, 106]],  # ~10-30 pairs
-        [[150, 150], [152, 150], [152, 152], [150, 152]],  # a few
-    ]
+    far = lambda i: [[5000 + 3 * i, 5000], [5001 + 3 * i, 5000], [5001 + 3 * i, 5001], [5000 + 3 * i, 5001]]
+    rings_p = [[[0, 0], [300, 0], [300, 300], [0, 300]]]  # > 4096 pairs: its 128-polygon tile overflows its bucket
+    rings_p += [far(i) for i in range(127)]
+    rings_p += [[[10, 10], [70, 10], [70, 70], [10, 70]],  # ~400 pairs: sorted by the compaction pass
+                [[100, 100], [112, 100], [112, 106], [100, 106]],  # ~10-30 pairs: sorted by its thread
+                [[150, 150], [152, 150], [152, 152], [150, 152]],  # a few: sorted in registers
+                [[20, 200], [80, 200], [80, 240], [20, 240]]]  # ~270 pairs, same tile as the ~400
     A, B = synth.pack(rings_p), synth.pack(rings_q)
     got = sccg.filter_pairs(dev(A, sccg), dev(B, sccg)).cpu().numpy()
     want = oracle.join(A, B)
     assert got.tolist() == want.tolist()
-    counts = np.bincount(want[:, 0], minlength=4)
-    assert counts[0] > 4096 and 32 < counts[1] <= 4096 and 4 < counts[2] <= 32, counts
+    counts = np.bincount(want[:, 0], minlength=132)
+    assert counts[0] > 4096 and 32 < counts[128] <= 1024 and 4 < counts[129] <= 32 and counts[131] > 32, counts
 
 
 def test_filter_closed_matches_oracle(sccg, tile_sets):
