@@ -37,7 +37,8 @@ sys.path.insert(0, ROOT)
 
 METRIC = "polygon pairs/sec (and pixels tested/sec) at 1/2/4/8 B200 vs int-issue peak"
 SMS_B200 = 148
-ISSUE_LANES_PER_CLK_SM = 128  # 4 SMSPs x 1 warp-instruction x 32 lanes (guide: B300_MICROARCH "Per-warp issue")
+ISSUE_LANES_PER_CLK_SM = 128  # 4 SMSPs x 1 warp-instruction x 32 lanes (nominal dispatch)
+ALU_LANES_PER_CLK_SM = 64  # measured: ALU pipe 2 warp-inst/clk/SM (profiles/int_peak.json, scripts/int_peak.cu)
 OPS_PER_ROWTEST = 3  # sub, unsigned compare, predicated xor
 OPS_PER_BOXEDGE = 8  # one lane classifying one edge against all sub-boxes of a split (minimum)
 
@@ -120,6 +121,36 @@ def prep_algorithmic_bytes(sccg, S) -> int:
     rast = (ec[:, 1] & sccg.RASTER_FLAG) != 0
     rows = int(((m[:, 3] - m[:, 1]) * rast).sum())
     return 8 * S.nv + 8 * (S.n + 1) + 32 * S.n + 8 * int(ec[:, 0].sum()) + 4 * rows
+
+
+def pixelbox_issue(config, pix_s, sms, clocks):
+    """PixelBox warp-instruction issue rate against the measured integer-issue
+    peak: ncu's instruction count of the small kernel for this
+    workload (profiles/issue_counts.json; fixed by the workload) over the live
+    PixelBox stage time (CUDA events; includes the item kernel and the graph
+    launch, so the rate is a lower bound).  Peak = the best integer mix of the
+    microbenchmark (profiles/int_peak.json, LOP3 + IMAD on the ALU and FMA
+    pipes) x SMs x the SM clock sampled during the run."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "issue_counts.json")) as f:
+            counts = json.load(f).get(config)
+        with open(os.path.join(ROOT, "profiles", "int_peak.json")) as f:
+            ip = json.load(f)
+    except Exception:
+        return None
+    if not counts or "small_kernel" not in counts:
+        return None
+    best = max(r["warp_inst_per_clk_per_sm"] for r in ip["results"])
+    alu = max(r["warp_inst_per_clk_per_sm"] for r in ip["results"] if r["pipe"] == "alu")
+    mhz = clocks.get("sm_mhz") or clocks.get("sm_max_mhz") or 1965.0
+    achieved = counts["small_kernel"] / pix_s
+    peak = best * sms * mhz * 1e6
+    return {"achieved": achieved, "peak": peak, "unit": "warp-inst/s", "frac": achieved / peak,
+            "frac_of_nominal_issue": achieved / (4 * sms * mhz * 1e6),
+            "warp_inst_per_launch": counts["small_kernel"], "kernel": "small_kernel",
+            "peak_source": f"measured integer mix {best:.3f} warp-inst/clk/SM (ALU pipe alone {alu:.3f}; "
+                           f"profiles/int_peak.json) x {sms} SMs x {mhz:.0f} MHz",
+            "count_source": "ncu smsp__inst_executed.sum (profiles/issue_counts.json) / live stage time"}
 
 
 def hbm_peak():
@@ -310,7 +341,8 @@ def run_ours(args, rank, world, local_rank):
     pix_s = pix_ms_max / 1e3
     peak_mhz = clocks["sm_max_mhz"] or 1965.0
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
-    alu_peak = sms * ISSUE_LANES_PER_CLK_SM * peak_mhz * 1e6 / 1e9
+    alu_peak = sms * ALU_LANES_PER_CLK_SM * peak_mhz * 1e6 / 1e9
+    issue = pixelbox_issue(args.config, pix_s, sms, clocks)
     launches_per_step = 11  # our kernels per step: prep init + prep, join 6 (incl. CUB scan x2), pixelbox 2 (profiles/)
     out = {
         "metric": METRIC,
@@ -348,7 +380,9 @@ def run_ours(args, rank, world, local_rank):
                      "peak_source": peak_src},
         "pixelbox_alu": {"achieved": ops / pix_s / 1e9, "peak": alu_peak, "unit": "Gop/s",
                          "frac": ops / pix_s / 1e9 / alu_peak,
-                         "peak_source": f"{sms} SMs x 128 int lanes/clk x {peak_mhz:.0f} MHz (issue peak)"},
+                         "peak_source": f"{sms} SMs x 64 ALU-pipe lanes/clk (measured, profiles/int_peak.json) x "
+                                        f"{peak_mhz:.0f} MHz"},
+        "pixelbox_issue": issue,
         "e2e": {"value": e2e_value, "unit": "pairs/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                 "steps": e2e_steps},
         "gpu_launches": launches_per_step * args.steps,
