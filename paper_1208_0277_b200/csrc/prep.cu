@@ -18,10 +18,16 @@
 
 namespace sccg {
 
-constexpr int kPrepThreads = 128;
-constexpr int kPrepPolys = 128;   // one ring per thread per tile
-static_assert(kPrepPolys == kPrepThreads, "one ring per thread per tile");
-constexpr int kPrepVerts = 5120;
+#ifndef SCCG_PREP_THREADS
+#define SCCG_PREP_THREADS 128
+#endif
+#ifndef SCCG_PREP_VERTS
+#define SCCG_PREP_VERTS 5120
+#endif
+constexpr int kPrepThreads = SCCG_PREP_THREADS;
+constexpr int kPrepPolys = kPrepThreads;  // one ring per thread per tile
+static_assert(kPrepThreads % 32 == 0 && kPrepThreads <= 256, "whole warps; ring indices fit a byte");
+constexpr int kPrepVerts = SCCG_PREP_VERTS;
 constexpr size_t kPrepSmem = kPrepVerts * sizeof(int2);  // 40 KB of int2 staged per tile (dynamic shared memory)
 
 
@@ -53,6 +59,19 @@ __device__ __forceinline__ void bulk_store(void* dst, const void* src, unsigned 
 }
 __device__ __forceinline__ void bulk_store_drain() { asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory"); }
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+
+// Predicated shared-memory store / return-free XOR reduction (no divergent
+// branch around a conditional access).
+__device__ __forceinline__ void sts64_if(uint64_t* p, uint64_t v, bool c) {
+  asm volatile("{\n .reg .pred q;\n setp.ne.u32 q, %2, 0;\n @q st.shared.u64 [%0], %1;\n}\n" ::"r"(smem_u32(p)), "l"(v),
+               "r"((unsigned)c)
+               : "memory");
+}
+__device__ __forceinline__ void red_xor_if(unsigned* p, unsigned v, bool c) {
+  asm volatile("{\n .reg .pred q;\n setp.ne.u32 q, %2, 0;\n @q red.shared.xor.b32 [%0], %1;\n}\n" ::"r"(smem_u32(p)),
+               "r"(v), "r"((unsigned)c)
+               : "memory");
+}
 
 __device__ __forceinline__ void flag(uint32_t* status, uint32_t bit, int64_t poly) {
   atomicOr(&status[0], bit);
@@ -161,18 +180,26 @@ __device__ __forceinline__ int4 prep_polygon_thread(int2* v, int V, int rot, int
     return m;
   }
   uint64_t* out = reinterpret_cast<uint64_t*>(v);
-  long long twice_area = 0;
+  // Area by Green's theorem on the rectilinear ring, A = |sum over vertical
+  // edges of x_i (y_{i+1} - y_i)| (the shoelace of P:193 with the horizontal
+  // edges' zero terms dropped, footnote P:205), accumulated mod 2^32: exact
+  // whenever A < 2^31, i.e. whenever W * H < 2^31 (else recomputed in int64
+  // from the records below).
+  unsigned area32 = 0u;
   bool diag = false;
   int nvert = 0, nhor = 0;
   const unsigned fx = v[0].x - xmin, fy = v[0].y - ymin;
   unsigned ax = fx, ay = fy;
   auto edge = [&](unsigned cx, unsigned cy) {
-    twice_area += (long long)(ax * cy) - (long long)(cx * ay);  // P:193, one term per vertex
-    const bool is_v = ax == cx && ay != cy;
-    nhor += (ay == cy && ax != cx) ? 1 : 0;
-    diag |= ax != cx && ay != cy;
-    const uint64_t rec = pack_edge(ax, min(ay, cy), max(ay, cy)) | (cy > ay ? kEdgeUp : 0ull);
-    if (is_v) out[nvert] = rec;
+    area32 += ax * (cy - ay);
+    const bool same_x = ax == cx, same_y = ay == cy;
+    const bool is_v = same_x && !same_y;
+    nhor += (same_y && !same_x) ? 1 : 0;
+    diag |= !same_x && !same_y;
+    // record: x | lo << 16 | hi << 32 | exit row << 48 (the row the ring
+    // leaves the edge at, read by the raster pass below; decoders mask it off)
+    const unsigned lo32 = ax | (min(ay, cy) << 16), hi32 = max(ay, cy) | (cy << 16);
+    sts64_if(out + nvert, ((uint64_t)hi32 << 32) | lo32, is_v);  // predicated: no divergent branch
     nvert += is_v ? 1 : 0;
     ax = cx;
     ay = cy;
@@ -194,7 +221,20 @@ __device__ __forceinline__ int4 prep_polygon_thread(int2* v, int V, int rot, int
     edge((unsigned)(c.x - xmin), (unsigned)(c.y - ymin));
   }
   edge(fx, fy);  // closing edge back to the first vertex
-  area[poly] = (twice_area < 0 ? -twice_area : twice_area) / 2;
+  const int W = xmax - xmin, H = ymax - ymin;
+  if ((unsigned long long)W * (unsigned long long)H < (1ull << 31)) {
+    const int a = (int)area32;
+    area[poly] = a < 0 ? -a : a;
+  } else {  // rare (a huge box): the same sum in int64 over the vertical records
+    long long a = 0;
+    for (int k = 0; k < nvert; k++) {
+      const uint64_t r = out[k];
+      const long long x = (long long)(r & 0xffffu), lo = (long long)((r >> 16) & 0xffffu),
+                      hi = (long long)((r >> 32) & 0xffffu);
+      a += ((r >> 48) == (uint64_t)hi) ? x * (hi - lo) : -x * (hi - lo);
+    }
+    area[poly] = a < 0 ? -a : a;
+  }
   // Raster: pixel (x, y) of the MBR is inside
   // iff an odd number of the row's vertical edges lie at or left of x (R19) --
   // PIXELINPOLY depends on the polygon alone, so it is computed once here.
@@ -202,29 +242,27 @@ __device__ __forceinline__ int4 prep_polygon_thread(int2* v, int V, int rot, int
   // vertical edge XORs its suffix mask into rows lo and hi (paired per row
   // below) -- then a prefix XOR over rows.  Stored in the slot's free tail (words 2 nv .. 2 nv + H), which
   // exists when 2 (V - nv) >= H; MBR width <= 32.
-  const int W = xmax - xmin, H = ymax - ymin;
 #ifndef SCCG_PREP_RASTER
 #define SCCG_PREP_RASTER 1
 #endif
   bool raster = SCCG_PREP_RASTER && !diag && W <= 32 && 2 * (V - nvert) >= H;
   if (raster) {
-    // In ring order a record's exit row (its upper end when traversed upward,
-    // kEdgeUp) is the next record's entry row -- y only changes along vertical
-    // edges -- so every endpoint row gets both of its suffix masks in ONE
-    // update: D[exit_k] ^= mask_k ^ mask_{k+1} (cyclically).  Updates are
-    // return-free shared atomics (no load -> store chain), records read four
-    // at a time; the prefix pass reads four rows ahead of its stores.
+    // In ring order a record's exit row is the next record's entry row -- y
+    // only changes along vertical edges -- so every endpoint row gets both of
+    // its suffix masks in ONE update: D[exit_k] ^= mask_k ^ mask_{k+1}
+    // (cyclically).  Updates are predicated return-free shared reductions (no
+    // branch, no load -> store chain), records read four at a time; the prefix
+    // pass reads four rows ahead of its stores.
     unsigned* D = reinterpret_cast<unsigned*>(out + nvert);
     for (int r = 0; r < H; r++) D[r] = 0u;
     const uint64_t first = out[0];
-    uint64_t cur = first;
+    unsigned mc = shl_clamp(0xffffffffu, (unsigned)first & 0xffffu), yc = (unsigned)(first >> 48);
+    const unsigned m0 = mc;
     auto apply = [&](uint64_t nxt) {
-      int c, lo, hi, cn, lon, hin;
-      unpack_edge(cur, c, lo, hi);
-      unpack_edge(nxt, cn, lon, hin);
-      const int y = (cur & kEdgeUp) ? hi : lo;
-      if (y < H) atomicXor(&D[y], suffix_mask(c) ^ suffix_mask(cn));
-      cur = nxt;
+      const unsigned mn = shl_clamp(0xffffffffu, (unsigned)nxt & 0xffffu);
+      red_xor_if(D + yc, mc ^ mn, yc < (unsigned)H);
+      mc = mn;
+      yc = (unsigned)(nxt >> 48);
     };
     int k = 1;
     for (; k + 4 <= nvert; k += 4) {
@@ -235,7 +273,7 @@ __device__ __forceinline__ int4 prep_polygon_thread(int2* v, int V, int rot, int
       apply(r3);
     }
     for (; k < nvert; k++) apply(out[k]);
-    apply(first);  // the last record's exit is the first record's entry
+    red_xor_if(D + yc, mc ^ m0, yc < (unsigned)H);  // the last record's exit is the first record's entry
     unsigned acc = 0u;
     const unsigned wmask = low_bits(W);
     int r = 0;
@@ -457,11 +495,19 @@ __global__ void __launch_bounds__(kPrepThreads) prep_kernel(const __grid_constan
         for (int64_t i = threadIdx.x; i < nv; i += blockDim.x) s_xy[i] = xy[v0 + i];
       }
     }
-    if (threadIdx.x < np) {
-      int rank = pos;
-      for (int k = 0; k < key; k++) rank += s_cnt[k];
-      s_perm[rank] = (unsigned char)threadIdx.x;
+    __syncthreads();  // every ring counted
+    if (threadIdx.x < 32) {  // exclusive scan of the bucket counts (two per lane)
+      const int c0 = s_cnt[2 * threadIdx.x], c1 = s_cnt[2 * threadIdx.x + 1];
+      int incl = c0 + c1;
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, incl, o);
+        if ((int)threadIdx.x >= o) incl += t;
+      }
+      s_cnt[2 * threadIdx.x] = incl - c0 - c1;
+      s_cnt[2 * threadIdx.x + 1] = incl - c1;
     }
+    __syncthreads();
+    if (threadIdx.x < np) s_perm[s_cnt[key] + pos] = (unsigned char)threadIdx.x;
     __syncthreads();
     // thread per small ring (records in place in the tile)
     if (s_perm[threadIdx.x] != 0xff) {
