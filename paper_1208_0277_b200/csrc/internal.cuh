@@ -99,6 +99,31 @@ struct Carve {
   }
 };
 
+// Programmatic dependent launch (PDL): a kernel launched with launch_pdl may
+// be scheduled while its predecessor on the stream drains; it must execute
+// pdl_wait() before touching anything the predecessor writes (the wait
+// returns once the predecessor has completed and its writes are visible).
+// pdl_trigger() lets the successor's CTAs launch early.  Both are no-ops
+// without a programmatic dependency.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                       Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 // error slot (api.cu)
 int set_error(int code, const char* msg, int64_t index = -1);
 int check_cuda(cudaError_t e, const char* where);

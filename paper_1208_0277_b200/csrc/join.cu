@@ -48,6 +48,7 @@ __device__ __forceinline__ void set_entries(const SetStats* s, int k, int grow, 
 // exceeds the largest MBR extent each MBR covers at most 2 x 2 cells.
 __global__ void grid_select_kernel(const SetStats* __restrict__ sp, const SetStats* __restrict__ sq, long long ccap,
                                    long long ecap, int grow, Grid* g) {
+  pdl_trigger();
   // one warp: lane j evaluates k = 3 + j (k <= 30), then an argmin over lanes
   const int lane = threadIdx.x & 31;
   if (threadIdx.x >= 32) return;
@@ -110,6 +111,8 @@ template <bool FILL>
 __global__ void grid_bucket_kernel(const int4* __restrict__ mq, int64_t nq, const Grid* __restrict__ gp,
                                    const int* __restrict__ cell_start, int* __restrict__ cell_count,
                                    int* __restrict__ items, int4* __restrict__ item_mbr, int grow) {
+  pdl_trigger();
+  pdl_wait();
   const Grid g = *gp;
   if (g.empty) return;
   const int lane = threadIdx.x & 31;
@@ -327,6 +330,8 @@ __global__ void __launch_bounds__(kProbeTile) probe_kernel(const int4* __restric
   __shared__ int s_runs[COMPACT ? 2 * kProbeTile + 1 : 1];  // ... long runs (start, length), count
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int tile = blockIdx.x;
+  pdl_trigger();
+  pdl_wait();
   int2* dst;  // this tile's output: its bucket, or its final place
   if (COMPACT) {
     long long sum = 0;  // this tile's offset: the preceding tiles' counts
@@ -594,19 +599,16 @@ static int filter_enqueue(const sccg_polyset* P, const sccg_polyset* Q, FilterWs
                                                                         nullptr, nullptr, grow);
   cub::DeviceScan::ExclusiveSum(w.tmp, w.tmp_bytes, w.cell_count, w.cell_start, (int)(C + 1), stream);
   if (nq > 0)
-    grid_bucket_kernel<true><<<blocks_for(nq, 256), 256, 0, stream>>>(mq, nq, w.grid, w.cell_start, w.cell_count,
-                                                                        w.items, w.item_mbr, grow);
+    launch_pdl(grid_bucket_kernel<true>, dim3(blocks_for(nq, 256)), dim3(256), 0, stream, mq, nq, w.grid,
+               w.cell_start, w.cell_count, w.items, w.item_mbr, grow);
   // 2. probe into tile buckets; compaction (offsets, copies, total)
   if (np > 0) {
-    probe_kernel<false><<<(unsigned)T, kProbeTile, 0, stream>>>(mp, np, w.grid, w.cell_start, w.items, w.item_mbr,
-                                                                 w.tile_cnt, w.tile_long, w.bucket, nullptr, 0, nullptr,
-                                                                 nullptr,
-                                                                 nullptr, nullptr, grow);
-    probe_kernel<true><<<(unsigned)T, kProbeTile, 0, stream>>>(mp, np, w.grid, w.cell_start, w.items, w.item_mbr,
-                                                                w.tile_cnt, w.tile_long, w.bucket,
-                                                                reinterpret_cast<int2*>(pairs),
-                                                                pairs ? cap : 0, w.total, result, P->status,
-                                                                Q->status, grow);
+    launch_pdl(probe_kernel<false>, dim3((unsigned)T), dim3(kProbeTile), 0, stream, mp, np, w.grid, w.cell_start,
+               w.items, w.item_mbr, w.tile_cnt, w.tile_long, w.bucket, (int2*)nullptr, (long long)0,
+               (long long*)nullptr, (long long*)nullptr, (const uint32_t*)nullptr, (const uint32_t*)nullptr, grow);
+    launch_pdl(probe_kernel<true>, dim3((unsigned)T), dim3(kProbeTile), 0, stream, mp, np, w.grid, w.cell_start,
+               w.items, w.item_mbr, w.tile_cnt, w.tile_long, w.bucket, reinterpret_cast<int2*>(pairs),
+               (long long)(pairs ? cap : 0), w.total, result, P->status, Q->status, grow);
   } else {
     cudaMemsetAsync(w.total, 0, sizeof(long long), stream);
     if (result) filter_result_kernel<<<1, 32, 0, stream>>>(w.total, P->status, Q->status, result);

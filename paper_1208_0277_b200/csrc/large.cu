@@ -483,6 +483,8 @@ __global__ void __launch_bounds__(kLWarps * 32, 4)
                 unsigned* __restrict__ hit_p, unsigned* __restrict__ hit_q) {
   extern __shared__ __align__(16) unsigned char s_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  pdl_trigger();
+  pdl_wait();  // the small kernel's items and counters
   unsigned char* base = s_raw + (size_t)warp * kLSmemPerWarp;
   LocalPoly P, Q;
   P.V = reinterpret_cast<uint64_t*>(base);
@@ -670,10 +672,14 @@ int launch_large(const DevSet& Ps, const DevSet& Qs, const int2* pairs, const La
   }
   const bool count = counters != nullptr;
   const unsigned ib = (unsigned)(sms * max(per_sm[count], 1));
+  cudaError_t e;
   if (count)
-    item_kernel<true><<<ib, kLWarps * 32, kLSmem, stream>>>(Ps, Qs, pairs, w, T, mode, inter, uni, counters, sums, hit_p, hit_q);
+    e = launch_pdl(item_kernel<true>, dim3(ib), dim3(kLWarps * 32), kLSmem, stream, Ps, Qs, pairs, w, T, mode, inter,
+                   uni, counters, sums, hit_p, hit_q);
   else
-    item_kernel<false><<<ib, kLWarps * 32, kLSmem, stream>>>(Ps, Qs, pairs, w, T, mode, inter, uni, nullptr, sums, hit_p, hit_q);
+    e = launch_pdl(item_kernel<false>, dim3(ib), dim3(kLWarps * 32), kLSmem, stream, Ps, Qs, pairs, w, T, mode, inter,
+                   uni, (long long*)nullptr, sums, hit_p, hit_q);
+  if (int r = check_cuda(e, "pixelbox large launch")) return r;
   return check_cuda(cudaGetLastError(), "pixelbox large launch");
 }
 

@@ -126,6 +126,8 @@ __global__ void __launch_bounds__(kSmallWarps * 32, SCCG_SMALL_MINB)
                  LargeWs lw, long long* counters, unsigned* __restrict__ hit_p, unsigned* __restrict__ hit_q,
                  long long np_,
                  long long nq_) {
+  pdl_trigger();
+  pdl_wait();
   // pair count: host-given, or (async path) the filter's device-side count clamped to the buffer
   const long long n = dev_result ? min(dev_result[0], n_cap) : n_cap;
   if (dev_result && blockIdx.x == 0 && threadIdx.x == 0 && dev_result[1])

@@ -395,6 +395,8 @@ __device__ void flush_stats(StatAcc& acc, SetStats* stats, unsigned long long* s
 }
 
 __global__ void __launch_bounds__(kPrepThreads) prep_kernel(const __grid_constant__ PrepArgs args) {
+  pdl_trigger();
+  pdl_wait();  // prep_init's counters
   extern __shared__ int4 s_dyn4[];  // kPrepVerts int2 (16-byte aligned)
   int2* s_xy = reinterpret_cast<int2*>(s_dyn4);
   __shared__ int64_t s_off[kPrepPolys + 1];
@@ -574,6 +576,7 @@ __global__ void __launch_bounds__(kPrepThreads) prep_kernel(const __grid_constan
 }
 
 __global__ void prep_init_kernel(PrepArgs args) {
+  pdl_trigger();
   const int i = threadIdx.x;
   if (i < args.nsets) {
     uint32_t* status = args.set[i].status;
@@ -628,7 +631,7 @@ cudaError_t launch_prep(const sccg_polyset* const* sets, int count, int validate
     int64_t blocks = tiles;
     const int64_t cap = (int64_t)sms * (per_sm > 0 ? per_sm : 1);
     if (blocks > cap) blocks = cap;
-    prep_kernel<<<(unsigned)blocks, kPrepThreads, kPrepSmem, st>>>(a);
+    if (cudaError_t e = launch_pdl(prep_kernel, dim3((unsigned)blocks), dim3(kPrepThreads), kPrepSmem, st, a)) return e;
   }
   return cudaGetLastError();
 }
