@@ -494,8 +494,16 @@ int run_pixelbox(const sccg_polyset* p, const sccg_polyset* q, const int32_t* pa
   bool lok = true;
   const LargeWs lw = large_ws(n, w.large, w.large_bytes, lok);
   if (!lok) return set_error(SCCG_E_WORKSPACE, "pixelbox (large) workspace too small");
-  cudaMemsetAsync(w.queue, 0, 4 * sizeof(unsigned long long), stream);
-  cudaMemsetAsync(lw.ctr, 0, 4 * sizeof(unsigned long long), stream);
+  // the small kernel's queue and the large path's counters: one memset when
+  // they are neighbours in the workspace (they are: pixelbox_layout)
+  const char* qa = reinterpret_cast<const char*>(w.queue);
+  const char* ca = reinterpret_cast<const char*>(lw.ctr);
+  if (ca > qa && ca - qa <= 1024) {
+    cudaMemsetAsync(w.queue, 0, (size_t)(ca - qa) + 4 * sizeof(unsigned long long), stream);
+  } else {
+    cudaMemsetAsync(w.queue, 0, 4 * sizeof(unsigned long long), stream);
+    cudaMemsetAsync(lw.ctr, 0, 4 * sizeof(unsigned long long), stream);
+  }
   if (n == 0) return check_cuda(cudaGetLastError(), "pixelbox");
   const bool count = cfg && cfg->counters;
   long long* counters = count ? reinterpret_cast<long long*>(cfg->counters) : nullptr;

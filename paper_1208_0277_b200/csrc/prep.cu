@@ -323,7 +323,10 @@ struct StatAcc {
   }
 };
 
-constexpr int kThreadMaxV = 192;  // rings up to this size are prepped by one thread
+#ifndef SCCG_PREP_THREAD_MAXV
+#define SCCG_PREP_THREAD_MAXV 192
+#endif
+constexpr int kThreadMaxV = SCCG_PREP_THREAD_MAXV;  // rings up to this size are prepped by one thread
 constexpr int kSortKeys = 64;     // counting-sort buckets (V / 4) for dealing rings to threads
 
 // One launch preps up to kPrepMaxSets sets: their tiles form one index

@@ -19,6 +19,11 @@ for k in prep_kernel probe_kernel small_kernel; do
     -o $OUT/ncu_$k -f python bench.py --steps 1 --warmup 3 --no-cpu-baseline --e2e-steps 1 > $OUT/ncu_$k.txt 2>&1
   echo "ncu $k rc=$?"
 done
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:item_kernel -s 1 -c 1 \
+  -o $OUT/ncu_item_kernel_combs -f python bench.py --config combs --steps 1 --warmup 3 --no-cpu-baseline --e2e-steps 1 > $OUT/ncu_item.txt 2>&1
+echo "ncu item rc=$?"
+nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/int_peak scripts/int_peak.cu && timeout 300 /tmp/int_peak > $OUT/int_peak.json
+echo "int_peak rc=$?"
 for c in tile skewed combs; do
   timeout 900 python bench.py --config $c --steps 20 --warmup 3 --no-cpu-baseline > $OUT/bench_$c.json 2> $OUT/bench_$c.err
   echo "bench $c rc=$?"
