@@ -180,11 +180,12 @@ __device__ __forceinline__ int4 prep_polygon_thread(int2* v, int V, int rot, int
     return m;
   }
   uint64_t* out = reinterpret_cast<uint64_t*>(v);
-  // Area by Green's theorem on the rectilinear ring, A = |sum over vertical
-  // edges of x_i (y_{i+1} - y_i)| (the shoelace of P:193 with the horizontal
-  // edges' zero terms dropped, footnote P:205), accumulated mod 2^32: exact
-  // whenever A < 2^31, i.e. whenever W * H < 2^31 (else recomputed in int64
-  // from the records below).
+  // Area: the shoelace of P:193 in trapezoid form, A = 1/2 |sum (x_i +
+  // x_{i+1}) (y_{i+1} - y_i)| (the same sum re-associated), which on a
+  // rectilinear ring is |sum over vertical edges of x_i (y_{i+1} - y_i)|
+  // (horizontal edges add 0, vertical ones have x_i = x_{i+1}); accumulated
+  // mod 2^32: exact whenever A < 2^31, i.e. whenever W * H < 2^31 (else
+  // recomputed in int64 from the records below).
   unsigned area32 = 0u;
   bool diag = false;
   int nvert = 0, nhor = 0;
