@@ -96,7 +96,7 @@ __global__ void grid_select_kernel(const SetStats* __restrict__ sp, const SetSta
 // handled by their whole warp, lanes spread over the cells, so one polygon is
 // not a serial critical path of hundreds of dependent cell visits.
 #ifndef SCCG_COOP_CELLS
-#define SCCG_COOP_CELLS 32
+#define SCCG_COOP_CELLS 4
 #endif
 constexpr int kCoopCells = SCCG_COOP_CELLS;
 
@@ -323,6 +323,9 @@ __global__ void __launch_bounds__(kProbeTile) probe_kernel(const int4* __restric
   __shared__ int s_warp[kProbeTile / 32];
   __shared__ long long s_sum[kProbeTile / 32];
   __shared__ int s_fill[kProbeTile / 32];
+  __shared__ int s_coop[kProbeTile];     // threads of this tile whose MBR the warps probe together
+  __shared__ int s_coopval[kProbeTile];  // ... their pair count, then their output offset
+  __shared__ int s_cw[kProbeTile / 32];
   __shared__ int s_sort[kSortBuf];
   __shared__ int s_lock;
   __shared__ int2 s_pairs[COMPACT ? kBucket : 1];      // compaction: the tile's bucket
@@ -432,12 +435,32 @@ __global__ void __launch_bounds__(kProbeTile) probe_kernel(const int4* __restric
   int4 keep = make_int4(0, 0, 0, 0);
   const bool coop = act && mbr_cells(a, g.k) > kCoopCells;  // big MBR: its warp probes it together
   int n = act && !coop ? probe_cells<false>(a, p, g, cell_start, items, item_mbr, nullptr, keep) : 0;
-  const unsigned coop_mask = __ballot_sync(0xffffffffu, coop);
-  for (unsigned bm = coop_mask; bm; bm &= bm - 1) {
-    const int j = __ffs(bm) - 1;
-    const int cnt = coop_cells<false>(shfl4(a, j), p - threadIdx.x + (warp * 32 + j), g, cell_start, items, item_mbr,
-                                      nullptr, nullptr);
-    if (lane == j) n = cnt;
+  // big MBRs of the whole tile (glands among nuclei, C3: often consecutive in
+  // p) are dealt round-robin to the tile's warps, so their serial cell walks
+  // run side by side instead of queueing on the one warp that holds them
+  int ncoop = 0;
+  if (__syncthreads_or(coop)) {
+    const unsigned cm = __ballot_sync(0xffffffffu, coop);
+    if (lane == 0) s_cw[warp] = __popc(cm);
+    __syncthreads();
+    int off = 0;
+    for (int w = 0; w < kProbeTile / 32; w++) {
+      off += w < warp ? s_cw[w] : 0;
+      ncoop += s_cw[w];
+    }
+    if (coop) s_coop[off + __popc(cm & lanemask_lt())] = threadIdx.x;
+    __syncthreads();
+    for (int t = warp; t < ncoop; t += kProbeTile / 32) {
+      const int j = s_coop[t];
+      int4 aj = mp[(int64_t)tile * kProbeTile + j];
+      aj.z += grow;
+      aj.w += grow;
+      const int cnt = coop_cells<false>(aj, (int64_t)tile * kProbeTile + j, g, cell_start, items, item_mbr, nullptr,
+                                        nullptr);
+      if (lane == 0) s_coopval[j] = cnt;
+    }
+    __syncthreads();
+    if (coop) n = s_coopval[threadIdx.x];
   }
   // CTA exclusive scan of the counts
   int x = n;
@@ -459,12 +482,19 @@ __global__ void __launch_bounds__(kProbeTile) probe_kernel(const int4* __restric
     if (agg > kBucket) return;  // rare: the compact pass probes this tile again
   }
   const bool fits = n > 0;
-  // big MBRs: gathered by the warp, unsorted
-  for (unsigned bm = __ballot_sync(0xffffffffu, coop && fits); bm; bm &= bm - 1) {
-    const int j = __ffs(bm) - 1;
-    int2* seg = dst + __shfl_sync(0xffffffffu, base, j);
-    coop_cells<true>(shfl4(a, j), p - threadIdx.x + (warp * 32 + j), g, cell_start, items, item_mbr, seg,
-                     &s_fill[warp]);
+  // big MBRs: gathered by the warps (round-robin as above), unsorted
+  if (ncoop > 0) {
+    if (coop) s_coopval[threadIdx.x] = fits ? base : -1;
+    __syncthreads();
+    for (int t = warp; t < ncoop; t += kProbeTile / 32) {
+      const int j = s_coop[t];
+      if (s_coopval[j] < 0) continue;  // warp-uniform
+      int4 aj = mp[(int64_t)tile * kProbeTile + j];
+      aj.z += grow;
+      aj.w += grow;
+      coop_cells<true>(aj, (int64_t)tile * kProbeTile + j, g, cell_start, items, item_mbr, dst + s_coopval[j],
+                       &s_fill[warp]);
+    }
   }
   if (fits && !coop) {
     int2* seg = dst + base;
