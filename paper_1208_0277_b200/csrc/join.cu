@@ -495,6 +495,19 @@ __global__ void __launch_bounds__(kProbeTile) probe_kernel(const int4* __restric
       coop_cells<true>(aj, (int64_t)tile * kProbeTile + j, g, cell_start, items, item_mbr, dst + s_coopval[j],
                        &s_fill[warp]);
     }
+    __syncthreads();  // the warps' writes are visible to the segment's own thread
+    if (coop && fits && n <= kThreadSortMax) {  // short segment: its thread sorts it by q (longer: see below)
+      int2* seg = dst + base;
+      for (int i = 1; i < n; i++) {
+        const int2 v = seg[i];
+        int j = i - 1;
+        while (j >= 0 && seg[j].y > v.y) {
+          seg[j + 1] = seg[j];
+          j--;
+        }
+        seg[j + 1] = v;
+      }
+    }
   }
   if (fits && !coop) {
     int2* seg = dst + base;
@@ -534,12 +547,12 @@ __global__ void __launch_bounds__(kProbeTile) probe_kernel(const int4* __restric
   // long segments (big MBRs, or many hits): sorted by the compaction pass for
   // a bucket, here by the warp when writing in place (an overflowed tile)
   if (!COMPACT) {
-    const int any_long = __syncthreads_or(fits && (coop || n > kThreadSortMax));
+    const int any_long = __syncthreads_or(fits && n > kThreadSortMax);
     if (threadIdx.x == 0) tile_long[tile] = any_long ? 1 : 0;
     return;
   }
   __syncthreads();  // s_lock initialised; every segment written
-  for (unsigned bm = __ballot_sync(0xffffffffu, fits && (coop || n > kThreadSortMax)); bm; bm &= bm - 1) {
+  for (unsigned bm = __ballot_sync(0xffffffffu, fits && n > kThreadSortMax); bm; bm &= bm - 1) {
     const int j = __ffs(bm) - 1;
     warp_sort_segment(dst + __shfl_sync(0xffffffffu, base, j), __shfl_sync(0xffffffffu, n, j), s_sort, &s_lock);
   }

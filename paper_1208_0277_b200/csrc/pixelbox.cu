@@ -232,12 +232,10 @@ __global__ void __launch_bounds__(kSmallWarps * 32, SCCG_SMALL_MINB)
         s_rsh[warp][lane] = (unsigned)(-(int)(short)(mm.y & 0xffff)) | ((unsigned)(-(int)(short)(mm.z & 0xffff)) << 8) |
                             ((unsigned)W << 16) | ((unsigned)H << 24);
       }
-      // item -> pair map, written cooperatively pair by pair
-      for (unsigned m = rmask; m; m &= m - 1) {
-        const int j = __ffs(m) - 1;
-        const int st = __shfl_sync(FULL, sc - hl, j), hj = __shfl_sync(FULL, hl, j);
-        if (lane < hj) rmap[st + lane] = (unsigned char)j;
-      }
+      // item -> pair map: each lane writes its own pair's run (a loop of
+      // max(hl) <= 16 byte stores; a pair-by-pair cooperative loop over the
+      // ~32 raster pairs cost ~30 % of the kernel's instructions, profiles/r01)
+      for (int i = 0, st = sc - hl; i < hl; i++) rmap[st + i] = (unsigned char)lane;
       __syncwarp();
       const unsigned le = lanemask_lt() | (1u << lane);
       // four 32-item groups per round: all row loads are issued before any is
