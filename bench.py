@@ -39,6 +39,7 @@ METRIC = "polygon pairs/sec (and pixels tested/sec) at 1/2/4/8 B200 vs int-issue
 SMS_B200 = 148
 ISSUE_LANES_PER_CLK_SM = 128  # 4 SMSPs x 1 warp-instruction x 32 lanes (nominal dispatch)
 ALU_LANES_PER_CLK_SM = 64  # measured: ALU pipe 2 warp-inst/clk/SM (profiles/int_peak.json, scripts/int_peak.cu)
+STAGE_EVERY = 10  # per-stage CUDA events on every 10th timed step
 OPS_PER_ROWTEST = 3  # sub, unsigned compare, predicated xor
 OPS_PER_BOXEDGE = 8  # one lane classifying one edge against all sub-boxes of a split (minimum)
 
@@ -209,18 +210,22 @@ def run_ours(args, rank, world, local_rank):
     stream = torch.cuda.current_stream()
     # the whole step (prep x2, join, PixelBox) device-resident, no host sync until
     # the sums are read; replayed as two CUDA graphs (join | PixelBox)
-    pipe = sccg.Pipeline(P, Q, cap=3 * max(P.n, Q.n) + 1024, threshold=args.threshold, graph=True)
     # Steps are pipelined on the host: step i+1 is enqueued before step i's
-    # sums are read (the D2H copy is in-stream into one of two pinned buffers),
-    # so the GPU never idles on the host's per-step read-back; every step's
-    # result is still read and checked.
+    # sums are read (the read-back is in-stream into one of two pinned
+    # buffers), so the GPU never idles on the host's per-step read-back; every
+    # step's result is still read and checked.  One GPU: the PixelBox graph
+    # ends with sccg_sums_copy into the pinned buffer (the GPU writes it, no
+    # copy-engine transfer).  N > 1: all_reduce first, then the copy.
     host_bufs = [torch.zeros(len(sccg.SUMS_FIELDS), dtype=torch.int64).pin_memory() for _ in range(2)]
     done_ev = [torch.cuda.Event() for _ in range(2)]
+    pipe = sccg.Pipeline(P, Q, cap=3 * max(P.n, Q.n) + 1024, threshold=args.threshold, graph=True,
+                         readback=host_bufs if world == 1 else ())
 
     def enqueue(i, events=None):
-        sums = pipe.run(events)
-        sdist.allreduce_sums(sums)  # row a9: the only collective (NCCL, int64 SUM)
-        host_bufs[i % 2].copy_(sums, non_blocking=True)
+        sums = pipe.run(events, slot=i % 2)
+        if world > 1:
+            sdist.allreduce_sums(sums)  # row a9: the only collective (NCCL, int64 SUM)
+            host_bufs[i % 2].copy_(sums, non_blocking=True)
         done_ev[i % 2].record()
 
     def collect(i):
@@ -243,21 +248,24 @@ def run_ours(args, rank, world, local_rank):
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    # prep | join | PixelBox: live CUDA events on the launch stream, per step
-    stage_ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    # prep | join | PixelBox: live CUDA events on the launch stream, recorded
+    # around the stages of every STAGE_EVERY-th timed step (each event record
+    # between graphs costs the step ~2.5 us, so sampling keeps the step honest)
+    sampled = list(range(0, args.steps, STAGE_EVERY))
+    stage_ev = {i: [torch.cuda.Event(enable_timing=True) for _ in range(4)] for i in sampled}
     results = []
     with ClockSampler(local_rank) as clk:
         t0.record(stream)
         wall0 = time.perf_counter()
         for i in range(args.steps):
-            enqueue(i, stage_ev[i])
+            enqueue(i, stage_ev.get(i))
             if i > 0:
                 results.append(collect(i - 1))
         results.append(collect(args.steps - 1))
         t1.record(stream)
         torch.cuda.synchronize()
         wall1 = time.perf_counter()
-    stage_ms = [sum(ev[k].elapsed_time(ev[k + 1]) for ev in stage_ev) for k in range(3)]
+    stage_ms = [sum(ev[k].elapsed_time(ev[k + 1]) for ev in stage_ev.values()) for k in range(3)]
     host = results[-1]
     if any(bytes(r) != bytes(first) for r in results):
         raise RuntimeError("a timed step's sums differ from the warm-up's (nondeterminism)")
@@ -265,7 +273,7 @@ def run_ours(args, rank, world, local_rank):
         dist.barrier()
     pipe.check()
     ms = t0.elapsed_time(t1)
-    times = torch.tensor([ms] + [t / args.steps for t in stage_ms] + [float(n_local)], dtype=torch.float64,
+    times = torch.tensor([ms] + [t / len(sampled) for t in stage_ms] + [float(n_local)], dtype=torch.float64,
                          device=dev)
     if world > 1:
         mx = times.clone()
@@ -370,7 +378,8 @@ def run_ours(args, rank, world, local_rank):
             "parallelism": f"image-sharded x{world}" if world > 1 else "1 GPU",
         },
         "pixels_tested_per_s": cnt[sccg.CNT_PIXELS] * world / pix_s,
-        "stage_ms": {"prep": prep_ms_max, "join": join_ms_max, "pixelbox": pix_ms_max},
+        "stage_ms": {"prep": prep_ms_max, "join": join_ms_max, "pixelbox": pix_ms_max,
+                     "sampled_steps": len(sampled), "every": STAGE_EVERY},
         "jprime": jprime,
         "pooled_jaccard": pooled,
         "counters": {"pixels": cnt[0], "rowtests": cnt[1], "boxes": cnt[2], "boxedges": cnt[3], "splits": cnt[4],

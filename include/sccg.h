@@ -229,6 +229,14 @@ SCCG_API int sccg_touches(const sccg_polyset* p, const sccg_polyset* q, const in
  * same pairs.  Returns SCCG_E_EMPTY and NaN when n_nonzero == 0. */
 SCCG_API int sccg_jaccard(const sccg_sums* sums_host, double* jprime, double* pooled);
 
+/* Copy a sums block (88 bytes) from `src` (device) to `dst` with one single-warp kernel on `stream`, so a
+ * step's result read-back needs no copy-engine round trip (it can sit inside a CUDA graph).  `dst` may be
+ * device memory or page-locked host memory the device addresses through unified virtual addressing
+ * (cudaHostAlloc / a pinned torch tensor); the stores are fenced system-wide, so the host sees them once an
+ * event recorded after the call has completed.  Asynchronous.  Errors: SCCG_E_ARG for a null or
+ * misaligned (not 8-byte) pointer. */
+SCCG_API int sccg_sums_copy(const sccg_sums* src, sccg_sums* dst, sccg_stream_t stream);
+
 /* ------------------------------------------------------------------ misc */
 SCCG_API const char* sccg_strerror(int code);
 SCCG_API const char* sccg_last_error_string(void); /* thread-local detail of the last failure */

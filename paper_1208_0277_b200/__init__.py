@@ -38,7 +38,7 @@ SUMS_FIELDS = ("n_pairs", "n_nonzero", "sum_inter", "sum_union", "sum_area_p", "
                "limb2", "limb3", "status")
 SYMBOLS = ("sccg_polyset_bytes", "sccg_polyset_bind", "sccg_prep", "sccg_prep_sets", "sccg_filter_workspace_bytes",
            "sccg_filter_pairs", "sccg_filter_pairs_closed", "sccg_filter_pairs_async", "sccg_touches", "sccg_pixelbox_workspace_bytes", "sccg_pixelbox",
-           "sccg_pixelbox_async", "sccg_count_missing", "sccg_jaccard", "sccg_strerror", "sccg_last_error_string", "sccg_last_error_index",
+           "sccg_pixelbox_async", "sccg_count_missing", "sccg_jaccard", "sccg_sums_copy", "sccg_strerror", "sccg_last_error_string", "sccg_last_error_index",
            "sccg_version")
 
 
@@ -141,6 +141,8 @@ def load(build: bool = True):
         lib.sccg_jaccard.argtypes = [ctypes.POINTER(Sums), ctypes.POINTER(ctypes.c_double),
                                      ctypes.POINTER(ctypes.c_double)]
         lib.sccg_jaccard.restype = cint
+        lib.sccg_sums_copy.argtypes = [vp, vp, vp]
+        lib.sccg_sums_copy.restype = cint
         lib.sccg_strerror.argtypes = [cint]
         lib.sccg_strerror.restype = ctypes.c_char_p
         lib.sccg_last_error_string.argtypes = []
@@ -288,7 +290,7 @@ class Pipeline:
     ``run()`` returns the device sums vector; read it (one sync) for J'."""
 
     def __init__(self, P: "DeviceSet", Q: "DeviceSet", cap: int | None = None, threshold: int = 0, graph: bool = True,
-                 validate: bool = True, raster: bool = True):
+                 validate: bool = True, raster: bool = True, readback=()):
         torch = _torch()
         self.lib = load()
         self.P, self.Q = P, Q
@@ -304,6 +306,11 @@ class Pipeline:
         self.cfg = Config(threshold, 0, 0 if raster else FLAG_NO_RASTER, 0, None, None, None)
         self.validate = 1 if validate else 0
         self._sets = (PolySet * 2)(P.c, Q.c)  # copies of the bound descriptors (pointers only)
+        # readback: pinned host int64 [11] buffers; run(slot=k) ends the step by
+        # writing the sums into readback[k] from the GPU (sccg_sums_copy inside
+        # the PixelBox graph: no copy-engine transfer, no extra launch)
+        self.readback = tuple(readback)
+        self._slot = 0
         self.graphs = None
         if graph:
             s = torch.cuda.Stream(device=dev)
@@ -320,6 +327,13 @@ class Pipeline:
                     stage()
                 graphs.append(g)
             self.graphs = tuple(graphs)
+            self._pix_rb = []
+            for k in range(len(self.readback)):
+                self._slot = k
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g):
+                    self._enqueue_pixelbox()
+                self._pix_rb.append(g)
 
     @property
     def _stages(self):
@@ -341,17 +355,22 @@ class Pipeline:
                                             self.result.data_ptr(), self.cap, None, None, self.sums.data_ptr(),
                                             ctypes.byref(self.cfg), self.pws.data_ptr(), self.pws_bytes, _stream_ptr()),
                "sccg_pixelbox_async")
+        if self.readback:
+            sums_copy(self.sums, self.readback[self._slot])
 
-    def run(self, events=None):
+    def run(self, events=None, slot: int = 0):
         """One step: prep(P) + prep(Q) | MBR join | PixelBox, three graphs (or
         eager launches) back to back on the current stream.  events = four CUDA
         events recorded before prep, after prep, after the join and after
-        PixelBox (per-stage device times)."""
+        PixelBox (per-stage device times).  With readback buffers, the step's
+        sums also land in readback[slot] (read them after an event recorded
+        after run() has completed)."""
+        self._slot = slot
         for k, stage in enumerate(self._stages):
             if events:
                 events[k].record()
             if self.graphs is not None:
-                self.graphs[k].replay()
+                (self._pix_rb[slot] if k == 2 and self.readback else self.graphs[k]).replay()
             else:
                 stage()
         if events:
@@ -446,6 +465,14 @@ def contains(inter, area_inner):
 def sums_to_host(sums) -> Sums:
     vals = [int(v) for v in (sums.tolist() if hasattr(sums, "tolist") else sums)]
     return Sums(*vals)
+
+
+def sums_copy(src, dst, stream=None):
+    """Enqueue a copy of the sums vector `src` (device int64 [11]) into `dst`
+    (device tensor, or a pinned host tensor the GPU writes directly): one
+    single-warp kernel instead of a copy-engine transfer (sccg_sums_copy)."""
+    _check(load().sccg_sums_copy(src.data_ptr(), dst.data_ptr(), _stream_ptr(stream)), "sccg_sums_copy")
+    return dst
 
 
 def jaccard(sums) -> tuple[float, float]:

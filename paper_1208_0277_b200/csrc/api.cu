@@ -251,6 +251,12 @@ int sccg_count_missing(const uint32_t* hit, int64_t n, int64_t* missing_dev, scc
   return count_missing(hit, n, missing_dev, reinterpret_cast<cudaStream_t>(stream));
 }
 
+int sccg_sums_copy(const sccg_sums* src, sccg_sums* dst, sccg_stream_t stream) {
+  set_error(SCCG_OK, "", -1);
+  if (!src || !dst || !aligned(src, 8) || !aligned(dst, 8)) return set_error(SCCG_E_ARG, "sccg_sums_copy: null or misaligned pointer");
+  return check_cuda(launch_sums_copy(src, dst, reinterpret_cast<cudaStream_t>(stream)), "sccg_sums_copy");
+}
+
 int sccg_jaccard(const sccg_sums* s, double* jprime, double* pooled) {
   set_error(SCCG_OK, "", -1);
   if (!s || !jprime) return set_error(SCCG_E_ARG, "null argument");

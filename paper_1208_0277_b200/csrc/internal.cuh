@@ -130,5 +130,6 @@ int check_cuda(cudaError_t e, const char* where);
 
 // launchers
 cudaError_t launch_prep(const sccg_polyset* const* sets, int count, int validate, cudaStream_t st);
+cudaError_t launch_sums_copy(const sccg_sums* src, sccg_sums* dst, cudaStream_t st);
 
 }  // namespace sccg

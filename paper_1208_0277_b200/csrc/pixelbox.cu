@@ -558,6 +558,20 @@ __global__ void count_missing_kernel(const unsigned* __restrict__ hit, long long
 }
 
 __global__ void set_kernel(long long* out, long long v) { *out = v; }
+
+// sccg_sums_copy: 11 int64 by one warp; the fence makes host-memory
+// destinations visible system-wide before the kernel completes
+__global__ void sums_copy_kernel(const long long* __restrict__ src, volatile long long* dst) {
+  pdl_wait();
+  constexpr int kWords = (int)(sizeof(sccg_sums) / sizeof(long long));
+  if (threadIdx.x < kWords) dst[threadIdx.x] = src[threadIdx.x];
+  __threadfence_system();
+}
+
+cudaError_t launch_sums_copy(const sccg_sums* src, sccg_sums* dst, cudaStream_t st) {
+  return launch_pdl(sums_copy_kernel, dim3(1), dim3(32), 0, st, reinterpret_cast<const long long*>(src),
+                    reinterpret_cast<volatile long long*>(dst));
+}
 __global__ void finish_missing_kernel(long long* out, long long n) { *out = n - *out; }
 
 int count_missing(const uint32_t* hit, int64_t n, int64_t* out, cudaStream_t st) {

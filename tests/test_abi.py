@@ -88,6 +88,9 @@ def test_jaccard_host_logic_against_oracle():
     lib = sccg.load()
     jj = ctypes.c_double()
     assert lib.sccg_jaccard(ctypes.byref(sccg.Sums()), ctypes.byref(jj), None) == sccg.E_EMPTY
+    # sccg_sums_copy: null / misaligned pointers are rejected before anything is enqueued
+    assert lib.sccg_sums_copy(None, None, None) == sccg.E_ARG
+    assert lib.sccg_sums_copy(8, 12, None) == sccg.E_ARG
 
 
 def test_host_argument_checks():

@@ -466,6 +466,11 @@ def test_async_pipeline_matches_sync(sccg, tile_sets):
         assert torch.equal(s, ref)
         assert pipe.check() == pairs.shape[0]
         assert torch.equal(pipe.pairs[: pairs.shape[0]], pairs)
+    # the read-back kernel (sccg_sums_copy) into device memory and into pinned host memory
+    d = sccg.sums_copy(ref, torch.empty_like(ref))
+    h = sccg.sums_copy(ref, torch.zeros(ref.shape, dtype=torch.int64).pin_memory())
+    torch.cuda.synchronize()
+    assert torch.equal(d, ref) and h.tolist() == ref.tolist()
     tiny = sccg.Pipeline(P, Q, cap=10, graph=False)
     tiny.run()
     with pytest.raises(sccg.SccgError) as e:
