@@ -62,13 +62,13 @@ __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.a
 
 // Predicated shared-memory store / return-free XOR reduction (no divergent
 // branch around a conditional access).
-__device__ __forceinline__ void sts64_if(uint64_t* p, uint64_t v, bool c) {
-  asm volatile("{\n .reg .pred q;\n setp.ne.u32 q, %2, 0;\n @q st.shared.u64 [%0], %1;\n}\n" ::"r"(smem_u32(p)), "l"(v),
-               "r"((unsigned)c)
+__device__ __forceinline__ void sts64_if(unsigned saddr, unsigned lo, unsigned hi, bool c) {
+  asm volatile("{\n .reg .pred q;\n setp.ne.u32 q, %3, 0;\n @q st.shared.v2.u32 [%0], {%1, %2};\n}\n" ::"r"(saddr),
+               "r"(lo), "r"(hi), "r"((unsigned)c)
                : "memory");
 }
-__device__ __forceinline__ void red_xor_if(unsigned* p, unsigned v, bool c) {
-  asm volatile("{\n .reg .pred q;\n setp.ne.u32 q, %2, 0;\n @q red.shared.xor.b32 [%0], %1;\n}\n" ::"r"(smem_u32(p)),
+__device__ __forceinline__ void red_xor_if(unsigned saddr, unsigned v, bool c) {
+  asm volatile("{\n .reg .pred q;\n setp.ne.u32 q, %2, 0;\n @q red.shared.xor.b32 [%0], %1;\n}\n" ::"r"(saddr),
                "r"(v), "r"((unsigned)c)
                : "memory");
 }
@@ -187,20 +187,23 @@ __device__ __forceinline__ int4 prep_polygon_thread(int2* v, int V, int rot, int
   // mod 2^32: exact whenever A < 2^31, i.e. whenever W * H < 2^31 (else
   // recomputed in int64 from the records below).
   unsigned area32 = 0u;
-  bool diag = false;
-  int nvert = 0, nhor = 0;
+  // edge classes by counts: nsx = edges with dx == 0, nsy = with dy == 0;
+  // vertical = dx == 0 != dy (nvert), zero-length = nsx - nvert, horizontal =
+  // nsy - (nsx - nvert), diagonal = V - nsy - nvert
+  int nvert = 0, nsx = 0, nsy = 0;
   const unsigned fx = v[0].x - xmin, fy = v[0].y - ymin;
+  const unsigned sbase = smem_u32(out);
   unsigned ax = fx, ay = fy;
   auto edge = [&](unsigned cx, unsigned cy) {
     area32 += ax * (cy - ay);
     const bool same_x = ax == cx, same_y = ay == cy;
     const bool is_v = same_x && !same_y;
-    nhor += (same_y && !same_x) ? 1 : 0;
-    diag |= !same_x && !same_y;
+    nsx += same_x ? 1 : 0;
+    nsy += same_y ? 1 : 0;
     // record: x | lo << 16 | hi << 32 | exit row << 48 (the row the ring
     // leaves the edge at, read by the raster pass below; decoders mask it off)
-    const unsigned lo32 = ax | (min(ay, cy) << 16), hi32 = max(ay, cy) | (cy << 16);
-    sts64_if(out + nvert, ((uint64_t)hi32 << 32) | lo32, is_v);  // predicated: no divergent branch
+    const unsigned lo32 = __byte_perm(ax, min(ay, cy), 0x5410), hi32 = __byte_perm(max(ay, cy), cy, 0x5410);
+    sts64_if(sbase + 8u * (unsigned)nvert, lo32, hi32, is_v);  // predicated: no divergent branch
     nvert += is_v ? 1 : 0;
     ax = cx;
     ay = cy;
@@ -222,6 +225,8 @@ __device__ __forceinline__ int4 prep_polygon_thread(int2* v, int V, int rot, int
     edge((unsigned)(c.x - xmin), (unsigned)(c.y - ymin));
   }
   edge(fx, fy);  // closing edge back to the first vertex
+  const int nhor = nsy - (nsx - nvert);
+  const bool diag = V - nsy - nvert != 0;
   const int W = xmax - xmin, H = ymax - ymin;
   if ((unsigned long long)W * (unsigned long long)H < (1ull << 31)) {
     const int a = (int)area32;
@@ -255,13 +260,14 @@ __device__ __forceinline__ int4 prep_polygon_thread(int2* v, int V, int rot, int
     // branch, no load -> store chain), records read four at a time; the prefix
     // pass reads four rows ahead of its stores.
     unsigned* D = reinterpret_cast<unsigned*>(out + nvert);
+    const unsigned dbase = sbase + 8u * (unsigned)nvert;
     for (int r = 0; r < H; r++) D[r] = 0u;
     const uint64_t first = out[0];
     unsigned mc = shl_clamp(0xffffffffu, (unsigned)first & 0xffffu), yc = (unsigned)(first >> 48);
     const unsigned m0 = mc;
     auto apply = [&](uint64_t nxt) {
       const unsigned mn = shl_clamp(0xffffffffu, (unsigned)nxt & 0xffffu);
-      red_xor_if(D + yc, mc ^ mn, yc < (unsigned)H);
+      red_xor_if(dbase + 4u * yc, mc ^ mn, yc < (unsigned)H);
       mc = mn;
       yc = (unsigned)(nxt >> 48);
     };
@@ -274,7 +280,7 @@ __device__ __forceinline__ int4 prep_polygon_thread(int2* v, int V, int rot, int
       apply(r3);
     }
     for (; k < nvert; k++) apply(out[k]);
-    red_xor_if(D + yc, mc ^ m0, yc < (unsigned)H);  // the last record's exit is the first record's entry
+    red_xor_if(dbase + 4u * yc, mc ^ m0, yc < (unsigned)H);  // the last record's exit is the first record's entry
     unsigned acc = 0u;
     const unsigned wmask = low_bits(W);
     int r = 0;
@@ -398,7 +404,7 @@ __device__ void flush_stats(StatAcc& acc, SetStats* stats, unsigned long long* s
   acc.init();
 }
 
-__global__ void __launch_bounds__(kPrepThreads) prep_kernel(const __grid_constant__ PrepArgs args) {
+__global__ void __launch_bounds__(kPrepThreads, 5) prep_kernel(const __grid_constant__ PrepArgs args) {
   pdl_trigger();
   pdl_wait();  // prep_init's counters
   extern __shared__ int4 s_dyn4[];  // kPrepVerts int2 (16-byte aligned)
