@@ -52,6 +52,9 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="slide", choices=["slide", "tile", "skewed", "combs"])
     ap.add_argument("--threshold", type=int, default=0)
+    ap.add_argument("--shard", default="image", choices=["image", "tile"],
+                    help="N > 1: image = one slide image per rank (weak scaling, configs[3]); tile = ONE slide cut "
+                         "into y bands of P with their Q halo (strong scaling, SURVEY 8(e))")
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--json-out", default=None)
@@ -171,6 +174,12 @@ def make_workload(config: str, image: int):
     return synth.generate(config, image=image)
 
 
+def synth_set(xy, offsets):
+    import synth
+
+    return synth.PolygonSet(xy, offsets)
+
+
 def config_desc(config):
     return {
         "slide": "configs[1]: one 100k x 100k whole-slide image, two synthetic result sets of ~500k nucleus polygons",
@@ -197,7 +206,16 @@ def run_ours(args, rank, world, local_rank):
     if world > 1:
         dist.barrier()
     sccg.load(build=False)
-    A, B = make_workload(args.config, image=rank)
+    if args.shard == "tile":
+        # one slide for all ranks: this rank's P band and the Q that can meet it
+        A, B = make_workload(args.config, image=0)
+        pl, ph = sdist.ring_bounds(A.xy, A.offsets)
+        ql, qh = sdist.ring_bounds(B.xy, B.offsets)
+        pi, qi = sdist.band_shards(pl, ph, ql, qh, world)[rank]
+        A = synth_set(*sdist.subset_rings(A.xy, A.offsets, pi))
+        B = synth_set(*sdist.subset_rings(B.xy, B.offsets, qi))
+    else:
+        A, B = make_workload(args.config, image=rank)
     xy_p = torch.from_numpy(A.xy).pin_memory()
     off_p = torch.from_numpy(A.offsets).pin_memory()
     xy_q = torch.from_numpy(B.xy).pin_memory()
@@ -363,7 +381,7 @@ def run_ours(args, rank, world, local_rank):
         "warmup": max(args.warmup, 3),
         "ms_per_step": ms_max / args.steps,
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "strong" if args.shard == "tile" and world > 1 else "weak",
         "vs_baseline": None,
         "dtype": "int32",
         "data": "synthetic (seeded generator synth/, nucleus polygons per PAPER.md §5.1)",
@@ -377,7 +395,7 @@ def run_ours(args, rank, world, local_rank):
             "threshold_T": args.threshold or 2048,
             "l2": "inputs larger than L2 (vertex + edge-record arrays ~%d MB per rank > 126 MB)" % (
                 (P.nv + Q.nv) * 16 // 2**20),
-            "parallelism": f"image-sharded x{world}" if world > 1 else "1 GPU",
+            "parallelism": (f"{args.shard}-sharded x{world}" if world > 1 else "1 GPU"),
         },
         "pixels_tested_per_s": cnt[sccg.CNT_PIXELS] * world / pix_s,
         "stage_ms": {"prep": prep_ms_max, "join": join_ms_max, "pixelbox": pix_ms_max,

@@ -41,6 +41,70 @@ def shard_for_rank(n_items: int, world: int, rank: int, costs=None) -> list[int]
     return lpt_shards(c, world)[rank]
 
 
+def ring_bounds(xy, offsets):
+    """Per-ring y extent [ylo, yhi) of packed rings (numpy; for the sharding
+    plan only -- the device computes its own MBRs in prep)."""
+    import numpy as np
+
+    xy = np.asarray(xy).reshape(-1, 2)
+    off = np.asarray(offsets, dtype=np.int64)
+    n = off.shape[0] - 1
+    ylo = np.full(n, np.iinfo(np.int64).max, np.int64)
+    yhi = np.full(n, np.iinfo(np.int64).min, np.int64)
+    nz = off[1:] > off[:-1]
+    if nz.any():
+        starts = off[:-1][nz]
+        ylo[nz] = np.minimum.reduceat(xy[:, 1].astype(np.int64), starts)
+        yhi[nz] = np.maximum.reduceat(xy[:, 1].astype(np.int64), starts)
+    return ylo, yhi
+
+
+def band_shards(p_ylo, p_yhi, q_ylo, q_yhi, world: int):
+    """One slide over ``world`` ranks (SURVEY §8(e) "C2 at 8"; the paper's
+    tile-granularity tasks): P is cut into ``world`` horizontal bands of
+    equal polygon count by its MBRs' ylo (each p owned by exactly one rank);
+    rank r gets every q whose y extent meets [min ylo, max yhi) of its P band.
+    Any q that overlaps a p of band r meets that range, so the join of
+    (P_r, Q_r) yields exactly the pairs whose p is in band r: the ranks' pair
+    lists partition the slide's, and their integer sums add up to the slide's
+    bit for bit.  Returns [(p_idx, q_idx)] per rank (sorted index arrays;
+    empty rings -- ylo > yhi -- go with band 0 and pair with nothing)."""
+    import numpy as np
+
+    if world < 1:
+        raise ValueError("world must be >= 1")
+    p_ylo, p_yhi = np.asarray(p_ylo, np.int64), np.asarray(p_yhi, np.int64)
+    q_ylo, q_yhi = np.asarray(q_ylo, np.int64), np.asarray(q_yhi, np.int64)
+    order = np.lexsort((np.arange(p_ylo.shape[0]), p_ylo))  # by ylo, ties by index
+    cuts = [(len(order) * r) // world for r in range(world + 1)]
+    out = []
+    for r in range(world):
+        pi = np.sort(order[cuts[r] : cuts[r + 1]])
+        live = pi[p_ylo[pi] < p_yhi[pi]]
+        if live.size == 0:
+            out.append((pi, np.zeros(0, np.int64)))
+            continue
+        lo, hi = int(p_ylo[live].min()), int(p_yhi[live].max())
+        qi = np.nonzero((q_ylo < hi) & (q_yhi > lo))[0].astype(np.int64)
+        out.append((pi, qi))
+    return out
+
+
+def subset_rings(xy, offsets, idx):
+    """The packed rings ``idx`` of (xy, offsets), vectorised: (xy, offsets)."""
+    import numpy as np
+
+    xy = np.asarray(xy).reshape(-1, 2)
+    off = np.asarray(offsets, dtype=np.int64)
+    idx = np.asarray(idx, dtype=np.int64)
+    lens = off[idx + 1] - off[idx]
+    new_off = np.zeros(idx.shape[0] + 1, np.int64)
+    np.cumsum(lens, out=new_off[1:])
+    total = int(new_off[-1])
+    src = np.repeat(off[idx] - new_off[:-1], lens) + np.arange(total, dtype=np.int64)
+    return np.ascontiguousarray(xy[src], dtype=np.int32), new_off
+
+
 def allreduce_sums(sums, group=None):
     """In-place SUM of an int64 sums vector over the process group (NCCL for
     CUDA tensors, gloo for CPU tensors).  Returns the tensor."""

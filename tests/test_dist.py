@@ -99,3 +99,47 @@ def test_gloo_two_ranks_allreduce_is_exact():
     j, _ = sccg.jaccard(out[0])
     ex = oracle.jaccard_exact([i for i, _ in allpairs], [u for _, u in allpairs])
     assert abs(j - float(ex)) <= 1e-12 * float(ex)
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 5])
+def test_band_shards_partition_the_slide_pairs(world):
+    """One slide over `world` ranks: P cut into y bands, Q_r =
+    the q that meet band r's y range.  The ranks' joins, mapped back to global
+    indices, partition the single-process join (each pair on exactly one rank)
+    and the ranks' integer sums add up to the slide's (oracle, CPU)."""
+    import oracle
+    import synth
+
+    A, B = synth.generate("tile", image=3)
+    pylo, pyhi = sdist.ring_bounds(A.xy, A.offsets)
+    qylo, qyhi = sdist.ring_bounds(B.xy, B.offsets)
+    want = oracle.join(A, B)
+    shards = sdist.band_shards(pylo, pyhi, qylo, qyhi, world)
+    assert sorted(np.concatenate([pi for pi, _ in shards]).tolist()) == list(range(A.n))
+    got, tot = [], None
+    for pi, qi in shards:
+        xa, oa = sdist.subset_rings(A.xy, A.offsets, pi)
+        xb, ob = sdist.subset_rings(B.xy, B.offsets, qi)
+        Ar, Br = synth.PolygonSet(xa, oa), synth.PolygonSet(xb, ob)
+        pr = oracle.join(Ar, Br)
+        if len(pr):
+            got.append(np.stack([pi[pr[:, 0]], qi[pr[:, 1]]], 1))
+            inter, uni = oracle.pair_areas(Ar, Br, pr, threads=1)
+            s = oracle.sums(Ar, Br, pr, inter, uni)
+            tot = s if tot is None else {k: tot[k] + s[k] for k in s}
+    got = np.concatenate(got) if got else np.zeros((0, 2), np.int64)
+    got = got[np.lexsort((got[:, 1], got[:, 0]))]
+    assert got.shape == want.shape and (got == want).all()  # each pair exactly once
+    inter, uni = oracle.pair_areas(A, B, want, threads=1)
+    full = oracle.sums(A, B, want, inter, uni)
+    assert {k: int(v) for k, v in tot.items()} == {k: int(v) for k, v in full.items()}
+
+
+def test_band_shards_degenerate():
+    # empty / zero-height rings belong to a band but pair with nothing; more ranks than polygons
+    s = sdist.band_shards([5, 9, 0], [5, 12, 4], [0, 10], [3, 11], 5)
+    assert sorted(np.concatenate([p for p, _ in s]).tolist()) == [0, 1, 2]
+    for pi, qi in s:
+        assert set(pi.tolist()) <= {0, 1, 2}
+    with pytest.raises(ValueError):
+        sdist.band_shards([0], [1], [0], [1], 0)
