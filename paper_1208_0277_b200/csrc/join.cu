@@ -632,14 +632,15 @@ static int filter_enqueue(const sccg_polyset* P, const sccg_polyset* Q, FilterWs
   const int4* mp = reinterpret_cast<const int4*>(P->mbr);
   const int4* mq = reinterpret_cast<const int4*>(Q->mbr);
   const int64_t C = cell_cap(np, nq), T = probe_tiles(np);
-  // 1. grid size from the prep statistics (device side), bucket Q
+  // 1. grid size from the prep statistics (device side), bucket Q (the count
+  // array is cleared first, so the bucketing chains onto the selection)
+  cudaMemsetAsync(w.cell_count, 0, sizeof(int) * (C + 1), stream);
   grid_select_kernel<<<1, 32, 0, stream>>>(reinterpret_cast<const SetStats*>(P->stats),
                                            reinterpret_cast<const SetStats*>(Q->stats), C, entry_cap(nq), grow,
                                            w.grid);
-  cudaMemsetAsync(w.cell_count, 0, sizeof(int) * (C + 1), stream);
   if (nq > 0)
-    grid_bucket_kernel<false><<<blocks_for(nq, 256), 256, 0, stream>>>(mq, nq, w.grid, nullptr, w.cell_count,
-                                                                        nullptr, nullptr, grow);
+    launch_pdl(grid_bucket_kernel<false>, dim3(blocks_for(nq, 256)), dim3(256), 0, stream, mq, nq, w.grid,
+               (const int*)nullptr, w.cell_count, (int*)nullptr, (int4*)nullptr, grow);
   cub::DeviceScan::ExclusiveSum(w.tmp, w.tmp_bytes, w.cell_count, w.cell_start, (int)(C + 1), stream);
   if (nq > 0)
     launch_pdl(grid_bucket_kernel<true>, dim3(blocks_for(nq, 256)), dim3(256), 0, stream, mq, nq, w.grid,
