@@ -210,10 +210,15 @@ __device__ __forceinline__ int4 shfl4(const int4& v, int j) {
                    __shfl_sync(0xffffffffu, v.w, j));
 }
 
-// A big MBR probed by its whole warp: lane l visits cells l, l + 32, ... of
-// its cell rectangle.  COUNT returns the pairs it owns (every lane gets the
-// total); WRITE appends them to seg[] in arbitrary order (slots from *fill,
-// reset here) -- warp_sort_segment restores the q order.
+// A big MBR probed by its whole warp.  Its cell rectangle is taken 32 cells
+// at a time (lane l reads cell l's entry range); the entries of those cells
+// are then flattened over the lanes (a warp scan of the range lengths, and a
+// 5-step shuffle search for each entry's cell), so a lane tests entry after
+// entry of ALL the cells with independent loads -- a gland whose cells hold
+// dozens of nuclei each (C3) is not a serial walk per cell.  COUNT returns the
+// pairs it owns (every lane gets the total); WRITE appends them to seg[] in
+// arbitrary order (slots from *fill, reset here) -- the q order is restored
+// by the segment sort.
 template <bool WRITE>
 __device__ int coop_cells(const int4 a, long long p, const Grid& g, const int* __restrict__ cell_start,
                           const int* __restrict__ items, const int4* __restrict__ item_mbr, int2* __restrict__ seg,
@@ -227,13 +232,36 @@ __device__ int coop_cells(const int4 a, long long p, const Grid& g, const int* _
     __syncwarp();
   }
   int cnt = 0;
-  for (int t = lane; t < nc; t += 32) {
-    const int c = (y0 + t / w - cy0) * ncx + (x0 + t % w - cx0);
-    for (int it = cell_start[c], e = cell_start[c + 1]; it < e; it++)
-      if (owns(a, item_mbr[it], k, cx0, cy0, ncx, c)) {
-        if (WRITE) seg[atomicAdd(fill, 1)] = make_int2((int)p, items[it]);
-        cnt++;
+  for (int base = 0; base < nc; base += 32) {  // warp-uniform
+    const int t = base + lane;
+    int c = 0, s = 0, len = 0;
+    if (t < nc) {
+      c = (y0 + t / w - cy0) * ncx + (x0 + t % w - cx0);
+      s = cell_start[c];
+      len = cell_start[c + 1] - s;
+    }
+    int incl = len;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    const int total = __shfl_sync(0xffffffffu, incl, 31);
+    const int excl = incl - len;
+    for (int f0 = 0; f0 < total; f0 += 32) {  // warp-uniform
+      const int f = f0 + lane;
+      int j = 0;  // the lane whose cell holds flattened entry f: #lanes with incl <= f
+      for (int b = 16; b; b >>= 1)
+        if (__shfl_sync(0xffffffffu, incl, j + b - 1) <= f) j += b;
+      const int cj = __shfl_sync(0xffffffffu, c, j), sj = __shfl_sync(0xffffffffu, s, j);
+      const int ej = __shfl_sync(0xffffffffu, excl, j);
+      if (f < total) {
+        const int it = sj + (f - ej);
+        if (owns(a, item_mbr[it], k, cx0, cy0, ncx, cj)) {
+          if (WRITE) seg[atomicAdd(fill, 1)] = make_int2((int)p, items[it]);
+          cnt++;
+        }
       }
+    }
   }
   for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
   return cnt;
@@ -306,9 +334,12 @@ __device__ void warp_sort_segment(int2* seg, int n, int* buf, int* lock) {
 // directly; the last tile writes the total (and the async result word).  Pairs
 // past `cap` are not written; the total is exact.
 constexpr int kBucket = 1024;
+#ifndef SCCG_PROBE_MINB
+#define SCCG_PROBE_MINB 12
+#endif
 
 template <bool COMPACT>
-__global__ void __launch_bounds__(kProbeTile) probe_kernel(const int4* __restrict__ mp, int64_t np,
+__global__ void __launch_bounds__(kProbeTile, SCCG_PROBE_MINB) probe_kernel(const int4* __restrict__ mp, int64_t np,
                                                            const Grid* __restrict__ gp,
                                                            const int* __restrict__ cell_start,
                                                            const int* __restrict__ items,
