@@ -34,6 +34,13 @@
 
 namespace sccg {
 
+#ifndef SCCG_DENSE_SPLIT
+#define SCCG_DENSE_SPLIT 1
+#endif
+#ifndef SCCG_DENSE_NUM  // a split is dense when more than NUM/DEN of its sub-boxes hover (1/4: measured best
+#define SCCG_DENSE_NUM 1   // of 1/4, 1/2, 3/4 on C3 and C5)
+#define SCCG_DENSE_DEN 4
+#endif
 constexpr int kLWarps = 4;          // warps per CTA
 constexpr int kLCap = 192;          // local records per list (vertical / horizontal) per polygon per warp
 constexpr int kLStage = 96;         // staged records per polygon for one pixelized box
@@ -438,12 +445,24 @@ __device__ longlong2 region_pixelbox(const LocalPoly& P, const LocalPoly& Q, int
     const unsigned cont = valid & ~(mode == 2 ? (i_dec & u_dec) : i_dec);
     const unsigned contrib_i = valid & in_p & in_q & ~cont;
     const unsigned contrib_u = valid & (in_p | in_q) & ~cont;
+    const int ncont = __popc(cont);
+    // Dense split: every sub-box is below T and most of them hover, so the next
+    // level would stage edges for up to 32 small boxes; pixelizing B as one box
+    // (bands: first row by crossings, then the difference trick) gives the same
+    // exact count for less (an implementation choice, not Alg. 1's order; the
+    // areas are identical by construction).
+    if (SCCG_DENSE_SPLIT && mode == 0 && ((long long)1 << (g.lsx + g.lsy)) < T &&
+        ncont * SCCG_DENSE_DEN > __popc(valid) * SCCG_DENSE_NUM) {
+      const longlong2 r = pixelize_local<COUNT>(P, Q, x0, y0, x1, y1, pip, piq, uni, sv, sh, counters);
+      ai += r.x;
+      au += r.y;
+      continue;
+    }
     const int sx0 = cc << g.lsx, sy0 = rr << g.lsy;
     const int sx1 = min(sx0 + (1 << g.lsx), Wb), sy1 = min(sy0 + (1 << g.lsy), Hb);
     const long long sz = (long long)(sx1 - sx0) * (sy1 - sy0);
     if ((contrib_i >> lane) & 1u) ai += sz;
     if (uni && ((contrib_u >> lane) & 1u)) au += sz;
-    const int ncont = __popc(cont);
     if (COUNT && lane == 0) {
       atomicAdd((unsigned long long*)&counters[SCCG_CNT_BOXES], (unsigned long long)__popc(valid));
       atomicAdd((unsigned long long*)&counters[SCCG_CNT_BOXEDGES], (unsigned long long)(P.nV + P.nH + Q.nV + Q.nH));
