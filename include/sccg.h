@@ -174,6 +174,10 @@ typedef struct {
 /* flags: per-pair pixelization from edge records even where prep stored a ring's
  * raster (the paper's schedule, Alg. 1 l.24-25; results are identical) */
 #define SCCG_FLAG_NO_RASTER 1
+/* flags: every continuing sub-box of a split is pushed and processed on its own (Alg. 1 l.36-38 as
+ * written).  By default a split whose sub-boxes are all below T and of which more than a quarter hover is
+ * pixelized as one box instead (results are identical) */
+#define SCCG_FLAG_PAPER_SPLIT 2
 
 /* counters[] slots (accumulated; measurement builds only) */
 #define SCCG_CNT_PIXELS 0      /* pixels classified by pixelization (each against both polygons) */

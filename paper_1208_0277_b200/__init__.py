@@ -33,6 +33,7 @@ _lib = None
 OK, E_ARG, E_NOT_RECTILINEAR, E_RANGE, E_CAPACITY, E_STACK, E_EMPTY, E_CUDA, E_WORKSPACE = range(9)
 RASTER_FLAG = 1 << 30  # ecount[i, 1] bit: prep stored polygon i's raster rows
 FLAG_NO_RASTER = 1
+FLAG_PAPER_SPLIT = 2
 CNT_PIXELS, CNT_ROWTESTS, CNT_BOXES, CNT_BOXEDGES, CNT_SPLITS, CNT_PIXBOXES, CNT_ROOTPX = range(7)
 SUMS_FIELDS = ("n_pairs", "n_nonzero", "sum_inter", "sum_union", "sum_area_p", "sum_area_q", "limb0", "limb1",
                "limb2", "limb3", "status")
@@ -408,8 +409,11 @@ def new_sums(device=None):
 
 
 def pixelbox(P: DeviceSet, Q: DeviceSet, pairs, threshold: int = 0, mode: int = 0, sums=None, want_inter=True,
-             want_union=True, counters=None, grid: int = 0, hits=None, raster: bool = True, stream=None):
+             want_union=True, counters=None, grid: int = 0, hits=None, raster: bool = True, paper_split: bool = False,
+             stream=None):
     """Per-pair |p n q| and |p u q| (int64, input order) + accumulated sums.
+    paper_split: push every continuing sub-box (Alg. 1 as written) instead of
+    pixelizing dense splits whole (SCCG_FLAG_PAPER_SPLIT; same results).
     hits = (hit_p, hit_q): optional int32 bitmaps (new_hits) marking polygons
     with a non-zero intersection, for missing_polygons()."""
     torch = _torch()
@@ -422,7 +426,7 @@ def pixelbox(P: DeviceSet, Q: DeviceSet, pairs, threshold: int = 0, mode: int = 
     if sums is None:
         sums = new_sums(dev)
     _require_cuda(sums, "sums", torch.int64)
-    cfg = Config(threshold, mode, 0 if raster else FLAG_NO_RASTER, grid,
+    cfg = Config(threshold, mode, (0 if raster else FLAG_NO_RASTER) | (FLAG_PAPER_SPLIT if paper_split else 0), grid,
                  counters.data_ptr() if counters is not None else None,
                  hits[0].data_ptr() if hits is not None else None, hits[1].data_ptr() if hits is not None else None)
     wsb = int(lib.sccg_pixelbox_workspace_bytes(n))

@@ -219,7 +219,8 @@ static int pixelbox_checks(const sccg_polyset* p, const sccg_polyset* q, const i
     return set_error(SCCG_E_ARG, "misaligned pointer");
   if (cfg) {
     if (cfg->threshold < 0) return set_error(SCCG_E_ARG, "config.threshold < 0");
-    if (cfg->flags & ~SCCG_FLAG_NO_RASTER) return set_error(SCCG_E_ARG, "config.flags: unknown bits");
+    if (cfg->flags & ~(SCCG_FLAG_NO_RASTER | SCCG_FLAG_PAPER_SPLIT))
+      return set_error(SCCG_E_ARG, "config.flags: unknown bits");
     if (cfg->grid < 0) return set_error(SCCG_E_ARG, "config.grid < 0");
   }
   return SCCG_OK;

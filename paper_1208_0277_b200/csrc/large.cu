@@ -408,7 +408,7 @@ __device__ __forceinline__ uint64_t pack_sb(int x0, int y0, int x1, int y1, int 
 // (§5.2: a box is decided only when both its intersection and union
 // contributions are).  Returns this lane's (I, U) share.
 template <bool COUNT>
-__device__ longlong2 region_pixelbox(const LocalPoly& P, const LocalPoly& Q, int Wr, int Hr, int T, int mode,
+__device__ longlong2 region_pixelbox(const LocalPoly& P, const LocalPoly& Q, int Wr, int Hr, int T, int mode, int dense,
                                      uint64_t* stk, int4* sv, int* sh, long long* counters, unsigned& status) {
   const int lane = threadIdx.x & 31;
   const bool uni = mode != 0;
@@ -451,7 +451,7 @@ __device__ longlong2 region_pixelbox(const LocalPoly& P, const LocalPoly& Q, int
     // (bands: first row by crossings, then the difference trick) gives the same
     // exact count for less (an implementation choice, not Alg. 1's order; the
     // areas are identical by construction).
-    if (SCCG_DENSE_SPLIT && mode == 0 && ((long long)1 << (g.lsx + g.lsy)) < T &&
+    if (SCCG_DENSE_SPLIT && dense && mode == 0 && ((long long)1 << (g.lsx + g.lsy)) < T &&
         ncont * SCCG_DENSE_DEN > __popc(valid) * SCCG_DENSE_NUM) {
       const longlong2 r = pixelize_local<COUNT>(P, Q, x0, y0, x1, y1, pip, piq, uni, sv, sh, counters);
       ai += r.x;
@@ -497,7 +497,7 @@ constexpr size_t kLSmem = kLWarps * kLSmemPerWarp;
 
 template <bool COUNT>
 __global__ void __launch_bounds__(kLWarps * 32, 4)
-    item_kernel(DevSet Ps, DevSet Qs, const int2* __restrict__ pairs, LargeWs w, int T, int mode,
+    item_kernel(DevSet Ps, DevSet Qs, const int2* __restrict__ pairs, LargeWs w, int T, int mode, int dense,
                 long long* __restrict__ inter, long long* __restrict__ uni, long long* counters, sccg_sums* sums,
                 unsigned* __restrict__ hit_p, unsigned* __restrict__ hit_q) {
   extern __shared__ __align__(16) unsigned char s_raw[];
@@ -590,7 +590,7 @@ __global__ void __launch_bounds__(kLWarps * 32, 4)
         __syncwarp();
         continue;
       }
-      const longlong2 r = region_pixelbox<COUNT>(P, Q, Wr, Hr, T, mode, stk, sv, sh, counters, status);
+      const longlong2 r = region_pixelbox<COUNT>(P, Q, Wr, Hr, T, mode, dense, stk, sv, sh, counters, status);
       acc += r.x;
       acc_u += r.y;
       __syncwarp();
@@ -672,7 +672,7 @@ LargeWs large_ws(long long n_cap, void* ws, size_t ws_bytes, bool& ok) {
 }
 
 int launch_large(const DevSet& Ps, const DevSet& Qs, const int2* pairs, const LargeWs& w, long long* inter,
-                 long long* uni, sccg_sums* sums, int T, int mode, long long* counters, unsigned* hit_p,
+                 long long* uni, sccg_sums* sums, int T, int mode, int dense, long long* counters, unsigned* hit_p,
                  unsigned* hit_q, cudaStream_t stream) {
   static cudaError_t attr = [] {
     cudaError_t e = cudaFuncSetAttribute(item_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kLSmem);
@@ -693,10 +693,10 @@ int launch_large(const DevSet& Ps, const DevSet& Qs, const int2* pairs, const La
   const unsigned ib = (unsigned)(sms * max(per_sm[count], 1));
   cudaError_t e;
   if (count)
-    e = launch_pdl(item_kernel<true>, dim3(ib), dim3(kLWarps * 32), kLSmem, stream, Ps, Qs, pairs, w, T, mode, inter,
+    e = launch_pdl(item_kernel<true>, dim3(ib), dim3(kLWarps * 32), kLSmem, stream, Ps, Qs, pairs, w, T, mode, dense, inter,
                    uni, counters, sums, hit_p, hit_q);
   else
-    e = launch_pdl(item_kernel<false>, dim3(ib), dim3(kLWarps * 32), kLSmem, stream, Ps, Qs, pairs, w, T, mode, inter,
+    e = launch_pdl(item_kernel<false>, dim3(ib), dim3(kLWarps * 32), kLSmem, stream, Ps, Qs, pairs, w, T, mode, dense, inter,
                    uni, (long long*)nullptr, sums, hit_p, hit_q);
   if (int r = check_cuda(e, "pixelbox large launch")) return r;
   return check_cuda(cudaGetLastError(), "pixelbox large launch");

@@ -533,7 +533,8 @@ int run_pixelbox(const sccg_polyset* p, const sccg_polyset* q, const int32_t* pa
         Ps, Qs, pr, n, dr, in, un, sums, T, mode, use_raster, w.queue, lw, nullptr, hp, hq, p->n_polygons,
         q->n_polygons);
   if (int r = check_cuda(cudaGetLastError(), "pixelbox small launch")) return r;
-  return launch_large(Ps, Qs, pr, lw, in, un, sums, T, mode, counters, hp, hq, stream);
+  const int dense = !(cfg && (cfg->flags & SCCG_FLAG_PAPER_SPLIT));
+  return launch_large(Ps, Qs, pr, lw, in, un, sums, T, mode, dense, counters, hp, hq, stream);
 }
 
 }  // namespace sccg

@@ -126,7 +126,7 @@ size_t large_ws_bytes(long long n_cap);
 LargeWs large_ws(long long n_cap, void* ws, size_t ws_bytes, bool& ok);
 // the region-item kernel over everything the small kernel routed to the large path
 int launch_large(const DevSet& Ps, const DevSet& Qs, const int2* pairs, const LargeWs& w, long long* inter,
-                 long long* uni, sccg_sums* sums, int T, int mode, long long* counters, unsigned* hit_p,
+                 long long* uni, sccg_sums* sums, int T, int mode, int dense, long long* counters, unsigned* hit_p,
                  unsigned* hit_q, cudaStream_t stream);
 
 }  // namespace sccg

@@ -47,7 +47,7 @@ def main():
             for r in range(args.reps + 1):
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record()
-                out = sccg.pixelbox(P, Q, pairs, mode=mode, threshold=T)
+                out = sccg.pixelbox(P, Q, pairs, mode=mode, threshold=T, paper_split=True)
                 e1.record()
                 torch.cuda.synchronize()
                 if r:

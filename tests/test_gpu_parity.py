@@ -316,6 +316,9 @@ def test_pixelbox_skewed_glands(sccg, T):
     check_batch(sccg, A, B, pairs.cpu().numpy(), inter, uni, sums)
     c = counters.cpu().tolist()
     assert c[sccg.CNT_SPLITS] > 0 and c[sccg.CNT_PIXBOXES] > 0
+    # Alg. 1's split order as written (no dense-split shortcut): the same areas
+    i2, u2, s2 = sccg.pixelbox(P, Q, pairs, threshold=T, paper_split=True)
+    assert torch.equal(i2, inter) and torch.equal(u2, uni) and torch.equal(s2, sums)
 
 
 def _staircase(x0, y0, n, step=1):
@@ -382,13 +385,15 @@ def test_pixelbox_combs_closed_form(sccg):
     assert pairs.cpu().numpy().tolist() == [[k, k] for k in range(96)]
     # small T: many small leaf boxes (per-row crossings); 2^30: whole regions
     # pixelized in bands (difference trick); modes 1/2 count the union directly
-    for T, mode in ((256, 0), (4096, 0), (1 << 30, 0), (1 << 30, 1), (4096, 2)):
-        inter, uni, sums = sccg.pixelbox(P, Q, pairs, threshold=T, mode=mode)
+    # paper_split: every continuing sub-box pushed (Alg. 1 as written) instead of dense splits pixelized whole
+    for T, mode, ps in ((256, 0, False), (256, 0, True), (2048, 0, False), (2048, 0, True), (4096, 0, False),
+                        (1 << 30, 0, False), (1 << 30, 1, False), (4096, 2, False)):
+        inter, uni, sums = sccg.pixelbox(P, Q, pairs, threshold=T, mode=mode, paper_split=ps)
         gi, gu = inter.cpu().numpy(), uni.cpu().numpy()
         for k in range(96):
             want = combs.rect_decomp_intersection(RA[k], RB[k])
-            assert gi[k] == want, (T, mode, k)
-            assert gu[k] == combs.rect_decomp_area(RA[k]) + combs.rect_decomp_area(RB[k]) - want, (T, mode, k)
+            assert gi[k] == want, (T, mode, ps, k)
+            assert gu[k] == combs.rect_decomp_area(RA[k]) + combs.rect_decomp_area(RB[k]) - want, (T, mode, ps, k)
     check_batch(sccg, A, B, pairs.cpu().numpy()[:24], *sccg.pixelbox(P, Q, pairs[:24]))
 
 
