@@ -28,6 +28,9 @@ constexpr int kPrepThreads = SCCG_PREP_THREADS;
 constexpr int kPrepPolys = kPrepThreads;  // one ring per thread per tile
 static_assert(kPrepThreads % 32 == 0 && kPrepThreads <= 256, "whole warps; ring indices fit a byte");
 constexpr int kPrepVerts = SCCG_PREP_VERTS;
+#ifndef SCCG_PREP_L2_PREFETCH
+#define SCCG_PREP_L2_PREFETCH 2  // 0: off, 1: after the ring phase, 2: before it (measured best)
+#endif
 constexpr size_t kPrepSmem = kPrepVerts * sizeof(int2);  // 40 KB of int2 staged per tile (dynamic shared memory)
 
 
@@ -521,6 +524,26 @@ __global__ void __launch_bounds__(kPrepThreads, 5) prep_kernel(const __grid_cons
     __syncthreads();
     if (threadIdx.x < np) s_perm[s_cnt[key] + pos] = (unsigned char)threadIdx.x;
     __syncthreads();
+#if SCCG_PREP_L2_PREFETCH == 2
+    if (threadIdx.x == 0) {
+      // thread 0 (warp 0 deals the smallest rings, so it has slack) starts
+      // pulling the next tile's vertex range into L2 while this tile's rings
+      // are worked on: that tile's TMA load then hits L2 instead of HBM
+      if (next_gt < ntiles) {
+        int si2, np2;
+        int64_t p02;
+        tile_range(next_gt, si2, p02, np2);
+        const PrepSet& S2 = args.set[si2];
+        if (S2.bulk) {
+          const int64_t w0 = S2.off[p02] & ~int64_t(1), w1 = S2.off[p02 + np2];
+          if (w0 >= 0 && w1 > w0 && w1 <= S2.nv_total && w1 - w0 <= kPrepVerts) {
+            const unsigned bytes = (unsigned)((w1 - w0 + 1) & ~int64_t(1)) * 8u;
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(S2.xy + w0), "r"(bytes) : "memory");
+          }
+        }
+      }
+    }
+#endif
     // thread per small ring (records in place in the tile)
     if (s_perm[threadIdx.x] != 0xff) {
       const int j = s_perm[threadIdx.x];
@@ -539,7 +562,27 @@ __global__ void __launch_bounds__(kPrepThreads, 5) prep_kernel(const __grid_cons
         acc.add(prep_polygon_thread(s_xy + (b - v0), (int)V, rot, poly, mbr, area, ecount, status, validate));
       }
     }
-    if (threadIdx.x == 0) s_tile = next_gt;
+    if (threadIdx.x == 0) {
+      s_tile = next_gt;
+#if SCCG_PREP_L2_PREFETCH == 1
+      // warp 0 deals the smallest rings and waits here for the others: its
+      // lane 0 starts pulling the next tile's vertex range into L2, so that
+      // tile's TMA load hits L2 instead of HBM
+      if (next_gt < ntiles) {
+        int si2, np2;
+        int64_t p02;
+        tile_range(next_gt, si2, p02, np2);
+        const PrepSet& S2 = args.set[si2];
+        if (S2.bulk) {
+          const int64_t w0 = S2.off[p02] & ~int64_t(1), w1 = S2.off[p02 + np2];
+          if (w0 >= 0 && w1 > w0 && w1 <= S2.nv_total && w1 - w0 <= kPrepVerts) {
+            const unsigned bytes = (unsigned)((w1 - w0 + 1) & ~int64_t(1)) * 8u;
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(S2.xy + w0), "r"(bytes) : "memory");
+          }
+        }
+      }
+#endif
+    }
     __syncthreads();
     const int64_t gt_next = s_tile;
     fetch_offsets(gt_next);  // in flight during the rest of this tile
