@@ -1,5 +1,6 @@
 """Small end-to-end run for compute-sanitizer (memcheck / racecheck / synccheck):
-tile + a skewed window with glands, counting and non-counting builds, all T."""
+tile + a skewed window with glands, counting and non-counting builds, all T,
+the bench's pipeline step, and comb pairs (dense splits / Alg. 1's split order)."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
@@ -16,5 +17,20 @@ for cfg, kw in [("tile", {}), ("skewed", dict(width=4096, height=4096))]:
         sccg.pixelbox(P, Q, pairs, threshold=T, counters=c)
         sccg.pixelbox(P, Q, pairs, threshold=T)
     sccg.pixelbox(P, Q, pairs, mode=1)
+    sccg.pixelbox(P, Q, pairs, threshold=2048, paper_split=True)
+    # the bench's step: prep of both sets in one launch, async join + PixelBox, read-back kernel
+    rb = [torch.zeros(len(sccg.SUMS_FIELDS), dtype=torch.int64).pin_memory()]
+    pipe = sccg.Pipeline(P, Q, graph=False, readback=rb)
+    pipe.run()
+    torch.cuda.synchronize()
+    pipe.check()
+# combs: dense splits pixelized whole, and Alg. 1's split order
+from synth import combs
+A, B = combs.generate(n_pairs=24)
+P = sccg.DeviceSet(*sccg.to_device(A.xy, A.offsets))
+Q = sccg.DeviceSet(*sccg.to_device(B.xy, B.offsets))
+pairs = sccg.filter_pairs(P, Q)
+for ps in (False, True):
+    sccg.pixelbox(P, Q, pairs, threshold=2048, paper_split=ps)
 torch.cuda.synchronize()
 print("sanitize case ok")
