@@ -427,27 +427,24 @@ __global__ void __launch_bounds__(kProbeTile, SCCG_PROBE_MINB) probe_kernel(cons
       }
       __syncthreads();
       const int nruns = s_runs[2 * kProbeTile];
-      for (int r = 0; r < nruns; r++) {  // CTA-wide ascending-only bitonic network on the run's q
-        int2* run = s_pairs + s_runs[2 * r];
-        const int n = s_runs[2 * r + 1];
-        int m = 1;
-        while (m < n) m <<= 1;
-        for (int k = 2; k <= m; k <<= 1)
-          for (int j = k >> 1; j > 0; j >>= 1) {
-            for (int i = threadIdx.x; i < m; i += kProbeTile) {
-              const int l = j == (k >> 1) ? (i ^ (k - 1)) : (i ^ j);
-              if (l > i && l < n) {
-                const int2 u = run[i], v = run[l];
-                if (v.y < u.y) {
-                  run[i] = v;
-                  run[l] = u;
-                }
-              }
-            }
-            __syncthreads();
-          }
-      }
       for (int i = threadIdx.x; i < cnt; i += kProbeTile) pairs[off + i] = s_pairs[i];
+      if (nruns == 0) return;
+      __syncthreads();  // the long runs' unsorted copies are overwritten below
+      // long runs: rank sort -- an entry's place in its run is the number of
+      // the run's q below its own (q are distinct within a run); every thread
+      // moves on to the next run without a barrier, so a tile with many glands
+      // costs its total run work, not a barrier-bound network per run
+      for (int r = 0; r < nruns; r++) {
+        const int s0 = s_runs[2 * r], n = s_runs[2 * r + 1];
+        const int2* run = s_pairs + s0;
+        for (int i = threadIdx.x; i < n; i += kProbeTile) {
+          const int2 v = run[i];
+          int rank = 0;
+#pragma unroll 4
+          for (int j = 0; j < n; j++) rank += run[j].y < v.y ? 1 : 0;
+          pairs[off + s0 + rank] = v;
+        }
+      }
       return;
     }
     dst = pairs + off;  // overflowed tile: probe again, write in place
