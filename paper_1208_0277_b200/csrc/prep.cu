@@ -529,19 +529,21 @@ __global__ void __launch_bounds__(kPrepThreads, 5) prep_kernel(const __grid_cons
       // thread 0 (warp 0 deals the smallest rings, so it has slack) starts
       // pulling the next tile's vertex range into L2 while this tile's rings
       // are worked on: that tile's TMA load then hits L2 instead of HBM
-      if (next_gt < ntiles) {
+      // (also prefetching the tile one grid-width further measured slower: 161 vs 159 us)
+      auto prefetch_tile = [&](long long g) {
+        if (g >= ntiles) return;
         int si2, np2;
         int64_t p02;
-        tile_range(next_gt, si2, p02, np2);
+        tile_range(g, si2, p02, np2);
         const PrepSet& S2 = args.set[si2];
-        if (S2.bulk) {
-          const int64_t w0 = S2.off[p02] & ~int64_t(1), w1 = S2.off[p02 + np2];
-          if (w0 >= 0 && w1 > w0 && w1 <= S2.nv_total && w1 - w0 <= kPrepVerts) {
-            const unsigned bytes = (unsigned)((w1 - w0 + 1) & ~int64_t(1)) * 8u;
-            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(S2.xy + w0), "r"(bytes) : "memory");
-          }
+        if (!S2.bulk) return;
+        const int64_t w0 = S2.off[p02] & ~int64_t(1), w1 = S2.off[p02 + np2];
+        if (w0 >= 0 && w1 > w0 && w1 <= S2.nv_total && w1 - w0 <= kPrepVerts) {
+          const unsigned bytes = (unsigned)((w1 - w0 + 1) & ~int64_t(1)) * 8u;
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(S2.xy + w0), "r"(bytes) : "memory");
         }
-      }
+      };
+      prefetch_tile(next_gt);
     }
 #endif
     // thread per small ring (records in place in the tile)
