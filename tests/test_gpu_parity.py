@@ -471,7 +471,14 @@ def test_async_pipeline_matches_sync(sccg, tile_sets):
         assert torch.equal(s, ref)
         assert pipe.check() == pairs.shape[0]
         assert torch.equal(pipe.pairs[: pairs.shape[0]], pairs)
-    # the read-back kernel (sccg_sums_copy) into device memory and into pinned host memory
+    # the bench's step: the PixelBox graph ends with the read-back kernel into pinned slot k
+    rb = [torch.zeros(ref.shape, dtype=torch.int64).pin_memory() for _ in range(2)]
+    pipe = sccg.Pipeline(P, Q, graph=True, readback=rb)
+    for i in range(4):
+        s = pipe.run(slot=i % 2)
+        torch.cuda.synchronize()
+        assert rb[i % 2].tolist() == ref.tolist() and torch.equal(s, ref)
+        # the read-back kernel (sccg_sums_copy) into device memory and into pinned host memory
     d = sccg.sums_copy(ref, torch.empty_like(ref))
     h = sccg.sums_copy(ref, torch.zeros(ref.shape, dtype=torch.int64).pin_memory())
     torch.cuda.synchronize()
