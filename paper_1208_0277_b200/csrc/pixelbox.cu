@@ -238,9 +238,12 @@ __global__ void __launch_bounds__(kSmallWarps * 32, SCCG_SMALL_MINB)
       for (int i = 0, st = sc - hl; i < hl; i++) rmap[st + i] = (unsigned char)lane;
       __syncwarp();
       const unsigned le = lanemask_lt() | (1u << lane);
-      // four 32-item groups per round: all row loads are issued before any is
+      // kU 32-item groups per round: all row loads are issued before any is
       // consumed (many loads in flight per lane)
-      constexpr int kU = 4;
+#ifndef SCCG_RASTER_GROUPS
+#define SCCG_RASTER_GROUPS 3  // row-load groups in flight per lane (measured: 3 < 2 < 4 < 6 in time)
+#endif
+      constexpr int kU = SCCG_RASTER_GROUPS;
       for (int t0 = 0; t0 < R; t0 += 32 * kU) {  // warp-uniform trip count
         unsigned wpv[kU], wqv[kU], wpw[kU], wqw[kU], shv[kU];
         int jrv[kU];
