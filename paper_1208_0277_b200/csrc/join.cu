@@ -153,7 +153,10 @@ __global__ void grid_bucket_kernel(const int4* __restrict__ mq, int64_t nq, cons
   }
 }
 
-constexpr int kProbeTile = 128;  // p per probe CTA
+#ifndef SCCG_PROBE_TILE
+#define SCCG_PROBE_TILE 128
+#endif
+constexpr int kProbeTile = SCCG_PROBE_TILE;  // p per probe CTA
 
 constexpr int kKeep = 4;  // hits kept in registers by the counting pass
 

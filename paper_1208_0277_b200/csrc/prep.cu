@@ -337,6 +337,9 @@ struct StatAcc {
 #define SCCG_PREP_THREAD_MAXV 192
 #endif
 constexpr int kThreadMaxV = SCCG_PREP_THREAD_MAXV;  // rings up to this size are prepped by one thread
+#ifndef SCCG_PREP_SORT_SHIFT
+#define SCCG_PREP_SORT_SHIFT 2  // counting-sort key = V >> shift
+#endif
 constexpr int kSortKeys = 64;     // counting-sort buckets (V / 4) for dealing rings to threads
 
 // One launch preps up to kPrepMaxSets sets: their tiles form one index
@@ -485,7 +488,7 @@ __global__ void __launch_bounds__(kPrepThreads, 5) prep_kernel(const __grid_cons
     // more instructions: measured, profiles/r01).
     int key = 0, pos = 0;
     if (threadIdx.x < np) {
-      key = (int)min((s_off[threadIdx.x + 1] - s_off[threadIdx.x]) >> 2, (int64_t)kSortKeys - 1);
+      key = (int)min((s_off[threadIdx.x + 1] - s_off[threadIdx.x]) >> SCCG_PREP_SORT_SHIFT, (int64_t)kSortKeys - 1);
       key = max(key, 0);
       pos = atomicAdd(&s_cnt[key], 1);
     }
