@@ -47,11 +47,15 @@ __device__ __forceinline__ void set_entries(const SetStats* s, int k, int grow, 
 // caps on cells C and (upper-bounded) Q-entries.  Always feasible: once 2^k
 // exceeds the largest MBR extent each MBR covers at most 2 x 2 cells.
 __global__ void grid_select_kernel(const SetStats* __restrict__ sp, const SetStats* __restrict__ sq, long long ccap,
-                                   long long ecap, int grow, Grid* g) {
+                                   long long ecap, int grow, Grid* g, int4* __restrict__ zero, long long zero_n4) {
   pdl_trigger();
-  // one warp: lane j evaluates k = 3 + j (k <= 30), then an argmin over lanes
+  // every CTA clears its share of the cell counts (zero_n4 int4s) ...
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < zero_n4; i += (long long)gridDim.x * blockDim.x)
+    zero[i] = make_int4(0, 0, 0, 0);
+  // ... and CTA 0's first warp picks the cell size: lane j evaluates k = 3 + j
+  // (k <= 30), then an argmin over lanes
   const int lane = threadIdx.x & 31;
-  if (threadIdx.x >= 32) return;
+  if (blockIdx.x != 0 || threadIdx.x >= 32) return;
   const bool empty = sp->nonempty == 0 || sq->nonempty == 0;
   const int xmin = min(sp->bounds[0], sq->bounds[0]), ymin = min(sp->bounds[1], sq->bounds[1]);
   const int xmax = max(sp->bounds[2], sq->bounds[2]) + grow, ymax = max(sp->bounds[3], sq->bounds[3]) + grow;
@@ -663,12 +667,12 @@ static int filter_enqueue(const sccg_polyset* P, const sccg_polyset* Q, FilterWs
   const int4* mp = reinterpret_cast<const int4*>(P->mbr);
   const int4* mq = reinterpret_cast<const int4*>(Q->mbr);
   const int64_t C = cell_cap(np, nq), T = probe_tiles(np);
-  // 1. grid size from the prep statistics (device side), bucket Q (the count
-  // array is cleared first, so the bucketing chains onto the selection)
-  cudaMemsetAsync(w.cell_count, 0, sizeof(int) * (C + 1), stream);
-  grid_select_kernel<<<1, 32, 0, stream>>>(reinterpret_cast<const SetStats*>(P->stats),
-                                           reinterpret_cast<const SetStats*>(Q->stats), C, entry_cap(nq), grow,
-                                           w.grid);
+  // 1. grid size from the prep statistics (device side) and the count array
+  // cleared in the same launch; bucket Q (chained onto it by PDL)
+  const long long zero_n4 = (long long)((sizeof(int) * (C + 1) + 15) / 16);  // cell_count's slice is 256-B aligned
+  grid_select_kernel<<<(unsigned)blocks_for(zero_n4, 256), 256, 0, stream>>>(
+      reinterpret_cast<const SetStats*>(P->stats), reinterpret_cast<const SetStats*>(Q->stats), C, entry_cap(nq),
+      grow, w.grid, reinterpret_cast<int4*>(w.cell_count), zero_n4);
   if (nq > 0)
     launch_pdl(grid_bucket_kernel<false>, dim3(blocks_for(nq, 256)), dim3(256), 0, stream, mq, nq, w.grid,
                (const int*)nullptr, w.cell_count, (int*)nullptr, (int4*)nullptr, grow);

@@ -480,6 +480,12 @@ size_t pixelbox_ws_bytes(int64_t n) {
   return pixelbox_layout(n, cv, w) + 256;
 }
 
+__global__ void zero_counters_kernel(unsigned long long* queue, unsigned long long* ctr) {
+  pdl_trigger();
+  if (threadIdx.x < 4) queue[threadIdx.x] = 0ull;
+  else if (threadIdx.x < 8) ctr[threadIdx.x - 4] = 0ull;
+}
+
 int run_pixelbox(const sccg_polyset* p, const sccg_polyset* q, const int32_t* pairs, int64_t n,
                  const int64_t* dev_result, int64_t* inter, int64_t* uni, sccg_sums* sums, const sccg_config* cfg,
                  void* ws, size_t ws_bytes, cudaStream_t stream) {
@@ -497,14 +503,8 @@ int run_pixelbox(const sccg_polyset* p, const sccg_polyset* q, const int32_t* pa
   if (!lok) return set_error(SCCG_E_WORKSPACE, "pixelbox (large) workspace too small");
   // the small kernel's queue and the large path's counters: one memset when
   // they are neighbours in the workspace (they are: pixelbox_layout)
-  const char* qa = reinterpret_cast<const char*>(w.queue);
-  const char* ca = reinterpret_cast<const char*>(lw.ctr);
-  if (ca > qa && ca - qa <= 1024) {
-    cudaMemsetAsync(w.queue, 0, (size_t)(ca - qa) + 4 * sizeof(unsigned long long), stream);
-  } else {
-    cudaMemsetAsync(w.queue, 0, 4 * sizeof(unsigned long long), stream);
-    cudaMemsetAsync(lw.ctr, 0, 4 * sizeof(unsigned long long), stream);
-  }
+  // (a one-warp kernel, so the small kernel chains onto it by PDL)
+  zero_counters_kernel<<<1, 32, 0, stream>>>(w.queue, lw.ctr);
   if (n == 0) return check_cuda(cudaGetLastError(), "pixelbox");
   const bool count = cfg && cfg->counters;
   long long* counters = count ? reinterpret_cast<long long*>(cfg->counters) : nullptr;
@@ -528,13 +528,13 @@ int run_pixelbox(const sccg_polyset* p, const sccg_polyset* q, const int32_t* pa
   unsigned* hp = cfg ? reinterpret_cast<unsigned*>(cfg->hit_p) : nullptr;
   unsigned* hq = cfg ? reinterpret_cast<unsigned*>(cfg->hit_q) : nullptr;
   if (count)
-    small_kernel<true><<<(unsigned)grid_s, kSmallWarps * 32, 0, stream>>>(
-        Ps, Qs, pr, n, dr, in, un, sums, T, mode, use_raster, w.queue, lw, counters, hp, hq, p->n_polygons,
-        q->n_polygons);
+    launch_pdl(small_kernel<true>, dim3((unsigned)grid_s), dim3(kSmallWarps * 32), 0, stream, Ps, Qs, pr, (long long)n,
+               dr, in, un, sums, T, mode, use_raster, w.queue, lw, counters, hp, hq, (long long)p->n_polygons,
+               (long long)q->n_polygons);
   else
-    small_kernel<false><<<(unsigned)grid_s, kSmallWarps * 32, 0, stream>>>(
-        Ps, Qs, pr, n, dr, in, un, sums, T, mode, use_raster, w.queue, lw, nullptr, hp, hq, p->n_polygons,
-        q->n_polygons);
+    launch_pdl(small_kernel<false>, dim3((unsigned)grid_s), dim3(kSmallWarps * 32), 0, stream, Ps, Qs, pr,
+               (long long)n, dr, in, un, sums, T, mode, use_raster, w.queue, lw, (long long*)nullptr, hp, hq,
+               (long long)p->n_polygons, (long long)q->n_polygons);
   if (int r = check_cuda(cudaGetLastError(), "pixelbox small launch")) return r;
   const int dense = !(cfg && (cfg->flags & SCCG_FLAG_PAPER_SPLIT));
   return launch_large(Ps, Qs, pr, lw, in, un, sums, T, mode, dense, counters, hp, hq, stream);
