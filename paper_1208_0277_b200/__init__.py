@@ -287,7 +287,8 @@ class Pipeline:
     """A device-resident, host-sync-free cross-comparison step for fixed sets:
     prep(P), prep(Q), MBR join and PixelBox enqueued back to back on one stream
     (sccg_filter_pairs_async / sccg_pixelbox_async: the pair count never leaves
-    the GPU), so the whole step can be captured and replayed as a CUDA graph.
+    the GPU), so the whole step is captured and replayed as ONE CUDA graph
+    (and as three stage graphs, used when run() is asked for stage events).
     ``run()`` returns the device sums vector; read it (one sync) for J'."""
 
     def __init__(self, P: "DeviceSet", Q: "DeviceSet", cap: int | None = None, threshold: int = 0, graph: bool = True,
@@ -335,6 +336,17 @@ class Pipeline:
                 with torch.cuda.graph(g):
                     self._enqueue_pixelbox()
                 self._pix_rb.append(g)
+            # the whole step as ONE graph (per read-back slot): no graph-to-graph
+            # gaps, and the stages chain by programmatic dependent launch too;
+            # run() uses it whenever no per-stage events are asked for
+            self._full = []
+            for k in range(max(1, len(self.readback))):
+                self._slot = k
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g):
+                    for stage in self._stages:
+                        stage()
+                self._full.append(g)
 
     @property
     def _stages(self):
@@ -367,6 +379,9 @@ class Pipeline:
         sums also land in readback[slot] (read them after an event recorded
         after run() has completed)."""
         self._slot = slot
+        if self.graphs is not None and not events:
+            self._full[slot if self.readback else 0].replay()
+            return self.sums
         for k, stage in enumerate(self._stages):
             if events:
                 events[k].record()

@@ -52,6 +52,7 @@ __global__ void grid_select_kernel(const SetStats* __restrict__ sp, const SetSta
   // every CTA clears its share of the cell counts (zero_n4 int4s) ...
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < zero_n4; i += (long long)gridDim.x * blockDim.x)
     zero[i] = make_int4(0, 0, 0, 0);
+  pdl_wait();  // prep's statistics (and, for what follows, everything before)
   // ... and CTA 0's first warp picks the cell size: lane j evaluates k = 3 + j
   // (k <= 30), then an argmin over lanes
   const int lane = threadIdx.x & 31;
@@ -670,9 +671,9 @@ static int filter_enqueue(const sccg_polyset* P, const sccg_polyset* Q, FilterWs
   // 1. grid size from the prep statistics (device side) and the count array
   // cleared in the same launch; bucket Q (chained onto it by PDL)
   const long long zero_n4 = (long long)((sizeof(int) * (C + 1) + 15) / 16);  // cell_count's slice is 256-B aligned
-  grid_select_kernel<<<(unsigned)blocks_for(zero_n4, 256), 256, 0, stream>>>(
-      reinterpret_cast<const SetStats*>(P->stats), reinterpret_cast<const SetStats*>(Q->stats), C, entry_cap(nq),
-      grow, w.grid, reinterpret_cast<int4*>(w.cell_count), zero_n4);
+  launch_pdl(grid_select_kernel, dim3((unsigned)blocks_for(zero_n4, 256)), dim3(256), 0, stream,
+             reinterpret_cast<const SetStats*>(P->stats), reinterpret_cast<const SetStats*>(Q->stats), (long long)C,
+             (long long)entry_cap(nq), grow, w.grid, reinterpret_cast<int4*>(w.cell_count), zero_n4);
   if (nq > 0)
     launch_pdl(grid_bucket_kernel<false>, dim3(blocks_for(nq, 256)), dim3(256), 0, stream, mq, nq, w.grid,
                (const int*)nullptr, w.cell_count, (int*)nullptr, (int4*)nullptr, grow);

@@ -482,6 +482,7 @@ size_t pixelbox_ws_bytes(int64_t n) {
 
 __global__ void zero_counters_kernel(unsigned long long* queue, unsigned long long* ctr) {
   pdl_trigger();
+  pdl_wait();  // the small kernel chains onto this one: its completion must imply the join's
   if (threadIdx.x < 4) queue[threadIdx.x] = 0ull;
   else if (threadIdx.x < 8) ctr[threadIdx.x - 4] = 0ull;
 }
@@ -504,7 +505,7 @@ int run_pixelbox(const sccg_polyset* p, const sccg_polyset* q, const int32_t* pa
   // the small kernel's queue and the large path's counters: one memset when
   // they are neighbours in the workspace (they are: pixelbox_layout)
   // (a one-warp kernel, so the small kernel chains onto it by PDL)
-  zero_counters_kernel<<<1, 32, 0, stream>>>(w.queue, lw.ctr);
+  launch_pdl(zero_counters_kernel, dim3(1), dim3(32), 0, stream, w.queue, lw.ctr);
   if (n == 0) return check_cuda(cudaGetLastError(), "pixelbox");
   const bool count = cfg && cfg->counters;
   long long* counters = count ? reinterpret_cast<long long*>(cfg->counters) : nullptr;
