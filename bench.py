@@ -369,9 +369,10 @@ def run_ours(args, rank, world, local_rank):
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
     alu_peak = sms * ALU_LANES_PER_CLK_SM * peak_mhz * 1e6 / 1e9
     issue = pixelbox_issue(args.config, pix_s, sms, clocks)
-    # our kernels per step: prep init + prep, join 6 (incl. CUB scan x2), pixelbox 2, + the sums read-back
-    # kernel on one GPU (profiles/r01/launches_slide_summary.txt)
-    launches_per_step = 11 + (1 if world == 1 else 0)
+    # our kernels per step: prep init + prep, join 6 (grid selection, count, CUB scan x2, fill, probe, compaction
+    # -- 7), PixelBox 3 (counter reset, small, item), + the sums read-back kernel on one GPU
+    # (profiles/r01/launches_slide_summary.txt)
+    launches_per_step = 12 + (1 if world == 1 else 0)
     out = {
         "metric": METRIC,
         "value": value,
