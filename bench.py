@@ -499,7 +499,7 @@ def main():
             dist.init_process_group(backend)
     out = run_ours(args, rank, world, local_rank)
     if rank == 0:
-        if not args.no_cpu_baseline:
+        if not args.no_cpu_baseline and world == 1:  # the oracle baseline: rank 0 at N = 1 only
             out["cpu_baseline"] = cpu_baseline(args.config, 0)
         line = json.dumps(out)
         print(line)
