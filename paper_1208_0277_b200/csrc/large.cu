@@ -83,42 +83,78 @@ __device__ bool build_local(const PolyRef& c, int X0, int Y0, int X1, int Y1, Lo
   const unsigned lt = lanemask_lt();
   const int Wr = X1 - X0, Hr = Y1 - Y0;
   int par = 0, cnt = 0;
-  for (int j0 = 0; j0 < c.nv; j0 += 32) {
-    const int j = j0 + lane;
-    bool keep = false;
-    uint64_t rec = 0;
-    if (j < c.nv) {
-      int cc, lo, hi;
-      unpack_edge(__ldg(c.ev + j), cc, lo, hi);
-      const int x = cc + c.dx, yl = lo + c.dy, yh = hi + c.dy;
-      par ^= (x > X0 && yl <= Y0 && Y0 < yh) ? 1 : 0;  // ray from (X0 + 1/2, Y0 + 1/2) toward +x
-      keep = x > X0 && x < X1 && yl < Y1 && yh > Y0;
-      rec = pack_loc(x - X0, max(yl - Y0, -1), min(yh - Y0, Hr + 1));
+  // records / vertices are read four 32-wide groups at a time (all loads in
+  // flight before any is used: this culling re-reads both rings per region
+  // item, and on comb pairs it is the kernel's main memory stall)
+  for (int j00 = 0; j00 < c.nv; j00 += 128) {
+    uint64_t rr[4];
+#pragma unroll
+    for (int u = 0; u < 4; u++) {
+      const int j = j00 + 32 * u + lane;
+      rr[u] = j < c.nv ? __ldg(c.ev + j) : 0ull;
     }
-    const unsigned b = __ballot_sync(FULL, keep);
-    const int pos = cnt + __popc(b & lt);
-    if (keep && pos < kLCap) L.V[pos] = rec;
-    cnt += __popc(b);
+#pragma unroll
+    for (int u = 0; u < 4; u++) {
+      const int j0 = j00 + 32 * u;
+      if (j0 >= c.nv) break;  // warp-uniform
+      const int j = j0 + lane;
+      bool keep = false;
+      uint64_t rec = 0;
+      if (j < c.nv) {
+        int cc, lo, hi;
+        unpack_edge(rr[u], cc, lo, hi);
+        const int x = cc + c.dx, yl = lo + c.dy, yh = hi + c.dy;
+        par ^= (x > X0 && yl <= Y0 && Y0 < yh) ? 1 : 0;  // ray from (X0 + 1/2, Y0 + 1/2) toward +x
+        keep = x > X0 && x < X1 && yl < Y1 && yh > Y0;
+        rec = pack_loc(x - X0, max(yl - Y0, -1), min(yh - Y0, Hr + 1));
+      }
+      const unsigned b = __ballot_sync(FULL, keep);
+      const int pos = cnt + __popc(b & lt);
+      if (keep && pos < kLCap) L.V[pos] = rec;
+      cnt += __popc(b);
+    }
   }
   L.nV = cnt;
   L.pi = __reduce_xor_sync(FULL, (unsigned)par) & 1;
   cnt = 0;
-  for (int j0 = 0; j0 < c.V; j0 += 32) {
-    const int j = j0 + lane;
-    bool keep = false;
-    uint64_t rec = 0;
-    if (j < c.V) {
-      const int2 a = __ldg(c.v + j), b2 = __ldg(c.v + (j + 1 == c.V ? 0 : j + 1));
-      if (a.y == b2.y && a.x != b2.x) {
-        const int f = a.y - c.oy, xl = min(a.x, b2.x) - c.ox, xh = max(a.x, b2.x) - c.ox;
-        keep = f > Y0 && f < Y1 && xl < X1 && xh > X0;
-        rec = pack_loc(f - Y0, max(xl - X0, -1), min(xh - X0, Wr + 1));
-      }
+  const int2 first = c.V > 0 ? __ldg(c.v) : make_int2(0, 0);
+  for (int j00 = 0; j00 < c.V; j00 += 128) {
+    int2 av[4];
+#pragma unroll
+    for (int u = 0; u < 4; u++) {
+      const int j = j00 + 32 * u + lane;
+      av[u] = j < c.V ? __ldg(c.v + j) : make_int2(0, 0);
     }
-    const unsigned b = __ballot_sync(FULL, keep);
-    const int pos = cnt + __popc(b & lt);
-    if (keep && pos < kLCap) L.H[pos] = rec;
-    cnt += __popc(b);
+    const int2 tail = j00 + 128 < c.V ? __ldg(c.v + j00 + 128) : first;  // the vertex after this block
+#pragma unroll
+    for (int u = 0; u < 4; u++) {
+      const int j0 = j00 + 32 * u;
+      if (j0 >= c.V) break;  // warp-uniform
+      const int j = j0 + lane;
+      // the edge from vertex j to j + 1: the next vertex is the next lane's
+      int2 b2;
+      b2.x = __shfl_down_sync(FULL, av[u].x, 1);
+      b2.y = __shfl_down_sync(FULL, av[u].y, 1);
+      const int2 nxt = u < 3 ? make_int2(__shfl_sync(FULL, av[u < 3 ? u + 1 : u].x, 0),
+                                         __shfl_sync(FULL, av[u < 3 ? u + 1 : u].y, 0))
+                             : tail;
+      if (lane == 31) b2 = nxt;
+      if (j + 1 == c.V) b2 = first;  // the ring closes
+      bool keep = false;
+      uint64_t rec = 0;
+      if (j < c.V) {
+        const int2 a = av[u];
+        if (a.y == b2.y && a.x != b2.x) {
+          const int f = a.y - c.oy, xl = min(a.x, b2.x) - c.ox, xh = max(a.x, b2.x) - c.ox;
+          keep = f > Y0 && f < Y1 && xl < X1 && xh > X0;
+          rec = pack_loc(f - Y0, max(xl - X0, -1), min(xh - X0, Wr + 1));
+        }
+      }
+      const unsigned b = __ballot_sync(FULL, keep);
+      const int pos = cnt + __popc(b & lt);
+      if (keep && pos < kLCap) L.H[pos] = rec;
+      cnt += __popc(b);
+    }
   }
   L.nH = cnt;
   return L.nV <= kLCap && L.nH <= kLCap;
