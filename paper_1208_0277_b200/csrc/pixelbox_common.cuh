@@ -82,7 +82,10 @@ __device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long v)
 // large list) always holds region 0; the other regions are appended after
 // n_cap.  rem[i] counts the pair's unfinished items; acc[i] accumulates its
 // pixel count.
-constexpr int kRegion = 128;       // target region side
+#ifndef SCCG_REGION
+#define SCCG_REGION 128
+#endif
+constexpr int kRegion = SCCG_REGION;  // target region side
 constexpr int kMaxSplit = 32;      // regions per axis at most
 constexpr int kMaxRegion = 32766;  // local coordinates are 15-bit (plus clamp margin)
 
