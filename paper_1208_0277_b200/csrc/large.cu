@@ -76,6 +76,11 @@ struct LocalPoly {
   int pi;       // parity of the region's corner pixel (1 = inside)
 };
 
+#ifndef SCCG_CULL_GROUPS
+#define SCCG_CULL_GROUPS 4
+#endif
+constexpr int kCullGroups = SCCG_CULL_GROUPS;  // 32-wide load groups in flight in the culling loops
+
 // Cull one polygon's edges to region R = [X0, X1) x [Y0, Y1) (root coords)
 // and cast the corner ray.  Returns false if a list overflows.
 __device__ bool build_local(const PolyRef& c, int X0, int Y0, int X1, int Y1, LocalPoly& L) {
@@ -86,15 +91,15 @@ __device__ bool build_local(const PolyRef& c, int X0, int Y0, int X1, int Y1, Lo
   // records / vertices are read four 32-wide groups at a time (all loads in
   // flight before any is used: this culling re-reads both rings per region
   // item, and on comb pairs it is the kernel's main memory stall)
-  for (int j00 = 0; j00 < c.nv; j00 += 128) {
-    uint64_t rr[4];
+  for (int j00 = 0; j00 < c.nv; j00 += 32 * kCullGroups) {
+    uint64_t rr[kCullGroups];
 #pragma unroll
-    for (int u = 0; u < 4; u++) {
+    for (int u = 0; u < kCullGroups; u++) {
       const int j = j00 + 32 * u + lane;
       rr[u] = j < c.nv ? __ldg(c.ev + j) : 0ull;
     }
 #pragma unroll
-    for (int u = 0; u < 4; u++) {
+    for (int u = 0; u < kCullGroups; u++) {
       const int j0 = j00 + 32 * u;
       if (j0 >= c.nv) break;  // warp-uniform
       const int j = j0 + lane;
@@ -118,16 +123,16 @@ __device__ bool build_local(const PolyRef& c, int X0, int Y0, int X1, int Y1, Lo
   L.pi = __reduce_xor_sync(FULL, (unsigned)par) & 1;
   cnt = 0;
   const int2 first = c.V > 0 ? __ldg(c.v) : make_int2(0, 0);
-  for (int j00 = 0; j00 < c.V; j00 += 128) {
-    int2 av[4];
+  for (int j00 = 0; j00 < c.V; j00 += 32 * kCullGroups) {
+    int2 av[kCullGroups];
 #pragma unroll
-    for (int u = 0; u < 4; u++) {
+    for (int u = 0; u < kCullGroups; u++) {
       const int j = j00 + 32 * u + lane;
       av[u] = j < c.V ? __ldg(c.v + j) : make_int2(0, 0);
     }
-    const int2 tail = j00 + 128 < c.V ? __ldg(c.v + j00 + 128) : first;  // the vertex after this block
+    const int2 tail = j00 + 32 * kCullGroups < c.V ? __ldg(c.v + j00 + 32 * kCullGroups) : first;  // the next block's first
 #pragma unroll
-    for (int u = 0; u < 4; u++) {
+    for (int u = 0; u < kCullGroups; u++) {
       const int j0 = j00 + 32 * u;
       if (j0 >= c.V) break;  // warp-uniform
       const int j = j0 + lane;
@@ -135,9 +140,9 @@ __device__ bool build_local(const PolyRef& c, int X0, int Y0, int X1, int Y1, Lo
       int2 b2;
       b2.x = __shfl_down_sync(FULL, av[u].x, 1);
       b2.y = __shfl_down_sync(FULL, av[u].y, 1);
-      const int2 nxt = u < 3 ? make_int2(__shfl_sync(FULL, av[u < 3 ? u + 1 : u].x, 0),
-                                         __shfl_sync(FULL, av[u < 3 ? u + 1 : u].y, 0))
-                             : tail;
+      const int2 nxt = u < kCullGroups - 1 ? make_int2(__shfl_sync(FULL, av[u < kCullGroups - 1 ? u + 1 : u].x, 0),
+                                                       __shfl_sync(FULL, av[u < kCullGroups - 1 ? u + 1 : u].y, 0))
+                                           : tail;
       if (lane == 31) b2 = nxt;
       if (j + 1 == c.V) b2 = first;  // the ring closes
       bool keep = false;
