@@ -40,6 +40,10 @@ SMS_B200 = 148
 ISSUE_LANES_PER_CLK_SM = 128  # 4 SMSPs x 1 warp-instruction x 32 lanes (nominal dispatch)
 ALU_LANES_PER_CLK_SM = 64  # measured: ALU pipe 2 warp-inst/clk/SM (profiles/int_peak.json, scripts/int_peak.cu)
 STAGE_EVERY = 10  # per-stage CUDA events on every 10th timed step
+# our kernels per step besides the read-back (one GPU) or the sums pack + unpack around the all-reduce (N > 1):
+# sums reset, prep init, prep, join (grid selection, Q count, Q fill, probe, compaction; CUB's two scan kernels
+# are not counted), PixelBox (counter reset, small, item)
+LAUNCHES_PER_STEP = 11
 OPS_PER_ROWTEST = 3  # sub, unsigned compare, predicated xor
 OPS_PER_BOXEDGE = 8  # one lane classifying one edge against all sub-boxes of a split (minimum)
 
@@ -127,22 +131,34 @@ def prep_algorithmic_bytes(sccg, S) -> int:
     return 8 * S.nv + 8 * (S.n + 1) + 32 * S.n + 8 * int(ec[:, 0].sum()) + 4 * rows
 
 
-def pixelbox_issue(config, pix_s, sms, clocks):
+def lib_digest() -> str:
+    """sha256 prefix of the loaded libsccg.so: static profile numbers
+    (profiles/issue_counts.json) apply only to the library they were taken on."""
+    import hashlib
+
+    import paper_1208_0277_b200 as sccg
+
+    with open(sccg.library_path(), "rb") as f:
+        return hashlib.sha256(f.read()).hexdigest()[:16]
+
+
+def pixelbox_issue(key, pix_s, sms, clocks):
     """PixelBox warp-instruction issue rate against the measured integer-issue
     peak: ncu's instruction count of the small kernel for this
-    workload (profiles/issue_counts.json; fixed by the workload) over the live
-    PixelBox stage time (CUDA events; includes the item kernel and the graph
-    launch, so the rate is a lower bound).  Peak = the best integer mix of the
-    microbenchmark (profiles/int_peak.json, LOP3 + IMAD on the ALU and FMA
-    pipes) x SMs x the SM clock sampled during the run."""
+    exact workload key (config/shard/world; profiles/issue_counts.json, taken on
+    the same library build -- otherwise None) over the live PixelBox stage time
+    (CUDA events; includes the item kernel and the graph launch, so the rate is
+    a lower bound).  Peak = the best integer mix of the microbenchmark
+    (profiles/int_peak.json, LOP3 + IMAD on the ALU and FMA pipes) x SMs x the
+    SM clock sampled during the run."""
     try:
         with open(os.path.join(ROOT, "profiles", "issue_counts.json")) as f:
-            counts = json.load(f).get(config)
+            counts = json.load(f).get(key)
         with open(os.path.join(ROOT, "profiles", "int_peak.json")) as f:
             ip = json.load(f)
     except Exception:
         return None
-    if not counts or "small_kernel" not in counts:
+    if not counts or "small_kernel" not in counts or counts.get("lib") != lib_digest():
         return None
     best = max(r["warp_inst_per_clk_per_sm"] for r in ip["results"])
     alu = max(r["warp_inst_per_clk_per_sm"] for r in ip["results"] if r["pipe"] == "alu")
@@ -151,10 +167,30 @@ def pixelbox_issue(config, pix_s, sms, clocks):
     peak = best * sms * mhz * 1e6
     return {"achieved": achieved, "peak": peak, "unit": "warp-inst/s", "frac": achieved / peak,
             "frac_of_nominal_issue": achieved / (4 * sms * mhz * 1e6),
-            "warp_inst_per_launch": counts["small_kernel"], "kernel": "small_kernel",
+            "warp_inst_per_launch": counts["small_kernel"], "kernel": "small_kernel", "key": key,
             "peak_source": f"measured integer mix {best:.3f} warp-inst/clk/SM (ALU pipe alone {alu:.3f}; "
                            f"profiles/int_peak.json) x {sms} SMs x {mhz:.0f} MHz",
-            "count_source": "ncu smsp__inst_executed.sum (profiles/issue_counts.json) / live stage time"}
+            "count_source": "ncu smsp__inst_executed.sum (profiles/issue_counts.json, same library) / live stage time"}
+
+
+def pixelbox_algorithmic_bytes(sccg, P, Q, pairs) -> int:
+    """Bytes the PixelBox stage must move for this pair list:
+    per pair its index pair (8 B) and outputs (16 B), both polygons' MBR (16 B),
+    area (8 B), ecount (8 B) and offset (8 B), and -- when both rings carry a
+    raster -- the box's rows of both rasters (4 B each), else both rings'
+    vertical-edge data (8 B per vertex slot used).  Computed with torch on the
+    device, untimed."""
+    import torch
+
+    pr = pairs.long()
+    p, q = pr[:, 0], pr[:, 1]
+    mp, mq = P.mbr.long()[p], Q.mbr.long()[q]
+    H = (torch.minimum(mp[:, 3], mq[:, 3]) - torch.maximum(mp[:, 1], mq[:, 1])).clamp(min=0)
+    ep, eq = P.ecount.long()[p], Q.ecount.long()[q]
+    rast = ((ep[:, 1] & sccg.RASTER_FLAG) != 0) & ((eq[:, 1] & sccg.RASTER_FLAG) != 0)
+    edge = 8 * (ep[:, 0] + eq[:, 0])
+    per = 24 + 2 * 40 + torch.where(rast, 8 * H, edge)
+    return int(per.sum())
 
 
 def hbm_peak():
@@ -190,6 +226,56 @@ def config_desc(config):
 
 
 # -------------------------------------------------------------- our arm
+def self_check(args, A, B, pipe, n_local, local_sums, threads):
+    """The benched step checks itself (rank-local, before any all-reduce): the
+    pair list, EVERY pair's (I, U) written by the step, the integer sums, the
+    exact ratio limbs and J' must equal the oracle's on the same workload
+    (oracle/, all host threads; the combs workload -- too slow for a full
+    oracle pass -- on a seeded 32-pair sample plus the size-free identities).
+    Raises on any mismatch.  Returns (summary, the oracle pass or None)."""
+    import numpy as np
+
+    import oracle
+
+    if local_sums[10] != 0:
+        raise RuntimeError(f"self-check: sums status bits {local_sums[10]:#x}")
+    pairs = pipe.pairs[:n_local].cpu().numpy()
+    gi = pipe.inter[:n_local].cpu().numpy()
+    gu = pipe.uni[:n_local].cpu().numpy()
+    units = sum(int(v) << (30 * k) for k, v in enumerate(local_sums[6:10]))
+    if args.config == "combs":
+        idx = np.sort(np.random.default_rng(7).choice(n_local, size=min(32, n_local), replace=False))
+        ei, eu = oracle.pair_areas(A, B, pairs[idx], threads=threads)
+        if not ((ei == gi[idx]).all() and (eu == gu[idx]).all()):
+            raise RuntimeError("self-check: sampled pairs differ from the oracle")
+        ap, _ = oracle.set_props(A)
+        aq, _ = oracle.set_props(B)
+        if not (gi + gu == ap[pairs[:, 0]] + aq[pairs[:, 1]]).all() or local_sums[2] != int(gi.sum()):
+            raise RuntimeError("self-check: size-free identities fail")
+        return {"oracle": "32 sampled pairs + identities", "pairs_checked": int(len(idx))}, None
+    ref = oracle_pass(A, B, threads)
+    if pairs.shape != ref["pairs"].shape or not (pairs == ref["pairs"]).all():
+        raise RuntimeError("self-check: pair list differs from the oracle's join")
+    bad = np.nonzero((gi != ref["inter"]) | (gu != ref["uni"]))[0]
+    if len(bad):
+        raise RuntimeError(f"self-check: {len(bad)} pairs differ from the oracle, first {bad[:5].tolist()}")
+    o = ref["sums"]
+    want = [o["n_pairs"], o["n_nonzero"], o["sum_inter"], o["sum_union"], o["sum_area_p"], o["sum_area_q"]]
+    if local_sums[:6] != want or units != ref["units"]:
+        raise RuntimeError(f"self-check: sums {local_sums} differ from the oracle's {want} / units")
+    rel = None
+    if ref["jprime_exact"] is not None:
+        import paper_1208_0277_b200 as sccg
+
+        j, _ = sccg.jaccard(local_sums)
+        ex = float(ref["jprime_exact"])
+        rel = abs(j - ex) / ex
+        if rel > 1e-12:
+            raise RuntimeError(f"self-check: J' {j} vs exact {ex}")
+    return {"oracle": "full pass (join, all pairs' I and U, sums, limbs, J')", "pairs_checked": int(n_local),
+            "jprime_rel_err_vs_exact": rel, "oracle_seconds": ref["seconds"], "oracle_threads": threads}, ref
+
+
 def run_ours(args, rank, world, local_rank):
     import numpy as np
     import torch
@@ -226,23 +312,32 @@ def run_ours(args, rank, world, local_rank):
     P = sccg.DeviceSet(d_xy_p, d_off_p, prep=False)
     Q = sccg.DeviceSet(d_xy_q, d_off_q, prep=False)
     stream = torch.cuda.current_stream()
-    # the whole step (prep x2, join, PixelBox) device-resident, no host sync until
-    # the sums are read; replayed as two CUDA graphs (join | PixelBox)
-    # Steps are pipelined on the host: step i+1 is enqueued before step i's
-    # sums are read (the read-back is in-stream into one of two pinned
-    # buffers), so the GPU never idles on the host's per-step read-back; every
-    # step's result is still read and checked.  One GPU: the PixelBox graph
-    # ends with sccg_sums_copy into the pinned buffer (the GPU writes it, no
-    # copy-engine transfer).  N > 1: all_reduce first, then the copy.
+    # The whole step (prep x2, join, PixelBox with the per-pair outputs) is
+    # device-resident with no host sync until the sums are read, replayed as
+    # ONE CUDA graph.  Steps are pipelined on the host: step i+1 is enqueued
+    # before step i's sums are read (the read-back is in-stream into one of two
+    # pinned buffers), so the GPU never idles on the host's per-step read-back;
+    # every step's result is still read and checked.  One GPU: the PixelBox
+    # graph ends with sccg_sums_copy into the pinned buffer (the GPU writes it,
+    # no copy-engine transfer).  N > 1: all_reduce first, then the copy.
     host_bufs = [torch.zeros(len(sccg.SUMS_FIELDS), dtype=torch.int64).pin_memory() for _ in range(2)]
     done_ev = [torch.cuda.Event() for _ in range(2)]
-    pipe = sccg.Pipeline(P, Q, cap=3 * max(P.n, Q.n) + 1024, threshold=args.threshold, graph=True,
+    cap = 3 * max(P.n, Q.n) + 1024
+    pipe = sccg.Pipeline(P, Q, cap=cap, threshold=args.threshold, graph=True,
                          readback=host_bufs if world == 1 else ())
+    threads = max(1, (os.cpu_count() or 1) // world)
+
+    # ---- self-check of the benched step against the oracle (rank-local, before any all-reduce)
+    pipe.run(slot=0)
+    torch.cuda.synchronize()
+    n_local = pipe.check()  # raises on a pair-buffer overflow or any device status bit
+    local = [int(v) for v in pipe.sums.tolist()]
+    check, ref_pass = self_check(args, A, B, pipe, n_local, local, threads)
 
     def enqueue(i, events=None):
         sums = pipe.run(events, slot=i % 2)
         if world > 1:
-            sdist.allreduce_sums(sums)  # row a9: the only collective (NCCL, int64 SUM)
+            sdist.allreduce_sums(sums)  # row a9: the only collective (NCCL, int64 SUM of the packed vector)
             host_bufs[i % 2].copy_(sums, non_blocking=True)
         done_ev[i % 2].record()
 
@@ -253,12 +348,14 @@ def run_ours(args, rank, world, local_rank):
     for i in range(max(args.warmup, 3)):
         enqueue(i)
         first = collect(i)
-    n_local = pipe.check()
+    if world == 1 and [getattr(first, f) for f in sccg.SUMS_FIELDS] != local:
+        raise RuntimeError("warm-up sums differ from the checked step's")
     # one untimed counting run for the algorithmic work per launch
     counters = torch.zeros(8, dtype=torch.int64, device=dev)
     sccg.pixelbox(P, Q, pipe.pairs[:n_local], threshold=args.threshold, counters=counters, want_inter=False,
                   want_union=False)
     cnt = counters.cpu().tolist()
+    pix_alg = pixelbox_algorithmic_bytes(sccg, P, Q, pipe.pairs[:n_local])
 
     # ---- timed region: K steps, barrier + synchronize on both sides
     t0 = torch.cuda.Event(enable_timing=True)
@@ -287,9 +384,12 @@ def run_ours(args, rank, world, local_rank):
     host = results[-1]
     if any(bytes(r) != bytes(first) for r in results):
         raise RuntimeError("a timed step's sums differ from the warm-up's (nondeterminism)")
+    if any(int(r.status) for r in results):
+        raise RuntimeError("a timed step's sums carry device status bits")
     if world > 1:
         dist.barrier()
-    pipe.check()
+    if pipe.check() != n_local:
+        raise RuntimeError("pair count changed between steps")
     ms = t0.elapsed_time(t1)
     times = torch.tensor([ms] + [t / len(sampled) for t in stage_ms] + [float(n_local)], dtype=torch.float64,
                          device=dev)
@@ -303,7 +403,6 @@ def run_ours(args, rank, world, local_rank):
     ms_max, prep_ms_max, join_ms_max, pix_ms_max = (float(v) for v in mx[:4])
     total_pairs = int(round(float(tot[4])))
     jprime, pooled = sccg.jaccard(host)
-    state = {"cap": 3 * max(P.n, Q.n) + 1024}
 
     # ---- e2e: public API from pinned host buffers, H2D + D2H inside the timed region
     e2e_steps = max(1, min(args.e2e_steps, args.steps))
@@ -317,12 +416,12 @@ def run_ours(args, rank, world, local_rank):
         d = off_q.to(dev, non_blocking=True)
         Pe = sccg.DeviceSet(a, b)
         Qe = sccg.DeviceSet(c, d)
-        pr = sccg.filter_pairs(Pe, Qe, cap=state["cap"])
+        pr = sccg.filter_pairs(Pe, Qe, cap=cap)
         s = sccg.new_sums(dev)
-        sccg.pixelbox(Pe, Qe, pr, threshold=args.threshold, sums=s, want_inter=False, want_union=False)
+        sccg.pixelbox(Pe, Qe, pr, threshold=args.threshold, sums=s, want_inter=False, want_union=False, check=False)
         if world > 1:
-            dist.all_reduce(s, op=dist.ReduceOp.SUM)
-        return sccg.jaccard(s.cpu())
+            sdist.allreduce_sums(s)
+        return sccg.jaccard(s.cpu())  # raises on device status bits
 
     e2e_step()
     if world > 1:
@@ -332,16 +431,18 @@ def run_ours(args, rank, world, local_rank):
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(e2e_steps):
-        e2e_step()
+        je, _ = e2e_step()
     e1.record(stream)
     torch.cuda.synchronize()
+    if not (je == jprime or (math.isnan(je) and math.isnan(jprime))):
+        raise RuntimeError("e2e J' differs from the device-resident step's")
     e_ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
     e2e_value = total_pairs * e2e_steps / (float(e_ms[0]) / 1e3)
 
     if rank != 0:
-        return None
+        return None, None
     value = total_pairs * args.steps / (ms_max / 1e3)
     clocks = clk.summary()
     # roofline of the dominant kernel: prep (HBM-bound; one launch preps both
@@ -358,7 +459,7 @@ def run_ours(args, rank, world, local_rank):
         try:
             with open(prof) as f:
                 pj = json.load(f)
-            if pj.get("config") == args.config:
+            if pj.get("config") == args.config and pj.get("lib") == lib_digest() and world == 1:
                 traffic = pj.get("dram_bytes_per_launch")
         except Exception:
             traffic = None
@@ -368,11 +469,12 @@ def run_ours(args, rank, world, local_rank):
     peak_mhz = clocks["sm_max_mhz"] or 1965.0
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
     alu_peak = sms * ALU_LANES_PER_CLK_SM * peak_mhz * 1e6 / 1e9
-    issue = pixelbox_issue(args.config, pix_s, sms, clocks)
-    # our kernels per step: prep init + prep, join 6 (grid selection, count, CUB scan x2, fill, probe, compaction
-    # -- 7), PixelBox 3 (counter reset, small, item), + the sums read-back kernel on one GPU
-    # (profiles/r01/launches_slide_summary.txt)
-    launches_per_step = 12 + (1 if world == 1 else 0)
+    issue = pixelbox_issue(f"{args.config}/{args.shard if world > 1 else 'image'}/{world}", pix_s, sms, clocks)
+    # our kernels per step (profiles/<round>/launches_slide_summary.txt)
+    launches_per_step = LAUNCHES_PER_STEP + (1 if world == 1 else 2)
+    cfg = workload_config(args.config, A, B, n_local, world, args.shard)
+    cfg.update({"pairs_total": total_pairs, "threshold_T": args.threshold or 2048,
+                "l2": "inputs larger than L2 (vertex arrays ~%d MB per rank > 126 MB)" % ((P.nv + Q.nv) * 8 // 2**20)})
     out = {
         "metric": METRIC,
         "value": value,
@@ -387,27 +489,22 @@ def run_ours(args, rank, world, local_rank):
         "dtype": "int32",
         "data": "synthetic (seeded generator synth/, nucleus polygons per PAPER.md §5.1)",
         "impl": "ours",
-        "config": {
-            "workload": args.config,
-            "description": config_desc(args.config),
-            "pairs_per_gpu": n_local,
-            "pairs_total": total_pairs,
-            "polygons_p": P.n, "polygons_q": Q.n, "vertices_p": P.nv, "vertices_q": Q.nv,
-            "threshold_T": args.threshold or 2048,
-            "l2": "inputs larger than L2 (vertex + edge-record arrays ~%d MB per rank > 126 MB)" % (
-                (P.nv + Q.nv) * 16 // 2**20),
-            "parallelism": (f"{args.shard}-sharded x{world}" if world > 1 else "1 GPU"),
-        },
+        "config": cfg,
         "pixels_tested_per_s": cnt[sccg.CNT_PIXELS] * world / pix_s,
         "stage_ms": {"prep": prep_ms_max, "join": join_ms_max, "pixelbox": pix_ms_max,
                      "sampled_steps": len(sampled), "every": STAGE_EVERY},
         "jprime": jprime,
         "pooled_jaccard": pooled,
+        "self_check": check,
         "counters": {"pixels": cnt[0], "rowtests": cnt[1], "boxes": cnt[2], "boxedges": cnt[3], "splits": cnt[4],
                      "pixboxes": cnt[5], "rootpx": cnt[6]},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "kernel": "prep_kernel (P and Q in one launch)", "algorithmic_bytes_per_launch": alg,
                      "peak_source": peak_src},
+        "pixelbox_hbm": {"achieved": pix_alg / pix_s / 1e9, "peak": peak, "unit": "GB/s",
+                         "frac": pix_alg / pix_s / 1e9 / peak, "algorithmic_bytes_per_step": pix_alg,
+                         "note": "PixelBox stage (small + item kernels): pair list, per-polygon metadata, raster rows "
+                                 "or edge records, per-pair outputs (bench.py pixelbox_algorithmic_bytes)"},
         "pixelbox_alu": {"achieved": ops / pix_s / 1e9, "peak": alu_peak, "unit": "Gop/s",
                          "frac": ops / pix_s / 1e9 / alu_peak,
                          "peak_source": f"{sms} SMs x 64 ALU-pipe lanes/clk (measured, profiles/int_peak.json) x "
@@ -419,27 +516,55 @@ def run_ours(args, rank, world, local_rank):
         "clocks": clocks,
         "wall_s": wall1 - wall0,
     }
-    return out
+    return out, (A, B, ref_pass)
 
 
-def cpu_baseline(config: str, image: int = 0, budget_s: float = 20.0):
-    """The oracle, as it stands, on this host's cores over a bounded sample of
-    the same workload: whole tiles of the slide (all rows of the path: areas,
-    join, per-pair areas, J') until ~budget_s seconds are spent."""
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def oracle_pass(A, B, threads: int) -> dict:
+    """One full pass of the oracle (oracle/, as it stands) over a workload:
+    shoelace areas + MBRs of both sets, the sweep join, per-pair I and U by
+    pixel counting, the integer sums, the exact ratio units and J' (Eq. 1).
+    Returns the results and the seconds it took."""
+    import oracle
+
+    t0 = time.perf_counter()
+    oracle.set_props(A)
+    oracle.set_props(B)
+    pairs = oracle.join(A, B)
+    inter, uni = oracle.pair_areas(A, B, pairs, threads=threads)
+    sums = oracle.sums(A, B, pairs, inter, uni)
+    j = oracle.jaccard(inter, uni)
+    sec = time.perf_counter() - t0
+    units = sum(oracle.ratio_units(i, u) for i, u in zip(inter.tolist(), uni.tolist()) if i)
+    return {"pairs": pairs, "inter": inter, "uni": uni, "sums": sums, "units": units, "jprime": j,
+            "jprime_exact": oracle.jaccard_exact(inter, uni), "seconds": sec}
+
+
+def oracle_sample(A, B, threads: int, budget_s: float) -> dict:
+    """The oracle on whole 4096 x 4096 tiles of the image (polygons by MBR
+    corner) in a seeded random order until ~budget_s seconds are spent: a
+    bounded sample of the same workload for slow settings (1 thread)."""
     import numpy as np
 
     import oracle
 
-    A, B = make_workload(config, image)
     _, ma = oracle.set_props(A)
     _, mb = oracle.set_props(B)
     tile = 4096
-    ta = (ma[:, 0] // tile) * 1000 + ma[:, 1] // tile
-    tb = (mb[:, 0] // tile) * 1000 + mb[:, 1] // tile
+    ta = (ma[:, 0] // tile) * 100000 + ma[:, 1] // tile
+    tb = (mb[:, 0] // tile) * 100000 + mb[:, 1] // tile
     tiles = sorted(set(ta.tolist()))
-    rng = np.random.default_rng(0)
-    rng.shuffle(tiles)
-    threads = os.cpu_count() or 1
+    np.random.default_rng(0).shuffle(tiles)
     done_pairs, spent, ntiles = 0, 0.0, 0
     for t in tiles:
         Ai = A.subset(np.nonzero(ta == t)[0])
@@ -455,24 +580,61 @@ def cpu_baseline(config: str, image: int = 0, budget_s: float = 20.0):
         ntiles += 1
         if spent > budget_s:
             break
-    return {"value": done_pairs / spent, "unit": "pairs/s", "cores": threads, "kind": "oracle",
-            "sample": f"{ntiles} of {len(tiles)} 4096x4096 tiles of the {config} image ({done_pairs} pairs), "
-                      f"full oracle path (shoelace areas, sweep join, pixel-count I/U, J')",
-            "seconds": spent, "ms_per_full_workload": 1e3 * spent * len(tiles) / max(ntiles, 1)}
+    return {"pairs": done_pairs, "seconds": spent, "tiles": ntiles, "of_tiles": len(tiles)}
+
+
+def cpu_baseline(config: str, A, B, full=None) -> dict:
+    """The oracle, as it stands, on this host's cores (rank 0, N = 1): all
+    threads over the whole workload (`full`, the pass bench.py also checks the
+    GPU against), and one thread over a bounded sample of whole tiles."""
+    threads = os.cpu_count() or 1
+    if full is None:
+        full = oracle_pass(A, B, threads)
+    one = oracle_sample(A, B, 1, budget_s=4.0)
+    n = len(full["pairs"])
+    return {"value": n / full["seconds"], "unit": "pairs/s", "cores": threads, "kind": "oracle",
+            "cpu_model": cpu_model(),
+            "sample": f"the whole {config} workload ({n} pairs): shoelace areas, sweep join, pixel-count I/U, "
+                      f"integer sums, J' -- all {threads} threads",
+            "seconds": full["seconds"],
+            "one_thread": {"value": one["pairs"] / one["seconds"], "unit": "pairs/s", "cores": 1,
+                           "sample": f"{one['tiles']} of {one['of_tiles']} 4096 x 4096 tiles ({one['pairs']} pairs), "
+                                     f"same path, 1 thread", "seconds": one["seconds"]}}
 
 
 def run_reference(args):
-    """--impl reference: the oracle is this tier's reference arm."""
-    base = cpu_baseline(args.config, 0, budget_s=max(5.0, min(60.0, 0.2 * (args.steps + args.warmup))))
+    """--impl reference: the oracle is this tier's reference arm.  Every step
+    is one full oracle pass over the same workload (all host threads), so the
+    line's steps / ms_per_step are what ran; warm-up passes untimed."""
+    A, B = make_workload(args.config, 0)
+    threads = os.cpu_count() or 1
+    for _ in range(max(args.warmup, 0)):
+        oracle_pass(A, B, threads)
+    secs, npairs = [], 0
+    for _ in range(args.steps):
+        r = oracle_pass(A, B, threads)
+        secs.append(r["seconds"])
+        npairs += len(r["pairs"])
+    tot = sum(secs)
+    value = npairs / tot
     out = {
-        "metric": METRIC, "value": base["value"], "unit": "pairs/s", "n_gpus": args.gpus, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": base["ms_per_full_workload"], "higher_is_better": True, "scaling": "weak",
+        "metric": METRIC, "value": value, "unit": "pairs/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "int32", "data": "synthetic", "impl": "reference",
-        "config": {"workload": args.config, "description": config_desc(args.config)},
-        "cpu_baseline": base,
-        "e2e": {"value": base["value"], "unit": "pairs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "config": workload_config(args.config, A, B, len(r["pairs"])),
+        "cpu_baseline": {"value": value, "unit": "pairs/s", "cores": threads, "kind": "oracle",
+                         "cpu_model": cpu_model(),
+                         "sample": f"each step: the whole {args.config} workload ({len(r['pairs'])} pairs), full "
+                                   f"oracle path, all {threads} threads"},
+        "e2e": {"value": value, "unit": "pairs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     return out
+
+
+def workload_config(config, A, B, n_pairs, world=1, shard="image"):
+    return {"workload": config, "description": config_desc(config), "pairs_per_gpu": n_pairs,
+            "polygons_p": A.n, "polygons_q": B.n, "vertices_p": int(A.offsets[-1]), "vertices_q": int(B.offsets[-1]),
+            "parallelism": (f"{shard}-sharded x{world}" if world > 1 else "1 GPU")}
 
 
 def main():
@@ -497,10 +659,11 @@ def main():
             dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
         else:
             dist.init_process_group(backend)
-    out = run_ours(args, rank, world, local_rank)
+    out, extra = run_ours(args, rank, world, local_rank)
     if rank == 0:
-        if not args.no_cpu_baseline and world == 1:  # the oracle baseline: rank 0 at N = 1 only
-            out["cpu_baseline"] = cpu_baseline(args.config, 0)
+        if not args.no_cpu_baseline and world == 1 and args.config != "combs":  # the oracle baseline: rank 0, N = 1
+            A, B, ref_pass = extra
+            out["cpu_baseline"] = cpu_baseline(args.config, A, B, ref_pass)
         line = json.dumps(out)
         print(line)
         if args.json_out:

@@ -74,6 +74,7 @@ typedef enum {
 #define SCCG_STATUS_NOT_RECTILINEAR (1u << 1)
 #define SCCG_STATUS_RANGE (1u << 2)
 #define SCCG_STATUS_STACK (1u << 3)
+#define SCCG_STATUS_CAPACITY (1u << 4) /* sccg_pixelbox_async: the pair list overflowed its buffer; no pair processed */
 
 /* One polygon set on the device: the caller's packed rings (inputs) plus the
  * per-polygon data sccg_prep derives from them (caller-allocated outputs; use
@@ -199,9 +200,11 @@ SCCG_API int sccg_pixelbox(const sccg_polyset* p, const sccg_polyset* q, const i
                   int64_t* inter, int64_t* uni, sccg_sums* sums, const sccg_config* cfg, void* workspace,
                   size_t ws_bytes, sccg_stream_t stream);
 
-/* Asynchronous variant: processes pairs[0 .. min(result_dev[0], cap)) where
- * result_dev is the device int64[2] written by sccg_filter_pairs_async, and
- * ORs result_dev[1] (prep status) into sums->status.  workspace as for
+/* Asynchronous variant: processes pairs[0 .. result_dev[0]) where result_dev
+ * is the device int64[2] written by sccg_filter_pairs_async, and ORs
+ * result_dev[1] (prep status) into sums->status.  If result_dev[0] > cap (the
+ * join overflowed the pair buffer, so the buffer is incomplete) no pair is
+ * processed and SCCG_STATUS_CAPACITY is set in sums->status.  workspace as for
  * sccg_pixelbox_workspace_bytes(cap). */
 SCCG_API int sccg_pixelbox_async(const sccg_polyset* p, const sccg_polyset* q, const int32_t* pairs,
                                  const int64_t* result_dev, int64_t cap, int64_t* inter, int64_t* uni,
@@ -227,11 +230,71 @@ SCCG_API int sccg_count_missing(const uint32_t* hit, int64_t n, int64_t* missing
 SCCG_API int sccg_touches(const sccg_polyset* p, const sccg_polyset* q, const int32_t* pairs, int64_t n_pairs,
                           const int64_t* inter, uint8_t* touches, sccg_stream_t stream);
 
+/* ST_Contains (§3.4: "computing the area of intersection and
+ * testing whether it equals the area of the object being contained"): for each
+ * pairs[k] = {p, q}, contains[k] bit 0 = p contains q (|p n q| == |q| > 0),
+ * bit 1 = q contains p (|p n q| == |p| > 0), on the pixel model (R1: the pixel
+ * set of the contained polygon is a subset of the other's).  inter: device
+ * int64 [n] = the |p n q| sccg_pixelbox computed for the same pairs; pairs:
+ * device int32 [n][2]; contains: device uint8 [n] (written; 0 for an
+ * out-of-range index).  Sets must be prepared (areas).  Asynchronous; SCCG_E_ARG
+ * for null / negative / misaligned arguments. */
+SCCG_API int sccg_contains(const sccg_polyset* p, const sccg_polyset* q, const int32_t* pairs, int64_t n_pairs,
+                           const int64_t* inter, uint8_t* contains, sccg_stream_t stream);
+
+/* -------------------------------------------------------------- report */
+/* Per-tile similarity report (SPEC S:343-346 SimilarityReport; Eq. 1 P:61 per
+ * tile; missing polygons P:63).  The image is cut into a grid of ntx x nty tiles
+ * of tile_w x tile_h pixels from (x0, y0); a polygon belongs to the tile holding
+ * its MBR's lower-left corner (xlo, ylo) (clamped into the grid), a pair to the
+ * tile of its p (reading R22). */
+typedef struct {
+  int32_t x0, y0;         /* grid origin */
+  int32_t tile_w, tile_h; /* tile size in pixels (> 0) */
+  int32_t ntx, nty;       /* tiles per row / column (> 0, ntx * nty < 2^31) */
+} sccg_tiling;
+
+/* One tile's entry: the pair totals of the tile's pairs in the sccg_sums
+ * layout (sccg_jaccard on .sums gives the tile's J'), the tile's polygon counts
+ * and its missing polygons (no pair with |p n q| != 0). */
+typedef struct {
+  sccg_sums sums;    /* status is 0 */
+  int64_t n_poly_p;  /* polygons of P in the tile */
+  int64_t n_poly_q;
+  int64_t missing_p; /* ... of which appear in no pair with |p n q| != 0 */
+  int64_t missing_q;
+} sccg_tile_report;  /* 15 x int64 */
+
+/* Accumulate the per-tile report of a pair batch into tiles[ntx * nty]
+ * (device, caller-zeroed): pair totals from pairs / inter / uni (as written by
+ * sccg_pixelbox for the same pairs), polygon and missing counts from the hit
+ * bitmaps sccg_pixelbox filled (config.hit_p / hit_q; after every batch of the
+ * image).  Polygon counts are added once per call: call it once per image with
+ * all of the image's pairs (n_pairs may be 0).  Asynchronous; SCCG_E_ARG for
+ * null / misaligned pointers or a bad tiling. */
+SCCG_API int sccg_report(const sccg_polyset* p, const sccg_polyset* q, const int32_t* pairs, int64_t n_pairs,
+                         const int64_t* inter, const int64_t* uni, const uint32_t* hit_p, const uint32_t* hit_q,
+                         const sccg_tiling* tiling, sccg_tile_report* tiles, sccg_stream_t stream);
+
 /* ---------------------------------------------------------------- jaccard */
 /* J' of Eq. (1) from host-resident sums: the mean of r(p, q) over the
  * pairs with |p n q| != 0.  *pooled (nullable) = sum_inter / sum_union over the
- * same pairs.  Returns SCCG_E_EMPTY and NaN when n_nonzero == 0. */
+ * same pairs.  Returns SCCG_E_EMPTY and NaN when n_nonzero == 0.  Sums that
+ * carry status bits (a device-side error in any batch) are rejected: NaN and
+ * the matching code (SCCG_E_ARG, _NOT_RECTILINEAR, _RANGE, _STACK, _CAPACITY,
+ * checked in that order). */
 SCCG_API int sccg_jaccard(const sccg_sums* sums_host, double* jprime, double* pooled);
+
+/* Cross-GPU reduction of sums: sccg_sums_pack writes the
+ * SCCG_REDUCE_WORDS int64 vector whose element-wise SUM over ranks (one NCCL
+ * all-reduce) sccg_sums_unpack turns back into sums: words 0..9 are the ten
+ * additive fields, words 10..25 status bit b (b < 16) as 0/1, so the reduced
+ * status is the OR of the ranks' status words (a plain SUM of status would
+ * carry bits into each other).  Device pointers, one single-warp kernel each;
+ * asynchronous and graph-capturable.  SCCG_E_ARG for null / misaligned. */
+#define SCCG_REDUCE_WORDS 26
+SCCG_API int sccg_sums_pack(const sccg_sums* src, int64_t* vec, sccg_stream_t stream);
+SCCG_API int sccg_sums_unpack(const int64_t* vec, sccg_sums* dst, sccg_stream_t stream);
 
 /* Copy a sums block (88 bytes) from `src` (device) to `dst` with one single-warp kernel on `stream`, so a
  * step's result read-back needs no copy-engine round trip (it can sit inside a CUDA graph).  `dst` may be

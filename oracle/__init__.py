@@ -22,6 +22,10 @@ DESIGN.md):
 * ``sums`` -- the integer totals the C-ABI reports in ``sccg_sums``.
 * ``touches`` -- ST_Touches (reading R21) on the pixel model: no common
   pixel and some pixel of each polygon sharing at least a corner.
+* ``contains`` -- ST_Contains on the pixel model: every pixel of the
+  contained ring is a pixel of the other (checked pixel by pixel over its MBR).
+* ``report`` -- the per-tile SimilarityReport (reading R22 for
+  the tile of a polygon / pair), from per-pair areas.
 
 Pins (tests/test_oracle.py) tie each of these to something other than itself:
 generator masks, the shoelace closed form, rectangles / combs / the SPEC
@@ -224,11 +228,18 @@ def jaccard(inter, uni) -> float:
 
 
 def jaccard_exact(inter, uni) -> Fraction | None:
-    """J' with exact rational arithmetic (for the 1e-12 check); None if empty."""
-    keep = [(int(i), int(u)) for i, u in zip(inter, uni) if int(i) != 0]
-    if not keep:
+    """J' with exact rational arithmetic (for the 1e-12 check); None if empty.
+    The ratios are grouped by their union first (sum_u (sum I) / u: the same
+    rational, with one Fraction addition per distinct u instead of per pair)."""
+    by_u: dict[int, int] = {}
+    n = 0
+    for i, u in zip(np.asarray(inter, np.int64).tolist(), np.asarray(uni, np.int64).tolist()):
+        if i != 0:
+            by_u[u] = by_u.get(u, 0) + i
+            n += 1
+    if not n:
         return None
-    return sum((Fraction(i, u) for i, u in keep), Fraction(0)) / len(keep)
+    return sum((Fraction(i, u) for u, i in sorted(by_u.items())), Fraction(0)) / n
 
 
 def sums(pset, qset, pairs, inter, uni) -> dict:
@@ -258,3 +269,85 @@ def missing(n: int, pairs, inter, side: int) -> int:
     inter = np.asarray(inter, np.int64)
     seen = set(pairs[inter != 0, side].tolist())
     return int(n - len(seen))
+
+
+# ------------------------------------------------------------ ST_Contains
+def contains(ring_p, ring_q) -> bool:
+    """ST_Contains on the pixel model: q is non-empty and every pixel
+    of q (scanned over q's MBR) is a pixel of p."""
+    x0, y0, x1, y1 = mbr(ring_q)
+    if x1 <= x0 or y1 <= y0:
+        return False
+    mq = mask(ring_q, x0, y0, x1 - x0, y1 - y0)
+    if not mq.any():
+        return False
+    mp = mask(ring_p, x0, y0, x1 - x0, y1 - y0)
+    return bool(((mq == 1) <= (mp == 1)).all())
+
+
+def contains_pairs(pset, qset, pairs) -> np.ndarray:
+    """uint8 [n]: bit 0 = p contains q, bit 1 = q contains p."""
+    pairs = np.asarray(pairs, np.int64).reshape(-1, 2)
+    out = np.zeros(len(pairs), np.uint8)
+    for k, (p, q) in enumerate(pairs):
+        rp, rq = pset.ring(int(p)), qset.ring(int(q))
+        out[k] = (1 if contains(rp, rq) else 0) | (2 if contains(rq, rp) else 0)
+    return out
+
+
+# ------------------------------------------------------------------ report
+REPORT_FIELDS = ("n_pairs", "n_nonzero", "sum_inter", "sum_union", "sum_area_p", "sum_area_q", "limb0", "limb1",
+                 "limb2", "limb3", "status", "n_poly_p", "n_poly_q", "missing_p", "missing_q")
+
+
+def ratio_units(i: int, u: int) -> int:
+    """RN64(I/U) as an exact integer count of 2^-116 (reading R12): Python's
+    int / int is the correctly rounded binary64 quotient."""
+    return int(Fraction(int(i) / int(u)) * (1 << 116))
+
+
+def tile_index(xlo: int, ylo: int, tiling) -> int:
+    """Reading R22: the tile holding (xlo, ylo), clamped into the grid."""
+    x0, y0, tw, th, ntx, nty = tiling
+    tx = min(max((xlo - x0) // tw, 0), ntx - 1)
+    ty = min(max((ylo - y0) // th, 0), nty - 1)
+    return ty * ntx + tx
+
+
+def report(pset, qset, pairs, inter, uni, tiling) -> np.ndarray:
+    """Per-tile SimilarityReport rows int64 [ntx * nty, 15] (REPORT_FIELDS):
+    a pair counts in the tile of its p, a polygon in its own tile; missing =
+    polygons in no pair with I != 0; ratio limbs = the exact sum of
+    RN64(I/U) over the tile's pairs with I != 0 in 30-bit limbs (Eq. 1)."""
+    pairs = np.asarray(pairs, np.int64).reshape(-1, 2)
+    inter = np.asarray(inter, np.int64)
+    uni = np.asarray(uni, np.int64)
+    ap, mp = set_props(pset)
+    aq, mq = set_props(qset)
+    nt = tiling[4] * tiling[5]
+    rows = [[0] * len(REPORT_FIELDS) for _ in range(nt)]
+    units = [0] * nt
+    hit_p, hit_q = set(), set()
+    for (p, q), i, u in zip(pairs.tolist(), inter.tolist(), uni.tolist()):
+        t = tile_index(int(mp[p, 0]), int(mp[p, 1]), tiling)
+        r = rows[t]
+        r[0] += 1
+        r[2] += i
+        r[4] += int(ap[p])
+        r[5] += int(aq[q])
+        if i != 0:
+            r[1] += 1
+            r[3] += u
+            units[t] += ratio_units(i, u)
+            hit_p.add(p)
+            hit_q.add(q)
+    for t in range(nt):
+        for k in range(4):
+            rows[t][6 + k] = (units[t] >> (30 * k)) & ((1 << 30) - 1) if k < 3 else units[t] >> 90
+    for side, (m, hit) in enumerate(((mp, hit_p), (mq, hit_q))):
+        for i in range(len(m)):
+            t = tile_index(int(m[i, 0]), int(m[i, 1]), tiling)
+            rows[t][11 + side] += 1
+            if i not in hit:
+                rows[t][13 + side] += 1
+    return np.array(rows, np.int64).reshape(nt, len(REPORT_FIELDS))

@@ -39,8 +39,12 @@ SUMS_FIELDS = ("n_pairs", "n_nonzero", "sum_inter", "sum_union", "sum_area_p", "
                "limb2", "limb3", "status")
 SYMBOLS = ("sccg_polyset_bytes", "sccg_polyset_bind", "sccg_prep", "sccg_prep_sets", "sccg_filter_workspace_bytes",
            "sccg_filter_pairs", "sccg_filter_pairs_closed", "sccg_filter_pairs_async", "sccg_touches", "sccg_pixelbox_workspace_bytes", "sccg_pixelbox",
-           "sccg_pixelbox_async", "sccg_count_missing", "sccg_jaccard", "sccg_sums_copy", "sccg_strerror", "sccg_last_error_string", "sccg_last_error_index",
+           "sccg_pixelbox_async", "sccg_count_missing", "sccg_contains", "sccg_report", "sccg_jaccard", "sccg_sums_copy",
+           "sccg_sums_pack", "sccg_sums_unpack", "sccg_strerror", "sccg_last_error_string", "sccg_last_error_index",
            "sccg_version")
+STATUS_ARG, STATUS_NOT_RECTILINEAR, STATUS_RANGE, STATUS_STACK, STATUS_CAPACITY = 1, 2, 4, 8, 16
+REDUCE_WORDS = 26  # SCCG_REDUCE_WORDS
+REPORT_FIELDS = SUMS_FIELDS[:10] + ("status", "n_poly_p", "n_poly_q", "missing_p", "missing_q")
 
 
 class SccgError(RuntimeError):
@@ -70,6 +74,10 @@ class PolySet(ctypes.Structure):
 
 class Sums(ctypes.Structure):
     _fields_ = [(f, ctypes.c_int64) for f in SUMS_FIELDS]
+
+
+class Tiling(ctypes.Structure):
+    _fields_ = [(f, ctypes.c_int32) for f in ("x0", "y0", "tile_w", "tile_h", "ntx", "nty")]
 
 
 class Config(ctypes.Structure):
@@ -139,6 +147,14 @@ def load(build: bool = True):
         lib.sccg_pixelbox.restype = cint
         lib.sccg_count_missing.argtypes = [vp, i64, vp, vp]
         lib.sccg_count_missing.restype = cint
+        lib.sccg_contains.argtypes = [ps, ps, vp, i64, vp, vp, vp]
+        lib.sccg_contains.restype = cint
+        lib.sccg_report.argtypes = [ps, ps, vp, i64, vp, vp, vp, vp, ctypes.POINTER(Tiling), vp, vp]
+        lib.sccg_report.restype = cint
+        lib.sccg_sums_pack.argtypes = [vp, vp, vp]
+        lib.sccg_sums_pack.restype = cint
+        lib.sccg_sums_unpack.argtypes = [vp, vp, vp]
+        lib.sccg_sums_unpack.restype = cint
         lib.sccg_jaccard.argtypes = [ctypes.POINTER(Sums), ctypes.POINTER(ctypes.c_double),
                                      ctypes.POINTER(ctypes.c_double)]
         lib.sccg_jaccard.restype = cint
@@ -292,7 +308,7 @@ class Pipeline:
     ``run()`` returns the device sums vector; read it (one sync) for J'."""
 
     def __init__(self, P: "DeviceSet", Q: "DeviceSet", cap: int | None = None, threshold: int = 0, graph: bool = True,
-                 validate: bool = True, raster: bool = True, readback=()):
+                 validate: bool = True, raster: bool = True, readback=(), outputs: bool = True):
         torch = _torch()
         self.lib = load()
         self.P, self.Q = P, Q
@@ -301,6 +317,10 @@ class Pipeline:
         self.pairs = torch.empty((max(self.cap, 1), 2), dtype=torch.int32, device=dev)
         self.result = torch.zeros(2, dtype=torch.int64, device=dev)
         self.sums = new_sums(dev)
+        self._zero = new_sums(dev)  # the step's sums are reset by our copy kernel (no torch fill kernel in the graph)
+        # per-pair |p n q| and |p u q| (row a7's outputs), written every step; valid for pairs[:n]
+        self.inter = torch.empty(max(self.cap, 1), dtype=torch.int64, device=dev) if outputs else None
+        self.uni = torch.empty(max(self.cap, 1), dtype=torch.int64, device=dev) if outputs else None
         self.fws_bytes = int(self.lib.sccg_filter_workspace_bytes(P.n, Q.n))
         self.fws = torch.empty(self.fws_bytes, dtype=torch.uint8, device=dev)
         self.pws_bytes = int(self.lib.sccg_pixelbox_workspace_bytes(self.cap))
@@ -355,7 +375,7 @@ class Pipeline:
     def _enqueue_prep(self):
         st = _stream_ptr()
         lib = self.lib
-        self.sums.zero_()
+        sums_copy(self._zero, self.sums)
         _check(lib.sccg_prep_sets(self._sets, 2, self.validate, st), "sccg_prep_sets")
 
     def _enqueue_join(self):
@@ -365,7 +385,9 @@ class Pipeline:
 
     def _enqueue_pixelbox(self):
         _check(self.lib.sccg_pixelbox_async(ctypes.byref(self.P.c), ctypes.byref(self.Q.c), self.pairs.data_ptr(),
-                                            self.result.data_ptr(), self.cap, None, None, self.sums.data_ptr(),
+                                            self.result.data_ptr(), self.cap,
+                                            self.inter.data_ptr() if self.inter is not None else None,
+                                            self.uni.data_ptr() if self.uni is not None else None, self.sums.data_ptr(),
                                             ctypes.byref(self.cfg), self.pws.data_ptr(), self.pws_bytes, _stream_ptr()),
                "sccg_pixelbox_async")
         if self.readback:
@@ -394,12 +416,14 @@ class Pipeline:
         return self.sums
 
     def check(self):
-        """After a run: raise if the pair buffer overflowed or prep flagged input."""
+        """After a run: raise if the pair buffer overflowed, prep flagged input or
+        PixelBox flagged a device-side error (the sums' status word)."""
         n, status = (int(v) for v in self.result.tolist())
         if n > self.cap:
             raise SccgError(E_CAPACITY, f"Pipeline: {n} pairs > cap {self.cap}")
         if status:
             raise SccgError(E_ARG, f"Pipeline: prep status bits {status:#x}")
+        check_status(self.sums.cpu(), "Pipeline")
         return n
 
 
@@ -425,8 +449,10 @@ def new_sums(device=None):
 
 def pixelbox(P: DeviceSet, Q: DeviceSet, pairs, threshold: int = 0, mode: int = 0, sums=None, want_inter=True,
              want_union=True, counters=None, grid: int = 0, hits=None, raster: bool = True, paper_split: bool = False,
-             stream=None):
+             stream=None, check: bool = True):
     """Per-pair |p n q| and |p u q| (int64, input order) + accumulated sums.
+    check: read the sums' status word after the call (one sync) and raise
+    SccgError if a device-side error was flagged (check=False: stay async).
     paper_split: push every continuing sub-box (Alg. 1 as written) instead of
     pixelizing dense splits whole (SCCG_FLAG_PAPER_SPLIT; same results).
     hits = (hit_p, hit_q): optional int32 bitmaps (new_hits) marking polygons
@@ -451,7 +477,19 @@ def pixelbox(P: DeviceSet, Q: DeviceSet, pairs, threshold: int = 0, mode: int = 
                              uni.data_ptr() if uni is not None else None, sums.data_ptr(), ctypes.byref(cfg),
                              ws.data_ptr(), wsb, _stream_ptr(stream))
     _check(code, "sccg_pixelbox")
+    if check:
+        check_status(sums, "sccg_pixelbox")
     return inter, uni, sums
+
+
+def check_status(sums, where="sums"):
+    """Raise SccgError if a sums vector carries device status bits (one sync)."""
+    st = int(sums[10]) if not isinstance(sums, Sums) else int(sums.status)
+    if st:
+        code = (E_ARG if st & STATUS_ARG else E_NOT_RECTILINEAR if st & STATUS_NOT_RECTILINEAR else
+                E_RANGE if st & STATUS_RANGE else E_STACK if st & STATUS_STACK else
+                E_CAPACITY if st & STATUS_CAPACITY else E_ARG)
+        raise SccgError(code, f"{where}: device status bits {st:#x}")
 
 
 def new_hits(P: "DeviceSet", Q: "DeviceSet"):
@@ -475,10 +513,68 @@ def missing_polygons(hits, P: "DeviceSet", Q: "DeviceSet", stream=None) -> tuple
     return int(a), int(b)
 
 
-def contains(inter, area_inner):
-    """ST_Contains by areas: the inner polygon lies in the outer one iff
-    |outer n inner| == |inner| (pixel sets; per pair, elementwise)."""
-    return inter == area_inner
+def contains(P: DeviceSet, Q: DeviceSet, pairs, inter, stream=None):
+    """ST_Contains by areas (sccg_contains): uint8 [N], bit 0 = p
+    contains q (|p n q| == |q| > 0), bit 1 = q contains p; inter from pixelbox."""
+    torch = _torch()
+    _require_cuda(pairs, "pairs", torch.int32)
+    _require_cuda(inter, "inter", torch.int64)
+    n = int(pairs.shape[0])
+    out = torch.empty(n, dtype=torch.uint8, device=pairs.device)
+    _check(load().sccg_contains(ctypes.byref(P.c), ctypes.byref(Q.c), pairs.data_ptr(), n, inter.data_ptr(),
+                                out.data_ptr(), _stream_ptr(stream)), "sccg_contains")
+    return out
+
+
+def tile_report(P: DeviceSet, Q: DeviceSet, pairs, inter, uni, hits, tiling, tiles=None, stream=None):
+    """Per-tile report (sccg_report): int64 [ntx * nty, 15]
+    device tensor (fields REPORT_FIELDS), accumulated into `tiles` if given.
+    tiling = Tiling or (x0, y0, tile_w, tile_h, ntx, nty)."""
+    torch = _torch()
+    t = tiling if isinstance(tiling, Tiling) else Tiling(*tiling)
+    n = int(pairs.shape[0])
+    if tiles is None:
+        tiles = torch.zeros((t.ntx * t.nty, len(REPORT_FIELDS)), dtype=torch.int64, device=P.xy.device)
+    _check(load().sccg_report(ctypes.byref(P.c), ctypes.byref(Q.c), pairs.data_ptr() if n else None, n,
+                              inter.data_ptr() if n else None, uni.data_ptr() if n else None, hits[0].data_ptr(),
+                              hits[1].data_ptr(), ctypes.byref(t), tiles.data_ptr(), _stream_ptr(stream)),
+           "sccg_report")
+    return tiles
+
+
+def similarity_report(P: DeviceSet, Q: DeviceSet, pairs, inter, uni, hits, tiling, stream=None) -> dict:
+    """The SimilarityReport of SPEC S:343-346 from one image's pairs: per tile
+    {tile_id, pairs, intersecting, jaccard, ratio_limbs, missing_p, missing_q,
+    polygons_p, polygons_q}, the image J' (Eq. 1 over all pairs) and the totals."""
+    tiles = tile_report(P, Q, pairs, inter, uni, hits, tiling, stream=stream).cpu().tolist()
+    per_tile = []
+    tot = [0] * 11
+    for tid, row in enumerate(tiles):
+        s = Sums(*row[:11])
+        j, _ = jaccard(s)
+        per_tile.append(dict(tile_id=tid, pairs=row[0], intersecting=row[1], jaccard=None if math.isnan(j) else j,
+                             ratio_limbs=row[6:10], polygons_p=row[11], polygons_q=row[12], missing_p=row[13],
+                             missing_q=row[14]))
+        tot = [a + b for a, b in zip(tot, row[:11])]
+    j, pooled = jaccard(Sums(*tot))
+    return dict(tiles=per_tile, jaccard=None if math.isnan(j) else j, pooled=None if math.isnan(pooled) else pooled,
+                pairs=tot[0], intersecting=tot[1], polygons_p=P.n, polygons_q=Q.n,
+                missing_p=sum(t["missing_p"] for t in per_tile), missing_q=sum(t["missing_q"] for t in per_tile))
+
+
+def sums_pack(sums, vec=None, stream=None):
+    """sccg_sums_pack: the REDUCE_WORDS int64 all-reduce vector of a device sums vector."""
+    torch = _torch()
+    if vec is None:
+        vec = torch.empty(REDUCE_WORDS, dtype=torch.int64, device=sums.device)
+    _check(load().sccg_sums_pack(sums.data_ptr(), vec.data_ptr(), _stream_ptr(stream)), "sccg_sums_pack")
+    return vec
+
+
+def sums_unpack(vec, sums, stream=None):
+    """sccg_sums_unpack: sums (device int64 [11]) from a (reduced) vector."""
+    _check(load().sccg_sums_unpack(vec.data_ptr(), sums.data_ptr(), _stream_ptr(stream)), "sccg_sums_unpack")
+    return sums
 
 
 def sums_to_host(sums) -> Sums:
@@ -502,7 +598,7 @@ def jaccard(sums) -> tuple[float, float]:
     code = lib.sccg_jaccard(ctypes.byref(s), ctypes.byref(j), ctypes.byref(pooled))
     if code == E_EMPTY:
         return math.nan, math.nan
-    _check(code, "sccg_jaccard")
+    _check(code, "sccg_jaccard")  # sums carrying device status bits are rejected
     return j.value, pooled.value
 
 
@@ -523,7 +619,9 @@ def compare(xy_p, off_p, xy_q, off_q, threshold: int = 0, device="cuda", stream=
     P = DeviceSet(dxp, dop, stream=stream)
     Q = DeviceSet(dxq, doq, stream=stream)
     pairs = filter_pairs(P, Q, stream=stream)
-    _, _, sums = pixelbox(P, Q, pairs, threshold=threshold, want_inter=False, want_union=False, stream=stream)
+    _, _, sums = pixelbox(P, Q, pairs, threshold=threshold, want_inter=False, want_union=False, stream=stream,
+                          check=False)
     host = sums_to_host(sums.cpu())
+    check_status(host, "compare")
     j, pooled = jaccard(host)
     return dict(jprime=j, pooled=pooled, **{f: getattr(host, f) for f in SUMS_FIELDS})

@@ -31,6 +31,13 @@ int filter_pairs(const sccg_polyset* P, const sccg_polyset* Q, int32_t* pairs, i
 int run_touches(const sccg_polyset* P, const sccg_polyset* Q, const int32_t* pairs, int64_t n, const int64_t* inter,
                 uint8_t* out, cudaStream_t stream);
 size_t pixelbox_ws_bytes(int64_t n);
+int run_contains(const sccg_polyset* P, const sccg_polyset* Q, const int32_t* pairs, int64_t n, const int64_t* inter,
+                 uint8_t* out, cudaStream_t stream);
+int run_report(const sccg_polyset* P, const sccg_polyset* Q, const int32_t* pairs, int64_t n, const int64_t* inter,
+               const int64_t* uni, const uint32_t* hit_p, const uint32_t* hit_q, const sccg_tiling* tl,
+               sccg_tile_report* tiles, cudaStream_t stream);
+cudaError_t launch_sums_pack(const sccg_sums* src, int64_t* vec, cudaStream_t st);
+cudaError_t launch_sums_unpack(const int64_t* vec, sccg_sums* dst, cudaStream_t st);
 int count_missing(const uint32_t* hit, int64_t n, int64_t* out, cudaStream_t st);
 int filter_pairs_async(const sccg_polyset* P, const sccg_polyset* Q, int32_t* pairs, int64_t cap,
                        int64_t* result_dev, void* ws, size_t ws_bytes, cudaStream_t stream);
@@ -193,6 +200,50 @@ int sccg_touches(const sccg_polyset* p, const sccg_polyset* q, const int32_t* pa
   return run_touches(p, q, pairs, n_pairs, inter, touches, reinterpret_cast<cudaStream_t>(stream));
 }
 
+int sccg_contains(const sccg_polyset* p, const sccg_polyset* q, const int32_t* pairs, int64_t n_pairs,
+                  const int64_t* inter, uint8_t* contains, sccg_stream_t stream) {
+  set_error(SCCG_OK, "", -1);
+  if (int r = check_set(p, true, "p")) return r;
+  if (int r = check_set(q, true, "q")) return r;
+  if (n_pairs < 0) return set_error(SCCG_E_ARG, "negative pair count");
+  if (n_pairs == 0) return SCCG_OK;
+  if (!pairs || !aligned(pairs, 8)) return set_error(SCCG_E_ARG, "pairs must be a non-null 8-byte aligned device array");
+  if (!inter || !aligned(inter, 8)) return set_error(SCCG_E_ARG, "inter must be a non-null aligned device int64 array");
+  if (!contains) return set_error(SCCG_E_ARG, "contains is null");
+  return run_contains(p, q, pairs, n_pairs, inter, contains, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int sccg_report(const sccg_polyset* p, const sccg_polyset* q, const int32_t* pairs, int64_t n_pairs,
+                const int64_t* inter, const int64_t* uni, const uint32_t* hit_p, const uint32_t* hit_q,
+                const sccg_tiling* tiling, sccg_tile_report* tiles, sccg_stream_t stream) {
+  set_error(SCCG_OK, "", -1);
+  if (int r = check_set(p, true, "p")) return r;
+  if (int r = check_set(q, true, "q")) return r;
+  if (n_pairs < 0) return set_error(SCCG_E_ARG, "negative pair count");
+  if (n_pairs > 0 && (!pairs || !inter || !uni)) return set_error(SCCG_E_ARG, "pairs / inter / uni is null");
+  if (!aligned(pairs, 8) || !aligned(inter, 8) || !aligned(uni, 8)) return set_error(SCCG_E_ARG, "misaligned pointer");
+  if ((p->n_polygons > 0 && !hit_p) || (q->n_polygons > 0 && !hit_q) || !aligned(hit_p, 4) || !aligned(hit_q, 4))
+    return set_error(SCCG_E_ARG, "hit bitmaps must be non-null aligned device arrays");
+  if (!tiling || !tiles || !aligned(tiles, 8)) return set_error(SCCG_E_ARG, "tiling / tiles is null or misaligned");
+  if (tiling->tile_w <= 0 || tiling->tile_h <= 0 || tiling->ntx <= 0 || tiling->nty <= 0 ||
+      (int64_t)tiling->ntx * tiling->nty >= (int64_t(1) << 31))
+    return set_error(SCCG_E_ARG, "bad tiling (sizes and tile counts must be positive)");
+  return run_report(p, q, pairs, n_pairs, inter, uni, hit_p, hit_q, tiling, tiles,
+                    reinterpret_cast<cudaStream_t>(stream));
+}
+
+int sccg_sums_pack(const sccg_sums* src, int64_t* vec, sccg_stream_t stream) {
+  set_error(SCCG_OK, "", -1);
+  if (!src || !vec || !aligned(src, 8) || !aligned(vec, 8)) return set_error(SCCG_E_ARG, "sccg_sums_pack: null or misaligned pointer");
+  return check_cuda(launch_sums_pack(src, vec, reinterpret_cast<cudaStream_t>(stream)), "sccg_sums_pack");
+}
+
+int sccg_sums_unpack(const int64_t* vec, sccg_sums* dst, sccg_stream_t stream) {
+  set_error(SCCG_OK, "", -1);
+  if (!vec || !dst || !aligned(vec, 8) || !aligned(dst, 8)) return set_error(SCCG_E_ARG, "sccg_sums_unpack: null or misaligned pointer");
+  return check_cuda(launch_sums_unpack(vec, dst, reinterpret_cast<cudaStream_t>(stream)), "sccg_sums_unpack");
+}
+
 int sccg_filter_pairs_async(const sccg_polyset* p, const sccg_polyset* q, int32_t* pairs, int64_t cap,
                             int64_t* result_dev, void* workspace, size_t ws_bytes, sccg_stream_t stream) {
   set_error(SCCG_OK, "", -1);
@@ -261,6 +312,20 @@ int sccg_sums_copy(const sccg_sums* src, sccg_sums* dst, sccg_stream_t stream) {
 int sccg_jaccard(const sccg_sums* s, double* jprime, double* pooled) {
   set_error(SCCG_OK, "", -1);
   if (!s || !jprime) return set_error(SCCG_E_ARG, "null argument");
+  if (s->status) {  // a batch hit a device-side error: its totals are not the pairs' totals
+    *jprime = NAN;
+    if (pooled) *pooled = NAN;
+    const int64_t b = s->status;
+    const int code = (b & SCCG_STATUS_ARG) ? SCCG_E_ARG
+                     : (b & SCCG_STATUS_NOT_RECTILINEAR) ? SCCG_E_NOT_RECTILINEAR
+                     : (b & SCCG_STATUS_RANGE) ? SCCG_E_RANGE
+                     : (b & SCCG_STATUS_STACK) ? SCCG_E_STACK
+                     : (b & SCCG_STATUS_CAPACITY) ? SCCG_E_CAPACITY
+                                                  : SCCG_E_ARG;
+    char buf[96];
+    snprintf(buf, sizeof(buf), "sums carry device status bits %#llx", (unsigned long long)b);
+    return set_error(code, buf);
+  }
   if (s->n_nonzero <= 0) {
     *jprime = NAN;
     if (pooled) *pooled = NAN;

@@ -129,9 +129,12 @@ __global__ void __launch_bounds__(kSmallWarps * 32, SCCG_SMALL_MINB)
   pdl_trigger();
   pdl_wait();
   // pair count: host-given, or (async path) the filter's device-side count clamped to the buffer
-  const long long n = dev_result ? min(dev_result[0], n_cap) : n_cap;
-  if (dev_result && blockIdx.x == 0 && threadIdx.x == 0 && dev_result[1])
-    atomicOr(reinterpret_cast<unsigned long long*>(&sums->status), (unsigned long long)dev_result[1]);
+  // (a join that overflowed the buffer left it incomplete: nothing is processed, the status says so)
+  const bool overflow = dev_result && dev_result[0] > n_cap;
+  const long long n = dev_result ? (overflow ? 0 : dev_result[0]) : n_cap;
+  if (dev_result && blockIdx.x == 0 && threadIdx.x == 0 && (dev_result[1] || overflow))
+    atomicOr(reinterpret_cast<unsigned long long*>(&sums->status),
+             (unsigned long long)dev_result[1] | (overflow ? (unsigned long long)SCCG_STATUS_CAPACITY : 0ull));
   __shared__ __align__(16) int2 s_buf[kSmallWarps][2 * kSmallQOff];
   __shared__ int4 s_meta[kSmallWarps][32];
   __shared__ int2 s_ep[kSmallWarps][32];

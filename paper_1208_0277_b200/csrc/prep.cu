@@ -473,6 +473,9 @@ __global__ void __launch_bounds__(kPrepThreads, 5) prep_kernel(const __grid_cons
     uint64_t* __restrict__ edges = S.edges;
     uint32_t* __restrict__ status = S.status;
     const int bulk = S.bulk;
+    // the previous tile's bulk write-back must have read the buffer before anything (TMA load or, for a set
+    // without 16-byte alignment, plain stores) overwrites it -- whatever the current set's mode
+    if (threadIdx.x == 0) bulk_store_drain();
     __syncthreads();  // previous tile's shared data fully consumed
     if ((int)threadIdx.x <= np) s_off[threadIdx.x] = off_a;
     if (threadIdx.x == 0) s_off[np] = off_b;

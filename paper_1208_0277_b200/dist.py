@@ -105,16 +105,50 @@ def subset_rings(xy, offsets, idx):
     return np.ascontiguousarray(xy[src], dtype=np.int32), new_off
 
 
-def allreduce_sums(sums, group=None):
-    """In-place SUM of an int64 sums vector over the process group (NCCL for
-    CUDA tensors, gloo for CPU tensors).  Returns the tensor."""
+REDUCE_WORDS = 26  # SCCG_REDUCE_WORDS: 10 additive fields + 16 status bits as 0/1
+
+
+def pack_sums(sums):
+    """Host mirror of sccg_sums_pack for CPU tensors (gloo): the int64 vector
+    whose element-wise SUM over ranks unpacks to the reduced sums."""
+    import torch
+
+    st = int(sums[10])
+    bits = torch.tensor([(st >> b) & 1 for b in range(REDUCE_WORDS - 10)], dtype=torch.int64)
+    return torch.cat([sums[:10].to(torch.int64), bits])
+
+
+def unpack_sums(vec, sums):
+    """Host mirror of sccg_sums_unpack: status = OR of the ranks' status words
+    (bit b set iff some rank set it), the other fields summed."""
+    sums[:10] = vec[:10]
+    sums[10] = sum(1 << b for b in range(REDUCE_WORDS - 10) if int(vec[10 + b]) != 0)
+    return sums
+
+
+def allreduce_sums(sums, group=None, force: bool = False):
+    """In-place reduction of an int64 sums vector over the process group: the
+    ten additive fields are summed, the status words OR-ed (NCCL has no
+    bitwise-or: the status bits travel as 0/1 counts in the one SUM
+    all-reduce, sccg_sums_pack / sccg_sums_unpack on the GPU).  Bit-exact for
+    any rank count.  force: run the collective even at world size 1 (tests).
+    Returns the tensor."""
     import torch
     import torch.distributed as dist
 
     if sums.dtype != torch.int64:
         raise TypeError("sums must be int64 (exact integer reduction)")
-    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
-        dist.all_reduce(sums, op=dist.ReduceOp.SUM, group=group)
+    if dist.is_available() and dist.is_initialized() and (dist.get_world_size(group) > 1 or force):
+        if sums.is_cuda:
+            import paper_1208_0277_b200 as sccg
+
+            vec = sccg.sums_pack(sums)
+            dist.all_reduce(vec, op=dist.ReduceOp.SUM, group=group)
+            sccg.sums_unpack(vec, sums)
+        else:
+            vec = pack_sums(sums)
+            dist.all_reduce(vec, op=dist.ReduceOp.SUM, group=group)
+            unpack_sums(vec, sums)
     return sums
 
 

@@ -27,35 +27,30 @@ def comb(x0: int, y0: int, k: int, w: int, g: int, h: int, b: int, two_sided: bo
         rects.append((tx, yb1, tx + w, yb1 + h))
         if two_sided:
             rects.append((tx, y0, tx + w, yb0))
-    ring = []
-    # bottom side, left to right
-    if two_sided:
-        for i in range(k):
-            tx = x0 + i * p
-            ring += [(tx, y0), (tx + w, y0)]
-            if i < k - 1:
-                ring += [(tx + w, yb0), (tx + p, yb0)]
+    # the ring, vertex by vertex (vectorised): bottom side left to right, then
+    # the top side right to left; the left and right ends are straight columns
+    txs = x0 + np.arange(k, dtype=np.int64) * p
+    if two_sided:  # per tooth i: (tx, y0), (tx + w, y0), then (tx + w, yb0), (tx + p, yb0) between teeth
+        bot = np.empty((k, 4, 2), np.int64)
+        bot[:, 0] = np.stack([txs, np.full(k, y0)], 1)
+        bot[:, 1] = np.stack([txs + w, np.full(k, y0)], 1)
+        bot[:, 2] = np.stack([txs + w, np.full(k, yb0)], 1)
+        bot[:, 3] = np.stack([txs + p, np.full(k, yb0)], 1)
+        bot = bot.reshape(-1, 2)[:-2]
     else:
-        ring += [(x0, yb0), (x0 + W, yb0)]
-    # top side, right to left
-    for i in range(k - 1, -1, -1):
-        tx = x0 + i * p
-        ring += [(tx + w, yb1 + h), (tx, yb1 + h)]
-        if i > 0:
-            ring += [(tx, yb1), (tx - g, yb1)]
-    if two_sided:
-        # close: from (x0, yb1+h) down to (x0, y0) is one straight left edge
-        pass
-    r = np.asarray(ring, np.int32)
-    # drop collinear vertices (left/right ends are straight columns)
-    keep = []
-    n = len(r)
-    for i in range(n):
-        a, c, d = r[i - 1], r[i], r[(i + 1) % n]
-        if (a[0] == c[0] == d[0]) or (a[1] == c[1] == d[1]):
-            continue
-        keep.append(c)
-    return np.asarray(keep, np.int32), rects
+        bot = np.array([(x0, yb0), (x0 + W, yb0)], np.int64)
+    rt = txs[::-1]  # top side, right to left: (tx + w, top), (tx, top), then (tx, yb1), (tx - g, yb1) between teeth
+    top = np.empty((k, 4, 2), np.int64)
+    top[:, 0] = np.stack([rt + w, np.full(k, yb1 + h)], 1)
+    top[:, 1] = np.stack([rt, np.full(k, yb1 + h)], 1)
+    top[:, 2] = np.stack([rt, np.full(k, yb1)], 1)
+    top[:, 3] = np.stack([rt - g, np.full(k, yb1)], 1)
+    top = top.reshape(-1, 2)[:-2]
+    r = np.concatenate([bot, top]).astype(np.int32)
+    # drop collinear vertices
+    a, d = np.roll(r, 1, axis=0), np.roll(r, -1, axis=0)
+    col = ((a[:, 0] == r[:, 0]) & (r[:, 0] == d[:, 0])) | ((a[:, 1] == r[:, 1]) & (r[:, 1] == d[:, 1]))
+    return np.ascontiguousarray(r[~col], np.int32), rects
 
 
 def _rng(seed: int, i: int) -> np.random.Generator:

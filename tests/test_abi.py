@@ -10,6 +10,7 @@ import subprocess
 from fractions import Fraction
 
 import numpy as np
+import pytest
 
 import oracle
 import paper_1208_0277_b200 as sccg
@@ -115,3 +116,27 @@ def test_host_argument_checks():
     assert lib.sccg_filter_pairs(None, None, None, 0, ctypes.byref(n), None, 0, None) == sccg.E_ARG
     cfg = sccg.Config(-1, 0, 0, 0, None, None, None)
     assert lib.sccg_pixelbox(None, None, None, 0, None, None, None, ctypes.byref(cfg), None, 0, None) == sccg.E_ARG
+
+
+def test_jaccard_rejects_status_bits_and_new_entry_points():
+    """sums carrying device status bits never yield a J' (NaN and
+    the matching code, checked in the documented order); argument checks of
+    sccg_contains / sccg_report / sccg_sums_pack / unpack (host-only)."""
+    lib = sccg.load()
+    base = _sums_from([1, 1], [7, 1])
+    for bits, code in ((sccg.STATUS_ARG, sccg.E_ARG), (sccg.STATUS_NOT_RECTILINEAR, sccg.E_NOT_RECTILINEAR),
+                       (sccg.STATUS_RANGE, sccg.E_RANGE), (sccg.STATUS_STACK, sccg.E_STACK),
+                       (sccg.STATUS_CAPACITY, sccg.E_CAPACITY), (sccg.STATUS_STACK | sccg.STATUS_RANGE, sccg.E_RANGE),
+                       (1 << 9, sccg.E_ARG)):
+        s = sccg.Sums(*[getattr(base, f) for f in sccg.SUMS_FIELDS])
+        s.status = bits
+        jj, pp = ctypes.c_double(0.0), ctypes.c_double(0.0)
+        assert lib.sccg_jaccard(ctypes.byref(s), ctypes.byref(jj), ctypes.byref(pp)) == code
+        assert math.isnan(jj.value) and math.isnan(pp.value)
+        with pytest.raises(sccg.SccgError):
+            sccg.jaccard(s)
+    assert lib.sccg_contains(None, None, None, 0, None, None, None) == sccg.E_ARG
+    t = sccg.Tiling(0, 0, 0, 10, 1, 1)
+    assert lib.sccg_report(None, None, None, 0, None, None, None, None, ctypes.byref(t), None, None) == sccg.E_ARG
+    assert lib.sccg_sums_pack(None, None, None) == sccg.E_ARG
+    assert lib.sccg_sums_unpack(8, 12, None) == sccg.E_ARG

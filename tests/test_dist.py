@@ -72,7 +72,8 @@ def _free_port():
 
 
 @pytest.mark.timeout(300)
-def test_gloo_two_ranks_allreduce_is_exact():
+@pytest.mark.parametrize("world", [2, 3])
+def test_gloo_ranks_allreduce_is_exact(world):
     import oracle
     import paper_1208_0277_b200 as sccg
 
@@ -81,13 +82,13 @@ def test_gloo_two_ranks_allreduce_is_exact():
     mgr = ctx.Manager()
     out = mgr.dict()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, images, out)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, images, out)) for r in range(world)]
     for p in procs:
         p.start()
     for p in procs:
         p.join(240)
         assert p.exitcode == 0
-    assert out[0] == out[1]
+    assert all(out[r] == out[0] for r in range(world))
     # single-process reference over all images
     ref = [0] * 11
     allpairs = []
@@ -143,3 +144,46 @@ def test_band_shards_degenerate():
         assert set(pi.tolist()) <= {0, 1, 2}
     with pytest.raises(ValueError):
         sdist.band_shards([0], [1], [0], [1], 0)
+
+
+def _status_worker(rank, world, port, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    # rank r: additive fields r + 1, status bits: every rank sets ARG (bit 0); rank 0 STACK (bit 3), rank 1
+    # CAPACITY (bit 4) -- a plain SUM would carry 1 + 1 into bit 1 and lose bit 0
+    st = 1 | (8 if rank == 0 else 0) | (16 if rank == 1 else 0)
+    v = torch.tensor([rank + 1] * 10 + [st], dtype=torch.int64)
+    sdist.allreduce_sums(v)
+    out[rank] = v.tolist()
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.timeout(120)
+@pytest.mark.parametrize("world", [2, 3])
+def test_gloo_allreduce_ors_status_bits(world):
+    """the status word is an OR of SCCG_STATUS_* bits, never summed
+    across ranks (pack: bits as 0/1 counts, one SUM, unpack: count > 0)."""
+    ctx = mp.get_context("spawn")
+    mgr = ctx.Manager()
+    out = mgr.dict()
+    port = _free_port()
+    procs = [ctx.Process(target=_status_worker, args=(r, world, port, out)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(100)
+        assert p.exitcode == 0
+    want = [sum(range(1, world + 1))] * 10 + [1 | 8 | 16]
+    for r in range(world):
+        assert out[r] == want
+
+
+def test_pack_unpack_host_mirror():
+    v = torch.tensor(list(range(10)) + [0b10110], dtype=torch.int64)
+    vec = sdist.pack_sums(v)
+    assert vec.shape[0] == sdist.REDUCE_WORDS and vec[:10].tolist() == list(range(10))
+    assert vec[10:].tolist() == [0, 1, 1, 0, 1] + [0] * 11
+    back = sdist.unpack_sums(vec * 3, torch.zeros(11, dtype=torch.int64))  # three ranks with the same bits
+    assert back[:10].tolist() == [3 * i for i in range(10)] and int(back[10]) == 0b10110

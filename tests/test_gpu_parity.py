@@ -437,8 +437,8 @@ def test_pixelbox_edge_cases(sccg, tile_sets):
     assert sccg.jaccard(sums)[0] == 1.0
     # out-of-range pair index: skipped and flagged, never read out of bounds
     bad = torch.tensor([[0, 10**6]], dtype=torch.int32, device="cuda")
-    _, _, sums = sccg.pixelbox(P, Q, bad)
-    assert sums.cpu().tolist()[10] != 0
+    _, _, sums = sccg.pixelbox(P, Q, bad, check=False)
+    assert sums.cpu().tolist()[10] == sccg.STATUS_ARG
 
 
 def test_sums_accumulate_and_launch_shape_invariance(sccg, tile_sets):
@@ -492,7 +492,8 @@ def test_async_pipeline_matches_sync(sccg, tile_sets):
 
 def test_missing_polygons_and_contains(sccg, tile_sets):
     """NEXT(f3)/(f4): missing-polygon counts from the kernels' hit
-    bitmaps, and ST_Contains by areas, against the oracle."""
+    bitmaps, and ST_Contains by areas (sccg_contains), against the
+    oracle's pixel-set definitions."""
     A, B = tile_sets
     for cfg in ("tile", "skewed"):
         if cfg == "skewed":
@@ -504,9 +505,65 @@ def test_missing_polygons_and_contains(sccg, tile_sets):
         pn = pairs.cpu().numpy()
         ei, _ = oracle.pair_areas(A, B, pn)
         assert sccg.missing_polygons(hits, P, Q) == (oracle.missing(A.n, pn, ei, 0), oracle.missing(B.n, pn, ei, 1))
-        aq, _ = oracle.set_props(B)
-        got = sccg.contains(inter, Q.area[pairs[:, 1].long()]).cpu().numpy()
-        assert (got == (ei == aq[pn[:, 1]])).all()
+        got = sccg.contains(P, Q, pairs, inter).cpu().numpy()
+        assert (got == oracle.contains_pairs(A, B, pn)).all()
+    # hand-made containment cases: nested, identical, sharing sides, L-shape notch, overlap, disjoint MBR pair
+    sq = lambda x, y, w, h: [[x, y], [x + w, y], [x + w, y + h], [x, y + h]]
+    L = lambda x, y: [[x, y], [x + 6, y], [x + 6, y + 3], [x + 3, y + 3], [x + 3, y + 6], [x, y + 6]]
+    cases = [(sq(0, 0, 8, 8), sq(2, 2, 3, 3), 1), (sq(2, 2, 3, 3), sq(0, 0, 8, 8), 2), (sq(0, 0, 4, 4), sq(0, 0, 4, 4), 3),
+             (sq(0, 0, 8, 8), sq(0, 0, 8, 3), 1), (L(0, 0), sq(3, 3, 3, 3), 0), (L(0, 0), sq(0, 0, 3, 6), 1),
+             (sq(0, 0, 4, 4), sq(2, 2, 4, 4), 0), (sq(0, 0, 40, 40), sq(5, 5, 30, 30), 1)]
+    PP = synth.pack([np.asarray(a, np.int32) + np.array([100 * i, 0], np.int32) for i, (a, _, _) in enumerate(cases)])
+    QQ = synth.pack([np.asarray(b, np.int32) + np.array([100 * i, 0], np.int32) for i, (_, b, _) in enumerate(cases)])
+    P, Q = dev(PP, sccg), dev(QQ, sccg)
+    pairs = torch.tensor([[i, i] for i in range(len(cases))], dtype=torch.int32, device="cuda")
+    inter, _, _ = sccg.pixelbox(P, Q, pairs)
+    got = sccg.contains(P, Q, pairs, inter).cpu().numpy().tolist()
+    assert got == [c for _, _, c in cases]
+    assert got == oracle.contains_pairs(PP, QQ, pairs.cpu().numpy()).tolist()
+
+
+def _report_check(sccg, A, B, tiling):
+    P, Q = dev(A, sccg), dev(B, sccg)
+    pairs = sccg.filter_pairs(P, Q)
+    hits = sccg.new_hits(P, Q)
+    inter, uni, sums = sccg.pixelbox(P, Q, pairs, hits=hits)
+    got = sccg.tile_report(P, Q, pairs, inter, uni, hits, tiling).cpu().numpy()
+    pn = pairs.cpu().numpy()
+    ei, eu = oracle.pair_areas(A, B, pn)
+    want = oracle.report(A, B, pn, ei, eu, tiling)
+    limbs = slice(6, 10)
+    units = lambda r: sum(int(v) << (30 * k) for k, v in enumerate(r[limbs]))
+    for t in range(got.shape[0]):
+        g, w = got[t].tolist(), want[t].tolist()
+        assert g[:6] == w[:6] and g[10:] == w[10:], (t, g, w)
+        assert units(got[t]) == units(want[t]), t
+    rep = sccg.similarity_report(P, Q, pairs, inter, uni, hits, tiling)
+    ex = oracle.jaccard_exact(ei, eu)
+    assert abs(rep["jaccard"] - float(ex)) <= 1e-12 * float(ex)
+    assert (rep["missing_p"], rep["missing_q"]) == (oracle.missing(A.n, pn, ei, 0), oracle.missing(B.n, pn, ei, 1))
+    for t in rep["tiles"]:
+        row = want[t["tile_id"]]
+        if row[1]:
+            exact = Fraction(units(row), 1 << 116) / int(row[1])
+            assert abs(t["jaccard"] - float(exact)) <= 1e-12 * float(exact)
+        else:
+            assert t["jaccard"] is None
+    return got
+
+
+def test_tile_report_matches_oracle(sccg, tile_sets):
+    """NEXT(f3): the per-tile SimilarityReport (reading R22) --
+    pair totals, exact ratio limbs, per-tile J', polygon and missing counts --
+    against the oracle's report, on a 3 x 3 grid over the tile set, a grid with
+    tiles outside the data (clamping), the skewed image and the whole slide
+    (25 x 25 tiles of 4096)."""
+    A, B = tile_sets
+    _report_check(sccg, A, B, (0, 0, 1500, 1500, 3, 3))
+    _report_check(sccg, A, B, (-1000, 500, 700, 900, 5, 4))
+    _report_check(sccg, *synth.generate("skewed", width=8192, height=8192), (0, 0, 4096, 4096, 2, 2))
+    got = _report_check(sccg, *synth.generate("slide"), (0, 0, 4096, 4096, 25, 25))
+    assert (got[:, 0] > 0).sum() > 500
 
 
 def test_maximum_sizes_closed_form(sccg):
@@ -565,8 +622,10 @@ def test_abi_errors(sccg):
 # --------------------------------------------------- full bench configuration
 def test_slide_full_size(sccg):
     """Config 2 (the bench workload) at full size, in the bench's launch
-    configuration: the whole pair list equals the oracle's sweep join, sampled
-    pairs are bit-exact, and size-independent properties hold for all pairs."""
+    configuration: the whole pair list equals the oracle's sweep join, EVERY
+    pair's (I, U) equals the oracle's pixel counts, the integer sums and the
+    ratio limbs equal the oracle-side totals, and J' is within 1e-12 of the
+    exact rational mean."""
     A, B = synth.generate("slide")
     P, Q = dev(A, sccg), dev(B, sccg)
     pairs = sccg.filter_pairs(P, Q)
@@ -574,28 +633,170 @@ def test_slide_full_size(sccg):
     want = oracle.join(A, B)
     assert pn.shape == want.shape and (pn == want).all()
     inter, uni, sums = sccg.pixelbox(P, Q, pairs)
-    gi, gu = inter.cpu().numpy(), uni.cpu().numpy()
-    rng = np.random.default_rng(2)
-    idx = np.sort(rng.choice(len(pn), size=20000, replace=False))
-    ei, eu = oracle.pair_areas(A, B, pn[idx])
-    assert (gi[idx] == ei).all() and (gu[idx] == eu).all()
-    ap, _ = oracle.set_props(A)
-    aq, _ = oracle.set_props(B)
-    a_p, a_q = ap[pn[:, 0]], aq[pn[:, 1]]
-    assert (gi >= 0).all() and (gi <= np.minimum(a_p, a_q)).all()
-    assert (gi + gu == a_p + a_q).all() and (gu >= np.maximum(a_p, a_q)).all()
-    s = sums.cpu().tolist()
-    assert s[0] == len(pn) and s[2] == int(gi.sum()) and s[4] == int(a_p.sum()) and s[5] == int(a_q.sum())
-    assert s[1] == int((gi > 0).sum()) and s[10] == 0
-    assert sum(l << (30 * i) for i, l in enumerate(s[6:10])) == exact_ratio_units(gi, gu)
+    ei, eu = check_batch(sccg, A, B, pn, inter, uni, sums)  # all pairs, sums, limbs, J'
     # determinism across thresholds and pixelization schedules: per-pair results identical
     i2, u2, s2 = sccg.pixelbox(P, Q, pairs, threshold=64)
     assert torch.equal(i2, inter) and torch.equal(s2, sums)
     i3, u3, s3 = sccg.pixelbox(P, Q, pairs, raster=False)
     assert torch.equal(i3, inter) and torch.equal(s3, sums)
-    # the bench's launch configuration (device-resident pipeline, CUDA graphs)
+    # the bench's launch configuration (device-resident pipeline, CUDA graphs, outputs written every step)
     pipe = sccg.Pipeline(P, Q, cap=3 * max(P.n, Q.n) + 1024, graph=True)
     for _ in range(2):
         ps = pipe.run()
     assert pipe.check() == len(pn)
     assert torch.equal(ps, sums)
+    n = len(pn)
+    assert torch.equal(pipe.inter[:n], inter) and torch.equal(pipe.uni[:n], uni)
+
+
+def test_skewed_full_size(sccg):
+    """Config 3 at full size (16384^2, nuclei + glands): every pair against the
+    oracle (join, per-pair areas, sums, limbs, J')."""
+    A, B = synth.generate("skewed")
+    P, Q = dev(A, sccg), dev(B, sccg)
+    pairs = sccg.filter_pairs(P, Q)
+    pn = pairs.cpu().numpy()
+    assert pn.tolist() == oracle.join(A, B).tolist()
+    inter, uni, sums = sccg.pixelbox(P, Q, pairs)
+    check_batch(sccg, A, B, pn, inter, uni, sums)
+    pipe = sccg.Pipeline(P, Q, graph=True)
+    pipe.run()
+    assert pipe.check() == len(pn) and torch.equal(pipe.sums, sums)
+
+
+def test_combs_full_size(sccg):
+    """Config 5 analog at full size (16,384 comb pairs, 500-2000 vertices):
+    EVERY pair pinned by its rectangle-decomposition closed form, and a seeded
+    512-pair subset by the oracle's brute-force pixel counts."""
+    A, B, (RA, RB) = combs.generate(want_rects=True)
+    P, Q = dev(A, sccg), dev(B, sccg)
+    pairs = sccg.filter_pairs(P, Q)
+    n = A.n
+    assert pairs.cpu().numpy().tolist() == [[k, k] for k in range(n)]
+    inter, uni, sums = sccg.pixelbox(P, Q, pairs)
+    gi, gu = inter.cpu().numpy(), uni.cpu().numpy()
+    wi = np.array([combs.rect_decomp_intersection(RA[k], RB[k]) for k in range(n)], np.int64)
+    wa = np.array([combs.rect_decomp_area(RA[k]) for k in range(n)], np.int64)
+    wb = np.array([combs.rect_decomp_area(RB[k]) for k in range(n)], np.int64)
+    bad = np.nonzero(gi != wi)[0]
+    assert len(bad) == 0, (bad[:5], gi[bad[:5]], wi[bad[:5]])
+    assert (gu == wa + wb - wi).all()
+    s = sums.cpu().tolist()
+    assert s[0] == n and s[1] == int((wi > 0).sum()) and s[2] == int(wi.sum()) and s[10] == 0
+    assert s[4] == int(wa.sum()) and s[5] == int(wb.sum())
+    assert sum(l << (30 * i) for i, l in enumerate(s[6:10])) == exact_ratio_units(wi, wa + wb - wi)
+    idx = np.sort(np.random.default_rng(5).choice(n, size=512, replace=False))
+    ei, eu = oracle.pair_areas(A, B, pairs.cpu().numpy()[idx])
+    assert (ei == gi[idx]).all() and (eu == gu[idx]).all()
+
+
+def _ring_variant(ring, rng, kind):
+    """The same pixel set, written differently (DESIGN R2/R3): clockwise,
+    duplicated consecutive vertices, extra collinear vertices, or the first
+    vertex repeated at the end."""
+    r = [tuple(int(c) for c in v) for v in np.asarray(ring)]
+    if kind == "cw":
+        return np.asarray(r[::-1], np.int32)
+    if kind == "closing":
+        return np.asarray(r + [r[0]], np.int32)
+    out = []
+    for i, a in enumerate(r):
+        b = r[(i + 1) % len(r)]
+        out.append(a)
+        if kind == "dup" and rng.random() < 0.3:
+            out.append(a)
+        if kind == "collinear" and rng.random() < 0.5:
+            dx, dy = np.sign(b[0] - a[0]), np.sign(b[1] - a[1])
+            ln = abs(b[0] - a[0]) + abs(b[1] - a[1])
+            if ln >= 2:
+                t = int(rng.integers(1, ln))
+                out.append((a[0] + t * dx, a[1] + t * dy))
+    return np.asarray(out, np.int32)
+
+
+@pytest.mark.parametrize("kind", ["cw", "dup", "collinear", "closing", "mixed"])
+def test_ring_variants_same_results(sccg, tile_sets, kind):
+    """Input contract (sccg.h, DESIGN R2/R3): either orientation, duplicate or
+    collinear consecutive vertices and a repeated closing vertex are accepted
+    (validation on) and change nothing: per-pair results equal the oracle's on
+    the rewritten rings and the GPU's on the plain rings, bit for bit."""
+    A, B = tile_sets
+    rng = np.random.default_rng(hash(kind) & 0xFFFF)
+    kinds = ["cw", "dup", "collinear", "closing"]
+    pick = (lambda: kinds[int(rng.integers(4))]) if kind == "mixed" else (lambda: kind)
+    A2 = synth.pack([_ring_variant(A.ring(i), rng, pick()) for i in range(A.n)])
+    B2 = synth.pack([_ring_variant(B.ring(i), rng, pick()) for i in range(B.n)])
+    P, Q = dev(A, sccg), dev(B, sccg)
+    P2, Q2 = dev(A2, sccg), dev(B2, sccg)  # validate=True: no status bits
+    assert P2.status.cpu().tolist()[0] == 0 and Q2.status.cpu().tolist()[0] == 0
+    assert torch.equal(P2.area, P.area) and torch.equal(P2.mbr, P.mbr)
+    pairs = sccg.filter_pairs(P, Q)
+    pairs2 = sccg.filter_pairs(P2, Q2)
+    assert torch.equal(pairs, pairs2)
+    for T in (64, 2048):
+        ref = sccg.pixelbox(P, Q, pairs, threshold=T)
+        for raster in (True, False):
+            got = sccg.pixelbox(P2, Q2, pairs2, threshold=T, raster=raster)
+            assert torch.equal(got[0], ref[0]) and torch.equal(got[1], ref[1]) and torch.equal(got[2], ref[2])
+    check_batch(sccg, A2, B2, pairs2.cpu().numpy(), *sccg.pixelbox(P2, Q2, pairs2))
+
+
+def test_async_overflow_sets_status(sccg, tile_sets):
+    """ADVICE r1: a join that overflows the pair buffer leaves it incomplete;
+    sccg_pixelbox_async then processes nothing and flags SCCG_STATUS_CAPACITY,
+    so the sums are never silently wrong, and sccg_jaccard rejects them."""
+    A, B = tile_sets
+    P, Q = dev(A, sccg), dev(B, sccg)
+    pipe = sccg.Pipeline(P, Q, cap=10, graph=False)
+    s = pipe.run().cpu().tolist()
+    assert s[10] & sccg.STATUS_CAPACITY and s[0] == 0
+    with pytest.raises(sccg.SccgError) as e:
+        sccg.jaccard(s)
+    assert e.value.code == sccg.E_CAPACITY
+    # an out-of-range pair index: flagged, and pixelbox(check=True) raises
+    bad = torch.tensor([[0, 10**6]], dtype=torch.int32, device="cuda")
+    with pytest.raises(sccg.SccgError):
+        sccg.pixelbox(P, Q, bad)
+
+
+def test_sums_pack_unpack_and_nccl(sccg, tile_sets):
+    """Row a9 on the GPU: sccg_sums_pack / unpack equal the host mirror, and the
+    packed vector goes through a real NCCL all_reduce (world size 1, also
+    captured in a CUDA graph) and unpacks to the same sums."""
+    import os
+
+    import torch.distributed as dist
+
+    from paper_1208_0277_b200 import dist as sdist
+
+    A, B = tile_sets
+    P, Q = dev(A, sccg), dev(B, sccg)
+    _, _, sums = sccg.pixelbox(P, Q, sccg.filter_pairs(P, Q))
+    sums[10] = 0b10101
+    vec = sccg.sums_pack(sums)
+    assert vec.cpu().tolist() == sdist.pack_sums(sums.cpu()).tolist()
+    back = sccg.sums_unpack(vec * 3, torch.zeros_like(sums))
+    assert back.cpu().tolist() == sdist.unpack_sums(vec.cpu() * 3, torch.zeros(11, dtype=torch.int64)).tolist()
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29731")
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        ref = sums.clone()
+        out = sdist.allreduce_sums(sums.clone(), force=True)
+        assert torch.equal(out, ref)
+        g = torch.cuda.CUDAGraph()
+        buf = sums.clone()
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            sdist.allreduce_sums(buf, force=True)  # warm-up outside capture
+        torch.cuda.current_stream().wait_stream(s)
+        torch.cuda.synchronize()
+        with torch.cuda.graph(g):
+            sdist.allreduce_sums(buf, force=True)
+        for _ in range(3):
+            g.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(buf, ref)
+    finally:
+        dist.destroy_process_group()

@@ -373,3 +373,110 @@ def test_missing_polygons(tile_sets):
     # set B drops ~5 % of A's nuclei (synth recipe): A has about that many missing
     assert 0.02 * a.n < ma < 0.10 * a.n and 0 <= mb < 0.15 * b.n
     assert oracle.missing(7, np.zeros((0, 2)), [], 0) == 7
+
+
+# ------------------------------------------- closed join, missing, contains, report
+def test_join_closed_pinned_by_lattice_points():
+    """The closed-box join (oracle_join_nested_closed, the ST_Touches
+    candidates) against brute force on lattice points: two closed integer boxes
+    meet iff some integer point lies in both -- touching sides and corners
+    included, gaps excluded."""
+    rng = np.random.default_rng(41)
+    for trial in range(25):
+        n, m = (int(v) for v in rng.integers(1, 25, 2))
+
+        def boxes(k):
+            lo = rng.integers(0, 16, (k, 2))
+            wh = rng.integers(1, 6, (k, 2))
+            return np.concatenate([lo, lo + wh], 1).astype(np.int32)
+
+        bp, bq = boxes(n), boxes(m)
+        pts = lambda b: {(x, y) for x in range(b[0], b[2] + 1) for y in range(b[1], b[3] + 1)}
+        sp, sq = [pts(b) for b in bp], [pts(b) for b in bq]
+        exp = [[i, j] for i in range(n) for j in range(m) if sp[i] & sq[j]]
+        assert oracle.join_mbrs(bp, bq, "closed").tolist() == exp
+    side = np.array([[0, 0, 2, 2]], np.int32)
+    assert oracle.join_mbrs(side, np.array([[2, 0, 4, 2]], np.int32), "closed").tolist() == [[0, 0]]  # shared side
+    assert oracle.join_mbrs(side, np.array([[2, 2, 3, 3]], np.int32), "closed").tolist() == [[0, 0]]  # corner
+    assert oracle.join_mbrs(side, np.array([[3, 0, 4, 2]], np.int32), "closed").shape[0] == 0  # gap
+
+
+def _sq(x, y, w, h):
+    return [[x, y], [x + w, y], [x + w, y + h], [x, y + h]]
+
+
+def test_missing_hand_built():
+    """P:63 missing polygons on a hand-built pair of sets with known answers:
+    P = five squares; Q matches square 0 exactly, splits square 1 into two
+    halves, drops square 2, overlaps square 3 and adds a spurious far square,
+    and only touches square 4 (a shared side: no common pixel)."""
+    P = synth.pack([_sq(0, 0, 4, 4), _sq(10, 0, 4, 4), _sq(20, 0, 4, 4), _sq(30, 0, 4, 4), _sq(40, 0, 4, 4)])
+    Q = synth.pack([_sq(0, 0, 4, 4), _sq(10, 0, 2, 4), _sq(12, 0, 2, 4), _sq(31, 1, 4, 4), _sq(100, 100, 3, 3),
+                    _sq(44, 0, 2, 4)])
+    for kind in ("sweep", "closed"):
+        pairs = oracle.join(P, Q, kind)
+        inter, _ = oracle.pair_areas(P, Q, pairs)
+        assert oracle.missing(P.n, pairs, inter, 0) == 2  # squares 2 and 4
+        assert oracle.missing(Q.n, pairs, inter, 1) == 2  # the spurious and the touching square
+    assert oracle.join(P, Q, "closed").tolist() == [[0, 0], [1, 1], [1, 2], [3, 3], [4, 5]]
+
+
+def test_contains_rectangles_and_polyominoes():
+    """ST_Contains on the pixel model, pinned by interval containment of
+    rectangles (closed form) and by bitboard subset tests on all pairs of clean
+    3x3 polyominoes at offsets in [-1, 1]^2."""
+    rng = np.random.default_rng(43)
+    for _ in range(300):
+        a = [int(v) for v in rng.integers(0, 10, 2)] + [int(v) for v in rng.integers(1, 8, 2)]
+        b = [int(v) for v in rng.integers(0, 10, 2)] + [int(v) for v in rng.integers(1, 8, 2)]
+        inside = lambda u, v: u[0] <= v[0] and v[0] + v[2] <= u[0] + u[2] and u[1] <= v[1] and v[1] + v[3] <= u[1] + u[3]
+        assert oracle.contains(_sq(*a), _sq(*b)) == inside(a, b)
+    polys = []
+    for bits in range(1, 512):
+        m = np.array([(bits >> i) & 1 for i in range(9)], np.uint8).reshape(3, 3)
+        ring, cleaned = synth.trace_mask(m)
+        if ring is not None and (cleaned == m).all():
+            polys.append((ring, bits))
+    cells = lambda bits, dx, dy: {(i % 3 + dx, i // 3 + dy) for i in range(9) if (bits >> i) & 1}
+    for (ra, ba), (rb, bb) in itertools.product(polys[::4], polys[::5]):
+        for dx, dy in itertools.product((-1, 0, 1), repeat=2):
+            got = oracle.contains(ra, rb + np.array([dx, dy], np.int32))
+            assert got == (cells(bb, dx, dy) <= cells(ba, 0, 0)), (ba, bb, dx, dy)
+
+
+def test_report_hand_built_and_totals(tile_sets):
+    """The per-tile report (reading R22) on a hand-built 2 x 2
+    grid with known per-tile answers, and on the tile sets: the tiles add up to
+    the global sums, J' and missing counts (each pinned on its own)."""
+    P = synth.pack([_sq(0, 0, 4, 4), _sq(10, 0, 4, 4), _sq(60, 5, 4, 4), _sq(5, 60, 2, 2)])
+    Q = synth.pack([_sq(1, 1, 4, 4), _sq(10, 0, 4, 4), _sq(58, 5, 4, 2), _sq(90, 90, 2, 2)])
+    pairs = oracle.join(P, Q)
+    assert pairs.tolist() == [[0, 0], [1, 1], [2, 2]]
+    inter, uni = oracle.pair_areas(P, Q, pairs)
+    assert inter.tolist() == [9, 16, 4] and uni.tolist() == [23, 16, 20]
+    rows = oracle.report(P, Q, pairs, inter, uni, (0, 0, 50, 50, 2, 2))
+    f = {k: i for i, k in enumerate(oracle.REPORT_FIELDS)}
+    # tile 0 (x < 50, y < 50): pairs (0, 0), (1, 1); tile 1: pair (2, 2) (p = square at x 60); tile 2: P's
+    # square at (5, 60), missing; tile 3: Q's far square, missing
+    assert rows[:, f["n_pairs"]].tolist() == [2, 1, 0, 0]
+    assert rows[:, f["n_nonzero"]].tolist() == [2, 1, 0, 0]
+    assert rows[:, f["sum_inter"]].tolist() == [25, 4, 0, 0]
+    assert rows[:, f["sum_union"]].tolist() == [39, 20, 0, 0]
+    assert rows[:, f["n_poly_p"]].tolist() == [2, 1, 1, 0] and rows[:, f["n_poly_q"]].tolist() == [2, 1, 0, 1]
+    assert rows[:, f["missing_p"]].tolist() == [0, 0, 1, 0] and rows[:, f["missing_q"]].tolist() == [0, 0, 0, 1]
+    units = lambda r: sum(int(r[f["limb0"] + k]) << (30 * k) for k in range(4))
+    assert units(rows[0]) == int(Fraction(9 / 23) * (1 << 116)) + (1 << 116)  # 9/23 and exactly 1
+    assert units(rows[1]) == int(Fraction(4 / 20) * (1 << 116))
+    # tile sets over a 3 x 3 grid: the tiles add up to the global totals
+    a, b = tile_sets
+    pairs = oracle.join(a, b)
+    inter, uni = oracle.pair_areas(a, b, pairs)
+    rows = oracle.report(a, b, pairs, inter, uni, (0, 0, 1500, 1500, 3, 3))
+    s = oracle.sums(a, b, pairs, inter, uni)
+    for k in ("n_pairs", "n_nonzero", "sum_inter", "sum_union", "sum_area_p", "sum_area_q"):
+        assert int(rows[:, f[k]].sum()) == s[k], k
+    assert int(rows[:, f["missing_p"]].sum()) == oracle.missing(a.n, pairs, inter, 0)
+    assert int(rows[:, f["missing_q"]].sum()) == oracle.missing(b.n, pairs, inter, 1)
+    assert int(rows[:, f["n_poly_p"]].sum()) == a.n and int(rows[:, f["n_poly_q"]].sum()) == b.n
+    tot = sum(units(r) for r in rows)
+    assert abs(Fraction(tot, 1 << 116) / s["n_nonzero"] - oracle.jaccard_exact(inter, uni)) < Fraction(1, 10**12)
