@@ -41,9 +41,9 @@ ISSUE_LANES_PER_CLK_SM = 128  # 4 SMSPs x 1 warp-instruction x 32 lanes (nominal
 ALU_LANES_PER_CLK_SM = 64  # measured: ALU pipe 2 warp-inst/clk/SM (profiles/int_peak.json, scripts/int_peak.cu)
 STAGE_EVERY = 10  # per-stage CUDA events on every 10th timed step
 # our kernels per step besides the read-back (one GPU) or the sums pack + unpack around the all-reduce (N > 1):
-# sums reset, prep init, prep, join (grid selection, Q count, Q fill, probe, compaction; CUB's two scan kernels
-# are not counted), PixelBox (counter reset, small, item)
-LAUNCHES_PER_STEP = 11
+# sums reset, prep init, prep, join (grid selection, Q insert, probe, compaction), PixelBox (counter reset, small,
+# item)
+LAUNCHES_PER_STEP = 10
 OPS_PER_ROWTEST = 3  # sub, unsigned compare, predicated xor
 OPS_PER_BOXEDGE = 8  # one lane classifying one edge against all sub-boxes of a split (minimum)
 

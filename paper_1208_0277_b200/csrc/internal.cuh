@@ -108,6 +108,40 @@ struct Carve {
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
 
+// Control words a predecessor kernel of a PDL chain wrote (a grid
+// descriptor, a device-side count) are read with L1-bypassing loads after
+// pdl_wait(): a CTA launched early may otherwise see a stale L1 / read-only
+// cache line of a recycled address (measured on the join's grid descriptor).
+__device__ __forceinline__ long long ld_coherent(const long long* p) {
+  long long v;
+  asm volatile("ld.relaxed.gpu.global.s64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Where a kernel lets its successor launch.  Early (SCCG_PDL_LATE=0, the
+// round-1 order): trigger at entry, so the successor's CTAs -- and, since
+// they trigger at entry too, every later kernel's -- can become resident
+// while this one still runs, holding registers and warp slots as they wait.
+// Late (default): a kernel triggers after its own wait, and the two big
+// persistent kernels (prep, the small PixelBox kernel) only once their work
+// queue is drained, so at most the next kernel waits resident.
+#ifndef SCCG_PDL_LATE
+#define SCCG_PDL_LATE 1
+#endif
+__device__ __forceinline__ void pdl_entry() {
+  if (!SCCG_PDL_LATE) pdl_trigger();
+  pdl_wait();
+  if (SCCG_PDL_LATE) pdl_trigger();
+}
+// for kernels that trigger themselves once their main loop is done
+__device__ __forceinline__ void pdl_entry_deferred() {
+  if (!SCCG_PDL_LATE) pdl_trigger();
+  pdl_wait();
+}
+__device__ __forceinline__ void pdl_done() {
+  if (SCCG_PDL_LATE) pdl_trigger();
+}
+
 template <typename... KArgs, typename... Args>
 cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
                        Args&&... args) {

@@ -1,37 +1,102 @@
-// join.cu -- MBR-overlap join by a uniform grid hash.
+// join.cu -- MBR-overlap join by a hashed uniform grid, in
+// four launches.
 //
 // The paper's filter stage searches a Hilbert R-tree on one CPU thread
 // (§4.1) to produce "an array of polygon pairs with intersecting
 // MBRs"; the predicate is the `&&` MBR test of Fig. 1(b), here
 // half-open (reading R4).  On the GPU a uniform grid of 2^k-pixel cells is
-// cheaper: Q's MBRs are bucketed into every cell they cover, each P MBR probes
+// cheaper: Q's MBRs are inserted into every cell they cover, each P MBR probes
 // its cells, and a pair is emitted only from the cell holding its reference
-// point (max xlo, max ylo) so it is found exactly once.  Each P's pairs are
-// written to its own segment (one-pass probe with a decoupled look-back scan
-// of per-P counts) and sorted by q in place, so the output is sorted by (p, q)
-// without a global sort.
+// point (max xlo, max ylo) so it is found exactly once.
 //
-// The cell size is chosen on the device from the per-set statistics sccg_prep
-// gathered (no host round trip); the only host synchronisation is the final
-// pair count the ABI returns.
-#include <cub/device/device_scan.cuh>
-
+//   1. grid_select_kernel -- clears the bucket counters and the probe's tile
+//      states; one warp picks the cell size 2^k and the bucket wrap from the
+//      per-set statistics sccg_prep gathered (no host round trip).
+//   2. grid_insert_kernel -- each Q MBR takes a slot in the bucket of every
+//      cell it covers (fixed-capacity buckets, an overflow chain past
+//      kSlots): no count pass and no scan.
+//   3. probe_kernel<false> -- thread per P (a warp per P that covers many
+//      cells) counts its pairs, the CTA scans the counts and writes each P's
+//      pairs, sorted by q, into the tile's own bucket.
+//   4. probe_kernel<true> -- each tile sums the preceding tiles' counts for
+//      its offset and copies its bucket into place: the output is sorted by
+//      (p, q) without a global sort.  (A single pass with a decoupled
+//      look-back was measured 2-3x slower: a tile whose P sit in a crowded
+//      cluster holds back every tile after it, and the waiting CTAs hold the
+//      SMs.)
+//
+// Cells are hashed onto 2^ax x 2^ay buckets by wrapping (a torus: bucket =
+// (cy mod 2^ay, cx mod 2^ax)), so the cell size is not bound by the memory a
+// dense grid over the whole slide would take; the wrap is at least as wide
+// and tall as the largest Q MBR's cell span, so no Q MBR lands twice in one
+// bucket, which -- with the reference-point rule -- keeps every pair emitted
+// exactly once (proof in DESIGN.md §6, "join").
 #include "internal.cuh"
 
 namespace sccg {
 
-struct Grid {
-  int k, cx0, cy0, ncx, ncy, empty;
-  __device__ __forceinline__ int cell(int x, int y) const { return ((y >> k) - cy0) * ncx + ((x >> k) - cx0); }
+struct __align__(16) Grid {
+  int k, ax, ay, empty;
+  __device__ __forceinline__ int bucket(int cx, int cy) const {
+    return ((cy & ((1 << ay) - 1)) << ax) | (cx & ((1 << ax) - 1));
+  }
 };
+
+// The grid is written by the selection kernel two launches earlier: read it
+// with an L1-bypassing load (ld.relaxed.gpu), never through the read-only /
+// L1 path -- under programmatic dependent launch a CTA that started early
+// could otherwise see a stale copy of a recycled workspace (measured: a
+// previous join's grid at the same address).
+__device__ __forceinline__ Grid load_grid(const Grid* gp) {
+  const int* w = reinterpret_cast<const int*>(gp);
+  Grid g;
+  asm volatile("ld.relaxed.gpu.global.v4.s32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(g.k), "=r"(g.ax), "=r"(g.ay), "=r"(g.empty)
+               : "l"(w)
+               : "memory");
+  return g;
+}
 
 __device__ __forceinline__ bool mbr_empty(const int4& m) { return m.x >= m.z || m.y >= m.w; }
 
-static int64_t cell_cap(int64_t np, int64_t nq) { return np + nq + 1024; }
+// A bucket's entries live in kLevels levels of kLevelSlots slots: entry j of
+// bucket b is slot (j / kLevelSlots, b, j % kLevelSlots) of a level-major
+// array, so the first four entries of neighbouring buckets share cache lines
+// (level 0 is the dense part; the higher levels are touched only by crowded
+// buckets), and every slot address is known before the bucket's count is
+// read.  Past kSlots entries an overflow chain takes the rest.
+#ifndef SCCG_JOIN_CSTRIDE
+#define SCCG_JOIN_CSTRIDE 1  // bucket counters per int of spacing (8: one per 32-byte sector)
+#endif
+constexpr int kCStride = SCCG_JOIN_CSTRIDE;
+#ifndef SCCG_JOIN_LEVELS
+#define SCCG_JOIN_LEVELS 8
+#endif
+constexpr int kLevelSlots = 4, kLevels = SCCG_JOIN_LEVELS, kSlots = kLevelSlots * kLevels;
+// 2^hb buckets, hb = ceil(log2(max(nq, 512))) (+ SCCG_JOIN_HB_EXTRA)
+#ifndef SCCG_JOIN_HB_EXTRA
+#define SCCG_JOIN_HB_EXTRA 0
+#endif
+static int bucket_bits(int64_t nq) {
+  int b = 9;
+  while (b < 27 && (int64_t(1) << b) < nq) b++;
+  return b + SCCG_JOIN_HB_EXTRA;
+}
+// An entry: a Q MBR (grown for the closed join) and its index in 16 bytes --
+// {xlo, ylo, (w - 1) | (h - 1) << 16, q} (w, h <= 65536 after growing).
+__device__ __forceinline__ int4 pack_entry(const int4& m, int q) {
+  return make_int4(m.x, m.y, (int)((unsigned)(m.z - m.x - 1) | ((unsigned)(m.w - m.y - 1) << 16)), q);
+}
+__device__ __forceinline__ int4 entry_box(const int4& e) {
+  return make_int4(e.x, e.y, e.x + (int)((unsigned)e.z & 0xffffu) + 1, e.y + (int)((unsigned)e.z >> 16) + 1);
+}
+// overflow pool: the grid selection only accepts cell sizes whose upper bound
+// on Q's cell incidences fits it, so it never runs out
 static int64_t entry_cap(int64_t nq) { return 8 * nq + 1024; }
 
-// Upper bound and expectation of the 2^k-cell entries of one set (SetStats).
-// `grow` = 1: the boxes are grown by one pixel on the high side (closed join).
+// Upper bound and expectation of the 2^k-cell incidences of one set
+// (SetStats).  `grow` = 1: the boxes are grown by one pixel on the high side
+// (closed join).
 __device__ __forceinline__ void set_entries(const SetStats* s, int k, int grow, double& bound, double& expect) {
   const double c = 1.0 / (double)(1ll << k), n = (double)s->nonempty;
   const double sw = (double)s->sw + grow * n, sh = (double)s->sh + grow * n;
@@ -42,19 +107,40 @@ __device__ __forceinline__ void set_entries(const SetStats* s, int k, int grow, 
   expect = n + (sw + sh) * c + swh * c * c;
 }
 
-// Cell size 2^k minimising the expected work E_p + E_q + C/4 + E_p E_q / C
-// (bucket inserts + probes + scan + candidate tests) subject to the workspace
-// caps on cells C and (upper-bounded) Q-entries.  Always feasible: once 2^k
-// exceeds the largest MBR extent each MBR covers at most 2 x 2 cells.
-__global__ void grid_select_kernel(const SetStats* __restrict__ sp, const SetStats* __restrict__ sq, long long ccap,
+__device__ __forceinline__ int ceil_log2(long long v) {
+  int b = 0;
+  while ((1ll << b) < v) b++;
+  return b;
+}
+
+// Cell size 2^k and bucket wrap.  Lane j evaluates k = 3 + j: the expected
+// work E_p + E_q + E_p * L / W (cell visits and inserts, candidate tests),
+// where the candidates per visit L = E_q / min(cells, buckets).  Cell visits
+// and inserts are dependent round trips (an atomic each for an insert) while
+// a candidate test is one more load in flight: W = 10 is fitted to the
+// measured join times of C2 and C3 at k = 5..9 ("join").
+// (SCCG_JOIN_PACK=1 adds a packing estimate of clustered nuclei -- the
+// number of Q MBRs of mean size w x h meeting a cell of side s when they tile
+// the plane, (s + w)(s + h) / (w h) / 4; measured slower: it picks smaller
+// cells, and more incidences cost more than the extra candidates.)
+// Feasible: the wrap covers the largest Q MBR's cell span and the incidence
+// bound fits the overflow pool; k = 30 always is.
+#ifndef SCCG_JOIN_PACK
+#define SCCG_JOIN_PACK 0
+#endif
+#ifndef SCCG_JOIN_TESTW
+#define SCCG_JOIN_TESTW 10.0
+#endif
+__global__ void grid_select_kernel(const SetStats* __restrict__ sp, const SetStats* __restrict__ sq, int hb,
                                    long long ecap, int grow, Grid* g, int4* __restrict__ zero, long long zero_n4) {
-  pdl_trigger();
-  // every CTA clears its share of the cell counts (zero_n4 int4s) ...
+  // No global access before the wait: under programmatic dependent launch
+  // this kernel starts while its predecessor drains, and the workspace may be
+  // memory a caching allocator just recycled from a buffer that predecessor
+  // still reads (clearing before the wait zeroed live data; measured).
+  pdl_entry();  // prep's statistics (and, for what follows, everything before)
+  // every CTA clears its share of the bucket counters ...
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < zero_n4; i += (long long)gridDim.x * blockDim.x)
     zero[i] = make_int4(0, 0, 0, 0);
-  pdl_wait();  // prep's statistics (and, for what follows, everything before)
-  // ... and CTA 0's first warp picks the cell size: lane j evaluates k = 3 + j
-  // (k <= 30), then an argmin over lanes
   const int lane = threadIdx.x & 31;
   if (blockIdx.x != 0 || threadIdx.x >= 32) return;
   const bool empty = sp->nonempty == 0 || sq->nonempty == 0;
@@ -62,44 +148,56 @@ __global__ void grid_select_kernel(const SetStats* __restrict__ sp, const SetSta
   const int xmax = max(sp->bounds[2], sq->bounds[2]) + grow, ymax = max(sp->bounds[3], sq->bounds[3]) + grow;
   const int k = 3 + lane;
   double cost = 1e300;
+  int ax = 0;
   if (!empty && k <= 30) {
-    const double ncx = (double)(((xmax - 1) >> k) - (xmin >> k) + 1);
-    const double ncy = (double)(((ymax - 1) >> k) - (ymin >> k) + 1);
-    const double C = ncx * ncy;
+    const long long ncx = (long long)(((xmax - 1) >> k) - (xmin >> k) + 1);
+    const long long ncy = (long long)(((ymax - 1) >> k) - (ymin >> k) + 1);
+    const int need_x = ceil_log2(((sq->maxext[0] - 1 + grow) >> k) + 2);
+    const int need_y = ceil_log2(((sq->maxext[1] - 1 + grow) >> k) + 2);
+    ax = min(max(ceil_log2(ncx), need_x), hb - need_y);
     double bp, ep, bq, eq;
     set_entries(sp, k, grow, bp, ep);
     set_entries(sq, k, grow, bq, eq);
-    if (C <= (double)ccap && bq <= (double)ecap) cost = ep + eq + 0.25 * C + ep * eq / C;
+#ifdef SCCG_JOIN_FORCE_K
+    if (k != SCCG_JOIN_FORCE_K) ax = -1;
+#endif
+    if (ax >= need_x && bq <= (double)ecap) {
+      const double C = (double)ncx * (double)ncy, H = (double)(1ll << hb);
+      const double s = (double)(1ll << k), n = (double)sq->nonempty;
+      const double w = (double)sq->sw / n + 1.0 + grow, h = (double)sq->sh / n + 1.0 + grow;
+      const double uni = eq / (C < H ? C : H), pack = 0.25 * (s + w) * (s + h) / (w * h);
+      cost = ep + eq + ep * (SCCG_JOIN_PACK ? (uni > pack ? uni : pack) : uni) / SCCG_JOIN_TESTW;
+    }
   }
   // argmin (ties -> smaller k); k = 30 is always feasible
-  int best = k <= 30 ? k : 30;
+  int best = k <= 30 ? k : 30, bax = ax;
   double bc = cost;
   for (int o = 16; o; o >>= 1) {
     const double oc = __shfl_xor_sync(0xffffffffu, bc, o);
     const int ok = __shfl_xor_sync(0xffffffffu, best, o);
+    const int oa = __shfl_xor_sync(0xffffffffu, bax, o);
     if (oc < bc || (oc == bc && ok < best)) {
       bc = oc;
       best = ok;
+      bax = oa;
     }
   }
   if (lane == 0) {
-    Grid r{30, 0, 0, 1, 1, 0};
+    Grid r{30, 1, hb - 1, 0};
     if (empty) {
       r.empty = 1;
-    } else {
-      r.k = bc < 1e300 ? best : 30;
-      r.cx0 = xmin >> r.k;
-      r.cy0 = ymin >> r.k;
-      r.ncx = ((xmax - 1) >> r.k) - r.cx0 + 1;
-      r.ncy = ((ymax - 1) >> r.k) - r.cy0 + 1;
+    } else if (bc < 1e300) {
+      r.k = best;
+      r.ax = bax;
+      r.ay = hb - bax;
     }
     *g = r;
   }
 }
 
 // MBRs covering more than kCoopCells cells (a gland among nuclei, C3) are
-// handled by their whole warp, lanes spread over the cells, so one polygon is
-// not a serial critical path of hundreds of dependent cell visits.
+// inserted and probed by their whole warp, lanes spread over the cells, so
+// one polygon is not a serial critical path of hundreds of cell visits.
 #ifndef SCCG_COOP_CELLS
 #define SCCG_COOP_CELLS 4
 #endif
@@ -109,28 +207,45 @@ __device__ __forceinline__ int mbr_cells(const int4& m, int k) {
   return (((m.z - 1) >> k) - (m.x >> k) + 1) * (((m.w - 1) >> k) - (m.y >> k) + 1);
 }
 
-// Bucket Q: COUNT (FILL = false) adds one per covered cell; FILL takes a slot
-// per covered cell (counts are decremented back to zero as slots are taken,
-// so the count array needs no second memset) and stores q and its MBR there.
-template <bool FILL>
-__global__ void grid_bucket_kernel(const int4* __restrict__ mq, int64_t nq, const Grid* __restrict__ gp,
-                                   const int* __restrict__ cell_start, int* __restrict__ cell_count,
-                                   int* __restrict__ items, int4* __restrict__ item_mbr, int grow) {
-  pdl_trigger();
-  pdl_wait();
-  const Grid g = *gp;
+// The hashed grid: bucket b holds count[b] entries, the first kSlots in its
+// slots (level-major, see kLevelSlots), the rest in a chain through the
+// overflow pool starting at head[b] (most recent first; the probe follows
+// exactly count[b] - kSlots links, so head needs no clearing).
+struct Tables {
+  int* count;
+  int4* slot;  // [kLevels][H][kLevelSlots] packed entries
+  int* head;
+  int4* ovf;  // [E] packed entries
+  int* ovf_next;
+  int* ovf_n;
+  int hb;
+  __device__ __forceinline__ size_t at(int b, int j) const {
+    return ((size_t)(j / kLevelSlots) << (hb + 2)) + ((size_t)b << 2) + (j % kLevelSlots);
+  }
+};
+
+// Insert Q: each MBR (grown for the closed join) takes a slot in the bucket of
+// every cell it covers.
+__global__ void grid_insert_kernel(const int4* __restrict__ mq, int64_t nq, const Grid* __restrict__ gp, Tables t,
+                                   int grow) {
+  pdl_entry();
+  const Grid g = load_grid(gp);
   if (g.empty) return;
   const int lane = threadIdx.x & 31;
   const int64_t wid = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
-  auto insert = [&](int c, int q, const int4& m) {
-    if (FILL) {
-      const int slot = cell_start[c] + atomicSub(&cell_count[c], 1) - 1;
-      items[slot] = q;
-      item_mbr[slot] = m;  // the probe tests MBRs straight from the cell's entries
+  auto place = [&](int b, int j, const int4& e) {  // entry j of bucket b
+    if (j < kSlots) {
+      t.slot[t.at(b, j)] = e;  // the probe tests MBRs straight from the bucket
     } else {
-      atomicAdd(&cell_count[c], 1);
+      const int o = atomicAdd(t.ovf_n, 1);
+      t.ovf[o] = e;
+      t.ovf_next[o] = atomicExch(&t.head[b], o);
     }
+  };
+  auto insert = [&](int cx, int cy, int q, const int4& m) {
+    const int b = g.bucket(cx, cy);
+    place(b, atomicAdd(&t.count[(size_t)b * kCStride], 1), pack_entry(m, q));
   };
   for (int64_t base = wid * 32; base < nq; base += nw * 32) {  // warp-uniform trip count
     const int64_t i = base + lane;
@@ -143,9 +258,20 @@ __global__ void grid_bucket_kernel(const int4* __restrict__ mq, int64_t nq, cons
       m.w += grow;
     }
     const bool coop = ok && mbr_cells(m, g.k) > kCoopCells;
-    if (ok && !coop)
-      for (int cy = m.y >> g.k; cy <= (m.w - 1) >> g.k; cy++)
-        for (int cx = m.x >> g.k; cx <= (m.z - 1) >> g.k; cx++) insert((cy - g.cy0) * g.ncx + cx - g.cx0, (int)i, m);
+    if (ok && !coop) {  // at most kCoopCells cells: all slot claims in flight before the stores
+      const int x0 = m.x >> g.k, y0 = m.y >> g.k, nx = ((m.z - 1) >> g.k) - x0 + 1;
+      const int nc = nx * (((m.w - 1) >> g.k) - y0 + 1);
+      int bk[kCoopCells], sl[kCoopCells];
+#pragma unroll
+      for (int c = 0; c < kCoopCells; c++) {
+        bk[c] = g.bucket(x0 + c % nx, y0 + c / nx);
+        sl[c] = c < nc ? atomicAdd(&t.count[(size_t)bk[c] * kCStride], 1) : 0;
+      }
+      const int4 e = pack_entry(m, (int)i);
+#pragma unroll
+      for (int c = 0; c < kCoopCells; c++)
+        if (c < nc) place(bk[c], sl[c], e);
+    }
     for (unsigned bm = __ballot_sync(0xffffffffu, coop); bm; bm &= bm - 1) {
       const int j = __ffs(bm) - 1;
       const int4 mj = make_int4(__shfl_sync(0xffffffffu, m.x, j), __shfl_sync(0xffffffffu, m.y, j),
@@ -153,7 +279,7 @@ __global__ void grid_bucket_kernel(const int4* __restrict__ mq, int64_t nq, cons
       const int qj = (int)(base + j);
       const int x0 = mj.x >> g.k, y0 = mj.y >> g.k, w = ((mj.z - 1) >> g.k) - x0 + 1;
       const int nc = w * (((mj.w - 1) >> g.k) - y0 + 1);
-      for (int t = lane; t < nc; t += 32) insert((y0 + t / w - g.cy0) * g.ncx + x0 + t % w - g.cx0, qj, mj);
+      for (int c = lane; c < nc; c += 32) insert(x0 + c % w, y0 + c / w, qj, mj);
     }
   }
 }
@@ -162,77 +288,83 @@ __global__ void grid_bucket_kernel(const int4* __restrict__ mq, int64_t nq, cons
 #define SCCG_PROBE_TILE 128
 #endif
 constexpr int kProbeTile = SCCG_PROBE_TILE;  // p per probe CTA
+constexpr int kKeep = 4;                     // hits kept in registers by the counting pass
 
-constexpr int kKeep = 4;  // hits kept in registers by the counting pass
-
-// Visit p's cells; count the pairs it owns.  WRITE: store them to out[0..n);
-// otherwise keep the first kKeep q indices in keep[].  Entries are tested four
-// at a time (independent 16-byte loads in flight).
-__device__ __forceinline__ bool owns(const int4& a, const int4& b, int k, int cx0, int cy0, int ncx, int c) {
-  return a.x < b.z && b.x < a.z && a.y < b.w && b.y < a.w &&
-         ((max(a.y, b.y) >> k) - cy0) * ncx + ((max(a.x, b.x) >> k) - cx0) == c;
+// (p, q) is owned by cell (cx, cy) iff the boxes overlap (half-open, R4) and
+// the reference point (max xlo, max ylo) lies in that cell.
+__device__ __forceinline__ bool owns(const int4& a, const int4& b, int k, int cx, int cy) {
+  return a.x < b.z && b.x < a.z && a.y < b.w && b.y < a.w && (max(a.x, b.x) >> k) == cx && (max(a.y, b.y) >> k) == cy;
 }
 
-template <bool WRITE>
-__device__ __forceinline__ int probe_cells(const int4& a, long long p, const Grid& gr, const int* __restrict__ cell_start,
-                                           const int* __restrict__ items, const int4* __restrict__ item_mbr,
-                                           int2* __restrict__ out, int4& keep) {
-  const int k = gr.k, cx0 = gr.cx0, cy0 = gr.cy0, ncx = gr.ncx;
-  int n = 0;
-  int4 kp = keep;
-#define SCCG_TAKE(IT)                          \
-  {                                            \
-    const int q = items[IT];                   \
-    if (WRITE) {                               \
-      out[n] = make_int2((int)p, q);           \
-    } else {                                   \
-      kp.x = n == 0 ? q : kp.x;                \
-      kp.y = n == 1 ? q : kp.y;                \
-      kp.z = n == 2 ? q : kp.z;                \
-      kp.w = n == 3 ? q : kp.w;                \
-    }                                          \
-    n++;                                       \
-  }
-  for (int cy = a.y >> k; cy <= (a.w - 1) >> k; cy++)
-    for (int cx = a.x >> k; cx <= (a.z - 1) >> k; cx++) {
-      const int c = (cy - cy0) * ncx + cx - cx0;
-      int it = cell_start[c];
-      const int e = cell_start[c + 1];
-      for (; it + 4 <= e; it += 4) {
-        const int4 b0 = item_mbr[it], b1 = item_mbr[it + 1], b2 = item_mbr[it + 2], b3 = item_mbr[it + 3];
-        if (owns(a, b0, k, cx0, cy0, ncx, c)) SCCG_TAKE(it)
-        if (owns(a, b1, k, cx0, cy0, ncx, c)) SCCG_TAKE(it + 1)
-        if (owns(a, b2, k, cx0, cy0, ncx, c)) SCCG_TAKE(it + 2)
-        if (owns(a, b3, k, cx0, cy0, ncx, c)) SCCG_TAKE(it + 3)
+// Test one visited cell's bucket against `a`; take(h, q) for each entry
+// tested (h: the entry is owned -- branch-free bookkeeping in the caller).
+// The bucket's first two entries (one 32-byte sector) are loaded together
+// with its count; loading a sector no insert wrote costs a DRAM miss, so the
+// next ones only when the count says they exist.
+#ifndef SCCG_JOIN_SPEC
+#define SCCG_JOIN_SPEC 2
+#endif
+template <class Take>
+__device__ __forceinline__ void visit(const int4& a, int k, int cx, int cy, int b, const Tables& t, Take&& take) {
+  const int4* s0 = t.slot + t.at(b, 0);
+  const int cnt = t.count[(size_t)b * kCStride];
+  const int4 e0 = s0[0];
+#if SCCG_JOIN_SPEC >= 2
+  const int4 e1 = s0[1];
+#endif
+  take(cnt > 0 && owns(a, entry_box(e0), k, cx, cy), e0.w);
+  if (cnt > 1) {
+#if SCCG_JOIN_SPEC < 2
+    const int4 e1 = s0[1];
+#endif
+    take(owns(a, entry_box(e1), k, cx, cy), e1.w);
+    if (cnt > 2) {
+      const int4 e2 = s0[2], e3 = s0[3];
+      take(owns(a, entry_box(e2), k, cx, cy), e2.w);
+      take(cnt > 3 && owns(a, entry_box(e3), k, cx, cy), e3.w);
+      if (cnt > kLevelSlots) {  // a crowded bucket: the higher levels, then the overflow chain
+        const int ns = min(cnt, kSlots);
+        for (int j = kLevelSlots; j < ns; j += kLevelSlots) {
+          const int4* s = t.slot + t.at(b, j);
+          const int4 f0 = s[0], f1 = s[1], f2 = s[2], f3 = s[3];
+          take(owns(a, entry_box(f0), k, cx, cy), f0.w);
+          take(j + 1 < ns && owns(a, entry_box(f1), k, cx, cy), f1.w);
+          take(j + 2 < ns && owns(a, entry_box(f2), k, cx, cy), f2.w);
+          take(j + 3 < ns && owns(a, entry_box(f3), k, cx, cy), f3.w);
+        }
+        if (cnt > kSlots) {  // rare
+          int o = t.head[b];
+          for (int r = kSlots; r < cnt; r++) {
+            const int4 e = t.ovf[o];
+            take(owns(a, entry_box(e), k, cx, cy), e.w);
+            o = t.ovf_next[o];
+          }
+        }
       }
-      for (; it < e; it++)
-        if (owns(a, item_mbr[it], k, cx0, cy0, ncx, c)) SCCG_TAKE(it)
     }
-#undef SCCG_TAKE
-  keep = kp;
-  return n;
+  }
 }
 
-__device__ __forceinline__ int4 shfl4(const int4& v, int j) {
-  return make_int4(__shfl_sync(0xffffffffu, v.x, j), __shfl_sync(0xffffffffu, v.y, j), __shfl_sync(0xffffffffu, v.z, j),
-                   __shfl_sync(0xffffffffu, v.w, j));
+// Visit p's cells (at most kCoopCells), one after the other.
+template <class Take>
+__device__ __forceinline__ void probe_cells(const int4& a, const Grid& g, const Tables& t, Take&& take) {
+  const int k = g.k;
+  for (int cy = a.y >> k; cy <= (a.w - 1) >> k; cy++)
+    for (int cx = a.x >> k; cx <= (a.z - 1) >> k; cx++) visit(a, k, cx, cy, g.bucket(cx, cy), t, take);
 }
 
 // A big MBR probed by its whole warp.  Its cell rectangle is taken 32 cells
-// at a time (lane l reads cell l's entry range); the entries of those cells
-// are then flattened over the lanes (a warp scan of the range lengths, and a
-// 5-step shuffle search for each entry's cell), so a lane tests entry after
-// entry of ALL the cells with independent loads -- a gland whose cells hold
-// dozens of nuclei each (C3) is not a serial walk per cell.  COUNT returns the
-// pairs it owns (every lane gets the total); WRITE appends them to seg[] in
-// arbitrary order (slots from *fill, reset here) -- the q order is restored
-// by the segment sort.
+// at a time (lane l reads cell l's counter); the slot entries of those cells
+// are flattened over the lanes (a warp scan of min(count, kSlots), a 5-step
+// shuffle search for each entry's cell), so a lane tests entry after entry of
+// ALL the cells with independent loads; a cell's overflow chain is walked by
+// its own lane.  COUNT returns the pairs it owns (every lane gets the total);
+// WRITE appends them to seg[] in arbitrary order (slots from *fill, reset
+// here) -- the q order is restored by the segment sort.
 template <bool WRITE>
-__device__ int coop_cells(const int4 a, long long p, const Grid& g, const int* __restrict__ cell_start,
-                          const int* __restrict__ items, const int4* __restrict__ item_mbr, int2* __restrict__ seg,
-                          int* fill) {
+__device__ int coop_cells(const int4 a, long long p, const Grid& g, const Tables& t, int2* __restrict__ seg, int* fill) {
   const int lane = threadIdx.x & 31;
-  const int k = g.k, cx0 = g.cx0, cy0 = g.cy0, ncx = g.ncx;
+  const int k = g.k;
   const int x0 = a.x >> k, y0 = a.y >> k, w = ((a.z - 1) >> k) - x0 + 1;
   const int nc = w * (((a.w - 1) >> k) - y0 + 1);
   if (WRITE) {
@@ -240,13 +372,21 @@ __device__ int coop_cells(const int4 a, long long p, const Grid& g, const int* _
     __syncwarp();
   }
   int cnt = 0;
+  auto take = [&](bool h, int q) {
+    if (h) {
+      if (WRITE) seg[atomicAdd(fill, 1)] = make_int2((int)p, q);
+      cnt++;
+    }
+  };
   for (int base = 0; base < nc; base += 32) {  // warp-uniform
-    const int t = base + lane;
-    int c = 0, s = 0, len = 0;
-    if (t < nc) {
-      c = (y0 + t / w - cy0) * ncx + (x0 + t % w - cx0);
-      s = cell_start[c];
-      len = cell_start[c + 1] - s;
+    const int c = base + lane;
+    int cx = 0, cy = 0, b = 0, n = 0, len = 0;
+    if (c < nc) {
+      cx = x0 + c % w;
+      cy = y0 + c / w;
+      b = g.bucket(cx, cy);
+      n = t.count[(size_t)b * kCStride];
+      len = min(n, kSlots);
     }
     int incl = len;
     for (int o = 1; o < 32; o <<= 1) {
@@ -258,16 +398,21 @@ __device__ int coop_cells(const int4 a, long long p, const Grid& g, const int* _
     for (int f0 = 0; f0 < total; f0 += 32) {  // warp-uniform
       const int f = f0 + lane;
       int j = 0;  // the lane whose cell holds flattened entry f: #lanes with incl <= f
-      for (int b = 16; b; b >>= 1)
-        if (__shfl_sync(0xffffffffu, incl, j + b - 1) <= f) j += b;
-      const int cj = __shfl_sync(0xffffffffu, c, j), sj = __shfl_sync(0xffffffffu, s, j);
-      const int ej = __shfl_sync(0xffffffffu, excl, j);
+      for (int s = 16; s; s >>= 1)
+        if (__shfl_sync(0xffffffffu, incl, j + s - 1) <= f) j += s;
+      const int cxj = __shfl_sync(0xffffffffu, cx, j), cyj = __shfl_sync(0xffffffffu, cy, j);
+      const int bj = __shfl_sync(0xffffffffu, b, j), ej = __shfl_sync(0xffffffffu, excl, j);
       if (f < total) {
-        const int it = sj + (f - ej);
-        if (owns(a, item_mbr[it], k, cx0, cy0, ncx, cj)) {
-          if (WRITE) seg[atomicAdd(fill, 1)] = make_int2((int)p, items[it]);
-          cnt++;
-        }
+        const int4 e = t.slot[t.at(bj, f - ej)];
+        take(owns(a, entry_box(e), k, cxj, cyj), e.w);
+      }
+    }
+    if (n > kSlots) {  // rare
+      int o = t.head[b];
+      for (int r = kSlots; r < n; r++) {
+        const int4 e = t.ovf[o];
+        take(owns(a, entry_box(e), k, cx, cy), e.w);
+        o = t.ovf_next[o];
       }
     }
   }
@@ -279,9 +424,8 @@ __device__ int coop_cells(const int4 a, long long p, const Grid& g, const int* _
 // network in its ascending-only form (each merge starts by comparing i with
 // its mirror i ^ (k - 1)), so positions >= n behave as +inf and are never
 // touched -- no padding needed.  Up to kSortBuf keys are sorted in a shared
-// buffer (one per CTA, under a lock -- long segments are rare; kept small so
-// the L1 the probe lives on stays large); longer segments in place in global
-// memory (L1/L2-resident).
+// buffer (one per CTA, under a lock -- long segments are rare); longer
+// segments in place in global memory (L1/L2-resident).
 constexpr int kSortBuf = 1024;
 constexpr int kThreadSortMax = 32;  // segments up to this length: the owning thread sorts
 
@@ -330,53 +474,117 @@ __device__ void warp_sort_segment(int2* seg, int n, int* buf, int* lock) {
   __syncwarp();
 }
 
-// Probe, per CTA tile of kProbeTile consecutive p (thread per p).  A pair is
-// owned by the cell that holds its reference point (max xlo, max ylo).  Each
-// thread counts its pairs (keeping up to kKeep hits in registers; MBRs over
-// many cells are counted by their whole warp) and the CTA scans the counts.
-// BUCKET pass: the tile writes its (p, q)-sorted pairs into its own bucket of
-// kBucket slots (no cross-CTA dependency) and records its count.  COMPACT pass:
-// each tile sums the preceding tiles' counts (all known by then; a few
-// vectorized L2 loads per thread) for its offset, copies its bucket there, or
-// -- when the tile overflowed its bucket -- probes again and writes there
-// directly; the last tile writes the total (and the async result word).  Pairs
-// past `cap` are not written; the total is exact.
-constexpr int kBucket = 1024;
-#ifndef SCCG_PROBE_MINB
-#define SCCG_PROBE_MINB 12
-#endif
+__device__ __forceinline__ void insertion_sort_q(int2* seg, int n) {
+  for (int i = 1; i < n; i++) {
+    const int2 v = seg[i];
+    int j = i - 1;
+    while (j >= 0 && seg[j].y > v.y) {
+      seg[j + 1] = seg[j];
+      j--;
+    }
+    seg[j + 1] = v;
+  }
+}
 
+// Tile states of the compaction's decoupled look-back: flag in bits 62-63
+// (0 = not yet, 1 = the tile's own count, 2 = inclusive prefix), value below;
+// one 64-bit word, so value and flag are published together.
+constexpr unsigned long long kFlagAgg = 1ull << 62, kFlagPre = 2ull << 62, kValMask = (1ull << 62) - 1;
+__device__ __forceinline__ unsigned long long ld_relaxed(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ int ld_coherent_i(const int* p) {
+  int v;
+  asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+#ifndef SCCG_JOIN_LOOKBACK
+#define SCCG_JOIN_LOOKBACK 0  // 1: the compaction's offsets by decoupled look-back (measured slower)
+#endif
+#ifndef SCCG_PROBE_MINB
+#define SCCG_PROBE_MINB 8
+#endif
+constexpr int kBucket = 1024;  // pairs per probe tile held in its bucket between the two passes
+
+// Probe, per CTA tile of kProbeTile consecutive p (thread per p; MBRs over
+// many cells by the tile's warps together).  Each thread counts the pairs its
+// p owns -- keeping up to kKeep q in registers -- and the CTA scans the counts.
+// BUCKET pass (COMPACT = false): the tile's pairs go to its own bucket of
+// kBucket slots, each p's segment sorted by q, and its count to tile_cnt (no
+// cross-CTA dependency).  COMPACT pass: each tile sums the preceding tiles'
+// counts (all known by then; a few vectorized L2 loads per thread) for its
+// offset and copies its bucket there -- or, when the tile overflowed its
+// bucket, probes again and writes in place; the last tile writes the total
+// (and the async result word).  Pairs past `cap` are not written (a p whose
+// segment would cross it is skipped whole); the total is exact.
 template <bool COMPACT>
-__global__ void __launch_bounds__(kProbeTile, SCCG_PROBE_MINB) probe_kernel(const int4* __restrict__ mp, int64_t np,
-                                                           const Grid* __restrict__ gp,
-                                                           const int* __restrict__ cell_start,
-                                                           const int* __restrict__ items,
-                                                           const int4* __restrict__ item_mbr,
-                                                           int* __restrict__ tile_cnt,
-                                                           unsigned char* __restrict__ tile_long,
-                                                           int2* __restrict__ bucket, int2* __restrict__ pairs,
-                                                           long long cap, long long* __restrict__ total,
-                                                           long long* __restrict__ result,
-                                                           const uint32_t* __restrict__ status_p,
-                                                           const uint32_t* __restrict__ status_q, int grow) {
+__global__ void __launch_bounds__(kProbeTile, SCCG_PROBE_MINB)
+    probe_kernel(const int4* __restrict__ mp, int64_t np, const Grid* __restrict__ gp, Tables t,
+                 int* __restrict__ tile_cnt, int2* __restrict__ bucket, unsigned long long* __restrict__ tstate,
+                 unsigned long long* __restrict__ ticket, int2* __restrict__ pairs, long long cap,
+                 long long* __restrict__ total, long long* __restrict__ result, const uint32_t* __restrict__ status_p,
+                 const uint32_t* __restrict__ status_q, int grow) {
   __shared__ int s_warp[kProbeTile / 32];
   __shared__ long long s_sum[kProbeTile / 32];
   __shared__ int s_fill[kProbeTile / 32];
   __shared__ int s_coop[kProbeTile];     // threads of this tile whose MBR the warps probe together
-  __shared__ int s_coopval[kProbeTile];  // ... their pair count, then their output offset
+  __shared__ int s_coopval[kProbeTile];  // ... their pair count, then their segment start
   __shared__ int s_cw[kProbeTile / 32];
   __shared__ int s_sort[kSortBuf];
   __shared__ int s_lock;
-  __shared__ int2 s_pairs[COMPACT ? kBucket : 1];      // compaction: the tile's bucket
-  __shared__ unsigned s_head[COMPACT ? kBucket / 32 : 1];  // ... first pair of each p
-  __shared__ int s_runs[COMPACT ? 2 * kProbeTile + 1 : 1];  // ... long runs (start, length), count
+  __shared__ long long s_tile;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int tile = blockIdx.x;
-  pdl_trigger();
-  pdl_wait();
-  int2* dst;  // this tile's output: its bucket, or its final place
+  int tile = blockIdx.x;
+  pdl_entry();
+  int2* dst;       // this tile's output: its bucket, or its final place
+  long long room;  // slots available from dst
   if (COMPACT) {
-    long long sum = 0;  // this tile's offset: the preceding tiles' counts
+#if SCCG_JOIN_LOOKBACK
+    // this tile's offset: a decoupled look-back over the preceding tiles'
+    // counts (every count is known from the bucket pass, so each tile
+    // publishes its own at once and the look-back never waits on work);
+    // tiles are taken in ticket order, so every predecessor is running
+    if (threadIdx.x == 0) s_tile = (long long)atomicAdd(ticket, 1ull);
+    __syncthreads();
+    tile = (int)s_tile;
+    const int cnt = ld_coherent_i(tile_cnt + tile);
+    if (warp == 0) {
+      long long excl = 0;
+      if (tile == 0) {
+        if (lane == 0) st_relaxed(&tstate[0], kFlagPre | (unsigned long long)cnt);
+      } else {
+        if (lane == 0) st_relaxed(&tstate[tile], kFlagAgg | (unsigned long long)cnt);
+        long long idx = tile - 1;
+        for (;;) {  // warp-uniform
+          const long long i = idx - lane;
+          unsigned long long v;
+          do {
+            v = i >= 0 ? ld_relaxed(&tstate[i]) : kFlagPre;
+          } while (__any_sync(0xffffffffu, (v >> 62) == 0));
+          const unsigned pm = __ballot_sync(0xffffffffu, (v >> 62) == 2);
+          const int stop = pm ? __ffs(pm) - 1 : 31;
+          long long val = lane <= stop ? (long long)(v & kValMask) : 0;
+          for (int o = 16; o; o >>= 1) val += __shfl_xor_sync(0xffffffffu, val, o);
+          excl += val;
+          if (pm) break;
+          idx -= 32;
+        }
+        if (lane == 0) st_relaxed(&tstate[tile], kFlagPre | (unsigned long long)(excl + cnt));
+      }
+      if (lane == 0) s_sum[0] = excl;
+    }
+    __syncthreads();
+    const long long off = s_sum[0];
+#else
+    // this tile's offset: the preceding tiles' counts (all known by now; a
+    // few vectorized L2 loads per thread)
+    long long sum = 0;
     const int4* c4 = reinterpret_cast<const int4*>(tile_cnt);
     for (int i = threadIdx.x; i < (tile >> 2); i += kProbeTile) {
       const int4 v = c4[i];
@@ -389,6 +597,7 @@ __global__ void __launch_bounds__(kProbeTile, SCCG_PROBE_MINB) probe_kernel(cons
     long long off = 0;
     for (int w = 0; w < kProbeTile / 32; w++) off += s_sum[w];
     const int cnt = tile_cnt[tile];
+#endif
     if (tile == (int)gridDim.x - 1 && threadIdx.x == 0) {
       *total = off + cnt;
       if (result) {
@@ -396,84 +605,42 @@ __global__ void __launch_bounds__(kProbeTile, SCCG_PROBE_MINB) probe_kernel(cons
         result[1] = (long long)(status_p[0] | status_q[0]);
       }
     }
-    if (cnt == 0 || pairs == nullptr || off + cnt > cap) return;
-    if (cnt <= kBucket && !tile_long[tile]) {  // copy the bucket
+    if (cnt == 0 || pairs == nullptr || off >= cap) return;
+    if (cnt <= kBucket) {  // copy the bucket (already sorted)
       const int2* src = bucket + (size_t)tile * kBucket;
-      for (int i = threadIdx.x; i < cnt; i += kProbeTile) pairs[off + i] = src[i];
-      return;
-    }
-    if (cnt <= kBucket) {
-      // stage the bucket; runs of one p longer than kThreadSortMax were left
-      // unsorted by the bucket pass -- the whole CTA sorts each by q here
-      const int2* src = bucket + (size_t)tile * kBucket;
-      for (int i = threadIdx.x; i < kBucket / 32; i += kProbeTile) s_head[i] = 0u;
-      if (threadIdx.x == 0) s_runs[2 * kProbeTile] = 0;
-      __syncthreads();
-      for (int i = threadIdx.x; i < cnt; i += kProbeTile) {
-        const int2 v = src[i];
-        s_pairs[i] = v;
-        if (i == 0 || src[i - 1].x != v.x) atomicOr(&s_head[i >> 5], 1u << (i & 31));
-      }
-      __syncthreads();
-      for (int i = threadIdx.x; i < cnt; i += kProbeTile) {
-        if (!((s_head[i >> 5] >> (i & 31)) & 1u)) continue;
-        int e = i + 1;  // next head (or the end)
-        while (e < cnt) {
-          const unsigned w = s_head[e >> 5] >> (e & 31);
-          if (w) {
-            e += __ffs(w) - 1;
-            break;
-          }
-          e = (e | 31) + 1;
-        }
-        if (e > cnt) e = cnt;
-        if (e - i > kThreadSortMax) {
-          const int r = atomicAdd(&s_runs[2 * kProbeTile], 1);
-          s_runs[2 * r] = i;
-          s_runs[2 * r + 1] = e - i;
-        }
-      }
-      __syncthreads();
-      const int nruns = s_runs[2 * kProbeTile];
-      for (int i = threadIdx.x; i < cnt; i += kProbeTile) pairs[off + i] = s_pairs[i];
-      if (nruns == 0) return;
-      __syncthreads();  // the long runs' unsorted copies are overwritten below
-      // long runs: rank sort -- an entry's place in its run is the number of
-      // the run's q below its own (q are distinct within a run); every thread
-      // moves on to the next run without a barrier, so a tile with many glands
-      // costs its total run work, not a barrier-bound network per run
-      for (int r = 0; r < nruns; r++) {
-        const int s0 = s_runs[2 * r], n = s_runs[2 * r + 1];
-        const int2* run = s_pairs + s0;
-        for (int i = threadIdx.x; i < n; i += kProbeTile) {
-          const int2 v = run[i];
-          int rank = 0;
-#pragma unroll 4
-          for (int j = 0; j < n; j++) rank += run[j].y < v.y ? 1 : 0;
-          pairs[off + s0 + rank] = v;
-        }
-      }
+      const long long m = min((long long)cnt, cap - off);
+      for (int i = threadIdx.x; i < m; i += kProbeTile) pairs[off + i] = src[i];
       return;
     }
     dst = pairs + off;  // overflowed tile: probe again, write in place
+    room = cap - off;
   } else {
     dst = bucket + (size_t)tile * kBucket;
+    room = kBucket;
   }
   if (threadIdx.x == 0) s_lock = 0;
   const int64_t p = (int64_t)tile * kProbeTile + threadIdx.x;
-  const Grid g = *gp;
+  const Grid g = load_grid(gp);
   int4 a = make_int4(0, 0, 0, 0);
   const bool live = p < np && !g.empty;
   if (live) a = mp[p];
   const bool act = live && !mbr_empty(a);
   a.z += grow;  // closed join: boxes grown by one pixel on the high side
   a.w += grow;
+  const bool coop = act && mbr_cells(a, g.k) > kCoopCells;  // big MBR: the warps probe it together
+  int n = 0;
   int4 keep = make_int4(0, 0, 0, 0);
-  const bool coop = act && mbr_cells(a, g.k) > kCoopCells;  // big MBR: its warp probes it together
-  int n = act && !coop ? probe_cells<false>(a, p, g, cell_start, items, item_mbr, nullptr, keep) : 0;
+  if (act && !coop)
+    probe_cells(a, g, t, [&](bool h, int q) {
+      keep.x = h && n == 0 ? q : keep.x;
+      keep.y = h && n == 1 ? q : keep.y;
+      keep.z = h && n == 2 ? q : keep.z;
+      keep.w = h && n == 3 ? q : keep.w;
+      n += h ? 1 : 0;
+    });
   // big MBRs of the whole tile (glands among nuclei, C3: often consecutive in
-  // p) are dealt round-robin to the tile's warps, so their serial cell walks
-  // run side by side instead of queueing on the one warp that holds them
+  // p) are dealt round-robin to the tile's warps, so their cell walks run side
+  // by side instead of queueing on the one warp that holds them
   int ncoop = 0;
   if (__syncthreads_or(coop)) {
     const unsigned cm = __ballot_sync(0xffffffffu, coop);
@@ -486,13 +653,12 @@ __global__ void __launch_bounds__(kProbeTile, SCCG_PROBE_MINB) probe_kernel(cons
     }
     if (coop) s_coop[off + __popc(cm & lanemask_lt())] = threadIdx.x;
     __syncthreads();
-    for (int t = warp; t < ncoop; t += kProbeTile / 32) {
-      const int j = s_coop[t];
+    for (int c = warp; c < ncoop; c += kProbeTile / 32) {
+      const int j = s_coop[c];
       int4 aj = mp[(int64_t)tile * kProbeTile + j];
       aj.z += grow;
       aj.w += grow;
-      const int cnt = coop_cells<false>(aj, (int64_t)tile * kProbeTile + j, g, cell_start, items, item_mbr, nullptr,
-                                        nullptr);
+      const int cnt = coop_cells<false>(aj, (int64_t)tile * kProbeTile + j, g, t, nullptr, nullptr);
       if (lane == 0) s_coopval[j] = cnt;
     }
     __syncthreads();
@@ -515,46 +681,34 @@ __global__ void __launch_bounds__(kProbeTile, SCCG_PROBE_MINB) probe_kernel(cons
   const int base = wbase + x - n;
   if (!COMPACT) {
     if (threadIdx.x == 0) tile_cnt[tile] = agg;
-    if (agg > kBucket) return;  // rare: the compact pass probes this tile again
+    if (agg > kBucket) return;  // rare: the compaction pass probes this tile again
   }
-  const bool fits = n > 0;
+  int2* seg = dst + base;
+  const bool fits = n > 0 && base + n <= room;
   // big MBRs: gathered by the warps (round-robin as above), unsorted
   if (ncoop > 0) {
     if (coop) s_coopval[threadIdx.x] = fits ? base : -1;
     __syncthreads();
-    for (int t = warp; t < ncoop; t += kProbeTile / 32) {
-      const int j = s_coop[t];
+    for (int c = warp; c < ncoop; c += kProbeTile / 32) {
+      const int j = s_coop[c];
       if (s_coopval[j] < 0) continue;  // warp-uniform
       int4 aj = mp[(int64_t)tile * kProbeTile + j];
       aj.z += grow;
       aj.w += grow;
-      coop_cells<true>(aj, (int64_t)tile * kProbeTile + j, g, cell_start, items, item_mbr, dst + s_coopval[j],
-                       &s_fill[warp]);
+      coop_cells<true>(aj, (int64_t)tile * kProbeTile + j, g, t, dst + s_coopval[j], &s_fill[warp]);
     }
     __syncthreads();  // the warps' writes are visible to the segment's own thread
-    if (coop && fits && n <= kThreadSortMax) {  // short segment: its thread sorts it by q (longer: see below)
-      int2* seg = dst + base;
-      for (int i = 1; i < n; i++) {
-        const int2 v = seg[i];
-        int j = i - 1;
-        while (j >= 0 && seg[j].y > v.y) {
-          seg[j + 1] = seg[j];
-          j--;
-        }
-        seg[j + 1] = v;
-      }
-    }
+    if (coop && fits && n <= kThreadSortMax) insertion_sort_q(seg, n);
   }
   if (fits && !coop) {
-    int2* seg = dst + base;
     if (n <= kKeep) {  // the counting pass kept them: sort in registers, write
       const int big = 0x7fffffff;  // pad the unused slots so a 4-sorting network applies
       int k0 = keep.x, k1 = n > 1 ? keep.y : big, k2 = n > 2 ? keep.z : big, k3 = n > 3 ? keep.w : big;
-#define SCCG_CSWAP(U, V)        \
-  {                             \
-    const int lo = min(U, V);   \
-    V = max(U, V);              \
-    U = lo;                     \
+#define SCCG_CSWAP(U, V)      \
+  {                           \
+    const int lo = min(U, V); \
+    V = max(U, V);            \
+    U = lo;                   \
   }
       SCCG_CSWAP(k0, k1)
       SCCG_CSWAP(k2, k3)
@@ -567,27 +721,15 @@ __global__ void __launch_bounds__(kProbeTile, SCCG_PROBE_MINB) probe_kernel(cons
       if (n > 2) seg[2] = make_int2((int)p, k2);
       if (n > 3) seg[3] = make_int2((int)p, k3);
     } else {
-      probe_cells<true>(a, p, g, cell_start, items, item_mbr, seg, keep);
-      if (n <= kThreadSortMax)
-        for (int i = 1; i < n; i++) {  // insertion sort of a short segment by q
-          const int2 v = seg[i];
-          int j = i - 1;
-          while (j >= 0 && seg[j].y > v.y) {
-            seg[j + 1] = seg[j];
-            j--;
-          }
-          seg[j + 1] = v;
-        }
+      int w = 0;
+      probe_cells(a, g, t, [&](bool h, int q) {
+        if (h) seg[w++] = make_int2((int)p, q);
+      });
+      if (n <= kThreadSortMax) insertion_sort_q(seg, n);
     }
   }
-  // long segments (big MBRs, or many hits): sorted by the compaction pass for
-  // a bucket, here by the warp when writing in place (an overflowed tile)
-  if (!COMPACT) {
-    const int any_long = __syncthreads_or(fits && n > kThreadSortMax);
-    if (threadIdx.x == 0) tile_long[tile] = any_long ? 1 : 0;
-    return;
-  }
-  __syncthreads();  // s_lock initialised; every segment written
+  // long segments (big MBRs, or many hits): sorted by the warp
+  __syncthreads();
   for (unsigned bm = __ballot_sync(0xffffffffu, fits && n > kThreadSortMax); bm; bm &= bm - 1) {
     const int j = __ffs(bm) - 1;
     warp_sort_segment(dst + __shfl_sync(0xffffffffu, base, j), __shfl_sync(0xffffffffu, n, j), s_sort, &s_lock);
@@ -595,40 +737,44 @@ __global__ void __launch_bounds__(kProbeTile, SCCG_PROBE_MINB) probe_kernel(cons
 }
 
 // --------------------------------------------------------------------- host
-static size_t cub_scan_bytes(int64_t n) {
-  size_t b32 = 0;
-  cub::DeviceScan::ExclusiveSum(nullptr, b32, (const int*)nullptr, (int*)nullptr, (int)n);
-  return b32;
-}
-
 static int64_t probe_tiles(int64_t np) { return (np + kProbeTile - 1) / kProbeTile; }
 
 struct FilterWs {
   Grid* grid;
-  int *cell_count, *cell_start, *items;
-  int4* item_mbr;
-  int* tile_cnt;   // [T] pairs per probe tile
-  unsigned char* tile_long;  // [T] the tile's bucket holds a segment the compaction sorts
-  int2* bucket;    // [T][kBucket] per-tile pair buckets
+  Tables t;
+  int* tile_cnt;  // [T] pairs per probe tile
+  unsigned long long* tstate;  // [T] the compaction's look-back states
+  unsigned long long* ticket;  // the compaction's tile ticket
+  int2* bucket;   // [T][kBucket] per-tile pair buckets
   long long* total;
-  void* tmp;
-  size_t tmp_bytes;
+  char* zero;     // cleared by the grid selection: bucket counters, overflow pool counter
+  size_t zero_bytes;
+  int hb;
 };
 
 static size_t filter_layout(int64_t np, int64_t nq, Carve& cv, FilterWs& w) {
-  const int64_t C = cell_cap(np, nq), E = entry_cap(nq);
+  const int hb = bucket_bits(nq);
+  const int64_t H = int64_t(1) << hb, E = entry_cap(nq), T = probe_tiles(np);
+  w.hb = hb;
   w.grid = cv.take<Grid>(1);
-  w.cell_count = cv.take<int>(C + 1);
-  w.cell_start = cv.take<int>(C + 1);
-  w.items = cv.take<int>(E);
-  w.item_mbr = cv.take<int4>(E);
-  const int64_t T = probe_tiles(np);
-  w.tile_cnt = cv.take<int>(T + 4);
-  w.tile_long = cv.take<unsigned char>(T + 1);
   w.total = cv.take<long long>(1);
+  // one contiguous cleared region: count[H] | pool counter, ticket | tile states[T]
+  const size_t cb = (size_t)4 * H * kCStride;
+  w.zero_bytes = cb + 16 + (size_t)8 * ((T + 1) & ~int64_t(1));
+  w.zero = cv.take<char>(w.zero_bytes);
+  if (w.zero) {
+    w.t.count = reinterpret_cast<int*>(w.zero);
+    w.t.ovf_n = reinterpret_cast<int*>(w.zero + cb);
+    w.ticket = reinterpret_cast<unsigned long long*>(w.zero + cb + 8);
+    w.tstate = reinterpret_cast<unsigned long long*>(w.zero + cb + 16);
+  }
+  w.tile_cnt = cv.take<int>(T + 4);
   w.bucket = cv.take<int2>(T * kBucket);
-  w.tmp_bytes = cub_scan_bytes(C + 1);
-  w.tmp = cv.take<char>(w.tmp_bytes);
+  w.t.hb = hb;
+  w.t.head = cv.take<int>(H);
+  w.t.slot = cv.take<int4>(H * kSlots);
+  w.t.ovf = cv.take<int4>(E);
+  w.t.ovf_next = cv.take<int>(E);
   return cv.used;
 }
 
@@ -651,48 +797,42 @@ static int blocks_for(int64_t n, int threads) {
   return (int)(b < 1 ? 1 : b);
 }
 
-__global__ void filter_result_kernel(const long long* __restrict__ total, const uint32_t* __restrict__ sp,
+__global__ void filter_result_kernel(long long* __restrict__ total, const uint32_t* __restrict__ sp,
                                      const uint32_t* __restrict__ sq, long long* result) {
+  pdl_entry();
   if (threadIdx.x == 0) {
-    result[0] = *total;
-    result[1] = (long long)(sp[0] | sq[0]);
+    *total = 0;
+    if (result) {
+      result[0] = 0;
+      result[1] = (long long)(sp[0] | sq[0]);
+    }
   }
 }
 
-// Enqueue the whole join: grid, Q buckets, probe into per-tile buckets, scan
-// of the tile counts, compaction (pairs written when they fit in `cap`; the
-// exact total always lands in w.total).
+// Enqueue the whole join: grid selection + clearing, Q insertion, one-pass
+// probe (pairs written when their p's segment fits in `cap`; the exact total
+// always lands in w.total).
 static int filter_enqueue(const sccg_polyset* P, const sccg_polyset* Q, FilterWs& w, int32_t* pairs, int64_t cap,
                           long long* result, int grow, cudaStream_t stream) {
   const int64_t np = P->n_polygons, nq = Q->n_polygons;
   const int4* mp = reinterpret_cast<const int4*>(P->mbr);
   const int4* mq = reinterpret_cast<const int4*>(Q->mbr);
-  const int64_t C = cell_cap(np, nq), T = probe_tiles(np);
-  // 1. grid size from the prep statistics (device side) and the count array
-  // cleared in the same launch; bucket Q (chained onto it by PDL)
-  const long long zero_n4 = (long long)((sizeof(int) * (C + 1) + 15) / 16);  // cell_count's slice is 256-B aligned
+  const int64_t T = probe_tiles(np);
+  const long long zero_n4 = (long long)(w.zero_bytes / 16);
   launch_pdl(grid_select_kernel, dim3((unsigned)blocks_for(zero_n4, 256)), dim3(256), 0, stream,
-             reinterpret_cast<const SetStats*>(P->stats), reinterpret_cast<const SetStats*>(Q->stats), (long long)C,
-             (long long)entry_cap(nq), grow, w.grid, reinterpret_cast<int4*>(w.cell_count), zero_n4);
+             reinterpret_cast<const SetStats*>(P->stats), reinterpret_cast<const SetStats*>(Q->stats), w.hb,
+             (long long)entry_cap(nq), grow, w.grid, reinterpret_cast<int4*>(w.zero), zero_n4);
   if (nq > 0)
-    launch_pdl(grid_bucket_kernel<false>, dim3(blocks_for(nq, 256)), dim3(256), 0, stream, mq, nq, w.grid,
-               (const int*)nullptr, w.cell_count, (int*)nullptr, (int4*)nullptr, grow);
-  cub::DeviceScan::ExclusiveSum(w.tmp, w.tmp_bytes, w.cell_count, w.cell_start, (int)(C + 1), stream);
-  if (nq > 0)
-    launch_pdl(grid_bucket_kernel<true>, dim3(blocks_for(nq, 256)), dim3(256), 0, stream, mq, nq, w.grid,
-               w.cell_start, w.cell_count, w.items, w.item_mbr, grow);
-  // 2. probe into tile buckets; compaction (offsets, copies, total)
+    launch_pdl(grid_insert_kernel, dim3(blocks_for(nq, 256)), dim3(256), 0, stream, mq, nq, w.grid, w.t, grow);
   if (np > 0) {
-    launch_pdl(probe_kernel<false>, dim3((unsigned)T), dim3(kProbeTile), 0, stream, mp, np, w.grid, w.cell_start,
-               w.items, w.item_mbr, w.tile_cnt, w.tile_long, w.bucket, (int2*)nullptr, (long long)0,
-               (long long*)nullptr, (long long*)nullptr, (const uint32_t*)nullptr, (const uint32_t*)nullptr, grow);
-    launch_pdl(probe_kernel<true>, dim3((unsigned)T), dim3(kProbeTile), 0, stream, mp, np, w.grid, w.cell_start,
-               w.items, w.item_mbr, w.tile_cnt, w.tile_long, w.bucket, reinterpret_cast<int2*>(pairs),
-               (long long)(pairs ? cap : 0), w.total, result, P->status, Q->status, grow);
-  } else {
-    cudaMemsetAsync(w.total, 0, sizeof(long long), stream);
-    if (result) filter_result_kernel<<<1, 32, 0, stream>>>(w.total, P->status, Q->status, result);
-  }
+    launch_pdl(probe_kernel<false>, dim3((unsigned)T), dim3(kProbeTile), 0, stream, mp, np, w.grid, w.t, w.tile_cnt,
+               w.bucket, w.tstate, w.ticket, (int2*)nullptr, (long long)0, (long long*)nullptr, (long long*)nullptr,
+               (const uint32_t*)nullptr, (const uint32_t*)nullptr, grow);
+    launch_pdl(probe_kernel<true>, dim3((unsigned)T), dim3(kProbeTile), 0, stream, mp, np, w.grid, w.t, w.tile_cnt,
+               w.bucket, w.tstate, w.ticket, reinterpret_cast<int2*>(pairs), (long long)(pairs ? cap : 0), w.total, result, P->status,
+               Q->status, grow);
+  } else
+    launch_pdl(filter_result_kernel, dim3(1), dim3(32), 0, stream, w.total, P->status, Q->status, result);
   return check_cuda(cudaGetLastError(), "filter enqueue");
 }
 

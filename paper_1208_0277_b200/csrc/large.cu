@@ -543,8 +543,7 @@ __global__ void __launch_bounds__(kLWarps * 32, 4)
                 unsigned* __restrict__ hit_p, unsigned* __restrict__ hit_q) {
   extern __shared__ __align__(16) unsigned char s_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  pdl_trigger();
-  pdl_wait();  // the small kernel's items and counters
+  pdl_entry();  // the small kernel's items and counters
   unsigned char* base = s_raw + (size_t)warp * kLSmemPerWarp;
   LocalPoly P, Q;
   P.V = reinterpret_cast<uint64_t*>(base);
@@ -556,8 +555,8 @@ __global__ void __launch_bounds__(kLWarps * 32, 4)
   uint64_t* stk = reinterpret_cast<uint64_t*>(sh + 2 * kLStage);
   int4* istk = reinterpret_cast<int4*>(stk + kLStack);
   const long long n_cap = w.n_cap;
-  const long long nl = min((long long)(w.ctr[2] & 0xffffffffull), n_cap);
-  const long long ne = min((long long)w.ctr[1], w.extra_cap);
+  const long long nl = min((long long)(ld_coherent(reinterpret_cast<const long long*>(w.ctr) + 2) & 0xffffffffll), n_cap);
+  const long long ne = min(ld_coherent(reinterpret_cast<const long long*>(w.ctr) + 1), w.extra_cap);
   const long long total = nl + ne;
   if (total == 0) return;  // no large pairs in this batch
   unsigned status = 0;

@@ -126,15 +126,15 @@ __global__ void __launch_bounds__(kSmallWarps * 32, SCCG_SMALL_MINB)
                  LargeWs lw, long long* counters, unsigned* __restrict__ hit_p, unsigned* __restrict__ hit_q,
                  long long np_,
                  long long nq_) {
-  pdl_trigger();
-  pdl_wait();
+  pdl_entry_deferred();
   // pair count: host-given, or (async path) the filter's device-side count clamped to the buffer
   // (a join that overflowed the buffer left it incomplete: nothing is processed, the status says so)
-  const bool overflow = dev_result && dev_result[0] > n_cap;
-  const long long n = dev_result ? (overflow ? 0 : dev_result[0]) : n_cap;
-  if (dev_result && blockIdx.x == 0 && threadIdx.x == 0 && (dev_result[1] || overflow))
+  const long long r0 = dev_result ? ld_coherent(dev_result) : 0, r1 = dev_result ? ld_coherent(dev_result + 1) : 0;
+  const bool overflow = dev_result && r0 > n_cap;
+  const long long n = dev_result ? (overflow ? 0 : r0) : n_cap;
+  if (dev_result && blockIdx.x == 0 && threadIdx.x == 0 && (r1 || overflow))
     atomicOr(reinterpret_cast<unsigned long long*>(&sums->status),
-             (unsigned long long)dev_result[1] | (overflow ? (unsigned long long)SCCG_STATUS_CAPACITY : 0ull));
+             (unsigned long long)r1 | (overflow ? (unsigned long long)SCCG_STATUS_CAPACITY : 0ull));
   __shared__ __align__(16) int2 s_buf[kSmallWarps][2 * kSmallQOff];
   __shared__ int4 s_meta[kSmallWarps][32];
   __shared__ int2 s_ep[kSmallWarps][32];
@@ -444,6 +444,7 @@ __global__ void __launch_bounds__(kSmallWarps * 32, SCCG_SMALL_MINB)
       }
     }
   }
+  pdl_done();  // the queue is drained: the item kernel may launch
   status = __reduce_or_sync(FULL, status);
   if (lane == 0) s_acc[warp][10] |= status;
   __syncthreads();
@@ -484,8 +485,7 @@ size_t pixelbox_ws_bytes(int64_t n) {
 }
 
 __global__ void zero_counters_kernel(unsigned long long* queue, unsigned long long* ctr) {
-  pdl_trigger();
-  pdl_wait();  // the small kernel chains onto this one: its completion must imply the join's
+  pdl_entry();  // the small kernel chains onto this one: its completion must imply the join's
   if (threadIdx.x < 4) queue[threadIdx.x] = 0ull;
   else if (threadIdx.x < 8) ctr[threadIdx.x - 4] = 0ull;
 }
@@ -572,7 +572,7 @@ __global__ void set_kernel(long long* out, long long v) { *out = v; }
 __global__ void sums_copy_kernel(const long long* __restrict__ src, volatile long long* dst) {
   pdl_wait();
   constexpr int kWords = (int)(sizeof(sccg_sums) / sizeof(long long));
-  if (threadIdx.x < kWords) dst[threadIdx.x] = src[threadIdx.x];
+  if (threadIdx.x < kWords) dst[threadIdx.x] = ld_coherent(src + threadIdx.x);  // written by atomics of the previous kernels
   __threadfence_system();
 }
 

@@ -411,8 +411,7 @@ __device__ void flush_stats(StatAcc& acc, SetStats* stats, unsigned long long* s
 }
 
 __global__ void __launch_bounds__(kPrepThreads, 5) prep_kernel(const __grid_constant__ PrepArgs args) {
-  pdl_trigger();
-  pdl_wait();  // prep_init's counters
+  pdl_entry_deferred();  // prep_init's counters
   extern __shared__ int4 s_dyn4[];  // kPrepVerts int2 (16-byte aligned)
   int2* s_xy = reinterpret_cast<int2*>(s_dyn4);
   __shared__ int64_t s_off[kPrepPolys + 1];
@@ -632,6 +631,7 @@ __global__ void __launch_bounds__(kPrepThreads, 5) prep_kernel(const __grid_cons
     }
     gt = gt_next;
   }
+  pdl_done();  // no tile left: the join's first kernel may launch
   if (threadIdx.x == 0) bulk_store_drain();
   if (cur >= 0) flush_stats(acc, args.set[cur].stats, s_acc, s_b);
 }
