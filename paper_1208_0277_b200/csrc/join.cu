@@ -353,80 +353,34 @@ __device__ __forceinline__ void probe_cells(const int4& a, const Grid& g, const 
     for (int cx = a.x >> k; cx <= (a.z - 1) >> k; cx++) visit(a, k, cx, cy, g.bucket(cx, cy), t, take);
 }
 
-// A big MBR probed by its whole warp.  Its cell rectangle is taken 32 cells
-// at a time (lane l reads cell l's counter); the slot entries of those cells
-// are flattened over the lanes (a warp scan of min(count, kSlots), a 5-step
-// shuffle search for each entry's cell), so a lane tests entry after entry of
-// ALL the cells with independent loads; a cell's overflow chain is walked by
-// its own lane.  COUNT returns the pairs it owns (every lane gets the total);
-// WRITE appends them to seg[] in arbitrary order (slots from *fill, reset
-// here) -- the q order is restored by the segment sort.
-template <bool WRITE>
-__device__ int coop_cells(const int4 a, long long p, const Grid& g, const Tables& t, int2* __restrict__ seg, int* fill) {
-  const int lane = threadIdx.x & 31;
+// The (big MBR, cell) visits of a probe tile, flattened over its threads:
+// visit v (v < nv) is cell v - cstart[j] of thread j's MBR, j the last thread
+// with cstart[j] <= v (cstart non-decreasing in j; threads without a big MBR
+// have empty ranges).  take(j, owned, q) for every entry tested.
+template <class Take>
+__device__ __forceinline__ void coop_visits(int nv, const int* cstart, const int4* __restrict__ mp, int64_t p0,
+                                            const Grid& g, const Tables& t, int grow, Take&& take) {
   const int k = g.k;
-  const int x0 = a.x >> k, y0 = a.y >> k, w = ((a.z - 1) >> k) - x0 + 1;
-  const int nc = w * (((a.w - 1) >> k) - y0 + 1);
-  if (WRITE) {
-    if (lane == 0) *fill = 0;
-    __syncwarp();
+  for (int v = threadIdx.x; v < nv; v += kProbeTile) {
+    int j = 0;
+    for (int s = kProbeTile / 2; s; s >>= 1)
+      if (cstart[j + s] <= v) j += s;
+    int4 a = mp[p0 + j];
+    a.z += grow;
+    a.w += grow;
+    const int x0 = a.x >> k, y0 = a.y >> k, w = ((a.z - 1) >> k) - x0 + 1;
+    const int c = v - cstart[j];
+    const int cx = x0 + c % w, cy = y0 + c / w;
+    visit(a, k, cx, cy, g.bucket(cx, cy), t, [&](bool h, int q) { take(j, h, q); });
   }
-  int cnt = 0;
-  auto take = [&](bool h, int q) {
-    if (h) {
-      if (WRITE) seg[atomicAdd(fill, 1)] = make_int2((int)p, q);
-      cnt++;
-    }
-  };
-  for (int base = 0; base < nc; base += 32) {  // warp-uniform
-    const int c = base + lane;
-    int cx = 0, cy = 0, b = 0, n = 0, len = 0;
-    if (c < nc) {
-      cx = x0 + c % w;
-      cy = y0 + c / w;
-      b = g.bucket(cx, cy);
-      n = t.count[(size_t)b * kCStride];
-      len = min(n, kSlots);
-    }
-    int incl = len;
-    for (int o = 1; o < 32; o <<= 1) {
-      const int v = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += v;
-    }
-    const int total = __shfl_sync(0xffffffffu, incl, 31);
-    const int excl = incl - len;
-    for (int f0 = 0; f0 < total; f0 += 32) {  // warp-uniform
-      const int f = f0 + lane;
-      int j = 0;  // the lane whose cell holds flattened entry f: #lanes with incl <= f
-      for (int s = 16; s; s >>= 1)
-        if (__shfl_sync(0xffffffffu, incl, j + s - 1) <= f) j += s;
-      const int cxj = __shfl_sync(0xffffffffu, cx, j), cyj = __shfl_sync(0xffffffffu, cy, j);
-      const int bj = __shfl_sync(0xffffffffu, b, j), ej = __shfl_sync(0xffffffffu, excl, j);
-      if (f < total) {
-        const int4 e = t.slot[t.at(bj, f - ej)];
-        take(owns(a, entry_box(e), k, cxj, cyj), e.w);
-      }
-    }
-    if (n > kSlots) {  // rare
-      int o = t.head[b];
-      for (int r = kSlots; r < n; r++) {
-        const int4 e = t.ovf[o];
-        take(owns(a, entry_box(e), k, cx, cy), e.w);
-        o = t.ovf_next[o];
-      }
-    }
-  }
-  for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
-  return cnt;
 }
 
 // Sort seg[0..n) by q (distinct within a segment) with the warp: a bitonic
 // network in its ascending-only form (each merge starts by comparing i with
 // its mirror i ^ (k - 1)), so positions >= n behave as +inf and are never
-// touched -- no padding needed.  Up to kSortBuf keys are sorted in a shared
-// buffer (one per CTA, under a lock -- long segments are rare); longer
-// segments in place in global memory (L1/L2-resident).
-constexpr int kSortBuf = 1024;
+// touched -- no padding needed.  Up to kSortBuf keys are sorted in the warp's
+// shared buffer; longer segments in place in global memory (L1/L2-resident).
+constexpr int kSortBuf = 512;  // keys per warp buffer
 constexpr int kThreadSortMax = 32;  // segments up to this length: the owning thread sorts
 
 template <typename Key, typename Get, typename Put>
@@ -450,24 +404,16 @@ __device__ __forceinline__ void warp_bitonic(int n, Get get, Put put) {
     }
 }
 
-__device__ void warp_sort_segment(int2* seg, int n, int* buf, int* lock) {
+__device__ void warp_sort_segment(int2* seg, int n, int* buf) {
   const int lane = threadIdx.x & 31;
   if (n <= 1) return;
-  if (n <= kSortBuf) {
-    if (lane == 0)
-      while (atomicCAS(lock, 0, 1) != 0) {
-      }
-    __syncwarp();
-    const int p = seg[0].x;
+  const int p = seg[0].x;
+  if (n <= kSortBuf) {  // in the warp's own shared buffer
     for (int i = lane; i < n; i += 32) buf[i] = seg[i].y;
     __syncwarp();
     warp_bitonic<int>(n, [&](int i) { return buf[i]; }, [&](int i, int v) { buf[i] = v; });
     for (int i = lane; i < n; i += 32) seg[i] = make_int2(p, buf[i]);
-    __threadfence_block();
-    __syncwarp();
-    if (lane == 0) atomicExch(lock, 0);
   } else {
-    const int p = seg[0].x;
     __syncwarp();
     warp_bitonic<int>(n, [&](int i) { return seg[i].y; }, [&](int i, int v) { seg[i] = make_int2(p, v); });
   }
@@ -532,12 +478,12 @@ __global__ void __launch_bounds__(kProbeTile, SCCG_PROBE_MINB)
                  const uint32_t* __restrict__ status_q, int grow) {
   __shared__ int s_warp[kProbeTile / 32];
   __shared__ long long s_sum[kProbeTile / 32];
-  __shared__ int s_fill[kProbeTile / 32];
-  __shared__ int s_coop[kProbeTile];     // threads of this tile whose MBR the warps probe together
-  __shared__ int s_coopval[kProbeTile];  // ... their pair count, then their segment start
+  __shared__ int s_fillc[kProbeTile];   // big MBRs' segment fill counters
+  __shared__ int s_cstart[kProbeTile];   // first (big MBR, cell) visit of each thread's MBR
+  __shared__ int s_coopval[kProbeTile];  // big MBRs' pair count, then their segment start
   __shared__ int s_cw[kProbeTile / 32];
-  __shared__ int s_sort[kSortBuf];
-  __shared__ int s_lock;
+  __shared__ int s_sort[kProbeTile / 32][kSortBuf];
+  __shared__ int s_long[kProbeTile];  // threads whose segment is longer than kThreadSortMax
   __shared__ long long s_tile;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   int tile = blockIdx.x;
@@ -618,7 +564,6 @@ __global__ void __launch_bounds__(kProbeTile, SCCG_PROBE_MINB)
     dst = bucket + (size_t)tile * kBucket;
     room = kBucket;
   }
-  if (threadIdx.x == 0) s_lock = 0;
   const int64_t p = (int64_t)tile * kProbeTile + threadIdx.x;
   const Grid g = load_grid(gp);
   int4 a = make_int4(0, 0, 0, 0);
@@ -638,29 +583,34 @@ __global__ void __launch_bounds__(kProbeTile, SCCG_PROBE_MINB)
       keep.w = h && n == 3 ? q : keep.w;
       n += h ? 1 : 0;
     });
-  // big MBRs of the whole tile (glands among nuclei, C3: often consecutive in
-  // p) are dealt round-robin to the tile's warps, so their cell walks run side
-  // by side instead of queueing on the one warp that holds them
-  int ncoop = 0;
+  // Big MBRs of the whole tile (glands among nuclei, C3: often consecutive in
+  // p): their (MBR, cell) visits are flattened over all the tile's threads --
+  // thread v takes visit v, v + kProbeTile, ... -- so a tile holding many
+  // glands is neither a serial walk per warp nor per gland.  s_cstart = the
+  // exclusive scan of the big MBRs' cell counts in thread order; visit v
+  // belongs to the last thread j with s_cstart[j] <= v.
+  const int mycells = coop ? mbr_cells(a, g.k) : 0;
+  int ncv = 0;  // visits in the tile
   if (__syncthreads_or(coop)) {
-    const unsigned cm = __ballot_sync(0xffffffffu, coop);
-    if (lane == 0) s_cw[warp] = __popc(cm);
+    int xc = mycells;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, xc, o);
+      if (lane >= o) xc += y;
+    }
+    if (lane == 31) s_cw[warp] = xc;
     __syncthreads();
-    int off = 0;
+    int wb = 0;
     for (int w = 0; w < kProbeTile / 32; w++) {
-      off += w < warp ? s_cw[w] : 0;
-      ncoop += s_cw[w];
+      wb += w < warp ? s_cw[w] : 0;
+      ncv += s_cw[w];
     }
-    if (coop) s_coop[off + __popc(cm & lanemask_lt())] = threadIdx.x;
+    s_cstart[threadIdx.x] = wb + xc - mycells;
+    if (coop) s_coopval[threadIdx.x] = 0;
     __syncthreads();
-    for (int c = warp; c < ncoop; c += kProbeTile / 32) {
-      const int j = s_coop[c];
-      int4 aj = mp[(int64_t)tile * kProbeTile + j];
-      aj.z += grow;
-      aj.w += grow;
-      const int cnt = coop_cells<false>(aj, (int64_t)tile * kProbeTile + j, g, t, nullptr, nullptr);
-      if (lane == 0) s_coopval[j] = cnt;
-    }
+    coop_visits(ncv, s_cstart, mp, (int64_t)tile * kProbeTile, g, t, grow, [&](int j, bool h, int q) {
+      (void)q;
+      if (h) atomicAdd(&s_coopval[j], 1);
+    });
     __syncthreads();
     if (coop) n = s_coopval[threadIdx.x];
   }
@@ -685,19 +635,17 @@ __global__ void __launch_bounds__(kProbeTile, SCCG_PROBE_MINB)
   }
   int2* seg = dst + base;
   const bool fits = n > 0 && base + n <= room;
-  // big MBRs: gathered by the warps (round-robin as above), unsorted
-  if (ncoop > 0) {
-    if (coop) s_coopval[threadIdx.x] = fits ? base : -1;
-    __syncthreads();
-    for (int c = warp; c < ncoop; c += kProbeTile / 32) {
-      const int j = s_coop[c];
-      if (s_coopval[j] < 0) continue;  // warp-uniform
-      int4 aj = mp[(int64_t)tile * kProbeTile + j];
-      aj.z += grow;
-      aj.w += grow;
-      coop_cells<true>(aj, (int64_t)tile * kProbeTile + j, g, t, dst + s_coopval[j], &s_fill[warp]);
+  // big MBRs: gathered by all threads' visits (as above), unsorted
+  if (ncv > 0) {
+    if (coop) {
+      s_coopval[threadIdx.x] = fits ? base : -1;
+      s_fillc[threadIdx.x] = 0;
     }
-    __syncthreads();  // the warps' writes are visible to the segment's own thread
+    __syncthreads();
+    coop_visits(ncv, s_cstart, mp, (int64_t)tile * kProbeTile, g, t, grow, [&](int j, bool h, int q) {
+      if (h && s_coopval[j] >= 0) dst[s_coopval[j] + atomicAdd(&s_fillc[j], 1)] = make_int2((int)(tile * kProbeTile + j), q);
+    });
+    __syncthreads();  // the visits' writes are visible to the segment's own thread
     if (coop && fits && n <= kThreadSortMax) insertion_sort_q(seg, n);
   }
   if (fits && !coop) {
@@ -728,11 +676,29 @@ __global__ void __launch_bounds__(kProbeTile, SCCG_PROBE_MINB)
       if (n <= kThreadSortMax) insertion_sort_q(seg, n);
     }
   }
-  // long segments (big MBRs, or many hits): sorted by the warp
-  __syncthreads();
-  for (unsigned bm = __ballot_sync(0xffffffffu, fits && n > kThreadSortMax); bm; bm &= bm - 1) {
-    const int j = __ffs(bm) - 1;
-    warp_sort_segment(dst + __shfl_sync(0xffffffffu, base, j), __shfl_sync(0xffffffffu, n, j), s_sort, &s_lock);
+  // long segments (big MBRs, or many hits): dealt round-robin to the warps
+  // (s_coopval / s_fillc reused: each one's start and length)
+  const bool lng = fits && n > kThreadSortMax;
+  int nlong = 0;
+  if (__syncthreads_or(lng)) {
+    const unsigned lm = __ballot_sync(0xffffffffu, lng);
+    if (lane == 0) s_cw[warp] = __popc(lm);
+    __syncthreads();
+    int off = 0;
+    for (int w = 0; w < kProbeTile / 32; w++) {
+      off += w < warp ? s_cw[w] : 0;
+      nlong += s_cw[w];
+    }
+    if (lng) {
+      s_long[off + __popc(lm & lanemask_lt())] = threadIdx.x;
+      s_coopval[threadIdx.x] = base;
+      s_fillc[threadIdx.x] = n;
+    }
+    __syncthreads();
+    for (int c = warp; c < nlong; c += kProbeTile / 32) {
+      const int j = s_long[c];
+      warp_sort_segment(dst + s_coopval[j], s_fillc[j], s_sort[warp]);
+    }
   }
 }
 
