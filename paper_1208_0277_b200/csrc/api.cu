@@ -5,9 +5,19 @@
 #include <stdio.h>
 #include <string.h>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "internal.cuh"
 
 namespace sccg {
+
+// NVTX range around each enqueueing entry point (header-only NVTX v3: a no-op
+// unless a tool -- nsys, ncu --nvtx -- is attached), so a timeline or an ncu
+// --nvtx-include filter can attribute kernels to the ABI call that issued them.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 
 static thread_local char t_msg[256] = "";
 static thread_local int64_t t_index = -1;
@@ -138,12 +148,14 @@ int sccg_polyset_bind(sccg_polyset* set, void* buf, size_t bytes) {
 }
 
 int sccg_prep(const sccg_polyset* set, int32_t validate, sccg_stream_t stream) {
+  NvtxRange nvtx_range("sccg_prep");
   set_error(SCCG_OK, "", -1);
   if (int r = check_set(set, true, "set")) return r;
   return check_cuda(launch_prep(&set, 1, validate, reinterpret_cast<cudaStream_t>(stream)), "sccg_prep");
 }
 
 int sccg_prep_sets(const sccg_polyset* sets, int32_t count, int32_t validate, sccg_stream_t stream) {
+  NvtxRange nvtx_range("sccg_prep_sets");
   set_error(SCCG_OK, "", -1);
   if (!sets || count < 1 || count > 4) return set_error(SCCG_E_ARG, "sccg_prep_sets: sets must hold 1..4 sets");
   const sccg_polyset* ptrs[4];
@@ -179,16 +191,19 @@ static int filter_checked(const sccg_polyset* p, const sccg_polyset* q, int32_t*
 
 int sccg_filter_pairs(const sccg_polyset* p, const sccg_polyset* q, int32_t* pairs, int64_t cap,
                       int64_t* n_pairs_host, void* workspace, size_t ws_bytes, sccg_stream_t stream) {
+  NvtxRange nvtx_range("sccg_filter_pairs");
   return filter_checked(p, q, pairs, cap, n_pairs_host, workspace, ws_bytes, 0, stream);
 }
 
 int sccg_filter_pairs_closed(const sccg_polyset* p, const sccg_polyset* q, int32_t* pairs, int64_t cap,
                              int64_t* n_pairs_host, void* workspace, size_t ws_bytes, sccg_stream_t stream) {
+  NvtxRange nvtx_range("sccg_filter_pairs_closed");
   return filter_checked(p, q, pairs, cap, n_pairs_host, workspace, ws_bytes, 1, stream);
 }
 
 int sccg_touches(const sccg_polyset* p, const sccg_polyset* q, const int32_t* pairs, int64_t n_pairs,
                  const int64_t* inter, uint8_t* touches, sccg_stream_t stream) {
+  NvtxRange nvtx_range("sccg_touches");
   set_error(SCCG_OK, "", -1);
   if (int r = check_set(p, true, "p")) return r;
   if (int r = check_set(q, true, "q")) return r;
@@ -202,6 +217,7 @@ int sccg_touches(const sccg_polyset* p, const sccg_polyset* q, const int32_t* pa
 
 int sccg_contains(const sccg_polyset* p, const sccg_polyset* q, const int32_t* pairs, int64_t n_pairs,
                   const int64_t* inter, uint8_t* contains, sccg_stream_t stream) {
+  NvtxRange nvtx_range("sccg_contains");
   set_error(SCCG_OK, "", -1);
   if (int r = check_set(p, true, "p")) return r;
   if (int r = check_set(q, true, "q")) return r;
@@ -216,6 +232,7 @@ int sccg_contains(const sccg_polyset* p, const sccg_polyset* q, const int32_t* p
 int sccg_report(const sccg_polyset* p, const sccg_polyset* q, const int32_t* pairs, int64_t n_pairs,
                 const int64_t* inter, const int64_t* uni, const uint32_t* hit_p, const uint32_t* hit_q,
                 const sccg_tiling* tiling, sccg_tile_report* tiles, sccg_stream_t stream) {
+  NvtxRange nvtx_range("sccg_report");
   set_error(SCCG_OK, "", -1);
   if (int r = check_set(p, true, "p")) return r;
   if (int r = check_set(q, true, "q")) return r;
@@ -233,12 +250,14 @@ int sccg_report(const sccg_polyset* p, const sccg_polyset* q, const int32_t* pai
 }
 
 int sccg_sums_pack(const sccg_sums* src, int64_t* vec, sccg_stream_t stream) {
+  NvtxRange nvtx_range("sccg_sums_pack");
   set_error(SCCG_OK, "", -1);
   if (!src || !vec || !aligned(src, 8) || !aligned(vec, 8)) return set_error(SCCG_E_ARG, "sccg_sums_pack: null or misaligned pointer");
   return check_cuda(launch_sums_pack(src, vec, reinterpret_cast<cudaStream_t>(stream)), "sccg_sums_pack");
 }
 
 int sccg_sums_unpack(const int64_t* vec, sccg_sums* dst, sccg_stream_t stream) {
+  NvtxRange nvtx_range("sccg_sums_unpack");
   set_error(SCCG_OK, "", -1);
   if (!vec || !dst || !aligned(vec, 8) || !aligned(dst, 8)) return set_error(SCCG_E_ARG, "sccg_sums_unpack: null or misaligned pointer");
   return check_cuda(launch_sums_unpack(vec, dst, reinterpret_cast<cudaStream_t>(stream)), "sccg_sums_unpack");
@@ -246,6 +265,7 @@ int sccg_sums_unpack(const int64_t* vec, sccg_sums* dst, sccg_stream_t stream) {
 
 int sccg_filter_pairs_async(const sccg_polyset* p, const sccg_polyset* q, int32_t* pairs, int64_t cap,
                             int64_t* result_dev, void* workspace, size_t ws_bytes, sccg_stream_t stream) {
+  NvtxRange nvtx_range("sccg_filter_pairs_async");
   set_error(SCCG_OK, "", -1);
   if (int r = check_set(p, true, "p")) return r;
   if (int r = check_set(q, true, "q")) return r;
@@ -280,6 +300,7 @@ static int pixelbox_checks(const sccg_polyset* p, const sccg_polyset* q, const i
 int sccg_pixelbox_async(const sccg_polyset* p, const sccg_polyset* q, const int32_t* pairs, const int64_t* result_dev,
                         int64_t cap, int64_t* inter, int64_t* uni, sccg_sums* sums, const sccg_config* cfg,
                         void* workspace, size_t ws_bytes, sccg_stream_t stream) {
+  NvtxRange nvtx_range("sccg_pixelbox_async");
   set_error(SCCG_OK, "", -1);
   if (!result_dev || !aligned(result_dev, 8)) return set_error(SCCG_E_ARG, "result_dev must be a non-null aligned device int64[2]");
   if (int r = pixelbox_checks(p, q, pairs, cap, inter, uni, sums, cfg)) return r;
@@ -290,6 +311,7 @@ int sccg_pixelbox_async(const sccg_polyset* p, const sccg_polyset* q, const int3
 int sccg_pixelbox(const sccg_polyset* p, const sccg_polyset* q, const int32_t* pairs, int64_t n_pairs, int64_t* inter,
                   int64_t* uni, sccg_sums* sums, const sccg_config* cfg, void* workspace, size_t ws_bytes,
                   sccg_stream_t stream) {
+  NvtxRange nvtx_range("sccg_pixelbox");
   set_error(SCCG_OK, "", -1);
   if (int r = pixelbox_checks(p, q, pairs, n_pairs, inter, uni, sums, cfg)) return r;
   return run_pixelbox(p, q, pairs, n_pairs, nullptr, inter, uni, sums, cfg, workspace, ws_bytes,
@@ -297,6 +319,7 @@ int sccg_pixelbox(const sccg_polyset* p, const sccg_polyset* q, const int32_t* p
 }
 
 int sccg_count_missing(const uint32_t* hit, int64_t n, int64_t* missing_dev, sccg_stream_t stream) {
+  NvtxRange nvtx_range("sccg_count_missing");
   set_error(SCCG_OK, "", -1);
   if (n < 0 || !missing_dev || (n > 0 && !hit)) return set_error(SCCG_E_ARG, "sccg_count_missing: bad argument");
   if (!aligned(hit, 4) || !aligned(missing_dev, 8)) return set_error(SCCG_E_ARG, "sccg_count_missing: misaligned");
@@ -304,6 +327,7 @@ int sccg_count_missing(const uint32_t* hit, int64_t n, int64_t* missing_dev, scc
 }
 
 int sccg_sums_copy(const sccg_sums* src, sccg_sums* dst, sccg_stream_t stream) {
+  NvtxRange nvtx_range("sccg_sums_copy");
   set_error(SCCG_OK, "", -1);
   if (!src || !dst || !aligned(src, 8) || !aligned(dst, 8)) return set_error(SCCG_E_ARG, "sccg_sums_copy: null or misaligned pointer");
   return check_cuda(launch_sums_copy(src, dst, reinterpret_cast<cudaStream_t>(stream)), "sccg_sums_copy");

@@ -112,11 +112,7 @@ __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\
 // descriptor, a device-side count) are read with L1-bypassing loads after
 // pdl_wait(): a CTA launched early may otherwise see a stale L1 / read-only
 // cache line of a recycled address (measured on the join's grid descriptor).
-__device__ __forceinline__ long long ld_coherent(const long long* p) {
-  long long v;
-  asm volatile("ld.relaxed.gpu.global.s64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
+__device__ __forceinline__ long long ld_coherent(const long long* p) { return __ldcg(p); }  // ld.global.cg: L2
 
 // Where a kernel lets its successor launch.  Early (SCCG_PDL_LATE=0, the
 // round-1 order): trigger at entry, so the successor's CTAs -- and, since

@@ -43,18 +43,13 @@ struct __align__(16) Grid {
 };
 
 // The grid is written by the selection kernel two launches earlier: read it
-// with an L1-bypassing load (ld.relaxed.gpu), never through the read-only /
+// with an L1-bypassing load (ld.global.cg), never through the read-only /
 // L1 path -- under programmatic dependent launch a CTA that started early
 // could otherwise see a stale copy of a recycled workspace (measured: a
 // previous join's grid at the same address).
 __device__ __forceinline__ Grid load_grid(const Grid* gp) {
-  const int* w = reinterpret_cast<const int*>(gp);
-  Grid g;
-  asm volatile("ld.relaxed.gpu.global.v4.s32 {%0, %1, %2, %3}, [%4];"
-               : "=r"(g.k), "=r"(g.ax), "=r"(g.ay), "=r"(g.empty)
-               : "l"(w)
-               : "memory");
-  return g;
+  const int4 v = __ldcg(reinterpret_cast<const int4*>(gp));
+  return Grid{v.x, v.y, v.z, v.w};
 }
 
 __device__ __forceinline__ bool mbr_empty(const int4& m) { return m.x >= m.z || m.y >= m.w; }
@@ -432,27 +427,7 @@ __device__ __forceinline__ void insertion_sort_q(int2* seg, int n) {
   }
 }
 
-// Tile states of the compaction's decoupled look-back: flag in bits 62-63
-// (0 = not yet, 1 = the tile's own count, 2 = inclusive prefix), value below;
-// one 64-bit word, so value and flag are published together.
-constexpr unsigned long long kFlagAgg = 1ull << 62, kFlagPre = 2ull << 62, kValMask = (1ull << 62) - 1;
-__device__ __forceinline__ unsigned long long ld_relaxed(const unsigned long long* p) {
-  unsigned long long v;
-  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_relaxed(unsigned long long* p, unsigned long long v) {
-  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ int ld_coherent_i(const int* p) {
-  int v;
-  asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
 
-#ifndef SCCG_JOIN_LOOKBACK
-#define SCCG_JOIN_LOOKBACK 0  // 1: the compaction's offsets by decoupled look-back (measured slower)
-#endif
 #ifndef SCCG_PROBE_MINB
 #define SCCG_PROBE_MINB 8
 #endif
@@ -472,8 +447,7 @@ constexpr int kBucket = 1024;  // pairs per probe tile held in its bucket betwee
 template <bool COMPACT>
 __global__ void __launch_bounds__(kProbeTile, SCCG_PROBE_MINB)
     probe_kernel(const int4* __restrict__ mp, int64_t np, const Grid* __restrict__ gp, Tables t,
-                 int* __restrict__ tile_cnt, int2* __restrict__ bucket, unsigned long long* __restrict__ tstate,
-                 unsigned long long* __restrict__ ticket, int2* __restrict__ pairs, long long cap,
+                 int* __restrict__ tile_cnt, int2* __restrict__ bucket, int2* __restrict__ pairs, long long cap,
                  long long* __restrict__ total, long long* __restrict__ result, const uint32_t* __restrict__ status_p,
                  const uint32_t* __restrict__ status_q, int grow) {
   __shared__ int s_warp[kProbeTile / 32];
@@ -484,50 +458,12 @@ __global__ void __launch_bounds__(kProbeTile, SCCG_PROBE_MINB)
   __shared__ int s_cw[kProbeTile / 32];
   __shared__ int s_sort[kProbeTile / 32][kSortBuf];
   __shared__ int s_long[kProbeTile];  // threads whose segment is longer than kThreadSortMax
-  __shared__ long long s_tile;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  int tile = blockIdx.x;
+  const int tile = blockIdx.x;
   pdl_entry();
   int2* dst;       // this tile's output: its bucket, or its final place
   long long room;  // slots available from dst
   if (COMPACT) {
-#if SCCG_JOIN_LOOKBACK
-    // this tile's offset: a decoupled look-back over the preceding tiles'
-    // counts (every count is known from the bucket pass, so each tile
-    // publishes its own at once and the look-back never waits on work);
-    // tiles are taken in ticket order, so every predecessor is running
-    if (threadIdx.x == 0) s_tile = (long long)atomicAdd(ticket, 1ull);
-    __syncthreads();
-    tile = (int)s_tile;
-    const int cnt = ld_coherent_i(tile_cnt + tile);
-    if (warp == 0) {
-      long long excl = 0;
-      if (tile == 0) {
-        if (lane == 0) st_relaxed(&tstate[0], kFlagPre | (unsigned long long)cnt);
-      } else {
-        if (lane == 0) st_relaxed(&tstate[tile], kFlagAgg | (unsigned long long)cnt);
-        long long idx = tile - 1;
-        for (;;) {  // warp-uniform
-          const long long i = idx - lane;
-          unsigned long long v;
-          do {
-            v = i >= 0 ? ld_relaxed(&tstate[i]) : kFlagPre;
-          } while (__any_sync(0xffffffffu, (v >> 62) == 0));
-          const unsigned pm = __ballot_sync(0xffffffffu, (v >> 62) == 2);
-          const int stop = pm ? __ffs(pm) - 1 : 31;
-          long long val = lane <= stop ? (long long)(v & kValMask) : 0;
-          for (int o = 16; o; o >>= 1) val += __shfl_xor_sync(0xffffffffu, val, o);
-          excl += val;
-          if (pm) break;
-          idx -= 32;
-        }
-        if (lane == 0) st_relaxed(&tstate[tile], kFlagPre | (unsigned long long)(excl + cnt));
-      }
-      if (lane == 0) s_sum[0] = excl;
-    }
-    __syncthreads();
-    const long long off = s_sum[0];
-#else
     // this tile's offset: the preceding tiles' counts (all known by now; a
     // few vectorized L2 loads per thread)
     long long sum = 0;
@@ -543,7 +479,6 @@ __global__ void __launch_bounds__(kProbeTile, SCCG_PROBE_MINB)
     long long off = 0;
     for (int w = 0; w < kProbeTile / 32; w++) off += s_sum[w];
     const int cnt = tile_cnt[tile];
-#endif
     if (tile == (int)gridDim.x - 1 && threadIdx.x == 0) {
       *total = off + cnt;
       if (result) {
@@ -709,8 +644,6 @@ struct FilterWs {
   Grid* grid;
   Tables t;
   int* tile_cnt;  // [T] pairs per probe tile
-  unsigned long long* tstate;  // [T] the compaction's look-back states
-  unsigned long long* ticket;  // the compaction's tile ticket
   int2* bucket;   // [T][kBucket] per-tile pair buckets
   long long* total;
   char* zero;     // cleared by the grid selection: bucket counters, overflow pool counter
@@ -724,15 +657,13 @@ static size_t filter_layout(int64_t np, int64_t nq, Carve& cv, FilterWs& w) {
   w.hb = hb;
   w.grid = cv.take<Grid>(1);
   w.total = cv.take<long long>(1);
-  // one contiguous cleared region: count[H] | pool counter, ticket | tile states[T]
+  // one contiguous cleared region: count[H] | pool counter
   const size_t cb = (size_t)4 * H * kCStride;
-  w.zero_bytes = cb + 16 + (size_t)8 * ((T + 1) & ~int64_t(1));
+  w.zero_bytes = cb + 16;
   w.zero = cv.take<char>(w.zero_bytes);
   if (w.zero) {
     w.t.count = reinterpret_cast<int*>(w.zero);
     w.t.ovf_n = reinterpret_cast<int*>(w.zero + cb);
-    w.ticket = reinterpret_cast<unsigned long long*>(w.zero + cb + 8);
-    w.tstate = reinterpret_cast<unsigned long long*>(w.zero + cb + 16);
   }
   w.tile_cnt = cv.take<int>(T + 4);
   w.bucket = cv.take<int2>(T * kBucket);
@@ -792,10 +723,10 @@ static int filter_enqueue(const sccg_polyset* P, const sccg_polyset* Q, FilterWs
     launch_pdl(grid_insert_kernel, dim3(blocks_for(nq, 256)), dim3(256), 0, stream, mq, nq, w.grid, w.t, grow);
   if (np > 0) {
     launch_pdl(probe_kernel<false>, dim3((unsigned)T), dim3(kProbeTile), 0, stream, mp, np, w.grid, w.t, w.tile_cnt,
-               w.bucket, w.tstate, w.ticket, (int2*)nullptr, (long long)0, (long long*)nullptr, (long long*)nullptr,
+               w.bucket, (int2*)nullptr, (long long)0, (long long*)nullptr, (long long*)nullptr,
                (const uint32_t*)nullptr, (const uint32_t*)nullptr, grow);
     launch_pdl(probe_kernel<true>, dim3((unsigned)T), dim3(kProbeTile), 0, stream, mp, np, w.grid, w.t, w.tile_cnt,
-               w.bucket, w.tstate, w.ticket, reinterpret_cast<int2*>(pairs), (long long)(pairs ? cap : 0), w.total, result, P->status,
+               w.bucket, reinterpret_cast<int2*>(pairs), (long long)(pairs ? cap : 0), w.total, result, P->status,
                Q->status, grow);
   } else
     launch_pdl(filter_result_kernel, dim3(1), dim3(32), 0, stream, w.total, P->status, Q->status, result);

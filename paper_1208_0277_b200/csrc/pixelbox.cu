@@ -129,12 +129,15 @@ __global__ void __launch_bounds__(kSmallWarps * 32, SCCG_SMALL_MINB)
   pdl_entry_deferred();
   // pair count: host-given, or (async path) the filter's device-side count clamped to the buffer
   // (a join that overflowed the buffer left it incomplete: nothing is processed, the status says so)
-  const long long r0 = dev_result ? ld_coherent(dev_result) : 0, r1 = dev_result ? ld_coherent(dev_result + 1) : 0;
+  const long long r0 = dev_result ? ld_coherent(dev_result) : 0;
   const bool overflow = dev_result && r0 > n_cap;
   const long long n = dev_result ? (overflow ? 0 : r0) : n_cap;
-  if (dev_result && blockIdx.x == 0 && threadIdx.x == 0 && (r1 || overflow))
-    atomicOr(reinterpret_cast<unsigned long long*>(&sums->status),
-             (unsigned long long)r1 | (overflow ? (unsigned long long)SCCG_STATUS_CAPACITY : 0ull));
+  if (dev_result && blockIdx.x == 0 && threadIdx.x == 0) {
+    const long long r1 = ld_coherent(dev_result + 1);
+    if (r1 || overflow)
+      atomicOr(reinterpret_cast<unsigned long long*>(&sums->status),
+               (unsigned long long)r1 | (overflow ? (unsigned long long)SCCG_STATUS_CAPACITY : 0ull));
+  }
   __shared__ __align__(16) int2 s_buf[kSmallWarps][2 * kSmallQOff];
   __shared__ int4 s_meta[kSmallWarps][32];
   __shared__ int2 s_ep[kSmallWarps][32];
