@@ -54,7 +54,9 @@ def parse():
     ap.add_argument("--steps", type=int, default=300)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="slide", choices=["slide", "tile", "skewed", "combs"])
+    ap.add_argument("--config", default="slide", choices=["slide", "tile", "skewed", "combs", "study"])
+    ap.add_argument("--images", type=int, default=100, help="study: whole-slide image pairs in the study (configs[3])")
+    ap.add_argument("--bases", type=int, default=2, help="study: distinct generated slides the images are instanced from")
     ap.add_argument("--threshold", type=int, default=0)
     ap.add_argument("--shard", default="image", choices=["image", "tile"],
                     help="N > 1: image = one slide image per rank (weak scaling, configs[3]); tile = ONE slide cut "
@@ -222,6 +224,8 @@ def config_desc(config):
         "tile": "configs[0]: one 4096x4096 tile, ~1,000 nucleus polygons per set",
         "skewed": "configs[2]: 4x4 tiles, nuclei + 16 glands per tile (MBR side up to 512)",
         "combs": "configs[4] analog: 16,384 independent highly concave comb pairs, 500-2000 vertices",
+        "study": "configs[3]: a multi-image study of whole-slide image pairs (100k x 100k, ~500k nuclei per set), "
+                 "sharded by image over the GPUs, one all-reduce of the integer sums",
     }[config]
 
 
@@ -519,6 +523,239 @@ def run_ours(args, rank, world, local_rank):
     return out, (A, B, ref_pass)
 
 
+# ----------------------------------------------------------- configs[3]
+def study_images(n_images: int, n_bases: int):
+    """The study's image list: image i is base slide i % n_bases under grid
+    symmetry (i // n_bases) % 8 (transpose, then mirror x / y) and an integer
+    translation.  A symmetry of the pixel lattice maps pixel cells to pixel
+    cells, so every pair's |p n q| and |p u q| -- and the MBR pair list -- are
+    the base's (pinned by the oracle's symmetry invariants, tests/test_oracle.py);
+    the coordinates, ring orientation (mirrors make rings clockwise) and raster
+    shapes (transposes) differ per image."""
+    out = []
+    for i in range(n_images):
+        sym = (i // n_bases) % 8
+        out.append({"image": i, "base": i % n_bases, "sym": sym,
+                    "dx": 200_000 + 131_072 * (i % 64), "dy": 200_000 + 131_072 * (i // 64)})
+    return out
+
+
+def instance_xy(xy, sym: int, dx: int, dy: int):
+    """Device-side instancing of one image from its base (torch on the GPU;
+    input synthesis, not a step of the path): (x, y) -> symmetry -> + (dx, dy)."""
+    import torch
+
+    x, y = xy[:, 0], xy[:, 1]
+    if sym & 4:
+        x, y = y, x
+    if sym & 1:
+        x = -x
+    if sym & 2:
+        y = -y
+    return torch.stack([x + dx, y + dy], 1).to(torch.int32).contiguous()
+
+
+def run_study(args, rank, world, local_rank):
+    """configs[3]: the study's images sharded over the ranks by LPT (equal
+    costs per base: round robin), each rank's images resident in HBM and run
+    back to back as ONE graph (sccg.Study: prep, join, PixelBox per image, all
+    adding into one device sums vector), then ONE all-reduce of the packed
+    int64 sums (NCCL, captured in the same graph; gloo: after it).  A step =
+    one pass over all images of the study.  The rank-local sums must equal
+    the sum of the oracle's sums of each image's base (self-check)."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_1208_0277_b200 as sccg
+    from paper_1208_0277_b200 import dist as sdist
+
+    local_rank = local_rank % max(torch.cuda.device_count(), 1)
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if rank == 0:
+        sccg.load(build=True)
+    if world > 1:
+        dist.barrier()
+    sccg.load(build=False)
+    plan = study_images(args.images, args.bases)
+    mine = [plan[i] for i in sdist.shard_for_rank(len(plan), world, rank)]
+    bases_needed = sorted({im["base"] for im in mine})
+    threads = max(1, (os.cpu_count() or 1) // world)
+    host, dbase, ref = {}, {}, {}
+    for b in bases_needed:
+        A, B = make_workload("slide", image=b)
+        t = [torch.from_numpy(v).pin_memory() for v in (A.xy, A.offsets, B.xy, B.offsets)]
+        host[b] = t
+        dbase[b] = [v.to(dev) for v in t]
+        r = oracle_pass(A, B, threads)  # the self-check's expected sums for every image of this base
+        o = r["sums"]
+        ref[b] = {"sums": [o["n_pairs"], o["n_nonzero"], o["sum_inter"], o["sum_union"], o["sum_area_p"],
+                           o["sum_area_q"]], "units": r["units"], "seconds": r["seconds"], "A": A, "B": B}
+    images = []
+    for im in mine:
+        xp, op, xq, oq = dbase[im["base"]]
+        images.append((instance_xy(xp, im["sym"], im["dx"], im["dy"]), op,
+                       instance_xy(xq, im["sym"], im["dx"], im["dy"]), oq))
+    torch.cuda.synchronize()
+    backend = dist.get_backend() if world > 1 else None
+    host_bufs = [torch.zeros(len(sccg.SUMS_FIELDS), dtype=torch.int64).pin_memory() for _ in range(2)]
+    done_ev = [torch.cuda.Event() for _ in range(2)]
+    # the all-reduce inside the step graph when NCCL (graph-capturable); gloo runs it after the graph
+    in_graph = world > 1 and backend == "nccl"
+    study = sccg.Study(images, threshold=args.threshold, graph=True, readback=host_bufs if world == 1 or in_graph else (),
+                       allreduce=sdist.allreduce_sums if in_graph else None)
+    # the self-check needs the rank-local sums: one eager pass without the all-reduce
+    study.allreduce = None
+    study.run(events=[[torch.cuda.Event() for _ in range(4)] for _ in images])
+    torch.cuda.synchronize()
+    study.check()
+    local = [int(v) for v in study.sums.tolist()]
+    want = [sum(ref[im["base"]]["sums"][f] for im in mine) for f in range(6)]
+    units = sum(int(v) << (30 * k) for k, v in enumerate(local[6:10]))
+    if local[:6] != want or units != sum(ref[im["base"]]["units"] for im in mine):
+        raise RuntimeError(f"study self-check: rank sums {local[:6]} != the oracle's {want} (or ratio units)")
+    study.allreduce = sdist.allreduce_sums if in_graph else None
+    check = {"oracle": f"full oracle pass of each base slide; every image's sums = its base's (lattice symmetry), "
+                       f"rank-local sums == sum over its {len(mine)} images", "images_checked": len(mine),
+             "oracle_seconds": sum(ref[b]["seconds"] for b in bases_needed)}
+
+    def enqueue(i, events=None):
+        sums = study.run(events, slot=i % 2)
+        if world > 1 and not in_graph:
+            sdist.allreduce_sums(sums)
+            host_bufs[i % 2].copy_(sums, non_blocking=True)
+        done_ev[i % 2].record()
+
+    def collect(i):
+        done_ev[i % 2].synchronize()
+        return sccg.sums_to_host(host_bufs[i % 2])
+
+    for i in range(max(args.warmup, 3)):
+        enqueue(i)
+        first = collect(i)
+    if world == 1 and [getattr(first, f) for f in sccg.SUMS_FIELDS] != local:
+        raise RuntimeError("study warm-up sums differ from the checked pass's")
+    # algorithmic prep bytes of every image (untimed: each image prepped once on its own)
+    alg = 0
+    for xp, op, xq, oq in images:
+        for xy, off in ((xp, op), (xq, oq)):
+            S = sccg.DeviceSet(xy, off)
+            alg += prep_algorithmic_bytes(sccg, S)
+            del S
+    stream = torch.cuda.current_stream()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    sampled = list(range(0, args.steps, STAGE_EVERY))
+    stage_ev = {i: [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in images] for i in sampled}
+    results = []
+    with ClockSampler(local_rank) as clk:
+        t0.record(stream)
+        wall0 = time.perf_counter()
+        for i in range(args.steps):
+            enqueue(i, stage_ev.get(i))
+            if i > 0:
+                results.append(collect(i - 1))
+        results.append(collect(args.steps - 1))
+        t1.record(stream)
+        torch.cuda.synchronize()
+        wall1 = time.perf_counter()
+    stage_ms = [sum(ev[k].elapsed_time(ev[k + 1]) for evs in stage_ev.values() for ev in evs) for k in range(3)]
+    final = results[-1]
+    if any(bytes(r) != bytes(first) for r in results):
+        raise RuntimeError("a timed study step's sums differ from the warm-up's (nondeterminism)")
+    if any(int(r.status) for r in results):
+        raise RuntimeError("a timed study step's sums carry device status bits")
+    if world > 1:
+        dist.barrier()
+    ms = t0.elapsed_time(t1)
+    times = torch.tensor([ms] + [t / len(sampled) for t in stage_ms] + [float(local[0]), float(alg)],
+                         dtype=torch.float64, device=dev)
+    if world > 1:
+        mx = times.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        tot = times.clone()
+        dist.all_reduce(tot, op=dist.ReduceOp.SUM)
+    else:
+        mx, tot = times, times
+    ms_max, prep_ms_max, join_ms_max, pix_ms_max = (float(v) for v in mx[:4])
+    total_pairs = int(round(float(tot[4])))
+    if int(final.n_pairs) != total_pairs:
+        raise RuntimeError("all-reduced pair count differs from the ranks' total")
+    jprime, pooled = sccg.jaccard(final)
+
+    # e2e: each image through the public API from pinned host memory (H2D of its inputs -- the base slide's
+    # buffers: an image differs from its base only by an exact lattice symmetry, so the bytes moved and the
+    # areas are the same), join, PixelBox, all-reduce, D2H of the sums
+    e2e_steps = 1
+    h2d = 0
+    for im in mine:
+        h2d += sum(t.numel() * t.element_size() for t in host[im["base"]])
+
+    def e2e_step():
+        s = sccg.new_sums(dev)
+        for im in mine:
+            a, b, c, d = (t.to(dev, non_blocking=True) for t in host[im["base"]])
+            Pe, Qe = sccg.DeviceSet(a, b), sccg.DeviceSet(c, d)
+            pr = sccg.filter_pairs(Pe, Qe, cap=study.cap)
+            sccg.pixelbox(Pe, Qe, pr, threshold=args.threshold, sums=s, want_inter=False, want_union=False,
+                          check=False)
+        if world > 1:
+            sdist.allreduce_sums(s)
+        return sccg.jaccard(s.cpu())
+
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    je, _ = e2e_step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if not (je == jprime or (math.isnan(je) and math.isnan(jprime))):
+        raise RuntimeError("study e2e J' differs from the device-resident step's")
+    e_ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
+    e2e_value = total_pairs * e2e_steps / (float(e_ms[0]) / 1e3)
+    if rank != 0:
+        return None, None
+    clocks = clk.summary()
+    alg_rank0 = float(times[5])
+    achieved = alg_rank0 / (prep_ms_max / 1e3) / 1e9
+    peak, peak_src = hbm_peak()
+    cfg = {"workload": "study", "description": config_desc("study"), "images": args.images, "bases": args.bases,
+           "images_per_gpu": len(mine), "pairs_total": total_pairs, "pairs_per_image": ref[bases_needed[0]]["sums"][0],
+           "instancing": "image i = base slide i % bases under lattice symmetry (i // bases) % 8 + translation, "
+                         "instanced on the device before the timed region",
+           "parallelism": f"image-sharded x{world} (LPT)" if world > 1 else "1 GPU",
+           "allreduce": ("NCCL, in the step graph" if in_graph else "gloo, after the graph") if world > 1 else None,
+           "threshold_T": args.threshold or 2048,
+           "l2": "inputs larger than L2 (~%d MB of vertices per image)" % ((images[0][0].numel() + images[0][2].numel()) * 4 // 2**20)}
+    out = {
+        "metric": METRIC, "value": total_pairs * args.steps / (ms_max / 1e3), "unit": "pairs/s", "n_gpus": world,
+        "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": ms_max / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int32",
+        "data": "synthetic (seeded generator synth/, instanced per image on the device)", "impl": "ours",
+        "config": cfg,
+        "stage_ms": {"prep": prep_ms_max, "join": join_ms_max, "pixelbox": pix_ms_max, "sampled_steps": len(sampled),
+                     "every": STAGE_EVERY, "note": "summed over the rank's images (sampled steps run eagerly)"},
+        "jprime": jprime, "pooled_jaccard": pooled, "self_check": check,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": None, "kernel": "prep_kernel (P and Q in one launch per image)",
+                     "algorithmic_bytes_per_launch": alg_rank0 / max(1, len(mine)), "peak_source": peak_src},
+        "e2e": {"value": e2e_value, "unit": "pairs/s", "h2d_bytes_per_step": int(h2d),
+                "d2h_bytes_per_step": len(sccg.SUMS_FIELDS) * 8, "steps": e2e_steps},
+        "gpu_launches": (LAUNCHES_PER_STEP - 1) * len(mine) * args.steps + (2 if world == 1 else 4) * args.steps,
+        "clocks": clocks, "wall_s": wall1 - wall0,
+    }
+    return out, None
+
+
 def cpu_model() -> str:
     try:
         with open("/proc/cpuinfo") as f:
@@ -659,9 +896,9 @@ def main():
             dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
         else:
             dist.init_process_group(backend)
-    out, extra = run_ours(args, rank, world, local_rank)
+    out, extra = (run_study if args.config == "study" else run_ours)(args, rank, world, local_rank)
     if rank == 0:
-        if not args.no_cpu_baseline and world == 1 and args.config != "combs":  # the oracle baseline: rank 0, N = 1
+        if not args.no_cpu_baseline and world == 1 and args.config not in ("combs", "study"):  # rank 0, N = 1
             A, B, ref_pass = extra
             out["cpu_baseline"] = cpu_baseline(args.config, A, B, ref_pass)
         line = json.dumps(out)

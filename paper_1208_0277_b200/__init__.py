@@ -427,6 +427,126 @@ class Pipeline:
         return n
 
 
+class Study:
+    """Many image pairs on one GPU (configs[3]: a multi-image study, "hundreds
+    of whole slide images are common"; image-granularity tasks).
+
+    Each image's inputs (xy, offsets of both sets) stay resident in HBM; the
+    derived buffers, the pair buffer, the per-pair outputs and the workspaces
+    are sized for the largest image and shared -- the images run one after the
+    other on one stream (prep, MBR join, PixelBox per image, the async ABI: no
+    host sync) and every image's PixelBox adds into ONE device sums vector.  The
+    rank's whole pass -- optionally followed by the all-reduce of the sums
+    (``allreduce``: a callable enqueued after the last image, e.g. NCCL, which
+    graphs can capture) and the read-back -- is ONE CUDA graph.
+
+    images: list of (xy_p, off_p, xy_q, off_q) CUDA tensors (int32 [V, 2], int64 [n + 1])."""
+
+    def __init__(self, images, cap: int | None = None, threshold: int = 0, graph: bool = True, validate: bool = True,
+                 raster: bool = True, readback=(), allreduce=None):
+        torch = _torch()
+        self.lib = lib = load()
+        if not images:
+            raise ValueError("Study needs at least one image")
+        dev = images[0][0].device
+        for t4 in images:
+            for t, name, dt in zip(t4, ("xy_p", "off_p", "xy_q", "off_q"), (torch.int32, torch.int64, torch.int32,
+                                                                            torch.int64)):
+                _require_cuda(t, name, dt)
+        self.images = list(images)
+        dims = [(int(op.numel()) - 1, int(xp.numel()) // 2, int(oq.numel()) - 1, int(xq.numel()) // 2)
+                for xp, op, xq, oq in self.images]
+        self.n_images = len(dims)
+        # shared derived buffers, one per side, bound per image (the layout is carved from each image's sizes)
+        bp = max(int(lib.sccg_polyset_bytes(a, b)) for a, b, _, _ in dims)
+        bq = max(int(lib.sccg_polyset_bytes(c, d)) for _, _, c, d in dims)
+        self._bufs = (torch.empty(bp, dtype=torch.uint8, device=dev), torch.empty(bq, dtype=torch.uint8, device=dev))
+        self._sets = []
+        for (xp, op, xq, oq), (n_p, nv_p, n_q, nv_q) in zip(self.images, dims):
+            cp = PolySet(xp.data_ptr(), op.data_ptr(), n_p, nv_p, None, None, None, None, None, None)
+            cq = PolySet(xq.data_ptr(), oq.data_ptr(), n_q, nv_q, None, None, None, None, None, None)
+            _check(lib.sccg_polyset_bind(ctypes.byref(cp), self._bufs[0].data_ptr(), bp), "sccg_polyset_bind")
+            _check(lib.sccg_polyset_bind(ctypes.byref(cq), self._bufs[1].data_ptr(), bq), "sccg_polyset_bind")
+            self._sets.append((PolySet * 2)(cp, cq))
+        self.cap = int(cap) if cap is not None else max(3 * max(a, c) + 1024 for a, _, c, _ in dims)
+        self.pairs = torch.empty((self.cap, 2), dtype=torch.int32, device=dev)
+        self.result = torch.zeros(2, dtype=torch.int64, device=dev)
+        self.inter = torch.empty(self.cap, dtype=torch.int64, device=dev)  # each image's (I, U) per pair (row a7)
+        self.uni = torch.empty(self.cap, dtype=torch.int64, device=dev)
+        self.fws_bytes = max(int(lib.sccg_filter_workspace_bytes(a, c)) for a, _, c, _ in dims)
+        self.fws = torch.empty(self.fws_bytes, dtype=torch.uint8, device=dev)
+        self.pws_bytes = int(lib.sccg_pixelbox_workspace_bytes(self.cap))
+        self.pws = torch.empty(max(self.pws_bytes, 256), dtype=torch.uint8, device=dev)
+        self.sums = new_sums(dev)
+        self._zero = new_sums(dev)
+        self.cfg = Config(threshold, 0, 0 if raster else FLAG_NO_RASTER, 0, None, None, None)
+        self.validate = 1 if validate else 0
+        self.readback = tuple(readback)
+        self.allreduce = allreduce
+        self._slot = 0
+        self._graphs = None
+        if graph:
+            s = torch.cuda.Stream(device=dev)
+            s.wait_stream(torch.cuda.current_stream(dev))
+            with torch.cuda.stream(s):  # warm-up outside capture
+                self._enqueue()
+            torch.cuda.current_stream(dev).wait_stream(s)
+            torch.cuda.synchronize(dev)
+            self._graphs = []
+            for k in range(max(1, len(self.readback))):
+                self._slot = k
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g):
+                    self._enqueue()
+                self._graphs.append(g)
+
+    def _image(self, i, stage):
+        lib, st = self.lib, _stream_ptr()
+        sets = self._sets[i]
+        if stage == 0:
+            _check(lib.sccg_prep_sets(sets, 2, self.validate, st), "sccg_prep_sets")
+        elif stage == 1:
+            _check(lib.sccg_filter_pairs_async(ctypes.byref(sets[0]), ctypes.byref(sets[1]), self.pairs.data_ptr(),
+                                               self.cap, self.result.data_ptr(), self.fws.data_ptr(), self.fws_bytes,
+                                               st), "sccg_filter_pairs_async")
+        else:
+            _check(lib.sccg_pixelbox_async(ctypes.byref(sets[0]), ctypes.byref(sets[1]), self.pairs.data_ptr(),
+                                           self.result.data_ptr(), self.cap, self.inter.data_ptr(),
+                                           self.uni.data_ptr(), self.sums.data_ptr(), ctypes.byref(self.cfg),
+                                           self.pws.data_ptr(), self.pws_bytes, st), "sccg_pixelbox_async")
+
+    def _enqueue(self, events=None):
+        sums_copy(self._zero, self.sums)
+        for i in range(self.n_images):
+            for stage in range(3):
+                if events is not None:
+                    events[i][stage].record()
+                self._image(i, stage)
+            if events is not None:
+                events[i][3].record()
+        if self.allreduce is not None:
+            self.allreduce(self.sums)
+        if self.readback:
+            sums_copy(self.sums, self.readback[self._slot])
+
+    def run(self, events=None, slot: int = 0):
+        """One pass over all images (one graph replay).  events: per image four
+        CUDA events (before prep, after prep, after the join, after PixelBox):
+        that pass is launched eagerly with the events between its stages."""
+        self._slot = slot
+        if self._graphs is not None and events is None:
+            self._graphs[slot if self.readback else 0].replay()
+        else:
+            self._enqueue(events)
+        return self.sums
+
+    def check(self):
+        """After a run: raise on any device status bit (a join that overflowed
+        the pair buffer, invalid input, a PixelBox error) in the summed status."""
+        check_status(self.sums.cpu(), "Study")
+        return int(self.sums[0])
+
+
 def touches(P: DeviceSet, Q: DeviceSet, pairs, inter, stream=None):
     """ST_Touches (reading R21) per pair: uint8 [N], 1 iff |p n q| == 0
     (inter: the pairs' intersections from pixelbox) and the boundaries meet.

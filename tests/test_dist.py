@@ -187,3 +187,34 @@ def test_pack_unpack_host_mirror():
     assert vec[10:].tolist() == [0, 1, 1, 0, 1] + [0] * 11
     back = sdist.unpack_sums(vec * 3, torch.zeros(11, dtype=torch.int64))  # three ranks with the same bits
     assert back[:10].tolist() == [3 * i for i in range(10)] and int(back[10]) == 0b10110
+
+
+def test_study_instancing_preserves_every_pair():
+    """configs[3] instancing (bench.study_images / instance_xy): each image is
+    its base under one of the 8 lattice symmetries plus a translation; the
+    oracle's MBR pair list and every pair's (I, U) must be the base's, so the
+    study's expected sums are sums of the bases' (the bench self-check)."""
+    import sys
+
+    import oracle
+    import synth
+
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import bench
+
+    plan = bench.study_images(16, 2)
+    assert sorted({p["sym"] for p in plan}) == list(range(8))
+    assert len({(p["dx"], p["dy"]) for p in plan}) == 16
+    A, B = synth.generate("tile", image=3)
+    A, B = A.subset(range(0, A.n, 3)), B.subset(range(0, B.n, 3))
+    base_pairs = oracle.join(A, B)
+    bi, bu = oracle.pair_areas(A, B, base_pairs)
+    for im in plan[:8]:
+        xa = bench.instance_xy(torch.from_numpy(A.xy), im["sym"], im["dx"], im["dy"]).numpy()
+        xb = bench.instance_xy(torch.from_numpy(B.xy), im["sym"], im["dx"], im["dy"]).numpy()
+        A2, B2 = synth.PolygonSet(xa, A.offsets), synth.PolygonSet(xb, B.offsets)
+        pairs = oracle.join(A2, B2)
+        assert np.array_equal(pairs, base_pairs)
+        i2, u2 = oracle.pair_areas(A2, B2, pairs)
+        assert np.array_equal(i2, bi) and np.array_equal(u2, bu)
+        assert (xa.min() > 0) and (xa.max() < 2**30)

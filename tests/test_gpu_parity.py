@@ -8,6 +8,7 @@ shared-memory overflow path), plus the full-size bench configuration on
 sampled pairs and on size-independent properties.
 """
 import math
+import os
 from fractions import Fraction
 
 import numpy as np
@@ -800,3 +801,49 @@ def test_sums_pack_unpack_and_nccl(sccg, tile_sets):
         assert torch.equal(buf, ref)
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_study_many_images_one_graph(sccg):
+    """configs[3] on one GPU (sccg.Study): images instanced from two tile bases
+    under the 8 lattice symmetries run back to back in ONE graph with shared
+    derived buffers and workspaces; the accumulated sums must equal the sum of
+    the oracle's sums of each image's base (every field, exact ratio units),
+    replays must be identical, and the last image's per-pair (I, U) must be its
+    base's."""
+    import sys
+
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import bench
+
+    bases = []
+    for b in range(2):
+        A, B = synth.generate("tile", image=10 + b)
+        pairs = oracle.join(A, B)
+        ei, eu = oracle.pair_areas(A, B, pairs)
+        bases.append((A, B, pairs, ei, eu, oracle.sums(A, B, pairs, ei, eu)))
+    plan = bench.study_images(9, 2)
+    images = []
+    for im in plan:
+        A, B = bases[im["base"]][:2]
+        xa, oa = sccg.to_device(A.xy, A.offsets)
+        xb, ob = sccg.to_device(B.xy, B.offsets)
+        images.append((bench.instance_xy(xa, im["sym"], im["dx"], im["dy"]), oa,
+                       bench.instance_xy(xb, im["sym"], im["dx"], im["dy"]), ob))
+    study = sccg.Study(images, graph=True)
+    s1 = study.run().clone()
+    s2 = study.run().clone()
+    torch.cuda.synchronize()
+    assert torch.equal(s1, s2)
+    study.check()
+    got = s1.cpu().tolist()
+    keys = ["n_pairs", "n_nonzero", "sum_inter", "sum_union", "sum_area_p", "sum_area_q"]
+    want = [sum(bases[im["base"]][5][k] for im in plan) for k in keys]
+    assert got[:6] == want
+    units = sum(int(v) << (30 * k) for k, v in enumerate(got[6:10]))
+    assert units == sum(exact_ratio_units(bases[im["base"]][3], bases[im["base"]][4]) for im in plan)
+    last = bases[plan[-1]["base"]]
+    n = len(last[2])
+    assert np.array_equal(study.pairs[:n].cpu().numpy(), last[2])
+    assert np.array_equal(study.inter[:n].cpu().numpy(), last[3])
+    assert np.array_equal(study.uni[:n].cpu().numpy(), last[4])
