@@ -308,7 +308,8 @@ class Pipeline:
     ``run()`` returns the device sums vector; read it (one sync) for J'."""
 
     def __init__(self, P: "DeviceSet", Q: "DeviceSet", cap: int | None = None, threshold: int = 0, graph: bool = True,
-                 validate: bool = True, raster: bool = True, readback=(), outputs: bool = True):
+                 validate: bool = True, raster: bool = True, readback=(), outputs: bool = True,
+                 paper_split: bool = False):
         torch = _torch()
         self.lib = load()
         self.P, self.Q = P, Q
@@ -325,7 +326,8 @@ class Pipeline:
         self.fws = torch.empty(self.fws_bytes, dtype=torch.uint8, device=dev)
         self.pws_bytes = int(self.lib.sccg_pixelbox_workspace_bytes(self.cap))
         self.pws = torch.empty(max(self.pws_bytes, 256), dtype=torch.uint8, device=dev)
-        self.cfg = Config(threshold, 0, 0 if raster else FLAG_NO_RASTER, 0, None, None, None)
+        self.cfg = Config(threshold, 0, (0 if raster else FLAG_NO_RASTER) | (FLAG_PAPER_SPLIT if paper_split else 0), 0,
+                          None, None, None)
         self.validate = 1 if validate else 0
         self._sets = (PolySet * 2)(P.c, Q.c)  # copies of the bound descriptors (pointers only)
         # readback: pinned host int64 [11] buffers; run(slot=k) ends the step by

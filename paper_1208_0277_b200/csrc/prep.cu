@@ -672,6 +672,9 @@ cudaError_t launch_prep(const sccg_polyset* const* sets, int count, int validate
     d.status = s->status;
     d.stats = reinterpret_cast<SetStats*>(s->stats);
     d.bulk = ((reinterpret_cast<uintptr_t>(s->xy) | reinterpret_cast<uintptr_t>(s->edges)) & 15) == 0 ? 1 : 0;
+#ifdef SCCG_PREP_NO_TMA  // ablation build (scripts/fig9.py): tiles staged by plain LSU copies
+    d.bulk = 0;
+#endif
     tiles += (s->n_polygons + kPrepPolys - 1) / kPrepPolys;
     a.tile_end[i] = tiles;
   }

@@ -847,3 +847,46 @@ def test_study_many_images_one_graph(sccg):
     assert np.array_equal(study.pairs[:n].cpu().numpy(), last[2])
     assert np.array_equal(study.inter[:n].cpu().numpy(), last[3])
     assert np.array_equal(study.uni[:n].cpu().numpy(), last[4])
+
+
+_ABLATION_CHILD = r"""
+import sys
+import numpy as np
+sys.path.insert(0, {root!r})
+import oracle, synth
+import paper_1208_0277_b200 as sccg
+A, B = synth.generate("tile", image=2)
+for sf in (1, 3):
+    P = sccg.DeviceSet(*sccg.to_device(A.xy * sf, A.offsets))
+    Q = sccg.DeviceSet(*sccg.to_device(B.xy * sf, B.offsets))
+    pairs = sccg.filter_pairs(P, Q)
+    pn = pairs.cpu().numpy()
+    assert np.array_equal(pn, oracle.join(synth.PolygonSet(A.xy * sf, A.offsets), synth.PolygonSet(B.xy * sf, B.offsets)))
+    for raster, split in ((False, True), (True, False)):
+        pipe = sccg.Pipeline(P, Q, raster=raster, paper_split=split)
+        pipe.run()
+        n = pipe.check()
+        ei, eu = oracle.pair_areas(synth.PolygonSet(A.xy * sf, A.offsets), synth.PolygonSet(B.xy * sf, B.offsets), pn)
+        assert np.array_equal(pipe.inter[:n].cpu().numpy(), ei) and np.array_equal(pipe.uni[:n].cpu().numpy(), eu)
+print("ABLATION-OK", sccg.library_path())
+"""
+
+
+@pytest.mark.parametrize("variant,flags", [("noopt", ["-DSCCG_NO_PDL", "-DSCCG_PREP_NO_TMA"]),
+                                           ("nopdl", ["-DSCCG_NO_PDL"])])
+def test_ablation_builds_match_oracle(variant, flags):
+    """The Fig. 9 analog's build variants (scripts/fig9.py: prep without TMA
+    staging, launches without PDL) and runtime variants (no rasters, Alg. 1's
+    split order) give the oracle's pair list and per-pair areas at SF 1 and 3."""
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    lib = os.path.join(root, "paper_1208_0277_b200", f"libsccg_{variant}.so")
+    if not os.path.exists(lib):
+        subprocess.run([sys.executable, os.path.join(root, "paper_1208_0277_b200", "build.py"), "--variant", variant,
+                        *flags], check=True, capture_output=True)
+    env = dict(os.environ, SCCG_LIB=lib)
+    r = subprocess.run([sys.executable, "-c", _ABLATION_CHILD.format(root=root)], env=env, capture_output=True,
+                       text=True, timeout=600)
+    assert r.returncode == 0 and "ABLATION-OK" in r.stdout and lib in r.stdout, r.stdout + r.stderr
