@@ -28,6 +28,9 @@ constexpr int kPrepThreads = SCCG_PREP_THREADS;
 constexpr int kPrepPolys = kPrepThreads;  // one ring per thread per tile
 static_assert(kPrepThreads % 32 == 0 && kPrepThreads <= 256, "whole warps; ring indices fit a byte");
 constexpr int kPrepVerts = SCCG_PREP_VERTS;
+#ifndef SCCG_PREP_USED_ONLY
+#define SCCG_PREP_USED_ONLY 0  // 1: write back only each ring's defined words, one bulk store per ring (measured slower: 177 vs 168 us on C2)
+#endif
 #ifndef SCCG_PREP_L2_PREFETCH
 #define SCCG_PREP_L2_PREFETCH 2  // 0: off, 1: after the ring phase, 2: before it (measured best)
 #endif
@@ -88,7 +91,8 @@ __device__ __forceinline__ void flag(uint32_t* status, uint32_t bit, int64_t pol
 __device__ __forceinline__ int4 prep_polygon(const int2* v, int64_t V, int64_t poly, uint64_t* out,
                                              int4* __restrict__ mbr, int64_t* __restrict__ area,
                                              int2* __restrict__ ecount, uint32_t* __restrict__ status,
-                                             int validate) {
+                                             int validate, int& nv_out) {
+  nv_out = 0;
   const int lane = threadIdx.x & 31;
   int xmin = INT_MAX, ymin = INT_MAX, xmax = INT_MIN, ymax = INT_MIN;
   for (int64_t i = lane; i < V; i += 32) {
@@ -141,6 +145,7 @@ __device__ __forceinline__ int4 prep_polygon(const int2* v, int64_t V, int64_t p
   }
   for (int o = 16; o; o >>= 1) twice_area += __shfl_xor_sync(0xffffffffu, twice_area, o);
   diag = __any_sync(0xffffffffu, diag);
+  nv_out = nvert;  // warp-uniform
   if (lane == 0) {
     area[poly] = (twice_area < 0 ? -twice_area : twice_area) / 2;
     mbr[poly] = m;
@@ -158,7 +163,8 @@ __device__ __forceinline__ int4 prep_polygon(const int2* v, int64_t V, int64_t p
 // k <= i - 1 while vertex i is being read.
 __device__ __forceinline__ int4 prep_polygon_thread(int2* v, int V, int rot, int64_t poly, int4* __restrict__ mbr,
                                                     int64_t* __restrict__ area, int2* __restrict__ ecount,
-                                                    uint32_t* __restrict__ status, int validate) {
+                                                    uint32_t* __restrict__ status, int validate, int& used8) {
+  used8 = 0;
   // MBR: order-free, so each thread starts at vertex `rot` (chosen by the
   // caller so the lockstep reads of a half-warp hit distinct bank pairs) and
   // wraps around
@@ -305,7 +311,22 @@ __device__ __forceinline__ int4 prep_polygon_thread(int2* v, int V, int rot, int
   }
   ecount[poly] = make_int2(nvert, nhor | (raster ? kRasterFlag : 0));
   if (validate && diag) flag(status, SCCG_STATUS_NOT_RECTILINEAR, poly);
+  used8 = nvert + (raster ? (H + 1) / 2 : 0);  // the slot's defined 8-byte words: records, then raster rows
   return m;
+}
+
+// Write back the defined part of one ring's slot -- its records (and raster
+// rows) -- from the tile: the 16-byte-aligned body by one TMA bulk store, an
+// odd first / last 8-byte word by plain stores.  The rest of the slot is left
+// unwritten (nothing reads it), so the write traffic is what prep defines,
+// not the whole vertex range.
+__device__ __forceinline__ void store_used(uint64_t* __restrict__ edges, int64_t b, const uint64_t* src, int u) {
+  if (u <= 0) return;
+  const int64_t a0 = (b + 1) & ~int64_t(1), a1 = (b + u) & ~int64_t(1);
+  fence_async_smem();  // this thread's shared-memory writes -> async proxy
+  if (a1 > a0) bulk_store(edges + a0, src + (a0 - b), (unsigned)(a1 - a0) * 8u);
+  if (b < a0) edges[b] = src[0];
+  if (a1 < b + u && a1 >= a0) edges[a1] = src[a1 - b];
 }
 
 struct StatAcc {
@@ -474,7 +495,11 @@ __global__ void __launch_bounds__(kPrepThreads, 5) prep_kernel(const __grid_cons
     const int bulk = S.bulk;
     // the previous tile's bulk write-back must have read the buffer before anything (TMA load or, for a set
     // without 16-byte alignment, plain stores) overwrites it -- whatever the current set's mode
+#if SCCG_PREP_USED_ONLY
+    bulk_store_drain();  // this thread's write-backs of the previous tile have read the buffer
+#else
     if (threadIdx.x == 0) bulk_store_drain();
+#endif
     __syncthreads();  // previous tile's shared data fully consumed
     if ((int)threadIdx.x <= np) s_off[threadIdx.x] = off_a;
     if (threadIdx.x == 0) s_off[np] = off_b;
@@ -566,7 +591,13 @@ __global__ void __launch_bounds__(kPrepThreads, 5) prep_kernel(const __grid_cons
         atomicOr(&s_big[j >> 5], 1u << (j & 31));
       } else {
         const int rot = (int)((lane - (b - v0)) & 15) % (int)V;
-        acc.add(prep_polygon_thread(s_xy + (b - v0), (int)V, rot, poly, mbr, area, ecount, status, validate));
+        int used8;
+        acc.add(prep_polygon_thread(s_xy + (b - v0), (int)V, rot, poly, mbr, area, ecount, status, validate, used8));
+#if SCCG_PREP_USED_ONLY
+        if (bulk) store_used(edges, b, reinterpret_cast<const uint64_t*>(s_xy + (b - v0)), used8);
+        else
+          for (int i = 0; i < used8; i++) edges[b + i] = reinterpret_cast<const uint64_t*>(s_xy + (b - v0))[i];
+#endif
       }
     }
     if (threadIdx.x == 0) {
@@ -605,15 +636,28 @@ __global__ void __launch_bounds__(kPrepThreads, 5) prep_kernel(const __grid_cons
         const int64_t b = s_off[j], e = s_off[j + 1];
         int2* src = tiled ? s_xy + (b - v0) : const_cast<int2*>(xy) + b;
         uint64_t* out = tiled ? reinterpret_cast<uint64_t*>(src) : edges + b;
-        const int4 m = prep_polygon(src, e - b, poly, out, mbr, area, ecount, status, validate);
+        int nv;
+        const int4 m = prep_polygon(src, e - b, poly, out, mbr, area, ecount, status, validate, nv);
         if (lane == 0) acc.add(m);
+#if SCCG_PREP_USED_ONLY
+        if (tiled) {  // records are in the tile: write them back
+          __syncwarp();
+          if (bulk) {
+            fence_async_smem();
+            __syncwarp();
+            if (lane == 0) store_used(edges, b, out, nv);
+          } else {
+            for (int i = lane; i < nv; i += 32) edges[b + i] = out[i];
+          }
+        }
+#endif
       }
     }
     __syncthreads();
     // write-back of the tile's slots [off[p0], v1) -- exactly this tile's rings
     // (v0 may be the previous tile's last slot): one TMA bulk store of the
     // 16-byte-aligned body, the odd ends by a thread
-    if (tiled) {
+    if (tiled && !SCCG_PREP_USED_ONLY) {
       const int64_t s0 = s_off[0];
       const int64_t a0 = (s0 + 1) & ~int64_t(1), a1 = v1 & ~int64_t(1);
       const uint64_t* rec = reinterpret_cast<const uint64_t*>(s_xy);
@@ -632,7 +676,7 @@ __global__ void __launch_bounds__(kPrepThreads, 5) prep_kernel(const __grid_cons
     gt = gt_next;
   }
   pdl_done();  // no tile left: the join's first kernel may launch
-  if (threadIdx.x == 0) bulk_store_drain();
+  if (SCCG_PREP_USED_ONLY || threadIdx.x == 0) bulk_store_drain();  // shared memory must outlive the write-backs
   if (cur >= 0) flush_stats(acc, args.set[cur].stats, s_acc, s_b);
 }
 
