@@ -27,7 +27,13 @@ KEYS = [
 def ncu_summary(rep):
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(raw.splitlines()))
-    h, units, vals = rows[0], rows[1], rows[2]
+    lines = []
+    for vals in rows[2:]:
+        lines += ncu_one(rows[0], rows[1], vals)
+    return "\n".join(lines) + "\n"
+
+
+def ncu_one(h, units, vals):
     d = {h[i]: (vals[i], units[i]) for i in range(len(h))}
     lines = [f"kernel: {d.get('Kernel Name', ('?', ''))[0]}"]
     for k in KEYS:
@@ -41,7 +47,7 @@ def ncu_summary(rep):
             except ValueError:
                 pass
     lines.append("stalls (warps per issue): " + ", ".join(f"{n}={v:.2f}" for v, n in sorted(st, reverse=True)[:8]))
-    return "\n".join(lines) + "\n"
+    return lines
 
 
 def launch_summary(path):
@@ -68,8 +74,50 @@ def launch_summary(path):
     return "\n".join(out) + "\n"
 
 
+def ncu_rows(rep):
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(raw.splitlines()))
+    return [dict(zip(rows[0], r)) for r in rows[2:]]
+
+
+def num(v):
+    return float(str(v).replace(",", ""))
+
+
+def static_profiles(src, dst):
+    """profiles/prep_traffic.json (DRAM bytes of one prep launch) and
+    profiles/issue_counts.json (the small kernel's warp instructions per launch),
+    keyed by the library digest the bench checks before using them."""
+    dig = open(os.path.join(src, "lib_digest.txt")).read().strip()
+    root = os.path.dirname(os.path.abspath(dst.rstrip("/")))
+    prep = os.path.join(src, "ncu_prep_kernel.ncu-rep")
+    if os.path.exists(prep):
+        d = ncu_rows(prep)[0]
+        mb = {"MB": 1e6, "Mbyte": 1e6, "GB": 1e9, "Gbyte": 1e9, "KB": 1e3, "Kbyte": 1e3, "byte": 1}
+        raw = subprocess.run(["ncu", "-i", prep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+        rows = list(csv.reader(raw.splitlines()))
+        units = dict(zip(rows[0], rows[1]))
+        rd = num(d["dram__bytes_read.sum"]) * mb.get(units["dram__bytes_read.sum"], 1)
+        wr = num(d["dram__bytes_write.sum"]) * mb.get(units["dram__bytes_write.sum"], 1)
+        with open(os.path.join(root, "prep_traffic.json"), "w") as f:
+            json.dump({"config": "slide", "kernel": "prep_kernel (P and Q in one launch)", "lib": dig,
+                       "source": f"ncu --set full --clock-control none, {dst}/ncu_prep_kernel.txt (one launch)",
+                       "dram_bytes_read": int(rd), "dram_bytes_write": int(wr), "dram_bytes_per_launch": int(rd + wr)},
+                      f, indent=1)
+    small = os.path.join(src, "ncu_small_kernel.ncu-rep")
+    if os.path.exists(small):
+        d = ncu_rows(small)[0]
+        with open(os.path.join(root, "issue_counts.json"), "w") as f:
+            json.dump({"source": "ncu --set full --clock-control none, smsp__inst_executed.sum of one launch "
+                                 "(bench.py --config slide); fixed by the workload and the library build",
+                       "slide/image/1": {"small_kernel": int(num(d["smsp__inst_executed.sum"])), "lib": dig}},
+                      f, indent=1)
+
+
 def main(src, dst):
     os.makedirs(dst, exist_ok=True)
+    if os.path.exists(os.path.join(src, "lib_digest.txt")):
+        static_profiles(src, dst)
     for name in sorted(os.listdir(src)):
         p = os.path.join(src, name)
         if name.startswith("bench_") and name.endswith(".json"):
@@ -85,6 +133,8 @@ def main(src, dst):
         elif name.endswith(".ncu-rep"):
             with open(os.path.join(dst, name.replace(".ncu-rep", ".txt")), "w") as f:
                 f.write(ncu_summary(p))
+        elif name.startswith("sanitize_summary"):
+            shutil.copy(p, os.path.join(dst, "sanitize.txt"))
 
 
 if __name__ == "__main__":

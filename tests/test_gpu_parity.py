@@ -890,3 +890,23 @@ def test_ablation_builds_match_oracle(variant, flags):
     r = subprocess.run([sys.executable, "-c", _ABLATION_CHILD.format(root=root)], env=env, capture_output=True,
                        text=True, timeout=600)
     assert r.returncode == 0 and "ABLATION-OK" in r.stdout and lib in r.stdout, r.stdout + r.stderr
+
+
+def test_filter_recycled_workspaces(sccg):
+    """Joins of different sizes back to back, each with a freshly allocated
+    (so recycled, stale) workspace, PixelBox in between: every pair list equals
+    the oracle's.  (With kernels triggering their successors at entry, a probe
+    CTA once read the previous join's grid descriptor from such a workspace
+    and the next join found no pairs.)"""
+    A, B = synth.generate("skewed", width=8192, height=8192)
+    C, D = synth.generate("tile")
+    ref_ab, ref_cd = oracle.join(A, B), oracle.join(C, D)
+    for it in range(4):
+        P2, Q2 = dev(C, sccg), dev(D, sccg)
+        assert np.array_equal(sccg.filter_pairs(P2, Q2).cpu().numpy(), ref_cd)
+        P, Q = dev(A, sccg), dev(B, sccg)  # no synchronisation: prep is still running when the join starts
+        pairs = sccg.filter_pairs(P, Q)
+        assert np.array_equal(pairs.cpu().numpy(), ref_ab), it
+        counters = torch.zeros(8, dtype=torch.int64, device="cuda")
+        sccg.pixelbox(P, Q, pairs, threshold=64, counters=counters)
+        assert counters[sccg.CNT_SPLITS].item() > 0
