@@ -445,7 +445,7 @@ class Study:
     images: list of (xy_p, off_p, xy_q, off_q) CUDA tensors (int32 [V, 2], int64 [n + 1])."""
 
     def __init__(self, images, cap: int | None = None, threshold: int = 0, graph: bool = True, validate: bool = True,
-                 raster: bool = True, readback=(), allreduce=None):
+                 raster: bool = True, readback=(), allreduce=None, overlap: bool = True):
         torch = _torch()
         self.lib = lib = load()
         if not images:
@@ -459,17 +459,27 @@ class Study:
         dims = [(int(op.numel()) - 1, int(xp.numel()) // 2, int(oq.numel()) - 1, int(xq.numel()) // 2)
                 for xp, op, xq, oq in self.images]
         self.n_images = len(dims)
-        # shared derived buffers, one per side, bound per image (the layout is carved from each image's sizes)
+        # shared derived buffers bound per image (the layout is carved from each image's sizes); with overlap,
+        # two sets used alternately: image i + 1's prep (HBM-bound) runs on a side stream while image i's join
+        # and PixelBox (latency-bound) run on the main one
+        self.overlap = bool(overlap) and len(dims) > 1
+        nbuf = 2 if self.overlap else 1
         bp = max(int(lib.sccg_polyset_bytes(a, b)) for a, b, _, _ in dims)
         bq = max(int(lib.sccg_polyset_bytes(c, d)) for _, _, c, d in dims)
-        self._bufs = (torch.empty(bp, dtype=torch.uint8, device=dev), torch.empty(bq, dtype=torch.uint8, device=dev))
+        self._bufs = [(torch.empty(bp, dtype=torch.uint8, device=dev), torch.empty(bq, dtype=torch.uint8, device=dev))
+                      for _ in range(nbuf)]
         self._sets = []
-        for (xp, op, xq, oq), (n_p, nv_p, n_q, nv_q) in zip(self.images, dims):
+        for i, ((xp, op, xq, oq), (n_p, nv_p, n_q, nv_q)) in enumerate(zip(self.images, dims)):
             cp = PolySet(xp.data_ptr(), op.data_ptr(), n_p, nv_p, None, None, None, None, None, None)
             cq = PolySet(xq.data_ptr(), oq.data_ptr(), n_q, nv_q, None, None, None, None, None, None)
-            _check(lib.sccg_polyset_bind(ctypes.byref(cp), self._bufs[0].data_ptr(), bp), "sccg_polyset_bind")
-            _check(lib.sccg_polyset_bind(ctypes.byref(cq), self._bufs[1].data_ptr(), bq), "sccg_polyset_bind")
+            b = self._bufs[i % nbuf]
+            _check(lib.sccg_polyset_bind(ctypes.byref(cp), b[0].data_ptr(), bp), "sccg_polyset_bind")
+            _check(lib.sccg_polyset_bind(ctypes.byref(cq), b[1].data_ptr(), bq), "sccg_polyset_bind")
             self._sets.append((PolySet * 2)(cp, cq))
+        if self.overlap:
+            self._side = torch.cuda.Stream(device=dev)
+            self._ev_prep = [torch.cuda.Event() for _ in dims]
+            self._ev_done = [torch.cuda.Event() for _ in dims]
         self.cap = int(cap) if cap is not None else max(3 * max(a, c) + 1024 for a, _, c, _ in dims)
         self.pairs = torch.empty((self.cap, 2), dtype=torch.int32, device=dev)
         self.result = torch.zeros(2, dtype=torch.int64, device=dev)
@@ -518,14 +528,31 @@ class Study:
                                            self.pws.data_ptr(), self.pws_bytes, st), "sccg_pixelbox_async")
 
     def _enqueue(self, events=None):
+        torch = _torch()
         sums_copy(self._zero, self.sums)
-        for i in range(self.n_images):
-            for stage in range(3):
+        if self.overlap and events is None:
+            main = torch.cuda.current_stream()
+            side = self._side
+            side.wait_stream(main)  # fork
+            for i in range(self.n_images):
+                if i >= 2:
+                    side.wait_event(self._ev_done[i - 2])  # image i - 2's join and PixelBox are done with this buffer set
+                with torch.cuda.stream(side):
+                    self._image(i, 0)
+                    self._ev_prep[i].record(side)
+                main.wait_event(self._ev_prep[i])
+                self._image(i, 1)
+                self._image(i, 2)
+                self._ev_done[i].record(main)
+            main.wait_stream(side)  # join
+        else:
+            for i in range(self.n_images):
+                for stage in range(3):
+                    if events is not None:
+                        events[i][stage].record()
+                    self._image(i, stage)
                 if events is not None:
-                    events[i][stage].record()
-                self._image(i, stage)
-            if events is not None:
-                events[i][3].record()
+                    events[i][3].record()
         if self.allreduce is not None:
             self.allreduce(self.sums)
         if self.readback:
@@ -534,7 +561,8 @@ class Study:
     def run(self, events=None, slot: int = 0):
         """One pass over all images (one graph replay).  events: per image four
         CUDA events (before prep, after prep, after the join, after PixelBox):
-        that pass is launched eagerly with the events between its stages."""
+        that pass is launched eagerly, without the prep overlap, with the
+        events between its stages."""
         self._slot = slot
         if self._graphs is not None and events is None:
             self._graphs[slot if self.readback else 0].replay()

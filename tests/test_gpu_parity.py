@@ -830,11 +830,12 @@ def test_study_many_images_one_graph(sccg):
         xb, ob = sccg.to_device(B.xy, B.offsets)
         images.append((bench.instance_xy(xa, im["sym"], im["dx"], im["dy"]), oa,
                        bench.instance_xy(xb, im["sym"], im["dx"], im["dy"]), ob))
-    study = sccg.Study(images, graph=True)
+    study = sccg.Study(images, graph=True)  # image i + 1's prep overlapped with image i's join and PixelBox
     s1 = study.run().clone()
     s2 = study.run().clone()
+    s3 = sccg.Study(images, graph=True, overlap=False).run().clone()
     torch.cuda.synchronize()
-    assert torch.equal(s1, s2)
+    assert torch.equal(s1, s2) and torch.equal(s1, s3)
     study.check()
     got = s1.cpu().tolist()
     keys = ["n_pairs", "n_nonzero", "sum_inter", "sum_union", "sum_area_p", "sum_area_q"]
