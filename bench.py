@@ -63,6 +63,7 @@ def parse():
                          "into y bands of P with their Q halo (strong scaling, SURVEY 8(e))")
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true", help="skip the skewed / combs lines added to the slide run")
     ap.add_argument("--json-out", default=None)
     return ap.parse_args()
 
@@ -530,6 +531,53 @@ def run_ours(args, rank, world, local_rank):
     return out, (A, B, ref_pass)
 
 
+# ------------------------------------------------- extra configs (N = 1)
+def extra_configs(args, dev, names=("skewed", "combs"), steps: int = 20):
+    """Short device-resident runs of the sampling-box configs beside the
+    headline line (configs[2] glands and the configs[4] comb analog: the
+    large-pair path the slide hardly enters), each self-checked against the
+    oracle like the main step, timed as whole-step graph replays (CUDA events,
+    inputs resident) plus one stage-event pass."""
+    import torch
+
+    import paper_1208_0277_b200 as sccg
+
+    out = {}
+    threads = os.cpu_count() or 1
+    for name in names:
+        A, B = make_workload(name, 0)
+        P = sccg.DeviceSet(*sccg.to_device(A.xy, A.offsets, dev), prep=False)
+        Q = sccg.DeviceSet(*sccg.to_device(B.xy, B.offsets, dev), prep=False)
+        pipe = sccg.Pipeline(P, Q, cap=3 * max(P.n, Q.n) + 1024, threshold=args.threshold, graph=True)
+        pipe.run()
+        torch.cuda.synchronize()
+        n = pipe.check()
+        local = [int(v) for v in pipe.sums.tolist()]
+        sub = argparse.Namespace(**{**vars(args), "config": name})
+        chk, _ = self_check(sub, A, B, pipe, n, local, threads)
+        for _ in range(3):
+            pipe.run()
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        pipe.run(ev)
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        t0.record()
+        for _ in range(steps):
+            pipe.run()
+        t1.record()
+        torch.cuda.synchronize()
+        if [int(v) for v in pipe.sums.tolist()] != local:
+            raise RuntimeError(f"{name}: timed sums differ from the checked step's")
+        ms = t0.elapsed_time(t1) / steps
+        out[name] = {"description": config_desc(name), "pairs": n, "ms_per_step": ms, "value": n / (ms / 1e3),
+                     "unit": "pairs/s", "steps": steps,
+                     "stage_ms": {"prep": ev[0].elapsed_time(ev[1]), "join": ev[1].elapsed_time(ev[2]),
+                                  "pixelbox": ev[2].elapsed_time(ev[3])},
+                     "self_check": chk}
+        del pipe, P, Q
+    return out
+
+
 # ----------------------------------------------------------- configs[3]
 def study_images(n_images: int, n_bases: int):
     """The study's image list: image i is base slide i % n_bases under grid
@@ -908,6 +956,10 @@ def main():
         if not args.no_cpu_baseline and world == 1 and args.config not in ("combs", "study"):  # rank 0, N = 1
             A, B, ref_pass = extra
             out["cpu_baseline"] = cpu_baseline(args.config, A, B, ref_pass)
+        if not args.no_extras and world == 1 and args.config == "slide":
+            import torch
+
+            out["other_configs"] = extra_configs(args, torch.device("cuda", 0))
         line = json.dumps(out)
         print(line)
         if args.json_out:

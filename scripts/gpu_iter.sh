@@ -14,10 +14,10 @@ if [ -n "${SANITIZE:-}" ]; then
 fi
 for v in "" "$@"; do
   name=${v:-main}
-  SCCG_LIB=$v timeout 600 python bench.py --steps 30 --warmup 5 --no-cpu-baseline --json-out gpurun_out/bench_${TAG}_${name}.json > gpurun_out/bench_${TAG}_${name}.txt 2>&1
+  SCCG_LIB=$v timeout 600 python bench.py --steps 30 --warmup 5 --no-cpu-baseline --no-extras --json-out gpurun_out/bench_${TAG}_${name}.json > gpurun_out/bench_${TAG}_${name}.txt 2>&1
   echo "bench $name rc=$?"; python -c "
 import json; d=json.load(open('gpurun_out/bench_${TAG}_${name}.json')); print('$name', 'value %.3e'%d['value'], 'ms/step %.3f'%d['ms_per_step'], 'stages', d['stage_ms'], 'frac %.3f'%d['roofline']['frac'], 'e2e %.3e'%d['e2e']['value'], d['clocks'])" 2>&1 | tail -1
 done
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_${TAG}.csv \
-  python bench.py --steps 2 --warmup 3 --no-cpu-baseline --e2e-steps 1 > /dev/null 2>&1
+  python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-extras --e2e-steps 1 > /dev/null 2>&1
 echo "ncu rc=$?"

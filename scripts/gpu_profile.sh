@@ -14,19 +14,19 @@ python -c "import bench; print(bench.lib_digest())" > $OUT/lib_digest.txt
 timeout 900 python bench.py > $OUT/bench_slide.json 2> $OUT/bench_slide.err
 echo "bench rc=$?"
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches_slide.csv \
-  python bench.py --steps 2 --warmup 3 --no-cpu-baseline --e2e-steps 1 > $OUT/launches_bench.txt 2>&1
+  python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-extras --e2e-steps 1 > $OUT/launches_bench.txt 2>&1
 echo "launch list rc=$?"
 for k in prep_kernel grid_insert_kernel small_kernel; do
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:$k -s 1 -c 1 \
-    -o $OUT/ncu_$k -f python bench.py --steps 1 --warmup 3 --no-cpu-baseline --e2e-steps 1 > $OUT/ncu_$k.txt 2>&1
+    -o $OUT/ncu_$k -f python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-extras --e2e-steps 1 > $OUT/ncu_$k.txt 2>&1
   echo "ncu $k rc=$?"
 done
 # both probe passes (bucket pass, compaction)
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:probe_kernel -s 2 -c 2 \
-  -o $OUT/ncu_probe_kernel -f python bench.py --steps 1 --warmup 3 --no-cpu-baseline --e2e-steps 1 > $OUT/ncu_probe.txt 2>&1
+  -o $OUT/ncu_probe_kernel -f python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-extras --e2e-steps 1 > $OUT/ncu_probe.txt 2>&1
 echo "ncu probe rc=$?"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:item_kernel -s 1 -c 1 \
-  -o $OUT/ncu_item_kernel_combs -f python bench.py --config combs --steps 1 --warmup 3 --no-cpu-baseline --e2e-steps 1 > $OUT/ncu_item.txt 2>&1
+  -o $OUT/ncu_item_kernel_combs -f python bench.py --config combs --steps 1 --warmup 3 --no-cpu-baseline --no-extras --e2e-steps 1 > $OUT/ncu_item.txt 2>&1
 echo "ncu item rc=$?"
 for tool in memcheck racecheck synccheck; do
   timeout 1200 compute-sanitizer --tool $tool --error-exitcode 9 python scripts/sanitize_case.py > $OUT/sanitize_$tool.txt 2>&1
