@@ -191,6 +191,18 @@ typedef struct {
 
 SCCG_API size_t sccg_pixelbox_workspace_bytes(int64_t n_pairs);
 
+/* Optional extra workspace for the large path's per-pair edge index: any bytes
+ * passed to sccg_pixelbox / sccg_pixelbox_async beyond
+ * sccg_pixelbox_workspace_bytes(n) are used as an index pool.  A pair cut into
+ * >= 4 region work items then has its rings' edges bucketed by region column
+ * and row once (by the warp taking its first item), so its other items cull
+ * only their buckets instead of both whole rings (Alg. 1 P:207-257 runs per
+ * region; the areas are identical with or without the pool).  This returns a
+ * pool size that indexes every large pair when each polygon is in about one
+ * large pair: 8 bytes per vertex of both sets plus 16 MiB; pairs that do not
+ * fit are processed unindexed.  n_vertices_* >= 0. */
+SCCG_API size_t sccg_pixelbox_index_bytes(int64_t n_vertices_p, int64_t n_vertices_q);
+
 /* PixelBox: for each pairs[k] = {p, q} (indices into the prepared
  * sets) write inter[k] = |p n q| and uni[k] = |p| + |q| - |p n q| (int64, input
  * order; either may be NULL to skip it) and add the batch's totals into *sums

@@ -38,7 +38,7 @@ CNT_PIXELS, CNT_ROWTESTS, CNT_BOXES, CNT_BOXEDGES, CNT_SPLITS, CNT_PIXBOXES, CNT
 SUMS_FIELDS = ("n_pairs", "n_nonzero", "sum_inter", "sum_union", "sum_area_p", "sum_area_q", "limb0", "limb1",
                "limb2", "limb3", "status")
 SYMBOLS = ("sccg_polyset_bytes", "sccg_polyset_bind", "sccg_prep", "sccg_prep_sets", "sccg_filter_workspace_bytes",
-           "sccg_filter_pairs", "sccg_filter_pairs_closed", "sccg_filter_pairs_async", "sccg_touches", "sccg_pixelbox_workspace_bytes", "sccg_pixelbox",
+           "sccg_filter_pairs", "sccg_filter_pairs_closed", "sccg_filter_pairs_async", "sccg_touches", "sccg_pixelbox_workspace_bytes", "sccg_pixelbox_index_bytes", "sccg_pixelbox",
            "sccg_pixelbox_async", "sccg_count_missing", "sccg_contains", "sccg_report", "sccg_jaccard", "sccg_sums_copy",
            "sccg_sums_pack", "sccg_sums_unpack", "sccg_strerror", "sccg_last_error_string", "sccg_last_error_index",
            "sccg_version")
@@ -143,6 +143,8 @@ def load(build: bool = True):
         lib.sccg_pixelbox_async.restype = cint
         lib.sccg_pixelbox_workspace_bytes.argtypes = [i64]
         lib.sccg_pixelbox_workspace_bytes.restype = sz
+        lib.sccg_pixelbox_index_bytes.argtypes = [i64, i64]
+        lib.sccg_pixelbox_index_bytes.restype = sz
         lib.sccg_pixelbox.argtypes = [ps, ps, vp, i64, vp, vp, vp, ctypes.POINTER(Config), vp, sz, vp]
         lib.sccg_pixelbox.restype = cint
         lib.sccg_count_missing.argtypes = [vp, i64, vp, vp]
@@ -309,7 +311,7 @@ class Pipeline:
 
     def __init__(self, P: "DeviceSet", Q: "DeviceSet", cap: int | None = None, threshold: int = 0, graph: bool = True,
                  validate: bool = True, raster: bool = True, readback=(), outputs: bool = True,
-                 paper_split: bool = False):
+                 paper_split: bool = False, index: bool = True):
         torch = _torch()
         self.lib = load()
         self.P, self.Q = P, Q
@@ -324,7 +326,9 @@ class Pipeline:
         self.uni = torch.empty(max(self.cap, 1), dtype=torch.int64, device=dev) if outputs else None
         self.fws_bytes = int(self.lib.sccg_filter_workspace_bytes(P.n, Q.n))
         self.fws = torch.empty(self.fws_bytes, dtype=torch.uint8, device=dev)
-        self.pws_bytes = int(self.lib.sccg_pixelbox_workspace_bytes(self.cap))
+        # required PixelBox workspace plus the large path's edge-index pool (sccg_pixelbox_index_bytes)
+        self.pws_bytes = int(self.lib.sccg_pixelbox_workspace_bytes(self.cap)) + (
+            int(self.lib.sccg_pixelbox_index_bytes(P.nv, Q.nv)) if index else 0)
         self.pws = torch.empty(max(self.pws_bytes, 256), dtype=torch.uint8, device=dev)
         self.cfg = Config(threshold, 0, (0 if raster else FLAG_NO_RASTER) | (FLAG_PAPER_SPLIT if paper_split else 0), 0,
                           None, None, None)
@@ -487,7 +491,8 @@ class Study:
         self.uni = torch.empty(self.cap, dtype=torch.int64, device=dev)
         self.fws_bytes = max(int(lib.sccg_filter_workspace_bytes(a, c)) for a, _, c, _ in dims)
         self.fws = torch.empty(self.fws_bytes, dtype=torch.uint8, device=dev)
-        self.pws_bytes = int(lib.sccg_pixelbox_workspace_bytes(self.cap))
+        self.pws_bytes = int(lib.sccg_pixelbox_workspace_bytes(self.cap)) + max(
+            int(lib.sccg_pixelbox_index_bytes(b, d)) for _, b, _, d in dims)
         self.pws = torch.empty(max(self.pws_bytes, 256), dtype=torch.uint8, device=dev)
         self.sums = new_sums(dev)
         self._zero = new_sums(dev)
@@ -599,7 +604,7 @@ def new_sums(device=None):
 
 def pixelbox(P: DeviceSet, Q: DeviceSet, pairs, threshold: int = 0, mode: int = 0, sums=None, want_inter=True,
              want_union=True, counters=None, grid: int = 0, hits=None, raster: bool = True, paper_split: bool = False,
-             stream=None, check: bool = True):
+             stream=None, check: bool = True, index: bool = True):
     """Per-pair |p n q| and |p u q| (int64, input order) + accumulated sums.
     check: read the sums' status word after the call (one sync) and raise
     SccgError if a device-side error was flagged (check=False: stay async).
@@ -620,7 +625,7 @@ def pixelbox(P: DeviceSet, Q: DeviceSet, pairs, threshold: int = 0, mode: int = 
     cfg = Config(threshold, mode, (0 if raster else FLAG_NO_RASTER) | (FLAG_PAPER_SPLIT if paper_split else 0), grid,
                  counters.data_ptr() if counters is not None else None,
                  hits[0].data_ptr() if hits is not None else None, hits[1].data_ptr() if hits is not None else None)
-    wsb = int(lib.sccg_pixelbox_workspace_bytes(n))
+    wsb = int(lib.sccg_pixelbox_workspace_bytes(n)) + (int(lib.sccg_pixelbox_index_bytes(P.nv, Q.nv)) if index else 0)
     ws = torch.empty(max(wsb, 256), dtype=torch.uint8, device=dev)
     code = lib.sccg_pixelbox(ctypes.byref(P.c), ctypes.byref(Q.c), pairs.data_ptr(), n,
                              inter.data_ptr() if inter is not None else None,

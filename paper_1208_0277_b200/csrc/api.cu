@@ -279,6 +279,11 @@ int sccg_filter_pairs_async(const sccg_polyset* p, const sccg_polyset* q, int32_
 
 size_t sccg_pixelbox_workspace_bytes(int64_t n_pairs) { return n_pairs < 0 ? 0 : pixelbox_ws_bytes(n_pairs); }
 
+size_t sccg_pixelbox_index_bytes(int64_t n_vertices_p, int64_t n_vertices_q) {
+  if (n_vertices_p < 0 || n_vertices_q < 0) return 0;
+  return (size_t)8 * (size_t)(n_vertices_p + n_vertices_q) + ((size_t)1 << 24);
+}
+
 static int pixelbox_checks(const sccg_polyset* p, const sccg_polyset* q, const int32_t* pairs, int64_t n_pairs,
                            int64_t* inter, int64_t* uni, sccg_sums* sums, const sccg_config* cfg) {
   if (int r = check_set(p, true, "p")) return r;

@@ -165,6 +165,213 @@ __device__ bool build_local(const PolyRef& c, int X0, int Y0, int X1, int Y1, Lo
   return L.nV <= kLCap && L.nH <= kLCap;
 }
 
+// ------------------------------------------------------ per-pair edge index
+// build_local streams both whole rings for every region item; a pair cut into
+// many regions (a comb, C5; a gland, C3) re-culls its rings once per region,
+// which is most of the item kernel's instructions on combs.  So the warp that
+// takes a pair's FIRST item (items[0 .. nl) come before every extra item in
+// the queue) buckets each ring's vertical edges by region column and its
+// horizontal edges by region row -- an edge goes to the column (row) whose
+// open interior it lies strictly inside, else to none: then it cannot meet
+// any region's open interior -- and computes every region corner's ray parity
+// (an XOR difference grid over rows of column masks), into the optional pool.
+// The pair's other items cull only their column's and row's buckets.  A
+// region's culled lists are the same sets build_local makes (in another
+// order; every use of them is order-free), so the areas are unchanged.
+#ifndef SCCG_IX_MIN
+#define SCCG_IX_MIN 4  // regions per pair worth an index (a build costs two ring passes)
+#endif
+constexpr int kIxMin = SCCG_IX_MIN;
+constexpr int kIxReady = 2, kIxNone = 3;
+
+__device__ __forceinline__ uint64_t pack_ix(int a, int lo, int hi) {
+  return (uint64_t)(a & 0x1fffff) | ((uint64_t)(lo & 0x1fffff) << 21) | ((uint64_t)(hi & 0x1fffff) << 42);
+}
+__device__ __forceinline__ int sx21(uint64_t v) { return ((int)(unsigned)(v & 0x1fffffu) << 11) >> 11; }
+__device__ __forceinline__ void unpack_ix(uint64_t r, int& a, int& lo, int& hi) {
+  a = sx21(r);
+  lo = sx21(r >> 21);
+  hi = sx21(r >> 42);
+}
+// number of the boundaries b[t] = floor(t * L / n), t = 0..n, below the
+// integer v: floor(t L / n) < v  <=>  t L / n < v  <=>  t < v n / L, so the
+// count is min(n + 1, ceil(v n / L)) for v > 0 (v n < 2^22: 32-bit exact)
+__device__ __forceinline__ int count_below(int v, int n, int L) {
+  return v <= 0 ? 0 : min(n + 1, (int)(((unsigned)v * (unsigned)n + (unsigned)L - 1u) / (unsigned)L));
+}
+__device__ __forceinline__ int ld_acquire_i(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_i(int* p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+// header words (u32) of one polygon's index: vertical bucket starts [nx + 1],
+// horizontal bucket starts [ny + 1] (relative to the horizontal block),
+// corner parity masks [ny]; padded to whole 8-byte words
+__device__ __forceinline__ int ix_header_words(int nx, int ny) { return (nx + 1 + ny + 1 + ny + 1) / 2; }
+
+// Build pair i's index (one warp).  sc: >= 264 ints of the warp's shared
+// scratch.  Returns the pool offset of polygon 0's index, or -1 (no room).
+__device__ long long build_index(const PolyRef* pr, int W, int H, int nx, int ny, const LargeWs& w, int* sc) {
+  const int lane = threadIdx.x & 31;
+  int* X = sc;
+  int* Y = sc + 33;
+  for (int t = lane; t < 33; t += 32) {
+    X[t] = t <= nx ? (int)((long long)t * W / nx) : INT_MAX;
+    Y[t] = t <= ny ? (int)((long long)t * H / ny) : INT_MAX;
+  }
+  for (int t = lane; t < 198; t += 32) sc[66 + t] = 0;
+  __syncwarp();
+  // pass 1: bucket counts and corner parities
+  for (int s = 0; s < 2; s++) {
+    const PolyRef& c = pr[s];
+    int* cv = sc + 66 + 99 * s;
+    int* ch = cv + 33;
+    int* D = ch + 33;
+    for (int j = lane; j < c.nv; j += 32) {
+      int cc, lo, hi;
+      unpack_edge(__ldg(c.ev + j), cc, lo, hi);
+      const int x = cc + c.dx, yl = lo + c.dy, yh = hi + c.dy;
+      const int cm = count_below(x, nx, W);
+      if (cm >= 1 && cm <= nx && X[cm] != x) atomicAdd(&cv[cm - 1], 1);
+      const int cols = min(cm, nx);  // corners (X_c, Y_r) whose ray toward +x crosses this edge: X_c < x ...
+      const int r0 = min(count_below(yl, ny, H), ny), r1 = min(count_below(yh, ny, H), ny);  // ... and yl <= Y_r < yh
+      if (cols > 0 && r0 < r1) {
+        atomicXor(reinterpret_cast<unsigned*>(&D[r0]), low_bits(cols));
+        atomicXor(reinterpret_cast<unsigned*>(&D[r1]), low_bits(cols));
+      }
+    }
+    for (int j = lane; j < c.V; j += 32) {
+      const int2 a = __ldg(c.v + j), b = __ldg(c.v + (j + 1 == c.V ? 0 : j + 1));
+      if (a.y == b.y && a.x != b.x) {
+        const int f = a.y - c.oy;
+        const int rm = count_below(f, ny, H);
+        if (rm >= 1 && rm <= ny && Y[rm] != f) atomicAdd(&ch[rm - 1], 1);
+      }
+    }
+  }
+  __syncwarp();
+  // bucket starts (exclusive scans over <= 32 buckets), parities (prefix XOR)
+  int totv[2], toth[2];
+  for (int s = 0; s < 2; s++) {
+    int* cv = sc + 66 + 99 * s;
+    int* ch = cv + 33;
+    int* D = ch + 33;
+    int v = lane < nx ? cv[lane] : 0, h = lane < ny ? ch[lane] : 0;
+    unsigned d = lane < ny ? (unsigned)D[lane] : 0u;
+    int iv = v, ih = h;
+    unsigned id = d;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int a = __shfl_up_sync(FULL, iv, o), b = __shfl_up_sync(FULL, ih, o);
+      const unsigned e = __shfl_up_sync(FULL, id, o);
+      if (lane >= o) {
+        iv += a;
+        ih += b;
+        id ^= e;
+      }
+    }
+    totv[s] = __shfl_sync(FULL, iv, 31);
+    toth[s] = __shfl_sync(FULL, ih, 31);
+    __syncwarp();
+    if (lane < nx) cv[lane] = iv - v;
+    if (lane < ny) {
+      ch[lane] = ih - h;
+      D[lane] = (int)id;
+    }
+    __syncwarp();
+  }
+  const int hw = ix_header_words(nx, ny);
+  const long long need0 = hw + totv[0] + toth[0], need = need0 + hw + totv[1] + toth[1];
+  long long base = 0;
+  if (lane == 0) base = (long long)atomicAdd(&w.ctr[3], (unsigned long long)need);
+  base = __shfl_sync(FULL, base, 0);
+  if (base + need > w.pool_cap) return -1;
+  // headers, then the records (pass 2, each to its bucket's next slot)
+  for (int s = 0; s < 2; s++) {
+    const PolyRef& c = pr[s];
+    int* cv = sc + 66 + 99 * s;
+    int* ch = cv + 33;
+    const int* D = ch + 33;
+    uint64_t* blk = w.pool + base + (s ? need0 : 0);
+    unsigned* hdr = reinterpret_cast<unsigned*>(blk);
+    for (int t = lane; t <= nx; t += 32) hdr[t] = t < nx ? (unsigned)cv[t] : (unsigned)totv[s];
+    for (int t = lane; t <= ny; t += 32) hdr[nx + 1 + t] = t < ny ? (unsigned)ch[t] : (unsigned)toth[s];
+    for (int t = lane; t < ny; t += 32) hdr[nx + ny + 2 + t] = (unsigned)D[t];
+    uint64_t* vrec = blk + hw;
+    uint64_t* hrec = vrec + totv[s];
+    for (int j = lane; j < c.nv; j += 32) {
+      int cc, lo, hi;
+      unpack_edge(__ldg(c.ev + j), cc, lo, hi);
+      const int x = cc + c.dx, yl = lo + c.dy, yh = hi + c.dy;
+      const int cm = count_below(x, nx, W);
+      if (cm >= 1 && cm <= nx && X[cm] != x) vrec[atomicAdd(&cv[cm - 1], 1)] = pack_ix(x, yl, yh);
+    }
+    for (int j = lane; j < c.V; j += 32) {
+      const int2 a = __ldg(c.v + j), b = __ldg(c.v + (j + 1 == c.V ? 0 : j + 1));
+      if (a.y == b.y && a.x != b.x) {
+        const int f = a.y - c.oy;
+        const int rm = count_below(f, ny, H);
+        if (rm >= 1 && rm <= ny && Y[rm] != f)
+          hrec[atomicAdd(&ch[rm - 1], 1)] = pack_ix(f, min(a.x, b.x) - c.ox, max(a.x, b.x) - c.ox);
+      }
+    }
+  }
+  return base;
+}
+
+// The culled lists of region R = [X0, X1) x [Y0, Y1), region (rx, ry) of the
+// pair's nx x ny split, from polygon s's index at blk (see build_index):
+// the same sets as build_local(R), corner parity from the header.
+__device__ bool cull_index(const uint64_t* blk, int nx, int ny, int rx, int ry, int X0, int Y0, int X1, int Y1,
+                           LocalPoly& L) {
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = lanemask_lt();
+  const int Wr = X1 - X0, Hr = Y1 - Y0;
+  const unsigned* hdr = reinterpret_cast<const unsigned*>(blk);
+  const int vs = (int)hdr[rx], ve = (int)hdr[rx + 1], totv = (int)hdr[nx];
+  const int hs = (int)hdr[nx + 1 + ry], he = (int)hdr[nx + 1 + ry + 1];
+  L.pi = (int)((hdr[nx + ny + 2 + ry] >> rx) & 1u);
+  const uint64_t* vrec = blk + ix_header_words(nx, ny);
+  const uint64_t* hrec = vrec + totv;
+  int cnt = 0;
+  for (int j0 = vs; j0 < ve; j0 += 32) {  // warp-uniform
+    const int j = j0 + lane;
+    bool keep = false;
+    uint64_t rec = 0;
+    if (j < ve) {
+      int x, yl, yh;
+      unpack_ix(vrec[j], x, yl, yh);  // x strictly inside the region's columns (its bucket)
+      keep = yl < Y1 && yh > Y0;
+      rec = pack_loc(x - X0, max(yl - Y0, -1), min(yh - Y0, Hr + 1));
+    }
+    const unsigned b = __ballot_sync(FULL, keep);
+    const int pos = cnt + __popc(b & lt);
+    if (keep && pos < kLCap) L.V[pos] = rec;
+    cnt += __popc(b);
+  }
+  L.nV = cnt;
+  cnt = 0;
+  for (int j0 = hs; j0 < he; j0 += 32) {
+    const int j = j0 + lane;
+    bool keep = false;
+    uint64_t rec = 0;
+    if (j < he) {
+      int f, xl, xh;
+      unpack_ix(hrec[j], f, xl, xh);  // f strictly inside the region's rows
+      keep = xl < X1 && xh > X0;
+      rec = pack_loc(f - Y0, max(xl - X0, -1), min(xh - X0, Wr + 1));
+    }
+    const unsigned b = __ballot_sync(FULL, keep);
+    const int pos = cnt + __popc(b & lt);
+    if (keep && pos < kLCap) L.H[pos] = rec;
+    cnt += __popc(b);
+  }
+  L.nH = cnt;
+  return L.nV <= kLCap && L.nH <= kLCap;
+}
+
 // Lemma 1 (reading R6-A) for the sub-boxes of box B = [x0, x1) x [y0, y1)
 // (region coords), edge-parallel over the local lists.  pi = parity of B's
 // corner pixel (x0, y0).  hov: sub-boxes whose open interior meets an edge;
@@ -403,8 +610,8 @@ __device__ longlong2 pixelize_bands(const LocalPoly& P, const LocalPoly& Q, int 
         }
       }
       __syncwarp();
-      for (int i = lane; i < rb * nw; i += 32) {
-        const int w = i % nw;
+      // word index i % nw, kept incrementally (no integer modulo in the loop)
+      for (int i = lane, w = lane % nw, step = 32 % nw; i < rb * nw; i += 32, w = w + step >= nw ? w + step - nw : w + step) {
         const unsigned valid = low_bits(sw - 32 * w);
         const unsigned mp = DP[i], mq = DQ[i];
         ai += __popc(mp & mq & valid);
@@ -592,11 +799,32 @@ __global__ void __launch_bounds__(kLWarps * 32, 4)
       pr[s].oy = rb.y;
     }
     long long acc = 0, acc_u = 0;
+    // the pair's edge index: built by the warp holding its first item, used
+    // by the others once ready (else they cull directly)
+    long long ixb = -1;
+    // only worth it when the first items alone keep every warp busy for a few
+    // rounds, so the extra items (queued after all first items) find their
+    // index built instead of racing the build
+    if (w.pool && nx * ny >= kIxMin && nl >= 4ll * gridDim.x * kLWarps) {
+      if ((long long)t < nl) {
+        ixb = build_index(pr, W, H, nx, ny, w, reinterpret_cast<int*>(sv));
+        __threadfence();
+        __syncwarp();
+        if (lane == 0) {
+          if (ixb >= 0) w.ixoff[i] = ixb;
+          __threadfence();
+          st_release_i(&w.ixstate[i], ixb >= 0 ? kIxReady : kIxNone);
+        }
+      } else if (ld_acquire_i(&w.ixstate[i]) == kIxReady) {
+        ixb = w.ixoff[i];
+      }
+    }
     // in-warp item stack: the region, split in two while its local lists overflow
     if (lane == 0)
       istk[0] = make_int4((int)((long long)rx * W / nx), (int)((long long)ry * H / ny),
                           (int)((long long)(rx + 1) * W / nx), (int)((long long)(ry + 1) * H / ny));
     int itop = 1;
+    bool whole = true;  // the popped region is the item's own region (not a split of it)
     __syncwarp();
     while (itop > 0) {
       const int4 R = istk[itop - 1];
@@ -604,11 +832,19 @@ __global__ void __launch_bounds__(kLWarps * 32, 4)
       __syncwarp();
       const int Wr = R.z - R.x, Hr = R.w - R.y;
       bool fits = Wr <= kMaxRegion && Hr <= kMaxRegion;
-      if (fits) {
+      if (fits && whole && ixb >= 0) {
+        const uint64_t* b0 = w.pool + ixb;
+        const unsigned* h0 = reinterpret_cast<const unsigned*>(b0);
+        const uint64_t* b1 = b0 + ix_header_words(nx, ny) + h0[nx] + h0[nx + 1 + ny];
+        const bool a = cull_index(b0, nx, ny, rx, ry, R.x, R.y, R.z, R.w, P);
+        const bool b = cull_index(b1, nx, ny, rx, ry, R.x, R.y, R.z, R.w, Q);
+        fits = a && b;
+      } else if (fits) {
         const bool a = build_local(pr[0], R.x, R.y, R.z, R.w, P);
         const bool b = build_local(pr[1], R.x, R.y, R.z, R.w, Q);
         fits = a && b;
       }
+      whole = false;
       __syncwarp();
       if (!fits) {
         if (itop + 2 > kLItems) {
@@ -691,9 +927,13 @@ static size_t large_layout(long long n_cap, Carve& cv, LargeWs& w) {
   w.acc = cv.take<long long>(n);
   w.acc_u = cv.take<long long>(n);
   w.rem = cv.take<unsigned>(n);
+  w.ixstate = cv.take<int>(n);
+  w.ixoff = cv.take<long long>(n);
   w.n_cap = n_cap;
   w.extra_cap = extra_cap_for(n_cap);
   w.items = cv.take<uint64_t>(n + w.extra_cap);
+  w.pool = nullptr;
+  w.pool_cap = 0;
   return cv.used;
 }
 
@@ -703,11 +943,15 @@ size_t large_ws_bytes(long long n_cap) {
   return large_layout(n_cap, cv, w) + 256;
 }
 
-LargeWs large_ws(long long n_cap, void* ws, size_t ws_bytes, bool& ok) {
+LargeWs large_ws(long long n_cap, void* ws, size_t ws_bytes, void* pool, size_t pool_bytes, bool& ok) {
   Carve cv{reinterpret_cast<char*>(ws), ws_bytes};
   LargeWs w;
   large_layout(n_cap, cv, w);
   ok = cv.ok && ws != nullptr;
+  if (pool && pool_bytes >= 4096) {  // optional edge-index pool (8-byte words, 16-byte aligned by the caller)
+    w.pool = reinterpret_cast<uint64_t*>(pool);
+    w.pool_cap = (long long)(pool_bytes / 8);
+  }
   return w;
 }
 

@@ -142,10 +142,6 @@ __global__ void __launch_bounds__(kSmallWarps * 32, SCCG_SMALL_MINB)
   __shared__ int4 s_meta[kSmallWarps][32];
   __shared__ int2 s_ep[kSmallWarps][32];
   __shared__ unsigned long long s_acc[kSmallWarps][16];
-  // per-lane running totals of the 64-bit fields (sums_fields 3..9: sum_union,
-  // the areas, the ratio limbs), reduced once per CTA at the end instead of
-  // one warp reduction per field per chunk
-  __shared__ unsigned long long s_lacc[kSmallWarps][7][32];
   __shared__ int s_rstart[kSmallWarps][33];  // raster pairs: first (pair, row) item of each pair
   __shared__ unsigned s_rcnt[kSmallWarps][32];
   __shared__ const unsigned* s_rp[kSmallWarps][32];  // raster row of box row 0, per pair (p and q)
@@ -159,7 +155,6 @@ __global__ void __launch_bounds__(kSmallWarps * 32, SCCG_SMALL_MINB)
   int2* epq = s_ep[warp];
   if (lane == 0)
     for (int i = 0; i < 16; i++) s_acc[warp][i] = 0;
-  for (int f = 0; f < 7; f++) s_lacc[warp][f][lane] = 0ull;
   unsigned status = 0;
   for (;;) {
     unsigned long long k0 = 0;
@@ -403,7 +398,7 @@ __global__ void __launch_bounds__(kSmallWarps * 32, SCCG_SMALL_MINB)
     // ---- lane-parallel outputs and batch totals
     const unsigned long long c_px_all = COUNT ? warp_sum_u64(small ? (unsigned long long)W * H : 0ull) : 0ull;
     const bool done = ok && (small || empty);
-    unsigned long long v_i = 0;
+    unsigned long long v_i = 0, v_u = 0, v_ap = 0, v_aq = 0, l0 = 0, l1 = 0, l2 = 0, l3 = 0;
     unsigned nz = 0;
     if (done) {
       const long long ap = Ps.area[pq.x], aq = Qs.area[pq.y];
@@ -412,30 +407,39 @@ __global__ void __launch_bounds__(kSmallWarps * 32, SCCG_SMALL_MINB)
       if (inter) inter[k] = I;
       if (uni) uni[k] = U;
       v_i = I;
-      s_lacc[warp][1][lane] += (unsigned long long)ap;
-      s_lacc[warp][2][lane] += (unsigned long long)aq;
+      v_ap = ap;
+      v_aq = aq;
       if (I != 0) {
         nz = 1;
+        v_u = U;
         if (hit_p) atomicOr(&hit_p[pq.x >> 5], 1u << (pq.x & 31));
         if (hit_q) atomicOr(&hit_q[pq.y >> 5], 1u << (pq.y & 31));
-        unsigned long long l0, l1, l2, l3;
         ratio_limbs(I, U, l0, l1, l2, l3);
-        s_lacc[warp][0][lane] += (unsigned long long)U;
-        s_lacc[warp][3][lane] += l0;
-        s_lacc[warp][4][lane] += l1;
-        s_lacc[warp][5][lane] += l2;
-        s_lacc[warp][6][lane] += l3;
       }
     }
     const unsigned n_small = __popc(__ballot_sync(FULL, small));
     const unsigned n_done = __popc(__ballot_sync(FULL, done));
     const unsigned n_nz = __popc(__ballot_sync(FULL, nz != 0));
     v_i = __reduce_add_sync(FULL, (unsigned)v_i);  // <= 32 * 1024
+    v_u = warp_sum_u64(v_u);
+    v_ap = warp_sum_u64(v_ap);
+    v_aq = warp_sum_u64(v_aq);
+    l0 = warp_sum_u64(l0);
+    l1 = warp_sum_u64(l1);
+    l2 = warp_sum_u64(l2);
+    l3 = warp_sum_u64(l3);
     if (lane == 0) {
       unsigned long long* a = s_acc[warp];
       a[0] += n_done;
       a[1] += n_nz;
       a[2] += v_i;
+      a[3] += v_u;
+      a[4] += v_ap;
+      a[5] += v_aq;
+      a[6] += l0;
+      a[7] += l1;
+      a[8] += l2;
+      a[9] += l3;
       if (COUNT) {
         a[11] += c_tests;
         a[12] += c_px_all;
@@ -450,9 +454,6 @@ __global__ void __launch_bounds__(kSmallWarps * 32, SCCG_SMALL_MINB)
   if (threadIdx.x < 14) {
     unsigned long long v = 0;
     for (int w = 0; w < kSmallWarps; w++) v = threadIdx.x == 10 ? (v | s_acc[w][10]) : v + s_acc[w][threadIdx.x];
-    if (threadIdx.x >= 3 && threadIdx.x <= 9)  // the per-lane 64-bit totals
-      for (int w = 0; w < kSmallWarps; w++)
-        for (int l = 0; l < 32; l++) v += s_lacc[w][threadIdx.x - 3][l];
     unsigned long long* dst = reinterpret_cast<unsigned long long*>(sums);
     if (threadIdx.x < 10) {
       if (v) atomicAdd(&dst[threadIdx.x], v);
@@ -499,13 +500,17 @@ int run_pixelbox(const sccg_polyset* p, const sccg_polyset* q, const int32_t* pa
   PixelboxWs w;
   pixelbox_layout(n, cv, w);
   if (!cv.ok || ws == nullptr) return set_error(SCCG_E_WORKSPACE, "pixelbox workspace too small");
+  // workspace beyond the required part: the large path's edge-index pool (optional)
+  const size_t used = (cv.used + 255) & ~size_t(255);
+  void* pool = ws_bytes > used ? reinterpret_cast<char*>(ws) + used : nullptr;
+  const size_t pool_bytes = ws_bytes > used ? ws_bytes - used : 0;
   int T = cfg && cfg->threshold > 0 ? cfg->threshold : 2048;
   const int mode = cfg ? cfg->mode : 0;
   const bool use_raster = !(cfg && (cfg->flags & SCCG_FLAG_NO_RASTER));
   if (T < 2) T = 2;
   if (mode < 0 || mode > 2) return set_error(SCCG_E_ARG, "config.mode must be 0 (PixelBox), 1 (PixelOnly) or 2 (NoSep)");
   bool lok = true;
-  const LargeWs lw = large_ws(n, w.large, w.large_bytes, lok);
+  const LargeWs lw = large_ws(n, w.large, w.large_bytes, pool, pool_bytes, lok);
   if (!lok) return set_error(SCCG_E_WORKSPACE, "pixelbox (large) workspace too small");
   // the small kernel's queue and the large path's counters: one memset when
   // they are neighbours in the workspace (they are: pixelbox_layout)

@@ -90,12 +90,17 @@ constexpr int kMaxSplit = 32;      // regions per axis at most
 constexpr int kMaxRegion = 32766;  // local coordinates are 15-bit (plus clamp margin)
 
 struct LargeWs {
-  unsigned long long* ctr;  // [0] item queue, [1] extra item count, [2] large-pair count (low 32 bits)
+  unsigned long long* ctr;  // [0] item queue, [1] extra item count, [2] large-pair count (low 32 bits),
+                            // [3] words of the edge-index pool taken
   long long* list;          // [n_cap] pair index of large pair i
   long long* acc;           // [n_cap] |p n q| of large pair i
   long long* acc_u;         // [n_cap] |p u q| of large pair i (modes 1, 2: union counted directly)
   unsigned* rem;            // [n_cap] items of pair i not yet finished
   uint64_t* items;          // [n_cap + extra_cap]
+  int* ixstate;             // [n_cap] edge index of pair i: 0 none yet, 2 ready, 3 not built (large.cu)
+  long long* ixoff;         // [n_cap] its first pool word
+  uint64_t* pool;           // the edge-index pool (workspace beyond sccg_pixelbox_workspace_bytes), or null
+  long long pool_cap;       // its words
   long long n_cap, extra_cap;
 };
 
@@ -111,6 +116,7 @@ __device__ __forceinline__ void emit_large(const LargeWs& w, unsigned i, long lo
   w.list[i] = k;
   w.acc[i] = 0;
   w.acc_u[i] = 0;
+  w.ixstate[i] = 0;
   const int extra = nx * ny - 1;
   if (extra > 0) {
     const long long base = (long long)atomicAdd(&w.ctr[1], (unsigned long long)extra);
@@ -126,7 +132,7 @@ __device__ __forceinline__ void emit_large(const LargeWs& w, unsigned i, long lo
 }
 
 size_t large_ws_bytes(long long n_cap);
-LargeWs large_ws(long long n_cap, void* ws, size_t ws_bytes, bool& ok);
+LargeWs large_ws(long long n_cap, void* ws, size_t ws_bytes, void* pool, size_t pool_bytes, bool& ok);
 // the region-item kernel over everything the small kernel routed to the large path
 int launch_large(const DevSet& Ps, const DevSet& Qs, const int2* pairs, const LargeWs& w, long long* inter,
                  long long* uni, sccg_sums* sums, int T, int mode, int dense, long long* counters, unsigned* hit_p,

@@ -4,7 +4,7 @@
 set -u
 OUT=${1:-gpurun_out}
 mkdir -p $OUT
-timeout 300 python __graft_entry__.py > /dev/null 2>&1
+timeout 300 python __graft_entry__.py > gpurun_out/build_check.txt 2>&1 || { echo "BUILD FAILED"; tail -20 gpurun_out/build_check.txt; exit 1; }
 timeout 900 python scripts/fig9.py --lib libsccg_noopt.so --variants V0,V1,V2 --out $OUT/fig9_a.json > $OUT/fig9_a.txt 2>&1; echo "a rc=$?"
 timeout 900 python scripts/fig9.py --lib libsccg_nopdl.so --variants V3 --out $OUT/fig9_b.json > $OUT/fig9_b.txt 2>&1; echo "b rc=$?"
 timeout 900 python scripts/fig9.py --variants V4 --out $OUT/fig9_c.json > $OUT/fig9_c.txt 2>&1; echo "c rc=$?"

@@ -4,7 +4,7 @@
 set -u
 mkdir -p gpurun_out
 TAG=${TAG:-v}
-timeout 300 python __graft_entry__.py > /dev/null 2>&1
+timeout 300 python __graft_entry__.py > gpurun_out/build_check.txt 2>&1 || { echo "BUILD FAILED"; tail -20 gpurun_out/build_check.txt; exit 1; }
 for v in main ${VARIANTS:-}; do
   lib=""; [ "$v" != main ] && lib=libsccg_$v.so
   for c in ${CFG:-slide}; do
