@@ -183,6 +183,31 @@ def test_filter_long_segments(sccg):
     assert counts[0] > 4096 and 32 < counts[128] <= 1024 and 4 < counts[129] <= 32 and counts[131] > 32, counts
 
 
+def test_filter_crowded_buckets_overflow_chains(sccg):
+    """Many Q MBRs in one grid cell: a bucket's count runs past its 32 slots
+    into the overflow chain (walked by thread-per-p visits and by big-MBR
+    visits), and stacked identical boxes; also the closed join and every pair
+    list against the nested-loop oracle."""
+    rng = np.random.default_rng(5)
+    rings_q = [[[0, 0], [4, 0], [4, 4], [0, 4]] for _ in range(150)]  # 150 identical boxes
+    for _ in range(400):  # a crowd of small boxes in a 40 x 40 patch
+        x, y = (int(v) for v in rng.integers(0, 40, 2))
+        rings_q.append([[x, y], [x + 3, y], [x + 3, y + 3], [x, y + 3]])
+    rings_q += [[[5000 + 10 * i, 0], [5004 + 10 * i, 0], [5004 + 10 * i, 4], [5000 + 10 * i, 4]] for i in range(50)]
+    rings_p = [[[1, 1], [3, 1], [3, 3], [1, 3]], [[0, 0], [45, 0], [45, 45], [0, 45]],  # small, crowd-wide
+               [[-2000, -2000], [3000, -2000], [3000, 3000], [-2000, 3000]]]  # a big MBR over many cells
+    for _ in range(200):
+        x, y = (int(v) for v in rng.integers(-10, 50, 2))
+        rings_p.append([[x, y], [x + 2, y], [x + 2, y + 5], [x, y + 5]])
+    A, B = synth.pack(rings_p), synth.pack(rings_q)
+    P, Q = dev(A, sccg), dev(B, sccg)
+    got = sccg.filter_pairs(P, Q).cpu().numpy()
+    assert got.tolist() == oracle.join(A, B, "nested").tolist()
+    assert np.bincount(got[:, 0]).max() > 500
+    gotc = sccg.filter_pairs(P, Q, closed=True).cpu().numpy()
+    assert gotc.tolist() == oracle.join(A, B, "closed").tolist()
+
+
 def test_filter_closed_matches_oracle(sccg, tile_sets):
     """Closed-box join (touching MBRs pair too): the ST_Touches candidates."""
     A, B = tile_sets
