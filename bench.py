@@ -135,19 +135,21 @@ def prep_algorithmic_bytes(sccg, S) -> int:
 
 
 def lib_digest() -> str:
-    """sha256 prefix of the library's SOURCES (csrc/*, include/sccg.h, build.py
-    flags; nvcc output is not byte-reproducible): static profile numbers
+    """sha256 prefix of the library's SOURCES (csrc/*, include/sccg.h, the nvcc
+    flags of build.py; nvcc output is not byte-reproducible): static profile numbers
     (profiles/prep_traffic.json, issue_counts.json) apply only to the code they
     were taken on.  An experiment variant (SCCG_LIB) gets its own tag."""
     import glob
     import hashlib
 
+    from paper_1208_0277_b200 import build as sbuild
+
     h = hashlib.sha256()
     pkg = os.path.join(ROOT, "paper_1208_0277_b200")
-    for f in sorted(glob.glob(os.path.join(pkg, "csrc", "*"))) + [os.path.join(ROOT, "include", "sccg.h"),
-                                                                   os.path.join(pkg, "build.py")]:
+    for f in sorted(glob.glob(os.path.join(pkg, "csrc", "*"))) + [os.path.join(ROOT, "include", "sccg.h")]:
         with open(f, "rb") as fh:
             h.update(os.path.basename(f).encode() + b"\0" + fh.read())
+    h.update(" ".join(sbuild.ARCH + sbuild.FLAGS).encode())  # the compile flags, not build.py's other logic
     h.update((os.environ.get("SCCG_LIB") or "").encode())
     return h.hexdigest()[:16]
 

@@ -34,10 +34,10 @@ def _deps():
     return _sources() + glob.glob(os.path.join(CSRC, "*.cuh")) + [os.path.join(INCLUDE, "sccg.h"), __file__]
 
 
-def _stale() -> bool:
-    if not os.path.exists(LIB):
+def _stale(lib: str = LIB) -> bool:
+    if not os.path.exists(lib):
         return True
-    t = os.path.getmtime(LIB)
+    t = os.path.getmtime(lib)
     return any(os.path.getmtime(d) > t for d in _deps())
 
 
@@ -45,8 +45,8 @@ def build(force: bool = False, verbose: bool = False, extra: list[str] | None = 
     """Compile csrc/*.cu for sm_100a and link libsccg.so (or `out`, an
     experiment variant built with `extra` nvcc flags).  Returns its path."""
     lib = out or LIB
-    if not force and out is None and not _stale():
-        return LIB
+    if not force and not _stale(lib):
+        return lib
     bdir = BUILD if out is None else BUILD + "_" + os.path.basename(out).replace(".so", "")
     os.makedirs(bdir, exist_ok=True)
     extra = list(extra or [])

@@ -908,10 +908,10 @@ def test_ablation_builds_match_oracle(variant, flags):
     import sys
 
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    from paper_1208_0277_b200 import build as sbuild
+
     lib = os.path.join(root, "paper_1208_0277_b200", f"libsccg_{variant}.so")
-    if not os.path.exists(lib):
-        subprocess.run([sys.executable, os.path.join(root, "paper_1208_0277_b200", "build.py"), "--variant", variant,
-                        *flags], check=True, capture_output=True)
+    sbuild.build(extra=flags, out=lib)  # rebuilt when older than any source
     env = dict(os.environ, SCCG_LIB=lib)
     r = subprocess.run([sys.executable, "-c", _ABLATION_CHILD.format(root=root)], env=env, capture_output=True,
                        text=True, timeout=600)
