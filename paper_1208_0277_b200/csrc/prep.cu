@@ -431,7 +431,10 @@ __device__ void flush_stats(StatAcc& acc, SetStats* stats, unsigned long long* s
   acc.init();
 }
 
-__global__ void __launch_bounds__(kPrepThreads, 5) prep_kernel(const __grid_constant__ PrepArgs args) {
+#ifndef SCCG_PREP_MINB
+#define SCCG_PREP_MINB (640 / SCCG_PREP_THREADS)  // 5 CTAs of 128 threads per SM (shared memory)
+#endif
+__global__ void __launch_bounds__(kPrepThreads, SCCG_PREP_MINB) prep_kernel(const __grid_constant__ PrepArgs args) {
   pdl_entry_deferred();  // prep_init's counters
   extern __shared__ int4 s_dyn4[];  // kPrepVerts int2 (16-byte aligned)
   int2* s_xy = reinterpret_cast<int2*>(s_dyn4);
@@ -506,7 +509,7 @@ __global__ void __launch_bounds__(kPrepThreads, 5) prep_kernel(const __grid_cons
     long long next_gt = 0;
     if (threadIdx.x == 0) next_gt = (long long)atomicAdd(args.ticket, 1ull);  // the next tile, in flight
     if (threadIdx.x < kPrepPolys / 32) s_big[threadIdx.x] = 0;
-    if (threadIdx.x < kSortKeys) s_cnt[threadIdx.x] = 0;
+    for (int t = threadIdx.x; t < kSortKeys; t += kPrepThreads) s_cnt[t] = 0;
     s_perm[threadIdx.x] = 0xff;
     __syncthreads();
     // Rings are dealt to threads in order of vertex count (counting sort on
