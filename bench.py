@@ -337,8 +337,11 @@ def run_ours(args, rank, world, local_rank):
     host_bufs = [torch.zeros(len(sccg.SUMS_FIELDS), dtype=torch.int64).pin_memory() for _ in range(2)]
     done_ev = [torch.cuda.Event() for _ in range(2)]
     cap = 3 * max(P.n, Q.n) + 1024
+    # N > 1 over NCCL: the all-reduce is captured in the step graph (before the
+    # read-back); gloo (several ranks sharing one GPU, tests) runs it after the graph
+    in_graph = world > 1 and dist.get_backend() == "nccl"
     pipe = sccg.Pipeline(P, Q, cap=cap, threshold=args.threshold, graph=True,
-                         readback=host_bufs if world == 1 else ())
+                         readback=host_bufs if world == 1 or in_graph else ())
     threads = max(1, (os.cpu_count() or 1) // world)
 
     # ---- self-check of the benched step against the oracle (rank-local, before any all-reduce)
@@ -347,11 +350,14 @@ def run_ours(args, rank, world, local_rank):
     n_local = pipe.check()  # raises on a pair-buffer overflow or any device status bit
     local = [int(v) for v in pipe.sums.tolist()]
     check, ref_pass = self_check(args, A, B, pipe, n_local, local, threads)
+    if in_graph:  # recapture with the collective inside (the self-check needed the rank-local sums)
+        pipe = sccg.Pipeline(P, Q, cap=cap, threshold=args.threshold, graph=True, readback=host_bufs,
+                             allreduce=sdist.allreduce_sums)
 
     def enqueue(i, events=None):
         sums = pipe.run(events, slot=i % 2)
-        if world > 1:
-            sdist.allreduce_sums(sums)  # row a9: the only collective (NCCL, int64 SUM of the packed vector)
+        if world > 1 and not in_graph:
+            sdist.allreduce_sums(sums)  # row a9: the only collective (int64 SUM of the packed vector)
             host_bufs[i % 2].copy_(sums, non_blocking=True)
         done_ev[i % 2].record()
 

@@ -311,7 +311,7 @@ class Pipeline:
 
     def __init__(self, P: "DeviceSet", Q: "DeviceSet", cap: int | None = None, threshold: int = 0, graph: bool = True,
                  validate: bool = True, raster: bool = True, readback=(), outputs: bool = True,
-                 paper_split: bool = False, index: bool = True):
+                 paper_split: bool = False, index: bool = True, allreduce=None):
         torch = _torch()
         self.lib = load()
         self.P, self.Q = P, Q
@@ -334,6 +334,9 @@ class Pipeline:
                           None, None, None)
         self.validate = 1 if validate else 0
         self._sets = (PolySet * 2)(P.c, Q.c)  # copies of the bound descriptors (pointers only)
+        # allreduce: a callable (e.g. dist.allreduce_sums over NCCL) enqueued after PixelBox and before the
+        # read-back, so the multi-GPU step's one collective is inside the step graph
+        self.allreduce = allreduce
         # readback: pinned host int64 [11] buffers; run(slot=k) ends the step by
         # writing the sums into readback[k] from the GPU (sccg_sums_copy inside
         # the PixelBox graph: no copy-engine transfer, no extra launch)
@@ -396,6 +399,8 @@ class Pipeline:
                                             self.uni.data_ptr() if self.uni is not None else None, self.sums.data_ptr(),
                                             ctypes.byref(self.cfg), self.pws.data_ptr(), self.pws_bytes, _stream_ptr()),
                "sccg_pixelbox_async")
+        if self.allreduce is not None:
+            self.allreduce(self.sums)
         if self.readback:
             sums_copy(self.sums, self.readback[self._slot])
 
