@@ -316,6 +316,18 @@ SCCG_API int sccg_sums_unpack(const int64_t* vec, sccg_sums* dst, sccg_stream_t 
  * misaligned (not 8-byte) pointer. */
 SCCG_API int sccg_sums_copy(const sccg_sums* src, sccg_sums* dst, sccg_stream_t stream);
 
+/* Compact rectilinear rings, decoded on the device (an input encoding for the
+ * host -> device transfer; the polygons are rectilinear, so a ring's
+ * edges alternate between horizontal and vertical).  Ring i (offsets[i] ..
+ * offsets[i + 1], as for sccg_polyset) starts at start[2i], start[2i + 1]; its
+ * vertex k >= 1 moves from vertex k - 1 by move[offsets[i] - i + k - 1] (int16)
+ * along x or y, alternating, the first move along y iff first_vertical[i] != 0.
+ * Writes xy[2 * offsets[i] + 2k, +1] (int32) for every vertex: the plain layout
+ * sccg_prep reads.  Device pointers; offsets must be valid (0 = offsets[0] <=
+ * ... <= offsets[n]); n >= 0.  Asynchronous. */
+SCCG_API int sccg_decode_rect(const int32_t* start, const int16_t* move, const uint8_t* first_vertical,
+                              const int64_t* offsets, int64_t n, int32_t* xy, sccg_stream_t stream);
+
 /* ------------------------------------------------------------------ misc */
 SCCG_API const char* sccg_strerror(int code);
 SCCG_API const char* sccg_last_error_string(void); /* thread-local detail of the last failure */

@@ -39,7 +39,7 @@ SUMS_FIELDS = ("n_pairs", "n_nonzero", "sum_inter", "sum_union", "sum_area_p", "
                "limb2", "limb3", "status")
 SYMBOLS = ("sccg_polyset_bytes", "sccg_polyset_bind", "sccg_prep", "sccg_prep_sets", "sccg_filter_workspace_bytes",
            "sccg_filter_pairs", "sccg_filter_pairs_closed", "sccg_filter_pairs_async", "sccg_touches", "sccg_pixelbox_workspace_bytes", "sccg_pixelbox_index_bytes", "sccg_pixelbox",
-           "sccg_pixelbox_async", "sccg_count_missing", "sccg_contains", "sccg_report", "sccg_jaccard", "sccg_sums_copy",
+           "sccg_pixelbox_async", "sccg_count_missing", "sccg_contains", "sccg_report", "sccg_jaccard", "sccg_sums_copy", "sccg_decode_rect",
            "sccg_sums_pack", "sccg_sums_unpack", "sccg_strerror", "sccg_last_error_string", "sccg_last_error_index",
            "sccg_version")
 STATUS_ARG, STATUS_NOT_RECTILINEAR, STATUS_RANGE, STATUS_STACK, STATUS_CAPACITY = 1, 2, 4, 8, 16
@@ -145,6 +145,8 @@ def load(build: bool = True):
         lib.sccg_pixelbox_workspace_bytes.restype = sz
         lib.sccg_pixelbox_index_bytes.argtypes = [i64, i64]
         lib.sccg_pixelbox_index_bytes.restype = sz
+        lib.sccg_decode_rect.argtypes = [vp, vp, vp, vp, i64, vp, vp]
+        lib.sccg_decode_rect.restype = cint
         lib.sccg_pixelbox.argtypes = [ps, ps, vp, i64, vp, vp, vp, ctypes.POINTER(Config), vp, sz, vp]
         lib.sccg_pixelbox.restype = cint
         lib.sccg_count_missing.argtypes = [vp, i64, vp, vp]
@@ -760,6 +762,57 @@ def jaccard(sums) -> tuple[float, float]:
         return math.nan, math.nan
     _check(code, "sccg_jaccard")  # sums carrying device status bits are rejected
     return j.value, pooled.value
+
+
+def encode_rect(xy, offsets):
+    """Compact rectilinear rings for the host -> device transfer (sccg_decode_rect):
+    (start int32 [n, 2], move int16 [V - n], first_vertical uint8 [n]) with
+    2 bytes per vertex after each ring's first, or None when some ring is not
+    encodable (a zero-length or non-alternating move, a move beyond int16, an
+    empty ring).  Host-side numpy; lossless: the device decode is exact."""
+    import numpy as np
+
+    xy = np.asarray(xy, np.int64).reshape(-1, 2)
+    off = np.asarray(offsets, np.int64)
+    n = off.shape[0] - 1
+    V = np.diff(off)
+    if n == 0:
+        return np.zeros((0, 2), np.int32), np.zeros(0, np.int16), np.zeros(0, np.uint8)
+    if (V < 1).any():
+        return None
+    d = np.diff(xy, axis=0)  # d[j] = xy[j + 1] - xy[j]
+    first = np.zeros(xy.shape[0], bool)
+    first[off[:-1]] = True
+    keep = ~first[1:]  # moves within a ring: vertex j + 1 is not a ring start
+    mv = d[keep]
+    ring = np.repeat(np.arange(n), V - 1)
+    k = np.arange(mv.shape[0]) - np.repeat(off[:-1] - np.arange(n), V - 1) + 1  # vertex index in its ring (>= 1)
+    vert_move = mv[:, 0] == 0
+    if ((mv[:, 0] != 0) == (mv[:, 1] != 0)).any():  # exactly one coordinate changes
+        return None
+    fv = np.zeros(n, np.uint8)
+    has = V > 1
+    fv[has] = vert_move[(off[:-1] - np.arange(n))[has]]
+    expect_vert = ((k & 1) == 1) == (fv[ring] == 1)
+    if (vert_move != expect_vert).any():
+        return None
+    m = np.where(vert_move, mv[:, 1], mv[:, 0])
+    if m.size and (np.abs(m).max() > 32767):
+        return None
+    start = xy[off[:-1]].astype(np.int32)
+    return start, m.astype(np.int16), fv
+
+
+def decode_rect(start, move, first_vertical, offsets, stream=None):
+    """sccg_decode_rect on device tensors: the plain int32 [V, 2] vertices."""
+    torch = _torch()
+    n = int(offsets.numel()) - 1
+    nv = int(offsets[-1].item()) if n > 0 else 0
+    xy = torch.empty((max(nv, 1), 2), dtype=torch.int32, device=offsets.device)
+    _check(load().sccg_decode_rect(start.data_ptr(), move.data_ptr() if move.numel() else None,
+                                   first_vertical.data_ptr(), offsets.data_ptr(), n, xy.data_ptr(), _stream_ptr(stream)),
+           "sccg_decode_rect")
+    return xy[:nv]
 
 
 def to_device(xy, offsets, device="cuda", non_blocking=True):

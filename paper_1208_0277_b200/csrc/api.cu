@@ -35,6 +35,8 @@ int check_cuda(cudaError_t e, const char* where) {
   return set_error(SCCG_E_CUDA, buf);
 }
 
+int decode_rect(const int32_t* start, const int16_t* move, const uint8_t* first_vertical, const int64_t* offsets,
+                int64_t n, int32_t* xy, cudaStream_t stream);
 size_t filter_ws_bytes(int64_t np, int64_t nq);
 int filter_pairs(const sccg_polyset* P, const sccg_polyset* Q, int32_t* pairs, int64_t cap, int64_t* n_pairs_host,
                  void* ws, size_t ws_bytes, int closed, cudaStream_t stream);
@@ -329,6 +331,16 @@ int sccg_count_missing(const uint32_t* hit, int64_t n, int64_t* missing_dev, scc
   if (n < 0 || !missing_dev || (n > 0 && !hit)) return set_error(SCCG_E_ARG, "sccg_count_missing: bad argument");
   if (!aligned(hit, 4) || !aligned(missing_dev, 8)) return set_error(SCCG_E_ARG, "sccg_count_missing: misaligned");
   return count_missing(hit, n, missing_dev, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int sccg_decode_rect(const int32_t* start, const int16_t* move, const uint8_t* first_vertical,
+                     const int64_t* offsets, int64_t n, int32_t* xy, sccg_stream_t stream) {
+  NvtxRange nvtx_range("sccg_decode_rect");
+  set_error(SCCG_OK, "", -1);
+  if (n < 0 || (n > 0 && (!start || !first_vertical || !offsets || !xy)) || !aligned(start, 8) || !aligned(xy, 8) ||
+      !aligned(offsets, 8) || !aligned(move, 2))
+    return set_error(SCCG_E_ARG, "sccg_decode_rect: bad size or null / misaligned pointer");
+  return sccg::decode_rect(start, move, first_vertical, offsets, n, xy, reinterpret_cast<cudaStream_t>(stream));
 }
 
 int sccg_sums_copy(const sccg_sums* src, sccg_sums* dst, sccg_stream_t stream) {

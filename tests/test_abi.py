@@ -140,3 +140,45 @@ def test_jaccard_rejects_status_bits_and_new_entry_points():
     assert lib.sccg_report(None, None, None, 0, None, None, None, None, ctypes.byref(t), None, None) == sccg.E_ARG
     assert lib.sccg_sums_pack(None, None, None) == sccg.E_ARG
     assert lib.sccg_sums_unpack(8, 12, None) == sccg.E_ARG
+
+
+def _decode_rect_host(start, move, fv, off):
+    """Plain loop mirror of sccg_decode_rect (include/sccg.h)."""
+    n = len(off) - 1
+    xy = np.zeros((int(off[-1]), 2), np.int64)
+    for i in range(n):
+        x, y = (int(v) for v in start[i])
+        xy[off[i]] = (x, y)
+        mb = int(off[i]) - i
+        for k in range(1, int(off[i + 1] - off[i])):
+            d = int(move[mb + k - 1])
+            if ((k & 1) == 1) == (fv[i] == 1):
+                y += d
+            else:
+                x += d
+            xy[off[i] + k] = (x, y)
+    return xy
+
+
+def test_encode_rect_roundtrip_and_rejects(tile_sets):
+    """The compact rectilinear encoding (sccg_decode_rect's input): lossless on
+    clean rectilinear rings of either orientation and either first-edge axis;
+    rings it cannot express (a duplicate vertex, a collinear vertex, a move
+    beyond int16) are refused, never mis-encoded."""
+    import synth
+
+    for S in tile_sets:
+        start, move, fv = sccg.encode_rect(S.xy, S.offsets)
+        assert move.dtype == np.int16 and len(move) == len(S.xy) - S.n
+        assert np.array_equal(_decode_rect_host(start, move, fv, S.offsets), S.xy)
+    sq = [[0, 0], [5, 0], [5, 3], [0, 3]]
+    rings = [sq, sq[::-1], [[2, 2], [2, 9], [7, 9], [7, 2]]]  # CCW, CW, first edge vertical
+    P = synth.pack(rings)
+    start, move, fv = sccg.encode_rect(P.xy, P.offsets)
+    assert fv.tolist() == [0, 1, 1]
+    assert np.array_equal(_decode_rect_host(start, move, fv, P.offsets), P.xy)
+    for bad in ([[0, 0], [0, 0], [5, 0], [5, 3], [0, 3]],  # duplicate vertex
+                [[0, 0], [2, 0], [5, 0], [5, 3], [0, 3]],  # collinear vertex
+                [[0, 0], [40000, 0], [40000, 3], [0, 3]]):  # move beyond int16
+        Q = synth.pack([sq, bad])
+        assert sccg.encode_rect(Q.xy, Q.offsets) is None

@@ -936,3 +936,31 @@ def test_filter_recycled_workspaces(sccg):
         counters = torch.zeros(8, dtype=torch.int64, device="cuda")
         sccg.pixelbox(P, Q, pairs, threshold=64, counters=counters)
         assert counters[sccg.CNT_SPLITS].item() > 0
+
+
+@pytest.mark.parametrize("config", ["tile", "combs", "slide"])
+def test_decode_rect_exact(sccg, config):
+    """sccg_decode_rect (the compact host -> device encoding) reproduces every
+    vertex of the plain layout exactly, and the path from the compact form
+    gives the same pairs and sums as from the plain one."""
+    if config == "combs":
+        A, B = combs.generate(n_pairs=64)
+    else:
+        A, B = synth.generate(config)
+    for S in (A, B):
+        enc = sccg.encode_rect(S.xy, S.offsets)
+        assert enc is not None
+        start, move, fv = (torch.from_numpy(a).cuda() for a in enc)
+        off = torch.from_numpy(S.offsets).cuda()
+        xy = sccg.decode_rect(start, move, fv, off)
+        assert torch.equal(xy.cpu(), torch.from_numpy(S.xy.astype(np.int32)))
+    if config == "tile":
+        P0, Q0 = dev(A, sccg), dev(B, sccg)
+        dec = []
+        for S in (A, B):
+            start, move, fv = (torch.from_numpy(a).cuda() for a in sccg.encode_rect(S.xy, S.offsets))
+            off = torch.from_numpy(S.offsets).cuda()
+            dec.append(sccg.DeviceSet(sccg.decode_rect(start, move, fv, off), off))
+        _, _, s0 = sccg.pixelbox(P0, Q0, sccg.filter_pairs(P0, Q0))
+        _, _, s1 = sccg.pixelbox(dec[0], dec[1], sccg.filter_pairs(dec[0], dec[1]))
+        assert torch.equal(s0, s1)
