@@ -175,7 +175,7 @@ def test_encode_rect_roundtrip_and_rejects(tile_sets):
     rings = [sq, sq[::-1], [[2, 2], [2, 9], [7, 9], [7, 2]]]  # CCW, CW, first edge vertical
     P = synth.pack(rings)
     start, move, fv = sccg.encode_rect(P.xy, P.offsets)
-    assert fv.tolist() == [0, 1, 1]
+    assert fv.tolist() == [0, 0, 1]
     assert np.array_equal(_decode_rect_host(start, move, fv, P.offsets), P.xy)
     for bad in ([[0, 0], [0, 0], [5, 0], [5, 3], [0, 3]],  # duplicate vertex
                 [[0, 0], [2, 0], [5, 0], [5, 3], [0, 3]],  # collinear vertex
