@@ -964,3 +964,68 @@ def test_decode_rect_exact(sccg, config):
         _, _, s0 = sccg.pixelbox(P0, Q0, sccg.filter_pairs(P0, Q0))
         _, _, s1 = sccg.pixelbox(dec[0], dec[1], sccg.filter_pairs(dec[0], dec[1]))
         assert torch.equal(s0, s1)
+
+
+def _study_rank(rank, world, port, out):
+    import os
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    import torch
+    import torch.distributed as dist
+
+    import bench
+    import paper_1208_0277_b200 as sccg
+    from paper_1208_0277_b200 import dist as sdist
+    import synth
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    plan = bench.study_images(7, 2)
+    mine = [plan[i] for i in sdist.shard_for_rank(len(plan), world, rank)]
+    bases = {b: synth.generate("tile", image=20 + b) for b in (0, 1)}
+    images = []
+    for im in mine:
+        A, B = bases[im["base"]]
+        xa, oa = sccg.to_device(A.xy, A.offsets)
+        xb, ob = sccg.to_device(B.xy, B.offsets)
+        images.append((bench.instance_xy(xa, im["sym"], im["dx"], im["dy"]), oa,
+                       bench.instance_xy(xb, im["sym"], im["dx"], im["dy"]), ob))
+    sums = sccg.Study(images).run().clone() if images else sccg.new_sums("cuda")
+    sdist.allreduce_sums(sums, force=True)
+    out[rank] = sums.cpu().tolist()
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.timeout(600)
+def test_study_gloo_ranks_bit_identical(sccg):
+    """configs[3] over 1, 2 and 3 ranks (gloo, sharing cuda:0): LPT shards of
+    the same 7 instanced images, each rank's pass one Study graph, one
+    all-reduce -- the reduced sums are bit-identical for every rank count."""
+    import socket
+
+    import torch.multiprocessing as tmp
+
+    results = {}
+    for world in (1, 2, 3):
+        ctx = tmp.get_context("spawn")
+        mgr = ctx.Manager()
+        out = mgr.dict()
+        s = socket.socket()
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+        s.close()
+        procs = [ctx.Process(target=_study_rank, args=(r, world, port, out)) for r in range(world)]
+        for p in procs:
+            p.start()
+        for p in procs:
+            p.join(500)
+            assert p.exitcode == 0
+        assert all(out[r] == out[0] for r in range(world))
+        results[world] = out[0]
+    assert results[1] == results[2] == results[3]
+    assert results[1][10] == 0 and results[1][0] > 0
