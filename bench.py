@@ -135,8 +135,9 @@ def prep_algorithmic_bytes(sccg, S) -> int:
 
 
 def lib_digest() -> str:
-    """sha256 prefix of the library's SOURCES (csrc/*, include/sccg.h, the nvcc
-    flags of build.py; nvcc output is not byte-reproducible): static profile numbers
+    """sha256 prefix of the library's SOURCES (csrc/*, include/sccg.h without
+    comments and blank space, the nvcc flags of build.py; nvcc output is not
+    byte-reproducible): static profile numbers
     (profiles/prep_traffic.json, issue_counts.json) apply only to the code they
     were taken on.  An experiment variant (SCCG_LIB) gets its own tag."""
     import glob
@@ -146,9 +147,16 @@ def lib_digest() -> str:
 
     h = hashlib.sha256()
     pkg = os.path.join(ROOT, "paper_1208_0277_b200")
+    import re
+
     for f in sorted(glob.glob(os.path.join(pkg, "csrc", "*"))) + [os.path.join(ROOT, "include", "sccg.h")]:
-        with open(f, "rb") as fh:
-            h.update(os.path.basename(f).encode() + b"\0" + fh.read())
+        with open(f, encoding="utf-8") as fh:
+            code = fh.read()
+        # comments and blank space do not change the code: drop them before hashing
+        code = re.sub(r"/\*.*?\*/", "", code, flags=re.S)
+        code = re.sub(r"//[^\n]*", "", code)
+        code = "\n".join(line.strip() for line in code.splitlines() if line.strip())
+        h.update(os.path.basename(f).encode() + b"\0" + code.encode())
     h.update(" ".join(sbuild.ARCH + sbuild.FLAGS).encode())  # the compile flags, not build.py's other logic
     h.update((os.environ.get("SCCG_LIB") or "").encode())
     return h.hexdigest()[:16]

@@ -9,8 +9,8 @@
 // its cells, and a pair is emitted only from the cell holding its reference
 // point (max xlo, max ylo) so it is found exactly once.
 //
-//   1. grid_select_kernel -- clears the bucket counters and the probe's tile
-//      states; one warp picks the cell size 2^k and the bucket wrap from the
+//   1. grid_select_kernel -- clears the bucket counters and the overflow-pool
+//      counter; one warp picks the cell size 2^k and the bucket wrap from the
 //      per-set statistics sccg_prep gathered (no host round trip).
 //   2. grid_insert_kernel -- each Q MBR takes a slot in the bucket of every
 //      cell it covers (fixed-capacity buckets, an overflow chain past
