@@ -114,11 +114,16 @@ SCCG_API int sccg_prep(const sccg_polyset* set, int32_t validate, sccg_stream_t 
 SCCG_API int sccg_prep_sets(const sccg_polyset* sets, int32_t count, int32_t validate, sccg_stream_t stream);
 
 /* ---------------------------------------------------------------- filter */
-/* Workspace bytes sccg_filter_pairs needs for sets of these sizes. */
+/* Workspace bytes sccg_filter_pairs needs for sets of these sizes (the hashed
+ * grid's bucket counters, 32 slots per bucket and an overflow pool, and the
+ * probe tiles' pair buckets: about 700 bytes per Q polygon plus 8 KiB per
+ * 128 P polygons).  The contents need no initialisation: every call clears
+ * what it reads. */
 SCCG_API size_t sccg_filter_workspace_bytes(int64_t n_p, int64_t n_q);
 
-/* MBR-overlap join of two prepared sets by a grid hash on
- * the device.  Writes the candidate pairs, unique and sorted by (p, q), as
+/* MBR-overlap join of two prepared sets by a hashed
+ * uniform grid on the device (four kernels, no host round trip before the
+ * count).  Writes the candidate pairs, unique and sorted by (p, q), as
  * pairs[k] = {p, q} (int32 [cap][2]) and sets *n_pairs_host (host) to their
  * count.  If cap < count (or pairs == NULL) SCCG_E_CAPACITY is returned with
  * *n_pairs_host = required count (the contents of pairs are then unspecified:
