@@ -358,9 +358,16 @@ def run_ours(args, rank, world, local_rank):
     n_local = pipe.check()  # raises on a pair-buffer overflow or any device status bit
     local = [int(v) for v in pipe.sums.tolist()]
     check, ref_pass = self_check(args, A, B, pipe, n_local, local, threads)
+    collective = "eager after the graph" if world > 1 else None
     if in_graph:  # recapture with the collective inside (the self-check needed the rank-local sums)
-        pipe = sccg.Pipeline(P, Q, cap=cap, threshold=args.threshold, graph=True, readback=host_bufs,
-                             allreduce=sdist.allreduce_sums)
+        try:
+            pipe = sccg.Pipeline(P, Q, cap=cap, threshold=args.threshold, graph=True, readback=host_bufs,
+                                 allreduce=sdist.allreduce_sums)
+            collective = "NCCL, captured in the step graph"
+        except Exception as exc:  # keep the run: the same collective, launched after each replay
+            print(f"[bench] NCCL capture failed ({exc!r}); all-reduce after the graph", file=sys.stderr)
+            in_graph = False
+            pipe = sccg.Pipeline(P, Q, cap=cap, threshold=args.threshold, graph=True, readback=())
 
     def enqueue(i, events=None):
         sums = pipe.run(events, slot=i % 2)
@@ -546,7 +553,7 @@ def run_ours(args, rank, world, local_rank):
     # our kernels per step (profiles/<round>/launches_slide_summary.txt)
     launches_per_step = LAUNCHES_PER_STEP + (1 if world == 1 else 2)
     cfg = workload_config(args.config, A, B, n_local, world, args.shard)
-    cfg.update({"pairs_total": total_pairs, "threshold_T": args.threshold or 2048,
+    cfg.update({"pairs_total": total_pairs, "threshold_T": args.threshold or 2048, "allreduce": collective,
                 "l2": "inputs larger than L2 (vertex arrays ~%d MB per rank > 126 MB)" % ((P.nv + Q.nv) * 8 // 2**20)})
     out = {
         "metric": METRIC,
@@ -719,8 +726,16 @@ def run_study(args, rank, world, local_rank):
     done_ev = [torch.cuda.Event() for _ in range(2)]
     # the all-reduce inside the step graph when NCCL (graph-capturable); gloo runs it after the graph
     in_graph = world > 1 and backend == "nccl"
-    study = sccg.Study(images, threshold=args.threshold, graph=True, readback=host_bufs if world == 1 or in_graph else (),
-                       allreduce=sdist.allreduce_sums if in_graph else None)
+    try:
+        study = sccg.Study(images, threshold=args.threshold, graph=True,
+                           readback=host_bufs if world == 1 or in_graph else (),
+                           allreduce=sdist.allreduce_sums if in_graph else None)
+    except Exception as exc:  # keep the run: the same collective, launched after each replay
+        if not in_graph:
+            raise
+        print(f"[bench] NCCL capture failed ({exc!r}); all-reduce after the graph", file=sys.stderr)
+        in_graph = False
+        study = sccg.Study(images, threshold=args.threshold, graph=True, readback=())
     # the self-check needs the rank-local sums: one eager pass without the all-reduce
     study.allreduce = None
     study.run(events=[[torch.cuda.Event() for _ in range(4)] for _ in images])
