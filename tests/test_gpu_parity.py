@@ -643,6 +643,8 @@ def test_abi_errors(sccg):
     # empty sets
     empty = synth.PolygonSet(np.zeros((0, 2), np.int32), np.zeros(1, np.int64))
     assert sccg.filter_pairs(dev(empty, sccg), dev(good, sccg)).shape[0] == 0
+    assert sccg.filter_pairs(dev(good, sccg), dev(empty, sccg)).shape[0] == 0
+    assert sccg.filter_pairs(dev(empty, sccg), dev(empty, sccg)).shape[0] == 0
 
 
 # --------------------------------------------------- full bench configuration
