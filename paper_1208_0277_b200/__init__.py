@@ -589,6 +589,90 @@ class Study:
         return int(self.sums[0])
 
 
+class Streamer:
+    """End-to-end comparison of image pairs arriving in host memory, pipelined.
+
+    Each submitted pair of sets travels host -> device in the compact
+    rectilinear encoding (encode_rect: a quarter of the vertex bytes), is
+    decoded on the GPU (sccg_decode_rect) and runs the whole step (a Pipeline
+    graph: prep, join, PixelBox, the sums written into pinned host memory by
+    the GPU).  `depth` slots of device buffers rotate: the host -> device copy
+    of step i + 1 runs on a copy stream while step i computes, so a PCIe-bound
+    stream of images moves at the link's speed.  Shapes are fixed per slot
+    (n polygons and vertices of each set, as in the first submit's sizes).
+
+        st = Streamer(A.n, A.nv, B.n, B.nv)
+        t = st.submit(encoded_a, off_a, encoded_b, off_b)   # pinned host tensors
+        sums = st.result(t)                                  # waits for that step"""
+
+    def __init__(self, n_p: int, nv_p: int, n_q: int, nv_q: int, cap: int | None = None, threshold: int = 0,
+                 depth: int = 2, device=None):
+        torch = _torch()
+        dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.depth = depth
+        self.shapes = (n_p, nv_p, n_q, nv_q)
+        cap = int(cap) if cap is not None else 3 * max(n_p, n_q) + 1024
+        self.slots = []
+        for _ in range(depth):
+            sl = {}
+            for side, n, nv in (("p", n_p, nv_p), ("q", n_q, nv_q)):
+                sl["start_" + side] = torch.empty((max(n, 1), 2), dtype=torch.int32, device=dev)
+                sl["move_" + side] = torch.empty(max(nv - n, 1), dtype=torch.int16, device=dev)
+                sl["fv_" + side] = torch.empty(max(n, 1), dtype=torch.uint8, device=dev)
+                sl["off_" + side] = torch.zeros(n + 1, dtype=torch.int64, device=dev)
+                sl["xy_" + side] = torch.empty((max(nv, 1), 2), dtype=torch.int32, device=dev)
+            sl["rb"] = torch.zeros(len(SUMS_FIELDS), dtype=torch.int64).pin_memory()
+            P = DeviceSet(sl["xy_p"][:nv_p], sl["off_p"], prep=False)
+            Q = DeviceSet(sl["xy_q"][:nv_q], sl["off_q"], prep=False)
+            sl["sets"] = (P, Q)
+            sl["pipe"] = Pipeline(P, Q, cap=cap, threshold=threshold, graph=True, readback=[sl["rb"]])
+            sl["copied"], sl["done"] = torch.cuda.Event(), torch.cuda.Event()
+            self.slots.append(sl)
+        self.copy_stream = torch.cuda.Stream(device=dev)
+        self.count = 0
+
+    def _decode(self, sl):
+        for side in ("p", "q"):
+            n = int(sl["off_" + side].numel()) - 1
+            _check(load().sccg_decode_rect(sl["start_" + side].data_ptr(), sl["move_" + side].data_ptr(),
+                                           sl["fv_" + side].data_ptr(), sl["off_" + side].data_ptr(), n,
+                                           sl["xy_" + side].data_ptr(), _stream_ptr()), "sccg_decode_rect")
+
+    def submit(self, enc_p, off_p, enc_q, off_q) -> int:
+        """Enqueue one step for host sets given as encode_rect tuples (start,
+        move, first_vertical) of pinned CPU tensors plus their offsets.  Returns
+        a ticket for result()."""
+        torch = _torch()
+        k = self.count % self.depth
+        sl = self.slots[k]
+        main = torch.cuda.current_stream()
+        cs = self.copy_stream
+        cs.wait_event(sl["done"])  # the slot's previous step no longer reads its buffers
+        with torch.cuda.stream(cs):
+            for side, (st, mv, fv), off in (("p", enc_p, off_p), ("q", enc_q, off_q)):
+                sl["start_" + side][: st.shape[0]].copy_(st, non_blocking=True)
+                if mv.numel():
+                    sl["move_" + side][: mv.shape[0]].copy_(mv, non_blocking=True)
+                sl["fv_" + side][: fv.shape[0]].copy_(fv, non_blocking=True)
+                sl["off_" + side].copy_(off, non_blocking=True)
+            sl["copied"].record(cs)
+        main.wait_event(sl["copied"])
+        self._decode(sl)
+        sl["pipe"].run(slot=0)
+        sl["done"].record(main)
+        self.count += 1
+        return self.count - 1
+
+    def result(self, ticket: int):
+        """The sums of step `ticket` (waits for it; its slot must not have been
+        reused since: at most `depth` steps in flight)."""
+        if ticket < self.count - self.depth:
+            raise ValueError("Streamer: that step's slot has been reused")
+        sl = self.slots[ticket % self.depth]
+        sl["done"].synchronize()
+        return sums_to_host(sl["rb"])
+
+
 def touches(P: DeviceSet, Q: DeviceSet, pairs, inter, stream=None):
     """ST_Touches (reading R21) per pair: uint8 [N], 1 iff |p n q| == 0
     (inter: the pairs' intersections from pixelbox) and the boundaries meet.

@@ -1031,3 +1031,29 @@ def test_study_gloo_ranks_bit_identical(sccg):
         results[world] = out[0]
     assert results[1] == results[2] == results[3]
     assert results[1][10] == 0 and results[1][0] > 0
+
+
+def test_streamer_matches_pipeline(sccg):
+    """sccg.Streamer (compact host -> device transfer on a copy stream, decode,
+    the step graph, read-back; two slots in flight): every step's sums equal
+    the device-resident Pipeline's for the same sets, steps of two different
+    images interleaved."""
+    imgs = []
+    for image in (30, 31):
+        A, B = synth.generate("tile", image=image)
+        P, Q = dev(A, sccg), dev(B, sccg)
+        pipe = sccg.Pipeline(P, Q, graph=False)
+        pipe.run()
+        torch.cuda.synchronize()
+        enc = [[torch.from_numpy(a).pin_memory() for a in sccg.encode_rect(S.xy, S.offsets)] for S in (A, B)]
+        offs = [torch.from_numpy(S.offsets).pin_memory() for S in (A, B)]
+        imgs.append((A, B, enc, offs, pipe.sums.cpu().tolist()))
+    # one Streamer per shape (slots are shaped by the first sets); same-shaped repeats of each image
+    for A, B, enc, offs, ref in imgs:
+        st = sccg.Streamer(A.n, int(A.offsets[-1]), B.n, int(B.offsets[-1]))
+        tickets = [st.submit(enc[0], offs[0], enc[1], offs[1]) for _ in range(2)]
+        got = [st.result(t) for t in tickets]
+        tickets = [st.submit(enc[0], offs[0], enc[1], offs[1]) for _ in range(2)]
+        got += [st.result(t) for t in tickets]
+        for g in got:
+            assert [getattr(g, f) for f in sccg.SUMS_FIELDS] == ref
