@@ -33,4 +33,16 @@ pairs = sccg.filter_pairs(P, Q)
 for ps in (False, True):
     sccg.pixelbox(P, Q, pairs, threshold=2048, paper_split=ps)
 torch.cuda.synchronize()
+if os.environ.get("SANITIZE_INDEX"):
+    # enough comb pairs that the large path builds per-pair edge indexes (first items >= 4 x the item
+    # kernel's warps), with and without the pool
+    A, B = combs.generate(n_pairs=12000)
+    P = sccg.DeviceSet(*sccg.to_device(A.xy, A.offsets))
+    Q = sccg.DeviceSet(*sccg.to_device(B.xy, B.offsets))
+    pairs = sccg.filter_pairs(P, Q)
+    i1, u1, s1 = sccg.pixelbox(P, Q, pairs, threshold=2048)
+    i2, u2, s2 = sccg.pixelbox(P, Q, pairs, threshold=2048, index=False)
+    torch.cuda.synchronize()
+    assert torch.equal(i1, i2) and torch.equal(s1, s2)
+torch.cuda.synchronize()
 print("sanitize case ok")
