@@ -287,8 +287,20 @@ constexpr int kKeep = 4;                     // hits kept in registers by the co
 
 // (p, q) is owned by cell (cx, cy) iff the boxes overlap (half-open, R4) and
 // the reference point (max xlo, max ylo) lies in that cell.
-__device__ __forceinline__ bool owns(const int4& a, const int4& b, int k, int cx, int cy) {
-  return a.x < b.z && b.x < a.z && a.y < b.w && b.y < a.w && (max(a.x, b.x) >> k) == cx && (max(a.y, b.y) >> k) == cy;
+// With the cell bounds hoisted out of the entry loop: for a cell
+// (cx, cy) that p covers, max(a.x, b.x) lies in column cx iff b.x < the
+// column's end and -- unless cx is p's first column, where a.x already starts
+// it -- b.x >= its start (a.x < the end of every column p covers); likewise y.
+struct Own {
+  int lx, hx, ly, hy;
+};
+__device__ __forceinline__ Own own_bounds(const int4& a, int k, int cx, int cy) {
+  const long long ex = ((long long)cx + 1) << k, ey = ((long long)cy + 1) << k;
+  return Own{cx == (a.x >> k) ? INT_MIN : (int)((long long)cx << k), (int)min(ex, (long long)INT_MAX),
+             cy == (a.y >> k) ? INT_MIN : (int)((long long)cy << k), (int)min(ey, (long long)INT_MAX)};
+}
+__device__ __forceinline__ bool owns(const int4& a, const int4& b, const Own& o) {
+  return a.x < b.z && b.x < a.z && a.y < b.w && b.y < a.w && b.x >= o.lx && b.x < o.hx && b.y >= o.ly && b.y < o.hy;
 }
 
 // Test one visited cell's bucket against `a`; take(h, q) for each entry
@@ -303,36 +315,37 @@ template <class Take>
 __device__ __forceinline__ void visit(const int4& a, int k, int cx, int cy, int b, const Tables& t, Take&& take) {
   const int4* s0 = t.slot + t.at(b, 0);
   const int cnt = t.count[(size_t)b * kCStride];
+  const Own o = own_bounds(a, k, cx, cy);
   const int4 e0 = s0[0];
 #if SCCG_JOIN_SPEC >= 2
   const int4 e1 = s0[1];
 #endif
-  take(cnt > 0 && owns(a, entry_box(e0), k, cx, cy), e0.w);
+  take(cnt > 0 && owns(a, entry_box(e0), o), e0.w);
   if (cnt > 1) {
 #if SCCG_JOIN_SPEC < 2
     const int4 e1 = s0[1];
 #endif
-    take(owns(a, entry_box(e1), k, cx, cy), e1.w);
+    take(owns(a, entry_box(e1), o), e1.w);
     if (cnt > 2) {
       const int4 e2 = s0[2], e3 = s0[3];
-      take(owns(a, entry_box(e2), k, cx, cy), e2.w);
-      take(cnt > 3 && owns(a, entry_box(e3), k, cx, cy), e3.w);
+      take(owns(a, entry_box(e2), o), e2.w);
+      take(cnt > 3 && owns(a, entry_box(e3), o), e3.w);
       if (cnt > kLevelSlots) {  // a crowded bucket: the higher levels, then the overflow chain
         const int ns = min(cnt, kSlots);
         for (int j = kLevelSlots; j < ns; j += kLevelSlots) {
           const int4* s = t.slot + t.at(b, j);
           const int4 f0 = s[0], f1 = s[1], f2 = s[2], f3 = s[3];
-          take(owns(a, entry_box(f0), k, cx, cy), f0.w);
-          take(j + 1 < ns && owns(a, entry_box(f1), k, cx, cy), f1.w);
-          take(j + 2 < ns && owns(a, entry_box(f2), k, cx, cy), f2.w);
-          take(j + 3 < ns && owns(a, entry_box(f3), k, cx, cy), f3.w);
+          take(owns(a, entry_box(f0), o), f0.w);
+          take(j + 1 < ns && owns(a, entry_box(f1), o), f1.w);
+          take(j + 2 < ns && owns(a, entry_box(f2), o), f2.w);
+          take(j + 3 < ns && owns(a, entry_box(f3), o), f3.w);
         }
         if (cnt > kSlots) {  // rare
-          int o = t.head[b];
+          int oi = t.head[b];
           for (int r = kSlots; r < cnt; r++) {
-            const int4 e = t.ovf[o];
-            take(owns(a, entry_box(e), k, cx, cy), e.w);
-            o = t.ovf_next[o];
+            const int4 e = t.ovf[oi];
+            take(owns(a, entry_box(e), o), e.w);
+            oi = t.ovf_next[oi];
           }
         }
       }
@@ -512,11 +525,13 @@ __global__ void __launch_bounds__(kProbeTile, SCCG_PROBE_MINB)
   int4 keep = make_int4(0, 0, 0, 0);
   if (act && !coop)
     probe_cells(a, g, t, [&](bool h, int q) {
-      keep.x = h && n == 0 ? q : keep.x;
-      keep.y = h && n == 1 ? q : keep.y;
-      keep.z = h && n == 2 ? q : keep.z;
-      keep.w = h && n == 3 ? q : keep.w;
-      n += h ? 1 : 0;
+      if (h) {  // rare (about one candidate in ten is owned): a branch, not selects per candidate
+        keep.x = n == 0 ? q : keep.x;
+        keep.y = n == 1 ? q : keep.y;
+        keep.z = n == 2 ? q : keep.z;
+        keep.w = n == 3 ? q : keep.w;
+        n++;
+      }
     });
   // Big MBRs of the whole tile (glands among nuclei, C3: often consecutive in
   // p): their (MBR, cell) visits are flattened over all the tile's threads --
