@@ -62,8 +62,10 @@ def launch_summary(path):
     # a P-only prep window followed by the Q prep + join + PixelBox window
     wins = [seq[a:b] for a, b in zip(idx, idx[1:])]
     has_join = [any("grid_select" in n for n, _ in w) for w in wins]
-    full = [wins[i] for i in range(1, len(wins)) if has_join[i] and has_join[i - 1]
-            and not any("small_kernel<1>" in n for n, _ in wins[i])]
+    # a timed step: only our kernels (no torch kernels of the untimed bookkeeping, no e2e decode), the join in it
+    clean = [not any(n.startswith("at::") or "decode" in n or "small_kernel<1>" in n or "void at::" in n
+                     for n, _ in w) for w in wins]
+    full = [wins[i] for i in range(1, len(wins)) if has_join[i] and has_join[i - 1] and clean[i]]
     step = full[-1] if full else seq
     out = ["one bench step (timed Pipeline), ncu --metrics gpu__time_duration.sum --clock-control none",
            "(cold caches, serialised: compare shares, not absolute times)", ""]
