@@ -116,6 +116,14 @@ def test_host_argument_checks():
     assert lib.sccg_filter_pairs(None, None, None, 0, ctypes.byref(n), None, 0, None) == sccg.E_ARG
     cfg = sccg.Config(-1, 0, 0, 0, None, None, None)
     assert lib.sccg_pixelbox(None, None, None, 0, None, None, None, ctypes.byref(cfg), None, 0, None) == sccg.E_ARG
+    # the compact-transfer decode and the index-pool sizer: argument checks (nothing enqueued)
+    assert lib.sccg_decode_rect(None, None, None, None, -1, None, None) == sccg.E_ARG
+    assert lib.sccg_decode_rect(None, None, None, None, 3, None, None) == sccg.E_ARG
+    assert lib.sccg_decode_rect(0x1004, 0x2000, 0x3000, 0x4000, 3, 0x5000, None) == sccg.E_ARG  # start misaligned
+    assert lib.sccg_decode_rect(0x1000, 0x2001, 0x3000, 0x4000, 3, 0x5000, None) == sccg.E_ARG  # move misaligned
+    assert lib.sccg_decode_rect(None, None, None, None, 0, None, None) == sccg.OK  # nothing to decode
+    assert lib.sccg_pixelbox_index_bytes(-1, 5) == 0
+    assert lib.sccg_pixelbox_index_bytes(100, 200) == 8 * 300 + (1 << 24)
 
 
 def test_jaccard_rejects_status_bits_and_new_entry_points():
