@@ -28,6 +28,9 @@ constexpr int kPrepThreads = SCCG_PREP_THREADS;
 constexpr int kPrepPolys = kPrepThreads;  // one ring per thread per tile
 static_assert(kPrepThreads % 32 == 0 && kPrepThreads <= 256, "whole warps; ring indices fit a byte");
 constexpr int kPrepVerts = SCCG_PREP_VERTS;
+#ifndef SCCG_PREP_RES_DEAL
+#define SCCG_PREP_RES_DEAL 1
+#endif
 #ifndef SCCG_PREP_USED_ONLY
 #define SCCG_PREP_USED_ONLY 0  // 1: write back only each ring's defined words, one bulk store per ring (measured slower: 177 vs 168 us on C2)
 #endif
@@ -557,6 +560,25 @@ __global__ void __launch_bounds__(kPrepThreads, SCCG_PREP_MINB) prep_kernel(cons
     __syncthreads();
     if (threadIdx.x < np) s_perm[s_cnt[key] + pos] = (unsigned char)threadIdx.x;
     __syncthreads();
+#if SCCG_PREP_RES_DEAL
+    // Within each warp's 32 rings (similar lengths, from the sort above), deal
+    // the rings to lanes by the shared-memory bank of their first vertex
+    // ((offset - v0) mod 16 vertices = 128 bytes): rings sorted by that residue
+    // go alternately to the two half-warps, so a half-warp's lockstep reads of
+    // vertex i of 16 rings mostly hit distinct bank pairs in the edge pass.
+    {
+      const int j = s_perm[threadIdx.x];
+      const int res = j != 0xff ? (int)((s_off[j] - v0) & 15) : 16;
+      int rank = 0;
+      for (int l = 0; l < 32; l++) {
+        const int rl = __shfl_sync(0xffffffffu, res, l);
+        rank += (rl < res || (rl == res && l < lane)) ? 1 : 0;
+      }
+      __syncwarp();
+      s_perm[warp * 32 + (rank & 1) * 16 + (rank >> 1)] = (unsigned char)j;
+      __syncthreads();
+    }
+#endif
 #if SCCG_PREP_L2_PREFETCH == 2
     if (threadIdx.x == 0) {
       // thread 0 (warp 0 deals the smallest rings, so it has slack) starts
