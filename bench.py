@@ -478,21 +478,22 @@ def run_ours(args, rank, world, local_rank):
     e2e = {"value": e2e_value, "unit": "pairs/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
            "steps": e2e_steps, "encoding": "plain int32 vertices"}
 
-    # the same through the compact rectilinear encoding (sccg_decode_rect): the
-    # host holds each ring as its first vertex plus int16 axis-alternating
-    # moves, a quarter of the vertex bytes over PCIe, decoded exactly on the GPU
-    enc = [sccg.encode_rect(S.xy, S.offsets) for S in (A, B)]
+    # the same through the packed rectilinear encoding (sccg_decode_rect_packed):
+    # the host holds each ring as a 16-bit head (vertex count, move width, first
+    # axis), its start as an int16 delta and its axis-alternating moves at 4, 8
+    # or 16 bits -- ~0.8 bytes per vertex over PCIe instead of 8, no offsets --
+    # decoded exactly on the GPU (offsets rebuilt by a block scan)
+    enc = [sccg.encode_rect_packed(S.xy, S.offsets) for S in (A, B)]
     e2e_plain = None
     if all(e is not None for e in enc):
-        cp = [[torch.from_numpy(a).pin_memory() for a in e] for e in enc]
-        h2d_c = sum(t.numel() * t.element_size() for e in cp for t in e) + off_p.numel() * 8 + off_q.numel() * 8
+        cp = [sccg.pin_packed(e) for e in enc]
+        h2d_c = sum(t.numel() * t.element_size() for e in cp for t in e.values())
 
         def e2e_compact_step():
             sets = []
-            for (st, mv, fv), off in zip(cp, (off_p, off_q)):
-                o = off.to(dev, non_blocking=True)
-                xy = sccg.decode_rect(st.to(dev, non_blocking=True), mv.to(dev, non_blocking=True),
-                                      fv.to(dev, non_blocking=True), o)
+            for e, S in zip(cp, (A, B)):
+                xy, o = sccg.decode_rect_packed({k: t.to(dev, non_blocking=True) for k, t in e.items()},
+                                                int(S.offsets[-1]))
                 sets.append(sccg.DeviceSet(xy, o))
             pr = sccg.filter_pairs(sets[0], sets[1], cap=cap)
             s = sccg.new_sums(dev)
@@ -505,7 +506,7 @@ def run_ours(args, rank, world, local_rank):
         if world == 1:
             # streamed: step i + 1's host -> device copy (copy stream) overlaps step i's decode and compute
             st = sccg.Streamer(A.n, int(A.offsets[-1]), B.n, int(B.offsets[-1]), cap=cap, threshold=args.threshold)
-            args_c = (cp[0], off_p, cp[1], off_q)
+            args_c = (cp[0], cp[1])
             st.result(st.submit(*args_c))  # warm-up (each slot's graph was captured at construction)
             torch.cuda.synchronize()
             e0.record(stream)
@@ -536,7 +537,8 @@ def run_ours(args, rank, world, local_rank):
         e2e_plain = e2e
         e2e = {"value": total_pairs * e2e_steps / (float(c_ms[0]) / 1e3), "unit": "pairs/s",
                "h2d_bytes_per_step": int(h2d_c), "d2h_bytes_per_step": int(d2h), "steps": e2e_steps,
-               "encoding": "compact rectilinear rings (first vertex + int16 moves), decoded by sccg_decode_rect",
+               "encoding": ("packed rectilinear rings (16-bit head, int16 start delta, 4/8/16-bit axis-alternating "
+                            "moves; no offsets), decoded by sccg_decode_rect_packed"),
                "pipelining": ("sccg.Streamer: each step's host -> device copy on a copy stream overlaps the previous "
                               "step's decode + step graph; every step's sums read back" if world == 1 else None)}
 
@@ -840,19 +842,18 @@ def run_study(args, rank, world, local_rank):
     # e2e: each image through the public API from pinned host memory (H2D of its inputs -- the base slide's
     # buffers: an image differs from its base only by an exact lattice symmetry, so the bytes moved and the
     # areas are the same), join, PixelBox, all-reduce, D2H of the sums
-    # (the compact rectilinear encoding when both sets of the base encode: a quarter of the vertex bytes)
+    # (the packed rectilinear encoding when both sets of the base encode: ~0.8 bytes per vertex, no offsets)
     e2e_steps = 1
     compact = {}
     for b in bases_needed:
-        ea, eb = (sccg.encode_rect(S.xy, S.offsets) for S in (ref[b]["A"], ref[b]["B"]))
+        ea, eb = (sccg.encode_rect_packed(S.xy, S.offsets) for S in (ref[b]["A"], ref[b]["B"]))
         if ea is not None and eb is not None:
-            compact[b] = [[torch.from_numpy(a).pin_memory() for a in e] for e in (ea, eb)]
+            compact[b] = [sccg.pin_packed(e) for e in (ea, eb)]
     h2d = 0
     for im in mine:
         b = im["base"]
         if b in compact:
-            h2d += sum(t.numel() * t.element_size() for e in compact[b] for t in e)
-            h2d += host[b][1].numel() * 8 + host[b][3].numel() * 8
+            h2d += sum(t.numel() * t.element_size() for e in compact[b] for t in e.values())
         else:
             h2d += sum(t.numel() * t.element_size() for t in host[b])
 
@@ -861,10 +862,10 @@ def run_study(args, rank, world, local_rank):
             a, o1, c, o2 = (t.to(dev, non_blocking=True) for t in host[b])
             return sccg.DeviceSet(a, o1), sccg.DeviceSet(c, o2)
         sets = []
-        for (st, mv, fv), off in zip(compact[b], (host[b][1], host[b][3])):
-            o = off.to(dev, non_blocking=True)
-            sets.append(sccg.DeviceSet(sccg.decode_rect(st.to(dev, non_blocking=True), mv.to(dev, non_blocking=True),
-                                                        fv.to(dev, non_blocking=True), o), o))
+        for e, S in zip(compact[b], (ref[b]["A"], ref[b]["B"])):
+            xy, o = sccg.decode_rect_packed({k: t.to(dev, non_blocking=True) for k, t in e.items()},
+                                            int(S.offsets[-1]))
+            sets.append(sccg.DeviceSet(xy, o))
         return sets
 
     def e2e_step():
@@ -921,7 +922,7 @@ def run_study(args, rank, world, local_rank):
                      "algorithmic_bytes_per_launch": alg_rank0 / max(1, len(mine)), "peak_source": peak_src},
         "e2e": {"value": e2e_value, "unit": "pairs/s", "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": len(sccg.SUMS_FIELDS) * 8, "steps": e2e_steps,
-                "encoding": "compact rectilinear rings (sccg_decode_rect)" if compact else "plain int32 vertices"},
+                "encoding": "packed rectilinear rings (sccg_decode_rect_packed)" if compact else "plain int32 vertices"},
         "gpu_launches": (LAUNCHES_PER_STEP - 1) * len(mine) * args.steps + (2 if world == 1 else 4) * args.steps,
         "clocks": clocks, "wall_s": wall1 - wall0,
     }

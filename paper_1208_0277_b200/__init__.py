@@ -40,6 +40,7 @@ SUMS_FIELDS = ("n_pairs", "n_nonzero", "sum_inter", "sum_union", "sum_area_p", "
 SYMBOLS = ("sccg_polyset_bytes", "sccg_polyset_bind", "sccg_prep", "sccg_prep_sets", "sccg_filter_workspace_bytes",
            "sccg_filter_pairs", "sccg_filter_pairs_closed", "sccg_filter_pairs_async", "sccg_touches", "sccg_pixelbox_workspace_bytes", "sccg_pixelbox_index_bytes", "sccg_pixelbox",
            "sccg_pixelbox_async", "sccg_count_missing", "sccg_contains", "sccg_report", "sccg_jaccard", "sccg_sums_copy", "sccg_decode_rect",
+           "sccg_decode_rect_packed",
            "sccg_sums_pack", "sccg_sums_unpack", "sccg_strerror", "sccg_last_error_string", "sccg_last_error_index",
            "sccg_version")
 STATUS_ARG, STATUS_NOT_RECTILINEAR, STATUS_RANGE, STATUS_STACK, STATUS_CAPACITY = 1, 2, 4, 8, 16
@@ -147,6 +148,8 @@ def load(build: bool = True):
         lib.sccg_pixelbox_index_bytes.restype = sz
         lib.sccg_decode_rect.argtypes = [vp, vp, vp, vp, i64, vp, vp]
         lib.sccg_decode_rect.restype = cint
+        lib.sccg_decode_rect_packed.argtypes = [vp, vp, vp, vp, i64, vp, vp, vp]
+        lib.sccg_decode_rect_packed.restype = cint
         lib.sccg_pixelbox.argtypes = [ps, ps, vp, i64, vp, vp, vp, ctypes.POINTER(Config), vp, sz, vp]
         lib.sccg_pixelbox.restype = cint
         lib.sccg_count_missing.argtypes = [vp, i64, vp, vp]
@@ -592,23 +595,25 @@ class Study:
 class Streamer:
     """End-to-end comparison of image pairs arriving in host memory, pipelined.
 
-    Each submitted pair of sets travels host -> device in the compact
-    rectilinear encoding (encode_rect: a quarter of the vertex bytes), is
-    decoded on the GPU (sccg_decode_rect) and runs the whole step (a Pipeline
-    graph: prep, join, PixelBox, the sums written into pinned host memory by
-    the GPU).  `depth` slots of device buffers rotate: the host -> device copy
-    of step i + 1 runs on a copy stream while step i computes, so a PCIe-bound
-    stream of images moves at the link's speed.  Shapes are fixed per slot
-    (n polygons and vertices of each set, as in the first submit's sizes).
+    Each submitted pair of sets travels host -> device in the packed
+    rectilinear encoding (encode_rect_packed: ~0.8 bytes per vertex instead of
+    8, and no offsets), is decoded on the GPU (sccg_decode_rect_packed, which
+    also rebuilds the offsets) and runs the whole step (a Pipeline graph: prep,
+    join, PixelBox, the sums written into pinned host memory by the GPU).
+    `depth` slots of device buffers rotate: the host -> device copy of step
+    i + 1 runs on a copy stream while step i computes, so a PCIe-bound stream
+    of images moves at the link's speed.  Shapes are fixed per slot (n
+    polygons and vertices of each set); the encoded buffers grow as needed.
 
         st = Streamer(A.n, A.nv, B.n, B.nv)
-        t = st.submit(encoded_a, off_a, encoded_b, off_b)   # pinned host tensors
-        sums = st.result(t)                                  # waits for that step"""
+        t = st.submit(packed_a, packed_b)   # encode_rect_packed dicts of pinned tensors
+        sums = st.result(t)                 # waits for that step"""
 
     def __init__(self, n_p: int, nv_p: int, n_q: int, nv_q: int, cap: int | None = None, threshold: int = 0,
                  depth: int = 2, device=None):
         torch = _torch()
         dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.device = dev
         self.depth = depth
         self.shapes = (n_p, nv_p, n_q, nv_q)
         cap = int(cap) if cap is not None else 3 * max(n_p, n_q) + 1024
@@ -616,11 +621,9 @@ class Streamer:
         for _ in range(depth):
             sl = {}
             for side, n, nv in (("p", n_p, nv_p), ("q", n_q, nv_q)):
-                sl["start_" + side] = torch.empty((max(n, 1), 2), dtype=torch.int32, device=dev)
-                sl["move_" + side] = torch.empty(max(nv - n, 1), dtype=torch.int16, device=dev)
-                sl["fv_" + side] = torch.empty(max(n, 1), dtype=torch.uint8, device=dev)
                 sl["off_" + side] = torch.zeros(n + 1, dtype=torch.int64, device=dev)
                 sl["xy_" + side] = torch.empty((max(nv, 1), 2), dtype=torch.int32, device=dev)
+                sl["enc_" + side] = {}
             sl["rb"] = torch.zeros(len(SUMS_FIELDS), dtype=torch.int64).pin_memory()
             P = DeviceSet(sl["xy_p"][:nv_p], sl["off_p"], prep=False)
             Q = DeviceSet(sl["xy_q"][:nv_q], sl["off_q"], prep=False)
@@ -631,33 +634,34 @@ class Streamer:
         self.copy_stream = torch.cuda.Stream(device=dev)
         self.count = 0
 
-    def _decode(self, sl):
-        for side in ("p", "q"):
-            n = int(sl["off_" + side].numel()) - 1
-            _check(load().sccg_decode_rect(sl["start_" + side].data_ptr(), sl["move_" + side].data_ptr(),
-                                           sl["fv_" + side].data_ptr(), sl["off_" + side].data_ptr(), n,
-                                           sl["xy_" + side].data_ptr(), _stream_ptr()), "sccg_decode_rect")
-
-    def submit(self, enc_p, off_p, enc_q, off_q) -> int:
-        """Enqueue one step for host sets given as encode_rect tuples (start,
-        move, first_vertical) of pinned CPU tensors plus their offsets.  Returns
-        a ticket for result()."""
+    def submit(self, enc_p, enc_q) -> int:
+        """Enqueue one step for host sets given as encode_rect_packed dicts of
+        (pinned) CPU tensors.  Returns a ticket for result()."""
         torch = _torch()
         k = self.count % self.depth
         sl = self.slots[k]
         main = torch.cuda.current_stream()
         cs = self.copy_stream
         cs.wait_event(sl["done"])  # the slot's previous step no longer reads its buffers
+        n_p, nv_p, n_q, nv_q = self.shapes
+        views = {}
         with torch.cuda.stream(cs):
-            for side, (st, mv, fv), off in (("p", enc_p, off_p), ("q", enc_q, off_q)):
-                sl["start_" + side][: st.shape[0]].copy_(st, non_blocking=True)
-                if mv.numel():
-                    sl["move_" + side][: mv.shape[0]].copy_(mv, non_blocking=True)
-                sl["fv_" + side][: fv.shape[0]].copy_(fv, non_blocking=True)
-                sl["off_" + side].copy_(off, non_blocking=True)
+            for side, enc, n in (("p", enc_p, n_p), ("q", enc_q, n_q)):
+                if int(enc["head"].numel()) != n:
+                    raise ValueError(f"Streamer: set {side} has {int(enc['head'].numel())} rings, the slots {n}")
+                buf, v = sl["enc_" + side], {}
+                for key, t in enc.items():
+                    if key not in buf or buf[key].numel() < t.numel():
+                        buf[key] = torch.empty(max(t.numel(), 1), dtype=t.dtype, device=self.device)
+                    d = buf[key].view(-1)[: t.numel()].view(t.shape)
+                    if t.numel():
+                        d.copy_(t, non_blocking=True)
+                    v[key] = d
+                views[side] = v
             sl["copied"].record(cs)
         main.wait_event(sl["copied"])
-        self._decode(sl)
+        for side, nv in (("p", nv_p), ("q", nv_q)):
+            decode_rect_packed(views[side], nv, out=(sl["xy_" + side], sl["off_" + side]))
         sl["pipe"].run(slot=0)
         sl["done"].record(main)
         self.count += 1
@@ -671,6 +675,14 @@ class Streamer:
         sl = self.slots[ticket % self.depth]
         sl["done"].synchronize()
         return sums_to_host(sl["rb"])
+
+
+def pin_packed(enc):
+    """An encode_rect_packed dict as pinned CPU tensors (Streamer.submit's input)."""
+    import numpy as np
+
+    torch = _torch()
+    return {k: torch.from_numpy(np.ascontiguousarray(v)).pin_memory() for k, v in enc.items()}
 
 
 def touches(P: DeviceSet, Q: DeviceSet, pairs, inter, stream=None):
@@ -897,6 +909,114 @@ def decode_rect(start, move, first_vertical, offsets, stream=None):
                                    first_vertical.data_ptr(), offsets.data_ptr(), n, xy.data_ptr(), _stream_ptr(stream)),
            "sccg_decode_rect")
     return xy[:nv]
+
+
+RECTP_BLOCK = 256  # SCCG_RECTP_BLOCK
+
+
+def encode_rect_packed(xy, offsets):
+    """Packed rectilinear rings (sccg_decode_rect_packed, format 2 in
+    include/sccg.h): dict of numpy arrays head uint16 [n], start int16 [...],
+    units uint16 [...], block int64 [ceil(n / 256), 4] -- each ring's moves at
+    the narrowest of 4, 8 or 16 bits, starts as int16 deltas from the block's
+    first start where they fit, no offsets.  None when some ring is not
+    encodable (more than 8191 vertices, a zero-length or non-alternating move,
+    a move beyond int16).  Host-side numpy; lossless: the device decode is
+    exact.  Rings with 0 vertices are allowed."""
+    import numpy as np
+
+    xy = np.asarray(xy, np.int64).reshape(-1, 2)
+    off = np.asarray(offsets, np.int64)
+    n = off.shape[0] - 1
+    V = np.diff(off)
+    if n < 0 or (V < 0).any() or (V > 8191).any():
+        return None
+    m = np.maximum(V - 1, 0)  # moves per ring
+    nm = int(m.sum())
+    ring = np.repeat(np.arange(n), m)
+    # move j of ring i: xy[off[i] + j + 1] - xy[off[i] + j]
+    mstart = np.cumsum(m) - m
+    j = np.arange(nm) - np.repeat(mstart, m)
+    src = np.repeat(off[:-1], m) + j
+    d = xy[src + 1] - xy[src] if nm else np.zeros((0, 2), np.int64)
+    if ((d[:, 0] != 0) == (d[:, 1] != 0)).any():  # exactly one coordinate changes
+        return None
+    ymove = d[:, 0] == 0
+    fv = np.zeros(n, np.int64)
+    has = m > 0
+    fv[has] = ymove[mstart[has]]
+    if (ymove != (((j & 1) == 0) == (fv[ring] == 1))).any():  # the axes alternate
+        return None
+    mv = np.where(ymove, d[:, 1], d[:, 0])
+    a = np.abs(mv)
+    if nm and a.max() > 32767:
+        return None
+    amax = np.zeros(n, np.int64)
+    if nm:
+        np.maximum.at(amax, ring, a)
+    w = np.where(amax <= 8, 0, np.where(amax <= 128, 1, 2))
+    c = np.array([4, 2, 1])[w]
+    nu = (m + c - 1) // c
+    u0 = np.cumsum(nu) - nu  # global unit offset of each ring
+    head = (V | (w << 13) | (fv << 15)).astype(np.uint16)
+    # units: 4-bit nibbles of a flat array, 4 per unit
+    nib = np.zeros(4 * int(nu.sum()), np.int64)
+    wr, cr = w[ring], c[ring]
+    pos = 4 * (u0[ring] + j // cr) + (j % cr) * (4 // cr)
+    small = wr < 2
+    bits = np.where(wr == 0, 4, 8)
+    code = np.where(mv < 0, 1, 0) << (bits - 1) | (a - 1)
+    for k in range(2):  # an 8-bit code spans two nibbles
+        sel = small & ((wr == 1) | (k == 0))
+        nib[pos[sel] + k] = (code[sel] >> (4 * k)) & 15
+    big = ~small
+    v16 = mv[big] & 0xFFFF
+    for k in range(4):
+        nib[pos[big] + k] = (v16 >> (4 * k)) & 15
+    units = (nib[0::4] | nib[1::4] << 4 | nib[2::4] << 8 | nib[3::4] << 12).astype(np.uint16)
+    # starts: per block of RECTP_BLOCK rings, int16 deltas from its first start or int32 pairs
+    nb = (n + RECTP_BLOCK - 1) // RECTP_BLOCK
+    block = np.zeros((max(nb, 0), 4), np.int64)
+    st = np.zeros((n, 2), np.int64)
+    st[V > 0] = xy[off[:-1][V > 0]]
+    parts, soff = [], 0
+    for b in range(nb):
+        lo, hi = b * RECTP_BLOCK, min(n, (b + 1) * RECTP_BLOCK)
+        s = st[lo:hi]
+        x0, y0 = int(s[0, 0]), int(s[0, 1])
+        dd = s - np.array([x0, y0])
+        wide = bool((np.abs(dd) > 32767).any())
+        if wide:
+            p = (s.astype(np.int64) & 0xFFFFFFFF)
+            part = np.stack([p[:, 0] & 0xFFFF, p[:, 0] >> 16, p[:, 1] & 0xFFFF, p[:, 1] >> 16], 1).reshape(-1)
+        else:
+            part = (dd & 0xFFFF).reshape(-1)
+        org = (x0 & 0xFFFFFFFF) | ((y0 & 0xFFFFFFFF) << 32)
+        block[b] = (off[lo], u0[lo], soff | (int(wide) << 62), org - (1 << 64) if org >= 1 << 63 else org)
+        parts.append(part.astype(np.uint16))
+        soff += part.shape[0]
+    start = (np.concatenate(parts) if parts else np.zeros(0, np.uint16)).view(np.int16)
+    return dict(head=head, start=start, units=units, block=block)
+
+
+def decode_rect_packed(enc, n_vertices: int, stream=None, out=None):
+    """sccg_decode_rect_packed on device tensors (the dict of encode_rect_packed
+    moved to the device): returns (xy int32 [V, 2], offsets int64 [n + 1]).
+    out = (xy, offsets) device buffers to fill instead of allocating."""
+    torch = _torch()
+    head = enc["head"]
+    n = int(head.numel())
+    dev = head.device
+    if out is None:
+        xy = torch.empty((max(n_vertices, 1), 2), dtype=torch.int32, device=dev)
+        off = torch.empty(n + 1, dtype=torch.int64, device=dev)
+    else:
+        xy, off = out
+    ptr = lambda t: t.data_ptr() if t.numel() else None  # noqa: E731
+    _check(load().sccg_decode_rect_packed(ptr(head), ptr(enc["start"]), ptr(enc["units"]), ptr(enc["block"]), n,
+                                          off.data_ptr(), xy.data_ptr(), _stream_ptr(stream)),
+           "sccg_decode_rect_packed")
+    return xy[:n_vertices], off
 
 
 def to_device(xy, offsets, device="cuda", non_blocking=True):

@@ -190,3 +190,105 @@ def test_encode_rect_roundtrip_and_rejects(tile_sets):
                 [[0, 0], [40000, 0], [40000, 3], [0, 3]]):  # move beyond int16
         Q = synth.pack([sq, bad])
         assert sccg.encode_rect(Q.xy, Q.offsets) is None
+
+
+def _decode_rect_packed_host(enc, n):
+    """Plain loop reading of the packed format as include/sccg.h states it
+    (sccg_decode_rect_packed): returns (xy, offsets)."""
+    head, start, units, block = (enc[k] for k in ("head", "start", "units", "block"))
+    start_u = start.view(np.uint16)
+    offs, xy = [0], []
+    for b in range((n + sccg.RECTP_BLOCK - 1) // sccg.RECTP_BLOCK):
+        v_off, u, sw, org = (int(t) for t in block[b])
+        org &= (1 << 64) - 1
+        assert v_off == offs[-1]
+        wide, s = (sw >> 62) & 1, sw & ((1 << 62) - 1)
+        x0 = int(np.uint32(org & 0xFFFFFFFF).view(np.int32))
+        y0 = int(np.uint32((org >> 32) & 0xFFFFFFFF).view(np.int32))
+        for jr in range(min(sccg.RECTP_BLOCK, n - b * sccg.RECTP_BLOCK)):
+            h = int(head[b * sccg.RECTP_BLOCK + jr])
+            V, wc, vert = h & 0x1FFF, (h >> 13) & 3, h >> 15
+            if wide:
+                q = [int(t) for t in start_u[s + 4 * jr: s + 4 * jr + 4]]
+                x = int(np.uint32(q[0] | q[1] << 16).view(np.int32))
+                y = int(np.uint32(q[2] | q[3] << 16).view(np.int32))
+            else:
+                x, y = x0 + int(start[s + 2 * jr]), y0 + int(start[s + 2 * jr + 1])
+            c = (4, 2, 1)[wc]
+            bits = 16 // c
+            if V > 0:
+                xy.append((x, y))
+            for k in range(1, V):
+                jm = k - 1
+                word = int(units[u + jm // c])
+                code = (word >> (bits * (jm % c))) & ((1 << bits) - 1)
+                if bits == 16:
+                    dv = code - (1 << 16) if code >= 1 << 15 else code
+                else:
+                    mag = (code & ((1 << (bits - 1)) - 1)) + 1
+                    dv = -mag if code >> (bits - 1) else mag
+                if ((k & 1) == 1) == (vert == 1):
+                    y += dv
+                else:
+                    x += dv
+                xy.append((x, y))
+            u += (V - 1 + c - 1) // c if V > 1 else 0
+            offs.append(offs[-1] + V)
+    return np.array(xy, np.int64).reshape(-1, 2), np.array(offs, np.int64)
+
+
+def _rect_ring(rng, x0, y0, steps, big=1):
+    """A closed rectilinear ring-like vertex walk (not necessarily simple --
+    the encoding does not care): alternating axis moves, nonzero."""
+    pts = [(x0, y0)]
+    x, y = x0, y0
+    for k in range(steps):
+        d = int(rng.integers(1, big + 1)) * (1 if rng.random() < 0.5 else -1)
+        if k % 2 == 0:
+            x += d
+        else:
+            y += d
+        pts.append((x, y))
+    return pts
+
+
+def test_encode_rect_packed_roundtrip_and_rejects(tile_sets):
+    """The packed rectilinear encoding (sccg_decode_rect_packed's input),
+    against a plain reading of the header's layout: lossless on the tile sets,
+    on rings whose moves need 4, 8 and 16 bits, on blocks whose starts need
+    int32 (wide) and on empty rings / a partial last block / no rings; rings it
+    cannot express are refused."""
+    import synth
+
+    for S in tile_sets:
+        enc = sccg.encode_rect_packed(S.xy, S.offsets)
+        xy, off = _decode_rect_packed_host(enc, S.n)
+        assert np.array_equal(off, S.offsets) and np.array_equal(xy, S.xy)
+        assert enc["units"].nbytes < 0.3 * S.xy.nbytes  # ~ 4-bit moves
+        assert ((enc["head"] >> 13 & 3) == 0).mean() > 0.5  # most rings: 4-bit moves
+    rng = np.random.default_rng(7)
+    rings = []
+    for i in range(700):  # > 2 blocks, the last partial
+        big = (1, 8, 9, 128, 129, 32767)[i % 6]
+        x0 = int(rng.integers(-2**30, 2**30)) if i == 300 else 5000 + int(rng.integers(-10000, 10000))
+        rings.append(_rect_ring(rng, x0, int(rng.integers(-5000, 5000)), int(rng.integers(0, 40)) * 2 + 3, big))
+    rings[3] = rings[3][::-1]
+    P = synth.pack(rings)
+    # empty rings in the middle: offsets repeat
+    off = np.concatenate([P.offsets[:10], P.offsets[9:300], P.offsets[299:]])
+    enc = sccg.encode_rect_packed(P.xy, off)
+    n = len(off) - 1
+    xy, off2 = _decode_rect_packed_host(enc, n)
+    assert np.array_equal(off2, off) and np.array_equal(xy, P.xy)
+    widths = set(((enc["head"] >> 13) & 3).tolist())
+    assert widths == {0, 1, 2}
+    assert any((enc["block"][:, 2] >> 62) & 1) and not all((enc["block"][:, 2] >> 62) & 1)
+    e0 = sccg.encode_rect_packed(np.zeros((0, 2), np.int32), np.zeros(1, np.int64))
+    assert e0["head"].size == 0 and e0["block"].shape == (0, 4)
+    sq = [[0, 0], [5, 0], [5, 3], [0, 3]]
+    for bad in ([[0, 0], [0, 0], [5, 0], [5, 3], [0, 3]],  # duplicate vertex
+                [[0, 0], [2, 0], [5, 0], [5, 3], [0, 3]],  # collinear vertex
+                [[0, 0], [40000, 0], [40000, 3], [0, 3]],  # move beyond int16
+                _rect_ring(rng, 0, 0, 8191)):  # 8192 vertices
+        Q = synth.pack([sq, bad])
+        assert sccg.encode_rect_packed(Q.xy, Q.offsets) is None

@@ -968,6 +968,54 @@ def test_decode_rect_exact(sccg, config):
         assert torch.equal(s0, s1)
 
 
+def _packed_to_device(enc):
+    return {k: torch.from_numpy(np.ascontiguousarray(v)).cuda() for k, v in enc.items()}
+
+
+@pytest.mark.parametrize("config", ["tile", "combs", "slide", "edge"])
+def test_decode_rect_packed_exact(sccg, config):
+    """sccg_decode_rect_packed (format 2: per-ring 4/8/16-bit moves, int16 start
+    deltas, offsets rebuilt on the device) reproduces the plain rings and their
+    offsets exactly -- including moves of every width, wide start blocks, empty
+    rings and a partial last block -- and the path from it gives the same sums."""
+    if config == "combs":
+        A, B = combs.generate(n_pairs=64)
+        sets = (A, B)
+    elif config == "edge":
+        from test_abi import _rect_ring
+
+        rng = np.random.default_rng(11)
+        rings = [_rect_ring(rng, int(rng.integers(-2**30, 2**30)) if i == 300 else int(rng.integers(-9000, 9000)),
+                         int(rng.integers(-5000, 5000)), int(rng.integers(0, 60)) * 2 + 3,
+                         (1, 8, 9, 128, 129, 32767)[i % 6]) for i in range(777)]
+        rings.append(_rect_ring(rng, 0, 0, 8189, 3))  # 8190 vertices, the largest count a head holds
+        P = synth.pack(rings)
+        off = np.concatenate([P.offsets[:10], P.offsets[9:300], P.offsets[299:]])  # an empty ring
+        sets = ((P.xy, off),)
+    else:
+        A, B = synth.generate(config)
+        sets = (A, B)
+    for S in sets:
+        xy_h, off_h = (S if isinstance(S, tuple) else (S.xy, S.offsets))
+        enc = sccg.encode_rect_packed(xy_h, off_h)
+        assert enc is not None
+        xy, off = sccg.decode_rect_packed(_packed_to_device(enc), int(off_h[-1]))
+        assert torch.equal(off.cpu(), torch.from_numpy(np.asarray(off_h, np.int64)))
+        assert torch.equal(xy.cpu(), torch.from_numpy(np.asarray(xy_h, np.int32)))
+    # no rings: offsets[0] = 0
+    e0 = sccg.encode_rect_packed(np.zeros((0, 2), np.int32), np.zeros(1, np.int64))
+    out = (torch.empty((1, 2), dtype=torch.int32, device="cuda"), torch.full((1,), 7, dtype=torch.int64, device="cuda"))
+    _, off0 = sccg.decode_rect_packed(_packed_to_device(e0), 0, out=out)
+    assert off0.tolist() == [0]
+    if config == "tile":
+        P0, Q0 = dev(A, sccg), dev(B, sccg)
+        dec = [sccg.DeviceSet(*sccg.decode_rect_packed(_packed_to_device(sccg.encode_rect_packed(S.xy, S.offsets)),
+                                                       int(S.offsets[-1]))) for S in (A, B)]
+        _, _, s0 = sccg.pixelbox(P0, Q0, sccg.filter_pairs(P0, Q0))
+        _, _, s1 = sccg.pixelbox(dec[0], dec[1], sccg.filter_pairs(dec[0], dec[1]))
+        assert torch.equal(s0, s1)
+
+
 def _study_rank(rank, world, port, out):
     import os
     import sys
@@ -1034,7 +1082,7 @@ def test_study_gloo_ranks_bit_identical(sccg):
 
 
 def test_streamer_matches_pipeline(sccg):
-    """sccg.Streamer (compact host -> device transfer on a copy stream, decode,
+    """sccg.Streamer (packed host -> device transfer on a copy stream, decode,
     the step graph, read-back; two slots in flight): every step's sums equal
     the device-resident Pipeline's for the same sets, steps of two different
     images interleaved."""
@@ -1045,15 +1093,14 @@ def test_streamer_matches_pipeline(sccg):
         pipe = sccg.Pipeline(P, Q, graph=False)
         pipe.run()
         torch.cuda.synchronize()
-        enc = [[torch.from_numpy(a).pin_memory() for a in sccg.encode_rect(S.xy, S.offsets)] for S in (A, B)]
-        offs = [torch.from_numpy(S.offsets).pin_memory() for S in (A, B)]
-        imgs.append((A, B, enc, offs, pipe.sums.cpu().tolist()))
+        enc = [sccg.pin_packed(sccg.encode_rect_packed(S.xy, S.offsets)) for S in (A, B)]
+        imgs.append((A, B, enc, pipe.sums.cpu().tolist()))
     # one Streamer per shape (slots are shaped by the first sets); same-shaped repeats of each image
-    for A, B, enc, offs, ref in imgs:
+    for A, B, enc, ref in imgs:
         st = sccg.Streamer(A.n, int(A.offsets[-1]), B.n, int(B.offsets[-1]))
-        tickets = [st.submit(enc[0], offs[0], enc[1], offs[1]) for _ in range(2)]
+        tickets = [st.submit(enc[0], enc[1]) for _ in range(2)]
         got = [st.result(t) for t in tickets]
-        tickets = [st.submit(enc[0], offs[0], enc[1], offs[1]) for _ in range(2)]
+        tickets = [st.submit(enc[0], enc[1]) for _ in range(2)]
         got += [st.result(t) for t in tickets]
         for g in got:
             assert [getattr(g, f) for f in sccg.SUMS_FIELDS] == ref
