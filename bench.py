@@ -505,19 +505,23 @@ def run_ours(args, rank, world, local_rank):
 
         if world == 1:
             # streamed: step i + 1's host -> device copy (copy stream) overlaps step i's decode and compute
-            st = sccg.Streamer(A.n, int(A.offsets[-1]), B.n, int(B.offsets[-1]), cap=cap, threshold=args.threshold)
+            # three slots: the host reads step i - 2's result while steps i - 1 and i are in flight, so
+            # enqueueing (Python) never delays the next copy
+            st = sccg.Streamer(A.n, int(A.offsets[-1]), B.n, int(B.offsets[-1]), cap=cap, threshold=args.threshold,
+                               depth=3)
             args_c = (cp[0], cp[1])
-            st.result(st.submit(*args_c))  # warm-up (each slot's graph was captured at construction)
+            for _ in range(st.depth):  # warm-up: every slot once (each slot's graph was captured at construction)
+                st.result(st.submit(*args_c))
             torch.cuda.synchronize()
             e0.record(stream)
             st.copy_stream.wait_event(e0)  # the first copy starts inside the timed region
-            prev = None
+            inflight = []
             for _ in range(e2e_steps):
-                t = st.submit(*args_c)
-                if prev is not None:
-                    jc, _ = sccg.jaccard(st.result(prev))
-                prev = t
-            jc, _ = sccg.jaccard(st.result(prev))
+                inflight.append(st.submit(*args_c))
+                if len(inflight) == st.depth:
+                    jc, _ = sccg.jaccard(st.result(inflight.pop(0)))
+            for t in inflight:
+                jc, _ = sccg.jaccard(st.result(t))
             e1.record(stream)
             torch.cuda.synchronize()
         else:

@@ -84,71 +84,30 @@ __host__ __device__ __forceinline__ int rp_units(int m, int w) {  // 16-bit unit
   return w == 0 ? (m + 3) >> 2 : w == 1 ? (m + 1) >> 1 : m;
 }
 
-// One ring by one warp, C moves of BITS bits per 16-bit unit: a pass decodes
-// 32 units (lane j unit j), lane-local prefix sums split into x and y (move i
-// leads to vertex i + 1, which changes y iff (i + 1 odd) == vert), a warp scan
-// of the lane totals, the pass's vertices staged in shared memory and stored
-// coalesced.
-template <int C, int BITS>
-__device__ __forceinline__ void rp_ring(const unsigned short* __restrict__ up, int m, int vert, int cx, int cy,
-                                        int2* __restrict__ dst, int2* stg) {
-  const int lane = threadIdx.x & 31;
-  const int nu = (m + C - 1) / C;
-  for (int p0 = 0; p0 < nu; p0 += 32) {  // warp-uniform
-    const int ui = p0 + lane;
-    const unsigned u = ui < nu ? (unsigned)up[ui] : 0u;
-    int px[C], py[C], sx = 0, sy = 0;
-#pragma unroll
-    for (int t = 0; t < C; t++) {
-      int d;
-      if (BITS == 16) {
-        d = (int)(short)(u & 0xffffu);
-      } else {
-        const unsigned c = (u >> (BITS * t)) & ((1u << BITS) - 1u);
-        const int mag = (int)(c & ((1u << (BITS - 1)) - 1u)) + 1;
-        d = (c >> (BITS - 1)) ? -mag : mag;
-      }
-      const int i = ui * C + t;
-      if (i >= m) d = 0;
-      const bool ymove = ((i & 1) == 0) == (vert != 0);
-      sx += ymove ? 0 : d;
-      sy += ymove ? d : 0;
-      px[t] = sx;
-      py[t] = sy;
-    }
-    int ex = sx, ey = sy;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int a = __shfl_up_sync(0xffffffffu, ex, o), b = __shfl_up_sync(0xffffffffu, ey, o);
-      if (lane >= o) {
-        ex += a;
-        ey += b;
-      }
-    }
-    const int tx = __shfl_sync(0xffffffffu, ex, 31), ty = __shfl_sync(0xffffffffu, ey, 31);
-    ex += cx - sx;  // this lane's first move starts from here
-    ey += cy - sy;
-#pragma unroll
-    for (int t = 0; t < C; t++) stg[lane * C + t] = make_int2(ex + px[t], ey + py[t]);
-    __syncwarp();
-    const int base = p0 * C, cnt = min(32 * C, m - base);
-    for (int t = lane; t < cnt; t += 32) dst[base + t] = stg[t];
-    __syncwarp();
-    cx += tx;
-    cy += ty;
-  }
-}
+// Staging capacity: a block's vertices (thread per ring, ~8.7 k vertices for
+// 256 nucleus rings) are assembled in shared memory and leave by coalesced
+// stores; its move units arrive by one coalesced pass.  Rings past either
+// capacity (blocks of very long rings) read / write global memory directly.
+constexpr int kRpStage = 7168;  // int2 vertices (56 KB)
+constexpr int kRpUnits = 4096;  // 16-bit units (8 KB)
+constexpr size_t kRpSmem = kRpStage * sizeof(int2) + kRpUnits * sizeof(unsigned short);
 }  // namespace
 
+// CTA per block of kRpBlock rings, thread per ring: heads -> block scan of
+// (vertices, units) -> the block's offsets; units staged; each thread walks
+// its ring's moves (vertex k >= 1 changes y iff (k odd) == the first-vertical
+// bit; the width class selects 4, 2 or 1 moves per unit) writing vertices into
+// the staged block; the staged range is stored coalesced.
 __global__ void __launch_bounds__(kRpBlock) decode_rect_packed_kernel(const unsigned short* __restrict__ head,
                                                                       const short* __restrict__ start,
                                                                       const unsigned short* __restrict__ units,
                                                                       const long long* __restrict__ block, int64_t n,
                                                                       int64_t* __restrict__ off, int2* __restrict__ xy) {
-  __shared__ int s_v[kRpBlock], s_u[kRpBlock], s_h[kRpBlock];
-  __shared__ int2 s_s[kRpBlock];
+  extern __shared__ __align__(16) unsigned char rp_smem[];
+  int2* s_stage = reinterpret_cast<int2*>(rp_smem);
+  unsigned short* s_units = reinterpret_cast<unsigned short*>(rp_smem + kRpStage * sizeof(int2));
   __shared__ int s_warp[2][kRpWarps];
-  __shared__ int2 s_stage[kRpWarps][128];
+  __shared__ int s_lim;
   pdl_entry();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t b = blockIdx.x, r = b * kRpBlock + threadIdx.x;
@@ -159,9 +118,7 @@ __global__ void __launch_bounds__(kRpBlock) decode_rect_packed_kernel(const unsi
   const long long vbase = block[4 * b], ubase = block[4 * b + 1], sw = block[4 * b + 2], org = block[4 * b + 3];
   const bool wide = (sw >> 62) & 1;
   const long long soff = sw & ((1ll << 62) - 1);
-  // ring head, start and unit count; block scan of (vertices, units)
-  int V = 0, nu = 0, h = 0;
-  int2 s0 = make_int2(0, 0);
+  int V = 0, nu = 0, h = 0, x = 0, y = 0;
   if (r < n) {
     h = head[r];
     V = h & 0x1fff;
@@ -169,12 +126,14 @@ __global__ void __launch_bounds__(kRpBlock) decode_rect_packed_kernel(const unsi
     const int j = threadIdx.x;
     if (wide) {
       const unsigned short* sp = reinterpret_cast<const unsigned short*>(start) + soff + 4 * j;
-      s0 = make_int2((int)((unsigned)sp[0] | ((unsigned)sp[1] << 16)), (int)((unsigned)sp[2] | ((unsigned)sp[3] << 16)));
+      x = (int)((unsigned)sp[0] | ((unsigned)sp[1] << 16));
+      y = (int)((unsigned)sp[2] | ((unsigned)sp[3] << 16));
     } else {
-      s0 = make_int2((int)(unsigned)(org & 0xffffffffll) + start[soff + 2 * j],
-                     (int)(unsigned)((unsigned long long)org >> 32) + start[soff + 2 * j + 1]);
+      x = (int)(unsigned)(org & 0xffffffffll) + start[soff + 2 * j];
+      y = (int)(unsigned)((unsigned long long)org >> 32) + start[soff + 2 * j + 1];
     }
   }
+  // block scan of (vertices, units)
   int xv = V, xu = nu;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
@@ -188,47 +147,62 @@ __global__ void __launch_bounds__(kRpBlock) decode_rect_packed_kernel(const unsi
     s_warp[0][warp] = xv;
     s_warp[1][warp] = xu;
   }
+  if (threadIdx.x == 0) s_lim = INT_MAX;
   __syncthreads();
-  int bv = 0, bu = 0;
-  for (int w = 0; w < warp; w++) {
-    bv += s_warp[0][w];
-    bu += s_warp[1][w];
+  int bv = 0, bu = 0, tv = 0, tu = 0;
+  for (int w = 0; w < kRpWarps; w++) {
+    bv += w < warp ? s_warp[0][w] : 0;
+    bu += w < warp ? s_warp[1][w] : 0;
+    tv += s_warp[0][w];
+    tu += s_warp[1][w];
   }
-  s_v[threadIdx.x] = bv + xv - V;
-  s_u[threadIdx.x] = bu + xu - nu;
-  s_h[threadIdx.x] = h;
-  s_s[threadIdx.x] = s0;
+  const int v0 = bv + xv - V, u0 = bu + xu - nu;  // this ring's vertex / unit offsets in the block
   if (r < n) {
-    off[r] = vbase + bv + xv - V;
-    if (r == n - 1) off[n] = vbase + bv + xv;
+    off[r] = vbase + v0;
+    if (r == n - 1) off[n] = vbase + v0 + V;
+  }
+  const bool staged = v0 + V <= kRpStage;
+  if (r < n && !staged) atomicMin(&s_lim, v0);
+  // the block's units, coalesced
+  const int nus = min(tu, kRpUnits);
+  for (int i = threadIdx.x; i < nus; i += kRpBlock) s_units[i] = units[ubase + i];
+  __syncthreads();
+  if (r < n && V > 0) {
+    const int w = (h >> 13) & 3, vert = h >> 15;
+    const int lc = w == 0 ? 2 : w == 1 ? 1 : 0;  // log2(moves per unit)
+    const int bits = 16 >> lc;
+    const unsigned mask = bits == 16 ? 0xffffu : (1u << bits) - 1u, mmag = mask >> 1;
+    const unsigned short* up = u0 + nu <= kRpUnits ? s_units + u0 : units + ubase + u0;
+    int2* dst = staged ? s_stage + v0 : xy + vbase + v0;
+    dst[0] = make_int2(x, y);
+    const int cm = (1 << lc) - 1;
+    unsigned cur = 0u;
+    for (int k = 1; k < V; k++) {
+      const int mi = k - 1;
+      if ((mi & cm) == 0) cur = up[mi >> lc];  // a unit is read once (predicated, not per move)
+      const unsigned code = (cur >> ((mi & cm) * bits)) & mask;
+      const int mag = (int)(code & mmag) + 1;
+      const int d = bits == 16 ? (int)(short)code : ((code > mmag) ? -mag : mag);
+      const bool ymove = (k & 1) == vert;
+      x += ymove ? 0 : d;
+      y += ymove ? d : 0;
+      dst[k] = make_int2(x, y);
+    }
   }
   __syncthreads();
-  // warp per ring: a pass decodes 32 units (up to 128 moves), lane j unit j;
-  // lane-local prefix sums, a warp scan of the lane totals, vertices staged in
-  // shared memory and stored coalesced
-  const int nr = (int)min((int64_t)kRpBlock, n - b * kRpBlock);
-  int2* stg = s_stage[warp];
-  for (int j = warp; j < nr; j += kRpWarps) {
-    const int hj = s_h[j], Vj = hj & 0x1fff, wj = (hj >> 13) & 3, vert = hj >> 15;
-    const int m = max(Vj - 1, 0);
-    const int64_t vo = vbase + s_v[j];
-    const unsigned short* up = units + ubase + s_u[j];
-    int cx = s_s[j].x, cy = s_s[j].y;
-    if (Vj > 0 && lane == 0) xy[vo] = make_int2(cx, cy);
-    int2* dst = xy + vo + 1;
-    if (wj == 0)
-      rp_ring<4, 4>(up, m, vert, cx, cy, dst, stg);
-    else if (wj == 1)
-      rp_ring<2, 8>(up, m, vert, cx, cy, dst, stg);
-    else
-      rp_ring<1, 16>(up, m, vert, cx, cy, dst, stg);
-  }
+  const int lim = min(tv, s_lim);
+  for (int i = threadIdx.x; i < lim; i += kRpBlock) xy[vbase + i] = s_stage[i];
 }
 
 int decode_rect_packed(const uint16_t* head, const int16_t* start, const uint16_t* units, const int64_t* block,
                        int64_t n, int64_t* offsets, int32_t* xy, cudaStream_t stream) {
   const int64_t nb = n > 0 ? (n + kRpBlock - 1) / kRpBlock : 1;
-  launch_pdl(decode_rect_packed_kernel, dim3((unsigned)nb), dim3(kRpBlock), 0, stream,
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(decode_rect_packed_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRpSmem);
+    attr = true;
+  }
+  launch_pdl(decode_rect_packed_kernel, dim3((unsigned)nb), dim3(kRpBlock), kRpSmem, stream,
              reinterpret_cast<const unsigned short*>(head), reinterpret_cast<const short*>(start),
              reinterpret_cast<const unsigned short*>(units), reinterpret_cast<const long long*>(block), n, offsets,
              reinterpret_cast<int2*>(xy));
