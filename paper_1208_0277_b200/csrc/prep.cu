@@ -29,7 +29,7 @@ constexpr int kPrepPolys = kPrepThreads;  // one ring per thread per tile
 static_assert(kPrepThreads % 32 == 0 && kPrepThreads <= 256, "whole warps; ring indices fit a byte");
 constexpr int kPrepVerts = SCCG_PREP_VERTS;
 #ifndef SCCG_PREP_RES_DEAL
-#define SCCG_PREP_RES_DEAL 1
+#define SCCG_PREP_RES_DEAL 2  // 0: V-sorted order, 1: residue-sorted alternation, 2: residue occurrences alternated
 #endif
 #ifndef SCCG_PREP_USED_ONLY
 #define SCCG_PREP_USED_ONLY 0  // 1: write back only each ring's defined words, one bulk store per ring (measured slower: 177 vs 168 us on C2)
@@ -560,7 +560,32 @@ __global__ void __launch_bounds__(kPrepThreads, SCCG_PREP_MINB) prep_kernel(cons
     __syncthreads();
     if (threadIdx.x < np) s_perm[s_cnt[key] + pos] = (unsigned char)threadIdx.x;
     __syncthreads();
-#if SCCG_PREP_RES_DEAL
+#if SCCG_PREP_RES_DEAL == 2
+    // Within each warp's 32 rings (similar lengths, from the sort above), deal
+    // the rings to the two half-warps so that each half's rings start at
+    // distinct shared-memory bank pairs as far as possible (residue = (offset
+    // - v0) mod 16 vertices = 128 bytes; a half-warp's lockstep 8-byte reads of
+    // vertex i of 16 rings are one wavefront when the residues differ): the
+    // occurrences of each residue alternate between the halves, and the halves
+    // are evened out by moving the last occurrence of half of the residues
+    // that occur an odd number of times.  A residue occurring c times costs
+    // ceil(c / 2) wavefronts per half instead of up to c.
+    {
+      const int j = s_perm[threadIdx.x];
+      const int res = j != 0xff ? (int)((s_off[j] - v0) & 15) : 16 + (lane & 15);
+      const unsigned peers = __match_any_sync(0xffffffffu, res);
+      const int o = __popc(peers & lanemask_lt()), c = __popc(peers);
+      int half = o & 1;
+      const bool cand = (c & 1) && o == c - 1;  // the extra occurrence of an odd count (in half 0)
+      const unsigned cm = __ballot_sync(0xffffffffu, cand);
+      if (cand && __popc(cm & lanemask_lt()) < (__popc(cm) >> 1)) half = 1;
+      const unsigned hm = __ballot_sync(0xffffffffu, half == 1);
+      const int pos = __popc((half ? hm : ~hm) & lanemask_lt());
+      __syncwarp();
+      s_perm[warp * 32 + half * 16 + pos] = (unsigned char)j;
+      __syncthreads();
+    }
+#elif SCCG_PREP_RES_DEAL == 1
     // Within each warp's 32 rings (similar lengths, from the sort above), deal
     // the rings to lanes by the shared-memory bank of their first vertex
     // ((offset - v0) mod 16 vertices = 128 bytes): rings sorted by that residue
