@@ -129,9 +129,10 @@ def prep_algorithmic_bytes(sccg, S) -> int:
     one 8-byte record per vertical edge and one 4-byte word per raster row."""
     ec = S.ecount.long()
     m = S.mbr.long()
-    rast = (ec[:, 1] & sccg.RASTER_FLAG) != 0
+    rast = (ec[:, 0] & sccg.RASTER_FLAG) != 0
+    nv = ec[:, 0] & (sccg.RASTER_FLAG - 1)
     rows = int(((m[:, 3] - m[:, 1]) * rast).sum())
-    return 8 * S.nv + 8 * (S.n + 1) + 32 * S.n + 8 * int(ec[:, 0].sum()) + 4 * rows
+    return 8 * S.nv + 8 * (S.n + 1) + 32 * S.n + 8 * int(nv.sum()) + 4 * rows
 
 
 def lib_digest() -> str:
@@ -207,8 +208,8 @@ def pixelbox_algorithmic_bytes(sccg, P, Q, pairs) -> int:
     mp, mq = P.mbr.long()[p], Q.mbr.long()[q]
     H = (torch.minimum(mp[:, 3], mq[:, 3]) - torch.maximum(mp[:, 1], mq[:, 1])).clamp(min=0)
     ep, eq = P.ecount.long()[p], Q.ecount.long()[q]
-    rast = ((ep[:, 1] & sccg.RASTER_FLAG) != 0) & ((eq[:, 1] & sccg.RASTER_FLAG) != 0)
-    edge = 8 * (ep[:, 0] + eq[:, 0])
+    rast = ((ep[:, 0] & sccg.RASTER_FLAG) != 0) & ((eq[:, 0] & sccg.RASTER_FLAG) != 0)
+    edge = 8 * ((ep[:, 0] & (sccg.RASTER_FLAG - 1)) + (eq[:, 0] & (sccg.RASTER_FLAG - 1)))
     per = 24 + 2 * 40 + torch.where(rast, 8 * H, edge)
     return int(per.sum())
 

@@ -88,7 +88,8 @@ typedef struct {
   /* derived by sccg_prep (§3.2 P:193 areas; MBRs for the filter) */
   int32_t* mbr;           /* [n_polygons][4] xlo, ylo, xhi, yhi (half-open pixel MBR) */
   int64_t* area;          /* [n_polygons] |p| (shoelace) */
-  int32_t* ecount;        /* [n_polygons][2] number of vertical, horizontal edges */
+  int32_t* ecount;        /* [n_polygons][2] vertical-edge count (bits 0-29) | raster flag (bit 30); the edge
+                           * records' 16-bit rebase (internal layout) */
   uint64_t* edges;        /* [n_vertices] edge records (internal layout) */
   uint32_t* status;       /* [2] device: status bits (OR), lowest offending polygon (MIN) */
   void* stats;            /* [128 bytes] device: set statistics the join sizes its grid from (internal) */

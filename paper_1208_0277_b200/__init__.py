@@ -31,7 +31,7 @@ _lib = None
 
 # status codes (include/sccg.h)
 OK, E_ARG, E_NOT_RECTILINEAR, E_RANGE, E_CAPACITY, E_STACK, E_EMPTY, E_CUDA, E_WORKSPACE = range(9)
-RASTER_FLAG = 1 << 30  # ecount[i, 1] bit: prep stored polygon i's raster rows
+RASTER_FLAG = 1 << 30  # ecount[i, 0] bit: prep stored polygon i's raster rows (the count is the low 30 bits)
 FLAG_NO_RASTER = 1
 FLAG_PAPER_SPLIT = 2
 CNT_PIXELS, CNT_ROWTESTS, CNT_BOXES, CNT_BOXEDGES, CNT_SPLITS, CNT_PIXBOXES, CNT_ROOTPX = range(7)
@@ -251,7 +251,8 @@ class DeviceSet:
 
     @property
     def ecount(self):
-        """int32 [n, 2]: vertical-edge records, horizontal edges | RASTER_FLAG."""
+        """int32 [n, 2]: vertical-edge records | RASTER_FLAG, the records' 16-bit rebase
+        (x0 - xlo) | (y0 - ylo) << 16 (include/sccg.h, internal.cuh decode_edge)."""
         return self._view("ecount", _torch().int32, (self.n, 2))
 
     @property
@@ -270,8 +271,8 @@ class DeviceSet:
         edges = self._view("edges", torch.int64, (self.nv,))
         ec = self.ecount.long()
         m = self.mbr.long()
-        rast = (ec[:, 1] & RASTER_FLAG) != 0
-        used = ec[:, 0] + torch.where(rast, (m[:, 3] - m[:, 1] + 1) // 2, torch.zeros_like(ec[:, 0]))
+        rast = (ec[:, 0] & RASTER_FLAG) != 0
+        used = (ec[:, 0] & (RASTER_FLAG - 1)) + torch.where(rast, (m[:, 3] - m[:, 1] + 1) // 2, torch.zeros_like(ec[:, 0]))
         off = self.offsets[:-1]
         idx = torch.repeat_interleave(off, used) + (
             torch.arange(int(used.sum()), device=used.device) - torch.repeat_interleave(torch.cumsum(used, 0) - used, used))

@@ -8,10 +8,11 @@
 
 namespace sccg {
 
-// Vertical-edge record (8 bytes, sccg_polyset.edges), relative to the
-// polygon's MBR lower-left corner so every field fits 16 bits (MBR extent
-// <= 65535): edge x = const from ymin to ymax:
-//   c = x - xlo, lo = ymin - ylo, hi = ymax - ylo.
+// Vertical-edge record (8 bytes, sccg_polyset.edges): edge x = const from
+// ymin to ymax as three 16-bit fields c = x, lo = ymin, hi = ymax relative to
+// an origin of the ring, mod 2^16 (decode_edge with ecount[i].y rebases them
+// to the MBR lower-left corner: every field then fits 16 bits, MBR extent
+// <= 65535).
 // The records of polygon i occupy edges[off[i] .. off[i] + nv) in ring order
 // (the rest of the polygon's slot is unspecified).  Horizontal edges are not
 // stored: only sampling-box classification needs them, and it reads them from
@@ -51,10 +52,22 @@ __device__ __forceinline__ unsigned suffix_mask(int k) { return shl_clamp(0xffff
 // Low `n` bits (n in [0, 32]).
 __device__ __forceinline__ unsigned low_bits(int n) { return ~shl_clamp(0xffffffffu, (unsigned)max(n, 0)); }
 
-// ecount[i].y carries this flag when polygon i has a raster: H = ymax - ylo
-// 32-bit row words (bit x = pixel (xlo + x, ylo + r) inside) stored right after
-// its vertical records, i.e. at (uint32*)(edges + off[i] + nv) (prep.cu).
+// ecount[i] = {nv | kRasterFlag when polygon i has a raster, o0}: nv = the
+// vertical-edge count (bits 0-29); the raster is H = ymax - ylo 32-bit row
+// words (bit x = pixel (xlo + x, ylo + r) inside) stored right after its
+// vertical records, i.e. at (uint32*)(edges + off[i] + nv) (prep.cu).  The
+// records' 16-bit fields are stored relative to some origin of the ring
+// (its first vertex on the one-pass thread path, the MBR origin on the warp
+// path) and o0 = (origin.x - xlo) | (origin.y - ylo) << 16 rebases them:
+// decode_edge adds it mod 2^16 (every field of a valid ring lies in
+// [0, 65535] relative to the MBR origin).
 constexpr int kRasterFlag = 1 << 30;
+constexpr int kNvMask = kRasterFlag - 1;
+__device__ __forceinline__ void decode_edge(uint64_t r, unsigned o0, int& c, int& lo, int& hi) {
+  c = (int)(((unsigned)r + o0) & 0xffffu);
+  lo = (int)((((unsigned)(r >> 16) & 0xffffu) + (o0 >> 16)) & 0xffffu);
+  hi = (int)((((unsigned)(r >> 32) & 0xffffu) + (o0 >> 16)) & 0xffffu);
+}
 
 // Per-set statistics written by sccg_prep (sccg_polyset.stats), read by the
 // join's on-device grid selection: moments of the MBR extents over non-empty

@@ -481,8 +481,9 @@ __global__ void __launch_bounds__(kProbeTile, SCCG_PROBE_MINB)
     // few vectorized L2 loads per thread)
     long long sum = 0;
     const int4* c4 = reinterpret_cast<const int4*>(tile_cnt);
-    for (int i = threadIdx.x; i < (tile >> 2); i += kProbeTile) {
-      const int4 v = c4[i];
+#pragma unroll 4
+    for (int i = threadIdx.x; i < (tile >> 2); i += kProbeTile) {  // unrolled: the loads go out together
+      const int4 v = __ldcg(c4 + i);
       sum += (long long)v.x + v.y + v.z + v.w;
     }
     for (int i = (tile & ~3) + threadIdx.x; i < tile; i += kProbeTile) sum += tile_cnt[i];

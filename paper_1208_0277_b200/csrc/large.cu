@@ -48,7 +48,8 @@ constexpr int kLStack = 256;        // sampling boxes per warp stack
 constexpr int kLItems = 48;         // in-warp item stack (overflow splits)
 
 struct PolyRef {
-  const uint64_t* ev;  // vertical records (relative to the polygon MBR origin)
+  const uint64_t* ev;  // vertical records (decode_edge with o0: relative to the polygon MBR origin)
+  unsigned o0;         // the records' rebase (ecount.y)
   const int2* v;       // raw ring (horizontal edges)
   int nv, V;
   int dx, dy;          // polygon MBR origin - root-box origin
@@ -107,7 +108,7 @@ __device__ bool build_local(const PolyRef& c, int X0, int Y0, int X1, int Y1, Lo
       uint64_t rec = 0;
       if (j < c.nv) {
         int cc, lo, hi;
-        unpack_edge(rr[u], cc, lo, hi);
+        decode_edge(rr[u], c.o0, cc, lo, hi);
         const int x = cc + c.dx, yl = lo + c.dy, yh = hi + c.dy;
         par ^= (x > X0 && yl <= Y0 && Y0 < yh) ? 1 : 0;  // ray from (X0 + 1/2, Y0 + 1/2) toward +x
         keep = x > X0 && x < X1 && yl < Y1 && yh > Y0;
@@ -232,7 +233,7 @@ __device__ long long build_index(const PolyRef* pr, int W, int H, int nx, int ny
     int* D = ch + 33;
     for (int j = lane; j < c.nv; j += 32) {
       int cc, lo, hi;
-      unpack_edge(__ldg(c.ev + j), cc, lo, hi);
+      decode_edge(__ldg(c.ev + j), c.o0, cc, lo, hi);
       const int x = cc + c.dx, yl = lo + c.dy, yh = hi + c.dy;
       const int cm = count_below(x, nx, W);
       if (cm >= 1 && cm <= nx && X[cm] != x) atomicAdd(&cv[cm - 1], 1);
@@ -303,7 +304,7 @@ __device__ long long build_index(const PolyRef* pr, int W, int H, int nx, int ny
     uint64_t* hrec = vrec + totv[s];
     for (int j = lane; j < c.nv; j += 32) {
       int cc, lo, hi;
-      unpack_edge(__ldg(c.ev + j), cc, lo, hi);
+      decode_edge(__ldg(c.ev + j), c.o0, cc, lo, hi);
       const int x = cc + c.dx, yl = lo + c.dy, yh = hi + c.dy;
       const int cm = count_below(x, nx, W);
       if (cm >= 1 && cm <= nx && X[cm] != x) vrec[atomicAdd(&cv[cm - 1], 1)] = pack_ix(x, yl, yh);
@@ -791,7 +792,9 @@ __global__ void __launch_bounds__(kLWarps * 32, 4)
       const long long o = S.off[id];
       pr[s].ev = S.edges + o;
       pr[s].v = S.xy + o;
-      pr[s].nv = S.ecount[id].x;
+      const int2 ec = S.ecount[id];
+      pr[s].nv = ec.x & kNvMask;
+      pr[s].o0 = (unsigned)ec.y;
       pr[s].V = (int)(S.off[id + 1] - o);
       pr[s].dx = m.x - rb.x;
       pr[s].dy = m.y - rb.y;

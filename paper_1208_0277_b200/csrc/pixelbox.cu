@@ -39,12 +39,12 @@ constexpr int kSmallQOff = 136;  // q buffer offset in records (8 B): 1088 B, so
 // edge toggles.  Edges crossing no row are culled; every slot of the 32-record
 // block (64 with `two`) is written -- kept records first, then zero records
 // (no-ops) -- so no padding pass is needed.  Returns the loop length.
-__device__ __forceinline__ int stage_rows(uint64_t r0, uint64_t r1, int nv, bool two, int dx, int dy, int H,
-                                          int2* buf) {
+__device__ __forceinline__ int stage_rows(uint64_t r0, uint64_t r1, int nv, bool two, unsigned o0, int dx, int dy,
+                                          int H, int2* buf) {
   const int lane = threadIdx.x & 31;
   const unsigned lt = lanemask_lt();
   int c, lo, hi;
-  unpack_edge(r0, c, lo, hi);
+  decode_edge(r0, o0, c, lo, hi);
   unsigned rows = low_bits(min(hi + dy, H)) & ~low_bits(lo + dy);
   bool keep = lane < nv && rows != 0;
   unsigned b = __ballot_sync(FULL, keep);
@@ -52,7 +52,7 @@ __device__ __forceinline__ int stage_rows(uint64_t r0, uint64_t r1, int nv, bool
   buf[keep ? __popc(b & lt) : cnt + __popc(~b & lt)] =
       keep ? make_int2((int)rows, (int)suffix_mask(c + dx)) : make_int2(0, 0);
   if (!two) return cnt;
-  unpack_edge(r1, c, lo, hi);
+  decode_edge(r1, o0, c, lo, hi);
   rows = low_bits(min(hi + dy, H)) & ~low_bits(lo + dy);
   keep = lane + 32 < nv && rows != 0;
   b = __ballot_sync(FULL, keep);
@@ -64,8 +64,8 @@ __device__ __forceinline__ int stage_rows(uint64_t r0, uint64_t r1, int nv, bool
 
 // stage_rows for up to 4 blocks of 32 records read from `rec` (L1-resident
 // after the first window); returns 32 (nb - 1) + the last block's kept count.
-__device__ __forceinline__ int stage_blocks(const uint64_t* __restrict__ rec, int nv, int nb, int dx, int dy, int H,
-                                            int2* buf) {
+__device__ __forceinline__ int stage_blocks(const uint64_t* __restrict__ rec, int nv, int nb, unsigned o0, int dx,
+                                            int dy, int H, int2* buf) {
   const int lane = threadIdx.x & 31;
   const unsigned lt = lanemask_lt();
   int cnt = 0;
@@ -73,7 +73,7 @@ __device__ __forceinline__ int stage_blocks(const uint64_t* __restrict__ rec, in
   for (int blk = 0; blk < 4; blk++) {
     if (blk < nb) {
       int c, lo, hi;
-      unpack_edge(lane + 32 * blk < nv ? __ldg(rec + 32 * blk + lane) : 0ull, c, lo, hi);
+      decode_edge(lane + 32 * blk < nv ? __ldg(rec + 32 * blk + lane) : 0ull, o0, c, lo, hi);
       const unsigned rows = low_bits(min(hi + dy, H)) & ~low_bits(lo + dy);
       const bool keep = lane + 32 * blk < nv && rows != 0;
       const unsigned b = __ballot_sync(FULL, keep);
@@ -141,6 +141,7 @@ __global__ void __launch_bounds__(kSmallWarps * 32, SCCG_SMALL_MINB)
   __shared__ __align__(16) int2 s_buf[kSmallWarps][2 * kSmallQOff];
   __shared__ int4 s_meta[kSmallWarps][32];
   __shared__ int2 s_ep[kSmallWarps][32];
+  __shared__ uint2 s_o0[kSmallWarps][32];  // the pair's record rebases (ecount.y of p and q)
   __shared__ unsigned long long s_acc[kSmallWarps][16];
   __shared__ int s_rstart[kSmallWarps][33];  // raster pairs: first (pair, row) item of each pair
   __shared__ unsigned s_rcnt[kSmallWarps][32];
@@ -174,7 +175,8 @@ __global__ void __launch_bounds__(kSmallWarps * 32, SCCG_SMALL_MINB)
     }
     if (ok) {
       const int4 mp = Ps.mbr[pq.x], mq = Qs.mbr[pq.y];
-      const int2 cp = Ps.ecount[pq.x], cq = Qs.ecount[pq.y];
+      const int2 cpr = Ps.ecount[pq.x], cqr = Qs.ecount[pq.y];
+      const int2 cp = make_int2(cpr.x & kNvMask, cpr.y), cq = make_int2(cqr.x & kNvMask, cqr.y);
       const long long op = Ps.off[pq.x], oq = Qs.off[pq.y];
       const int bx0 = max(mp.x, mq.x), by0 = max(mp.y, mq.y);
       W = min(mp.z, mq.z) - bx0;
@@ -190,12 +192,13 @@ __global__ void __launch_bounds__(kSmallWarps * 32, SCCG_SMALL_MINB)
       }
       // both rings carry a raster (prep): the pair reads pixel classifications instead of edges.
       // meta.x: W (bits 0-6), H (7-13), nv_p (14-21), nv_q (22-29), raster (30)
-      rast = (small && use_raster && W <= 32 && H <= 32 && (cp.y & kRasterFlag) && (cq.y & kRasterFlag)) ? 1u : 0u;
+      rast = (small && use_raster && W <= 32 && H <= 32 && (cpr.x & kRasterFlag) && (cqr.x & kRasterFlag)) ? 1u : 0u;
       meta[lane] = make_int4((int)((unsigned)W | ((unsigned)H << 7) | ((unsigned)cp.x << 14) | ((unsigned)cq.x << 22) |
                                    (rast << 30)),
                              (int)(((unsigned)dxp & 0xffffu) | ((unsigned)dyp << 16)),
                              (int)(((unsigned)dxq & 0xffffu) | ((unsigned)dyq << 16)), 0);
       epq[lane] = make_int2((int)op, (int)oq);
+      s_o0[warp][lane] = make_uint2((unsigned)cp.y, (unsigned)cq.y);
     }
     __syncwarp();
     // ---- everything else goes to the generic kernel (warp-aggregated append)
@@ -339,8 +342,9 @@ __global__ void __launch_bounds__(kSmallWarps * 32, SCCG_SMALL_MINB)
       for (int wy = 0; wy < Hb; wy += 32)
         for (int wx = 0; wx < Wb; wx += 32) {
           const int W = min(32, Wb - wx), H = min(32, Hb - wy);
-          const int cntp = stage_rows(cp0, cp1, nvp, two, dxp - wx, dyp - wy, H, bp);
-          const int cntq = stage_rows(cq0, cq1, nvq, two, dxq - wx, dyq - wy, H, bq);
+          const uint2 rb = s_o0[warp][j];
+          const int cntp = stage_rows(cp0, cp1, nvp, two, rb.x, dxp - wx, dyp - wy, H, bp);
+          const int cntq = stage_rows(cq0, cq1, nvq, two, rb.y, dxq - wx, dyq - wy, H, bq);
           // half-warp per polygon (lanes 0-15: p, 16-31: q), rows lane&15 (+16)
           const int npad = (max(cntp, cntq) + 3) & ~3;
           __syncwarp();
@@ -376,8 +380,9 @@ __global__ void __launch_bounds__(kSmallWarps * 32, SCCG_SMALL_MINB)
       for (int wy = 0; wy < Hb; wy += 32)
         for (int wx = 0; wx < Wb; wx += 32) {
           const int W = min(32, Wb - wx), H = min(32, Hb - wy);
-          const int cntp = stage_blocks(rp, nvp, nb, dxp - wx, dyp - wy, H, bp);
-          const int cntq = stage_blocks(rq, nvq, nb, dxq - wx, dyq - wy, H, bq);
+          const uint2 rb = s_o0[warp][j];
+          const int cntp = stage_blocks(rp, nvp, nb, rb.x, dxp - wx, dyp - wy, H, bp);
+          const int cntq = stage_blocks(rq, nvq, nb, rb.y, dxq - wx, dyq - wy, H, bq);
           const int npad = (max(cntp, cntq) + 3) & ~3;
           __syncwarp();
           const int2* b = lane < 16 ? bp : bq;

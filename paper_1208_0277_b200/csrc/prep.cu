@@ -47,12 +47,40 @@ __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)_
 __device__ __forceinline__ void mbar_init(uint64_t* bar) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(bar)) : "memory");
 }
+// SCCG_PREP_EVICT_FIRST: the vertex tiles are read once per step (nothing
+// downstream of prep on the nucleus path reads xy), so their L2 lines are
+// marked evict-first and the derived buffers PixelBox reads next keep L2.
+#ifndef SCCG_PREP_EVICT_FIRST
+#define SCCG_PREP_EVICT_FIRST 0
+#endif
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(pol));
+  return pol;
+}
 __device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+#if SCCG_PREP_EVICT_FIRST
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;\n" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy_evict_first())
+      : "memory");
+#else
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(smem_u32(dst)),
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
+#endif
+}
+__device__ __forceinline__ void prefetch_l2(const void* src, unsigned bytes) {
+#if SCCG_PREP_EVICT_FIRST
+  asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;\n" ::"l"(src), "r"(bytes),
+               "l"(policy_evict_first())
+               : "memory");
+#else
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(src), "r"(bytes) : "memory");
+#endif
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
   asm volatile(
@@ -152,73 +180,69 @@ __device__ __forceinline__ int4 prep_polygon(const int2* v, int64_t V, int64_t p
   if (lane == 0) {
     area[poly] = (twice_area < 0 ? -twice_area : twice_area) / 2;
     mbr[poly] = m;
-    ecount[poly] = make_int2(nvert, nhor);
+    ecount[poly] = make_int2(nvert, 0);  // records relative to the MBR origin: zero rebase
+    (void)nhor;
     if (validate && diag) flag(status, SCCG_STATUS_NOT_RECTILINEAR, poly);
   }
   return m;
 }
 
 // One polygon by one thread (the common small ring): same results as
-// prep_polygon, serial over the ring's vertices in the shared-memory tile,
-// 32-bit arithmetic on MBR-rebased coordinates (extents <= 65535, so each
-// shoelace product fits 32 bits unsigned; the sum is int64).  Records are
-// written in place over the ring's own vertex slot: record k lands in slot
-// k <= i - 1 while vertex i is being read.
-__device__ __forceinline__ int4 prep_polygon_thread(int2* v, int V, int rot, int64_t poly, int4* __restrict__ mbr,
+// prep_polygon in ONE pass over the ring's vertices in the shared-memory tile
+// (no separate MBR pass: shared-memory wavefronts bound this kernel).  The
+// MBR is tracked on coordinates biased by 2^30 as unsigned (an out-of-range
+// vertex shows up as a huge value, so the range check needs no extra test),
+// and the records are written relative to the ring's FIRST vertex (16-bit
+// fields mod 2^16); ecount[i].y = (x0 - xlo) | (y0 - ylo) << 16 rebases them
+// to the MBR (decode_edge in internal.cuh).  Records are written in place
+// over the ring's own vertex slot: record k lands in slot k <= i - 1 while
+// vertex i is being read.
+__device__ __forceinline__ int4 prep_polygon_thread(int2* v, int V, int64_t poly, int4* __restrict__ mbr,
                                                     int64_t* __restrict__ area, int2* __restrict__ ecount,
                                                     uint32_t* __restrict__ status, int validate, int& used8) {
   used8 = 0;
-  // MBR: order-free, so each thread starts at vertex `rot` (chosen by the
-  // caller so the lockstep reads of a half-warp hit distinct bank pairs) and
-  // wraps around
-  int xmin = INT_MAX, ymin = INT_MAX, xmax = INT_MIN, ymax = INT_MIN;
-  auto take = [&](const int2 a) {
-    xmin = min(xmin, a.x);
-    xmax = max(xmax, a.x);
-    ymin = min(ymin, a.y);
-    ymax = max(ymax, a.y);
-  };
-#pragma unroll 4
-  for (int i = rot; i < V; i++) take(v[i]);
-#pragma unroll 4
-  for (int i = 0; i < rot; i++) take(v[i]);
-  const int4 m = make_int4(xmin, ymin, xmax, ymax);
-  mbr[poly] = m;
-  if ((int64_t)xmin < -kMaxCoord || (int64_t)xmax > kMaxCoord || (int64_t)ymin < -kMaxCoord ||
-      (int64_t)ymax > kMaxCoord || (int64_t)xmax - xmin > kMaxExtent || (int64_t)ymax - ymin > kMaxExtent) {
-    area[poly] = 0;
-    ecount[poly] = make_int2(0, 0);
-    flag(status, SCCG_STATUS_RANGE, poly);
-    return m;
-  }
+  constexpr unsigned kBias = 1u << 30;
   uint64_t* out = reinterpret_cast<uint64_t*>(v);
+  const int2 f = v[0];
+  const unsigned ux0 = (unsigned)f.x + kBias, uy0 = (unsigned)f.y + kBias;
+  unsigned uxmin = ux0, uxmax = ux0, uymin = uy0, uymax = uy0;
   // Area: the shoelace of P:193 in trapezoid form, A = 1/2 |sum (x_i +
   // x_{i+1}) (y_{i+1} - y_i)| (the same sum re-associated), which on a
   // rectilinear ring is |sum over vertical edges of x_i (y_{i+1} - y_i)|
-  // (horizontal edges add 0, vertical ones have x_i = x_{i+1}); accumulated
-  // mod 2^32: exact whenever A < 2^31, i.e. whenever W * H < 2^31 (else
-  // recomputed in int64 from the records below).
+  // (horizontal edges add 0, vertical ones have x_i = x_{i+1}); on
+  // coordinates relative to the first vertex (translation invariant: the
+  // y-steps of a closed ring sum to 0), accumulated mod 2^32: exact whenever
+  // A < 2^31, i.e. whenever W * H < 2^31 (else recomputed in int64 from the
+  // records below).
   unsigned area32 = 0u;
   // edge classes by counts: nsx = edges with dx == 0, nsy = with dy == 0;
   // vertical = dx == 0 != dy (nvert), zero-length = nsx - nvert, horizontal =
   // nsy - (nsx - nvert), diagonal = V - nsy - nvert
   int nvert = 0, nsx = 0, nsy = 0;
-  const unsigned fx = v[0].x - xmin, fy = v[0].y - ymin;
   const unsigned sbase = smem_u32(out);
-  unsigned ax = fx, ay = fy;
-  auto edge = [&](unsigned cx, unsigned cy) {
-    area32 += ax * (cy - ay);
+  int ax = 0, ay = 0;  // current vertex relative to the first
+  auto edge = [&](int cx, int cy) {
+    area32 += (unsigned)ax * (unsigned)(cy - ay);
     const bool same_x = ax == cx, same_y = ay == cy;
     const bool is_v = same_x && !same_y;
     nsx += same_x ? 1 : 0;
     nsy += same_y ? 1 : 0;
-    // record: x | lo << 16 | hi << 32 | exit row << 48 (the row the ring
-    // leaves the edge at, read by the raster pass below; decoders mask it off)
+    // record: x | lo << 16 | hi << 32 | exit row << 48 (16-bit fields relative
+    // to the first vertex; the exit row -- where the ring leaves the edge -- is
+    // read by the raster pass below; decoders mask it off)
     const unsigned lo32 = __byte_perm(ax, min(ay, cy), 0x5410), hi32 = __byte_perm(max(ay, cy), cy, 0x5410);
     sts64_if(sbase + 8u * (unsigned)nvert, lo32, hi32, is_v);  // predicated: no divergent branch
     nvert += is_v ? 1 : 0;
     ax = cx;
     ay = cy;
+  };
+  auto vert = [&](const int2 c) {  // bias, MBR, relative coordinates
+    const unsigned ux = (unsigned)c.x + kBias, uy = (unsigned)c.y + kBias;
+    uxmin = min(uxmin, ux);
+    uxmax = max(uxmax, ux);
+    uymin = min(uymin, uy);
+    uymax = max(uymax, uy);
+    edge((int)(ux - ux0), (int)(uy - uy0));
   };
   // Vertices are loaded four at a time ahead of the record stores: the store of
   // edge i lands in slot <= i - 1, below every prefetched vertex, so loading
@@ -227,19 +251,28 @@ __device__ __forceinline__ int4 prep_polygon_thread(int2* v, int V, int rot, int
   int i = 1;
   for (; i + 4 <= V; i += 4) {
     const int2 c0 = v[i], c1 = v[i + 1], c2 = v[i + 2], c3 = v[i + 3];
-    edge((unsigned)(c0.x - xmin), (unsigned)(c0.y - ymin));
-    edge((unsigned)(c1.x - xmin), (unsigned)(c1.y - ymin));
-    edge((unsigned)(c2.x - xmin), (unsigned)(c2.y - ymin));
-    edge((unsigned)(c3.x - xmin), (unsigned)(c3.y - ymin));
+    vert(c0);
+    vert(c1);
+    vert(c2);
+    vert(c3);
   }
-  for (; i < V; i++) {
-    const int2 c = v[i];
-    edge((unsigned)(c.x - xmin), (unsigned)(c.y - ymin));
+  for (; i < V; i++) vert(v[i]);
+  edge(0, 0);  // closing edge back to the first vertex
+  const int4 m = make_int4((int)(uxmin - kBias), (int)(uymin - kBias), (int)(uxmax - kBias), (int)(uymax - kBias));
+  mbr[poly] = m;
+  // |coordinates| <= 2^30 <=> every biased value <= 2^31 (below -2^30 wraps to >= 2^32 - 2^30)
+  if (uxmax > 2 * kBias || uymax > 2 * kBias || uxmax - uxmin > (unsigned)kMaxExtent ||
+      uymax - uymin > (unsigned)kMaxExtent) {
+    area[poly] = 0;
+    ecount[poly] = make_int2(0, 0);
+    flag(status, SCCG_STATUS_RANGE, poly);
+    return m;
   }
-  edge(fx, fy);  // closing edge back to the first vertex
+  const unsigned ox = ux0 - uxmin, oy = uy0 - uymin;  // first vertex - MBR origin: rebases the records
   const int nhor = nsy - (nsx - nvert);
+  (void)nhor;
   const bool diag = V - nsy - nvert != 0;
-  const int W = xmax - xmin, H = ymax - ymin;
+  const int W = (int)(uxmax - uxmin), H = (int)(uymax - uymin);
   if ((unsigned long long)W * (unsigned long long)H < (1ull << 31)) {
     const int a = (int)area32;
     area[poly] = a < 0 ? -a : a;
@@ -247,9 +280,9 @@ __device__ __forceinline__ int4 prep_polygon_thread(int2* v, int V, int rot, int
     long long a = 0;
     for (int k = 0; k < nvert; k++) {
       const uint64_t r = out[k];
-      const long long x = (long long)(r & 0xffffu), lo = (long long)((r >> 16) & 0xffffu),
-                      hi = (long long)((r >> 32) & 0xffffu);
-      a += ((r >> 48) == (uint64_t)hi) ? x * (hi - lo) : -x * (hi - lo);
+      int x, lo, hi;
+      decode_edge(r, ox | (oy << 16), x, lo, hi);
+      a += ((r >> 48) == ((r >> 32) & 0xffffu)) ? (long long)x * (hi - lo) : -(long long)x * (hi - lo);
     }
     area[poly] = a < 0 ? -a : a;
   }
@@ -275,13 +308,13 @@ __device__ __forceinline__ int4 prep_polygon_thread(int2* v, int V, int rot, int
     const unsigned dbase = sbase + 8u * (unsigned)nvert;
     for (int r = 0; r < H; r++) D[r] = 0u;
     const uint64_t first = out[0];
-    unsigned mc = shl_clamp(0xffffffffu, (unsigned)first & 0xffffu), yc = (unsigned)(first >> 48);
+    unsigned mc = shl_clamp(0xffffffffu, ((unsigned)first + ox) & 0xffffu), yc = ((unsigned)(first >> 48) + oy) & 0xffffu;
     const unsigned m0 = mc;
     auto apply = [&](uint64_t nxt) {
-      const unsigned mn = shl_clamp(0xffffffffu, (unsigned)nxt & 0xffffu);
+      const unsigned mn = shl_clamp(0xffffffffu, ((unsigned)nxt + ox) & 0xffffu);
       red_xor_if(dbase + 4u * yc, mc ^ mn, yc < (unsigned)H);
       mc = mn;
-      yc = (unsigned)(nxt >> 48);
+      yc = ((unsigned)(nxt >> 48) + oy) & 0xffffu;
     };
     int k = 1;
     for (; k + 4 <= nvert; k += 4) {
@@ -312,7 +345,7 @@ __device__ __forceinline__ int4 prep_polygon_thread(int2* v, int V, int rot, int
       D[r] = acc & wmask;
     }
   }
-  ecount[poly] = make_int2(nvert, nhor | (raster ? kRasterFlag : 0));
+  ecount[poly] = make_int2(nvert | (raster ? kRasterFlag : 0), (int)(ox | (oy << 16)));
   if (validate && diag) flag(status, SCCG_STATUS_NOT_RECTILINEAR, poly);
   used8 = nvert + (raster ? (H + 1) / 2 : 0);  // the slot's defined 8-byte words: records, then raster rows
   return m;
@@ -620,7 +653,7 @@ __global__ void __launch_bounds__(kPrepThreads, SCCG_PREP_MINB) prep_kernel(cons
         const int64_t w0 = S2.off[p02] & ~int64_t(1), w1 = S2.off[p02 + np2];
         if (w0 >= 0 && w1 > w0 && w1 <= S2.nv_total && w1 - w0 <= kPrepVerts) {
           const unsigned bytes = (unsigned)((w1 - w0 + 1) & ~int64_t(1)) * 8u;
-          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(S2.xy + w0), "r"(bytes) : "memory");
+          prefetch_l2(S2.xy + w0, bytes);
         }
       };
       prefetch_tile(next_gt);
@@ -640,9 +673,8 @@ __global__ void __launch_bounds__(kPrepThreads, SCCG_PREP_MINB) prep_kernel(cons
       } else if (V > kThreadMaxV || !tiled) {
         atomicOr(&s_big[j >> 5], 1u << (j & 31));
       } else {
-        const int rot = (int)((lane - (b - v0)) & 15) % (int)V;
         int used8;
-        acc.add(prep_polygon_thread(s_xy + (b - v0), (int)V, rot, poly, mbr, area, ecount, status, validate, used8));
+        acc.add(prep_polygon_thread(s_xy + (b - v0), (int)V, poly, mbr, area, ecount, status, validate, used8));
 #if SCCG_PREP_USED_ONLY
         if (bulk) store_used(edges, b, reinterpret_cast<const uint64_t*>(s_xy + (b - v0)), used8);
         else
@@ -665,7 +697,7 @@ __global__ void __launch_bounds__(kPrepThreads, SCCG_PREP_MINB) prep_kernel(cons
           const int64_t w0 = S2.off[p02] & ~int64_t(1), w1 = S2.off[p02 + np2];
           if (w0 >= 0 && w1 > w0 && w1 <= S2.nv_total && w1 - w0 <= kPrepVerts) {
             const unsigned bytes = (unsigned)((w1 - w0 + 1) & ~int64_t(1)) * 8u;
-            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(S2.xy + w0), "r"(bytes) : "memory");
+            prefetch_l2(S2.xy + w0, bytes);
           }
         }
       }

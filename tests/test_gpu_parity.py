@@ -392,7 +392,8 @@ def test_pixelbox_windows_and_wide_pairs(sccg):
     mp, mq = P.mbr.long()[pr[:, 0]], Q.mbr.long()[pr[:, 1]]
     W = torch.minimum(mp[:, 2], mq[:, 2]) - torch.maximum(mp[:, 0], mq[:, 0])
     H = torch.minimum(mp[:, 3], mq[:, 3]) - torch.maximum(mp[:, 1], mq[:, 1])
-    nv = torch.maximum(P.ecount.long()[pr[:, 0], 0], Q.ecount.long()[pr[:, 1], 0])
+    nvm = sccg.RASTER_FLAG - 1  # ecount[:, 0] = count | raster flag
+    nv = torch.maximum(P.ecount.long()[pr[:, 0], 0] & nvm, Q.ecount.long()[pr[:, 1], 0] & nvm)
     assert int(W.max()) <= 64 and int(H.max()) <= 64 and int(nv.max()) <= 128
     assert int(((W > 32) | (H > 32)).sum()) > 50 and int((nv > 64).sum()) > 50
     for raster in (True, False):
