@@ -197,7 +197,7 @@ __device__ __forceinline__ int4 prep_polygon(const int2* v, int64_t V, int64_t p
 // to the MBR (decode_edge in internal.cuh).  Records are written in place
 // over the ring's own vertex slot: record k lands in slot k <= i - 1 while
 // vertex i is being read.
-__device__ __forceinline__ int4 prep_polygon_thread(int2* v, int V, int64_t poly, int4* __restrict__ mbr,
+__device__ __forceinline__ int4 prep_polygon_thread(int2* v, int V, int rot, int64_t poly, int4* __restrict__ mbr,
                                                     int64_t* __restrict__ area, int2* __restrict__ ecount,
                                                     uint32_t* __restrict__ status, int validate, int& used8) {
   used8 = 0;
@@ -307,7 +307,12 @@ __device__ __forceinline__ int4 prep_polygon_thread(int2* v, int V, int64_t poly
     unsigned* D = reinterpret_cast<unsigned*>(out + nvert);
     const unsigned dbase = sbase + 8u * (unsigned)nvert;
     for (int r = 0; r < H; r++) D[r] = 0u;
-    const uint64_t first = out[0];
+    // The chain is cyclic and XOR is order-free, so each thread walks its
+    // records from record s (the caller's rotation: the lockstep reads of a
+    // warp's threads then hit distinct bank pairs, as far as the rings allow)
+    // around to s - 1.
+    const int s0 = nvert > 0 ? rot % nvert : 0;
+    const uint64_t first = out[s0];
     unsigned mc = shl_clamp(0xffffffffu, ((unsigned)first + ox) & 0xffffu), yc = ((unsigned)(first >> 48) + oy) & 0xffffu;
     const unsigned m0 = mc;
     auto apply = [&](uint64_t nxt) {
@@ -316,15 +321,19 @@ __device__ __forceinline__ int4 prep_polygon_thread(int2* v, int V, int64_t poly
       mc = mn;
       yc = ((unsigned)(nxt >> 48) + oy) & 0xffffu;
     };
-    int k = 1;
-    for (; k + 4 <= nvert; k += 4) {
-      const uint64_t r0 = out[k], r1 = out[k + 1], r2 = out[k + 2], r3 = out[k + 3];
+    auto at = [&](int j) {  // record s0 + j, cyclically (j < nvert)
+      const int k = s0 + j;
+      return k < nvert ? k : k - nvert;
+    };
+    int j = 1;
+    for (; j + 4 <= nvert; j += 4) {
+      const uint64_t r0 = out[at(j)], r1 = out[at(j + 1)], r2 = out[at(j + 2)], r3 = out[at(j + 3)];
       apply(r0);
       apply(r1);
       apply(r2);
       apply(r3);
     }
-    for (; k < nvert; k++) apply(out[k]);
+    for (; j < nvert; j++) apply(out[at(j)]);
     red_xor_if(dbase + 4u * yc, mc ^ m0, yc < (unsigned)H);  // the last record's exit is the first record's entry
     unsigned acc = 0u;
     const unsigned wmask = low_bits(W);
@@ -674,7 +683,8 @@ __global__ void __launch_bounds__(kPrepThreads, SCCG_PREP_MINB) prep_kernel(cons
         atomicOr(&s_big[j >> 5], 1u << (j & 31));
       } else {
         int used8;
-        acc.add(prep_polygon_thread(s_xy + (b - v0), (int)V, poly, mbr, area, ecount, status, validate, used8));
+        const int rot = (int)((lane - (b - v0)) & 15);  // raster pass: record rot first (bank pairs by lane)
+        acc.add(prep_polygon_thread(s_xy + (b - v0), (int)V, rot, poly, mbr, area, ecount, status, validate, used8));
 #if SCCG_PREP_USED_ONLY
         if (bulk) store_used(edges, b, reinterpret_cast<const uint64_t*>(s_xy + (b - v0)), used8);
         else
