@@ -306,7 +306,11 @@ __device__ __forceinline__ int4 prep_polygon_thread(int2* v, int V, int rot, int
     // pass reads four rows ahead of its stores.
     unsigned* D = reinterpret_cast<unsigned*>(out + nvert);
     const unsigned dbase = sbase + 8u * (unsigned)nvert;
-    for (int r = 0; r < H; r++) D[r] = 0u;
+    // 8-byte accesses to D (it starts on an 8-byte boundary; an odd H leaves
+    // one spare word in the slot, 2 (V - nv) >= H + 1): half the shared-memory
+    // instructions of 4-byte ones
+    uint2* D2 = reinterpret_cast<uint2*>(D);
+    for (int r = 0; r < H; r += 2) D2[r >> 1] = make_uint2(0u, 0u);
     // The chain is cyclic and XOR is order-free, so each thread walks its
     // records from record s (the caller's rotation: the lockstep reads of a
     // warp's threads then hit distinct bank pairs, as far as the rings allow)
@@ -338,20 +342,26 @@ __device__ __forceinline__ int4 prep_polygon_thread(int2* v, int V, int rot, int
     unsigned acc = 0u;
     const unsigned wmask = low_bits(W);
     int r = 0;
-    for (; r + 4 <= H; r += 4) {
-      const unsigned d0 = D[r], d1 = D[r + 1], d2 = D[r + 2], d3 = D[r + 3];
-      acc ^= d0;
-      D[r] = acc & wmask;
-      acc ^= d1;
-      D[r + 1] = acc & wmask;
-      acc ^= d2;
-      D[r + 2] = acc & wmask;
-      acc ^= d3;
-      D[r + 3] = acc & wmask;
+    for (; r + 4 <= H; r += 4) {  // rows four ahead of their stores, two per access
+      uint2 a = D2[r >> 1], b = D2[(r >> 1) + 1];
+      acc ^= a.x;
+      a.x = acc & wmask;
+      acc ^= a.y;
+      a.y = acc & wmask;
+      acc ^= b.x;
+      b.x = acc & wmask;
+      acc ^= b.y;
+      b.y = acc & wmask;
+      D2[r >> 1] = a;
+      D2[(r >> 1) + 1] = b;
     }
-    for (; r < H; r++) {
-      acc ^= D[r];
-      D[r] = acc & wmask;
+    for (; r < H; r += 2) {  // (an odd H also rewrites the spare word: not part of the raster)
+      uint2 a = D2[r >> 1];
+      acc ^= a.x;
+      a.x = acc & wmask;
+      acc ^= a.y;
+      a.y = acc & wmask;
+      D2[r >> 1] = a;
     }
   }
   ecount[poly] = make_int2(nvert | (raster ? kRasterFlag : 0), (int)(ox | (oy << 16)));
