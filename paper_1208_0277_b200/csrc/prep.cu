@@ -248,13 +248,20 @@ __device__ __forceinline__ int4 prep_polygon_thread(int2* v, int V, int rot, int
   // edge i lands in slot <= i - 1, below every prefetched vertex, so loading
   // early is safe (the compiler cannot prove it and would otherwise serialise
   // each load behind the previous store).
+  // 16-byte loads (two vertices each: a warp's lockstep loads then spread
+  // over 8 bank quads instead of 16 bank pairs, fewer wavefronts per vertex)
+  // after peeling one vertex when v + 1 is not 16-byte aligned
   int i = 1;
+  if (V > 1 && (smem_u32(v + 1) & 15u) != 0u) {
+    vert(v[1]);
+    i = 2;
+  }
   for (; i + 4 <= V; i += 4) {
-    const int2 c0 = v[i], c1 = v[i + 1], c2 = v[i + 2], c3 = v[i + 3];
-    vert(c0);
-    vert(c1);
-    vert(c2);
-    vert(c3);
+    const int4 a = *reinterpret_cast<const int4*>(v + i), b = *reinterpret_cast<const int4*>(v + i + 2);
+    vert(make_int2(a.x, a.y));
+    vert(make_int2(a.z, a.w));
+    vert(make_int2(b.x, b.y));
+    vert(make_int2(b.z, b.w));
   }
   for (; i < V; i++) vert(v[i]);
   edge(0, 0);  // closing edge back to the first vertex
