@@ -135,8 +135,10 @@ def main(src, dst):
         elif name.endswith(".ncu-rep"):
             with open(os.path.join(dst, name.replace(".ncu-rep", ".txt")), "w") as f:
                 f.write(ncu_summary(p))
-        elif name.startswith("sanitize_summary"):
+        elif name == "sanitize_summary.txt":
             shutil.copy(p, os.path.join(dst, "sanitize.txt"))
+        elif name == "sanitize_summary_index.txt":
+            shutil.copy(p, os.path.join(dst, "sanitize_index.txt"))
 
 
 if __name__ == "__main__":

@@ -16,7 +16,7 @@ echo "bench rc=$?"
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches_slide.csv \
   python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-extras --e2e-steps 1 > $OUT/launches_bench.txt 2>&1
 echo "launch list rc=$?"
-for k in prep_kernel grid_insert_kernel small_kernel; do
+for k in prep_kernel grid_insert_kernel small_kernel decode_rect_packed_kernel; do
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:$k -s 1 -c 1 \
     -o $OUT/ncu_$k -f python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-extras --e2e-steps 1 > $OUT/ncu_$k.txt 2>&1
   echo "ncu $k rc=$?"
@@ -32,6 +32,11 @@ for tool in memcheck racecheck synccheck; do
   timeout 1200 compute-sanitizer --tool $tool --error-exitcode 9 python scripts/sanitize_case.py > $OUT/sanitize_$tool.txt 2>&1
   echo "sanitizer $tool rc=$?" | tee -a $OUT/sanitize_summary.txt
   tail -3 $OUT/sanitize_$tool.txt >> $OUT/sanitize_summary.txt
+done
+for tool in memcheck racecheck; do
+  SANITIZE_INDEX=1 timeout 1500 compute-sanitizer --tool $tool --error-exitcode 9 python scripts/sanitize_case.py > $OUT/sanitize_index_$tool.txt 2>&1
+  echo "sanitizer (indexed large path) $tool rc=$?" | tee -a $OUT/sanitize_summary_index.txt
+  tail -3 $OUT/sanitize_index_$tool.txt >> $OUT/sanitize_summary_index.txt
 done
 for c in tile skewed combs; do
   timeout 900 python bench.py --config $c --steps 20 --warmup 3 --no-cpu-baseline > $OUT/bench_$c.json 2> $OUT/bench_$c.err

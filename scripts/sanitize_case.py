@@ -1,6 +1,7 @@
 """Small end-to-end run for compute-sanitizer (memcheck / racecheck / synccheck):
 tile + a skewed window with glands, counting and non-counting builds, all T,
-the bench's pipeline step, and comb pairs (dense splits / Alg. 1's split order)."""
+the bench's pipeline step, comb pairs (dense splits / Alg. 1's split order) and
+the packed transfer decode."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
@@ -33,6 +34,13 @@ pairs = sccg.filter_pairs(P, Q)
 for ps in (False, True):
     sccg.pixelbox(P, Q, pairs, threshold=2048, paper_split=ps)
 torch.cuda.synchronize()
+# the packed transfer encoding's decode (offsets rebuilt on the device, staged vertices), a partial last block
+A, B = synth.generate("tile")
+for S in (A, B):
+    enc = sccg.encode_rect_packed(S.xy, S.offsets)
+    xy, off = sccg.decode_rect_packed({k: torch.from_numpy(v).cuda() for k, v in enc.items()}, int(S.offsets[-1]))
+    torch.cuda.synchronize()
+    assert torch.equal(xy.cpu(), torch.from_numpy(S.xy.astype("int32")))
 if os.environ.get("SANITIZE_INDEX"):
     # enough comb pairs that the large path builds per-pair edge indexes (first items >= 4 x the item
     # kernel's warps), with and without the pool
