@@ -510,15 +510,16 @@ def run_ours(args, rank, world, local_rank):
             # enqueueing (Python) never delays the next copy
             st = sccg.Streamer(A.n, int(A.offsets[-1]), B.n, int(B.offsets[-1]), cap=cap, threshold=args.threshold,
                                depth=3)
-            args_c = (cp[0], cp[1])
+            step = sccg.PackedStep(enc[0], enc[1])  # both sets in one pinned buffer: one copy per step
+            h2d_c = step.nbytes
             for _ in range(st.depth):  # warm-up: every slot once (each slot's graph was captured at construction)
-                st.result(st.submit(*args_c))
+                st.result(st.submit_step(step))
             torch.cuda.synchronize()
             e0.record(stream)
             st.copy_stream.wait_event(e0)  # the first copy starts inside the timed region
             inflight = []
             for _ in range(e2e_steps):
-                inflight.append(st.submit(*args_c))
+                inflight.append(st.submit_step(step))
                 if len(inflight) == st.depth:
                     jc, _ = sccg.jaccard(st.result(inflight.pop(0)))
             for t in inflight:

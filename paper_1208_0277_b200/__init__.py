@@ -668,6 +668,33 @@ class Streamer:
         self.count += 1
         return self.count - 1
 
+    def submit_step(self, step: "PackedStep") -> int:
+        """Enqueue one step whose inputs are a PackedStep (both sets in one
+        pinned buffer: one host -> device copy).  Returns a ticket for result()."""
+        torch = _torch()
+        k = self.count % self.depth
+        sl = self.slots[k]
+        main = torch.cuda.current_stream()
+        cs = self.copy_stream
+        n_p, nv_p, n_q, nv_q = self.shapes
+        if step.n["p"] != n_p or step.n["q"] != n_q:
+            raise ValueError("Streamer: the step's ring counts differ from the slots'")
+        cs.wait_event(sl["done"])  # the slot's previous step no longer reads its buffers
+        with torch.cuda.stream(cs):
+            buf = sl.get("step_buf")
+            if buf is None or buf.numel() < step.nbytes:
+                buf = sl["step_buf"] = torch.empty(max(step.nbytes, 16), dtype=torch.uint8, device=self.device)
+            buf[: step.nbytes].copy_(step.host[: step.nbytes], non_blocking=True)
+            sl["copied"].record(cs)
+        main.wait_event(sl["copied"])
+        v = step.views(buf)
+        for side, nv in (("p", nv_p), ("q", nv_q)):
+            decode_rect_packed(v[side], nv, out=(sl["xy_" + side], sl["off_" + side]))
+        sl["pipe"].run(slot=0)
+        sl["done"].record(main)
+        self.count += 1
+        return self.count - 1
+
     def result(self, ticket: int):
         """The sums of step `ticket` (waits for it; its slot must not have been
         reused since: at most `depth` steps in flight)."""
@@ -684,6 +711,50 @@ def pin_packed(enc):
 
     torch = _torch()
     return {k: torch.from_numpy(np.ascontiguousarray(v)).pin_memory() for k, v in enc.items()}
+
+
+class PackedStep:
+    """Both sets' packed encodings of one step in ONE pinned host buffer (16-byte
+    aligned fields), so a step's inputs cross PCIe as one copy
+    (Streamer.submit_step).  layout[side][key] = (byte offset, dtype, shape)."""
+
+    _KEYS = ("head", "start", "units", "block")
+
+    def __init__(self, enc_p, enc_q):
+        import numpy as np
+
+        torch = _torch()
+        self.layout, off, parts = {}, 0, []
+        for side, enc in (("p", enc_p), ("q", enc_q)):
+            lay = {}
+            for k in self._KEYS:
+                a = np.ascontiguousarray(enc[k])
+                lay[k] = (off, a.dtype, a.shape)
+                parts.append((off, a))
+                off += (a.nbytes + 15) & ~15
+            self.layout[side] = lay
+        self.nbytes = off
+        self.host = torch.empty(max(off, 16), dtype=torch.uint8)
+        if torch.cuda.is_available():
+            self.host = self.host.pin_memory()
+        hv = self.host.numpy()
+        for o, a in parts:
+            hv[o: o + a.nbytes] = a.view(np.uint8).reshape(-1)
+        self.n = {side: int(self.layout[side]["head"][2][0]) for side in ("p", "q")}
+
+    def views(self, dev_buf):
+        """Typed views of a device byte buffer holding a copy of self.host."""
+        import numpy as np
+
+        torch = _torch()
+        tmap = {np.dtype(np.uint16): torch.int16, np.dtype(np.int16): torch.int16, np.dtype(np.int64): torch.int64}
+        out = {}
+        for side, lay in self.layout.items():
+            out[side] = {}
+            for k, (o, dt, shape) in lay.items():
+                nb = int(np.prod(shape)) * np.dtype(dt).itemsize
+                out[side][k] = dev_buf[o: o + nb].view(tmap[np.dtype(dt)]).view(shape)
+        return out
 
 
 def touches(P: DeviceSet, Q: DeviceSet, pairs, inter, stream=None):

@@ -28,16 +28,10 @@ echo "ncu probe rc=$?"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:item_kernel -s 1 -c 1 \
   -o $OUT/ncu_item_kernel_combs -f python bench.py --config combs --steps 1 --warmup 3 --no-cpu-baseline --no-extras --e2e-steps 1 > $OUT/ncu_item.txt 2>&1
 echo "ncu item rc=$?"
-for tool in memcheck racecheck synccheck; do
-  timeout 1200 compute-sanitizer --tool $tool --error-exitcode 9 python scripts/sanitize_case.py > $OUT/sanitize_$tool.txt 2>&1
-  echo "sanitizer $tool rc=$?" | tee -a $OUT/sanitize_summary.txt
-  tail -3 $OUT/sanitize_$tool.txt >> $OUT/sanitize_summary.txt
-done
-for tool in memcheck racecheck; do
-  SANITIZE_INDEX=1 timeout 1500 compute-sanitizer --tool $tool --error-exitcode 9 python scripts/sanitize_case.py > $OUT/sanitize_index_$tool.txt 2>&1
-  echo "sanitizer (indexed large path) $tool rc=$?" | tee -a $OUT/sanitize_summary_index.txt
-  tail -3 $OUT/sanitize_index_$tool.txt >> $OUT/sanitize_summary_index.txt
-done
+# compute-sanitizer runs (memcheck, racecheck, synccheck; SANITIZE_INDEX=1 for the indexed large path):
+# the sanitizer is closed on this pool since round 2's last sessions, so the committed
+# profiles/r02/sanitize*.txt are from the earlier library; run by hand where it is available:
+#   compute-sanitizer --tool memcheck --error-exitcode 9 python scripts/sanitize_case.py
 for c in tile skewed combs; do
   timeout 900 python bench.py --config $c --steps 20 --warmup 3 --no-cpu-baseline > $OUT/bench_$c.json 2> $OUT/bench_$c.err
   echo "bench $c rc=$?"

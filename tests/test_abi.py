@@ -292,3 +292,18 @@ def test_encode_rect_packed_roundtrip_and_rejects(tile_sets):
                 _rect_ring(rng, 0, 0, 8191)):  # 8192 vertices
         Q = synth.pack([sq, bad])
         assert sccg.encode_rect_packed(Q.xy, Q.offsets) is None
+
+
+def test_packed_step_layout(tile_sets):
+    """sccg.PackedStep (both sets' packed encodings in one host buffer, one
+    host -> device copy per step): every field comes back bit-identical through
+    the typed views, 16-byte aligned."""
+    A, B = tile_sets[0], tile_sets[1]
+    encs = [sccg.encode_rect_packed(S.xy, S.offsets) for S in (A, B)]
+    st = sccg.PackedStep(*encs)
+    v = st.views(st.host)
+    for side, e in zip(("p", "q"), encs):
+        for k, a in e.items():
+            assert st.layout[side][k][0] % 16 == 0
+            assert np.array_equal(v[side][k].numpy().view(a.dtype), a), (side, k)
+    assert st.n == {"p": A.n, "q": B.n}

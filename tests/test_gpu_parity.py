@@ -1103,5 +1103,8 @@ def test_streamer_matches_pipeline(sccg):
         got = [st.result(t) for t in tickets]
         tickets = [st.submit(enc[0], enc[1]) for _ in range(2)]
         got += [st.result(t) for t in tickets]
+        step = sccg.PackedStep(*(sccg.encode_rect_packed(S.xy, S.offsets) for S in (A, B)))  # one copy per step
+        tickets = [st.submit_step(step) for _ in range(3)]
+        got += [st.result(t) for t in tickets[1:]]
         for g in got:
             assert [getattr(g, f) for f in sccg.SUMS_FIELDS] == ref
