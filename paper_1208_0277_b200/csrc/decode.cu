@@ -93,52 +93,6 @@ constexpr int kRpUnits = 4096;  // 16-bit units (8 KB)
 constexpr size_t kRpSmem = kRpStage * sizeof(int2) + kRpUnits * sizeof(unsigned short);
 }  // namespace
 
-// One ring's moves by one thread, C moves of BITS bits per 16-bit unit
-// (compile-time: the threads of a warp take rings of one width class, see
-// below).  a accumulates the axis of the even moves (move i leads to vertex
-// i + 1, which changes y iff (i + 1 odd) == vert), b the odd ones.
-template <int C, int BITS>
-__device__ __forceinline__ void rp_walk(const unsigned short* __restrict__ up, int m, int vert, int x, int y,
-                                        int2* __restrict__ dst) {
-  int a = vert ? y : x, b = vert ? x : y;
-  auto put = [&](int i) { dst[i + 1] = vert ? make_int2(b, a) : make_int2(a, b); };
-  auto dec = [&](unsigned w, int t) {
-    if (BITS == 16) return (int)(short)(w & 0xffffu);
-    const unsigned c = (w >> (BITS * t)) & ((1u << BITS) - 1u);
-    const int mag = (int)(c & ((1u << (BITS - 1)) - 1u)) + 1;
-    return (c >> (BITS - 1)) ? -mag : mag;
-  };
-  if (C == 1) {  // one move per unit: two units per iteration keep the axis pattern static
-    int i = 0;
-    for (; i + 2 <= m; i += 2) {
-      const int d0 = dec(up[i], 0), d1 = dec(up[i + 1], 0);
-      a += d0;
-      put(i);
-      b += d1;
-      put(i + 1);
-    }
-    if (i < m) {
-      a += dec(up[i], 0);
-      put(i);
-    }
-  } else {
-    for (int u = 0; u * C < m; u++) {
-      const unsigned w = up[u];
-#pragma unroll
-      for (int t = 0; t < C; t++) {
-        const int i = u * C + t;
-        if (i < m) {
-          if ((t & 1) == 0)
-            a += dec(w, t);
-          else
-            b += dec(w, t);
-          put(i);
-        }
-      }
-    }
-  }
-}
-
 // CTA per block of kRpBlock rings, thread per ring: heads -> block scan of
 // (vertices, units) -> the block's offsets; units staged; each thread walks
 // its ring's moves (vertex k >= 1 changes y iff (k odd) == the first-vertical
@@ -154,10 +108,6 @@ __global__ void __launch_bounds__(kRpBlock) decode_rect_packed_kernel(const unsi
   unsigned short* s_units = reinterpret_cast<unsigned short*>(rp_smem + kRpStage * sizeof(int2));
   __shared__ int s_warp[2][kRpWarps];
   __shared__ int s_lim;
-  __shared__ int s_cls[3][kRpWarps];
-  __shared__ int4 s_ring[kRpBlock];  // per ring: vertex / unit offsets in the block, head | flags, units
-  __shared__ int2 s_xy0[kRpBlock];
-  __shared__ unsigned char s_perm[kRpBlock];
   pdl_entry();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t b = blockIdx.x, r = b * kRpBlock + threadIdx.x;
@@ -217,51 +167,26 @@ __global__ void __launch_bounds__(kRpBlock) decode_rect_packed_kernel(const unsi
   const int nus = min(tu, kRpUnits);
   for (int i = threadIdx.x; i < nus; i += kRpBlock) s_units[i] = units[ubase + i];
   __syncthreads();
-  // rings are walked by threads sorted by width class (a stable counting
-  // sort over the block), so a warp's threads run one specialised loop
-  {
-    const int cls = r < n ? (h >> 13) & 3 : 3;
-    const unsigned m0 = __ballot_sync(0xffffffffu, cls == 0), m1 = __ballot_sync(0xffffffffu, cls == 1),
-                   m2 = __ballot_sync(0xffffffffu, cls == 2);
-    if (lane == 0) {
-      s_cls[0][warp] = __popc(m0);
-      s_cls[1][warp] = __popc(m1);
-      s_cls[2][warp] = __popc(m2);
-    }
-    s_ring[threadIdx.x] = make_int4(v0, u0, h | (staged ? 0x10000 : 0) | (r < n ? 0x20000 : 0), nu);
-    s_xy0[threadIdx.x] = make_int2(x, y);
-    __syncthreads();
-    int base = 0, before = 0;
-    for (int c = 0; c < 4; c++) {
-      int tot = 0, pre = 0;
-      for (int w = 0; w < kRpWarps; w++) {
-        const int cnt = c < 3 ? s_cls[c][w] : 32 - s_cls[0][w] - s_cls[1][w] - s_cls[2][w];
-        tot += cnt;
-        pre += w < warp ? cnt : 0;
-      }
-      if (c == cls) before = base + pre;
-      base += tot;
-    }
-    const unsigned mine = cls == 0 ? m0 : cls == 1 ? m1 : cls == 2 ? m2 : ~(m0 | m1 | m2);
-    s_perm[before + __popc(mine & lanemask_lt())] = (unsigned char)threadIdx.x;
-  }
-  __syncthreads();
-  {
-    const int jr = s_perm[threadIdx.x];
-    const int4 ri = s_ring[jr];
-    const int hj = ri.z & 0xffff, Vj = hj & 0x1fff, wj = (hj >> 13) & 3, vert = hj >> 15;
-    if ((ri.z & 0x20000) && Vj > 0) {
-      const int2 p0 = s_xy0[jr];
-      const unsigned short* up = ri.y + ri.w <= kRpUnits ? s_units + ri.y : units + ubase + ri.y;
-      int2* dst = (ri.z & 0x10000) ? s_stage + ri.x : xy + vbase + ri.x;
-      dst[0] = p0;
-      const int m = Vj - 1;
-      if (wj == 0)
-        rp_walk<4, 4>(up, m, vert, p0.x, p0.y, dst);
-      else if (wj == 1)
-        rp_walk<2, 8>(up, m, vert, p0.x, p0.y, dst);
-      else
-        rp_walk<1, 16>(up, m, vert, p0.x, p0.y, dst);
+  if (r < n && V > 0) {
+    const int w = (h >> 13) & 3, vert = h >> 15;
+    const int lc = w == 0 ? 2 : w == 1 ? 1 : 0;  // log2(moves per unit)
+    const int bits = 16 >> lc;
+    const unsigned mask = bits == 16 ? 0xffffu : (1u << bits) - 1u, mmag = mask >> 1;
+    const unsigned short* up = u0 + nu <= kRpUnits ? s_units + u0 : units + ubase + u0;
+    int2* dst = staged ? s_stage + v0 : xy + vbase + v0;
+    dst[0] = make_int2(x, y);
+    const int cm = (1 << lc) - 1;
+    unsigned cur = 0u;
+    for (int k = 1; k < V; k++) {
+      const int mi = k - 1;
+      if ((mi & cm) == 0) cur = up[mi >> lc];  // a unit is read once (predicated, not per move)
+      const unsigned code = (cur >> ((mi & cm) * bits)) & mask;
+      const int mag = (int)(code & mmag) + 1;
+      const int d = bits == 16 ? (int)(short)code : ((code > mmag) ? -mag : mag);
+      const bool ymove = (k & 1) == vert;
+      x += ymove ? 0 : d;
+      y += ymove ? d : 0;
+      dst[k] = make_int2(x, y);
     }
   }
   __syncthreads();
