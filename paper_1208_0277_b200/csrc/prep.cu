@@ -50,6 +50,9 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar) {
 // SCCG_PREP_EVICT_FIRST: the vertex tiles are read once per step (nothing
 // downstream of prep on the nucleus path reads xy), so their L2 lines are
 // marked evict-first and the derived buffers PixelBox reads next keep L2.
+#ifndef SCCG_PREP_RASTER
+#define SCCG_PREP_RASTER 1  // memoized pixelization: prep stores each eligible ring's raster rows
+#endif
 #ifndef SCCG_PREP_EVICT_FIRST
 #define SCCG_PREP_EVICT_FIRST 0
 #endif
@@ -122,7 +125,7 @@ __device__ __forceinline__ void flag(uint32_t* status, uint32_t bit, int64_t pol
 __device__ __forceinline__ int4 prep_polygon(const int2* v, int64_t V, int64_t poly, uint64_t* out,
                                              int4* __restrict__ mbr, int64_t* __restrict__ area,
                                              int2* __restrict__ ecount, uint32_t* __restrict__ status,
-                                             int validate, int& nv_out) {
+                                             int validate, bool rast_ok, int& nv_out) {
   nv_out = 0;
   const int lane = threadIdx.x & 31;
   int xmin = INT_MAX, ymin = INT_MAX, xmax = INT_MIN, ymax = INT_MIN;
@@ -177,10 +180,30 @@ __device__ __forceinline__ int4 prep_polygon(const int2* v, int64_t V, int64_t p
   for (int o = 16; o; o >>= 1) twice_area += __shfl_xor_sync(0xffffffffu, twice_area, o);
   diag = __any_sync(0xffffffffu, diag);
   nv_out = nvert;  // warp-uniform
+  // Raster (as the thread path; ring in the shared-memory tile): lane per row,
+  // each row word the XOR of the suffix masks of the records crossing it
+  // (records read by broadcast), stored after the records.
+  const int W = xmax - xmin, H = ymax - ymin;
+  const bool raster = SCCG_PREP_RASTER && rast_ok && !diag && W <= 32 && H <= 128 && 2 * (V - nvert) >= H;
+  if (raster) {
+    unsigned* D = reinterpret_cast<unsigned*>(out + nvert);
+    const unsigned wm = low_bits(W);
+    for (int r0 = 0; r0 < H; r0 += 32) {
+      const int r = r0 + lane;
+      unsigned w = 0u;
+      for (int k = 0; k < nvert; k++) {
+        int c, lo, hi;
+        unpack_edge(out[k], c, lo, hi);
+        if (lo <= r && r < hi) w ^= shl_clamp(0xffffffffu, (unsigned)c);
+      }
+      if (r < H) D[r] = w & wm;
+    }
+    __syncwarp();
+  }
   if (lane == 0) {
     area[poly] = (twice_area < 0 ? -twice_area : twice_area) / 2;
     mbr[poly] = m;
-    ecount[poly] = make_int2(nvert, 0);  // records relative to the MBR origin: zero rebase
+    ecount[poly] = make_int2(nvert | (raster ? kRasterFlag : 0), 0);  // records relative to the MBR origin: zero rebase
     (void)nhor;
     if (validate && diag) flag(status, SCCG_STATUS_NOT_RECTILINEAR, poly);
   }
@@ -300,9 +323,6 @@ __device__ __forceinline__ int4 prep_polygon_thread(int2* v, int V, int rot, int
   // vertical edge XORs its suffix mask into rows lo and hi (paired per row
   // below) -- then a prefix XOR over rows.  Stored in the slot's free tail (words 2 nv .. 2 nv + H), which
   // exists when 2 (V - nv) >= H; MBR width <= 32.
-#ifndef SCCG_PREP_RASTER
-#define SCCG_PREP_RASTER 1
-#endif
   bool raster = SCCG_PREP_RASTER && !diag && W <= 32 && 2 * (V - nvert) >= H;
   if (raster) {
     // In ring order a record's exit row is the next record's entry row -- y
@@ -746,7 +766,7 @@ __global__ void __launch_bounds__(kPrepThreads, SCCG_PREP_MINB) prep_kernel(cons
         int2* src = tiled ? s_xy + (b - v0) : const_cast<int2*>(xy) + b;
         uint64_t* out = tiled ? reinterpret_cast<uint64_t*>(src) : edges + b;
         int nv;
-        const int4 m = prep_polygon(src, e - b, poly, out, mbr, area, ecount, status, validate, nv);
+        const int4 m = prep_polygon(src, e - b, poly, out, mbr, area, ecount, status, validate, tiled, nv);
         if (lane == 0) acc.add(m);
 #if SCCG_PREP_USED_ONLY
         if (tiled) {  // records are in the tile: write them back
