@@ -335,16 +335,22 @@ SCCG_API int sccg_decode_rect(const int32_t* start, const int16_t* move, const u
                               const int64_t* offsets, int64_t n, int32_t* xy, sccg_stream_t stream);
 
 /* Packed rectilinear rings (format 2): the compact encoding above with each ring's moves at the narrowest of
- * three widths and no offsets on the wire (rectilinear rings; segmentation contours traced from a mask
- * move 1-3 pixels at a time, so 4-bit moves cover ~99 % of them: ~0.6 bytes per vertex instead of 2 + 8 per ring).
+ * four codings and no offsets on the wire (rectilinear rings; segmentation contours traced from a mask
+ * move 1-3 pixels at a time, so a variable-length code takes ~2.2 bits per move instead of 16 + 64 per ring).
  * Rings are grouped in blocks of SCCG_RECTP_BLOCK consecutive rings (the last one partial).
- *   head[i]   uint16: vertex count V_i (bits 0-12, V_i <= 8191) | width class w_i << 13 (0: 4-bit moves, 1: 8-bit,
- *             2: 16-bit) | (first edge vertical) << 15.
- *   units     uint16 stream: ring i's V_i - 1 moves fill ceil((V_i - 1) / c) units from unit u_i on, c = 4, 2, 1 moves
- *             per unit; move j of a unit sits in bits [j * b, (j + 1) * b), b = 16 / c.  A 4- or 8-bit move is
- *             sign (top bit) and magnitude - 1 (|d| <= 8 / 128; moves are never 0); a 16-bit move is int16.
- *             Vertex k >= 1 of ring i moves from vertex k - 1 along x or y, alternating, the first move along y iff
- *             head bit 15 is set.  u_i = block[b][1] + the units of the block's earlier rings.
+ *   head[i]   uint16: vertex count V_i (bits 0-12, V_i <= 8191) | coding class w_i << 13 | (first edge vertical)
+ *             << 15.  Vertex k >= 1 of ring i moves from vertex k - 1 by d along x or y, alternating, the first
+ *             move along y iff head bit 15 is set; d != 0.
+ *   units     uint16 stream: ring i's moves fill its units from unit u_i on (u_i = block[b][1] + the units of the
+ *             block's earlier rings).  w = 0, 1, 2: fixed width, c = 4, 2, 1 moves per unit, move j of a unit in
+ *             bits [j * b, (j + 1) * b), b = 16 / c, ceil((V_i - 1) / c) units; a 4- or 8-bit move is sign (top
+ *             bit) and |d| - 1 (|d| <= 8 / 128); a 16-bit move is int16.  w = 3: variable length, vlen[i] units
+ *             (<= 255): the units are one bit stream read from bit 0 of the first unit upward (unit j holds bits
+ *             16j .. 16j + 15); move k - 1 is the symbol s = 2 (|d| - 1) + f, f = 1 iff the sign of d differs from
+ *             that of the previous move along the same axis (for the first move along each axis: from +), coded as
+ *             exp-Golomb LSB first: L zero bits, a one bit, then the L low bits of s + 1 (least significant
+ *             first), L = floor(log2(s + 1)); |d| <= 127.
+ *   vlen      uint8 [n]: units of ring i when w_i = 3 (read only then; may be NULL when no ring uses w = 3).
  *   start     int16 stream: ring j of block b starts at (x0 + start[s + 2j], y0 + start[s + 2j + 1]) when block b is
  *             narrow, at the int32 pair whose 16-bit halves are start[s + 4j .. s + 4j + 3] (x lo, x hi, y lo, y hi)
  *             when it is wide; s = block[b][2] & (2^62 - 1), wide = bit 62 of block[b][2], x0 = (int32) low half of
@@ -356,9 +362,9 @@ SCCG_API int sccg_decode_rect(const int32_t* start, const int16_t* move, const u
  * Device pointers; units / start 2-byte aligned, block / offsets / xy 8-byte aligned; n >= 0 (n = 0 writes
  * offsets[0] = 0).  Asynchronous.  Errors: SCCG_E_ARG for a negative n or a null / misaligned pointer. */
 #define SCCG_RECTP_BLOCK 256
-SCCG_API int sccg_decode_rect_packed(const uint16_t* head, const int16_t* start, const uint16_t* units,
-                                     const int64_t* block, int64_t n, int64_t* offsets, int32_t* xy,
-                                     sccg_stream_t stream);
+SCCG_API int sccg_decode_rect_packed(const uint16_t* head, const uint8_t* vlen, const int16_t* start,
+                                     const uint16_t* units, const int64_t* block, int64_t n, int64_t* offsets,
+                                     int32_t* xy, sccg_stream_t stream);
 
 /* ------------------------------------------------------------------ misc */
 SCCG_API const char* sccg_strerror(int code);

@@ -148,7 +148,7 @@ def load(build: bool = True):
         lib.sccg_pixelbox_index_bytes.restype = sz
         lib.sccg_decode_rect.argtypes = [vp, vp, vp, vp, i64, vp, vp]
         lib.sccg_decode_rect.restype = cint
-        lib.sccg_decode_rect_packed.argtypes = [vp, vp, vp, vp, i64, vp, vp, vp]
+        lib.sccg_decode_rect_packed.argtypes = [vp, vp, vp, vp, vp, i64, vp, vp, vp]
         lib.sccg_decode_rect_packed.restype = cint
         lib.sccg_pixelbox.argtypes = [ps, ps, vp, i64, vp, vp, vp, ctypes.POINTER(Config), vp, sz, vp]
         lib.sccg_pixelbox.restype = cint
@@ -630,9 +630,10 @@ class Streamer:
             Q = DeviceSet(sl["xy_q"][:nv_q], sl["off_q"], prep=False)
             sl["sets"] = (P, Q)
             sl["pipe"] = Pipeline(P, Q, cap=cap, threshold=threshold, graph=True, readback=[sl["rb"]])
-            sl["copied"], sl["done"] = torch.cuda.Event(), torch.cuda.Event()
+            sl["copied"], sl["done"], sl["decoded"] = torch.cuda.Event(), torch.cuda.Event(), torch.cuda.Event()
             self.slots.append(sl)
         self.copy_stream = torch.cuda.Stream(device=dev)
+        self.decode_stream = torch.cuda.Stream(device=dev)
         self.count = 0
 
     def submit(self, enc_p, enc_q) -> int:
@@ -686,10 +687,15 @@ class Streamer:
                 buf = sl["step_buf"] = torch.empty(max(step.nbytes, 16), dtype=torch.uint8, device=self.device)
             buf[: step.nbytes].copy_(step.host[: step.nbytes], non_blocking=True)
             sl["copied"].record(cs)
-        main.wait_event(sl["copied"])
+        # the decode runs on its own stream: step i + 1's decode overlaps step i's graph
+        ds = self.decode_stream
+        ds.wait_event(sl["copied"])
         v = step.views(buf)
-        for side, nv in (("p", nv_p), ("q", nv_q)):
-            decode_rect_packed(v[side], nv, out=(sl["xy_" + side], sl["off_" + side]))
+        with torch.cuda.stream(ds):
+            for side, nv in (("p", nv_p), ("q", nv_q)):
+                decode_rect_packed(v[side], nv, stream=ds, out=(sl["xy_" + side], sl["off_" + side]))
+            sl["decoded"].record(ds)
+        main.wait_event(sl["decoded"])
         sl["pipe"].run(slot=0)
         sl["done"].record(main)
         self.count += 1
@@ -718,7 +724,7 @@ class PackedStep:
     aligned fields), so a step's inputs cross PCIe as one copy
     (Streamer.submit_step).  layout[side][key] = (byte offset, dtype, shape)."""
 
-    _KEYS = ("head", "start", "units", "block")
+    _KEYS = ("head", "vlen", "start", "units", "block")
 
     def __init__(self, enc_p, enc_q):
         import numpy as np
@@ -747,7 +753,8 @@ class PackedStep:
         import numpy as np
 
         torch = _torch()
-        tmap = {np.dtype(np.uint16): torch.int16, np.dtype(np.int16): torch.int16, np.dtype(np.int64): torch.int64}
+        tmap = {np.dtype(np.uint16): torch.int16, np.dtype(np.int16): torch.int16, np.dtype(np.int64): torch.int64,
+                np.dtype(np.uint8): torch.uint8}
         out = {}
         for side, lay in self.layout.items():
             out[side] = {}
@@ -986,12 +993,15 @@ def decode_rect(start, move, first_vertical, offsets, stream=None):
 RECTP_BLOCK = 256  # SCCG_RECTP_BLOCK
 
 
-def encode_rect_packed(xy, offsets):
+def encode_rect_packed(xy, offsets, vlc: bool = True):
     """Packed rectilinear rings (sccg_decode_rect_packed, format 2 in
-    include/sccg.h): dict of numpy arrays head uint16 [n], start int16 [...],
-    units uint16 [...], block int64 [ceil(n / 256), 4] -- each ring's moves at
-    the narrowest of 4, 8 or 16 bits, starts as int16 deltas from the block's
-    first start where they fit, no offsets.  None when some ring is not
+    include/sccg.h): dict of numpy arrays head uint16 [n], vlen uint8 [n],
+    start int16 [...], units uint16 [...], block int64 [ceil(n / 256), 4] --
+    each ring's moves variable-length coded (class 3: exp-Golomb symbols of
+    magnitude and sign flip, ~2.2 bits per move on segmentation contours) or,
+    where that cannot hold them, at the narrowest of 4, 8 or 16 bits; starts as
+    int16 deltas from the block's first start where they fit; no offsets.
+    vlc=False keeps the fixed widths only.  None when some ring is not
     encodable (more than 8191 vertices, a zero-length or non-alternating move,
     a move beyond int16).  Host-side numpy; lossless: the device decode is
     exact.  Rings with 0 vertices are allowed."""
@@ -1027,25 +1037,59 @@ def encode_rect_packed(xy, offsets):
     if nm:
         np.maximum.at(amax, ring, a)
     w = np.where(amax <= 8, 0, np.where(amax <= 128, 1, 2))
-    c = np.array([4, 2, 1])[w]
-    nu = (m + c - 1) // c
+    # variable-length class: symbol 2 (|d| - 1) + flip (sign vs the previous move on the same axis, the first
+    # one on each axis vs +), exp-Golomb LSB first (2 L + 1 bits, L = floor(log2(symbol + 1)))
+    neg = (mv < 0).astype(np.int64)
+    prev = np.zeros(nm, np.int64)
+    back2 = j >= 2
+    prev[back2] = neg[np.nonzero(back2)[0] - 2]
+    sym = 2 * (a - 1) + (neg ^ prev)
+    v = sym + 1
+    L = np.zeros(nm, np.int64)
+    if nm:
+        L = np.floor(np.log2(v.astype(np.float64))).astype(np.int64)
+        L += (np.left_shift(1, L + 1) <= v).astype(np.int64)  # guard float rounding
+        L -= (np.left_shift(1, L) > v).astype(np.int64)
+    ln = 2 * L + 1
+    code = np.left_shift(1, L) | np.left_shift(v & (np.left_shift(1, L) - 1), L + 1)
+    rbits = np.bincount(ring, weights=ln, minlength=n).astype(np.int64) if nm else np.zeros(n, np.int64)
+    vunits = (rbits + 15) // 16
+    if vlc:
+        w = np.where((amax <= 127) & (vunits <= 255) & (m > 0), 3, w)
+    c = np.array([4, 2, 1, 1])[w]
+    nu = np.where(w == 3, vunits, (m + c - 1) // c)
     u0 = np.cumsum(nu) - nu  # global unit offset of each ring
     head = (V | (w << 13) | (fv << 15)).astype(np.uint16)
-    # units: 4-bit nibbles of a flat array, 4 per unit
-    nib = np.zeros(4 * int(nu.sum()), np.int64)
-    wr, cr = w[ring], c[ring]
+    vlen = np.where(w == 3, vunits, 0).astype(np.uint8)
+    units = np.zeros(int(nu.sum()), np.int64)
+    wr = w[ring]
+    # fixed classes: 4-bit nibbles of a flat array, 4 per unit
+    fx = wr < 3
+    nib = np.zeros(4 * units.shape[0], np.int64)
+    cr = c[ring]
     pos = 4 * (u0[ring] + j // cr) + (j % cr) * (4 // cr)
-    small = wr < 2
+    small = fx & (wr < 2)
     bits = np.where(wr == 0, 4, 8)
-    code = np.where(mv < 0, 1, 0) << (bits - 1) | (a - 1)
+    fcode = np.where(mv < 0, 1, 0) << (bits - 1) | (a - 1)
     for k in range(2):  # an 8-bit code spans two nibbles
         sel = small & ((wr == 1) | (k == 0))
-        nib[pos[sel] + k] = (code[sel] >> (4 * k)) & 15
-    big = ~small
+        nib[pos[sel] + k] = (fcode[sel] >> (4 * k)) & 15
+    big = fx & (wr == 2)
     v16 = mv[big] & 0xFFFF
     for k in range(4):
         nib[pos[big] + k] = (v16 >> (4 * k)) & 15
-    units = (nib[0::4] | nib[1::4] << 4 | nib[2::4] << 8 | nib[3::4] << 12).astype(np.uint16)
+    units |= nib[0::4] | nib[1::4] << 4 | nib[2::4] << 8 | nib[3::4] << 12
+    # variable-length class: each code at its ring's bit offset (a code spans at most two units)
+    vl = wr == 3
+    if vl.any():
+        bo = np.cumsum(ln) - ln - np.repeat(np.cumsum(rbits) - rbits, m)  # bit offset of each move in its ring
+        bp = 16 * u0[ring] + bo
+        sel = np.nonzero(vl)[0]
+        ui, sh, cd = bp[sel] >> 4, bp[sel] & 15, code[sel]
+        np.bitwise_or.at(units, ui, (cd << sh) & 0xFFFF)
+        spill = sh + ln[sel] > 16
+        np.bitwise_or.at(units, ui[spill] + 1, cd[spill] >> (16 - sh[spill]))
+    units = units.astype(np.uint16)
     # starts: per block of RECTP_BLOCK rings, int16 deltas from its first start or int32 pairs
     nb = (n + RECTP_BLOCK - 1) // RECTP_BLOCK
     block = np.zeros((max(nb, 0), 4), np.int64)
@@ -1068,7 +1112,7 @@ def encode_rect_packed(xy, offsets):
         parts.append(part.astype(np.uint16))
         soff += part.shape[0]
     start = (np.concatenate(parts) if parts else np.zeros(0, np.uint16)).view(np.int16)
-    return dict(head=head, start=start, units=units, block=block)
+    return dict(head=head, vlen=vlen, start=start, units=units, block=block)
 
 
 def decode_rect_packed(enc, n_vertices: int, stream=None, out=None):
@@ -1085,8 +1129,10 @@ def decode_rect_packed(enc, n_vertices: int, stream=None, out=None):
     else:
         xy, off = out
     ptr = lambda t: t.data_ptr() if t.numel() else None  # noqa: E731
-    _check(load().sccg_decode_rect_packed(ptr(head), ptr(enc["start"]), ptr(enc["units"]), ptr(enc["block"]), n,
-                                          off.data_ptr(), xy.data_ptr(), _stream_ptr(stream)),
+    vl = enc.get("vlen")
+    _check(load().sccg_decode_rect_packed(ptr(head), ptr(vl) if vl is not None else None, ptr(enc["start"]),
+                                          ptr(enc["units"]), ptr(enc["block"]), n, off.data_ptr(), xy.data_ptr(),
+                                          _stream_ptr(stream)),
            "sccg_decode_rect_packed")
     return xy[:n_vertices], off
 

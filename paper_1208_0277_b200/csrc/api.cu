@@ -37,8 +37,8 @@ int check_cuda(cudaError_t e, const char* where) {
 
 int decode_rect(const int32_t* start, const int16_t* move, const uint8_t* first_vertical, const int64_t* offsets,
                 int64_t n, int32_t* xy, cudaStream_t stream);
-int decode_rect_packed(const uint16_t* head, const int16_t* start, const uint16_t* units, const int64_t* block,
-                       int64_t n, int64_t* offsets, int32_t* xy, cudaStream_t stream);
+int decode_rect_packed(const uint16_t* head, const uint8_t* vlen, const int16_t* start, const uint16_t* units,
+                       const int64_t* block, int64_t n, int64_t* offsets, int32_t* xy, cudaStream_t stream);
 size_t filter_ws_bytes(int64_t np, int64_t nq);
 int filter_pairs(const sccg_polyset* P, const sccg_polyset* Q, int32_t* pairs, int64_t cap, int64_t* n_pairs_host,
                  void* ws, size_t ws_bytes, int closed, cudaStream_t stream);
@@ -386,14 +386,15 @@ int sccg_jaccard(const sccg_sums* s, double* jprime, double* pooled) {
   return SCCG_OK;
 }
 
-int sccg_decode_rect_packed(const uint16_t* head, const int16_t* start, const uint16_t* units, const int64_t* block,
-                            int64_t n, int64_t* offsets, int32_t* xy, sccg_stream_t stream) {
+int sccg_decode_rect_packed(const uint16_t* head, const uint8_t* vlen, const int16_t* start, const uint16_t* units,
+                            const int64_t* block, int64_t n, int64_t* offsets, int32_t* xy, sccg_stream_t stream) {
   NvtxRange nvtx_range("sccg_decode_rect_packed");
   set_error(SCCG_OK, "", -1);
   if (n < 0 || !offsets || (n > 0 && (!head || !start || !block || !xy)) || !aligned(head, 2) ||
       !aligned(start, 2) || !aligned(units, 2) || !aligned(block, 8) || !aligned(offsets, 8) || !aligned(xy, 8))
     return set_error(SCCG_E_ARG, "sccg_decode_rect_packed: bad size or null / misaligned pointer");
-  return sccg::decode_rect_packed(head, start, units, block, n, offsets, xy, reinterpret_cast<cudaStream_t>(stream));
+  return sccg::decode_rect_packed(head, vlen, start, units, block, n, offsets, xy,
+                                  reinterpret_cast<cudaStream_t>(stream));
 }
 
 }  // extern "C"

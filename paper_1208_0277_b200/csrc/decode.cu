@@ -99,6 +99,7 @@ constexpr size_t kRpSmem = kRpStage * sizeof(int2) + kRpUnits * sizeof(unsigned 
 // bit; the width class selects 4, 2 or 1 moves per unit) writing vertices into
 // the staged block; the staged range is stored coalesced.
 __global__ void __launch_bounds__(kRpBlock) decode_rect_packed_kernel(const unsigned short* __restrict__ head,
+                                                                      const unsigned char* __restrict__ vlen,
                                                                       const short* __restrict__ start,
                                                                       const unsigned short* __restrict__ units,
                                                                       const long long* __restrict__ block, int64_t n,
@@ -122,7 +123,8 @@ __global__ void __launch_bounds__(kRpBlock) decode_rect_packed_kernel(const unsi
   if (r < n) {
     h = head[r];
     V = h & 0x1fff;
-    nu = rp_units(max(V - 1, 0), (h >> 13) & 3);
+    const int w = (h >> 13) & 3;
+    nu = w == 3 ? (int)vlen[r] : rp_units(max(V - 1, 0), w);
     const int j = threadIdx.x;
     if (wide) {
       const unsigned short* sp = reinterpret_cast<const unsigned short*>(start) + soff + 4 * j;
@@ -169,24 +171,58 @@ __global__ void __launch_bounds__(kRpBlock) decode_rect_packed_kernel(const unsi
   __syncthreads();
   if (r < n && V > 0) {
     const int w = (h >> 13) & 3, vert = h >> 15;
-    const int lc = w == 0 ? 2 : w == 1 ? 1 : 0;  // log2(moves per unit)
-    const int bits = 16 >> lc;
-    const unsigned mask = bits == 16 ? 0xffffu : (1u << bits) - 1u, mmag = mask >> 1;
     const unsigned short* up = u0 + nu <= kRpUnits ? s_units + u0 : units + ubase + u0;
     int2* dst = staged ? s_stage + v0 : xy + vbase + v0;
     dst[0] = make_int2(x, y);
-    const int cm = (1 << lc) - 1;
-    unsigned cur = 0u;
-    for (int k = 1; k < V; k++) {
-      const int mi = k - 1;
-      if ((mi & cm) == 0) cur = up[mi >> lc];  // a unit is read once (predicated, not per move)
-      const unsigned code = (cur >> ((mi & cm) * bits)) & mask;
-      const int mag = (int)(code & mmag) + 1;
-      const int d = bits == 16 ? (int)(short)code : ((code > mmag) ? -mag : mag);
-      const bool ymove = (k & 1) == vert;
-      x += ymove ? 0 : d;
-      y += ymove ? d : 0;
-      dst[k] = make_int2(x, y);
+    if (w == 3) {
+      // variable-length moves: symbol s = 2 (|d| - 1) + flip, flip = the sign
+      // differs from the previous move on the same axis (the first one on each
+      // axis: from +), exp-Golomb coded LSB-first -- L zero bits, a one, the
+      // L low bits of s + 1; bits refilled 16 at a time into a 64-bit buffer
+      // (a code is at most 15 bits: |d| <= 127)
+      unsigned long long b = 0ull;
+      int nb = 0, ui = 0;
+      int sa = 0, sb = 0;  // sign state of the axis of the even / odd moves
+      for (int k = 1; k < V; k++) {
+        if (nb < 16) {
+          b |= (unsigned long long)up[ui] << nb;
+          ui++;
+          nb += 16;
+        }
+        const int L = __ffsll((long long)b) - 1;
+        const unsigned v = (1u << L) | ((unsigned)(b >> (L + 1)) & ((1u << L) - 1u));
+        b >>= 2 * L + 1;
+        nb -= 2 * L + 1;
+        const int sym = (int)v - 1, mag = (sym >> 1) + 1;
+        const bool odd = ((k - 1) & 1) != 0;  // move k - 1
+        int sg = (odd ? sb : sa) ^ (sym & 1);
+        if (odd)
+          sb = sg;
+        else
+          sa = sg;
+        const int d = sg ? -mag : mag;
+        const bool ymove = (k & 1) == vert;
+        x += ymove ? 0 : d;
+        y += ymove ? d : 0;
+        dst[k] = make_int2(x, y);
+      }
+    } else {
+      const int lc = w == 0 ? 2 : w == 1 ? 1 : 0;  // log2(moves per unit)
+      const int bits = 16 >> lc;
+      const unsigned mask = bits == 16 ? 0xffffu : (1u << bits) - 1u, mmag = mask >> 1;
+      const int cm = (1 << lc) - 1;
+      unsigned cur = 0u;
+      for (int k = 1; k < V; k++) {
+        const int mi = k - 1;
+        if ((mi & cm) == 0) cur = up[mi >> lc];  // a unit is read once (predicated, not per move)
+        const unsigned code = (cur >> ((mi & cm) * bits)) & mask;
+        const int mag = (int)(code & mmag) + 1;
+        const int d = bits == 16 ? (int)(short)code : ((code > mmag) ? -mag : mag);
+        const bool ymove = (k & 1) == vert;
+        x += ymove ? 0 : d;
+        y += ymove ? d : 0;
+        dst[k] = make_int2(x, y);
+      }
     }
   }
   __syncthreads();
@@ -194,8 +230,8 @@ __global__ void __launch_bounds__(kRpBlock) decode_rect_packed_kernel(const unsi
   for (int i = threadIdx.x; i < lim; i += kRpBlock) xy[vbase + i] = s_stage[i];
 }
 
-int decode_rect_packed(const uint16_t* head, const int16_t* start, const uint16_t* units, const int64_t* block,
-                       int64_t n, int64_t* offsets, int32_t* xy, cudaStream_t stream) {
+int decode_rect_packed(const uint16_t* head, const uint8_t* vlen, const int16_t* start, const uint16_t* units,
+                       const int64_t* block, int64_t n, int64_t* offsets, int32_t* xy, cudaStream_t stream) {
   const int64_t nb = n > 0 ? (n + kRpBlock - 1) / kRpBlock : 1;
   static bool attr = false;
   if (!attr) {
@@ -203,7 +239,7 @@ int decode_rect_packed(const uint16_t* head, const int16_t* start, const uint16_
     attr = true;
   }
   launch_pdl(decode_rect_packed_kernel, dim3((unsigned)nb), dim3(kRpBlock), kRpSmem, stream,
-             reinterpret_cast<const unsigned short*>(head), reinterpret_cast<const short*>(start),
+             reinterpret_cast<const unsigned short*>(head), vlen, reinterpret_cast<const short*>(start),
              reinterpret_cast<const unsigned short*>(units), reinterpret_cast<const long long*>(block), n, offsets,
              reinterpret_cast<int2*>(xy));
   return check_cuda(cudaGetLastError(), "decode_rect_packed");

@@ -214,10 +214,35 @@ def _decode_rect_packed_host(enc, n):
                 y = int(np.uint32(q[2] | q[3] << 16).view(np.int32))
             else:
                 x, y = x0 + int(start[s + 2 * jr]), y0 + int(start[s + 2 * jr + 1])
-            c = (4, 2, 1)[wc]
-            bits = 16 // c
             if V > 0:
                 xy.append((x, y))
+            if wc == 3:  # variable length: a bit stream over vlen units, exp-Golomb symbols LSB first
+                nu = int(enc["vlen"][b * sccg.RECTP_BLOCK + jr])
+                stream = 0
+                for t in range(nu):
+                    stream |= int(units[u + t]) << (16 * t)
+                bit, sign = 0, [0, 0]
+                for k in range(1, V):
+                    L = 0
+                    while not (stream >> (bit + L)) & 1:
+                        L += 1
+                    low = (stream >> (bit + L + 1)) & ((1 << L) - 1)
+                    bit += 2 * L + 1
+                    sym = ((1 << L) | low) - 1
+                    ax = (k - 1) & 1
+                    sign[ax] ^= sym & 1
+                    dv = -((sym >> 1) + 1) if sign[ax] else (sym >> 1) + 1
+                    if ((k & 1) == 1) == (vert == 1):
+                        y += dv
+                    else:
+                        x += dv
+                    xy.append((x, y))
+                assert bit <= 16 * nu
+                u += nu
+                offs.append(offs[-1] + V)
+                continue
+            c = (4, 2, 1)[wc]
+            bits = 16 // c
             for k in range(1, V):
                 jm = k - 1
                 word = int(units[u + jm // c])
@@ -261,11 +286,15 @@ def test_encode_rect_packed_roundtrip_and_rejects(tile_sets):
     import synth
 
     for S in tile_sets:
-        enc = sccg.encode_rect_packed(S.xy, S.offsets)
-        xy, off = _decode_rect_packed_host(enc, S.n)
-        assert np.array_equal(off, S.offsets) and np.array_equal(xy, S.xy)
-        assert enc["units"].nbytes < 0.3 * S.xy.nbytes  # ~ 4-bit moves
-        assert ((enc["head"] >> 13 & 3) == 0).mean() > 0.5  # most rings: 4-bit moves
+        for vlc in (True, False):
+            enc = sccg.encode_rect_packed(S.xy, S.offsets, vlc=vlc)
+            xy, off = _decode_rect_packed_host(enc, S.n)
+            assert np.array_equal(off, S.offsets) and np.array_equal(xy, S.xy)
+            if vlc:  # ~2.2 bits per move
+                assert enc["units"].nbytes < 0.05 * S.xy.nbytes and ((enc["head"] >> 13) & 3 == 3).all()
+            else:
+                assert enc["units"].nbytes < 0.3 * S.xy.nbytes  # ~ 4-bit moves
+                assert ((enc["head"] >> 13 & 3) == 0).mean() > 0.5  # most rings: 4-bit moves
     rng = np.random.default_rng(7)
     rings = []
     for i in range(700):  # > 2 blocks, the last partial
@@ -281,7 +310,11 @@ def test_encode_rect_packed_roundtrip_and_rejects(tile_sets):
     xy, off2 = _decode_rect_packed_host(enc, n)
     assert np.array_equal(off2, off) and np.array_equal(xy, P.xy)
     widths = set(((enc["head"] >> 13) & 3).tolist())
-    assert widths == {0, 1, 2}
+    assert {2, 3} <= widths  # variable length where |d| <= 127 (and <= 255 units), else the narrowest fixed width
+    enc_f = sccg.encode_rect_packed(P.xy, off, vlc=False)
+    assert set(((enc_f["head"] >> 13) & 3).tolist()) == {0, 1, 2}
+    xy, off2 = _decode_rect_packed_host(enc_f, n)
+    assert np.array_equal(off2, off) and np.array_equal(xy, P.xy)
     assert any((enc["block"][:, 2] >> 62) & 1) and not all((enc["block"][:, 2] >> 62) & 1)
     e0 = sccg.encode_rect_packed(np.zeros((0, 2), np.int32), np.zeros(1, np.int64))
     assert e0["head"].size == 0 and e0["block"].shape == (0, 4)
