@@ -180,26 +180,24 @@ __global__ void __launch_bounds__(kRpBlock) decode_rect_packed_kernel(const unsi
       // axis: from +), exp-Golomb coded LSB-first -- L zero bits, a one, the
       // L low bits of s + 1; bits refilled 16 at a time into a 64-bit buffer
       // (a code is at most 15 bits: |d| <= 127)
-      unsigned long long b = 0ull;
+      unsigned b = 0u;  // bit window (32-bit: a code is <= 15 bits, refills of 16 keep it >= 16 bits)
       int nb = 0, ui = 0;
       int sa = 0, sb = 0;  // sign state of the axis of the even / odd moves
       for (int k = 1; k < V; k++) {
         if (nb < 16) {
-          b |= (unsigned long long)up[ui] << nb;
+          b |= (unsigned)up[ui] << nb;
           ui++;
           nb += 16;
         }
-        const int L = __ffsll((long long)b) - 1;
-        const unsigned v = (1u << L) | ((unsigned)(b >> (L + 1)) & ((1u << L) - 1u));
-        b >>= 2 * L + 1;
+        const int L = __ffs((int)b) - 1;
+        const unsigned t = b >> (L + 1);
+        const int sym = (int)((1u << L) | (t & ((1u << L) - 1u))) - 1, mag = (sym >> 1) + 1;
+        b = t >> L;
         nb -= 2 * L + 1;
-        const int sym = (int)v - 1, mag = (sym >> 1) + 1;
         const bool odd = ((k - 1) & 1) != 0;  // move k - 1
-        int sg = (odd ? sb : sa) ^ (sym & 1);
-        if (odd)
-          sb = sg;
-        else
-          sa = sg;
+        const int sg = (odd ? sb : sa) ^ (sym & 1);
+        sb = odd ? sg : sb;
+        sa = odd ? sa : sg;
         const int d = sg ? -mag : mag;
         const bool ymove = (k & 1) == vert;
         x += ymove ? 0 : d;
