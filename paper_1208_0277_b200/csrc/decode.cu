@@ -183,7 +183,8 @@ __global__ void __launch_bounds__(kRpBlock) decode_rect_packed_kernel(const unsi
       unsigned b = 0u;  // bit window (32-bit: a code is <= 15 bits, refills of 16 keep it >= 16 bits)
       int nb = 0, ui = 0;
       int sa = 0, sb = 0;  // sign state of the axis of the even / odd moves
-      for (int k = 1; k < V; k++) {
+      int pa = vert ? y : x, pb = vert ? x : y;  // position along the axis of the even / odd moves
+      auto next = [&](int& sgn) {  // one symbol -> the signed move
         if (nb < 16) {
           b |= (unsigned)up[ui] << nb;
           ui++;
@@ -191,18 +192,24 @@ __global__ void __launch_bounds__(kRpBlock) decode_rect_packed_kernel(const unsi
         }
         const int L = __ffs((int)b) - 1;
         const unsigned t = b >> (L + 1);
-        const int sym = (int)((1u << L) | (t & ((1u << L) - 1u))) - 1, mag = (sym >> 1) + 1;
+        const int sym = (int)((1u << L) | (t & ((1u << L) - 1u))) - 1;
         b = t >> L;
         nb -= 2 * L + 1;
-        const bool odd = ((k - 1) & 1) != 0;  // move k - 1
-        const int sg = (odd ? sb : sa) ^ (sym & 1);
-        sb = odd ? sg : sb;
-        sa = odd ? sa : sg;
-        const int d = sg ? -mag : mag;
-        const bool ymove = (k & 1) == vert;
-        x += ymove ? 0 : d;
-        y += ymove ? d : 0;
-        dst[k] = make_int2(x, y);
+        sgn ^= sym & 1;
+        const int mag = (sym >> 1) + 1;
+        return sgn ? -mag : mag;
+      };
+      auto put = [&](int k) { dst[k] = vert ? make_int2(pb, pa) : make_int2(pa, pb); };
+      int k = 1;
+      for (; k + 2 <= V; k += 2) {  // moves k - 1 (even) and k (odd): the axis pattern is static
+        pa += next(sa);
+        put(k);
+        pb += next(sb);
+        put(k + 1);
+      }
+      if (k < V) {
+        pa += next(sa);
+        put(k);
       }
     } else {
       const int lc = w == 0 ? 2 : w == 1 ? 1 : 0;  // log2(moves per unit)
