@@ -197,16 +197,8 @@ __device__ __forceinline__ void unpack_ix(uint64_t r, int& a, int& lo, int& hi) 
 // number of the boundaries b[t] = floor(t * L / n), t = 0..n, below the
 // integer v: floor(t L / n) < v  <=>  t L / n < v  <=>  t < v n / L, so the
 // count is min(n + 1, ceil(v n / L)) for v > 0 (v n < 2^22: 32-bit exact)
-// (by a float reciprocal -- the quotient is within one of the exact one, num
-// < 2^22 -- corrected to the exact ceiling; an integer division costs ~20
-// instructions and this runs per edge in the index build)
 __device__ __forceinline__ int count_below(int v, int n, int L) {
-  if (v <= 0) return 0;
-  const unsigned num = (unsigned)v * (unsigned)n;
-  int q = __float2int_rn(__uint2float_rn(num) * __frcp_rn(__int2float_rn(L)));
-  q += (unsigned)q * (unsigned)L < num ? 1 : 0;                          // ceil: smallest q with q L >= num
-  q -= (q > 0 && (unsigned)(q - 1) * (unsigned)L >= num) ? 1 : 0;
-  return min(n + 1, q);
+  return v <= 0 ? 0 : min(n + 1, (int)(((unsigned)v * (unsigned)n + (unsigned)L - 1u) / (unsigned)L));
 }
 __device__ __forceinline__ int ld_acquire_i(const int* p) {
   int v;
