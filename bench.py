@@ -62,6 +62,9 @@ def parse():
                     help="N > 1: image = one slide image per rank (weak scaling, configs[3]); tile = ONE slide cut "
                          "into y bands of P with their Q halo (strong scaling, SURVEY 8(e))")
     ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--e2e-unfused", action="store_true",
+                    help="e2e: decode the packed rings with sccg_decode_rect_packed before the step graph "
+                         "instead of inside prep (sccg_prep_sets_packed)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extras", action="store_true", help="skip the skewed / combs lines added to the slide run")
     ap.add_argument("--json-out", default=None)
@@ -508,9 +511,10 @@ def run_ours(args, rank, world, local_rank):
             # streamed: step i + 1's host -> device copy (copy stream) overlaps step i's decode and compute
             # three slots: the host reads step i - 2's result while steps i - 1 and i are in flight, so
             # enqueueing (Python) never delays the next copy
-            st = sccg.Streamer(A.n, int(A.offsets[-1]), B.n, int(B.offsets[-1]), cap=cap, threshold=args.threshold,
-                               depth=3)
             step = sccg.PackedStep(enc[0], enc[1])  # both sets in one pinned buffer: one copy per step
+            # fused: the step graph's prep decodes the packed rings itself (sccg_prep_sets_packed)
+            st = sccg.Streamer(A.n, int(A.offsets[-1]), B.n, int(B.offsets[-1]), cap=cap, threshold=args.threshold,
+                               depth=3, fused=None if args.e2e_unfused else step)
             h2d_c = step.nbytes
             for _ in range(st.depth):  # warm-up: every slot once (each slot's graph was captured at construction)
                 st.result(st.submit_step(step))
@@ -543,8 +547,10 @@ def run_ours(args, rank, world, local_rank):
         e2e_plain = e2e
         e2e = {"value": total_pairs * e2e_steps / (float(c_ms[0]) / 1e3), "unit": "pairs/s",
                "h2d_bytes_per_step": int(h2d_c), "d2h_bytes_per_step": int(d2h), "steps": e2e_steps,
-               "encoding": ("packed rectilinear rings (16-bit head, int16 start delta, 4/8/16-bit axis-alternating "
-                            "moves; no offsets), decoded by sccg_decode_rect_packed"),
+               "encoding": ("packed rectilinear rings (16-bit head, int16 start delta, variable-length or 4/8/16-bit "
+                            "axis-alternating moves; no offsets), decoded "
+                            + ("by sccg_decode_rect_packed" if args.e2e_unfused or world > 1
+                               else "inside prep (sccg_prep_sets_packed)")),
                "pipelining": ("sccg.Streamer: each step's host -> device copy on a copy stream overlaps the previous "
                               "step's decode + step graph; every step's sums read back" if world == 1 else None)}
 

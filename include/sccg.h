@@ -114,6 +114,25 @@ SCCG_API int sccg_prep(const sccg_polyset* set, int32_t validate, sccg_stream_t 
  * SCCG_E_ARG for count outside 1..4, a bad set, or shared derived buffers. */
 SCCG_API int sccg_prep_sets(const sccg_polyset* sets, int32_t count, int32_t validate, sccg_stream_t stream);
 
+/* The rings of a set in the packed transfer encoding (format 2, see sccg_decode_rect_packed below). */
+typedef struct {
+  const uint16_t* head;   /* [n_polygons] */
+  const uint8_t* vlen;    /* [n_polygons], or NULL when no ring uses the variable-length class */
+  const int16_t* start;   /* start stream */
+  const uint16_t* units;  /* move units */
+  const int64_t* block;   /* [ceil(n_polygons / SCCG_RECTP_BLOCK)][4] */
+} sccg_rect_packed;
+
+/* sccg_prep_sets with the rings arriving packed (rectilinear rings; the end-to-end path): each tile of
+ * 128 rings is decoded straight into prep's shared-memory tile -- no separate decode kernel, no read of xy --
+ * and written out, so on return (stream order) sets[i].offsets and sets[i].xy hold exactly what
+ * sccg_decode_rect_packed would write (they are OUTPUT buffers here: device, writable, n_polygons + 1 int64 and
+ * n_vertices int32 pairs, n_vertices the encoded total), and every derived field is what sccg_prep_sets
+ * computes from them.  Device pointers; errors as sccg_prep_sets, and SCCG_E_ARG for a null or misaligned
+ * encoding.  Asynchronous. */
+SCCG_API int sccg_prep_sets_packed(const sccg_polyset* sets, const sccg_rect_packed* enc, int32_t count,
+                                   int32_t validate, sccg_stream_t stream);
+
 /* ---------------------------------------------------------------- filter */
 /* Workspace bytes sccg_filter_pairs needs for sets of these sizes (the hashed
  * grid's bucket counters, 32 slots per bucket and an overflow pool, and the

@@ -40,7 +40,7 @@ SUMS_FIELDS = ("n_pairs", "n_nonzero", "sum_inter", "sum_union", "sum_area_p", "
 SYMBOLS = ("sccg_polyset_bytes", "sccg_polyset_bind", "sccg_prep", "sccg_prep_sets", "sccg_filter_workspace_bytes",
            "sccg_filter_pairs", "sccg_filter_pairs_closed", "sccg_filter_pairs_async", "sccg_touches", "sccg_pixelbox_workspace_bytes", "sccg_pixelbox_index_bytes", "sccg_pixelbox",
            "sccg_pixelbox_async", "sccg_count_missing", "sccg_contains", "sccg_report", "sccg_jaccard", "sccg_sums_copy", "sccg_decode_rect",
-           "sccg_decode_rect_packed",
+           "sccg_decode_rect_packed", "sccg_prep_sets_packed",
            "sccg_sums_pack", "sccg_sums_unpack", "sccg_strerror", "sccg_last_error_string", "sccg_last_error_index",
            "sccg_version")
 STATUS_ARG, STATUS_NOT_RECTILINEAR, STATUS_RANGE, STATUS_STACK, STATUS_CAPACITY = 1, 2, 4, 8, 16
@@ -149,6 +149,8 @@ def load(build: bool = True):
         lib.sccg_decode_rect.argtypes = [vp, vp, vp, vp, i64, vp, vp]
         lib.sccg_decode_rect.restype = cint
         lib.sccg_decode_rect_packed.argtypes = [vp, vp, vp, vp, vp, i64, vp, vp, vp]
+        lib.sccg_prep_sets_packed.argtypes = [vp, vp, ctypes.c_int32, ctypes.c_int32, vp]
+        lib.sccg_prep_sets_packed.restype = cint
         lib.sccg_decode_rect_packed.restype = cint
         lib.sccg_pixelbox.argtypes = [ps, ps, vp, i64, vp, vp, vp, ctypes.POINTER(Config), vp, sz, vp]
         lib.sccg_pixelbox.restype = cint
@@ -204,6 +206,30 @@ def _require_cuda(t, name, dtype):
         raise TypeError(f"{name} must be {dtype}, got {t.dtype}")
     if not t.is_contiguous():
         raise ValueError(f"{name} must be contiguous")
+
+
+class RectPacked(ctypes.Structure):
+    """sccg_rect_packed: a set's rings in the packed transfer encoding (device pointers)."""
+    _fields_ = [("head", ctypes.c_void_p), ("vlen", ctypes.c_void_p), ("start", ctypes.c_void_p),
+                ("units", ctypes.c_void_p), ("block", ctypes.c_void_p)]
+
+
+def rect_packed(enc) -> RectPacked:
+    """RectPacked of an encode_rect_packed dict already on the device (tensors)."""
+    ptr = lambda t: t.data_ptr() if t is not None and t.numel() else None  # noqa: E731
+    return RectPacked(ptr(enc["head"]), ptr(enc.get("vlen")), ptr(enc["start"]), ptr(enc["units"]),
+                      ptr(enc["block"]))
+
+
+def prep_sets_packed(sets, encs, validate: bool = True, stream=None):
+    """sccg_prep_sets_packed: prep the DeviceSets (built with prep=False over
+    writable xy / offsets buffers) from their packed encodings (device dicts):
+    decodes xy and offsets into the sets' buffers and derives everything
+    sccg_prep_sets does, in one launch."""
+    arr = (PolySet * len(sets))(*[S.c for S in sets])
+    enc = (RectPacked * len(sets))(*[rect_packed(e) for e in encs])
+    _check(load().sccg_prep_sets_packed(arr, enc, len(sets), 1 if validate else 0, _stream_ptr(stream)),
+           "sccg_prep_sets_packed")
 
 
 class DeviceSet:
@@ -317,10 +343,13 @@ class Pipeline:
 
     def __init__(self, P: "DeviceSet", Q: "DeviceSet", cap: int | None = None, threshold: int = 0, graph: bool = True,
                  validate: bool = True, raster: bool = True, readback=(), outputs: bool = True,
-                 paper_split: bool = False, index: bool = True, allreduce=None):
+                 paper_split: bool = False, index: bool = True, allreduce=None, packed=None):
         torch = _torch()
         self.lib = load()
         self.P, self.Q = P, Q
+        # packed = (enc_p, enc_q): device dicts of the packed encoding at fixed addresses; the step's prep then
+        # decodes the rings itself (sccg_prep_sets_packed) into P's and Q's xy / offsets buffers
+        self._packed = (RectPacked * 2)(*[rect_packed(e) for e in packed]) if packed is not None else None
         dev = P.xy.device
         self.cap = int(cap) if cap is not None else 2 * max(P.n, Q.n) + 1024
         self.pairs = torch.empty((max(self.cap, 1), 2), dtype=torch.int32, device=dev)
@@ -391,7 +420,10 @@ class Pipeline:
         st = _stream_ptr()
         lib = self.lib
         sums_copy(self._zero, self.sums)
-        _check(lib.sccg_prep_sets(self._sets, 2, self.validate, st), "sccg_prep_sets")
+        if self._packed is not None:
+            _check(lib.sccg_prep_sets_packed(self._sets, self._packed, 2, self.validate, st), "sccg_prep_sets_packed")
+        else:
+            _check(lib.sccg_prep_sets(self._sets, 2, self.validate, st), "sccg_prep_sets")
 
     def _enqueue_join(self):
         _check(self.lib.sccg_filter_pairs_async(ctypes.byref(self.P.c), ctypes.byref(self.Q.c), self.pairs.data_ptr(),
@@ -611,12 +643,16 @@ class Streamer:
         sums = st.result(t)                 # waits for that step"""
 
     def __init__(self, n_p: int, nv_p: int, n_q: int, nv_q: int, cap: int | None = None, threshold: int = 0,
-                 depth: int = 2, device=None):
+                 depth: int = 2, device=None, fused: "PackedStep | None" = None):
+        """fused: a PackedStep whose layout every submit_step shares; the step
+        graph's prep then decodes the rings itself (sccg_prep_sets_packed: no
+        decode kernels, no read of xy) -- submit_step only."""
         torch = _torch()
         dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         self.device = dev
         self.depth = depth
         self.shapes = (n_p, nv_p, n_q, nv_q)
+        self.fused = fused
         cap = int(cap) if cap is not None else 3 * max(n_p, n_q) + 1024
         self.slots = []
         for _ in range(depth):
@@ -629,7 +665,14 @@ class Streamer:
             P = DeviceSet(sl["xy_p"][:nv_p], sl["off_p"], prep=False)
             Q = DeviceSet(sl["xy_q"][:nv_q], sl["off_q"], prep=False)
             sl["sets"] = (P, Q)
-            sl["pipe"] = Pipeline(P, Q, cap=cap, threshold=threshold, graph=True, readback=[sl["rb"]])
+            packed = None
+            if fused is not None:  # the slot's step buffer at a fixed address, captured in the graph
+                # zeroed: the graph capture's warm-up run decodes it (all rings empty)
+                sl["step_buf"] = torch.zeros(max(fused.nbytes, 16), dtype=torch.uint8, device=dev)
+                v = fused.views(sl["step_buf"])
+                sl["step_views"] = v
+                packed = (v["p"], v["q"])
+            sl["pipe"] = Pipeline(P, Q, cap=cap, threshold=threshold, graph=True, readback=[sl["rb"]], packed=packed)
             sl["copied"], sl["done"], sl["decoded"] = torch.cuda.Event(), torch.cuda.Event(), torch.cuda.Event()
             self.slots.append(sl)
         self.copy_stream = torch.cuda.Stream(device=dev)
@@ -680,6 +723,8 @@ class Streamer:
         n_p, nv_p, n_q, nv_q = self.shapes
         if step.n["p"] != n_p or step.n["q"] != n_q:
             raise ValueError("Streamer: the step's ring counts differ from the slots'")
+        if self.fused is not None and (step.nbytes != self.fused.nbytes or step.layout != self.fused.layout):
+            raise ValueError("Streamer(fused=...): the step's packed layout differs from the slots'")
         cs.wait_event(sl["done"])  # the slot's previous step no longer reads its buffers
         with torch.cuda.stream(cs):
             buf = sl.get("step_buf")
@@ -687,6 +732,12 @@ class Streamer:
                 buf = sl["step_buf"] = torch.empty(max(step.nbytes, 16), dtype=torch.uint8, device=self.device)
             buf[: step.nbytes].copy_(step.host[: step.nbytes], non_blocking=True)
             sl["copied"].record(cs)
+        if self.fused is not None:  # prep decodes inside the step graph
+            main.wait_event(sl["copied"])
+            sl["pipe"].run(slot=0)
+            sl["done"].record(main)
+            self.count += 1
+            return self.count - 1
         # the decode runs on its own stream: step i + 1's decode overlaps step i's graph
         ds = self.decode_stream
         ds.wait_event(sl["copied"])

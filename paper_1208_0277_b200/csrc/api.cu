@@ -173,6 +173,28 @@ int sccg_prep_sets(const sccg_polyset* sets, int32_t count, int32_t validate, sc
   return check_cuda(launch_prep(ptrs, count, validate, reinterpret_cast<cudaStream_t>(stream)), "sccg_prep_sets");
 }
 
+int sccg_prep_sets_packed(const sccg_polyset* sets, const sccg_rect_packed* enc, int32_t count, int32_t validate,
+                          sccg_stream_t stream) {
+  NvtxRange nvtx_range("sccg_prep_sets_packed");
+  set_error(SCCG_OK, "", -1);
+  if (!sets || !enc || count < 1 || count > 4)
+    return set_error(SCCG_E_ARG, "sccg_prep_sets_packed: sets / enc must hold 1..4 sets");
+  const sccg_polyset* ptrs[4];
+  for (int i = 0; i < count; i++) {
+    if (int r = check_set(&sets[i], true, "sets[i]")) return r;
+    for (int j = 0; j < i; j++)
+      if (sets[j].stats == sets[i].stats || sets[j].status == sets[i].status)
+        return set_error(SCCG_E_ARG, "sccg_prep_sets_packed: sets must not share derived buffers");
+    const sccg_rect_packed& e = enc[i];
+    if (sets[i].n_polygons > 0 && (!e.head || !e.start || !e.block || !aligned(e.head, 2) || !aligned(e.start, 2) ||
+                                   !aligned(e.units, 2) || !aligned(e.block, 8)))
+      return set_error(SCCG_E_ARG, "sccg_prep_sets_packed: null or misaligned encoding", i);
+    ptrs[i] = &sets[i];
+  }
+  return check_cuda(launch_prep(ptrs, count, validate, reinterpret_cast<cudaStream_t>(stream), enc),
+                    "sccg_prep_sets_packed");
+}
+
 size_t sccg_filter_workspace_bytes(int64_t n_p, int64_t n_q) {
   if (n_p < 0 || n_q < 0) return 0;
   return filter_ws_bytes(n_p, n_q);

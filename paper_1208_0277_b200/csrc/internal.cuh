@@ -185,7 +185,8 @@ int set_error(int code, const char* msg, int64_t index = -1);
 int check_cuda(cudaError_t e, const char* where);
 
 // launchers
-cudaError_t launch_prep(const sccg_polyset* const* sets, int count, int validate, cudaStream_t st);
+cudaError_t launch_prep(const sccg_polyset* const* sets, int count, int validate, cudaStream_t st,
+                        const sccg_rect_packed* pk = nullptr);
 cudaError_t launch_sums_copy(const sccg_sums* src, sccg_sums* dst, cudaStream_t st);
 
 }  // namespace sccg

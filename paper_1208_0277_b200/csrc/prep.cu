@@ -14,7 +14,7 @@
 // by a warp) in place, and writes the slots back with one TMA bulk store.
 // Ranges larger than the tile fall back to reading the polygon's vertices from
 // global memory (warp per polygon).
-#include "internal.cuh"
+#include "packed_decode.cuh"
 
 namespace sccg {
 
@@ -460,7 +460,16 @@ struct PrepSet {
   uint32_t* status;
   SetStats* stats;
   int bulk;
+  // packed mode (sccg_prep_sets_packed): the rings come in the packed
+  // transfer encoding; prep decodes each tile into shared memory and writes
+  // xy and the offsets (then `xy` / `off` above point at those outputs)
+  const unsigned short* ph;
+  const unsigned char* pvl;
+  const short* pst;
+  const unsigned short* pu;
+  const long long* pb;
 };
+static_assert(kRpBlock == 2 * kPrepPolys, "a prep tile is half a packed block");
 struct PrepArgs {
   PrepSet set[kPrepMaxSets];
   int64_t tile_end[kPrepMaxSets];  // exclusive prefix ends of the sets' tile ranges
@@ -516,6 +525,7 @@ __device__ void flush_stats(StatAcc& acc, SetStats* stats, unsigned long long* s
 #ifndef SCCG_PREP_MINB
 #define SCCG_PREP_MINB (640 / SCCG_PREP_THREADS)  // 5 CTAs of 128 threads per SM (shared memory)
 #endif
+template <bool PK>
 __global__ void __launch_bounds__(kPrepThreads, SCCG_PREP_MINB) prep_kernel(const __grid_constant__ PrepArgs args) {
   pdl_entry_deferred();  // prep_init's counters
   extern __shared__ int4 s_dyn4[];  // kPrepVerts int2 (16-byte aligned)
@@ -528,6 +538,9 @@ __global__ void __launch_bounds__(kPrepThreads, SCCG_PREP_MINB) prep_kernel(cons
   __shared__ int s_b[6];
   __shared__ uint64_t s_bar;
   __shared__ long long s_tile;
+  __shared__ int s_pk[2][kPrepThreads / 32 + 1];  // packed mode: per-warp scan totals, then the first half's
+  __shared__ int s_uoff[kPrepPolys];                // packed mode: each ring's first move unit (block-relative)
+  __shared__ int s_uend;                            // packed mode: the tile's end unit (block-relative)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   unsigned phase = 0;
   if (threadIdx.x == 0) mbar_init(&s_bar);
@@ -546,7 +559,7 @@ __global__ void __launch_bounds__(kPrepThreads, SCCG_PREP_MINB) prep_kernel(cons
   };
   int64_t off_a = 0, off_b = 0;
   auto fetch_offsets = [&](int64_t g) {
-    if (g >= ntiles) return;
+    if (PK || g >= ntiles) return;
     int si2, np2;
     int64_t p02;
     tile_range(g, si2, p02, np2);
@@ -586,13 +599,109 @@ __global__ void __launch_bounds__(kPrepThreads, SCCG_PREP_MINB) prep_kernel(cons
     if (threadIdx.x == 0) bulk_store_drain();
 #endif
     __syncthreads();  // previous tile's shared data fully consumed
-    if ((int)threadIdx.x <= np) s_off[threadIdx.x] = off_a;
-    if (threadIdx.x == 0) s_off[np] = off_b;
+    int pk_h = 0, pk_x = 0, pk_y = 0;  // packed mode: this thread's ring head and start
+    if (PK) {
+      // the tile is half of packed block b: the block scan of (vertices,
+      // units) over its 256 heads gives this half's offsets
+      const int64_t bb = p0 / kRpBlock;
+      const int half = (int)((p0 / kPrepPolys) & 1);
+      const long long* blk = args.set[si].pb + 4 * bb;
+      const long long vbase = blk[0], sw = blk[2], org = blk[3];
+      const int64_t r0 = bb * kRpBlock + threadIdx.x, r1 = r0 + kPrepPolys;
+      auto vu = [&](int64_t r, int& V, int& nu, int& h) {
+        V = nu = h = 0;
+        if (r < args.set[si].n) {
+          h = args.set[si].ph[r];
+          V = h & 0x1fff;
+          const int w = (h >> 13) & 3;
+          nu = w == 3 ? (int)args.set[si].pvl[r] : rp_units(max(V - 1, 0), w);
+        }
+      };
+      int Va, nua, ha, Vb, nub, hb;
+      vu(r0, Va, nua, ha);
+      vu(r1, Vb, nub, hb);
+      // first half's totals (needed by the second half), and this half's scan
+      int ta = Va, tu = nua, xv = half ? Vb : Va, xu = half ? nub : nua;
+      for (int o = 16; o; o >>= 1) {
+        ta += __shfl_xor_sync(0xffffffffu, ta, o);
+        tu += __shfl_xor_sync(0xffffffffu, tu, o);
+      }
+      for (int o = 1; o < 32; o <<= 1) {
+        const int a = __shfl_up_sync(0xffffffffu, xv, o), c = __shfl_up_sync(0xffffffffu, xu, o);
+        if (lane >= o) {
+          xv += a;
+          xu += c;
+        }
+      }
+      if (lane == 31) {
+        s_pk[0][warp] = xv;
+        s_pk[1][warp] = xu;
+      }
+      if (lane == 0) {
+        s_cnt[2 * warp] = ta;  // (s_cnt is cleared below, after use)
+        s_cnt[2 * warp + 1] = tu;
+      }
+      __syncthreads();
+      int bv = 0, bu = 0, fv = 0, fu = 0;
+      for (int w2 = 0; w2 < kPrepThreads / 32; w2++) {
+        bv += w2 < warp ? s_pk[0][w2] : 0;
+        bu += w2 < warp ? s_pk[1][w2] : 0;
+        fv += s_cnt[2 * w2];
+        fu += s_cnt[2 * w2 + 1];
+      }
+      const int myV = half ? Vb : Va, mynu = half ? nub : nua;
+      const int vpre = bv + xv - myV + (half ? fv : 0), upre = bu + xu - mynu + (half ? fu : 0);
+      pk_h = half ? hb : ha;
+      if ((int)threadIdx.x < np) {
+        s_off[threadIdx.x] = vbase + vpre;
+        s_uoff[threadIdx.x] = upre;
+        if ((int)threadIdx.x == np - 1) {
+          s_off[np] = vbase + vpre + myV;
+          s_uend = upre + mynu;
+        }
+        // start of this thread's ring (narrow block: int16 deltas from the block origin)
+        const int jb = half * kPrepPolys + threadIdx.x;
+        const long long so = sw & ((1ll << 62) - 1);
+        if ((sw >> 62) & 1) {
+          const unsigned short* sp = reinterpret_cast<const unsigned short*>(args.set[si].pst) + so + 4 * jb;
+          pk_x = (int)((unsigned)sp[0] | ((unsigned)sp[1] << 16));
+          pk_y = (int)((unsigned)sp[2] | ((unsigned)sp[3] << 16));
+        } else {
+          pk_x = (int)(unsigned)(org & 0xffffffffll) + args.set[si].pst[so + 2 * jb];
+          pk_y = (int)(unsigned)((unsigned long long)org >> 32) + args.set[si].pst[so + 2 * jb + 1];
+        }
+      }
+      __syncthreads();  // s_cnt / s_pk reused below
+      if ((int)threadIdx.x < np) {  // the offsets are an output of packed mode
+        int64_t* oo = const_cast<int64_t*>(args.set[si].off);
+        oo[p0 + threadIdx.x] = s_off[threadIdx.x];
+        if (p0 + np == args.set[si].n && (int)threadIdx.x == np - 1) oo[p0 + np] = s_off[np];
+      }
+    } else {
+      if ((int)threadIdx.x <= np) s_off[threadIdx.x] = off_a;
+      if (threadIdx.x == 0) s_off[np] = off_b;
+    }
     long long next_gt = 0;
     if (threadIdx.x == 0) next_gt = (long long)atomicAdd(args.ticket, 1ull);  // the next tile, in flight
     if (threadIdx.x < kPrepPolys / 32) s_big[threadIdx.x] = 0;
     for (int t = threadIdx.x; t < kSortKeys; t += kPrepThreads) s_cnt[t] = 0;
     s_perm[threadIdx.x] = 0xff;
+    // packed mode: the tile's move units staged in the free tail of the tile buffer (when the decoded
+    // vertices leave room), so each thread's bit-window refills are shared-memory loads
+    const unsigned short* pk_units = nullptr;
+    if (PK) {
+      const unsigned short* gu = args.set[si].pu + args.set[si].pb[4 * (p0 / kRpBlock) + 1];
+      const int u0 = np > 0 ? s_uoff[0] : 0, nunits = np > 0 ? s_uend - u0 : 0;
+      const int64_t tv0 = s_off[0] & ~int64_t(1), tnv = s_off[np] - tv0;
+      const int ubytes = (2 * nunits + 15) & ~15;
+      if (tnv >= 0 && tnv * 8 + ubytes <= (int64_t)kPrepSmem) {
+        unsigned short* su = reinterpret_cast<unsigned short*>(reinterpret_cast<char*>(s_dyn4) + kPrepSmem - ubytes);
+        for (int i = threadIdx.x; i < nunits; i += kPrepThreads) su[i] = __ldg(gu + u0 + i);
+        pk_units = su - u0;  // indexed by block-relative unit
+      } else {
+        pk_units = gu;
+      }
+    }
     __syncthreads();
     // Rings are dealt to threads in order of vertex count (counting sort on
     // V / 4), so the lanes of a warp run loops of similar length (dealing them
@@ -608,7 +717,20 @@ __global__ void __launch_bounds__(kPrepThreads, SCCG_PREP_MINB) prep_kernel(cons
     // 16-byte-aligned body, the odd last vertex by a thread
     const int64_t v0 = s_off[0] & ~int64_t(1), v1 = s_off[np];
     const bool tiled = s_off[0] >= 0 && v1 <= nv_total && v1 >= s_off[0] && v1 - v0 <= kPrepVerts;
-    if (tiled) {
+    if (PK) {
+      // decode this thread's ring into the tile (or, for a tile too large to
+      // stage, straight into xy); the tile then goes to xy by one bulk store
+      if ((int)threadIdx.x < np) {
+        const int V = pk_h & 0x1fff;
+        const int64_t rb = s_off[threadIdx.x];
+        if (V > 0 && rb >= 0 && rb + V <= nv_total) {  // (an encoding inconsistent with n_vertices writes nothing)
+          const unsigned short* up = pk_units + s_uoff[threadIdx.x];
+          int2* dst = tiled ? s_xy + (s_off[threadIdx.x] - v0) : const_cast<int2*>(xy) + s_off[threadIdx.x];
+          rp_walk_ring(up, V, (pk_h >> 13) & 3, pk_h >> 15, pk_x, pk_y, dst);
+        }
+      }
+      fence_async_smem();  // this thread's decoded vertices -> async proxy (the bulk store below)
+    } else if (tiled) {
       const int64_t nv = v1 - v0;
       if (bulk) {
         if (threadIdx.x == 0) {
@@ -625,7 +747,22 @@ __global__ void __launch_bounds__(kPrepThreads, SCCG_PREP_MINB) prep_kernel(cons
         for (int64_t i = threadIdx.x; i < nv; i += blockDim.x) s_xy[i] = xy[v0 + i];
       }
     }
-    __syncthreads();  // every ring counted
+    __syncthreads();  // every ring counted (packed mode: every ring decoded)
+    if (PK && tiled) {  // the decoded tile [off[p0], v1) -> xy, read out before the ring work rewrites it in place
+      const int64_t s0 = s_off[0];
+      const int64_t a0 = (s0 + 1) & ~int64_t(1), a1 = v1 & ~int64_t(1);
+      int2* xo = const_cast<int2*>(xy);
+      if (bulk) {
+        if (threadIdx.x == 0) {
+          if (a1 > a0) bulk_store(xo + a0, s_xy + (a0 - v0), (unsigned)(a1 - a0) * 8u);
+          if (s0 < a0 && s0 < v1) xo[s0] = s_xy[s0 - v0];
+          if (a1 < v1 && a1 >= a0) xo[a1] = s_xy[a1 - v0];
+          bulk_store_drain();  // read out of shared memory before anyone rewrites it
+        }
+      } else {
+        for (int64_t i = s0 + threadIdx.x; i < v1; i += blockDim.x) xo[i] = s_xy[i - v0];
+      }
+    }
     if (threadIdx.x < 32) {  // exclusive scan of the bucket counts (two per lane)
       const int c0 = s_cnt[2 * threadIdx.x], c1 = s_cnt[2 * threadIdx.x + 1];
       int incl = c0 + c1;
@@ -684,7 +821,7 @@ __global__ void __launch_bounds__(kPrepThreads, SCCG_PREP_MINB) prep_kernel(cons
     }
 #endif
 #if SCCG_PREP_L2_PREFETCH == 2
-    if (threadIdx.x == 0) {
+    if (!PK && threadIdx.x == 0) {
       // thread 0 (warp 0 deals the smallest rings, so it has slack) starts
       // pulling the next tile's vertex range into L2 while this tile's rings
       // are worked on: that tile's TMA load then hits L2 instead of HBM
@@ -826,7 +963,8 @@ __global__ void prep_init_kernel(PrepArgs args) {
   if (i == 0) *args.ticket = 0;
 }
 
-cudaError_t launch_prep(const sccg_polyset* const* sets, int count, int validate, cudaStream_t st) {
+cudaError_t launch_prep(const sccg_polyset* const* sets, int count, int validate, cudaStream_t st,
+                        const sccg_rect_packed* pk) {
   PrepArgs a{};
   a.nsets = count;
   a.validate = validate;
@@ -848,6 +986,13 @@ cudaError_t launch_prep(const sccg_polyset* const* sets, int count, int validate
 #ifdef SCCG_PREP_NO_TMA  // ablation build (scripts/fig9.py): tiles staged by plain LSU copies
     d.bulk = 0;
 #endif
+    if (pk) {
+      d.ph = pk[i].head;
+      d.pvl = pk[i].vlen;
+      d.pst = pk[i].start;
+      d.pu = pk[i].units;
+      d.pb = reinterpret_cast<const long long*>(pk[i].block);
+    }
     tiles += (s->n_polygons + kPrepPolys - 1) / kPrepPolys;
     a.tile_end[i] = tiles;
   }
@@ -856,19 +1001,25 @@ cudaError_t launch_prep(const sccg_polyset* const* sets, int count, int validate
   prep_init_kernel<<<1, 32, 0, st>>>(a);
   if (tiles > 0) {
     static cudaError_t attr =
-        cudaFuncSetAttribute(prep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPrepSmem);
+        cudaFuncSetAttribute(prep_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPrepSmem);
+    static cudaError_t attr_pk =
+        cudaFuncSetAttribute(prep_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPrepSmem);
     if (attr != cudaSuccess) return attr;
+    if (attr_pk != cudaSuccess) return attr_pk;
     static int sms = 0, per_sm = 1;
     if (sms == 0) {  // launch geometry, queried once per process
       int dev = 0;
       cudaGetDevice(&dev);
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, prep_kernel, kPrepThreads, kPrepSmem);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, prep_kernel<false>, kPrepThreads, kPrepSmem);
     }
     int64_t blocks = tiles;
     const int64_t cap = (int64_t)sms * (per_sm > 0 ? per_sm : 1);
     if (blocks > cap) blocks = cap;
-    if (cudaError_t e = launch_pdl(prep_kernel, dim3((unsigned)blocks), dim3(kPrepThreads), kPrepSmem, st, a)) return e;
+    if (cudaError_t e = pk ? launch_pdl(prep_kernel<true>, dim3((unsigned)blocks), dim3(kPrepThreads), kPrepSmem, st, a)
+                           : launch_pdl(prep_kernel<false>, dim3((unsigned)blocks), dim3(kPrepThreads), kPrepSmem, st,
+                                        a))
+      return e;
   }
   return cudaGetLastError();
 }

@@ -1017,6 +1017,60 @@ def test_decode_rect_packed_exact(sccg, config):
         assert torch.equal(s0, s1)
 
 
+@pytest.mark.parametrize("config", ["tile", "skewed", "combs", "edge"])
+def test_prep_sets_packed_matches_plain(sccg, config):
+    """sccg_prep_sets_packed (prep decoding the packed encoding tile by tile,
+    no decode kernel): xy and offsets exactly the plain rings, and every
+    derived output (MBR, area, edge counts and rebases, records and rasters,
+    status) identical to sccg_prep_sets on the plain sets -- thread-path
+    tiles, rings over 192 vertices (warp path), tiles too large to stage
+    (combs: decoded straight to global memory), every coding class."""
+    if config == "combs":
+        sets = combs.generate(n_pairs=48)
+    elif config == "edge":
+        from test_abi import _rect_ring
+
+        rng = np.random.default_rng(5)
+        rings = [_rect_ring(rng, int(rng.integers(-9000, 9000)), int(rng.integers(-5000, 5000)),
+                            int(rng.integers(2, 60)) * 2 + 2, (1, 8, 9, 128, 129, 300)[i % 6]) for i in range(600)]
+        sets = (synth.pack(rings),)
+    else:
+        sets = synth.generate(config)
+    for S in sets:
+        for vlc in (True, False):
+            enc = sccg.encode_rect_packed(S.xy, S.offsets, vlc=vlc)
+            assert enc is not None
+            ed = _packed_to_device(enc)
+            xy = torch.zeros((len(S.xy), 2), dtype=torch.int32, device="cuda")
+            off = torch.zeros(S.n + 1, dtype=torch.int64, device="cuda")
+            D = sccg.DeviceSet(xy, off, prep=False)
+            sccg.prep_sets_packed([D], [ed])
+            torch.cuda.synchronize()
+            assert torch.equal(off.cpu(), torch.from_numpy(np.asarray(S.offsets, np.int64)))
+            assert torch.equal(xy.cpu(), torch.from_numpy(np.asarray(S.xy, np.int32)))
+            R = dev(S, sccg)
+            for f in ("mbr", "area", "ecount", "status"):
+                assert torch.equal(getattr(D, f), getattr(R, f)), (config, vlc, f)
+            assert torch.equal(D.used_edge_words(), R.used_edge_words())
+
+
+def test_streamer_fused_matches_pipeline(sccg):
+    """sccg.Streamer(fused=...): the step graph's prep decodes the packed
+    rings itself; every step's sums equal the device-resident Pipeline's."""
+    A, B = synth.generate("tile", image=33)
+    P, Q = dev(A, sccg), dev(B, sccg)
+    pipe = sccg.Pipeline(P, Q, graph=False)
+    pipe.run()
+    torch.cuda.synchronize()
+    ref = pipe.sums.cpu().tolist()
+    step = sccg.PackedStep(*(sccg.encode_rect_packed(S.xy, S.offsets) for S in (A, B)))
+    st = sccg.Streamer(A.n, int(A.offsets[-1]), B.n, int(B.offsets[-1]), depth=3, fused=step)
+    tickets = [st.submit_step(step) for _ in range(5)]
+    got = [st.result(t) for t in tickets[2:]]
+    for g in got:
+        assert [getattr(g, f) for f in sccg.SUMS_FIELDS] == ref
+
+
 def _study_rank(rank, world, port, out):
     import os
     import sys
