@@ -122,6 +122,16 @@ def test_host_argument_checks():
     assert lib.sccg_decode_rect(0x1004, 0x2000, 0x3000, 0x4000, 3, 0x5000, None) == sccg.E_ARG  # start misaligned
     assert lib.sccg_decode_rect(0x1000, 0x2001, 0x3000, 0x4000, 3, 0x5000, None) == sccg.E_ARG  # move misaligned
     assert lib.sccg_decode_rect(None, None, None, None, 0, None, None) == sccg.OK  # nothing to decode
+    # packed decode / packed prep: argument checks before anything is enqueued
+    assert lib.sccg_decode_rect_packed(None, None, None, None, None, -1, None, None, None) == sccg.E_ARG
+    assert lib.sccg_decode_rect_packed(None, None, None, None, None, 3, 0x1000, None, None) == sccg.E_ARG
+    assert lib.sccg_decode_rect_packed(0x1001, None, 0x2000, 0x3000, 0x4000, 3, 0x5000, 0x6000, None) == sccg.E_ARG
+    assert lib.sccg_prep_sets_packed(None, None, 1, 1, None) == sccg.E_ARG
+    ps = sccg.PolySet()
+    assert lib.sccg_prep_sets_packed(ctypes.byref(ps), None, 1, 1, None) == sccg.E_ARG
+    enc = sccg.RectPacked()
+    assert lib.sccg_prep_sets_packed(ctypes.byref(ps), ctypes.byref(enc), 0, 1, None) == sccg.E_ARG
+    assert lib.sccg_prep_sets_packed(ctypes.byref(ps), ctypes.byref(enc), 5, 1, None) == sccg.E_ARG
     assert lib.sccg_pixelbox_index_bytes(-1, 5) == 0
     assert lib.sccg_pixelbox_index_bytes(100, 200) == 8 * 300 + (1 << 24)
 
