@@ -67,7 +67,12 @@ constexpr int kCStride = SCCG_JOIN_CSTRIDE;
 #ifndef SCCG_JOIN_LEVELS
 #define SCCG_JOIN_LEVELS 8
 #endif
-constexpr int kLevelSlots = 4, kLevels = SCCG_JOIN_LEVELS, kSlots = kLevelSlots * kLevels;
+#ifndef SCCG_JOIN_LS
+#define SCCG_JOIN_LS 4  // slots per level (4 or 8)
+#endif
+constexpr int kLevelSlots = SCCG_JOIN_LS, kLevels = SCCG_JOIN_LEVELS * 4 / SCCG_JOIN_LS,
+              kSlots = kLevelSlots * kLevels;
+static_assert(kLevelSlots == 4 || kLevelSlots == 8, "4 or 8 slots per level");
 // 2^hb buckets, hb = ceil(log2(max(nq, 512))) (+ SCCG_JOIN_HB_EXTRA)
 #ifndef SCCG_JOIN_HB_EXTRA
 #define SCCG_JOIN_HB_EXTRA 0
@@ -215,7 +220,8 @@ struct Tables {
   int* ovf_n;
   int hb;
   __device__ __forceinline__ size_t at(int b, int j) const {
-    return ((size_t)(j / kLevelSlots) << (hb + 2)) + ((size_t)b << 2) + (j % kLevelSlots);
+    constexpr int ls = kLevelSlots == 8 ? 3 : 2;
+    return ((size_t)(j / kLevelSlots) << (hb + ls)) + ((size_t)b << ls) + (j % kLevelSlots);
   }
 };
 
@@ -330,9 +336,16 @@ __device__ __forceinline__ void visit(const int4& a, int k, int cx, int cy, int 
       const int4 e2 = s0[2], e3 = s0[3];
       take(owns(a, entry_box(e2), o), e2.w);
       take(cnt > 3 && owns(a, entry_box(e3), o), e3.w);
+      if (kLevelSlots == 8 && cnt > 4) {  // the rest of the first level (one 128-byte line per bucket)
+        const int4 e4 = s0[4], e5 = s0[5], e6 = s0[6], e7 = s0[7];
+        take(owns(a, entry_box(e4), o), e4.w);
+        take(cnt > 5 && owns(a, entry_box(e5), o), e5.w);
+        take(cnt > 6 && owns(a, entry_box(e6), o), e6.w);
+        take(cnt > 7 && owns(a, entry_box(e7), o), e7.w);
+      }
       if (cnt > kLevelSlots) {  // a crowded bucket: the higher levels, then the overflow chain
         const int ns = min(cnt, kSlots);
-        for (int j = kLevelSlots; j < ns; j += kLevelSlots) {
+        for (int j = kLevelSlots; j < ns; j += 4) {  // four entries at a time (a level of 8 in two halves)
           const int4* s = t.slot + t.at(b, j);
           const int4 f0 = s[0], f1 = s[1], f2 = s[2], f3 = s[3];
           take(owns(a, entry_box(f0), o), f0.w);
