@@ -551,8 +551,11 @@ def run_ours(args, rank, world, local_rank):
                             "axis-alternating moves; no offsets), decoded "
                             + ("by sccg_decode_rect_packed" if args.e2e_unfused or world > 1
                                else "inside prep (sccg_prep_sets_packed)")),
-               "pipelining": ("sccg.Streamer: each step's host -> device copy on a copy stream overlaps the previous "
-                              "step's decode + step graph; every step's sums read back" if world == 1 else None)}
+               "pipelining": ("sccg.Streamer, three slots: each step's host -> device copy (one pinned buffer) on a "
+                              "copy stream overlaps the previous step's graph (" +
+                              ("decode kernels on a decode stream, then the step graph" if args.e2e_unfused
+                               else "prep decoding the packed rings, join, PixelBox") +
+                              "); every step's sums read back" if world == 1 else None)}
 
     if rank != 0:
         return None, None
