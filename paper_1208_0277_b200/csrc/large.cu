@@ -745,7 +745,10 @@ constexpr size_t kLSmemPerWarp = (size_t)4 * kLCap * sizeof(uint64_t) + (size_t)
 constexpr size_t kLSmem = kLWarps * kLSmemPerWarp;
 
 template <bool COUNT>
-__global__ void __launch_bounds__(kLWarps * 32, 4)
+#ifndef SCCG_ITEM_MINB
+#define SCCG_ITEM_MINB 4  // item-kernel CTAs per SM (registers: 4 -> up to 128 per thread)
+#endif
+__global__ void __launch_bounds__(kLWarps * 32, SCCG_ITEM_MINB)
     item_kernel(DevSet Ps, DevSet Qs, const int2* __restrict__ pairs, LargeWs w, int T, int mode, int dense,
                 long long* __restrict__ inter, long long* __restrict__ uni, long long* counters, sccg_sums* sums,
                 unsigned* __restrict__ hit_p, unsigned* __restrict__ hit_q) {
