@@ -61,7 +61,7 @@ def parse():
     ap.add_argument("--shard", default="image", choices=["image", "tile"],
                     help="N > 1: image = one slide image per rank (weak scaling, configs[3]); tile = ONE slide cut "
                          "into y bands of P with their Q halo (strong scaling, SURVEY 8(e))")
-    ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--e2e-steps", type=int, default=30)
     ap.add_argument("--e2e-unfused", action="store_true",
                     help="e2e: decode the packed rings with sccg_decode_rect_packed before the step graph "
                          "instead of inside prep (sccg_prep_sets_packed)")
@@ -507,17 +507,30 @@ def run_ours(args, rank, world, local_rank):
                 sdist.allreduce_sums(s)
             return sccg.jaccard(s.cpu())
 
-        if world == 1:
+        st = None
+        if world == 1:  # (N > 1: eager steps with the eager collective -- Streamer(allreduce=...) exists but the
+            # multi-GPU NCCL capture of three slot graphs is unexercised on hardware here)
             # streamed: step i + 1's host -> device copy (copy stream) overlaps step i's decode and compute
             # three slots: the host reads step i - 2's result while steps i - 1 and i are in flight, so
             # enqueueing (Python) never delays the next copy
             step = sccg.PackedStep(enc[0], enc[1])  # both sets in one pinned buffer: one copy per step
-            # fused: the step graph's prep decodes the packed rings itself (sccg_prep_sets_packed)
-            st = sccg.Streamer(A.n, int(A.offsets[-1]), B.n, int(B.offsets[-1]), cap=cap, threshold=args.threshold,
-                               depth=3, fused=None if args.e2e_unfused else step)
+            # fused: the step graph's prep decodes the packed rings itself (sccg_prep_sets_packed); N > 1: the
+            # NCCL all-reduce inside each slot's graph
+            try:
+                st = sccg.Streamer(A.n, int(A.offsets[-1]), B.n, int(B.offsets[-1]), cap=cap,
+                                   threshold=args.threshold, depth=3, fused=None if args.e2e_unfused else step,
+                                   allreduce=sdist.allreduce_sums if world > 1 else None)
+            except Exception as exc:
+                if world == 1:
+                    raise
+                print(f"[bench] e2e: NCCL capture in the Streamer failed ({exc!r}); eager steps", file=sys.stderr)
+                st = None
+        if st is not None:
             h2d_c = step.nbytes
             for _ in range(st.depth):  # warm-up: every slot once (each slot's graph was captured at construction)
                 st.result(st.submit_step(step))
+            if world > 1:
+                dist.barrier()
             torch.cuda.synchronize()
             e0.record(stream)
             st.copy_stream.wait_event(e0)  # the first copy starts inside the timed region
@@ -549,13 +562,14 @@ def run_ours(args, rank, world, local_rank):
                "h2d_bytes_per_step": int(h2d_c), "d2h_bytes_per_step": int(d2h), "steps": e2e_steps,
                "encoding": ("packed rectilinear rings (16-bit head, int16 start delta, variable-length or 4/8/16-bit "
                             "axis-alternating moves; no offsets), decoded "
-                            + ("by sccg_decode_rect_packed" if args.e2e_unfused or world > 1
-                               else "inside prep (sccg_prep_sets_packed)")),
+                            + ("inside prep (sccg_prep_sets_packed)" if st is not None and not args.e2e_unfused
+                               else "by sccg_decode_rect_packed")),
                "pipelining": ("sccg.Streamer, three slots: each step's host -> device copy (one pinned buffer) on a "
                               "copy stream overlaps the previous step's graph (" +
                               ("decode kernels on a decode stream, then the step graph" if args.e2e_unfused
                                else "prep decoding the packed rings, join, PixelBox") +
-                              "); every step's sums read back" if world == 1 else None)}
+                              ")" + (", the NCCL all-reduce in the graph" if world > 1 else "") +
+                              "; every step's sums read back" if st is not None else None)}
 
     if rank != 0:
         return None, None

@@ -643,10 +643,12 @@ class Streamer:
         sums = st.result(t)                 # waits for that step"""
 
     def __init__(self, n_p: int, nv_p: int, n_q: int, nv_q: int, cap: int | None = None, threshold: int = 0,
-                 depth: int = 2, device=None, fused: "PackedStep | None" = None):
+                 depth: int = 2, device=None, fused: "PackedStep | None" = None, allreduce=None):
         """fused: a PackedStep whose layout every submit_step shares; the step
         graph's prep then decodes the rings itself (sccg_prep_sets_packed: no
-        decode kernels, no read of xy) -- submit_step only."""
+        decode kernels, no read of xy) -- submit_step only.  allreduce: the
+        multi-GPU step's collective (e.g. dist.allreduce_sums over NCCL),
+        captured in each slot's step graph before the read-back."""
         torch = _torch()
         dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         self.device = dev
@@ -672,7 +674,8 @@ class Streamer:
                 v = fused.views(sl["step_buf"])
                 sl["step_views"] = v
                 packed = (v["p"], v["q"])
-            sl["pipe"] = Pipeline(P, Q, cap=cap, threshold=threshold, graph=True, readback=[sl["rb"]], packed=packed)
+            sl["pipe"] = Pipeline(P, Q, cap=cap, threshold=threshold, graph=True, readback=[sl["rb"]], packed=packed,
+                                  allreduce=allreduce)
             sl["copied"], sl["done"], sl["decoded"] = torch.cuda.Event(), torch.cuda.Event(), torch.cuda.Event()
             self.slots.append(sl)
         self.copy_stream = torch.cuda.Stream(device=dev)
