@@ -63,7 +63,8 @@ def launch_summary(path):
     wins = [seq[a:b] for a, b in zip(idx, idx[1:])]
     has_join = [any("grid_select" in n for n, _ in w) for w in wins]
     # a timed step: only our kernels (no torch kernels of the untimed bookkeeping, no e2e decode), the join in it
-    clean = [not any(n.startswith("at::") or "decode" in n or "small_kernel<1>" in n or "void at::" in n
+    clean = [not any(n.startswith("at::") or "decode" in n or "small_kernel<1>" in n or "void at::" in n or
+                     "prep_kernel<1>" in n  # the e2e step's prep from packed rings
                      for n, _ in w) for w in wins]
     full = [wins[i] for i in range(1, len(wins)) if has_join[i] and has_join[i - 1] and clean[i]]
     step = full[-1] if full else seq
