@@ -475,6 +475,7 @@ struct PrepArgs {
   int64_t tile_end[kPrepMaxSets];  // exclusive prefix ends of the sets' tile ranges
   int nsets;
   int validate;
+  int packed;  // sccg_prep_sets_packed
   unsigned long long* ticket;
 };
 
@@ -960,12 +961,15 @@ __global__ void prep_init_kernel(PrepArgs args) {
     st->pad[0] = st->pad[1] = 0;
     st->nonempty = st->sw = st->sh = st->swh = 0;
   }
+  if (args.packed && i < args.nsets && args.set[i].n == 0)  // packed mode, no rings: offsets[0]
+    const_cast<int64_t*>(args.set[i].off)[0] = 0;
   if (i == 0) *args.ticket = 0;
 }
 
 cudaError_t launch_prep(const sccg_polyset* const* sets, int count, int validate, cudaStream_t st,
                         const sccg_rect_packed* pk) {
   PrepArgs a{};
+  a.packed = pk ? 1 : 0;
   a.nsets = count;
   a.validate = validate;
   int64_t tiles = 0;

@@ -1054,6 +1054,22 @@ def test_prep_sets_packed_matches_plain(sccg, config):
             assert torch.equal(D.used_edge_words(), R.used_edge_words())
 
 
+def test_prep_sets_packed_empty_set(sccg):
+    """A set with no rings in packed mode: offsets[0] = 0 is still written."""
+    e0 = _packed_to_device(sccg.encode_rect_packed(np.zeros((0, 2), np.int32), np.zeros(1, np.int64)))
+    A, _ = synth.generate("tile")
+    ea = _packed_to_device(sccg.encode_rect_packed(A.xy, A.offsets))
+    xy0 = torch.zeros((1, 2), dtype=torch.int32, device="cuda")
+    off0 = torch.full((1,), 7, dtype=torch.int64, device="cuda")
+    xya = torch.zeros((len(A.xy), 2), dtype=torch.int32, device="cuda")
+    offa = torch.zeros(A.n + 1, dtype=torch.int64, device="cuda")
+    D0, Da = sccg.DeviceSet(xy0[:0], off0, prep=False), sccg.DeviceSet(xya, offa, prep=False)
+    sccg.prep_sets_packed([Da, D0], [ea, e0])
+    torch.cuda.synchronize()
+    assert off0.tolist() == [0]
+    assert torch.equal(offa.cpu(), torch.from_numpy(np.asarray(A.offsets, np.int64)))
+
+
 def test_streamer_fused_matches_pipeline(sccg):
     """sccg.Streamer(fused=...): the step graph's prep decodes the packed
     rings itself; every step's sums equal the device-resident Pipeline's."""
