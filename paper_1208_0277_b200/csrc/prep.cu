@@ -719,18 +719,7 @@ __global__ void __launch_bounds__(kPrepThreads, SCCG_PREP_MINB) prep_kernel(cons
     const int64_t v0 = s_off[0] & ~int64_t(1), v1 = s_off[np];
     const bool tiled = s_off[0] >= 0 && v1 <= nv_total && v1 >= s_off[0] && v1 - v0 <= kPrepVerts;
     if (PK) {
-      // decode this thread's ring into the tile (or, for a tile too large to
-      // stage, straight into xy); the tile then goes to xy by one bulk store
-      if ((int)threadIdx.x < np) {
-        const int V = pk_h & 0x1fff;
-        const int64_t rb = s_off[threadIdx.x];
-        if (V > 0 && rb >= 0 && rb + V <= nv_total) {  // (an encoding inconsistent with n_vertices writes nothing)
-          const unsigned short* up = pk_units + s_uoff[threadIdx.x];
-          int2* dst = tiled ? s_xy + (s_off[threadIdx.x] - v0) : const_cast<int2*>(xy) + s_off[threadIdx.x];
-          rp_walk_ring(up, V, (pk_h >> 13) & 3, pk_h >> 15, pk_x, pk_y, dst);
-        }
-      }
-      fence_async_smem();  // this thread's decoded vertices -> async proxy (the bulk store below)
+      // (decoded below, after the rings are dealt by length)
     } else if (tiled) {
       const int64_t nv = v1 - v0;
       if (bulk) {
@@ -749,21 +738,6 @@ __global__ void __launch_bounds__(kPrepThreads, SCCG_PREP_MINB) prep_kernel(cons
       }
     }
     __syncthreads();  // every ring counted (packed mode: every ring decoded)
-    if (PK && tiled) {  // the decoded tile [off[p0], v1) -> xy, read out before the ring work rewrites it in place
-      const int64_t s0 = s_off[0];
-      const int64_t a0 = (s0 + 1) & ~int64_t(1), a1 = v1 & ~int64_t(1);
-      int2* xo = const_cast<int2*>(xy);
-      if (bulk) {
-        if (threadIdx.x == 0) {
-          if (a1 > a0) bulk_store(xo + a0, s_xy + (a0 - v0), (unsigned)(a1 - a0) * 8u);
-          if (s0 < a0 && s0 < v1) xo[s0] = s_xy[s0 - v0];
-          if (a1 < v1 && a1 >= a0) xo[a1] = s_xy[a1 - v0];
-          bulk_store_drain();  // read out of shared memory before anyone rewrites it
-        }
-      } else {
-        for (int64_t i = s0 + threadIdx.x; i < v1; i += blockDim.x) xo[i] = s_xy[i - v0];
-      }
-    }
     if (threadIdx.x < 32) {  // exclusive scan of the bucket counts (two per lane)
       const int c0 = s_cnt[2 * threadIdx.x], c1 = s_cnt[2 * threadIdx.x + 1];
       int incl = c0 + c1;
@@ -821,6 +795,52 @@ __global__ void __launch_bounds__(kPrepThreads, SCCG_PREP_MINB) prep_kernel(cons
       __syncthreads();
     }
 #endif
+    if (PK) {
+      // decode the ring this thread was dealt (by length: a warp's serial
+      // walks have similar trip counts) into the tile -- or, for a tile too
+      // large to stage, straight into xy -- then the tile goes to xy by one
+      // bulk store, read out before the ring work rewrites it in place
+      const int j = s_perm[threadIdx.x];
+      if (j != 0xff) {
+        const int64_t r = p0 + j;
+        const int hj = args.set[si].ph[r], V = hj & 0x1fff;
+        const int64_t rb = s_off[j];
+        if (V > 0 && rb >= 0 && rb + V <= nv_total) {  // (an encoding inconsistent with n_vertices writes nothing)
+          const long long* blk = args.set[si].pb + 4 * (p0 / kRpBlock);
+          const long long sw = blk[2], org = blk[3], so = sw & ((1ll << 62) - 1);
+          const int jb = (int)(r - (p0 / kRpBlock) * kRpBlock);
+          int x, y;
+          if ((sw >> 62) & 1) {
+            const unsigned short* sp = reinterpret_cast<const unsigned short*>(args.set[si].pst) + so + 4 * jb;
+            x = (int)((unsigned)sp[0] | ((unsigned)sp[1] << 16));
+            y = (int)((unsigned)sp[2] | ((unsigned)sp[3] << 16));
+          } else {
+            x = (int)(unsigned)(org & 0xffffffffll) + args.set[si].pst[so + 2 * jb];
+            y = (int)(unsigned)((unsigned long long)org >> 32) + args.set[si].pst[so + 2 * jb + 1];
+          }
+          int2* dst = tiled ? s_xy + (rb - v0) : const_cast<int2*>(xy) + rb;
+          rp_walk_ring(pk_units + s_uoff[j], V, (hj >> 13) & 3, hj >> 15, x, y, dst);
+        }
+      }
+      fence_async_smem();  // this thread's decoded vertices -> async proxy (the bulk store below)
+      __syncthreads();
+      if (tiled) {  // the decoded tile [off[p0], v1) -> xy
+        const int64_t s0 = s_off[0];
+        const int64_t a0 = (s0 + 1) & ~int64_t(1), a1 = v1 & ~int64_t(1);
+        int2* xo = const_cast<int2*>(xy);
+        if (bulk) {
+          if (threadIdx.x == 0) {
+            if (a1 > a0) bulk_store(xo + a0, s_xy + (a0 - v0), (unsigned)(a1 - a0) * 8u);
+            if (s0 < a0 && s0 < v1) xo[s0] = s_xy[s0 - v0];
+            if (a1 < v1 && a1 >= a0) xo[a1] = s_xy[a1 - v0];
+            bulk_store_drain();  // read out of shared memory before anyone rewrites it
+          }
+        } else {
+          for (int64_t i = s0 + threadIdx.x; i < v1; i += blockDim.x) xo[i] = s_xy[i - v0];
+        }
+      }
+      __syncthreads();
+    }
 #if SCCG_PREP_L2_PREFETCH == 2
     if (!PK && threadIdx.x == 0) {
       // thread 0 (warp 0 deals the smallest rings, so it has slack) starts
